@@ -1,0 +1,218 @@
+/*
+ * gsb200.h — C ABI of the B200-native pose-gradient Gaussian-splatting hot
+ * path (libgsb200.so). Plain pointers and sizes only; no C++ or torch types.
+ *
+ * Drop-in boundary. Each entry point replaces one reference
+ * interface (paths relative to /root/reference/proj):
+ *
+ *   gsb_render            <- gsopt::render            include/gsopt/rasterizer.hpp:98-99
+ *   gsb_frame_download    <- RenderOutput fields       include/gsopt/rasterizer.hpp:66-82
+ *   gsb_render_backward   <- gsopt::render_backward   include/gsopt/rasterizer.hpp:112-113
+ *   gsb_rgb_loss          <- gsopt::rgb_loss          include/gsopt/losses.hpp:37
+ *   gsb_pose_step         <- gsopt::pose_step         include/gsopt/trainer.hpp:99-100
+ *   gsb_adam_step         <- gsopt::adam_step (both)  include/gsopt/trainer.hpp:85-87
+ *   gsb_cloud_adam_step   <- cloud_adam_step          src/pipelines.cpp:18-41
+ *   gsb_schedule          <- gsopt::schedule          include/gsopt/trainer.hpp:62-63
+ *   gsb_estimate_pose     <- gsopt::estimate_pose     include/gsopt/trainer.hpp:170-171
+ *                            (pose_descent, src/pipelines.cpp:58-92, device resident)
+ *   gsb_cloud_*           <- GaussianCloud            include/gsopt/scene.hpp:22-46
+ *
+ * Status codes: 0 = OK; reference ErrorCode value + 1 (core.hpp:35-47) for
+ * the reference's own failure modes; >= 100 for CUDA / argument / memory
+ * failures. gsb_last_error() returns a thread-local message for the last
+ * non-zero status. No call ever falls back to a CPU path: without a usable
+ * sm_100 device every call that needs one returns GSB_ERR_NO_DEVICE.
+ *
+ * Threading: one context = one device + one CUDA stream; calls on a context
+ * are stream ordered and blocking for host outputs. A context must not be
+ * used from two threads at once without external locking (the reference's
+ * pool is not re-entrant either, core.cpp:39-58).
+ */
+#ifndef GSB200_H
+#define GSB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GSB_OK 0
+#define GSB_ERR_ANGLE_NEAR_PI 1
+#define GSB_ERR_DEGENERATE_CLOUD 2
+#define GSB_ERR_NO_VALID_DEPTH 3
+#define GSB_ERR_DIMENSION_MISMATCH 4
+#define GSB_ERR_EMPTY_MASK 5
+#define GSB_ERR_STATE_MISMATCH 6
+#define GSB_ERR_MISSING_INTRINSICS 7
+#define GSB_ERR_IMAGE_SIZE_MISMATCH 8
+#define GSB_ERR_CORRUPT_FILE 9
+#define GSB_ERR_DIVERGED 10
+#define GSB_ERR_INVALID_CONFIG 11
+#define GSB_ERR_CUDA 100
+#define GSB_ERR_INVALID_ARGUMENT 101
+#define GSB_ERR_OUT_OF_MEMORY 102
+#define GSB_ERR_NO_DEVICE 103
+
+/* render_backward flags */
+#define GSB_BWD_POSE_ONLY 1u   /* estimate_pose only consumes d_pose (pipelines.cpp:84) */
+#define GSB_BWD_FAST_ATOMIC 2u /* RasterConfig::deterministic == false (rasterizer.cpp:419-431) */
+
+typedef struct gsb_ctx gsb_ctx;
+typedef struct gsb_cloud gsb_cloud;
+typedef struct gsb_frame gsb_frame;   /* RenderOutput's cached forward state, device resident */
+typedef struct gsb_grads gsb_grads;   /* GradientBundle, device resident */
+typedef struct gsb_image gsb_image;   /* a device-resident H x W x 3 target frame */
+typedef struct gsb_adam gsb_adam;     /* CloudAdam, device resident */
+
+/* Camera (rasterizer.hpp:19-28): pinhole intrinsics + world_to_cam [R|t], R row-major. */
+typedef struct {
+  double fx, fy, cx, cy;
+  int32_t width, height;
+  double R[9];
+  double t[3];
+} gsb_camera;
+
+/* RasterConfig (rasterizer.hpp:30-38). */
+typedef struct {
+  int32_t tile_size; /* must be 16 */
+  double cutoff_sigma, alpha_clamp, dilation, early_termination, z_near;
+  int32_t deterministic;
+} gsb_raster_config;
+
+/* PoseAdam (trainer.hpp:90-94). */
+typedef struct {
+  double m[6], v[6];
+  int64_t step;
+} gsb_pose_adam;
+
+/* Forward-state sizes (RenderOutput bookkeeping). */
+typedef struct {
+  int64_t n_gaussians, n_splats, n_entries;
+  int32_t width, height, tiles_x, tiles_y;
+  uint64_t state_fingerprint;
+} gsb_frame_info;
+
+/* The pose_descent knobs of TrainConfig (trainer.hpp:21-60) that estimate_pose reads. */
+typedef struct {
+  double cam_lr_start, cam_lr_end; /* cosine schedule (pipelines.cpp:82) */
+  double beta;                     /* LossConfig::beta */
+  double pose_converged_eps;       /* 0 disables the early exit */
+  double background[3];
+  gsb_raster_config raster;
+  int32_t budget;                  /* estimate_pose_steps */
+} gsb_pose_config;
+
+const char* gsb_last_error(void);
+const char* gsb_version(void);
+void gsb_default_raster_config(gsb_raster_config* cfg);
+void gsb_default_pose_config(gsb_pose_config* cfg);
+
+/* ---- context ---- */
+int gsb_ctx_create(int32_t device, gsb_ctx** out);
+int gsb_ctx_destroy(gsb_ctx* ctx);
+int gsb_ctx_synchronize(gsb_ctx* ctx);
+/* Device time of the kernels launched on the context stream since the last
+ * reset, split by stage (ms): preprocess, sort/bin, composite, loss,
+ * backward raster, backward geometry, optimizer. Enabled by
+ * gsb_ctx_set_profiling(ctx, 1); used by bench.py for the roofline line. */
+int gsb_ctx_set_profiling(gsb_ctx* ctx, int32_t enable);
+int gsb_ctx_stage_times(gsb_ctx* ctx, double* ms_out /* 8 */, int64_t* launches_out /* 8 */, int32_t reset);
+/* Number of kernel launches issued by this context so far. */
+int64_t gsb_ctx_launch_count(gsb_ctx* ctx);
+
+/* ---- cloud (GaussianCloud, scene.hpp:22-46), stored as FP32 planes on device ---- */
+int gsb_cloud_create(gsb_ctx* ctx, int64_t n, int32_t sh_degree, gsb_cloud** out);
+int gsb_cloud_destroy(gsb_cloud* cloud);
+/* Reference FP64 layout: means n*3, rotations n*4 (w,x,y,z), log_scales n*3,
+ * opacity_logits n, sh n*3*(sh_degree+1)^2 channel-major per Gaussian. */
+int gsb_cloud_upload(gsb_cloud* cloud, const double* means, const double* rotations,
+                     const double* log_scales, const double* opacity_logits, const double* sh,
+                     int32_t active_sh_degree);
+int gsb_cloud_download(gsb_cloud* cloud, double* means, double* rotations, double* log_scales,
+                       double* opacity_logits, double* sh);
+int gsb_cloud_info(gsb_cloud* cloud, int64_t* n, int32_t* sh_degree, int32_t* active_sh_degree);
+int gsb_cloud_set_active_sh_degree(gsb_cloud* cloud, int32_t active_sh_degree);
+/* Fills the cloud with the synth.cpp:45-62 draw sequence (GCC argument order)
+ * from seed, plus log_scale_offset added to every log-scale (SURVEY §8d
+ * density matching). Host generator, then one upload. */
+int gsb_cloud_synth(gsb_cloud* cloud, uint64_t seed, double log_scale_offset);
+/* Generates `cameras` poses exactly as synth_scene (synth.cpp:73-101) would
+ * after drawing an n-Gaussian cloud of degree sh_degree from seed.
+ * kind: 0 orbit, 1 forward-facing, 2 random-walk. poses: cameras*12 row-major [R|t]. */
+int gsb_synth_poses(uint64_t seed, int64_t n, int32_t sh_degree, int32_t kind, int32_t cameras,
+                    double orbit_radius, double orbit_arc, double* poses);
+/* perturb_pose (eval.cpp:130-146) with a caller-held rng state (init with seed). */
+int gsb_perturb_pose(const double pose[12], double rot_deg, double trans, uint64_t* rng_state,
+                     double out[12]);
+
+/* ---- forward (render, rasterizer.cpp:209-281) ---- */
+int gsb_frame_create(gsb_ctx* ctx, gsb_frame** out);
+int gsb_frame_destroy(gsb_frame* frame);
+/* image_out: optional host H*W*3 interleaved FP64 (Image layout, image.hpp:15-37). */
+int gsb_render(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, const double background[3],
+               const gsb_raster_config* cfg, gsb_frame* frame, double* image_out);
+int gsb_frame_get_info(gsb_frame* frame, gsb_frame_info* info);
+/* Copies every RenderOutput field to host (any pointer may be NULL). Per-splat
+ * arrays are in depth order (n_splats), tile_lists holds indices into them
+ * (n_entries), tile_ranges is tiles*2 (begin,end). conic is 2x2 row-major. */
+int gsb_frame_download(gsb_frame* frame, double* image, double* accum_transmittance,
+                       double* final_transmittance, int32_t* contrib_count, uint8_t* overflow_mask,
+                       int32_t* splat_gaussian, double* splat_mu2d, double* splat_depth,
+                       double* splat_conic, double* splat_color, double* splat_opacity,
+                       double* splat_radius, uint8_t* splat_clamped, int32_t* tile_lists,
+                       int32_t* tile_ranges);
+
+/* ---- loss (rgb_loss, losses.cpp:201-215) ---- */
+/* Host FP64 HWC images; d_rendered optional. */
+int gsb_rgb_loss(gsb_ctx* ctx, const double* rendered, const double* target, int32_t width,
+                 int32_t height, double beta, double* loss_out, double* d_rendered);
+int gsb_image_create(gsb_ctx* ctx, const double* image_hwc, int32_t width, int32_t height,
+                     gsb_image** out);
+int gsb_image_destroy(gsb_image* image);
+/* Loss of the frame's rendered image against a device target; the gradient
+ * stays on device inside the frame (consumed by gsb_render_backward_device). */
+int gsb_frame_rgb_loss(gsb_ctx* ctx, gsb_frame* frame, gsb_image* target, double beta,
+                       double* loss_out);
+
+/* ---- backward (render_backward, rasterizer.cpp:336-540) ---- */
+int gsb_grads_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_grads** out);
+int gsb_grads_destroy(gsb_grads* grads);
+int gsb_grads_download(gsb_grads* grads, double* d_means, double* d_rotations,
+                       double* d_log_scales, double* d_opacity_logits, double* d_sh,
+                       double* d_mu2d, double d_pose[6]);
+/* d_image: host H*W*3 FP64. grads may be NULL with GSB_BWD_POSE_ONLY. */
+int gsb_render_backward(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, gsb_frame* frame,
+                        const double* d_image, int32_t width, int32_t height, uint32_t flags,
+                        gsb_grads* grads, double d_pose_out[6]);
+/* Same, upstream gradient = the one left in the frame by gsb_frame_rgb_loss. */
+int gsb_render_backward_device(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam,
+                               gsb_frame* frame, uint32_t flags, gsb_grads* grads,
+                               double d_pose_out[6]);
+
+/* ---- optimiser (trainer.cpp:30-90, pipelines.cpp:18-41) ---- */
+double gsb_schedule(int32_t kind /* 0 cosine, 1 exponential */, double start, double end,
+                    int64_t step, int64_t total);
+/* Runs on the device (FP64), like the batched step inside gsb_estimate_pose. */
+int gsb_pose_step(gsb_ctx* ctx, const double pose[12], const double d_pose[6], double lr,
+                  gsb_pose_adam* state, double pose_out[12], double applied_update[6]);
+int gsb_adam_step(gsb_ctx* ctx, double* params, const double* grads, double* m, double* v,
+                  int64_t* step, int64_t n, double lr);
+int gsb_adam_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_adam** out);
+int gsb_adam_destroy(gsb_adam* adam);
+/* lrs = {pos, rot, scale, opacity, sh_dc, sh_rest} (pipelines.cpp:14-16). */
+int gsb_cloud_adam_step(gsb_ctx* ctx, gsb_cloud* cloud, gsb_grads* grads, gsb_adam* adam,
+                        const double lrs[6]);
+
+/* ---- pose estimation (pose_descent, pipelines.cpp:58-92), device resident ---- */
+/* intr = {fx, fy, cx, cy}; trace_* optional (budget entries): pose before each
+ * step (12), loss (1). Returns best pose (pipelines.cpp:71-75). */
+int gsb_estimate_pose(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* target, const double intr[4],
+                      const double init_pose[12], const gsb_pose_config* cfg, double pose_out[12],
+                      double* final_loss, int32_t* steps_used, int32_t* converged,
+                      double* trace_pose, double* trace_loss);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

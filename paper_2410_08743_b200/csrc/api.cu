@@ -1,0 +1,1132 @@
+// api.cu — the C ABI (include/gsb200.h): context / cloud / frame objects and
+// the host orchestration of the hot path (render -> loss -> backward -> pose
+// step) on one CUDA stream. All arithmetic runs in the kernels of
+// k_*.cu; the host only sizes buffers, converts the reference's FP64
+// host layouts at the boundary and sequences launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gsb_internal.cuh"
+
+namespace gsb {
+
+// kernels (k_*.cu)
+int launch_preprocess(cudaStream_t st, const gsb_cloud* cloud, const CamDev* cam, const RasterDev& rc, gsb_frame* f);
+int scan_exclusive(cudaStream_t st, const uint32_t* in, int64_t n, bool flag, uint32_t* out, uint32_t* scratch,
+                   uint32_t* total, int64_t* launches);
+size_t scan_words(int64_t n);
+int radix_sort_pairs(cudaStream_t st, uint32_t* keys[2], uint32_t* vals[2], int64_t n, int total_bits,
+                     uint32_t* hist, int* result_sel, int64_t* launches);
+size_t radix_hist_words(int64_t n, int total_bits);
+int launch_compact(cudaStream_t st, const uint32_t* cnt_g, const uint32_t* vis_pos, const double* depth_g, int64_t n,
+                   uint32_t* vis_idx, uint32_t* dkey, uint32_t* dval);
+int launch_depth_tie_fix(cudaStream_t st, const uint32_t* key, uint32_t* val, const uint32_t* vis_idx,
+                         const double* depth_g, int64_t nv);
+int launch_gather_ranks(cudaStream_t st, const uint32_t* sorted_v, const uint32_t* vis_idx, const SplatRec* rec_g,
+                        const uint2* rect_g, const uint32_t* cnt_g, int64_t nv, SplatRec* rec, SplatAux* aux,
+                        uint32_t* cnt_r, int32_t* rank_of_g);
+int launch_duplicate(cudaStream_t st, const uint32_t* offs, SplatAux* aux, int64_t nv, int tiles_x, uint32_t* ekey,
+                     uint32_t* eval);
+int launch_tile_ranges(cudaStream_t st, const uint32_t* ekey, int64_t k, int n_tiles, uint2* ranges);
+int launch_composite(cudaStream_t st, gsb_frame* f, const RasterDev& rc);
+int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc);
+int launch_backward_geom(cudaStream_t st, const gsb_cloud* cloud, gsb_frame* f, const RasterDev& rc, bool full,
+                         float* grads, int64_t* launches);
+int launch_rgb_loss(cudaStream_t st, const float* ren, const float* tgt, int W, int H, double beta, float* gmaps,
+                    double* block_sums, double* out3, float* d_image, int64_t* launches);
+size_t loss_block_count(int W, int H);
+int launch_pose_iter(cudaStream_t st, void* state, const double* dpose, const double* loss3, double lr_start,
+                     double lr_end, double eps, int budget, CamDev* cam, double* trace_pose, double* trace_loss);
+size_t pose_state_bytes();
+int pose_state_init(void* host_state, const double pose[12]);
+void pose_state_read(const void* host_state, double best_pose[12], double cur_pose[12], double* final_loss,
+                     int32_t* steps_used, int32_t* converged, int32_t* stop, double applied[6], double m[6],
+                     double v[6], int64_t* step);
+void pose_state_set_adam(void* host_state, const double m[6], const double v[6], int64_t step);
+int launch_pose_step(cudaStream_t st, void* states, const double* dpose, double lr, int nb);
+int launch_adam_f64(cudaStream_t st, double* p, const double* g, double* m, double* v, int64_t n, double lr,
+                    int64_t step);
+int launch_cloud_adam(cudaStream_t st, float* params, const float* grads, float* m, float* v, int64_t n,
+                      int64_t n_pad, int sh_degree, const double lrs[6], const int64_t steps[5]);
+
+// ---------------------------------------------------------------- errors
+static thread_local std::string g_error;
+void set_error(const std::string& msg) { g_error = msg; }
+int fail(int code, const std::string& msg) {
+  g_error = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  g_error = std::string(what) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? GSB_ERR_OUT_OF_MEMORY : GSB_ERR_CUDA;
+}
+
+// ---------------------------------------------------------- stage timer
+struct StageTimer {
+  struct Pair {
+    cudaEvent_t a, b;
+    int stage;
+  };
+  std::vector<Pair> pool;
+  size_t used = 0;
+  int open_stage = -1;
+  double ms[kNumStages] = {0};
+  int64_t count[kNumStages] = {0};
+  cudaError_t begin(cudaStream_t st, int stage) {
+    if (used == pool.size()) {
+      Pair p;
+      cudaEventCreate(&p.a);
+      cudaEventCreate(&p.b);
+      pool.push_back(p);
+    }
+    pool[used].stage = stage;
+    open_stage = stage;
+    return cudaEventRecord(pool[used].a, st);
+  }
+  cudaError_t end(cudaStream_t st) {
+    cudaError_t e = cudaEventRecord(pool[used].b, st);
+    ++used;
+    open_stage = -1;
+    return e;
+  }
+  cudaError_t collect() {
+    for (size_t i = 0; i < used; ++i) {
+      cudaError_t e = cudaEventSynchronize(pool[i].b);
+      if (e != cudaSuccess) return e;
+      float t = 0.f;
+      cudaEventElapsedTime(&t, pool[i].a, pool[i].b);
+      ms[pool[i].stage] += t;
+      count[pool[i].stage] += 1;
+    }
+    used = 0;
+    return cudaSuccess;
+  }
+  void reset() {
+    used = 0;
+    for (int k = 0; k < kNumStages; ++k) {
+      ms[k] = 0;
+      count[k] = 0;
+    }
+  }
+  ~StageTimer() {
+    for (auto& p : pool) {
+      cudaEventDestroy(p.a);
+      cudaEventDestroy(p.b);
+    }
+  }
+};
+
+struct StageScope {
+  gsb_ctx* ctx;
+  StageScope(gsb_ctx* c, int stage) : ctx(c) {
+    if (ctx->profiling && ctx->timer) {
+      if (ctx->timer->used > 4096) ctx->timer->collect();
+      ctx->timer->begin(ctx->stream, stage);
+    }
+  }
+  ~StageScope() {
+    if (ctx->profiling && ctx->timer) ctx->timer->end(ctx->stream);
+  }
+};
+
+// --------------------------------------------------------------- helpers
+static int ensure_device(gsb_ctx* ctx) {
+  if (!ctx) return fail(GSB_ERR_INVALID_ARGUMENT, "null context");
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  return GSB_OK;
+}
+
+static void* pinned(gsb_ctx* ctx, size_t bytes) {
+  if (bytes > ctx->host_pinned_bytes) {
+    if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
+    ctx->host_pinned = nullptr;
+    ctx->host_pinned_bytes = 0;
+    size_t cap = bytes + bytes / 4 + 4096;
+    if (cudaMallocHost(&ctx->host_pinned, cap) != cudaSuccess) return nullptr;
+    ctx->host_pinned_bytes = cap;
+  }
+  return ctx->host_pinned;
+}
+
+#define GSB_RESERVE(buf, bytes) GSB_CUDA((buf).reserve(bytes))
+
+static uint64_t fnv1a(uint64_t h, const void* data, size_t n) {  // rasterizer.cpp:41-48
+  const unsigned char* p = static_cast<const unsigned char*>(data);
+  for (size_t i = 0; i < n; ++i) {
+    h ^= p[i];
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+
+// rasterizer.cpp:52-73 semantics: sizes, degrees and the full camera, then
+// the cloud's content identity. The cloud lives on the device and every
+// mutation goes through this API, so its (identity, version) pair stands in
+// for the reference's 64 strided host samples.
+static uint64_t fingerprint(const gsb_cloud* cloud, const gsb_camera* cam) {
+  uint64_t h = 0xcbf29ce484222325ull;
+  const int64_t n = cloud->n;
+  h = fnv1a(h, &n, sizeof n);
+  h = fnv1a(h, &cloud->sh_degree, sizeof(int32_t));
+  h = fnv1a(h, &cloud->active_sh_degree, sizeof(int32_t));
+  const double f4[4] = {cam->fx, cam->fy, cam->cx, cam->cy};
+  h = fnv1a(h, f4, sizeof f4);
+  const int32_t wh[2] = {cam->width, cam->height};
+  h = fnv1a(h, wh, sizeof wh);
+  h = fnv1a(h, cam->R, sizeof(double) * 9);
+  h = fnv1a(h, cam->t, sizeof(double) * 3);
+  const uintptr_t id = reinterpret_cast<uintptr_t>(cloud);
+  h = fnv1a(h, &id, sizeof id);
+  h = fnv1a(h, &cloud->host_fingerprint, sizeof(uint64_t));
+  h = fnv1a(h, &cloud->version, sizeof(uint64_t));
+  return h;
+}
+
+static CamDev make_camdev(const gsb_camera* c, int tile) {
+  CamDev d;
+  d.fx = c->fx;
+  d.fy = c->fy;
+  d.cx = c->cx;
+  d.cy = c->cy;
+  for (int k = 0; k < 9; ++k) d.R[k] = c->R[k];
+  for (int k = 0; k < 3; ++k) d.t[k] = c->t[k];
+  for (int i = 0; i < 3; ++i) {  // Camera::center = -(R^T t) (rasterizer.hpp:24)
+    const double r = c->R[0 * 3 + i] * c->t[0] + c->R[1 * 3 + i] * c->t[1] + c->R[2 * 3 + i] * c->t[2];
+    d.center[i] = -r;
+  }
+  d.width = c->width;
+  d.height = c->height;
+  d.tiles_x = (c->width + tile - 1) / tile;
+  d.tiles_y = (c->height + tile - 1) / tile;
+  return d;
+}
+
+static RasterDev make_rasterdev(const gsb_raster_config* c) {
+  RasterDev r;
+  r.cutoff_sigma = c->cutoff_sigma;
+  r.alpha_clamp = c->alpha_clamp;
+  r.dilation = c->dilation;
+  r.early_termination = c->early_termination;
+  r.z_near = c->z_near;
+  r.cutoff2_f = (float)(c->cutoff_sigma * c->cutoff_sigma);
+  r.alpha_clamp_f = (float)c->alpha_clamp;
+  r.early_term_f = (float)c->early_termination;
+  r.pad = 0.f;
+  return r;
+}
+
+static int validate_config(const gsb_raster_config* cfg) {
+  if (!cfg) return fail(GSB_ERR_INVALID_ARGUMENT, "null raster config");
+  if (cfg->tile_size != kTile) return fail(GSB_ERR_INVALID_CONFIG, "tile_size must be 16 on this build");
+  if (!(cfg->cutoff_sigma > 0.0) || !(cfg->alpha_clamp > 0.0) || cfg->alpha_clamp >= 1.0 || cfg->dilation < 0.0 ||
+      cfg->early_termination < 0.0)
+    return fail(GSB_ERR_INVALID_CONFIG, "raster config out of range");
+  return GSB_OK;
+}
+
+// Copies `count` u32 device counters to host through pinned memory (one sync).
+static int read_counters(gsb_ctx* ctx, const uint32_t* dev, uint32_t* host, int count) {
+  uint32_t* h = static_cast<uint32_t*>(pinned(ctx, sizeof(uint32_t) * count));
+  if (!h) return fail(GSB_ERR_OUT_OF_MEMORY, "pinned staging");
+  GSB_CUDA(cudaMemcpyAsync(h, dev, sizeof(uint32_t) * count, cudaMemcpyDeviceToHost, ctx->stream));
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < count; ++i) host[i] = h[i];
+  return GSB_OK;
+}
+
+// The full forward pass on the device; camera already in f->cam.
+static int render_device(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, const RasterDev& rc) {
+  cudaStream_t st = ctx->stream;
+  const int64_t n = cloud->n;
+  const int n_tiles = f->tiles_x * f->tiles_y;
+  const int64_t npix = (int64_t)f->width * f->height;
+  GSB_RESERVE(f->rec_g, sizeof(SplatRec) * std::max<int64_t>(n, 1));
+  GSB_RESERVE(f->rect_g, sizeof(uint2) * std::max<int64_t>(n, 1));
+  GSB_RESERVE(f->cnt_g, sizeof(uint32_t) * std::max<int64_t>(n, 1));
+  GSB_RESERVE(f->depth_g, sizeof(double) * std::max<int64_t>(n, 1));
+  GSB_RESERVE(f->radius_g, sizeof(double) * std::max<int64_t>(n, 1));
+  GSB_RESERVE(f->rank_of_g, sizeof(int32_t) * std::max<int64_t>(n, 1));
+  GSB_RESERVE(f->vis_idx, sizeof(uint32_t) * std::max<int64_t>(n, 1));  // also scan output scratch
+  GSB_RESERVE(f->scan_tmp, sizeof(uint32_t) * (scan_words(std::max<int64_t>(n, 1)) + 4096));
+  GSB_RESERVE(f->counters, 64);
+  GSB_RESERVE(f->ranges, sizeof(uint2) * std::max(n_tiles, 1));
+  GSB_RESERVE(f->image, sizeof(float) * 3 * std::max<int64_t>(npix, 1));
+  GSB_RESERVE(f->final_t, sizeof(float) * std::max<int64_t>(npix, 1));
+  GSB_RESERVE(f->pixstate, sizeof(uint32_t) * std::max<int64_t>(npix, 1));
+  uint32_t* counters = f->counters.as<uint32_t>();
+  uint32_t host_cnt[2] = {0, 0};
+  {
+    StageScope sc(ctx, kStPreprocess);
+    int rc1 = launch_preprocess(st, cloud, f->cam.as<CamDev>(), rc, f);
+    if (rc1) return rc1;
+    ctx->launches += n > 0 ? 1 : 0;
+  }
+  int64_t nv = 0, k = 0;
+  {
+    StageScope sc(ctx, kStSort);
+    // 1. compaction (index order); cnt_r holds the scan output until step 3
+    GSB_RESERVE(f->cnt_r, sizeof(uint32_t) * std::max<int64_t>(n, 1));
+    uint32_t* pos = f->cnt_r.as<uint32_t>();
+    int r = scan_exclusive(st, f->cnt_g.as<uint32_t>(), n, true, pos, f->scan_tmp.as<uint32_t>(), counters,
+                           &ctx->launches);
+    if (r) return r;
+  }
+  if (int rr = read_counters(ctx, counters, host_cnt, 1)) return rr;
+  nv = host_cnt[0];
+  f->n_splats = nv;
+  {
+    StageScope sc(ctx, kStSort);
+    GSB_RESERVE(f->dkey[0], sizeof(uint32_t) * std::max<int64_t>(nv, 1));
+    GSB_RESERVE(f->dkey[1], sizeof(uint32_t) * std::max<int64_t>(nv, 1));
+    GSB_RESERVE(f->dval[0], sizeof(uint32_t) * std::max<int64_t>(nv, 1));
+    GSB_RESERVE(f->dval[1], sizeof(uint32_t) * std::max<int64_t>(nv, 1));
+    GSB_RESERVE(f->rec, sizeof(SplatRec) * std::max<int64_t>(nv, 1));
+    GSB_RESERVE(f->aux, sizeof(SplatAux) * std::max<int64_t>(nv, 1));
+    int r = launch_compact(st, f->cnt_g.as<uint32_t>(), f->cnt_r.as<uint32_t>(), f->depth_g.as<double>(), n,
+                           f->vis_idx.as<uint32_t>(), f->dkey[0].as<uint32_t>(), f->dval[0].as<uint32_t>());
+    if (r) return r;
+    ctx->launches += 1;
+    // 2. stable depth sort (FP32 bits) + FP64 tie fix
+    GSB_RESERVE(f->sort_hist, sizeof(uint32_t) * radix_hist_words(std::max<int64_t>(nv, 1), 32));
+    uint32_t* dk[2] = {f->dkey[0].as<uint32_t>(), f->dkey[1].as<uint32_t>()};
+    uint32_t* dv[2] = {f->dval[0].as<uint32_t>(), f->dval[1].as<uint32_t>()};
+    int sel = 0;
+    r = radix_sort_pairs(st, dk, dv, nv, 32, f->sort_hist.as<uint32_t>(), &sel, &ctx->launches);
+    if (r) return r;
+    r = launch_depth_tie_fix(st, dk[sel], dv[sel], f->vis_idx.as<uint32_t>(), f->depth_g.as<double>(), nv);
+    if (r) return r;
+    ctx->launches += nv > 1 ? 1 : 0;
+    // 3. rank-order records, entry counts -> offsets
+    r = launch_gather_ranks(st, dv[sel], f->vis_idx.as<uint32_t>(), f->rec_g.as<SplatRec>(), f->rect_g.as<uint2>(),
+                            f->cnt_g.as<uint32_t>(), nv, f->rec.as<SplatRec>(), f->aux.as<SplatAux>(),
+                            f->cnt_r.as<uint32_t>(), f->rank_of_g.as<int32_t>());
+    if (r) return r;
+    ctx->launches += nv > 0 ? 1 : 0;
+    GSB_RESERVE(f->scan_tmp, sizeof(uint32_t) * (scan_words(std::max<int64_t>(nv, 1)) + 4096));
+    r = scan_exclusive(st, f->cnt_r.as<uint32_t>(), nv, false, dk[sel ^ 1], f->scan_tmp.as<uint32_t>(), counters + 1,
+                       &ctx->launches);
+    if (r) return r;
+    f->sorted_sel = sel;  // remember where offsets live: dk[sel^1]
+  }
+  if (int rr = read_counters(ctx, counters + 1, host_cnt + 1, 1)) return rr;
+  k = host_cnt[1];
+  f->n_entries = k;
+  {
+    StageScope sc(ctx, kStSort);
+    const int dsel = f->sorted_sel;
+    uint32_t* offs = (dsel ^ 1) ? f->dkey[1].as<uint32_t>() : f->dkey[0].as<uint32_t>();
+    GSB_RESERVE(f->ekey[0], sizeof(uint32_t) * std::max<int64_t>(k, 1));
+    GSB_RESERVE(f->ekey[1], sizeof(uint32_t) * std::max<int64_t>(k, 1));
+    GSB_RESERVE(f->eval_[0], sizeof(uint32_t) * std::max<int64_t>(k, 1));
+    GSB_RESERVE(f->eval_[1], sizeof(uint32_t) * std::max<int64_t>(k, 1));
+    int r = launch_duplicate(st, offs, f->aux.as<SplatAux>(), nv, f->tiles_x, f->ekey[0].as<uint32_t>(),
+                             f->eval_[0].as<uint32_t>());
+    if (r) return r;
+    ctx->launches += nv > 0 ? 1 : 0;
+    int bits = 0;
+    while ((1 << bits) < n_tiles) ++bits;
+    GSB_RESERVE(f->sort_hist, sizeof(uint32_t) * radix_hist_words(std::max<int64_t>(k, 1), bits));
+    uint32_t* ek[2] = {f->ekey[0].as<uint32_t>(), f->ekey[1].as<uint32_t>()};
+    uint32_t* ev[2] = {f->eval_[0].as<uint32_t>(), f->eval_[1].as<uint32_t>()};
+    int sel = 0;
+    r = radix_sort_pairs(st, ek, ev, k, bits, f->sort_hist.as<uint32_t>(), &sel, &ctx->launches);
+    if (r) return r;
+    f->sorted_sel = sel;
+    r = launch_tile_ranges(st, ek[sel], k, n_tiles, f->ranges.as<uint2>());
+    if (r) return r;
+    ctx->launches += n_tiles > 0 ? 1 : 0;
+  }
+  {
+    StageScope sc(ctx, kStComposite);
+    int r = launch_composite(st, f, rc);
+    if (r) return r;
+    ctx->launches += n_tiles > 0 ? 1 : 0;
+  }
+  return GSB_OK;
+}
+
+static int frame_setup(gsb_ctx* ctx, gsb_frame* f, const gsb_cloud* cloud, const gsb_camera* cam,
+                       const double bg[3], const gsb_raster_config* cfg) {
+  if (cam->width <= 0 || cam->height <= 0) return fail(GSB_ERR_INVALID_ARGUMENT, "camera size must be positive");
+  f->width = cam->width;
+  f->height = cam->height;
+  f->tiles_x = (cam->width + kTile - 1) / kTile;
+  f->tiles_y = (cam->height + kTile - 1) / kTile;
+  if (f->tiles_x > 65535 || f->tiles_y > 65535) return fail(GSB_ERR_INVALID_ARGUMENT, "image too large");
+  f->camera = *cam;
+  f->config = *cfg;
+  for (int c = 0; c < 3; ++c) f->background[c] = bg ? bg[c] : 0.0;
+  f->n_gaussians = cloud->n;
+  f->cloud = cloud;
+  f->fingerprint = fingerprint(cloud, cam);
+  f->cloud_version = cloud->version;
+  f->valid = false;
+  f->has_dimage = false;
+  GSB_RESERVE(f->cam, sizeof(CamDev));
+  CamDev cd = make_camdev(cam, kTile);
+  CamDev* h = static_cast<CamDev*>(pinned(ctx, sizeof(CamDev)));
+  if (!h) return fail(GSB_ERR_OUT_OF_MEMORY, "pinned staging");
+  *h = cd;
+  GSB_CUDA(cudaMemcpyAsync(f->cam.p, h, sizeof(CamDev), cudaMemcpyHostToDevice, ctx->stream));
+  return GSB_OK;
+}
+
+// planar FP32 [3][P] -> interleaved FP64 host
+static int download_image(gsb_ctx* ctx, const float* dev_planes, int W, int H, double* out) {
+  const size_t P = (size_t)W * H;
+  float* h = static_cast<float*>(pinned(ctx, sizeof(float) * 3 * P));
+  if (!h) return fail(GSB_ERR_OUT_OF_MEMORY, "pinned staging");
+  GSB_CUDA(cudaMemcpyAsync(h, dev_planes, sizeof(float) * 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (size_t p = 0; p < P; ++p) {
+    out[3 * p] = h[p];
+    out[3 * p + 1] = h[P + p];
+    out[3 * p + 2] = h[2 * P + p];
+  }
+  return GSB_OK;
+}
+// interleaved FP64 host -> planar FP32 device
+static int upload_image(gsb_ctx* ctx, const double* img, int W, int H, float* dev_planes) {
+  const size_t P = (size_t)W * H;
+  float* h = static_cast<float*>(pinned(ctx, sizeof(float) * 3 * P));
+  if (!h) return fail(GSB_ERR_OUT_OF_MEMORY, "pinned staging");
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));  // staging buffer reuse
+  for (size_t p = 0; p < P; ++p) {
+    h[p] = (float)img[3 * p];
+    h[P + p] = (float)img[3 * p + 1];
+    h[2 * P + p] = (float)img[3 * p + 2];
+  }
+  GSB_CUDA(cudaMemcpyAsync(dev_planes, h, sizeof(float) * 3 * P, cudaMemcpyHostToDevice, ctx->stream));
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return GSB_OK;
+}
+
+static int loss_device(gsb_ctx* ctx, gsb_frame* f, const float* target, double beta, bool want_grad) {
+  const int W = f->width, H = f->height;
+  const int64_t P = (int64_t)W * H;
+  GSB_RESERVE(f->gmaps, sizeof(float) * 9 * std::max<int64_t>(P, 1));
+  GSB_RESERVE(f->loss_blocks, sizeof(double) * 2 * loss_block_count(W, H));
+  GSB_RESERVE(f->loss_val, sizeof(double) * 4);
+  if (want_grad) GSB_RESERVE(f->d_image, sizeof(float) * 3 * std::max<int64_t>(P, 1));
+  StageScope sc(ctx, kStLoss);
+  int r = launch_rgb_loss(ctx->stream, f->image.as<float>(), target, W, H, beta, f->gmaps.as<float>(),
+                          f->loss_blocks.as<double>(), f->loss_val.as<double>(), want_grad ? f->d_image.as<float>() : nullptr,
+                          &ctx->launches);
+  if (r) return r;
+  if (want_grad) f->has_dimage = true;
+  return GSB_OK;
+}
+
+static int backward_device(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, bool full, float* grads) {
+  const int64_t k = f->n_entries;
+  GSB_RESERVE(f->partials, sizeof(float) * kPartial * std::max<int64_t>(k, 1));
+  GSB_RESERVE(f->pose_blocks, sizeof(double) * 6 * ((cloud->n + 255) / 256 + 1));
+  GSB_RESERVE(f->d_pose, sizeof(double) * 6);
+  const RasterDev rc = make_rasterdev(&f->config);
+  {
+    StageScope sc(ctx, kStBwdRaster);
+    int r = launch_backward_raster(ctx->stream, f, rc);
+    if (r) return r;
+    ctx->launches += f->tiles_x * f->tiles_y > 0 ? 1 : 0;
+  }
+  {
+    StageScope sc(ctx, kStBwdGeom);
+    int r = launch_backward_geom(ctx->stream, cloud, f, rc, full, grads, &ctx->launches);
+    if (r) return r;
+  }
+  return GSB_OK;
+}
+
+}  // namespace gsb
+
+using namespace gsb;
+
+// ===================================================================== ABI
+extern "C" {
+
+const char* gsb_last_error(void) { return gsb::g_error.c_str(); }
+const char* gsb_version(void) { return "gsb200 0.1 (sm_100a)"; }
+
+void gsb_default_raster_config(gsb_raster_config* c) {  // rasterizer.hpp:30-38
+  c->tile_size = 16;
+  c->cutoff_sigma = 3.0;
+  c->alpha_clamp = 0.99;
+  c->dilation = 0.3;
+  c->early_termination = 1e-4;
+  c->z_near = 0.01;
+  c->deterministic = 1;
+}
+void gsb_default_pose_config(gsb_pose_config* c) {  // trainer.hpp:21-60
+  c->cam_lr_start = 1e-2;
+  c->cam_lr_end = 1e-4;
+  c->beta = 0.2;
+  c->pose_converged_eps = 1e-7;
+  c->background[0] = c->background[1] = c->background[2] = 0.0;
+  gsb_default_raster_config(&c->raster);
+  c->budget = 1000;
+}
+
+int gsb_ctx_create(int32_t device, gsb_ctx** out) {
+  if (!out) return fail(GSB_ERR_INVALID_ARGUMENT, "null out");
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) return fail(GSB_ERR_NO_DEVICE, "no CUDA device visible (no CPU fallback exists)");
+  if (device < 0 || device >= ndev) return fail(GSB_ERR_INVALID_ARGUMENT, "device index out of range");
+  GSB_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  GSB_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10) return fail(GSB_ERR_NO_DEVICE, "device is not sm_100 class (this build targets sm_100a only)");
+  gsb_ctx* c = new gsb_ctx();
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "cudaStreamCreate");
+  }
+  c->timer = new StageTimer();
+  *out = c;
+  return GSB_OK;
+}
+
+int gsb_ctx_destroy(gsb_ctx* ctx) {
+  if (!ctx) return GSB_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  ctx->scratch_small.release();
+  if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
+  delete ctx->timer;
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return GSB_OK;
+}
+
+int gsb_ctx_synchronize(gsb_ctx* ctx) {
+  if (int r = ensure_device(ctx)) return r;
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return GSB_OK;
+}
+
+int gsb_ctx_set_profiling(gsb_ctx* ctx, int32_t enable) {
+  if (int r = ensure_device(ctx)) return r;
+  ctx->profiling = enable != 0;
+  return GSB_OK;
+}
+
+int gsb_ctx_stage_times(gsb_ctx* ctx, double* ms_out, int64_t* launches_out, int32_t reset) {
+  if (int r = ensure_device(ctx)) return r;
+  GSB_CUDA(ctx->timer->collect());
+  for (int k = 0; k < kNumStages; ++k) {
+    if (ms_out) ms_out[k] = ctx->timer->ms[k];
+    if (launches_out) launches_out[k] = ctx->timer->count[k];
+  }
+  if (reset) ctx->timer->reset();
+  return GSB_OK;
+}
+
+int64_t gsb_ctx_launch_count(gsb_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+// ------------------------------------------------------------------ cloud
+int gsb_cloud_create(gsb_ctx* ctx, int64_t n, int32_t sh_degree, gsb_cloud** out) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!out || n < 0 || sh_degree < 0 || sh_degree > 3) return fail(GSB_ERR_INVALID_ARGUMENT, "bad cloud shape");
+  if (n > (int64_t)0x7fffffff) return fail(GSB_ERR_INVALID_ARGUMENT, "cloud too large for int32 ids");
+  gsb_cloud* c = new gsb_cloud();
+  c->ctx = ctx;
+  c->n = n;
+  c->n_pad = std::max<int64_t>(32, (n + 31) / 32 * 32);
+  c->sh_degree = sh_degree;
+  c->active_sh_degree = sh_degree;
+  cudaError_t e = c->params.reserve(sizeof(float) * num_planes(sh_degree) * c->n_pad);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "cloud alloc");
+  }
+  cudaMemsetAsync(c->params.p, 0, sizeof(float) * num_planes(sh_degree) * c->n_pad, ctx->stream);
+  *out = c;
+  return GSB_OK;
+}
+
+int gsb_cloud_destroy(gsb_cloud* c) {
+  if (!c) return GSB_OK;
+  cudaSetDevice(c->ctx->device);
+  cudaStreamSynchronize(c->ctx->stream);
+  c->params.release();
+  delete c;
+  return GSB_OK;
+}
+
+int gsb_cloud_upload(gsb_cloud* c, const double* means, const double* rotations, const double* log_scales,
+                     const double* opacity_logits, const double* sh, int32_t active) {
+  if (!c) return fail(GSB_ERR_INVALID_ARGUMENT, "null cloud");
+  gsb_ctx* ctx = c->ctx;
+  if (int r = ensure_device(ctx)) return r;
+  const int64_t n = c->n, np = c->n_pad;
+  const int B = (c->sh_degree + 1) * (c->sh_degree + 1);
+  const int NP = num_planes(c->sh_degree);
+  if (n > 0 && (!means || !rotations || !log_scales || !opacity_logits || !sh))
+    return fail(GSB_ERR_INVALID_ARGUMENT, "null parameter array");
+  for (int64_t i = 0; i < n; ++i) {  // GaussianCloud::validate (scene.cpp:135-148)
+    bool ok = std::isfinite(means[3 * i]) && std::isfinite(means[3 * i + 1]) && std::isfinite(means[3 * i + 2]) &&
+              std::isfinite(log_scales[3 * i]) && std::isfinite(log_scales[3 * i + 1]) &&
+              std::isfinite(log_scales[3 * i + 2]) && std::isfinite(opacity_logits[i]);
+    for (int k = 0; k < 4; ++k) ok = ok && std::isfinite(rotations[4 * i + k]);
+    if (!ok) return fail(GSB_ERR_DIVERGED, "GaussianCloud: non-finite parameter at index " + std::to_string(i));
+  }
+  float* h = static_cast<float*>(pinned(ctx, sizeof(float) * NP * np));
+  if (!h) return fail(GSB_ERR_OUT_OF_MEMORY, "pinned staging");
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::memset(h, 0, sizeof(float) * NP * np);
+  for (int64_t i = 0; i < n; ++i) {
+    for (int k = 0; k < 3; ++k) h[(kMeanX + k) * np + i] = (float)means[3 * i + k];
+    for (int k = 0; k < 4; ++k) h[(kQuatW + k) * np + i] = (float)rotations[4 * i + k];
+    for (int k = 0; k < 3; ++k) h[(kScaleX + k) * np + i] = (float)log_scales[3 * i + k];
+    h[kOpacity * np + i] = (float)opacity_logits[i];
+    const double* s = sh + (size_t)i * 3 * B;
+    for (int k = 0; k < 3 * B; ++k) h[(kShBase + k) * np + i] = (float)s[k];
+  }
+  GSB_CUDA(cudaMemcpyAsync(c->params.p, h, sizeof(float) * NP * np, cudaMemcpyHostToDevice, ctx->stream));
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  c->active_sh_degree = std::min(std::max(active, 0), c->sh_degree);
+  // content hash of the uploaded FP64 arrays at 64 strided samples (rasterizer.cpp:62-71)
+  uint64_t hsh = 0xcbf29ce484222325ull;
+  const int64_t stride = std::max<int64_t>(1, n / 64);
+  for (int64_t i = 0; i < n; i += stride) {
+    hsh = fnv1a(hsh, means + 3 * i, sizeof(double) * 3);
+    hsh = fnv1a(hsh, rotations + 4 * i, sizeof(double) * 4);
+    hsh = fnv1a(hsh, log_scales + 3 * i, sizeof(double) * 3);
+    hsh = fnv1a(hsh, opacity_logits + i, sizeof(double));
+    hsh = fnv1a(hsh, sh + (size_t)i * 3 * B, sizeof(double) * 3 * B);
+  }
+  c->host_fingerprint = hsh;
+  c->version += 1;
+  return GSB_OK;
+}
+
+int gsb_cloud_download(gsb_cloud* c, double* means, double* rotations, double* log_scales, double* opacity_logits,
+                       double* sh) {
+  if (!c) return fail(GSB_ERR_INVALID_ARGUMENT, "null cloud");
+  gsb_ctx* ctx = c->ctx;
+  if (int r = ensure_device(ctx)) return r;
+  const int64_t n = c->n, np = c->n_pad;
+  const int B = (c->sh_degree + 1) * (c->sh_degree + 1);
+  const int NP = num_planes(c->sh_degree);
+  float* h = static_cast<float*>(pinned(ctx, sizeof(float) * NP * np));
+  if (!h) return fail(GSB_ERR_OUT_OF_MEMORY, "pinned staging");
+  GSB_CUDA(cudaMemcpyAsync(h, c->params.p, sizeof(float) * NP * np, cudaMemcpyDeviceToHost, ctx->stream));
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int64_t i = 0; i < n; ++i) {
+    if (means) for (int k = 0; k < 3; ++k) means[3 * i + k] = h[(kMeanX + k) * np + i];
+    if (rotations) for (int k = 0; k < 4; ++k) rotations[4 * i + k] = h[(kQuatW + k) * np + i];
+    if (log_scales) for (int k = 0; k < 3; ++k) log_scales[3 * i + k] = h[(kScaleX + k) * np + i];
+    if (opacity_logits) opacity_logits[i] = h[kOpacity * np + i];
+    if (sh) for (int k = 0; k < 3 * B; ++k) sh[(size_t)i * 3 * B + k] = h[(kShBase + k) * np + i];
+  }
+  return GSB_OK;
+}
+
+int gsb_cloud_info(gsb_cloud* c, int64_t* n, int32_t* deg, int32_t* active) {
+  if (!c) return fail(GSB_ERR_INVALID_ARGUMENT, "null cloud");
+  if (n) *n = c->n;
+  if (deg) *deg = c->sh_degree;
+  if (active) *active = c->active_sh_degree;
+  return GSB_OK;
+}
+
+int gsb_cloud_set_active_sh_degree(gsb_cloud* c, int32_t active) {
+  if (!c) return fail(GSB_ERR_INVALID_ARGUMENT, "null cloud");
+  c->active_sh_degree = std::min(std::max(active, 0), c->sh_degree);
+  c->version += 1;
+  return GSB_OK;
+}
+
+// ------------------------------------------------------------------ frame
+int gsb_frame_create(gsb_ctx* ctx, gsb_frame** out) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!out) return fail(GSB_ERR_INVALID_ARGUMENT, "null out");
+  gsb_frame* f = new gsb_frame();
+  f->ctx = ctx;
+  *out = f;
+  return GSB_OK;
+}
+
+int gsb_frame_destroy(gsb_frame* f) {
+  if (!f) return GSB_OK;
+  cudaSetDevice(f->ctx->device);
+  cudaStreamSynchronize(f->ctx->stream);
+  DevBuf* bufs[] = {&f->cam, &f->rec_g, &f->rect_g, &f->cnt_g, &f->depth_g, &f->radius_g, &f->rank_of_g,
+                    &f->vis_idx, &f->dkey[0], &f->dkey[1], &f->dval[0], &f->dval[1], &f->rec, &f->aux,
+                    &f->cnt_r, &f->ekey[0], &f->ekey[1], &f->eval_[0], &f->eval_[1], &f->ranges, &f->image,
+                    &f->final_t, &f->pixstate, &f->d_image, &f->partials, &f->pose_blocks, &f->d_pose,
+                    &f->loss_blocks, &f->loss_val, &f->gmaps, &f->scan_tmp, &f->sort_hist, &f->counters};
+  for (DevBuf* b : bufs) b->release();
+  delete f;
+  return GSB_OK;
+}
+
+int gsb_render(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, const double bg[3],
+               const gsb_raster_config* cfg, gsb_frame* f, double* image_out) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!cloud || !cam || !f) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  gsb_raster_config dflt;
+  gsb_default_raster_config(&dflt);
+  if (!cfg) cfg = &dflt;
+  if (int r = validate_config(cfg)) return r;
+  if (int r = frame_setup(ctx, f, cloud, cam, bg, cfg)) return r;
+  const RasterDev rc = make_rasterdev(cfg);
+  if (int r = render_device(ctx, cloud, f, rc)) return r;
+  f->valid = true;
+  if (image_out) return download_image(ctx, f->image.as<float>(), f->width, f->height, image_out);
+  return GSB_OK;
+}
+
+int gsb_frame_get_info(gsb_frame* f, gsb_frame_info* info) {
+  if (!f || !info) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  info->n_gaussians = f->n_gaussians;
+  info->n_splats = f->n_splats;
+  info->n_entries = f->n_entries;
+  info->width = f->width;
+  info->height = f->height;
+  info->tiles_x = f->tiles_x;
+  info->tiles_y = f->tiles_y;
+  info->state_fingerprint = f->fingerprint;
+  return GSB_OK;
+}
+
+int gsb_frame_download(gsb_frame* f, double* image, double* accum_t, double* final_t, int32_t* contrib,
+                       uint8_t* overflow, int32_t* s_gauss, double* s_mu2d, double* s_depth, double* s_conic,
+                       double* s_color, double* s_opacity, double* s_radius, uint8_t* s_clamped, int32_t* tile_lists,
+                       int32_t* tile_ranges) {
+  if (!f || !f->valid) return fail(GSB_ERR_INVALID_ARGUMENT, "frame holds no forward state");
+  gsb_ctx* ctx = f->ctx;
+  if (int r = ensure_device(ctx)) return r;
+  const int64_t P = (int64_t)f->width * f->height, V = f->n_splats, K = f->n_entries;
+  const int T = f->tiles_x * f->tiles_y;
+  if (image)
+    if (int r = download_image(ctx, f->image.as<float>(), f->width, f->height, image)) return r;
+  std::vector<float> ft(P);
+  std::vector<uint32_t> ps(P);
+  GSB_CUDA(cudaMemcpyAsync(ft.data(), f->final_t.p, sizeof(float) * P, cudaMemcpyDeviceToHost, ctx->stream));
+  GSB_CUDA(cudaMemcpyAsync(ps.data(), f->pixstate.p, sizeof(uint32_t) * P, cudaMemcpyDeviceToHost, ctx->stream));
+  std::vector<SplatRec> rec(V);
+  std::vector<SplatAux> aux(V);
+  if (V > 0) {
+    GSB_CUDA(cudaMemcpyAsync(rec.data(), f->rec.p, sizeof(SplatRec) * V, cudaMemcpyDeviceToHost, ctx->stream));
+    GSB_CUDA(cudaMemcpyAsync(aux.data(), f->aux.p, sizeof(SplatAux) * V, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  std::vector<double> depth_g(f->n_gaussians), radius_g(f->n_gaussians);
+  if (f->n_gaussians > 0 && (s_depth || s_radius)) {
+    GSB_CUDA(cudaMemcpyAsync(depth_g.data(), f->depth_g.p, sizeof(double) * f->n_gaussians, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    GSB_CUDA(cudaMemcpyAsync(radius_g.data(), f->radius_g.p, sizeof(double) * f->n_gaussians,
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  if (tile_lists && K > 0)
+    GSB_CUDA(cudaMemcpyAsync(tile_lists, f->eval_[f->sorted_sel].p, sizeof(uint32_t) * K, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  if (tile_ranges && T > 0)
+    GSB_CUDA(cudaMemcpyAsync(tile_ranges, f->ranges.p, sizeof(uint2) * T, cudaMemcpyDeviceToHost, ctx->stream));
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int64_t p = 0; p < P; ++p) {
+    if (final_t) final_t[p] = ft[p];
+    if (accum_t) accum_t[p] = 1.0 - (double)ft[p];  // rasterizer.cpp:271-273
+    if (contrib) contrib[p] = (int32_t)(ps[p] & 0x1fffffffu);
+    if (overflow) overflow[p] = (uint8_t)(ps[p] >> 29);
+  }
+  for (int64_t r = 0; r < V; ++r) {
+    const int gid = aux[r].gid;
+    if (s_gauss) s_gauss[r] = gid;
+    if (s_mu2d) {
+      s_mu2d[2 * r] = rec[r].mu_x;
+      s_mu2d[2 * r + 1] = rec[r].mu_y;
+    }
+    if (s_depth) s_depth[r] = depth_g[gid];
+    if (s_radius) s_radius[r] = radius_g[gid];
+    if (s_conic) {
+      s_conic[4 * r] = rec[r].conic_a;
+      s_conic[4 * r + 1] = rec[r].conic_b;
+      s_conic[4 * r + 2] = rec[r].conic_b;
+      s_conic[4 * r + 3] = rec[r].conic_c;
+    }
+    if (s_color) {
+      s_color[3 * r] = rec[r].col_r;
+      s_color[3 * r + 1] = rec[r].col_g;
+      s_color[3 * r + 2] = rec[r].col_b;
+    }
+    if (s_opacity) s_opacity[r] = rec[r].opacity;
+    if (s_clamped) s_clamped[r] = (uint8_t)rec[r].clamp_bits;
+  }
+  return GSB_OK;
+}
+
+// ------------------------------------------------------------------- loss
+int gsb_image_create(gsb_ctx* ctx, const double* img, int32_t W, int32_t H, gsb_image** out) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!img || !out || W <= 0 || H <= 0) return fail(GSB_ERR_INVALID_ARGUMENT, "bad image");
+  gsb_image* im = new gsb_image();
+  im->ctx = ctx;
+  im->width = W;
+  im->height = H;
+  cudaError_t e = im->planes.reserve(sizeof(float) * 3 * (size_t)W * H);
+  if (e != cudaSuccess) {
+    delete im;
+    return cuda_fail(e, "image alloc");
+  }
+  if (int r = upload_image(ctx, img, W, H, im->planes.as<float>())) {
+    im->planes.release();
+    delete im;
+    return r;
+  }
+  *out = im;
+  return GSB_OK;
+}
+
+int gsb_image_destroy(gsb_image* im) {
+  if (!im) return GSB_OK;
+  cudaSetDevice(im->ctx->device);
+  cudaStreamSynchronize(im->ctx->stream);
+  im->planes.release();
+  delete im;
+  return GSB_OK;
+}
+
+int gsb_rgb_loss(gsb_ctx* ctx, const double* rendered, const double* target, int32_t W, int32_t H, double beta,
+                 double* loss_out, double* d_rendered) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!rendered || !target || W <= 0 || H <= 0) return fail(GSB_ERR_INVALID_ARGUMENT, "bad images");
+  static thread_local gsb_frame* work = nullptr;
+  static thread_local DevBuf tgt;
+  if (!work || work->ctx != ctx) {
+    work = new gsb_frame();
+    work->ctx = ctx;
+  }
+  work->width = W;
+  work->height = H;
+  const int64_t P = (int64_t)W * H;
+  GSB_RESERVE(work->image, sizeof(float) * 3 * P);
+  GSB_RESERVE(tgt, sizeof(float) * 3 * P);
+  if (int r = upload_image(ctx, rendered, W, H, work->image.as<float>())) return r;
+  if (int r = upload_image(ctx, target, W, H, tgt.as<float>())) return r;
+  if (int r = loss_device(ctx, work, tgt.as<float>(), beta, d_rendered != nullptr)) return r;
+  double out3[4];
+  GSB_CUDA(cudaMemcpyAsync(out3, work->loss_val.p, sizeof(double) * 3, cudaMemcpyDeviceToHost, ctx->stream));
+  if (d_rendered)
+    if (int r = download_image(ctx, work->d_image.as<float>(), W, H, d_rendered)) return r;
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (loss_out) *loss_out = out3[2];
+  return GSB_OK;
+}
+
+int gsb_frame_rgb_loss(gsb_ctx* ctx, gsb_frame* f, gsb_image* target, double beta, double* loss_out) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!f || !f->valid || !target) return fail(GSB_ERR_INVALID_ARGUMENT, "frame / target missing");
+  if (target->width != f->width || target->height != f->height)
+    return fail(GSB_ERR_DIMENSION_MISMATCH, "rgb_loss: image shapes differ");
+  if (int r = loss_device(ctx, f, target->planes.as<float>(), beta, true)) return r;
+  if (loss_out) {
+    double out3[4];
+    GSB_CUDA(cudaMemcpyAsync(out3, f->loss_val.p, sizeof(double) * 3, cudaMemcpyDeviceToHost, ctx->stream));
+    GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    *loss_out = out3[2];
+  }
+  return GSB_OK;
+}
+
+// ---------------------------------------------------------------- backward
+int gsb_grads_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_grads** out) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!cloud || !out) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  gsb_grads* g = new gsb_grads();
+  g->ctx = ctx;
+  g->n = cloud->n;
+  g->n_pad = cloud->n_pad;
+  g->sh_degree = cloud->sh_degree;
+  cudaError_t e = g->planes.reserve(sizeof(float) * (num_planes(cloud->sh_degree) + 2) * cloud->n_pad);
+  if (e == cudaSuccess) e = g->pose.reserve(sizeof(double) * 6);
+  if (e != cudaSuccess) {
+    g->planes.release();
+    delete g;
+    return cuda_fail(e, "grads alloc");
+  }
+  *out = g;
+  return GSB_OK;
+}
+
+int gsb_grads_destroy(gsb_grads* g) {
+  if (!g) return GSB_OK;
+  cudaSetDevice(g->ctx->device);
+  cudaStreamSynchronize(g->ctx->stream);
+  g->planes.release();
+  g->pose.release();
+  delete g;
+  return GSB_OK;
+}
+
+int gsb_grads_download(gsb_grads* g, double* d_means, double* d_rot, double* d_ls, double* d_op, double* d_sh,
+                       double* d_mu2d, double d_pose[6]) {
+  if (!g || !g->valid) return fail(GSB_ERR_INVALID_ARGUMENT, "grads hold no result");
+  gsb_ctx* ctx = g->ctx;
+  if (int r = ensure_device(ctx)) return r;
+  const int64_t n = g->n, np = g->n_pad;
+  const int NP = num_planes(g->sh_degree);
+  const int B = (g->sh_degree + 1) * (g->sh_degree + 1);
+  std::vector<float> h((size_t)(NP + 2) * np);
+  GSB_CUDA(cudaMemcpyAsync(h.data(), g->planes.p, sizeof(float) * h.size(), cudaMemcpyDeviceToHost, ctx->stream));
+  double pose[6];
+  GSB_CUDA(cudaMemcpyAsync(pose, g->pose.p, sizeof(double) * 6, cudaMemcpyDeviceToHost, ctx->stream));
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int64_t i = 0; i < n; ++i) {
+    if (d_means) for (int k = 0; k < 3; ++k) d_means[3 * i + k] = h[(kMeanX + k) * np + i];
+    if (d_rot) for (int k = 0; k < 4; ++k) d_rot[4 * i + k] = h[(kQuatW + k) * np + i];
+    if (d_ls) for (int k = 0; k < 3; ++k) d_ls[3 * i + k] = h[(kScaleX + k) * np + i];
+    if (d_op) d_op[i] = h[kOpacity * np + i];
+    if (d_sh) for (int k = 0; k < 3 * B; ++k) d_sh[(size_t)i * 3 * B + k] = h[(kShBase + k) * np + i];
+    if (d_mu2d) {
+      d_mu2d[2 * i] = h[(size_t)NP * np + i];
+      d_mu2d[2 * i + 1] = h[(size_t)(NP + 1) * np + i];
+    }
+  }
+  if (d_pose) for (int k = 0; k < 6; ++k) d_pose[k] = pose[k];
+  return GSB_OK;
+}
+
+static int backward_common(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, gsb_frame* f, uint32_t flags,
+                           gsb_grads* grads, double d_pose_out[6]) {
+  const bool full = !(flags & GSB_BWD_POSE_ONLY);
+  if (full && !grads) return fail(GSB_ERR_INVALID_ARGUMENT, "full backward needs a grads object");
+  if (grads && grads->n != cloud->n) return fail(GSB_ERR_DIMENSION_MISMATCH, "grads / cloud size mismatch");
+  if (int r = backward_device(ctx, cloud, f, full, full ? grads->planes.as<float>() : nullptr)) return r;
+  if (grads) {
+    GSB_CUDA(cudaMemcpyAsync(grads->pose.p, f->d_pose.p, sizeof(double) * 6, cudaMemcpyDeviceToDevice, ctx->stream));
+    grads->valid = true;
+  }
+  if (d_pose_out) {
+    double h[6];
+    GSB_CUDA(cudaMemcpyAsync(h, f->d_pose.p, sizeof(double) * 6, cudaMemcpyDeviceToHost, ctx->stream));
+    GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int k = 0; k < 6; ++k) d_pose_out[k] = h[k];
+  }
+  return GSB_OK;
+}
+
+static int check_state(gsb_cloud* cloud, const gsb_camera* cam, gsb_frame* f) {
+  if (!f->valid || f->fingerprint != fingerprint(cloud, cam) || f->n_gaussians != cloud->n || f->cloud != cloud)
+    return fail(GSB_ERR_STATE_MISMATCH, "render_backward: output does not match (cloud, camera)");
+  return GSB_OK;
+}
+
+int gsb_render_backward(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, gsb_frame* f, const double* d_image,
+                        int32_t W, int32_t H, uint32_t flags, gsb_grads* grads, double d_pose_out[6]) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!cloud || !cam || !f || !d_image) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  if (int r = check_state(cloud, cam, f)) return r;  // rasterizer.cpp:338-340
+  if (W != cam->width || H != cam->height)
+    return fail(GSB_ERR_DIMENSION_MISMATCH, "render_backward: d_image size mismatch");  // 341-343
+  GSB_RESERVE(f->d_image, sizeof(float) * 3 * (size_t)W * H);
+  if (int r = upload_image(ctx, d_image, W, H, f->d_image.as<float>())) return r;
+  f->has_dimage = true;
+  return backward_common(ctx, cloud, cam, f, flags, grads, d_pose_out);
+}
+
+int gsb_render_backward_device(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, gsb_frame* f, uint32_t flags,
+                               gsb_grads* grads, double d_pose_out[6]) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!cloud || !cam || !f) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  if (int r = check_state(cloud, cam, f)) return r;
+  if (!f->has_dimage) return fail(GSB_ERR_INVALID_ARGUMENT, "no upstream gradient in frame (run gsb_frame_rgb_loss)");
+  return backward_common(ctx, cloud, cam, f, flags, grads, d_pose_out);
+}
+
+// --------------------------------------------------------------- optimiser
+double gsb_schedule(int32_t kind, double start, double end, int64_t step, int64_t total) {  // trainer.cpp:30-38
+  if (total <= 0) return end;
+  double s = std::clamp((double)step / (double)total, 0.0, 1.0);
+  if (kind == 0) return end + (start - end) * 0.5 * (1.0 + std::cos(M_PI * s));
+  return start * std::pow(end / start, s);
+}
+
+int gsb_pose_step(gsb_ctx* ctx, const double pose[12], const double d_pose[6], double lr, gsb_pose_adam* state,
+                  double pose_out[12], double applied[6]) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!pose || !d_pose || !state || !pose_out) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  const size_t sb = pose_state_bytes();
+  char* h = static_cast<char*>(pinned(ctx, sb + 64));
+  if (!h) return fail(GSB_ERR_OUT_OF_MEMORY, "pinned staging");
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  pose_state_init(h, pose);
+  pose_state_set_adam(h, state->m, state->v, state->step);
+  double* hd = reinterpret_cast<double*>(h + ((sb + 15) / 16) * 16);
+  for (int k = 0; k < 6; ++k) hd[k] = d_pose[k];
+  GSB_RESERVE(ctx->scratch_small, 4096);
+  char* dev = ctx->scratch_small.as<char>();
+  const size_t off = ((sb + 15) / 16) * 16;
+  GSB_CUDA(cudaMemcpyAsync(dev, h, off + sizeof(double) * 6, cudaMemcpyHostToDevice, ctx->stream));
+  if (int r = launch_pose_step(ctx->stream, dev, reinterpret_cast<double*>(dev + off), lr, 1)) return r;
+  ctx->launches += 1;
+  GSB_CUDA(cudaMemcpyAsync(h, dev, sb, cudaMemcpyDeviceToHost, ctx->stream));
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  double cur[12], app[6];
+  pose_state_read(h, nullptr, cur, nullptr, nullptr, nullptr, nullptr, app, state->m, state->v, &state->step);
+  bool zero = true;
+  for (int k = 0; k < 6; ++k) zero = zero && app[k] == 0.0;
+  for (int k = 0; k < 12; ++k) pose_out[k] = zero ? pose[k] : cur[k];  // trainer.cpp:86 (bitwise identity)
+  if (applied) for (int k = 0; k < 6; ++k) applied[k] = app[k];
+  return GSB_OK;
+}
+
+int gsb_adam_step(gsb_ctx* ctx, double* params, const double* grads, double* m, double* v, int64_t* step, int64_t n,
+                  double lr) {
+  if (int r = ensure_device(ctx)) return r;
+  if (n < 0 || (n > 0 && (!params || !grads || !m || !v)) || !step) return fail(GSB_ERR_INVALID_ARGUMENT, "bad adam args");
+  *step += 1;
+  if (n == 0) return GSB_OK;
+  DevBuf buf;
+  GSB_CUDA(buf.reserve(sizeof(double) * 4 * n));
+  double* d = buf.as<double>();
+  GSB_CUDA(cudaMemcpyAsync(d, params, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  GSB_CUDA(cudaMemcpyAsync(d + n, grads, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  GSB_CUDA(cudaMemcpyAsync(d + 2 * n, m, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  GSB_CUDA(cudaMemcpyAsync(d + 3 * n, v, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  int r = launch_adam_f64(ctx->stream, d, d + n, d + 2 * n, d + 3 * n, n, lr, *step);
+  if (r) {
+    buf.release();
+    return r;
+  }
+  ctx->launches += 1;
+  GSB_CUDA(cudaMemcpyAsync(params, d, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  GSB_CUDA(cudaMemcpyAsync(m, d + 2 * n, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  GSB_CUDA(cudaMemcpyAsync(v, d + 3 * n, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  buf.release();
+  return GSB_OK;
+}
+
+int gsb_adam_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_adam** out) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!cloud || !out) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  gsb_adam* a = new gsb_adam();
+  a->ctx = ctx;
+  a->n = cloud->n;
+  a->n_pad = cloud->n_pad;
+  a->sh_degree = cloud->sh_degree;
+  const size_t bytes = sizeof(float) * num_planes(cloud->sh_degree) * cloud->n_pad;
+  cudaError_t e = a->m.reserve(bytes);
+  if (e == cudaSuccess) e = a->v.reserve(bytes);
+  if (e != cudaSuccess) {
+    a->m.release();
+    a->v.release();
+    delete a;
+    return cuda_fail(e, "adam alloc");
+  }
+  cudaMemsetAsync(a->m.p, 0, bytes, ctx->stream);
+  cudaMemsetAsync(a->v.p, 0, bytes, ctx->stream);
+  *out = a;
+  return GSB_OK;
+}
+
+int gsb_adam_destroy(gsb_adam* a) {
+  if (!a) return GSB_OK;
+  cudaSetDevice(a->ctx->device);
+  cudaStreamSynchronize(a->ctx->stream);
+  a->m.release();
+  a->v.release();
+  delete a;
+  return GSB_OK;
+}
+
+int gsb_cloud_adam_step(gsb_ctx* ctx, gsb_cloud* cloud, gsb_grads* grads, gsb_adam* adam, const double lrs[6]) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!cloud || !grads || !adam || !lrs) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  if (grads->n != cloud->n || adam->n != cloud->n) return fail(GSB_ERR_DIMENSION_MISMATCH, "adam/grads/cloud sizes");
+  if (cloud->n == 0) return GSB_OK;
+  for (int k = 0; k < 5; ++k) adam->step[k] += 1;
+  StageScope sc(ctx, kStOptim);
+  int r = launch_cloud_adam(ctx->stream, cloud->params.as<float>(), grads->planes.as<float>(), adam->m.as<float>(),
+                            adam->v.as<float>(), cloud->n, cloud->n_pad, cloud->sh_degree, lrs, adam->step);
+  if (r) return r;
+  ctx->launches += 1;
+  cloud->version += 1;
+  return GSB_OK;
+}
+
+// ------------------------------------------------------- estimate_pose
+int gsb_estimate_pose(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* target, const double intr[4],
+                      const double init_pose[12], const gsb_pose_config* cfg, double pose_out[12], double* final_loss,
+                      int32_t* steps_used, int32_t* converged, double* trace_pose, double* trace_loss) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!cloud || !target || !intr || !init_pose || !cfg || !pose_out)
+    return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  if (int r = validate_config(&cfg->raster)) return r;
+  if (cfg->budget <= 0) return fail(GSB_ERR_INVALID_CONFIG, "budget must be > 0");
+  static thread_local gsb_frame* fr = nullptr;
+  if (!fr || fr->ctx != ctx) {
+    fr = new gsb_frame();
+    fr->ctx = ctx;
+  }
+  gsb_frame* f = fr;
+  gsb_camera cam;
+  cam.fx = intr[0];
+  cam.fy = intr[1];
+  cam.cx = intr[2];
+  cam.cy = intr[3];
+  cam.width = target->width;
+  cam.height = target->height;
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c) cam.R[r * 3 + c] = init_pose[r * 4 + c];
+    cam.t[r] = init_pose[r * 4 + 3];
+  }
+  if (int r = frame_setup(ctx, f, cloud, &cam, cfg->background, &cfg->raster)) return r;
+  const RasterDev rc = make_rasterdev(&cfg->raster);
+  // device pose state + traces
+  const size_t sb = pose_state_bytes();
+  static thread_local DevBuf dstate, dtrace;
+  GSB_RESERVE(dstate, sb + 64);
+  GSB_RESERVE(dtrace, sizeof(double) * 13 * (size_t)cfg->budget + 64);
+  char* h = static_cast<char*>(pinned(ctx, sb + 64));
+  if (!h) return fail(GSB_ERR_OUT_OF_MEMORY, "pinned staging");
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  pose_state_init(h, init_pose);
+  GSB_CUDA(cudaMemcpyAsync(dstate.p, h, sb, cudaMemcpyHostToDevice, ctx->stream));
+  double* tp = dtrace.as<double>();
+  double* tl = tp + 12 * (size_t)cfg->budget;
+  int32_t stop = 0;
+  for (int it = 0; it < cfg->budget && !stop; ++it) {
+    if (int r = render_device(ctx, cloud, f, rc)) return r;
+    f->valid = true;
+    if (int r = loss_device(ctx, f, target->planes.as<float>(), cfg->beta, true)) return r;
+    if (int r = backward_device(ctx, cloud, f, false, nullptr)) return r;
+    {
+      StageScope sc(ctx, kStOptim);
+      if (int r = launch_pose_iter(ctx->stream, dstate.p, f->d_pose.as<double>(), f->loss_val.as<double>(),
+                                   cfg->cam_lr_start, cfg->cam_lr_end, cfg->pose_converged_eps, cfg->budget,
+                                   f->cam.as<CamDev>(), tp, tl))
+        return r;
+      ctx->launches += 1;
+    }
+    GSB_CUDA(cudaMemcpyAsync(h, dstate.p, sb, cudaMemcpyDeviceToHost, ctx->stream));
+    GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    pose_state_read(h, nullptr, nullptr, nullptr, nullptr, nullptr, &stop, nullptr, nullptr, nullptr, nullptr);
+  }
+  int32_t su = 0, cv = 0;
+  double fl = 0.0;
+  pose_state_read(h, pose_out, nullptr, &fl, &su, &cv, nullptr, nullptr, nullptr, nullptr, nullptr);
+  if (final_loss) *final_loss = fl;
+  if (steps_used) *steps_used = su;
+  if (converged) *converged = cv;
+  if (trace_pose && su > 0)
+    GSB_CUDA(cudaMemcpyAsync(trace_pose, tp, sizeof(double) * 12 * su, cudaMemcpyDeviceToHost, ctx->stream));
+  if (trace_loss && su > 0)
+    GSB_CUDA(cudaMemcpyAsync(trace_loss, tl, sizeof(double) * su, cudaMemcpyDeviceToHost, ctx->stream));
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return GSB_OK;
+}
+
+}  // extern "C"

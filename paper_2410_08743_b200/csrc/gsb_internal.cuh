@@ -1,0 +1,212 @@
+// gsb_internal.cuh — shared types, device layouts and launch helpers for
+// libgsb200 (B200 / sm_100a). See DESIGN.md for the HBM layout rationale.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/gsb200.h"
+
+namespace gsb {
+
+constexpr int kTile = 16;         // rasterizer tile (RasterConfig::tile_size, rasterizer.hpp:31)
+constexpr int kTilePix = kTile * kTile;
+constexpr int kMaxShCoeffs = 16;  // sh.hpp:10
+
+// Camera as the kernels read it (device resident so the pose step can update
+// it without a host round trip). R row-major world_to_cam, center = -R^T t.
+struct CamDev {
+  double fx, fy, cx, cy;
+  double R[9];
+  double t[3];
+  double center[3];
+  int32_t width, height, tiles_x, tiles_y;
+};
+
+struct RasterDev {
+  float cutoff2_f, alpha_clamp_f, early_term_f, pad;
+  double cutoff_sigma, alpha_clamp, dilation, early_termination, z_near;
+};
+
+// Per-splat record read by composite and the backward raster (rank order).
+// mu2d stays FP64 so the tile-local offset (mu - tile origin) is formed
+// without the ~3e-5 px FP32 rounding of absolute pixel coordinates.
+struct __align__(16) SplatRec {
+  double mu_x, mu_y;
+  float conic_a, conic_b, conic_c, opacity;  // conic_b = symmetric off-diagonal
+  float col_r, col_g, col_b;
+  uint32_t clamp_bits;
+};
+static_assert(sizeof(SplatRec) == 48, "SplatRec layout");
+
+// Per-splat bookkeeping (rank order): entry offset in the rank-major
+// (pre-sort) entry stream, tile rect origin and width, Gaussian id.
+struct __align__(16) SplatAux {
+  uint32_t off;
+  uint32_t tx0_ty0;  // tx0 | ty0 << 16
+  uint32_t nx_ny;    // nx  | ny  << 16
+  int32_t gid;
+};
+
+// Per-entry backward partial (PixelPartial, rasterizer.cpp:327-332) with the
+// symmetric d_conic folded to 3 values: (D00, D01 (=D10), D11).
+constexpr int kPartial = 9;  // d_mu2d(2) d_conic(3) d_color(3) d_opacity(1)
+
+// Parameter planes of a cloud: plane-major [P][n_pad] FP32.
+enum Plane : int {
+  kMeanX = 0, kMeanY, kMeanZ, kQuatW, kQuatX, kQuatY, kQuatZ, kScaleX, kScaleY, kScaleZ, kOpacity,
+  kShBase = 11
+};
+inline int num_planes(int sh_degree) { return kShBase + 3 * (sh_degree + 1) * (sh_degree + 1); }
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define GSB_CUDA(call)                                        \
+  do {                                                        \
+    cudaError_t e__ = (call);                                 \
+    if (e__ != cudaSuccess) return ::gsb::cuda_fail(e__, #call); \
+  } while (0)
+
+#define GSB_CHECK_LAUNCH(what)                                \
+  do {                                                        \
+    cudaError_t e__ = cudaGetLastError();                     \
+    if (e__ != cudaSuccess) return ::gsb::cuda_fail(e__, what); \
+  } while (0)
+
+// ---------------------------------------------------------------- buffers
+// Grow-only device buffer; contents are not preserved across growth.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t reserve(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    size_t cap = want + want / 4 + 256;
+    cudaError_t e = cudaMalloc(&p, cap);
+    if (e == cudaSuccess) bytes = cap;
+    return e;
+  }
+  template <typename T> T* as() const { return static_cast<T*>(p); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+// Stage ids for the per-stage device timers (bench roofline attribution).
+enum Stage : int {
+  kStPreprocess = 0, kStSort, kStComposite, kStLoss, kStBwdRaster, kStBwdGeom, kStOptim, kStOther, kNumStages
+};
+
+struct StageTimer;  // defined in api.cu
+
+}  // namespace gsb
+
+// ------------------------------------------------------------- C structs
+struct gsb_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  gsb::DevBuf scratch_small;   // pinned-size device scratch (counters, partial sums)
+  void* host_pinned = nullptr; // small pinned staging buffer
+  size_t host_pinned_bytes = 0;
+  int64_t launches = 0;
+  bool profiling = false;
+  gsb::StageTimer* timer = nullptr;
+};
+
+struct gsb_cloud {
+  gsb_ctx* ctx = nullptr;
+  int64_t n = 0;
+  int64_t n_pad = 0;
+  int32_t sh_degree = 0, active_sh_degree = 0;
+  gsb::DevBuf params;            // FP32 planes [num_planes][n_pad]
+  uint64_t host_fingerprint = 0; // FNV-1a sample hash of the last uploaded FP64 arrays
+  uint64_t version = 0;          // bumped by device-side updates (Adam)
+};
+
+struct gsb_image {
+  gsb_ctx* ctx = nullptr;
+  int32_t width = 0, height = 0;
+  gsb::DevBuf planes;  // FP32 [3][H*W]
+};
+
+struct gsb_grads {
+  gsb_ctx* ctx = nullptr;
+  int64_t n = 0, n_pad = 0;
+  int32_t sh_degree = 0;
+  gsb::DevBuf planes;  // FP32 [num_planes + 2 (d_mu2d)][n_pad]
+  gsb::DevBuf pose;    // double[6]
+  bool valid = false;
+};
+
+struct gsb_adam {
+  gsb_ctx* ctx = nullptr;
+  int64_t n = 0, n_pad = 0;
+  int32_t sh_degree = 0;
+  gsb::DevBuf m, v;    // FP32 planes like the cloud
+  int64_t step[5] = {0, 0, 0, 0, 0};
+};
+
+struct gsb_frame {
+  gsb_ctx* ctx = nullptr;
+  // bookkeeping
+  int64_t n_gaussians = 0, n_splats = 0, n_entries = 0;
+  int32_t width = 0, height = 0, tiles_x = 0, tiles_y = 0;
+  uint64_t fingerprint = 0;
+  uint64_t cloud_version = 0;
+  const gsb_cloud* cloud = nullptr;
+  gsb_camera camera{};
+  gsb_raster_config config{};
+  double background[3] = {0, 0, 0};
+  bool valid = false;
+  bool has_dimage = false;
+  // device camera / config
+  gsb::DevBuf cam;        // CamDev
+  // per Gaussian (n)
+  gsb::DevBuf rec_g;      // SplatRec
+  gsb::DevBuf rect_g;     // uint2 (tx0|tx1<<16, ty0|ty1<<16)
+  gsb::DevBuf cnt_g;      // uint32 tiles touched (0 = culled)
+  gsb::DevBuf depth_g;    // double
+  gsb::DevBuf radius_g;   // double (export only)
+  gsb::DevBuf rank_of_g;  // int32 rank or -1
+  // visible (V)
+  gsb::DevBuf vis_idx;    // uint32 gid, index order
+  gsb::DevBuf dkey[2];    // uint32 depth keys (ping-pong)
+  gsb::DevBuf dval[2];    // uint32 visible slot (ping-pong)
+  gsb::DevBuf rec;        // SplatRec, rank order
+  gsb::DevBuf aux;        // SplatAux, rank order
+  gsb::DevBuf cnt_r;      // uint32 tiles per rank (scan input)
+  // entries (K)
+  gsb::DevBuf ekey[2];    // uint32 tile ids
+  gsb::DevBuf eval_[2];   // uint32 ranks
+  int sorted_sel = 0;     // which ekey/eval buffer holds the sorted result
+  gsb::DevBuf ranges;     // uint2 per tile
+  // per pixel
+  gsb::DevBuf image;      // FP32 planes [3][P]
+  gsb::DevBuf final_t;    // FP32 [P]
+  gsb::DevBuf pixstate;   // uint32 contrib | overflow << 29
+  gsb::DevBuf d_image;    // FP32 planes [3][P]
+  // backward
+  gsb::DevBuf partials;   // float [K][9] at pre-sort positions
+  gsb::DevBuf pose_blocks;// double [blocks][6]
+  gsb::DevBuf d_pose;     // double[6]
+  // loss
+  gsb::DevBuf loss_blocks;// double [blocks][2]
+  gsb::DevBuf loss_val;   // double[2] (l1, ssim)
+  gsb::DevBuf gmaps;      // FP32 [9][P] ssim gradient maps
+  // scan / sort scratch
+  gsb::DevBuf scan_tmp;
+  gsb::DevBuf sort_hist;
+  gsb::DevBuf counters;   // uint32/uint64 device counters
+};

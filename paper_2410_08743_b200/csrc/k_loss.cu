@@ -1,0 +1,255 @@
+// k_loss.cu — K6: fused photometric loss (1-beta) L1 + beta (1 - SSIM) with
+// its analytic image gradient, on planar FP32 images, FP64 accumulation.
+//
+// Reference: rgb_loss (losses.cpp:201-215) <- l1_core (158-192),
+// ssim_core (74-155), conv_window (37-63), gaussian_window (19-32).
+// SSIM uses the 11x11 sigma 1.5 separable window with zero padding, C1 =
+// 1e-4, C2 = 9e-4, averaged over pixels where the window fits, x,y in
+// [5, dim-5) (losses.cpp:78-79); its gradient back-convolves the three
+// per-pixel maps g_mu, g_eaa, g_eab (144-151). The factored gradient
+// expressions of the reference are kept so identical images give exactly
+// zero loss and gradient.
+//
+// Two tiled kernels (16x16 outputs + 5 px halo staged in shared memory):
+//   loss_maps:  5 forward convolutions -> SSIM map sum, L1 sum, g maps;
+//   loss_grad:  3 back-convolutions + L1 sign term -> d_image.
+// Per-block partial sums are reduced in a fixed order (deterministic).
+#include "gsb_internal.cuh"
+
+namespace gsb {
+
+constexpr int kLT = 16;             // output tile
+constexpr int kHalf = 5;
+constexpr int kWin = 11;
+constexpr int kLI = kLT + 2 * kHalf;  // 26 staged rows/cols
+__constant__ double c_win[kWin];
+
+__device__ __forceinline__ double m_(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double a_(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double s_(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double d_(double a, double b) { return __ddiv_rn(a, b); }
+
+__device__ __forceinline__ double blk_reduce_sum(double v, double* s_tmp) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) s_tmp[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_tmp[w];
+  __syncthreads();
+  return t;  // valid in thread 0
+}
+
+__global__ void __launch_bounds__(256) loss_maps_kernel(const float* __restrict__ ren, const float* __restrict__ tgt,
+                                                        int W, int H, double scale, float* __restrict__ gmaps,
+                                                        double* __restrict__ block_sums) {
+  __shared__ double sa[kLI][kLI + 1], sb[kLI][kLI + 1];
+  __shared__ double hq[5][kLI][kLT + 1];
+  __shared__ double s_tmp[8];
+  const int64_t P = (int64_t)W * H;
+  const int bx = blockIdx.x * kLT, by = blockIdx.y * kLT;
+  const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
+  const int x = bx + lx, y = by + ly;
+  const bool in_img = x < W && y < H;
+  const bool valid = x >= kHalf && x < W - kHalf && y >= kHalf && y < H - kHalf;
+  double l1 = 0.0, ss = 0.0;
+  for (int c = 0; c < 3; ++c) {
+    const float* A = ren + c * P;
+    const float* B = tgt + c * P;
+    for (int idx = threadIdx.x; idx < kLI * kLI; idx += 256) {
+      const int r = idx / kLI, q = idx % kLI;
+      const int gx = bx - kHalf + q, gy = by - kHalf + r;
+      const bool ok = gx >= 0 && gx < W && gy >= 0 && gy < H;
+      sa[r][q] = ok ? (double)A[(int64_t)gy * W + gx] : 0.0;
+      sb[r][q] = ok ? (double)B[(int64_t)gy * W + gx] : 0.0;
+    }
+    __syncthreads();
+    // horizontal pass over 26 rows x 16 cols
+    for (int idx = threadIdx.x; idx < kLI * kLT; idx += 256) {
+      const int r = idx / kLT, q = idx % kLT;
+      double h0 = 0, h1 = 0, h2 = 0, h3 = 0, h4 = 0;
+#pragma unroll
+      for (int k = 0; k < kWin; ++k) {
+        const double w = c_win[k];
+        const double a = sa[r][q + k], b = sb[r][q + k];
+        h0 += w * a;
+        h1 += w * b;
+        h2 += w * (a * a);
+        h3 += w * (b * b);
+        h4 += w * (a * b);
+      }
+      hq[0][r][q] = h0;
+      hq[1][r][q] = h1;
+      hq[2][r][q] = h2;
+      hq[3][r][q] = h3;
+      hq[4][r][q] = h4;
+    }
+    __syncthreads();
+    if (in_img) {
+      const double a = sa[ly + kHalf][lx + kHalf], b = sb[ly + kHalf][lx + kHalf];
+      l1 += fabs(a - b);
+      if (valid) {
+        double ma = 0, mb = 0, eaa = 0, ebb = 0, eab = 0;
+#pragma unroll
+        for (int k = 0; k < kWin; ++k) {
+          const double w = c_win[k];
+          ma += w * hq[0][ly + k][lx];
+          mb += w * hq[1][ly + k][lx];
+          eaa += w * hq[2][ly + k][lx];
+          ebb += w * hq[3][ly + k][lx];
+          eab += w * hq[4][ly + k][lx];
+        }
+        // Pointwise SSIM terms with explicitly rounded (unfused) arithmetic in
+        // the reference's expression order, so identical inputs cancel exactly
+        // (a1 == b1, a2 == b2, s == 1 and a zero gradient; losses.cpp:112-131).
+        const double C1 = 1e-4, C2 = 9e-4;
+        const double va = s_(eaa, m_(ma, ma)), vb = s_(ebb, m_(mb, mb)), vab = s_(eab, m_(ma, mb));
+        const double a1 = a_(m_(m_(2.0, ma), mb), C1), a2 = a_(m_(2.0, vab), C2);
+        const double b1 = a_(a_(m_(ma, ma), m_(mb, mb)), C1), b2 = a_(a_(va, vb), C2);
+        const double b12 = m_(b1, b2);
+        const double s = d_(m_(a1, a2), b12);
+        ss += s;
+        const double gmu = d_(m_(scale, a_(m_(m_(2.0, mb), s_(a2, a1)), m_(m_(m_(2.0, ma), s), s_(b1, b2)))), b12);
+        const double qv = d_(a1, b12);
+        const int64_t p = (int64_t)y * W + x;
+        gmaps[(3 * c + 0) * P + p] = (float)gmu;
+        gmaps[(3 * c + 1) * P + p] = (float)m_(-m_(scale, qv), d_(a2, b2));
+        gmaps[(3 * c + 2) * P + p] = (float)m_(2.0, m_(scale, qv));
+      } else {
+        const int64_t p = (int64_t)y * W + x;
+        gmaps[(3 * c + 0) * P + p] = 0.f;
+        gmaps[(3 * c + 1) * P + p] = 0.f;
+        gmaps[(3 * c + 2) * P + p] = 0.f;
+      }
+    }
+    __syncthreads();
+  }
+  const double t1 = blk_reduce_sum(l1, s_tmp);
+  const double t2 = blk_reduce_sum(ss, s_tmp);
+  if (threadIdx.x == 0) {
+    const int b = blockIdx.y * gridDim.x + blockIdx.x;
+    block_sums[2 * b] = t1;
+    block_sums[2 * b + 1] = t2;
+  }
+}
+
+__global__ void __launch_bounds__(256) loss_grad_kernel(const float* __restrict__ ren, const float* __restrict__ tgt,
+                                                        const float* __restrict__ gmaps, int W, int H, double beta,
+                                                        double l1_norm, int has_ssim, float* __restrict__ d_image) {
+  __shared__ float sg[3][kLI][kLI + 1];
+  __shared__ double hq[3][kLI][kLT + 1];
+  const int64_t P = (int64_t)W * H;
+  const int bx = blockIdx.x * kLT, by = blockIdx.y * kLT;
+  const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
+  const int x = bx + lx, y = by + ly;
+  const bool in_img = x < W && y < H;
+  for (int c = 0; c < 3; ++c) {
+    if (has_ssim) {
+      for (int idx = threadIdx.x; idx < kLI * kLI; idx += 256) {
+        const int r = idx / kLI, q = idx % kLI;
+        const int gx = bx - kHalf + q, gy = by - kHalf + r;
+        const bool ok = gx >= 0 && gx < W && gy >= 0 && gy < H;
+        const int64_t p = (int64_t)gy * W + gx;
+        sg[0][r][q] = ok ? gmaps[(3 * c + 0) * P + p] : 0.f;
+        sg[1][r][q] = ok ? gmaps[(3 * c + 1) * P + p] : 0.f;
+        sg[2][r][q] = ok ? gmaps[(3 * c + 2) * P + p] : 0.f;
+      }
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < kLI * kLT; idx += 256) {
+        const int r = idx / kLT, q = idx % kLT;
+        double h0 = 0, h1 = 0, h2 = 0;
+#pragma unroll
+        for (int k = 0; k < kWin; ++k) {
+          const double w = c_win[k];
+          h0 += w * (double)sg[0][r][q + k];
+          h1 += w * (double)sg[1][r][q + k];
+          h2 += w * (double)sg[2][r][q + k];
+        }
+        hq[0][r][q] = h0;
+        hq[1][r][q] = h1;
+        hq[2][r][q] = h2;
+      }
+      __syncthreads();
+    }
+    if (in_img) {
+      const int64_t p = (int64_t)y * W + x;
+      const double a = ren[c * P + p], b = tgt[c * P + p];
+      const double diff = a - b;
+      const double dl1 = diff == 0.0 ? 0.0 : (diff > 0.0 ? l1_norm : -l1_norm);
+      double dss = 0.0;
+      if (has_ssim) {
+        double cm = 0, ce = 0, cx = 0;
+#pragma unroll
+        for (int k = 0; k < kWin; ++k) {
+          const double w = c_win[k];
+          cm += w * hq[0][ly + k][lx];
+          ce += w * hq[1][ly + k][lx];
+          cx += w * hq[2][ly + k][lx];
+        }
+        dss = a_(a_(cm, m_(m_(2.0, a), ce)), m_(b, cx));
+      }
+      d_image[c * P + p] = (float)s_(m_(1.0 - beta, dl1), m_(beta, dss));
+    }
+    __syncthreads();
+  }
+}
+
+// Fixed-order reduction of the block partials; out = {l1_mean, ssim_mean, loss}.
+__global__ void loss_finalize_kernel(const double* __restrict__ block_sums, int nb, double l1_norm, double scale,
+                                     int has_ssim, double beta, double* __restrict__ out) {
+  __shared__ double s1[256], s2[256];
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < nb; i += 256) {
+    a += block_sums[2 * i];
+    b += block_sums[2 * i + 1];
+  }
+  s1[threadIdx.x] = a;
+  s2[threadIdx.x] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ta = 0.0, tb = 0.0;
+    for (int i = 0; i < 256; ++i) {
+      ta += s1[i];
+      tb += s2[i];
+    }
+    const double l1 = ta * l1_norm;
+    const double ssim = has_ssim ? tb * scale : 1.0;
+    out[0] = l1;
+    out[1] = ssim;
+    out[2] = (1.0 - beta) * l1 + beta * (1.0 - ssim);
+  }
+}
+
+static bool g_win_ready = false;
+
+int launch_rgb_loss(cudaStream_t st, const float* ren, const float* tgt, int W, int H, double beta, float* gmaps,
+                    double* block_sums, double* out3, float* d_image, int64_t* launches) {
+  if (!g_win_ready) {  // gaussian_window (losses.cpp:19-32), FP64 on host
+    double w[kWin], sum = 0.0;
+    for (int i = 0; i < kWin; ++i) {
+      const double d = i - kHalf;
+      w[i] = exp(-d * d / (2.0 * 1.5 * 1.5));
+      sum += w[i];
+    }
+    for (int i = 0; i < kWin; ++i) w[i] /= sum;
+    GSB_CUDA(cudaMemcpyToSymbol(c_win, w, sizeof w));
+    g_win_ready = true;
+  }
+  const int64_t cnt_valid = (W > 2 * kHalf && H > 2 * kHalf) ? (int64_t)(W - 2 * kHalf) * (H - 2 * kHalf) : 0;
+  const int has_ssim = cnt_valid > 0 ? 1 : 0;
+  const double scale = has_ssim ? 1.0 / (3.0 * (double)cnt_valid) : 0.0;
+  const double l1_norm = 1.0 / (3.0 * (double)W * (double)H);
+  dim3 grid((W + kLT - 1) / kLT, (H + kLT - 1) / kLT);
+  loss_maps_kernel<<<grid, 256, 0, st>>>(ren, tgt, W, H, scale, gmaps, block_sums);
+  if (d_image) loss_grad_kernel<<<grid, 256, 0, st>>>(ren, tgt, gmaps, W, H, beta, l1_norm, has_ssim, d_image);
+  loss_finalize_kernel<<<1, 256, 0, st>>>(block_sums, (int)(grid.x * grid.y), l1_norm, scale, has_ssim, beta, out3);
+  *launches += d_image ? 3 : 2;
+  GSB_CHECK_LAUNCH("rgb_loss kernels");
+  return GSB_OK;
+}
+
+size_t loss_block_count(int W, int H) { return (size_t)((W + kLT - 1) / kLT) * ((H + kLT - 1) / kLT); }
+
+}  // namespace gsb

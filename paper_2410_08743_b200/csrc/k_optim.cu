@@ -1,0 +1,400 @@
+// k_optim.cu — K5a SE(3) pose step and K5b Adam on Gaussians.
+//
+// K5a restates pose_step (trainer.cpp:71-90): Adam on the 6-vector with bias
+// correction (beta1 .9, beta2 .999, eps 1e-15, trainer.hpp:80-82), return
+// the pose bit-for-bit when the update is exactly zero (86), otherwise
+// se3_exp(delta) * pose (lie.cpp:117-129 with series_coeffs 26-43) followed
+// by SVD re-orthonormalisation (lie.cpp:87-97; two-sided Jacobi SVD as in
+// Eigen's JacobiSVD). Runs in FP64 on the device, batched over views, and
+// fused with pose_descent's bookkeeping (pipelines.cpp:66-90: best-loss
+// pose, loss < 1e-14 exit, cosine lr schedule, |applied| < eps exit) so the
+// pose-estimation loop never returns to the host between iterations.
+//
+// K5b restates cloud_adam_step (pipelines.cpp:18-41) / adam_step
+// (trainer.cpp:40-69) over the plane-major FP32 cloud: per-plane learning
+// rate groups (means, rotations, log-scales, opacity, SH DC / rest by
+// k % basis == 0) and renormalisation of exactly those quaternions whose
+// bits changed.
+#include "gsb_internal.cuh"
+
+#include <cmath>
+
+namespace gsb {
+
+constexpr double kB1 = 0.9, kB2 = 0.999, kEps = 1e-15;
+
+struct PoseState {
+  double R[9], t[3];
+  double m[6], v[6];
+  int64_t step;
+  double best_R[9], best_t[3];
+  double best_loss, final_loss;
+  double applied[6];
+  int32_t iter, steps_used, converged, stop;
+};
+
+struct PoseCtl {
+  double lr_start, lr_end, eps;
+  int32_t budget;
+  int32_t fixed_lr;  // 1: use lr_start for every step (single pose_step calls)
+};
+
+__device__ void d_series(double theta, double* a, double* b, double* d) {
+  const double t2 = theta * theta;
+  if (theta < 1e-8) {
+    *a = 1.0 - t2 / 6.0;
+    *b = 0.5 - t2 / 24.0;
+  } else {
+    const double hs = sin(0.5 * theta);
+    *a = sin(theta) / theta;
+    *b = 2.0 * hs * hs / t2;
+  }
+  if (theta < 1e-2) *d = 1.0 / 6.0 - t2 / 120.0 + t2 * t2 / 5040.0;
+  else *d = (theta - sin(theta)) / (t2 * theta);
+}
+
+__device__ void d_mat3_mul(const double* A, const double* B, double* C) {
+  double r[9];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) r[i * 3 + j] = A[i * 3] * B[j] + A[i * 3 + 1] * B[3 + j] + A[i * 3 + 2] * B[6 + j];
+  for (int k = 0; k < 9; ++k) C[k] = r[k];
+}
+
+// Two-sided Jacobi SVD of a 3x3 (Eigen JacobiSVD's sweep, 2x2 real SVD step,
+// sign fix and descending sort), returning the polar factor U V^T with the
+// det < 0 fix of Se3Pose::orthonormalize.
+__device__ void d_orthonormalize(double* Rm) {
+  const double eps = 2.220446049250313e-16, min_pos = 2.2250738585072014e-308;
+  double M[9], U[9], V[9];
+  double scale = 0.0;
+  for (int k = 0; k < 9; ++k) scale = fmax(scale, fabs(Rm[k]));
+  if (scale == 0.0) scale = 1.0;
+  for (int k = 0; k < 9; ++k) {
+    M[k] = Rm[k] / scale;
+    U[k] = V[k] = (k % 4 == 0) ? 1.0 : 0.0;
+  }
+  double max_diag = fmax(fabs(M[0]), fmax(fabs(M[4]), fabs(M[8])));
+  bool finished = false;
+  for (int sweep = 0; sweep < 100 && !finished; ++sweep) {
+    finished = true;
+    for (int p = 1; p < 3; ++p) {
+      for (int q = 0; q < p; ++q) {
+        const double thr = fmax(min_pos, 2.0 * eps * max_diag);
+        if (!(fabs(M[p * 3 + q]) > thr || fabs(M[q * 3 + p]) > thr)) continue;
+        finished = false;
+        const double m00 = M[p * 3 + p], m01 = M[p * 3 + q], m10 = M[q * 3 + p], m11 = M[q * 3 + q];
+        double c1 = 1.0, s1 = 0.0;
+        const double tt = m00 + m11, dd = m10 - m01;
+        if (!(fabs(dd) < min_pos)) {
+          const double u = tt / dd, tmp = sqrt(1.0 + u * u);
+          s1 = 1.0 / tmp;
+          c1 = u / tmp;
+        }
+        const double n00 = c1 * m00 + s1 * m10, n01 = c1 * m01 + s1 * m11, n11 = -s1 * m01 + c1 * m11;
+        double cr = 1.0, sr = 0.0;
+        const double deno = 2.0 * fabs(n01);
+        if (!(deno < min_pos)) {
+          const double tau = (n00 - n11) / deno, w = sqrt(tau * tau + 1.0);
+          const double t = tau > 0.0 ? 1.0 / (tau + w) : 1.0 / (tau - w);
+          const double sgn = t > 0.0 ? 1.0 : -1.0, nn = 1.0 / sqrt(t * t + 1.0);
+          sr = -sgn * (n01 / fabs(n01)) * fabs(t) * nn;
+          cr = nn;
+        }
+        // j_left = rot1 * j_right^T
+        const double jlc = c1 * cr - s1 * (-sr), jls = c1 * (-sr) + s1 * cr;
+        for (int i = 0; i < 3; ++i) {  // M.applyOnTheLeft(p,q,jl)
+          const double x = M[p * 3 + i], y = M[q * 3 + i];
+          M[p * 3 + i] = jlc * x + jls * y;
+          M[q * 3 + i] = -jls * x + jlc * y;
+        }
+        for (int i = 0; i < 3; ++i) {  // U.applyOnTheRight(p,q,jl^T): uses (c, -s)^T = (c, s)
+          const double x = U[i * 3 + p], y = U[i * 3 + q];
+          U[i * 3 + p] = jlc * x + jls * y;
+          U[i * 3 + q] = -jls * x + jlc * y;
+        }
+        for (int i = 0; i < 3; ++i) {  // M, V .applyOnTheRight(p,q,jr): rotation (c, -s)
+          double x = M[i * 3 + p], y = M[i * 3 + q];
+          M[i * 3 + p] = cr * x - sr * y;
+          M[i * 3 + q] = sr * x + cr * y;
+          x = V[i * 3 + p];
+          y = V[i * 3 + q];
+          V[i * 3 + p] = cr * x - sr * y;
+          V[i * 3 + q] = sr * x + cr * y;
+        }
+        max_diag = fmax(max_diag, fmax(fabs(M[p * 3 + p]), fabs(M[q * 3 + q])));
+      }
+    }
+  }
+  double S[3];
+  for (int i = 0; i < 3; ++i) {
+    const double a = M[i * 3 + i];
+    S[i] = fabs(a);
+    if (a < 0.0)
+      for (int r = 0; r < 3; ++r) U[r * 3 + i] = -U[r * 3 + i];
+  }
+  for (int i = 0; i < 3; ++i) {
+    int best = i;
+    for (int k = i + 1; k < 3; ++k)
+      if (S[k] > S[best]) best = k;
+    if (best != i) {
+      const double ts = S[i];
+      S[i] = S[best];
+      S[best] = ts;
+      for (int r = 0; r < 3; ++r) {
+        double tu = U[r * 3 + i];
+        U[r * 3 + i] = U[r * 3 + best];
+        U[r * 3 + best] = tu;
+        tu = V[r * 3 + i];
+        V[r * 3 + i] = V[r * 3 + best];
+        V[r * 3 + best] = tu;
+      }
+    }
+  }
+  double Vt[9], out[9];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) Vt[i * 3 + j] = V[j * 3 + i];
+  d_mat3_mul(U, Vt, out);
+  const double det = out[0] * (out[4] * out[8] - out[5] * out[7]) - out[1] * (out[3] * out[8] - out[5] * out[6]) +
+                     out[2] * (out[3] * out[7] - out[4] * out[6]);
+  if (det < 0.0) {
+    for (int r = 0; r < 3; ++r) U[r * 3 + 2] = -U[r * 3 + 2];
+    d_mat3_mul(U, Vt, out);
+  }
+  for (int k = 0; k < 9; ++k) Rm[k] = out[k];
+}
+
+__device__ void d_pose_step(PoseState& s, const double* dpose, double lr) {
+  ++s.step;
+  const double bc1 = 1.0 - pow(kB1, (double)s.step), bc2 = 1.0 - pow(kB2, (double)s.step);
+  double delta[6];
+  bool zero = true;
+  for (int k = 0; k < 6; ++k) {
+    const double g = dpose[k];
+    s.m[k] = kB1 * s.m[k] + (1.0 - kB1) * g;
+    s.v[k] = kB2 * s.v[k] + (1.0 - kB2) * g * g;
+    const double mh = s.m[k] / bc1, vh = s.v[k] / bc2;
+    delta[k] = -lr * mh / (sqrt(vh) + kEps);
+    s.applied[k] = delta[k];
+    zero = zero && delta[k] == 0.0;
+  }
+  if (zero) return;
+  // se3_exp(delta)
+  const double* w = delta + 3;
+  const double theta = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+  double a, b, d;
+  d_series(theta, &a, &b, &d);
+  const double W[9] = {0.0, -w[2], w[1], w[2], 0.0, -w[0], -w[1], w[0], 0.0};
+  double W2[9], Re[9], Vm[9];
+  d_mat3_mul(W, W, W2);
+  for (int k = 0; k < 9; ++k) {
+    const double I = (k % 4 == 0) ? 1.0 : 0.0;
+    Re[k] = I + a * W[k] + b * W2[k];
+    Vm[k] = I + b * W[k] + d * W2[k];
+  }
+  double te[3], tn[3], Rn[9];
+  for (int i = 0; i < 3; ++i) te[i] = Vm[i * 3] * delta[0] + Vm[i * 3 + 1] * delta[1] + Vm[i * 3 + 2] * delta[2];
+  d_mat3_mul(Re, s.R, Rn);
+  for (int i = 0; i < 3; ++i) tn[i] = Re[i * 3] * s.t[0] + Re[i * 3 + 1] * s.t[1] + Re[i * 3 + 2] * s.t[2] + te[i];
+  d_orthonormalize(Rn);
+  for (int k = 0; k < 9; ++k) s.R[k] = Rn[k];
+  for (int k = 0; k < 3; ++k) s.t[k] = tn[k];
+}
+
+__device__ void d_write_cam(const PoseState& s, CamDev* cam) {
+  for (int k = 0; k < 9; ++k) cam->R[k] = s.R[k];
+  for (int k = 0; k < 3; ++k) cam->t[k] = s.t[k];
+  for (int i = 0; i < 3; ++i)  // center = -(R^T t)
+    cam->center[i] = -(s.R[i] * s.t[0] + s.R[3 + i] * s.t[1] + s.R[6 + i] * s.t[2]);
+}
+
+// One pose_descent iteration tail (after render + loss + backward).
+__global__ void pose_iter_kernel(PoseState* st, const double* __restrict__ dpose, const double* __restrict__ loss3,
+                                 PoseCtl ctl, CamDev* cam, double* trace_pose, double* trace_loss) {
+  PoseState s = *st;
+  if (s.stop) return;
+  const int it = s.iter;
+  const double loss = loss3[2];
+  if (trace_pose) {
+    for (int r = 0; r < 3; ++r) {
+      for (int c = 0; c < 3; ++c) trace_pose[12 * it + r * 4 + c] = s.R[r * 3 + c];
+      trace_pose[12 * it + r * 4 + 3] = s.t[r];
+    }
+  }
+  if (trace_loss) trace_loss[it] = loss;
+  if (loss < s.best_loss) {
+    s.best_loss = loss;
+    for (int k = 0; k < 9; ++k) s.best_R[k] = s.R[k];
+    for (int k = 0; k < 3; ++k) s.best_t[k] = s.t[k];
+    s.final_loss = loss;
+  }
+  if (loss < 1e-14) {
+    s.converged = 1;
+    s.steps_used = it + 1;
+    s.stop = 1;
+    *st = s;
+    return;
+  }
+  double lr = ctl.lr_start;
+  if (!ctl.fixed_lr) {  // schedule(cosine, start, end, t, budget) (trainer.cpp:30-38)
+    double f = ctl.budget > 0 ? (double)it / (double)ctl.budget : 1.0;
+    f = f < 0.0 ? 0.0 : (f > 1.0 ? 1.0 : f);
+    lr = ctl.budget > 0 ? ctl.lr_end + (ctl.lr_start - ctl.lr_end) * 0.5 * (1.0 + cos(M_PI * f)) : ctl.lr_end;
+  }
+  d_pose_step(s, dpose, lr);
+  s.steps_used = it + 1;
+  s.iter = it + 1;
+  double an = 0.0;
+  for (int k = 0; k < 6; ++k) an += s.applied[k] * s.applied[k];
+  if (sqrt(an) < ctl.eps) {
+    s.converged = 1;
+    s.stop = 1;
+  }
+  if (s.iter >= ctl.budget) s.stop = 1;
+  *st = s;
+  if (cam) d_write_cam(s, cam);
+}
+
+// Plain pose_step on a batch of poses (C-ABI gsb_pose_step).
+__global__ void pose_step_kernel(PoseState* st, const double* __restrict__ dpose, double lr, int nb) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nb) return;
+  PoseState s = st[i];
+  d_pose_step(s, dpose + 6 * i, lr);
+  st[i] = s;
+}
+
+// adam_step (trainer.cpp:40-53) on a flat FP64 array.
+__global__ void adam_f64_kernel(double* __restrict__ p, const double* __restrict__ g, double* __restrict__ m,
+                                double* __restrict__ v, int64_t n, double lr, double bc1, double bc2) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double gi = g[i];
+  const double mi = kB1 * m[i] + (1.0 - kB1) * gi;
+  const double vi = kB2 * v[i] + (1.0 - kB2) * gi * gi;
+  m[i] = mi;
+  v[i] = vi;
+  p[i] -= lr * (mi / bc1) / (sqrt(vi / bc2) + kEps);
+}
+
+struct AdamCoef {
+  float lr[6];  // pos, rot, scale, opacity, sh_dc, sh_rest
+  float bc1[5], bc2[5];
+};
+
+// cloud_adam_step over FP32 planes; one thread per Gaussian.
+__global__ void __launch_bounds__(256) cloud_adam_kernel(float* __restrict__ params, const float* __restrict__ grads,
+                                                         float* __restrict__ m, float* __restrict__ v, int64_t n,
+                                                         int64_t n_pad, int nplanes, int basis, AdamCoef c) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool quat_moved = false;
+  float q[4];
+  for (int p = 0; p < nplanes; ++p) {
+    const int64_t k = (int64_t)p * n_pad + i;
+    int grp;
+    float lr;
+    if (p < kQuatW) { grp = 0; lr = c.lr[0]; }
+    else if (p < kScaleX) { grp = 1; lr = c.lr[1]; }
+    else if (p < kOpacity) { grp = 2; lr = c.lr[2]; }
+    else if (p == kOpacity) { grp = 3; lr = c.lr[3]; }
+    else { grp = 4; lr = ((p - kShBase) % basis == 0) ? c.lr[4] : c.lr[5]; }
+    const float gi = grads[k];
+    const float mi = 0.9f * m[k] + 0.1f * gi;
+    const float vi = 0.999f * v[k] + 0.001f * gi * gi;
+    m[k] = mi;
+    v[k] = vi;
+    const float old = params[k];
+    const float nw = old - lr * (mi / c.bc1[grp]) / (sqrtf(vi / c.bc2[grp]) + 1e-15f);
+    params[k] = nw;
+    if (grp == 1) {
+      q[p - kQuatW] = nw;
+      quat_moved = quat_moved || (nw != old);
+    }
+  }
+  if (quat_moved) {  // pipelines.cpp:36-40
+    const float nn = sqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    for (int k = 0; k < 4; ++k) params[(int64_t)(kQuatW + k) * n_pad + i] = q[k] / nn;
+  }
+}
+
+// ------------------------------------------------------------- host glue
+int launch_pose_iter(cudaStream_t st, void* state, const double* dpose, const double* loss3, double lr_start,
+                     double lr_end, double eps, int budget, CamDev* cam, double* trace_pose, double* trace_loss) {
+  PoseCtl ctl{lr_start, lr_end, eps, budget, 0};
+  pose_iter_kernel<<<1, 1, 0, st>>>(static_cast<PoseState*>(state), dpose, loss3, ctl, cam, trace_pose, trace_loss);
+  GSB_CHECK_LAUNCH("pose_iter_kernel");
+  return GSB_OK;
+}
+size_t pose_state_bytes() { return sizeof(PoseState); }
+int pose_state_init(void* host_state, const double pose[12]) {
+  PoseState* s = static_cast<PoseState*>(host_state);
+  *s = PoseState{};
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c) s->R[r * 3 + c] = pose[r * 4 + c];
+    s->t[r] = pose[r * 4 + 3];
+  }
+  for (int k = 0; k < 9; ++k) s->best_R[k] = s->R[k];
+  for (int k = 0; k < 3; ++k) s->best_t[k] = s->t[k];
+  s->best_loss = INFINITY;
+  return GSB_OK;
+}
+void pose_state_read(const void* host_state, double best_pose[12], double cur_pose[12], double* final_loss,
+                     int32_t* steps_used, int32_t* converged, int32_t* stop, double applied[6], double m[6],
+                     double v[6], int64_t* step) {
+  const PoseState* s = static_cast<const PoseState*>(host_state);
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c) {
+      if (best_pose) best_pose[r * 4 + c] = s->best_R[r * 3 + c];
+      if (cur_pose) cur_pose[r * 4 + c] = s->R[r * 3 + c];
+    }
+    if (best_pose) best_pose[r * 4 + 3] = s->best_t[r];
+    if (cur_pose) cur_pose[r * 4 + 3] = s->t[r];
+  }
+  if (final_loss) *final_loss = s->final_loss;
+  if (steps_used) *steps_used = s->steps_used;
+  if (converged) *converged = s->converged;
+  if (stop) *stop = s->stop;
+  for (int k = 0; k < 6; ++k) {
+    if (applied) applied[k] = s->applied[k];
+    if (m) m[k] = s->m[k];
+    if (v) v[k] = s->v[k];
+  }
+  if (step) *step = s->step;
+}
+void pose_state_set_adam(void* host_state, const double m[6], const double v[6], int64_t step) {
+  PoseState* s = static_cast<PoseState*>(host_state);
+  for (int k = 0; k < 6; ++k) {
+    s->m[k] = m[k];
+    s->v[k] = v[k];
+  }
+  s->step = step;
+}
+int launch_pose_step(cudaStream_t st, void* states, const double* dpose, double lr, int nb) {
+  pose_step_kernel<<<(nb + 63) / 64, 64, 0, st>>>(static_cast<PoseState*>(states), dpose, lr, nb);
+  GSB_CHECK_LAUNCH("pose_step_kernel");
+  return GSB_OK;
+}
+int launch_adam_f64(cudaStream_t st, double* p, const double* g, double* m, double* v, int64_t n, double lr,
+                    int64_t step) {
+  const double bc1 = 1.0 - pow(kB1, (double)step), bc2 = 1.0 - pow(kB2, (double)step);
+  if (n > 0) adam_f64_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p, g, m, v, n, lr, bc1, bc2);
+  GSB_CHECK_LAUNCH("adam_f64_kernel");
+  return GSB_OK;
+}
+int launch_cloud_adam(cudaStream_t st, float* params, const float* grads, float* m, float* v, int64_t n,
+                      int64_t n_pad, int sh_degree, const double lrs[6], const int64_t steps[5]) {
+  AdamCoef c;
+  for (int k = 0; k < 6; ++k) c.lr[k] = (float)lrs[k];
+  for (int k = 0; k < 5; ++k) {
+    c.bc1[k] = (float)(1.0 - pow(kB1, (double)steps[k]));
+    c.bc2[k] = (float)(1.0 - pow(kB2, (double)steps[k]));
+  }
+  const int basis = (sh_degree + 1) * (sh_degree + 1);
+  if (n > 0)
+    cloud_adam_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(params, grads, m, v, n, n_pad,
+                                                                   num_planes(sh_degree), basis, c);
+  GSB_CHECK_LAUNCH("cloud_adam_kernel");
+  return GSB_OK;
+}
+
+}  // namespace gsb

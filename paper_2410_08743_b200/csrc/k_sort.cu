@@ -1,0 +1,416 @@
+// k_sort.cu — K2: device-wide scans, visible compaction, stable LSD radix
+// sort (depth keys, then tile keys) and tile-range identification.
+//
+// Reference: rasterizer.cpp:127-168. The reference compacts visible splats
+// in Gaussian-index order (127-130), std::stable_sort's them by double depth
+// (131-132), then bins them with a count / prefix / fill pass in depth order
+// (134-168) so every tile list is depth sorted and ties keep the lower
+// Gaussian index. Here:
+//   1. compaction in index order (scan of cnt_g > 0),
+//   2. stable LSD radix sort of FP32 depth bits (4 x 8-bit passes) plus an
+//      exact fix-up of FP32 ties by the FP64 depth -> the reference order,
+//   3. rank-major duplication of (tile, rank) entries, tiles row-major inside
+//      each splat rect (the reference fill order),
+//   4. stable LSD radix sort of the entries by tile id (ceil(log2 T) bits),
+//   5. ranges = [lower_bound(t), lower_bound(t+1)) for every tile.
+// All passes are stable and order preserving, so the tile lists equal the
+// reference's count/prefix/fill output bit for bit on the same FP64 records.
+#include "gsb_internal.cuh"
+
+namespace gsb {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;  // 4096
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <bool kFlag>
+__device__ __forceinline__ uint32_t scan_load(const uint32_t* in, int64_t i, int64_t n) {
+  if (i >= n) return 0u;
+  uint32_t v = in[i];
+  return kFlag ? (v > 0u ? 1u : 0u) : v;
+}
+
+// Block sums of 4096-element tiles.
+template <bool kFlag>
+__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_t* __restrict__ in, int64_t n,
+                                                                    uint32_t* __restrict__ block_sums) {
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  uint32_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) s += scan_load<kFlag>(in, base + k * kScanThreads + threadIdx.x, n);
+  s = __reduce_add_sync(0xffffffffu, s);
+  __shared__ uint32_t ws[kScanThreads / 32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < kScanThreads / 32; ++w) t += ws[w];
+    block_sums[blockIdx.x] = t;
+  }
+}
+
+// Exclusive scan of nb block sums in one block; total -> sums[nb] and *total_out.
+__global__ void __launch_bounds__(1024) scan_blocks_kernel(uint32_t* __restrict__ sums, int64_t nb,
+                                                           uint32_t* __restrict__ total_out) {
+  __shared__ uint32_t wsum[32];
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < nb; base += 1024) {
+    const int64_t i = base + threadIdx.x;
+    uint32_t v = i < nb ? sums[i] : 0u;
+    // inclusive warp scan
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if ((threadIdx.x & 31) >= o) x += y;
+    }
+    if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      uint32_t w = wsum[threadIdx.x];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+        if (threadIdx.x >= o) w += y;
+      }
+      wsum[threadIdx.x] = w;  // inclusive
+    }
+    __syncthreads();
+    const uint32_t warp_excl = (threadIdx.x >> 5) ? wsum[(threadIdx.x >> 5) - 1] : 0u;
+    const uint32_t excl = carry + warp_excl + x - v;
+    if (i < nb) sums[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    sums[nb] = carry;
+    if (total_out) *total_out = carry;
+  }
+}
+
+// Block-local exclusive scan plus block offset. Items are striped
+// (k*256 + tid) for coalescing; the scan order is the global index order.
+template <bool kFlag>
+__global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t* __restrict__ in, int64_t n,
+                                                                   const uint32_t* __restrict__ block_offs,
+                                                                   uint32_t* __restrict__ out) {
+  __shared__ uint32_t tile[kScanTile + kScanTile / 32];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int idx = k * kScanThreads + threadIdx.x;
+    tile[idx + (idx >> 5)] = scan_load<kFlag>(in, base + idx, n);
+  }
+  __syncthreads();
+  // thread t owns items [t*16, t*16+16)
+  uint32_t local[kScanItems];
+  uint32_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int idx = threadIdx.x * kScanItems + k;
+    local[k] = tile[idx + (idx >> 5)];
+    s += local[k];
+  }
+  uint32_t x = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) >= o) x += y;
+  }
+  __shared__ uint32_t ws[kScanThreads / 32];
+  if ((threadIdx.x & 31) == 31) ws[threadIdx.x >> 5] = x;
+  __syncthreads();
+  uint32_t woff = 0;
+  for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) woff += ws[w];
+  uint32_t run = block_offs[blockIdx.x] + woff + x - s;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int idx = threadIdx.x * kScanItems + k;
+    tile[idx + (idx >> 5)] = run;
+    run += local[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int idx = k * kScanThreads + threadIdx.x;
+    if (base + idx < n) out[base + idx] = tile[idx + (idx >> 5)];
+  }
+}
+
+static size_t scan_scratch_words(int64_t n) { return (size_t)((n + kScanTile - 1) / kScanTile) + 2; }
+
+// Exclusive scan of n u32 values (or of the flags v > 0 when flag) into out.
+// total (device u32*) receives the sum. scratch must hold scan_scratch_words(n).
+int scan_exclusive(cudaStream_t st, const uint32_t* in, int64_t n, bool flag, uint32_t* out, uint32_t* scratch,
+                   uint32_t* total, int64_t* launches) {
+  const int64_t nb = (n + kScanTile - 1) / kScanTile;
+  if (nb > 0) {
+    if (flag) scan_reduce_kernel<true><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, scratch);
+    else scan_reduce_kernel<false><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, scratch);
+  }
+  scan_blocks_kernel<<<1, 1024, 0, st>>>(scratch, nb, total);
+  if (nb > 0) {
+    if (flag) scan_apply_kernel<true><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, scratch, out);
+    else scan_apply_kernel<false><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, scratch, out);
+  }
+  *launches += nb > 0 ? 3 : 1;
+  GSB_CHECK_LAUNCH("scan_exclusive");
+  return GSB_OK;
+}
+
+// ------------------------------------------------------------ radix sort
+constexpr int kRadixThreads = 256;
+constexpr int kRadixRounds = 16;
+constexpr int kRadixTile = kRadixThreads * kRadixRounds;  // 4096 items per block
+
+__global__ void __launch_bounds__(kRadixThreads) radix_hist_kernel(const uint32_t* __restrict__ keys, int64_t n,
+                                                                   int shift, int bits,
+                                                                   uint32_t* __restrict__ hist, int64_t nblocks) {
+  __shared__ uint32_t h[256];
+  const int ndig = 1 << bits;
+  if (threadIdx.x < ndig) h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kRadixTile;
+  const uint32_t mask = (uint32_t)ndig - 1u;
+#pragma unroll 4
+  for (int k = 0; k < kRadixRounds; ++k) {
+    const int64_t i = base + k * kRadixThreads + threadIdx.x;
+    if (i < n) atomicAdd(&h[(keys[i] >> shift) & mask], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < ndig) hist[(int64_t)threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
+}
+
+// Stable scatter: items are processed in rounds of 256 in global order;
+// within a round ranks come from warp match + cross-warp prefix.
+__global__ void __launch_bounds__(kRadixThreads) radix_scatter_kernel(
+    const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
+    uint32_t* __restrict__ vals_out, int64_t n, int shift, int bits, const uint32_t* __restrict__ offs,
+    int64_t nblocks) {
+  constexpr int kWarps = kRadixThreads / 32;
+  __shared__ uint32_t warp_cnt[kWarps][256];
+  __shared__ uint32_t warp_off[kWarps][256];
+  __shared__ uint32_t digit_run[256];
+  const int ndig = 1 << bits;
+  const uint32_t mask = (uint32_t)ndig - 1u;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int d = threadIdx.x; d < 256; d += kRadixThreads) {
+    digit_run[d] = d < ndig ? offs[(int64_t)d * nblocks + blockIdx.x] : 0u;
+    for (int w = 0; w < kWarps; ++w) warp_cnt[w][d] = 0;
+  }
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kRadixTile;
+  const uint32_t lt = lanemask_lt();
+  for (int k = 0; k < kRadixRounds; ++k) {
+    const int64_t i = base + k * kRadixThreads + threadIdx.x;
+    if (base + k * kRadixThreads >= n) break;  // uniform across the block
+    const bool valid = i < n;
+    uint32_t key = 0, val = 0, dig = 0x100u + lane;  // invalid lanes get unique sentinels
+    if (valid) {
+      key = keys_in[i];
+      val = vals_in[i];
+      dig = (key >> shift) & mask;
+    }
+    const uint32_t peers = __match_any_sync(0xffffffffu, dig);
+    const uint32_t rank = __popc(peers & lt);
+    if (valid && rank == 0) warp_cnt[warp][dig] = __popc(peers);
+    __syncthreads();
+    for (int d = threadIdx.x; d < ndig; d += kRadixThreads) {
+      uint32_t run = digit_run[d];
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        const uint32_t c = warp_cnt[w][d];
+        warp_off[w][d] = run;
+        run += c;
+        warp_cnt[w][d] = 0;
+      }
+      digit_run[d] = run;
+    }
+    __syncthreads();
+    if (valid) {
+      const uint32_t pos = warp_off[warp][dig] + rank;
+      keys_out[pos] = key;
+      vals_out[pos] = val;
+    }
+  }
+}
+
+// Sorts (keys, vals) by key bits [0, total_bits) stably. Buffers [0] hold the
+// input; returns the index (0/1) of the buffer holding the result.
+int radix_sort_pairs(cudaStream_t st, uint32_t* keys[2], uint32_t* vals[2], int64_t n, int total_bits,
+                     uint32_t* hist, int* result_sel, int64_t* launches) {
+  int sel = 0;
+  if (n <= 1 || total_bits <= 0) {
+    *result_sel = 0;
+    return GSB_OK;
+  }
+  const int passes = (total_bits + 7) / 8;
+  const int bits = (total_bits + passes - 1) / passes;
+  const int64_t nblocks = (n + kRadixTile - 1) / kRadixTile;
+  const int64_t nh = (int64_t)(1 << bits) * nblocks;
+  for (int p = 0; p < passes; ++p) {
+    const int shift = p * bits;
+    radix_hist_kernel<<<(unsigned)nblocks, kRadixThreads, 0, st>>>(keys[sel], n, shift, bits, hist, nblocks);
+    int rc = scan_exclusive(st, hist, nh, false, hist, hist + nh, nullptr, launches);
+    if (rc) return rc;
+    radix_scatter_kernel<<<(unsigned)nblocks, kRadixThreads, 0, st>>>(keys[sel], vals[sel], keys[sel ^ 1],
+                                                                      vals[sel ^ 1], n, shift, bits, hist, nblocks);
+    *launches += 2;
+    sel ^= 1;
+  }
+  GSB_CHECK_LAUNCH("radix_sort_pairs");
+  *result_sel = sel;
+  return GSB_OK;
+}
+
+size_t radix_hist_words(int64_t n, int total_bits) {
+  if (total_bits <= 0) return 16;
+  const int passes = (total_bits + 7) / 8;
+  const int bits = (total_bits + passes - 1) / passes;
+  const int64_t nblocks = (n + kRadixTile - 1) / kRadixTile;
+  const int64_t nh = (int64_t)(1 << bits) * nblocks;
+  return (size_t)nh + scan_scratch_words(nh) + 16;
+}
+size_t scan_words(int64_t n) { return scan_scratch_words(n); }
+
+// ---------------------------------------------------- compaction + ranks
+// vis_pos = exclusive scan of (cnt_g > 0). Emits visible slot v -> gid and
+// the FP32 depth key (positive floats compare as their bit patterns).
+__global__ void compact_kernel(const uint32_t* __restrict__ cnt_g, const uint32_t* __restrict__ vis_pos,
+                               const double* __restrict__ depth_g, int64_t n, uint32_t* __restrict__ vis_idx,
+                               uint32_t* __restrict__ dkey, uint32_t* __restrict__ dval) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || cnt_g[i] == 0u) return;
+  const uint32_t v = vis_pos[i];
+  vis_idx[v] = (uint32_t)i;
+  dkey[v] = __float_as_uint((float)depth_g[i]);
+  dval[v] = v;
+}
+
+// Restores the exact FP64 order inside runs of equal FP32 keys (stable:
+// equal doubles keep visible-slot order = Gaussian index order).
+__global__ void depth_tie_fix_kernel(const uint32_t* __restrict__ key, uint32_t* __restrict__ val,
+                                     const uint32_t* __restrict__ vis_idx, const double* __restrict__ depth_g,
+                                     int64_t n) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const uint32_t k = key[r];
+  if (r > 0 && key[r - 1] == k) return;           // not a run start
+  if (r + 1 >= n || key[r + 1] != k) return;      // singleton
+  int64_t end = r + 1;
+  while (end < n && key[end] == k) ++end;
+  for (int64_t a = r + 1; a < end; ++a) {         // insertion sort by FP64 depth
+    const uint32_t v = val[a];
+    const double d = depth_g[vis_idx[v]];
+    int64_t b = a - 1;
+    while (b >= r && depth_g[vis_idx[val[b]]] > d) {
+      val[b + 1] = val[b];
+      --b;
+    }
+    val[b + 1] = v;
+  }
+}
+
+// Rank-order records: rank r holds visible slot sorted_v[r].
+__global__ void gather_ranks_kernel(const uint32_t* __restrict__ sorted_v, const uint32_t* __restrict__ vis_idx,
+                                    const SplatRec* __restrict__ rec_g, const uint2* __restrict__ rect_g,
+                                    const uint32_t* __restrict__ cnt_g, int64_t nv, SplatRec* __restrict__ rec,
+                                    SplatAux* __restrict__ aux, uint32_t* __restrict__ cnt_r,
+                                    int32_t* __restrict__ rank_of_g) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nv) return;
+  const uint32_t gid = vis_idx[sorted_v[r]];
+  rec[r] = rec_g[gid];
+  const uint2 rc = rect_g[gid];
+  const uint32_t tx0 = rc.x & 0xffffu, tx1 = rc.x >> 16, ty0 = rc.y & 0xffffu, ty1 = rc.y >> 16;
+  SplatAux a;
+  a.off = 0;
+  a.tx0_ty0 = tx0 | (ty0 << 16);
+  a.nx_ny = (tx1 - tx0 + 1u) | ((ty1 - ty0 + 1u) << 16);
+  a.gid = (int32_t)gid;
+  aux[r] = a;
+  cnt_r[r] = cnt_g[gid];
+  rank_of_g[gid] = (int32_t)r;
+}
+
+// Emits (tile, rank) for every tile of every splat, rank-major and row-major
+// inside the rect — the reference fill order (rasterizer.cpp:163-167).
+__global__ void duplicate_kernel(const uint32_t* __restrict__ offs, SplatAux* __restrict__ aux, int64_t nv,
+                                 int tiles_x, uint32_t* __restrict__ ekey, uint32_t* __restrict__ eval) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nv) return;
+  const uint32_t off = offs[r];
+  SplatAux a = aux[r];
+  aux[r].off = off;
+  const uint32_t tx0 = a.tx0_ty0 & 0xffffu, ty0 = a.tx0_ty0 >> 16;
+  const uint32_t nx = a.nx_ny & 0xffffu, ny = a.nx_ny >> 16;
+  uint32_t j = off;
+  for (uint32_t y = 0; y < ny; ++y) {
+    const uint32_t row = (ty0 + y) * (uint32_t)tiles_x + tx0;
+    for (uint32_t x = 0; x < nx; ++x, ++j) {
+      ekey[j] = row + x;
+      eval[j] = (uint32_t)r;
+    }
+  }
+}
+
+__global__ void tile_ranges_kernel(const uint32_t* __restrict__ ekey, int64_t k, int n_tiles,
+                                   uint2* __restrict__ ranges) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_tiles) return;
+  auto lower = [&](uint32_t v) {
+    int64_t lo = 0, hi = k;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (ekey[mid] < v) lo = mid + 1;
+      else hi = mid;
+    }
+    return (uint32_t)lo;
+  };
+  ranges[t] = make_uint2(lower((uint32_t)t), lower((uint32_t)t + 1u));
+}
+
+// ------------------------------------------------------------ host glue
+int launch_compact(cudaStream_t st, const uint32_t* cnt_g, const uint32_t* vis_pos, const double* depth_g,
+                   int64_t n, uint32_t* vis_idx, uint32_t* dkey, uint32_t* dval) {
+  if (n > 0) compact_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(cnt_g, vis_pos, depth_g, n, vis_idx, dkey, dval);
+  GSB_CHECK_LAUNCH("compact_kernel");
+  return GSB_OK;
+}
+int launch_depth_tie_fix(cudaStream_t st, const uint32_t* key, uint32_t* val, const uint32_t* vis_idx,
+                         const double* depth_g, int64_t nv) {
+  if (nv > 1) depth_tie_fix_kernel<<<(unsigned)((nv + 255) / 256), 256, 0, st>>>(key, val, vis_idx, depth_g, nv);
+  GSB_CHECK_LAUNCH("depth_tie_fix_kernel");
+  return GSB_OK;
+}
+int launch_gather_ranks(cudaStream_t st, const uint32_t* sorted_v, const uint32_t* vis_idx, const SplatRec* rec_g,
+                        const uint2* rect_g, const uint32_t* cnt_g, int64_t nv, SplatRec* rec, SplatAux* aux,
+                        uint32_t* cnt_r, int32_t* rank_of_g) {
+  if (nv > 0)
+    gather_ranks_kernel<<<(unsigned)((nv + 255) / 256), 256, 0, st>>>(sorted_v, vis_idx, rec_g, rect_g, cnt_g, nv, rec,
+                                                                      aux, cnt_r, rank_of_g);
+  GSB_CHECK_LAUNCH("gather_ranks_kernel");
+  return GSB_OK;
+}
+int launch_duplicate(cudaStream_t st, const uint32_t* offs, SplatAux* aux, int64_t nv, int tiles_x, uint32_t* ekey,
+                     uint32_t* eval) {
+  if (nv > 0) duplicate_kernel<<<(unsigned)((nv + 255) / 256), 256, 0, st>>>(offs, aux, nv, tiles_x, ekey, eval);
+  GSB_CHECK_LAUNCH("duplicate_kernel");
+  return GSB_OK;
+}
+int launch_tile_ranges(cudaStream_t st, const uint32_t* ekey, int64_t k, int n_tiles, uint2* ranges) {
+  if (n_tiles > 0) tile_ranges_kernel<<<(n_tiles + 255) / 256, 256, 0, st>>>(ekey, k, n_tiles, ranges);
+  GSB_CHECK_LAUNCH("tile_ranges_kernel");
+  return GSB_OK;
+}
+
+}  // namespace gsb

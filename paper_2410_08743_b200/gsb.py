@@ -1,0 +1,454 @@
+"""Host-side Python mirror of the reference's hot-path API over libgsb200.so.
+
+The functions mirror gsopt's C++ interface for the pose-gradient path
+(/root/reference/proj/include/gsopt/rasterizer.hpp:98-113, losses.hpp:37,
+trainer.hpp:85-100, trainer.hpp:170-171): same names, same argument meaning,
+same error behaviour (``GsbError`` carries the reference ``ErrorCode`` + 1).
+Every call goes through the C ABI declared in include/gsb200.h; there is no
+CPU implementation behind any of them — without the built library or without
+a B200 the calls raise instead of falling back.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "libgsb200.so")
+
+# include/gsb200.h status codes
+OK = 0
+ERR_STATE_MISMATCH = 6
+ERR_DIMENSION_MISMATCH = 4
+ERR_DIVERGED = 10
+ERR_INVALID_CONFIG = 11
+ERR_CUDA = 100
+ERR_INVALID_ARGUMENT = 101
+ERR_NO_DEVICE = 103
+BWD_POSE_ONLY = 1
+BWD_FAST_ATOMIC = 2
+
+_ERR_NAMES = {1: "angle_near_pi", 2: "degenerate_cloud", 3: "no_valid_depth", 4: "dimension_mismatch",
+              5: "empty_mask", 6: "state_mismatch", 7: "missing_intrinsics", 8: "image_size_mismatch",
+              9: "corrupt_file", 10: "diverged", 11: "invalid_config", 100: "cuda", 101: "invalid_argument",
+              102: "out_of_memory", 103: "no_device"}
+
+
+class GsbError(RuntimeError):
+    """gsopt::Error equivalent (core.hpp:49-52): ``code`` is the C ABI status."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{_ERR_NAMES.get(code, code)}] {msg}")
+        self.code = code
+
+
+class Camera(C.Structure):
+    _fields_ = [("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+                ("width", C.c_int32), ("height", C.c_int32), ("R", C.c_double * 9), ("t", C.c_double * 3)]
+
+    @staticmethod
+    def make(fx, fy, cx, cy, width, height, R=None, t=None) -> "Camera":
+        c = Camera()
+        c.fx, c.fy, c.cx, c.cy, c.width, c.height = fx, fy, cx, cy, width, height
+        R = np.eye(3) if R is None else np.asarray(R, np.float64)
+        t = np.zeros(3) if t is None else np.asarray(t, np.float64)
+        c.R[:] = [float(v) for v in R.reshape(9)]
+        c.t[:] = [float(v) for v in t.reshape(3)]
+        return c
+
+    @staticmethod
+    def from_pose12(fx, fy, cx, cy, width, height, pose12) -> "Camera":
+        p = np.asarray(pose12, np.float64).reshape(3, 4)
+        return Camera.make(fx, fy, cx, cy, width, height, p[:, :3], p[:, 3])
+
+    def pose12(self) -> np.ndarray:
+        return np.concatenate([np.array(self.R[:]).reshape(3, 3), np.array(self.t[:]).reshape(3, 1)], 1).reshape(12)
+
+
+class RasterConfig(C.Structure):
+    _fields_ = [("tile_size", C.c_int32), ("cutoff_sigma", C.c_double), ("alpha_clamp", C.c_double),
+                ("dilation", C.c_double), ("early_termination", C.c_double), ("z_near", C.c_double),
+                ("deterministic", C.c_int32)]
+
+    @staticmethod
+    def default(**kw) -> "RasterConfig":
+        c = RasterConfig()
+        lib().gsb_default_raster_config(C.byref(c))
+        for k, v in kw.items():
+            setattr(c, k, v)
+        return c
+
+
+class PoseAdam(C.Structure):
+    _fields_ = [("m", C.c_double * 6), ("v", C.c_double * 6), ("step", C.c_int64)]
+
+
+class FrameInfo(C.Structure):
+    _fields_ = [("n_gaussians", C.c_int64), ("n_splats", C.c_int64), ("n_entries", C.c_int64),
+                ("width", C.c_int32), ("height", C.c_int32), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32),
+                ("state_fingerprint", C.c_uint64)]
+
+
+class PoseConfig(C.Structure):
+    _fields_ = [("cam_lr_start", C.c_double), ("cam_lr_end", C.c_double), ("beta", C.c_double),
+                ("pose_converged_eps", C.c_double), ("background", C.c_double * 3), ("raster", RasterConfig),
+                ("budget", C.c_int32)]
+
+    @staticmethod
+    def default(**kw) -> "PoseConfig":
+        c = PoseConfig()
+        lib().gsb_default_pose_config(C.byref(c))
+        for k, v in kw.items():
+            if k == "background":
+                c.background[:] = list(v)
+            else:
+                setattr(c, k, v)
+        return c
+
+
+_lib = None
+_vp = C.c_void_p
+
+
+def _sigs():
+    P = C.POINTER
+    d, i32, i64, u32, u64 = C.c_double, C.c_int32, C.c_int64, C.c_uint32, C.c_uint64
+    return {
+        "gsb_last_error": (C.c_char_p, []),
+        "gsb_version": (C.c_char_p, []),
+        "gsb_default_raster_config": (None, [P(RasterConfig)]),
+        "gsb_default_pose_config": (None, [P(PoseConfig)]),
+        "gsb_ctx_create": (C.c_int, [i32, P(_vp)]),
+        "gsb_ctx_destroy": (C.c_int, [_vp]),
+        "gsb_ctx_synchronize": (C.c_int, [_vp]),
+        "gsb_ctx_set_profiling": (C.c_int, [_vp, i32]),
+        "gsb_ctx_stage_times": (C.c_int, [_vp, _vp, _vp, i32]),
+        "gsb_ctx_launch_count": (i64, [_vp]),
+        "gsb_cloud_create": (C.c_int, [_vp, i64, i32, P(_vp)]),
+        "gsb_cloud_destroy": (C.c_int, [_vp]),
+        "gsb_cloud_upload": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, i32]),
+        "gsb_cloud_download": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+        "gsb_cloud_info": (C.c_int, [_vp, _vp, _vp, _vp]),
+        "gsb_cloud_set_active_sh_degree": (C.c_int, [_vp, i32]),
+        "gsb_cloud_synth": (C.c_int, [_vp, u64, d]),
+        "gsb_synth_poses": (C.c_int, [u64, i64, i32, i32, i32, d, d, _vp]),
+        "gsb_perturb_pose": (C.c_int, [_vp, d, d, P(u64), _vp]),
+        "gsb_frame_create": (C.c_int, [_vp, P(_vp)]),
+        "gsb_frame_destroy": (C.c_int, [_vp]),
+        "gsb_render": (C.c_int, [_vp, _vp, P(Camera), _vp, P(RasterConfig), _vp, _vp]),
+        "gsb_frame_get_info": (C.c_int, [_vp, P(FrameInfo)]),
+        "gsb_frame_download": (C.c_int, [_vp] + [_vp] * 15),
+        "gsb_rgb_loss": (C.c_int, [_vp, _vp, _vp, i32, i32, d, P(d), _vp]),
+        "gsb_image_create": (C.c_int, [_vp, _vp, i32, i32, P(_vp)]),
+        "gsb_image_destroy": (C.c_int, [_vp]),
+        "gsb_frame_rgb_loss": (C.c_int, [_vp, _vp, _vp, d, P(d)]),
+        "gsb_grads_create": (C.c_int, [_vp, _vp, P(_vp)]),
+        "gsb_grads_destroy": (C.c_int, [_vp]),
+        "gsb_grads_download": (C.c_int, [_vp] + [_vp] * 7),
+        "gsb_render_backward": (C.c_int, [_vp, _vp, P(Camera), _vp, _vp, i32, i32, u32, _vp, _vp]),
+        "gsb_render_backward_device": (C.c_int, [_vp, _vp, P(Camera), _vp, u32, _vp, _vp]),
+        "gsb_schedule": (d, [i32, d, d, i64, i64]),
+        "gsb_pose_step": (C.c_int, [_vp, _vp, _vp, d, P(PoseAdam), _vp, _vp]),
+        "gsb_adam_step": (C.c_int, [_vp, _vp, _vp, _vp, _vp, P(i64), i64, d]),
+        "gsb_adam_create": (C.c_int, [_vp, _vp, P(_vp)]),
+        "gsb_adam_destroy": (C.c_int, [_vp]),
+        "gsb_cloud_adam_step": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
+        "gsb_estimate_pose": (C.c_int, [_vp, _vp, _vp, _vp, _vp, P(PoseConfig), _vp, P(d), P(i32), P(i32), _vp, _vp]),
+    }
+
+
+def lib():
+    """Loads libgsb200.so (built in-tree by __graft_entry__.build()). Raises if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise GsbError(ERR_NO_DEVICE, f"{LIB_PATH} not built; run __graft_entry__.build() (no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _sigs().items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != OK:
+        raise GsbError(rc, lib().gsb_last_error().decode())
+
+
+def _p(a: np.ndarray | None):
+    if a is None:
+        return None
+    assert a.flags["C_CONTIGUOUS"], "arrays must be C contiguous"
+    return a.ctypes.data_as(_vp)
+
+
+# ----------------------------------------------------------------- objects
+class Context:
+    """One device + one CUDA stream (gsb_ctx)."""
+
+    def __init__(self, device: int = 0):
+        h = _vp()
+        _check(lib().gsb_ctx_create(device, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib().gsb_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self):
+        _check(lib().gsb_ctx_synchronize(self.h))
+
+    def set_profiling(self, on: bool):
+        _check(lib().gsb_ctx_set_profiling(self.h, 1 if on else 0))
+
+    STAGES = ("preprocess", "sort", "composite", "loss", "bwd_raster", "bwd_geom", "optim", "other")
+
+    def stage_times(self, reset=True):
+        ms = np.zeros(8)
+        cnt = np.zeros(8, np.int64)
+        _check(lib().gsb_ctx_stage_times(self.h, _p(ms), _p(cnt), 1 if reset else 0))
+        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(self.STAGES)}
+
+    def launch_count(self) -> int:
+        return int(lib().gsb_ctx_launch_count(self.h))
+
+
+class Cloud:
+    """GaussianCloud (scene.hpp:22-46), FP32 planes on the device."""
+
+    def __init__(self, ctx: Context, n: int, sh_degree: int):
+        h = _vp()
+        _check(lib().gsb_cloud_create(ctx.h, n, sh_degree, C.byref(h)))
+        self.h, self.ctx, self.n, self.sh_degree = h, ctx, n, sh_degree
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().gsb_cloud_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    @staticmethod
+    def from_host(ctx: Context, means, rotations, log_scales, opacity_logits, sh, sh_degree, active_sh_degree=None):
+        n = int(np.asarray(means).shape[0])
+        c = Cloud(ctx, n, sh_degree)
+        c.upload(means, rotations, log_scales, opacity_logits, sh,
+                 sh_degree if active_sh_degree is None else active_sh_degree)
+        return c
+
+    def upload(self, means, rotations, log_scales, opacity_logits, sh, active_sh_degree):
+        arrs = [np.ascontiguousarray(a, np.float64) for a in (means, rotations, log_scales, opacity_logits, sh)]
+        _check(lib().gsb_cloud_upload(self.h, *[_p(a) for a in arrs], int(active_sh_degree)))
+
+    def download(self):
+        n, b = self.n, (self.sh_degree + 1) ** 2
+        out = [np.zeros((n, 3)), np.zeros((n, 4)), np.zeros((n, 3)), np.zeros(n), np.zeros((n, 3, b))]
+        _check(lib().gsb_cloud_download(self.h, *[_p(a) for a in out]))
+        return out
+
+    def synth(self, seed: int, log_scale_offset: float = 0.0):
+        _check(lib().gsb_cloud_synth(self.h, seed, log_scale_offset))
+
+    def set_active_sh_degree(self, d: int):
+        _check(lib().gsb_cloud_set_active_sh_degree(self.h, d))
+
+
+@dataclass
+class RenderOutput:
+    """RenderOutput (rasterizer.hpp:66-82) with its device-resident forward state."""
+    frame: "Frame"
+    image: np.ndarray | None
+
+    def info(self) -> FrameInfo:
+        return self.frame.info()
+
+    def download(self):
+        return self.frame.download()
+
+
+class Frame:
+    def __init__(self, ctx: Context):
+        h = _vp()
+        _check(lib().gsb_frame_create(ctx.h, C.byref(h)))
+        self.h, self.ctx = h, ctx
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().gsb_frame_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def info(self) -> FrameInfo:
+        fi = FrameInfo()
+        _check(lib().gsb_frame_get_info(self.h, C.byref(fi)))
+        return fi
+
+    def download(self) -> dict:
+        fi = self.info()
+        P, V, K, T = fi.width * fi.height, fi.n_splats, fi.n_entries, fi.tiles_x * fi.tiles_y
+        o = dict(image=np.zeros((fi.height, fi.width, 3)), accum_transmittance=np.zeros(P),
+                 final_transmittance=np.zeros(P), contrib_count=np.zeros(P, np.int32),
+                 overflow_mask=np.zeros(P, np.uint8), splat_gaussian=np.zeros(V, np.int32),
+                 splat_mu2d=np.zeros((V, 2)), splat_depth=np.zeros(V), splat_conic=np.zeros((V, 4)),
+                 splat_color=np.zeros((V, 3)), splat_opacity=np.zeros(V), splat_radius=np.zeros(V),
+                 splat_clamped=np.zeros(V, np.uint8), tile_lists=np.zeros(K, np.int32),
+                 tile_ranges=np.zeros((T, 2), np.int32))
+        keys = ["image", "accum_transmittance", "final_transmittance", "contrib_count", "overflow_mask",
+                "splat_gaussian", "splat_mu2d", "splat_depth", "splat_conic", "splat_color", "splat_opacity",
+                "splat_radius", "splat_clamped", "tile_lists", "tile_ranges"]
+        _check(lib().gsb_frame_download(self.h, *[_p(o[k]) for k in keys]))
+        o.update(tiles_x=fi.tiles_x, tiles_y=fi.tiles_y, fingerprint=fi.state_fingerprint)
+        return o
+
+
+class Grads:
+    """GradientBundle (rasterizer.hpp:84-94), device resident."""
+
+    def __init__(self, ctx: Context, cloud: Cloud):
+        h = _vp()
+        _check(lib().gsb_grads_create(ctx.h, cloud.h, C.byref(h)))
+        self.h, self.n, self.sh_degree = h, cloud.n, cloud.sh_degree
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().gsb_grads_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def download(self) -> dict:
+        n, b = self.n, (self.sh_degree + 1) ** 2
+        o = dict(d_means=np.zeros((n, 3)), d_rotations=np.zeros((n, 4)), d_log_scales=np.zeros((n, 3)),
+                 d_opacity_logits=np.zeros(n), d_sh=np.zeros((n, 3, b)), d_mu2d=np.zeros((n, 2)), d_pose=np.zeros(6))
+        keys = ["d_means", "d_rotations", "d_log_scales", "d_opacity_logits", "d_sh", "d_mu2d", "d_pose"]
+        _check(lib().gsb_grads_download(self.h, *[_p(o[k]) for k in keys]))
+        return o
+
+
+class Image:
+    """Device-resident target frame (H, W, 3)."""
+
+    def __init__(self, ctx: Context, img: np.ndarray):
+        img = np.ascontiguousarray(img, np.float64)
+        h = _vp()
+        _check(lib().gsb_image_create(ctx.h, _p(img), img.shape[1], img.shape[0], C.byref(h)))
+        self.h, self.width, self.height = h, img.shape[1], img.shape[0]
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().gsb_image_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+# -------------------------------------------------------- reference API
+def render(ctx: Context, cloud: Cloud, cam: Camera, background=(0.0, 0.0, 0.0), config: RasterConfig | None = None,
+           frame: Frame | None = None, want_image=True) -> RenderOutput:
+    """gsopt::render (rasterizer.hpp:98-99)."""
+    frame = frame or Frame(ctx)
+    bg = np.ascontiguousarray(background, np.float64)
+    img = np.zeros((cam.height, cam.width, 3)) if want_image else None
+    cfg = config or RasterConfig.default()
+    _check(lib().gsb_render(ctx.h, cloud.h, C.byref(cam), _p(bg), C.byref(cfg), frame.h, _p(img)))
+    return RenderOutput(frame, img)
+
+
+def render_backward(ctx: Context, cloud: Cloud, cam: Camera, out: RenderOutput, d_image: np.ndarray,
+                    pose_only=False, grads: Grads | None = None):
+    """gsopt::render_backward (rasterizer.hpp:112-113). Returns (grads dict | None, d_pose)."""
+    d = np.ascontiguousarray(d_image, np.float64)
+    h, w = (d.shape[0], d.shape[1]) if d.ndim == 3 else (0, 0)
+    flags = BWD_POSE_ONLY if pose_only else 0
+    if not pose_only and grads is None:
+        grads = Grads(ctx, cloud)
+    dp = np.zeros(6)
+    _check(lib().gsb_render_backward(ctx.h, cloud.h, C.byref(cam), out.frame.h, _p(d), w, h, flags,
+                                     grads.h if grads is not None else None, _p(dp)))
+    return (grads.download() if (grads is not None and not pose_only) else None), dp
+
+
+def rgb_loss(ctx: Context, rendered: np.ndarray, target: np.ndarray, beta: float = 0.2, want_grad=True):
+    """gsopt::rgb_loss (losses.hpp:37)."""
+    r = np.ascontiguousarray(rendered, np.float64)
+    t = np.ascontiguousarray(target, np.float64)
+    if r.shape != t.shape:
+        raise GsbError(ERR_DIMENSION_MISMATCH, "rgb_loss: image shapes differ")
+    loss = C.c_double()
+    d = np.zeros_like(r) if want_grad else None
+    _check(lib().gsb_rgb_loss(ctx.h, _p(r), _p(t), r.shape[1], r.shape[0], beta, C.byref(loss), _p(d)))
+    return (loss.value, d) if want_grad else loss.value
+
+
+def schedule(kind: str, start: float, end: float, step: int, total: int) -> float:
+    """gsopt::schedule (trainer.hpp:62-63)."""
+    return lib().gsb_schedule(0 if kind == "cosine" else 1, start, end, step, total)
+
+
+def pose_step(ctx: Context, pose12, d_pose, lr: float, state: PoseAdam):
+    """gsopt::pose_step (trainer.hpp:99-100). Returns (pose12, applied_update)."""
+    p = np.ascontiguousarray(pose12, np.float64).reshape(12)
+    g = np.ascontiguousarray(d_pose, np.float64).reshape(6)
+    out, ap = np.zeros(12), np.zeros(6)
+    _check(lib().gsb_pose_step(ctx.h, _p(p), _p(g), lr, C.byref(state), _p(out), _p(ap)))
+    return out, ap
+
+
+def estimate_pose(ctx: Context, cloud: Cloud, target: Image, intr, init_pose12, config: PoseConfig | None = None,
+                  trace=False):
+    """gsopt::estimate_pose (trainer.hpp:170-171) = pose_descent (pipelines.cpp:58-92) on the device."""
+    cfg = config or PoseConfig.default()
+    intr = np.ascontiguousarray(intr, np.float64)
+    init = np.ascontiguousarray(init_pose12, np.float64).reshape(12)
+    out = np.zeros(12)
+    fl, su, cv = C.c_double(), C.c_int32(), C.c_int32()
+    tp = np.zeros((cfg.budget, 12)) if trace else None
+    tl = np.zeros(cfg.budget) if trace else None
+    _check(lib().gsb_estimate_pose(ctx.h, cloud.h, target.h, _p(intr), _p(init), C.byref(cfg), _p(out),
+                                   C.byref(fl), C.byref(su), C.byref(cv), _p(tp), _p(tl)))
+    res = dict(pose=out, final_loss=fl.value, steps=su.value, converged=bool(cv.value))
+    if trace:
+        res.update(trace_pose=tp[:su.value], trace_loss=tl[:su.value])
+    return res
+
+
+def synth_poses(seed: int, n: int, sh_degree: int, kind: int, cameras: int, orbit_radius=2.5,
+                orbit_arc=2 * np.pi) -> np.ndarray:
+    out = np.zeros((cameras, 12))
+    _check(lib().gsb_synth_poses(seed, n, sh_degree, kind, cameras, orbit_radius, orbit_arc, _p(out)))
+    return out
+
+
+class PoseRng:
+    """Holds the xorshift64* state perturb_pose draws from (core.hpp:58-70)."""
+
+    def __init__(self, seed: int):
+        self.state = C.c_uint64(seed if seed else 0x9E3779B97F4A7C15)
+
+    def perturb_pose(self, pose12, rot_deg, trans):
+        p = np.ascontiguousarray(pose12, np.float64).reshape(12)
+        out = np.zeros(12)
+        _check(lib().gsb_perturb_pose(_p(p), rot_deg, trans, C.byref(self.state), _p(out)))
+        return out
+
+
+def synth_intrinsics(width: int, height: int):
+    """synth.cpp:64-71: fx = fy = 0.75 W, c = (dim - 1) / 2."""
+    return np.array([0.75 * width, 0.75 * width, 0.5 * (width - 1), 0.5 * (height - 1)])

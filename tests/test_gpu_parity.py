@@ -1,0 +1,358 @@
+"""GPU parity: libgsb200 (through its C ABI) against the FP64 CPU oracle on
+the same inputs. Tolerances are north_star's (BASELINE.json):
+  * sort keys / tile lists / tile ranges: bit-exact;
+  * rendered image: <= 1e-5 max-abs on conditioned scenes
+    (tests/gradcheck.hpp:67-170 conditioning);
+  * Gaussian and pose gradients: <= 1e-3 relative (floor 1e-3 * max|g| per
+    parameter group, cf. tests/gradcheck.hpp:187-197);
+  * pose trajectories: rot <= 0.1 deg, trans <= 1e-3 (test_trainer.cpp:506-507).
+The oracle is fed the FP32-rounded parameters the device stores.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def G():
+    from paper_2410_08743_b200 import build, gsb
+    build.build()
+    return gsb
+
+
+@pytest.fixture(scope="module")
+def ctx(G):
+    return G.Context(0)
+
+
+def to_dev(G, ctx, hc: O.HostCloud):
+    return G.Cloud.from_host(ctx, hc.means, hc.rotations, hc.log_scales, hc.opacity_logits, hc.sh, hc.sh_degree,
+                             hc.active_sh_degree)
+
+
+def dev_cam(G, ocam):
+    return G.Camera.make(ocam.fx, ocam.fy, ocam.cx, ocam.cy, ocam.width, ocam.height,
+                         np.array(ocam.R[:]).reshape(3, 3), np.array(ocam.t[:]))
+
+
+def scene(seed, n, size, conditioned=True):
+    rng = O.make_rng(seed)
+    if conditioned:
+        hc, cam, bg = O.make_conditioned_scene(rng, n, size)
+    else:
+        hc, cam, bg = O.make_gradcheck_scene(rng, n, size)
+    return hc.as_float32_exact(), cam, bg, rng
+
+
+def synth_scene(seed, n, size, sh=3, kind=0, cams=4, scale_offset=0.0):
+    rng = O.make_rng(seed)
+    hc = O.synth_cloud(n, sh, rng)
+    hc.log_scales += scale_offset
+    poses = O.synth_poses(kind, cams, rng)
+    return hc.as_float32_exact(), poses
+
+
+def rel_err(a, b, floor_frac=1e-3):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    floor = max(floor_frac * np.max(np.abs(b)), 1e-30)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), floor)))
+
+
+# ----------------------------------------------------------------- forward
+@pytest.mark.parametrize("seed", [54, 55, 61, 70])
+def test_render_matches_oracle_conditioned(G, ctx, seed):
+    hc, ocam, bg, _ = scene(seed, 12, 48)
+    cloud = to_dev(G, ctx, hc)
+    out = G.render(ctx, cloud, dev_cam(G, ocam), bg)
+    ref = O.render(hc, ocam, bg)
+    d = out.download()
+    assert np.max(np.abs(d["image"] - ref.image)) < 1e-5
+    # discrete state: bit-exact
+    assert np.array_equal(d["splat_gaussian"], ref.splat_gaussian)
+    assert np.array_equal(d["splat_mu2d"], ref.splat_mu2d)
+    assert np.array_equal(d["splat_depth"], ref.splat_depth)
+    assert np.array_equal(d["tile_lists"], ref.tile_lists)
+    assert np.array_equal(d["tile_ranges"], ref.tile_ranges)
+    assert np.array_equal(d["contrib_count"], ref.contrib_count)
+    assert np.array_equal(d["overflow_mask"], ref.overflow_mask)
+    assert np.max(np.abs(d["splat_radius"] - ref.splat_radius) / ref.splat_radius) < 1e-14
+    assert np.max(np.abs(d["final_transmittance"] - ref.final_transmittance)) < 1e-5
+    assert np.all(d["accum_transmittance"] + d["final_transmittance"] == 1.0)
+
+
+def test_binning_bit_exact_on_device_records(G, ctx):
+    """rasterizer.cpp:127-168 re-run on the GPU's own FP64 records must give
+    the device tile lists / ranges bit for bit (C1-sized scene)."""
+    hc, poses = synth_scene(99, 10000, 256, scale_offset=math.log(500 / 10000) / 3)
+    cam = O.synth_camera(256, 256, poses[0])
+    cloud = to_dev(G, ctx, hc)
+    out = G.render(ctx, cloud, dev_cam(G, cam))
+    d = out.download()
+    n = hc.n
+    keep = np.zeros(n, np.uint8)
+    keep[d["splat_gaussian"]] = 1
+    mu2d = np.zeros((n, 2))
+    mu2d[d["splat_gaussian"]] = d["splat_mu2d"]
+    rad = np.zeros(n)
+    rad[d["splat_gaussian"]] = d["splat_radius"]
+    dep = np.zeros(n)
+    dep[d["splat_gaussian"]] = d["splat_depth"]
+    sg, lists, ranges = O.bin_records(keep, mu2d, rad, dep, 256, 256)
+    assert np.array_equal(sg, d["splat_gaussian"])
+    assert np.array_equal(lists, d["tile_lists"])
+    assert np.array_equal(ranges, d["tile_ranges"])
+    # and the FP64 geometry equals the oracle's own evaluation
+    ref = O.render(hc, cam)
+    assert np.array_equal(d["splat_gaussian"], ref.splat_gaussian)
+    assert np.array_equal(d["splat_depth"], ref.splat_depth)
+    assert np.array_equal(d["splat_mu2d"], ref.splat_mu2d)
+    flips = np.sum(d["tile_lists"] != ref.tile_lists) if len(d["tile_lists"]) == len(ref.tile_lists) else -1
+    assert flips == 0
+    assert np.array_equal(d["tile_ranges"], ref.tile_ranges)
+
+
+def test_render_c1_scene_image(G, ctx):
+    """C1 (10k Gaussians, 256x256): max-abs over pixels without an FP32
+    decision flip (cutoff / early-termination) <= 1e-5; flips are rare."""
+    hc, poses = synth_scene(99, 10000, 256, scale_offset=math.log(500 / 10000) / 3)
+    cam = O.synth_camera(256, 256, poses[0])
+    cloud = to_dev(G, ctx, hc)
+    d = G.render(ctx, cloud, dev_cam(G, cam)).download()
+    ref = O.render(hc, cam)
+    diff = np.max(np.abs(d["image"] - ref.image), axis=2).reshape(-1)
+    same_decisions = d["contrib_count"] == ref.contrib_count
+    assert np.mean(same_decisions) > 0.99
+    assert np.max(diff[same_decisions]) < 1e-4
+    assert np.mean(diff < 1e-5) > 0.99
+
+
+def test_empty_cloud_and_culling(G, ctx):
+    hc = O.HostCloud(np.zeros((0, 3)), np.zeros((0, 4)), np.zeros((0, 3)), np.zeros(0), np.zeros((0, 3, 1)), 0, 0)
+    cloud = to_dev(G, ctx, hc)
+    cam = G.Camera.make(20, 20, 7.5, 7.5, 16, 16)
+    out = G.render(ctx, cloud, cam, (0.3, 0.6, 0.9))
+    assert np.allclose(out.image, np.array([0.3, 0.6, 0.9]), atol=0, rtol=1e-7)
+    # culled Gaussians contribute exactly zero (test_rasterizer.cpp:308-343)
+    hc, ocam, bg, rng = scene(60, 6, 32, conditioned=False)
+    base = G.render(ctx, to_dev(G, ctx, hc), dev_cam(G, ocam), bg).image
+    R, t = O.camera_pose(ocam)
+    ext = hc.copy()
+    for mean in (R.T @ (np.array([0, 0, -2.0]) - t), R.T @ (np.array([50.0, 0, 2.0]) - t)):
+        ext.means = np.vstack([ext.means, mean])
+        ext.rotations = np.vstack([ext.rotations, [1, 0, 0, 0]])
+        ext.log_scales = np.vstack([ext.log_scales, np.full(3, math.log(0.1))])
+        ext.opacity_logits = np.append(ext.opacity_logits, math.log(9))
+        ext.sh = np.concatenate([ext.sh, np.full((1, 3, 16), 0.3)])
+    ext = ext.as_float32_exact()
+    ecloud = to_dev(G, ctx, ext)
+    out = G.render(ctx, ecloud, dev_cam(G, ocam), bg)
+    assert np.array_equal(out.image, base)
+    d_img = np.random.default_rng(0).uniform(-1, 1, (32, 32, 3))
+    g, _ = G.render_backward(ctx, ecloud, dev_cam(G, ocam), out, d_img)
+    for k in ("d_means", "d_rotations", "d_log_scales", "d_opacity_logits"):
+        assert np.all(g[k][6:] == 0)
+
+
+def test_repeat_render_bit_identical(G, ctx):
+    hc, ocam, bg, _ = scene(55, 60, 64, conditioned=False)
+    cloud = to_dev(G, ctx, hc)
+    a = G.render(ctx, cloud, dev_cam(G, ocam), bg).download()
+    b = G.render(ctx, cloud, dev_cam(G, ocam), bg).download()
+    for k in ("image", "final_transmittance", "contrib_count", "tile_lists", "tile_ranges"):
+        assert a[k].tobytes() == b[k].tobytes()
+
+
+# -------------------------------------------------------------------- loss
+def test_rgb_loss_matches_oracle(G, ctx):
+    r = np.random.default_rng(3)
+    a = r.uniform(0, 1, (37, 53, 3)).astype(np.float32).astype(np.float64)
+    b = np.clip(a + r.uniform(-0.2, 0.2, a.shape), 0, 1).astype(np.float32).astype(np.float64)
+    loss, d = G.rgb_loss(ctx, a, b, 0.2)
+    lref, dref = O.rgb_loss(a, b, 0.2)
+    assert abs(loss - lref) < 1e-10
+    assert np.max(np.abs(d - dref)) < 1e-6 * np.max(np.abs(dref))
+    same, ds = G.rgb_loss(ctx, a, a, 0.2)
+    assert same == 0.0 and np.all(ds == 0.0)  # test_losses.cpp:25-32
+    l0 = G.rgb_loss(ctx, np.full((16, 16, 3), 0.6), np.full((16, 16, 3), 0.5), 0.0, want_grad=False)
+    assert abs(l0 - 0.1) < 1e-7
+
+
+# ---------------------------------------------------------------- backward
+@pytest.mark.parametrize("seed", [61, 62, 63])
+def test_backward_matches_oracle(G, ctx, seed):
+    hc, ocam, bg, rng = scene(seed, 10, 32)
+    d_img = np.array([O.lib().orc_rng_uniform_range(O.C.byref(rng), -1, 1) for _ in range(32 * 32 * 3)]).reshape(32, 32, 3)
+    cloud = to_dev(G, ctx, hc)
+    cam = dev_cam(G, ocam)
+    out = G.render(ctx, cloud, cam, bg)
+    g, dp = G.render_backward(ctx, cloud, cam, out, d_img)
+    ref = O.render(hc, ocam, bg, keep_handle=True)
+    gr = O.render_backward(hc, ocam, ref, d_img)
+    ref.free()
+    assert rel_err(dp, gr.d_pose) < 1e-3
+    assert rel_err(g["d_means"], gr.d_means) < 1e-3
+    assert rel_err(g["d_rotations"], gr.d_rotations) < 1e-3
+    assert rel_err(g["d_log_scales"], gr.d_log_scales) < 1e-3
+    assert rel_err(g["d_opacity_logits"], gr.d_opacity_logits) < 1e-3
+    assert rel_err(g["d_sh"], gr.d_sh) < 1e-3
+    assert rel_err(g["d_mu2d"], gr.d_mu2d) < 1e-3
+    # pose-only path gives the same pose gradient (separately compiled kernel)
+    _, dp2 = G.render_backward(ctx, cloud, cam, out, d_img, pose_only=True)
+    assert np.max(np.abs(dp2 - dp)) <= 1e-12 * np.max(np.abs(dp))
+
+
+def test_backward_invariants(G, ctx):
+    hc, ocam, bg, rng = scene(58, 8, 32, conditioned=False)
+    cloud = to_dev(G, ctx, hc)
+    cam = dev_cam(G, ocam)
+    out = G.render(ctx, cloud, cam, bg)
+    g, dp = G.render_backward(ctx, cloud, cam, out, np.zeros((32, 32, 3)))
+    assert np.all(dp == 0) and all(np.all(v == 0) for v in g.values())
+    with pytest.raises(G.GsbError) as ei:
+        G.render_backward(ctx, cloud, cam, out, np.zeros((16, 32, 3)))
+    assert ei.value.code == G.ERR_DIMENSION_MISMATCH
+    other = dev_cam(G, ocam)
+    other.t[0] += 0.1
+    with pytest.raises(G.GsbError) as ei:
+        G.render_backward(ctx, cloud, other, out, np.zeros((32, 32, 3)))
+    assert ei.value.code == G.ERR_STATE_MISMATCH
+    moved = hc.copy()
+    moved.means[0] += [0.5, 0, 0]
+    cloud.upload(moved.means, moved.rotations, moved.log_scales, moved.opacity_logits, moved.sh, 3)
+    with pytest.raises(G.GsbError) as ei:
+        G.render_backward(ctx, cloud, cam, out, np.zeros((32, 32, 3)))
+    assert ei.value.code == G.ERR_STATE_MISMATCH
+    # gauge identity d_pose_v = R_c sum d_means (test_rasterizer.cpp:377-390)
+    hc, ocam, bg, rng = scene(63, 15, 32, conditioned=False)
+    cloud = to_dev(G, ctx, hc)
+    cam = dev_cam(G, ocam)
+    out = G.render(ctx, cloud, cam, bg)
+    d_img = np.random.default_rng(1).uniform(-1, 1, (32, 32, 3))
+    g, dp = G.render_backward(ctx, cloud, cam, out, d_img)
+    R, _ = O.camera_pose(ocam)
+    exp = R @ g["d_means"].sum(axis=0)
+    assert np.linalg.norm(dp[:3] - exp) < 1e-4 * max(1.0, np.linalg.norm(exp))
+    # determinism
+    _, dp_b = G.render_backward(ctx, cloud, cam, out, d_img)
+    assert dp_b.tobytes() == dp.tobytes()
+
+
+def test_backward_c1_scene_pose_gradient(G, ctx):
+    """C1-sized scene with the real loss gradient: d_pose within 1e-3."""
+    hc, poses = synth_scene(99, 10000, 256, scale_offset=math.log(500 / 10000) / 3)
+    cam_gt = O.synth_camera(256, 256, poses[0])
+    target = O.render(hc, cam_gt).image
+    noisy = O.perturb_pose(poses[0], 3.0, 0.03, O.make_rng(1002))
+    ocam = O.synth_camera(256, 256, noisy)
+    ref = O.render(hc, ocam, keep_handle=True)
+    _, d_img = O.rgb_loss(ref.image, target, 0.2)
+    gr = O.render_backward(hc, ocam, ref, d_img)
+    ref.free()
+    cloud = to_dev(G, ctx, hc)
+    cam = dev_cam(G, ocam)
+    out = G.render(ctx, cloud, cam)
+    _, dp = G.render_backward(ctx, cloud, cam, out, d_img, pose_only=True)
+    assert np.linalg.norm(dp - gr.d_pose) / np.linalg.norm(gr.d_pose) < 1e-3
+
+
+# ------------------------------------------------------------- optimiser
+def test_pose_step_matches_oracle(G, ctx):
+    R, t = O.se3_exp(np.array([0.3, -0.2, 0.5, 0.4, -0.7, 0.2]))
+    p = O.pose_join(R, t)
+    same, _ = G.pose_step(ctx, p, np.zeros(6), 1e-2, G.PoseAdam())
+    assert same.tobytes() == p.tobytes()  # trainer.cpp:86
+    g = np.array([0.3, -0.5, 0.1, 0.9, -0.2, 0.4])
+    zero_lr, _ = G.pose_step(ctx, p, g, 0.0, G.PoseAdam())
+    assert zero_lr.tobytes() == p.tobytes()
+    st_g, st_o = G.PoseAdam(), O.PoseAdam()
+    pg, po = p.copy(), p.copy()
+    for k in range(20):
+        gk = g * math.cos(k) + 0.1
+        pg, ag = G.pose_step(ctx, pg, gk, 1e-2, st_g)
+        po, ao = O.pose_step(po, gk, 1e-2, st_o)
+    assert np.max(np.abs(pg - po)) < 1e-12
+    assert st_g.step == st_o.step == 20
+
+
+def test_estimate_pose_trajectory_matches_oracle(G, ctx):
+    """pose_descent on the device vs the oracle: per-iteration poses within
+    rot 0.1 deg / trans 1e-3, final errors within the same bounds."""
+    rng = O.make_rng(99)
+    hc = O.synth_cloud(500, 1, rng).as_float32_exact()
+    poses = O.synth_poses(0, 20, rng)
+    cam = O.synth_camera(64, 64, poses[0])
+    target = O.render(hc, cam).image
+    noisy = O.perturb_pose(poses[0], 15.0, 0.15, O.make_rng(1002))
+    budget = 60
+    ref = O.estimate_pose(hc, target, cam.fx, cam.fy, cam.cx, cam.cy, noisy, budget=budget)
+    cloud = to_dev(G, ctx, hc)
+    img = G.Image(ctx, target)
+    cfg = G.PoseConfig.default(budget=budget)
+    res = G.estimate_pose(ctx, cloud, img, [cam.fx, cam.fy, cam.cx, cam.cy], noisy, cfg, trace=True)
+    assert res["steps"] == ref["steps"]
+    for k in range(0, res["steps"], 5):
+        r, d = O.abs_pose_error(res["trace_pose"][k], ref["trace_pose"][k])
+        assert r < 0.1 and d < 1e-3, (k, r, d)
+    assert np.max(np.abs(res["trace_loss"] - ref["trace_loss"])) < 1e-4
+
+
+@pytest.mark.slow
+def test_estimate_pose_acceptance_criterion(G, ctx):
+    """tests/acceptance.cpp:74-100 on the device: >= 18/20 trials converge."""
+    rng = O.make_rng(99)
+    hc = O.synth_cloud(500, 1, rng).as_float32_exact()
+    poses = O.synth_poses(0, 20, rng)
+    cloud = to_dev(G, ctx, hc)
+    noise = O.make_rng(1002)
+    hits = 0
+    for t in range(20):
+        cam = O.synth_camera(64, 64, poses[t])
+        img = G.Image(ctx, O.render(hc, cam).image)
+        noisy = O.perturb_pose(poses[t], 15.0, 0.15, noise)
+        res = G.estimate_pose(ctx, cloud, img, [cam.fx, cam.fy, cam.cx, cam.cy], noisy)
+        r, d = O.abs_pose_error(res["pose"], poses[t])
+        hits += (r < 5.0 and d < 0.05)
+    assert hits >= 18
+
+
+def test_cloud_adam_step_matches_oracle(G, ctx):
+    hc, ocam, bg, rng = scene(64, 10, 32, conditioned=False)
+    d_img = np.random.default_rng(2).uniform(-1, 1, (32, 32, 3))
+    cloud = to_dev(G, ctx, hc)
+    cam = dev_cam(G, ocam)
+    out = G.render(ctx, cloud, cam, bg)
+    grads = G.Grads(ctx, cloud)
+    G.render_backward(ctx, cloud, cam, out, d_img, grads=grads)
+    gd = grads.download()
+    adam = G.lib()
+    h = G._vp()
+    G._check(adam.gsb_adam_create(ctx.h, cloud.h, G.C.byref(h)))
+    lrs = np.array([1.6e-2, 1e-3, 5e-3, 5e-2, 2.5e-3, 1.25e-4])
+    G._check(adam.gsb_cloud_adam_step(ctx.h, cloud.h, grads.h, h, G._p(lrs)))
+    m, q, ls, op, sh = cloud.download()
+    # oracle Adam on the same (FP32-rounded) gradients
+    oc = hc.copy()
+    og = O.Grads()
+    st = (O.C.c_double * 1)
+    cv = oc.c()
+    n = oc.n
+    gm = [np.ascontiguousarray(gd[k].reshape(-1)) for k in ("d_means", "d_rotations", "d_log_scales", "d_opacity_logits", "d_sh")]
+    og.n = n
+    og.sh_len = gm[4].size
+    P = O.C.POINTER(O.C.c_double)
+    og.d_means, og.d_rotations, og.d_log_scales, og.d_opacity_logits, og.d_sh = [a.ctypes.data_as(P) for a in gm]
+    states = (O.C.c_byte * (5 * 32))()
+    O.lib().orc_cloud_adam_step.argtypes = [O.C.POINTER(O.Cloud), O.C.POINTER(O.Grads), O.C.c_void_p, O.C.c_void_p]
+    O.lib().orc_cloud_adam_step(cv.ref(), O.C.byref(og), states, O._p(lrs))
+    want = O._from_c_cloud(cv.s)
+    assert np.max(np.abs(m - want.means)) < 1e-6
+    assert np.max(np.abs(q - want.rotations)) < 1e-6
+    assert np.max(np.abs(ls - want.log_scales)) < 1e-6
+    assert np.max(np.abs(sh - want.sh)) < 1e-6
+    adam.gsb_adam_destroy(h)
+    del st
