@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""Benchmark: forward + backward(pose gradient) pose-estimation iterations/s on
+a 1M-Gaussian, 1008x756 synthetic scene (BASELINE.json config C3), one
+process per GPU, views sharded across ranks with no data-path collective.
+
+One step = one pose_descent iteration (render -> L1+SSIM loss -> backward with
+the SE(3) pose gradient -> pose step; pipelines.cpp:66-90) for each of the
+rank's views, all inputs resident in HBM. `value` = iterations/s over all
+ranks (max-over-ranks device time). `e2e` = the same metric through the public
+C-ABI call a user makes (gsb_estimate_pose) starting from host FP64 images,
+host<->device copies inside the timed region. `--impl reference` times the
+reference algorithm on the host CPU (oracle port) on the same
+workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_GAUSS = 1_000_000
+WIDTH, HEIGHT = 1008, 756
+TOTAL_VIEWS = 64            # C3: 64 independent views
+VIEWS_PER_GPU = 8           # weak scaling: 8 views per rank (64 at 8 GPUs)
+SCENE_SEED = 3
+NOISE_SEED = 1002
+SH_DEGREE = 3
+METRIC = "fwd+bwd(pose grad) iters/sec @1M Gaussians 1008x756"
+
+
+def log_scale_offset(n):
+    """log_scales += ln(500/N)/3 keeps the reference's 500-Gaussian footprint density."""
+    return math.log(500.0 / n) / 3.0 if n > 500 else 0.0
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[3 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------- scene
+def all_views():
+    """GT poses (forward-facing, synth.cpp:86-90) and perturbed inits
+    (perturb_pose 15 deg / 0.15, eval.cpp:130-146, Rng(1002)) for all 64 views."""
+    from paper_2410_08743_b200 import gsb
+    gt = gsb.synth_poses(SCENE_SEED, N_GAUSS, SH_DEGREE, 1, TOTAL_VIEWS)
+    rng = gsb.PoseRng(NOISE_SEED)
+    init = np.stack([rng.perturb_pose(p, 15.0, 0.15) for p in gt])
+    return gt, init
+
+
+def my_views(rank, ws):
+    return [(rank * VIEWS_PER_GPU + k) % TOTAL_VIEWS for k in range(VIEWS_PER_GPU)]
+
+
+def fp32_peak_tflops(sm_count, clock_mhz):
+    return sm_count * 128 * 2 * clock_mhz * 1e6 / 1e12
+
+
+# ------------------------------------------------------------ our arm
+def run_ours(args, ws, rank, local):
+    from paper_2410_08743_b200 import gsb
+    dist = None
+    if ws > 1:
+        import torch
+        import torch.distributed as td
+        torch.cuda.set_device(local)
+        td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = td
+    ctx = gsb.Context(local)
+    cloud = gsb.Cloud(ctx, N_GAUSS, SH_DEGREE)
+    cloud.synth(SCENE_SEED, log_scale_offset(N_GAUSS))
+    gt, init = all_views()
+    intr = gsb.synth_intrinsics(WIDTH, HEIGHT)
+    views = my_views(rank, ws)
+    host_targets, images = {}, {}
+    for v in views:
+        cam = gsb.Camera.from_pose12(*intr, WIDTH, HEIGHT, gt[v])
+        host_targets[v] = gsb.render(ctx, cloud, cam).image
+        images[v] = gsb.Image(ctx, host_targets[v])
+    budget = max(100, args.warmup + args.steps + 2)
+    cfg = gsb.PoseConfig.default(budget=budget, pose_converged_eps=0.0)
+    sessions = [gsb.PoseSession(ctx, cloud, images[v], intr, init[v], cfg) for v in views]
+
+    def step():
+        for s in sessions:
+            s.step(1)
+
+    for _ in range(args.warmup):
+        step()
+    ctx.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ctx.set_profiling(True)
+    ctx.stage_times(reset=True)
+    launches0 = ctx.launch_count()
+    ctx.timer_start()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dev_ms = ctx.timer_stop()
+    wall_s = time.perf_counter() - t0
+    launches = ctx.launch_count() - launches0
+    stages = ctx.stage_times(reset=True)
+    ctx.set_profiling(False)
+    clk = clocks.stop()
+    if dist:
+        import torch
+        t = torch.tensor([dev_ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms = float(t.item())
+    iters = VIEWS_PER_GPU * ws * args.steps
+    value = iters / (dev_ms / 1e3)
+    fi = sessions[0].frame_info()
+    res = sessions[0].read()
+
+    # ---- e2e: gsb_estimate_pose from host FP64 images (the user-facing call)
+    e2e_iters = args.e2e_iters
+    e2e_cfg = gsb.PoseConfig.default(budget=e2e_iters, pose_converged_eps=0.0)
+    if dist:
+        dist.barrier()
+    ctx.synchronize()
+    t0 = time.perf_counter()
+    h2d = d2h = 0
+    for v in views:
+        img = gsb.Image(ctx, host_targets[v])                 # H2D of the view's frame
+        out = gsb.estimate_pose(ctx, cloud, img, intr, init[v], e2e_cfg)
+        h2d += host_targets[v].size * 4 + 12 * 8            # FP32 planes uploaded + pose
+        d2h += 12 * 8 + 8 + 8                                 # pose, loss, steps/flags
+        assert out["steps"] == e2e_iters
+        del img
+    ctx.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        import torch
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = VIEWS_PER_GPU * ws * e2e_iters / e2e_s
+
+    out = None
+    if rank == 0:
+        # roofline for the dominant stage
+        per_iter_stage_ms = {k: v[0] / (VIEWS_PER_GPU * args.steps) for k, v in stages.items() if v[1] > 0}
+        dom = max(per_iter_stage_ms, key=per_iter_stage_ms.get)
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+            os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+        cpu = None
+        work = None
+        if not args.no_cpu_baseline and ws == 1:
+            cpu, work = cpu_baseline(args, gt[views[0]], init[views[0]], intr)
+        roof = roofline(dom, per_iter_stage_ms[dom], fi, work, peaks, clk)
+        out = {
+            "metric": METRIC, "value": round(value, 3), "unit": "iters/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(dev_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (fp64 geometry, pose step and loss accumulation)",
+            "data": "synthetic (synth.cpp draw sequence, seed 3; targets rendered at GT poses)",
+            "config": {"workload": f"C3 pose estimation: {N_GAUSS} Gaussians SH3, {WIDTH}x{HEIGHT}, "
+                                   f"{VIEWS_PER_GPU} views/GPU ({TOTAL_VIEWS} at 8 GPUs), forward-facing, "
+                                   f"perturb 15deg/0.15", "views_per_gpu": VIEWS_PER_GPU,
+                       "n_gaussians": N_GAUSS, "width": WIDTH, "height": HEIGHT,
+                       "l2": "inputs larger than L2 (236 MB cloud + per-view state > 126 MB L2)",
+                       "parallelism": f"views sharded over {ws} GPU(s), no collective"},
+            "e2e": {"value": round(e2e_value, 3), "unit": "iters/s", "h2d_bytes_per_step": int(h2d * ws / e2e_iters),
+                    "d2h_bytes_per_step": int(d2h * ws / e2e_iters),
+                    "how": f"gsb_estimate_pose per view from host FP64 HWC image, {e2e_iters} iterations; "
+                           "bytes per iteration-of-all-views"},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "roofline": roof,
+            "stages_ms_per_iter": {k: round(v, 4) for k, v in per_iter_stage_ms.items()},
+            "scene": {"n_splats": int(fi.n_splats), "n_entries": int(fi.n_entries)},
+            "wall_s": round(wall_s, 3),
+            "pose_check": {"view": int(views[0]), "final_loss": res["final_loss"], "steps": res["steps"]},
+        }
+        if cpu is not None:
+            out["cpu_baseline"] = cpu
+        if work is not None:
+            out["work_counts"] = work
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return out
+
+
+def roofline(stage, ms, fi, work, peaks, clk):
+    """Dominant-stage roofline (SURVEY §8d units)."""
+    V, K = fi.n_splats, fi.n_entries
+    P = fi.width * fi.height
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md fallback 6.65 TB/s"
+    bytes_per = {
+        "preprocess": 12 * N_GAUSS + 224 * V + 52 * V,
+        "sort": 8 * V + 16 * V + 12 * K + 24 * K + 8 * K + 8 * fi.tiles_x * fi.tiles_y,
+        "loss": 24 * P + 12 * P,
+        "bwd_geom": 36 * K + 288 * V + 8 * V,
+    }
+    if stage in ("composite", "bwd_raster") and work is not None:
+        hf, cf, hb, cb = work["H_f"], work["C_f"], work["H_b"], work["C_b"]
+        flops = 26 * hf + 12 * cf if stage == "composite" else 64 * hb + 12 * cb
+        clk_mhz = peaks.get("sm_max_mhz", 1965.0)
+        peak = fp32_peak_tflops(148, clk_mhz)
+        achieved = flops / (ms / 1e3) / 1e12
+        return {"stage": stage, "bound": "fp32", "achieved": round(achieved, 3), "peak": round(peak, 2),
+                "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                "peak_source": "nominal FP32 = 148 SM x 128 lanes x 2 x sm_max_mhz (no FP32 entry in "
+                               "MEASURED_PEAKS.json)",
+                "frac_at_measured_clock": round(achieved / fp32_peak_tflops(148, clk["sm_mhz"]), 4)
+                if clk.get("sm_mhz") else None,
+                "algorithmic": f"{flops} FLOP per launch (SURVEY §8d)", "ms_per_launch": round(ms, 4)}
+    if stage in bytes_per:
+        b = bytes_per[stage]
+        achieved = b / (ms / 1e3) / 1e9
+        return {"stage": stage, "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(achieved / hbm_peak, 4), "traffic": None, "peak_source": hbm_src,
+                "algorithmic": f"{b} bytes per launch (SURVEY §8d)", "ms_per_launch": round(ms, 4)}
+    return {"stage": stage, "bound": "fp32", "achieved": None, "peak": None, "unit": "TFLOP/s", "frac": None,
+            "traffic": None, "note": "work counts unavailable (cpu baseline skipped)", "ms_per_launch": round(ms, 4)}
+
+
+# ------------------------------------------------------- CPU (oracle)
+def _oracle_scene():
+    from oracle import oracle as O
+    rng = O.make_rng(SCENE_SEED)
+    hc = O.synth_cloud(N_GAUSS, SH_DEGREE, rng)
+    hc.log_scales += log_scale_offset(N_GAUSS)
+    return O, hc.as_float32_exact()
+
+
+def cpu_baseline(args, gt12, init12, intr, iters=None):
+    """Reference algorithm (oracle port, FP64, all host threads) on the same
+    scene: pose_descent iterations on one view, timed per iteration."""
+    O, hc = _oracle_scene()
+    cam_gt = O.make_camera(intr[0], intr[1], intr[2], intr[3], WIDTH, HEIGHT, *O.pose_split(gt12))
+    target = O.render(hc, cam_gt).image
+    iters = iters or args.cpu_iters
+    t0 = time.perf_counter()
+    res = O.estimate_pose(hc, target, intr[0], intr[1], intr[2], intr[3], init12, budget=iters,
+                          pose_converged_eps=0.0)
+    dt = time.perf_counter() - t0
+    cam0 = O.make_camera(intr[0], intr[1], intr[2], intr[3], WIDTH, HEIGHT, *O.pose_split(init12))
+    rr = O.render(hc, cam0, keep_handle=True)
+    _, d_img = O.rgb_loss(rr.image, target, 0.2)
+    hf, cf, hb, cb = O.count_work(rr, d_img)
+    rr.free()
+    cpu = {"value": round(res["steps"] / dt, 5), "unit": "iters/s", "cores": O.num_threads(), "kind": "port",
+           "sample": f"{res['steps']} pose_descent iterations (render+rgb_loss+render_backward+pose_step) of view "
+                     f"0 at full size ({N_GAUSS} Gaussians, {WIDTH}x{HEIGHT}), FP64 oracle port, "
+                     f"{dt:.1f} s"}
+    work = {"H_f": hf, "C_f": cf, "H_b": hb, "C_b": cb, "source": "oracle count_work at the init pose of view 0"}
+    return cpu, work
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return None
+    from paper_2410_08743_b200 import gsb  # host-only helpers for the pose list (no device use)
+    gt = gsb.synth_poses(SCENE_SEED, N_GAUSS, SH_DEGREE, 1, TOTAL_VIEWS)
+    rng = gsb.PoseRng(NOISE_SEED)
+    init = rng.perturb_pose(gt[0], 15.0, 0.15)
+    intr = gsb.synth_intrinsics(WIDTH, HEIGHT)
+    O, hc = _oracle_scene()
+    cam_gt = O.make_camera(intr[0], intr[1], intr[2], intr[3], WIDTH, HEIGHT, *O.pose_split(gt[0]))
+    target = O.render(hc, cam_gt).image
+    # warmup W iterations, then K timed iterations (one step = one iteration of one view)
+    O.estimate_pose(hc, target, *intr, init, budget=max(args.warmup, 1), pose_converged_eps=0.0)
+    t0 = time.perf_counter()
+    res = O.estimate_pose(hc, target, *intr, init, budget=args.steps, pose_converged_eps=0.0)
+    dt = time.perf_counter() - t0
+    value = res["steps"] / dt
+    return {"metric": METRIC, "value": round(value, 5), "unit": "iters/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1e3 * dt / max(res["steps"], 1), 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp64",
+            "data": "synthetic (same scene as the GPU arm)", "impl": "reference",
+            "config": {"workload": f"C3 pose estimation: {N_GAUSS} Gaussians SH3, {WIDTH}x{HEIGHT}, one view per step",
+                       "parallelism": "host threads (OpenMP), rank 0 only"},
+            "cpu_baseline": {"value": round(value, 5), "unit": "iters/s", "cores": O.num_threads(), "kind": "port",
+                             "sample": f"{res['steps']} timed pose_descent iterations of view 0 at full size"},
+            "e2e": {"value": round(value, 5), "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-iters", type=int, default=10)
+    ap.add_argument("--cpu-iters", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_env()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        out = run_reference(args, ws, rank)
+    else:
+        out = run_ours(args, ws, rank, local)
+    if out is not None and rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -120,6 +120,9 @@ int gsb_ctx_set_profiling(gsb_ctx* ctx, int32_t enable);
 int gsb_ctx_stage_times(gsb_ctx* ctx, double* ms_out /* 8 */, int64_t* launches_out /* 8 */, int32_t reset);
 /* Number of kernel launches issued by this context so far. */
 int64_t gsb_ctx_launch_count(gsb_ctx* ctx);
+/* CUDA-event interval on the context stream (device time, ms). */
+int gsb_ctx_timer_start(gsb_ctx* ctx);
+int gsb_ctx_timer_stop(gsb_ctx* ctx, double* ms_out);
 
 /* ---- cloud (GaussianCloud, scene.hpp:22-46), stored as FP32 planes on device ---- */
 int gsb_cloud_create(gsb_ctx* ctx, int64_t n, int32_t sh_degree, gsb_cloud** out);
@@ -211,6 +214,23 @@ int gsb_estimate_pose(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* target, const d
                       const double init_pose[12], const gsb_pose_config* cfg, double pose_out[12],
                       double* final_loss, int32_t* steps_used, int32_t* converged,
                       double* trace_pose, double* trace_loss);
+
+/* ---- pose session: one view's pose_descent state kept on the device ----
+ * A session holds the view's target, pose, PoseAdam and best-loss pose; each
+ * gsb_session_step runs `iterations` pose_descent iterations (render ->
+ * rgb_loss -> render_backward(pose only) -> pose_step) without copying any
+ * image to the host. Sessions of one context share its scratch forward state.
+ * gsb_estimate_pose == create + step(budget) + read + destroy. */
+typedef struct gsb_session gsb_session;
+int gsb_session_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* target, const double intr[4],
+                       const double init_pose[12], const gsb_pose_config* cfg, gsb_session** out);
+int gsb_session_destroy(gsb_session* s);
+int gsb_session_step(gsb_ctx* ctx, gsb_session* s, int32_t iterations);
+/* current pose, best pose, best loss, steps used, converged, stopped (any may be NULL) */
+int gsb_session_read(gsb_session* s, double pose[12], double best_pose[12], double* final_loss,
+                     int32_t* steps_used, int32_t* converged, int32_t* stopped);
+/* Forward-state sizes of the session's last iteration (V, K) for work accounting. */
+int gsb_session_frame_info(gsb_session* s, gsb_frame_info* info);
 
 #ifdef __cplusplus
 }

@@ -1034,6 +1034,42 @@ int orc_render_backward(const orc_cloud* cloud, const orc_camera* cam, const orc
   return 0;
 }
 
+void orc_count_work(const orc_render_out* out, const double* d_image, int64_t counts[4]) {
+  const double cutoff2 = out->config.cutoff_sigma * out->config.cutoff_sigma;
+  const int tile = out->config.tile_size;
+  int64_t hf = 0, cf = 0, hb = 0, cb = 0;
+#pragma omp parallel for schedule(dynamic, 4) reduction(+ : hf, cf, hb, cb)
+  for (int y = 0; y < out->height; ++y) {
+    for (int x = 0; x < out->width; ++x) {
+      const size_t pix = (size_t)y * out->width + x;
+      const int t = (y / tile) * out->tiles_x + x / tile;
+      const int32_t lb = out->tile_ranges[2 * t];
+      int bwd = 0;
+      if (d_image) {
+        const uint8_t of = out->overflow_mask[pix];
+        for (int c = 0; c < 3; ++c)
+          if (!(of & (1u << c)) && d_image[pix * 3 + c] != 0.0) bwd = 1;
+      }
+      for (int32_t j = 0; j < out->contrib_count[pix]; ++j) {
+        const orc_splat* rec = &out->splats[out->tile_lists[lb + j]];
+        double d0 = x - rec->mu2d[0], d1 = y - rec->mu2d[1];
+        double c0 = rec->conic[0] * d0 + rec->conic[1] * d1, c1 = rec->conic[2] * d0 + rec->conic[3] * d1;
+        const int hit = !(d0 * c0 + d1 * c1 > cutoff2);
+        hf += hit;
+        cf += !hit;
+        if (bwd) {
+          hb += hit;
+          cb += !hit;
+        }
+      }
+    }
+  }
+  counts[0] = hf;
+  counts[1] = cf;
+  counts[2] = hb;
+  counts[3] = cb;
+}
+
 /* ---------------------------------------------------------------- losses */
 #define KWIN 11
 #define KHALF 5

@@ -197,6 +197,12 @@ double orc_gradcheck(const orc_cloud* cloud, const orc_camera* cam, const double
                      const orc_raster_config* cfg, orc_rng* rng, double step, int32_t* checked,
                      char* worst_label /* >= 32 bytes */);
 
+/* Work counts for the roofline: forward (pixel, entry) pairs with
+ * e < contrib_count that pass (H_f) / fail (C_f) the g <= cutoff^2 test, and
+ * the same over pixels with a non-zero (unclamped) upstream gradient (H_b,
+ * C_b). d_image may be NULL (then H_b = C_b = 0). */
+void orc_count_work(const orc_render_out* out, const double* d_image, int64_t counts[4]);
+
 /* helpers for ctypes users */
 void orc_cloud_alloc(orc_cloud* c, int64_t n, int32_t sh_degree);
 void orc_cloud_free(orc_cloud* c);

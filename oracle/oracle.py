@@ -139,6 +139,7 @@ def lib():
             "orc_cloud_alloc": (None, [P(Cloud), i64, i32]),
             "orc_cloud_free": (None, [P(Cloud)]),
             "orc_num_threads": (C.c_int, []),
+            "orc_count_work": (None, [P(RenderOut), vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -527,6 +528,15 @@ def gradcheck(cloud: HostCloud, cam: Camera, bg, rng: Rng, cfg=None, step=1e-5):
     err = lib().orc_gradcheck(cloud.c().ref(), C.byref(cam), _p(bgv), C.byref(cfg), C.byref(rng), step,
                               C.byref(checked), label)
     return err, checked.value, label.value.decode()
+
+
+def count_work(rr: RenderResult, d_image=None):
+    """(H_f, C_f, H_b, C_b) for the roofline's algorithmic FLOPs."""
+    assert rr._ptr is not None, "render(..., keep_handle=True) required"
+    out = np.zeros(4, np.int64)
+    d = None if d_image is None else np.ascontiguousarray(d_image, np.float64)
+    lib().orc_count_work(rr._ptr, _p(d) if d is not None else None, _p(out))
+    return tuple(int(v) for v in out)
 
 
 def num_threads() -> int:

@@ -136,6 +136,8 @@ struct StageScope {
 };
 
 // --------------------------------------------------------------- helpers
+static int cuda_fail_or_ok(cudaError_t e) { return e == cudaSuccess ? GSB_OK : cuda_fail(e, "cudaMemcpy"); }
+
 static int ensure_device(gsb_ctx* ctx) {
   if (!ctx) return fail(GSB_ERR_INVALID_ARGUMENT, "null context");
   cudaError_t e = cudaSetDevice(ctx->device);
@@ -504,6 +506,9 @@ int gsb_ctx_destroy(gsb_ctx* ctx) {
   ctx->scratch_small.release();
   if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
   delete ctx->timer;
+  if (ctx->work) gsb_frame_destroy(ctx->work);
+  if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
+  if (ctx->ev_stop) cudaEventDestroy(ctx->ev_stop);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
   return GSB_OK;
@@ -1057,76 +1062,188 @@ int gsb_cloud_adam_step(gsb_ctx* ctx, gsb_cloud* cloud, gsb_grads* grads, gsb_ad
   return GSB_OK;
 }
 
-// ------------------------------------------------------- estimate_pose
-int gsb_estimate_pose(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* target, const double intr[4],
-                      const double init_pose[12], const gsb_pose_config* cfg, double pose_out[12], double* final_loss,
-                      int32_t* steps_used, int32_t* converged, double* trace_pose, double* trace_loss) {
+// ------------------------------------------------------------ timer API
+int gsb_ctx_timer_start(gsb_ctx* ctx) {
   if (int r = ensure_device(ctx)) return r;
-  if (!cloud || !target || !intr || !init_pose || !cfg || !pose_out)
-    return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  if (!ctx->ev_start) GSB_CUDA(cudaEventCreate(&ctx->ev_start));
+  if (!ctx->ev_stop) GSB_CUDA(cudaEventCreate(&ctx->ev_stop));
+  GSB_CUDA(cudaEventRecord(ctx->ev_start, ctx->stream));
+  return GSB_OK;
+}
+
+int gsb_ctx_timer_stop(gsb_ctx* ctx, double* ms) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!ctx->ev_start || !ctx->ev_stop) return fail(GSB_ERR_INVALID_ARGUMENT, "timer not started");
+  GSB_CUDA(cudaEventRecord(ctx->ev_stop, ctx->stream));
+  GSB_CUDA(cudaEventSynchronize(ctx->ev_stop));
+  float t = 0.f;
+  GSB_CUDA(cudaEventElapsedTime(&t, ctx->ev_start, ctx->ev_stop));
+  if (ms) *ms = t;
+  return GSB_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ sessions
+struct gsb_session {
+  gsb_ctx* ctx = nullptr;
+  gsb_cloud* cloud = nullptr;
+  gsb_image* target = nullptr;
+  gsb_camera cam{};
+  gsb_pose_config cfg{};
+  DevBuf state;   // PoseState
+  DevBuf camdev;  // CamDev of the current pose
+  DevBuf trace;   // pose (12) + loss (1) per iteration
+  void* host_state = nullptr;
+  int64_t n_splats = 0, n_entries = 0;
+  int32_t stopped = 0;
+};
+
+extern "C" {
+
+int gsb_session_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* target, const double intr[4],
+                       const double init_pose[12], const gsb_pose_config* cfg, gsb_session** out) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!cloud || !target || !intr || !init_pose || !cfg || !out) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
   if (int r = validate_config(&cfg->raster)) return r;
   if (cfg->budget <= 0) return fail(GSB_ERR_INVALID_CONFIG, "budget must be > 0");
-  static thread_local gsb_frame* fr = nullptr;
-  if (!fr || fr->ctx != ctx) {
-    fr = new gsb_frame();
-    fr->ctx = ctx;
-  }
-  gsb_frame* f = fr;
-  gsb_camera cam;
-  cam.fx = intr[0];
-  cam.fy = intr[1];
-  cam.cx = intr[2];
-  cam.cy = intr[3];
-  cam.width = target->width;
-  cam.height = target->height;
+  gsb_session* s = new gsb_session();
+  s->ctx = ctx;
+  s->cloud = cloud;
+  s->target = target;
+  s->cfg = *cfg;
+  s->cam.fx = intr[0];
+  s->cam.fy = intr[1];
+  s->cam.cx = intr[2];
+  s->cam.cy = intr[3];
+  s->cam.width = target->width;
+  s->cam.height = target->height;
   for (int r = 0; r < 3; ++r) {
-    for (int c = 0; c < 3; ++c) cam.R[r * 3 + c] = init_pose[r * 4 + c];
-    cam.t[r] = init_pose[r * 4 + 3];
+    for (int c = 0; c < 3; ++c) s->cam.R[r * 3 + c] = init_pose[r * 4 + c];
+    s->cam.t[r] = init_pose[r * 4 + 3];
   }
-  if (int r = frame_setup(ctx, f, cloud, &cam, cfg->background, &cfg->raster)) return r;
-  const RasterDev rc = make_rasterdev(&cfg->raster);
-  // device pose state + traces
   const size_t sb = pose_state_bytes();
-  static thread_local DevBuf dstate, dtrace;
-  GSB_RESERVE(dstate, sb + 64);
-  GSB_RESERVE(dtrace, sizeof(double) * 13 * (size_t)cfg->budget + 64);
-  char* h = static_cast<char*>(pinned(ctx, sb + 64));
-  if (!h) return fail(GSB_ERR_OUT_OF_MEMORY, "pinned staging");
+  cudaError_t e = s->state.reserve(sb);
+  if (e == cudaSuccess) e = s->camdev.reserve(sizeof(CamDev));
+  if (e == cudaSuccess) e = s->trace.reserve(sizeof(double) * 13 * (size_t)cfg->budget);
+  if (e == cudaSuccess) e = cudaMallocHost(&s->host_state, sb);
+  if (e != cudaSuccess) {
+    gsb_session_destroy(s);
+    return cuda_fail(e, "session alloc");
+  }
+  pose_state_init(s->host_state, init_pose);
+  CamDev cd = make_camdev(&s->cam, kTile);
+  CamDev* h = static_cast<CamDev*>(pinned(ctx, sizeof(CamDev)));
+  if (!h) {
+    gsb_session_destroy(s);
+    return fail(GSB_ERR_OUT_OF_MEMORY, "pinned staging");
+  }
   GSB_CUDA(cudaStreamSynchronize(ctx->stream));
-  pose_state_init(h, init_pose);
-  GSB_CUDA(cudaMemcpyAsync(dstate.p, h, sb, cudaMemcpyHostToDevice, ctx->stream));
-  double* tp = dtrace.as<double>();
-  double* tl = tp + 12 * (size_t)cfg->budget;
-  int32_t stop = 0;
-  for (int it = 0; it < cfg->budget && !stop; ++it) {
-    if (int r = render_device(ctx, cloud, f, rc)) return r;
+  *h = cd;
+  GSB_CUDA(cudaMemcpyAsync(s->camdev.p, h, sizeof(CamDev), cudaMemcpyHostToDevice, ctx->stream));
+  GSB_CUDA(cudaMemcpyAsync(s->state.p, s->host_state, sb, cudaMemcpyHostToDevice, ctx->stream));
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  *out = s;
+  return GSB_OK;
+}
+
+int gsb_session_destroy(gsb_session* s) {
+  if (!s) return GSB_OK;
+  cudaSetDevice(s->ctx->device);
+  cudaStreamSynchronize(s->ctx->stream);
+  s->state.release();
+  s->camdev.release();
+  s->trace.release();
+  if (s->host_state) cudaFreeHost(s->host_state);
+  delete s;
+  return GSB_OK;
+}
+
+int gsb_session_step(gsb_ctx* ctx, gsb_session* s, int32_t iterations) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!s || s->ctx != ctx) return fail(GSB_ERR_INVALID_ARGUMENT, "session / context mismatch");
+  if (!ctx->work) {
+    ctx->work = new gsb_frame();
+    ctx->work->ctx = ctx;
+  }
+  gsb_frame* f = ctx->work;
+  const gsb_pose_config& cfg = s->cfg;
+  if (int r = frame_setup(ctx, f, s->cloud, &s->cam, cfg.background, &cfg.raster)) return r;
+  const RasterDev rc = make_rasterdev(&cfg.raster);
+  const size_t sb = pose_state_bytes();
+  double* tp = s->trace.as<double>();
+  double* tl = tp + 12 * (size_t)cfg.budget;
+  for (int it = 0; it < iterations && !s->stopped; ++it) {
+    GSB_CUDA(cudaMemcpyAsync(f->cam.p, s->camdev.p, sizeof(CamDev), cudaMemcpyDeviceToDevice, ctx->stream));
+    if (int r = render_device(ctx, s->cloud, f, rc)) return r;
     f->valid = true;
-    if (int r = loss_device(ctx, f, target->planes.as<float>(), cfg->beta, true)) return r;
-    if (int r = backward_device(ctx, cloud, f, false, nullptr)) return r;
+    if (int r = loss_device(ctx, f, s->target->planes.as<float>(), cfg.beta, true)) return r;
+    if (int r = backward_device(ctx, s->cloud, f, false, nullptr)) return r;
     {
       StageScope sc(ctx, kStOptim);
-      if (int r = launch_pose_iter(ctx->stream, dstate.p, f->d_pose.as<double>(), f->loss_val.as<double>(),
-                                   cfg->cam_lr_start, cfg->cam_lr_end, cfg->pose_converged_eps, cfg->budget,
-                                   f->cam.as<CamDev>(), tp, tl))
+      if (int r = launch_pose_iter(ctx->stream, s->state.p, f->d_pose.as<double>(), f->loss_val.as<double>(),
+                                   cfg.cam_lr_start, cfg.cam_lr_end, cfg.pose_converged_eps, cfg.budget,
+                                   s->camdev.as<CamDev>(), tp, tl))
         return r;
       ctx->launches += 1;
     }
-    GSB_CUDA(cudaMemcpyAsync(h, dstate.p, sb, cudaMemcpyDeviceToHost, ctx->stream));
+    GSB_CUDA(cudaMemcpyAsync(s->host_state, s->state.p, sb, cudaMemcpyDeviceToHost, ctx->stream));
     GSB_CUDA(cudaStreamSynchronize(ctx->stream));
-    pose_state_read(h, nullptr, nullptr, nullptr, nullptr, nullptr, &stop, nullptr, nullptr, nullptr, nullptr);
+    pose_state_read(s->host_state, nullptr, nullptr, nullptr, nullptr, nullptr, &s->stopped, nullptr, nullptr,
+                    nullptr, nullptr);
+    s->n_splats = f->n_splats;
+    s->n_entries = f->n_entries;
   }
-  int32_t su = 0, cv = 0;
-  double fl = 0.0;
-  pose_state_read(h, pose_out, nullptr, &fl, &su, &cv, nullptr, nullptr, nullptr, nullptr, nullptr);
-  if (final_loss) *final_loss = fl;
-  if (steps_used) *steps_used = su;
-  if (converged) *converged = cv;
-  if (trace_pose && su > 0)
-    GSB_CUDA(cudaMemcpyAsync(trace_pose, tp, sizeof(double) * 12 * su, cudaMemcpyDeviceToHost, ctx->stream));
-  if (trace_loss && su > 0)
-    GSB_CUDA(cudaMemcpyAsync(trace_loss, tl, sizeof(double) * su, cudaMemcpyDeviceToHost, ctx->stream));
-  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  f->valid = false;  // the scratch frame no longer matches any caller-visible camera
   return GSB_OK;
+}
+
+int gsb_session_read(gsb_session* s, double pose[12], double best_pose[12], double* final_loss, int32_t* steps_used,
+                     int32_t* converged, int32_t* stopped) {
+  if (!s) return fail(GSB_ERR_INVALID_ARGUMENT, "null session");
+  gsb_ctx* ctx = s->ctx;
+  if (int r = ensure_device(ctx)) return r;
+  GSB_CUDA(cudaMemcpyAsync(s->host_state, s->state.p, pose_state_bytes(), cudaMemcpyDeviceToHost, ctx->stream));
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  pose_state_read(s->host_state, best_pose, pose, final_loss, steps_used, converged, stopped, nullptr, nullptr,
+                  nullptr, nullptr);
+  return GSB_OK;
+}
+
+int gsb_session_frame_info(gsb_session* s, gsb_frame_info* info) {
+  if (!s || !info) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  std::memset(info, 0, sizeof *info);
+  info->n_gaussians = s->cloud->n;
+  info->n_splats = s->n_splats;
+  info->n_entries = s->n_entries;
+  info->width = s->cam.width;
+  info->height = s->cam.height;
+  info->tiles_x = (s->cam.width + kTile - 1) / kTile;
+  info->tiles_y = (s->cam.height + kTile - 1) / kTile;
+  return GSB_OK;
+}
+
+// pipelines.cpp:218-222 -> pose_descent (58-92), device resident.
+int gsb_estimate_pose(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* target, const double intr[4],
+                      const double init_pose[12], const gsb_pose_config* cfg, double pose_out[12], double* final_loss,
+                      int32_t* steps_used, int32_t* converged, double* trace_pose, double* trace_loss) {
+  if (!pose_out) return fail(GSB_ERR_INVALID_ARGUMENT, "null pose_out");
+  gsb_session* s = nullptr;
+  if (int r = gsb_session_create(ctx, cloud, target, intr, init_pose, cfg, &s)) return r;
+  int r = gsb_session_step(ctx, s, cfg->budget);
+  int32_t su = 0;
+  if (!r) r = gsb_session_read(s, nullptr, pose_out, final_loss, &su, converged, nullptr);
+  if (!r && steps_used) *steps_used = su;
+  if (!r && su > 0 && (trace_pose || trace_loss)) {
+    const double* tp = s->trace.as<double>();
+    if (trace_pose)
+      r = cuda_fail_or_ok(cudaMemcpy(trace_pose, tp, sizeof(double) * 12 * su, cudaMemcpyDeviceToHost));
+    if (!r && trace_loss)
+      r = cuda_fail_or_ok(cudaMemcpy(trace_loss, tp + 12 * (size_t)cfg->budget, sizeof(double) * su,
+                                     cudaMemcpyDeviceToHost));
+  }
+  gsb_session_destroy(s);
+  return r;
 }
 
 }  // extern "C"

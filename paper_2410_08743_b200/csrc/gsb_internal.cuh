@@ -123,6 +123,8 @@ struct gsb_ctx {
   int64_t launches = 0;
   bool profiling = false;
   gsb::StageTimer* timer = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+  gsb_frame* work = nullptr;   // scratch forward state shared by sessions
 };
 
 struct gsb_cloud {

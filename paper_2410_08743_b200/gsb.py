@@ -157,6 +157,13 @@ def _sigs():
         "gsb_adam_destroy": (C.c_int, [_vp]),
         "gsb_cloud_adam_step": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
         "gsb_estimate_pose": (C.c_int, [_vp, _vp, _vp, _vp, _vp, P(PoseConfig), _vp, P(d), P(i32), P(i32), _vp, _vp]),
+        "gsb_ctx_timer_start": (C.c_int, [_vp]),
+        "gsb_ctx_timer_stop": (C.c_int, [_vp, P(d)]),
+        "gsb_session_create": (C.c_int, [_vp, _vp, _vp, _vp, _vp, P(PoseConfig), P(_vp)]),
+        "gsb_session_destroy": (C.c_int, [_vp]),
+        "gsb_session_step": (C.c_int, [_vp, _vp, i32]),
+        "gsb_session_read": (C.c_int, [_vp, _vp, _vp, P(d), P(i32), P(i32), P(i32)]),
+        "gsb_session_frame_info": (C.c_int, [_vp, P(FrameInfo)]),
     }
 
 
@@ -223,6 +230,14 @@ class Context:
 
     def launch_count(self) -> int:
         return int(lib().gsb_ctx_launch_count(self.h))
+
+    def timer_start(self):
+        _check(lib().gsb_ctx_timer_start(self.h))
+
+    def timer_stop(self) -> float:
+        ms = C.c_double()
+        _check(lib().gsb_ctx_timer_stop(self.h, C.byref(ms)))
+        return ms.value
 
 
 class Cloud:
@@ -427,6 +442,41 @@ def estimate_pose(ctx: Context, cloud: Cloud, target: Image, intr, init_pose12, 
     if trace:
         res.update(trace_pose=tp[:su.value], trace_loss=tl[:su.value])
     return res
+
+
+class PoseSession:
+    """One view's device-resident pose_descent state (gsb_session)."""
+
+    def __init__(self, ctx: Context, cloud: Cloud, target: Image, intr, init_pose12, config: PoseConfig | None = None):
+        self.cfg = config or PoseConfig.default()
+        intr = np.ascontiguousarray(intr, np.float64)
+        init = np.ascontiguousarray(init_pose12, np.float64).reshape(12)
+        h = _vp()
+        _check(lib().gsb_session_create(ctx.h, cloud.h, target.h, _p(intr), _p(init), C.byref(self.cfg), C.byref(h)))
+        self.h, self.ctx, self._keep = h, ctx, (cloud, target)
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().gsb_session_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def step(self, iterations: int = 1):
+        _check(lib().gsb_session_step(self.ctx.h, self.h, iterations))
+
+    def read(self) -> dict:
+        pose, best = np.zeros(12), np.zeros(12)
+        fl, su, cv, st = C.c_double(), C.c_int32(), C.c_int32(), C.c_int32()
+        _check(lib().gsb_session_read(self.h, _p(pose), _p(best), C.byref(fl), C.byref(su), C.byref(cv), C.byref(st)))
+        return dict(pose=pose, best_pose=best, final_loss=fl.value, steps=su.value, converged=bool(cv.value),
+                    stopped=bool(st.value))
+
+    def frame_info(self) -> FrameInfo:
+        fi = FrameInfo()
+        _check(lib().gsb_session_frame_info(self.h, C.byref(fi)))
+        return fi
 
 
 def synth_poses(seed: int, n: int, sh_degree: int, kind: int, cameras: int, orbit_radius=2.5,
