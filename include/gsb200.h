@@ -226,6 +226,12 @@ int gsb_session_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* target, const 
                        const double init_pose[12], const gsb_pose_config* cfg, gsb_session** out);
 int gsb_session_destroy(gsb_session* s);
 int gsb_session_step(gsb_ctx* ctx, gsb_session* s, int32_t iterations);
+/* Enqueue iterations without waiting (the next gsb_session_step / _read
+ * synchronises; early exits are then honoured on the device). */
+int gsb_session_step_async(gsb_ctx* ctx, gsb_session* s, int32_t iterations);
+/* Per-stage device time (ms, 8 stages as gsb_ctx_stage_times) of the session's
+ * last iteration, recorded by events inside its CUDA graph while profiling. */
+int gsb_session_stage_times(gsb_session* s, double* ms_out);
 /* current pose, best pose, best loss, steps used, converged, stopped (any may be NULL) */
 int gsb_session_read(gsb_session* s, double pose[12], double best_pose[12], double* final_loss,
                      int32_t* steps_used, int32_t* converged, int32_t* stopped);

@@ -18,22 +18,23 @@ namespace gsb {
 
 // kernels (k_*.cu)
 int launch_preprocess(cudaStream_t st, const gsb_cloud* cloud, const CamDev* cam, const RasterDev& rc, gsb_frame* f);
-int scan_exclusive(cudaStream_t st, const uint32_t* in, int64_t n, bool flag, uint32_t* out, uint32_t* scratch,
-                   uint32_t* total, int64_t* launches);
+int scan_exclusive(cudaStream_t st, const uint32_t* in, int64_t cap, const uint32_t* n_dev, bool flag, uint32_t* out,
+                   uint32_t* scratch, uint32_t* total, int64_t* launches);
 size_t scan_words(int64_t n);
-int radix_sort_pairs(cudaStream_t st, uint32_t* keys[2], uint32_t* vals[2], int64_t n, int total_bits,
-                     uint32_t* hist, int* result_sel, int64_t* launches);
+int radix_sort_pairs(cudaStream_t st, uint32_t* keys[2], uint32_t* vals[2], int64_t cap, const uint32_t* n_dev,
+                     int total_bits, uint32_t* hist, int* result_sel, int64_t* launches);
 size_t radix_hist_words(int64_t n, int total_bits);
 int launch_compact(cudaStream_t st, const uint32_t* cnt_g, const uint32_t* vis_pos, const double* depth_g, int64_t n,
                    uint32_t* vis_idx, uint32_t* dkey, uint32_t* dval);
 int launch_depth_tie_fix(cudaStream_t st, const uint32_t* key, uint32_t* val, const uint32_t* vis_idx,
-                         const double* depth_g, int64_t nv);
+                         const double* depth_g, int64_t cap, const uint32_t* nv_dev);
 int launch_gather_ranks(cudaStream_t st, const uint32_t* sorted_v, const uint32_t* vis_idx, const SplatRec* rec_g,
-                        const uint2* rect_g, const uint32_t* cnt_g, int64_t nv, SplatRec* rec, SplatAux* aux,
-                        uint32_t* cnt_r, int32_t* rank_of_g);
-int launch_duplicate(cudaStream_t st, const uint32_t* offs, SplatAux* aux, int64_t nv, int tiles_x, uint32_t* ekey,
-                     uint32_t* eval);
-int launch_tile_ranges(cudaStream_t st, const uint32_t* ekey, int64_t k, int n_tiles, uint2* ranges);
+                        const uint2* rect_g, const uint32_t* cnt_g, int64_t cap, const uint32_t* nv_dev, SplatRec* rec,
+                        SplatAux* aux, uint32_t* cnt_r, int32_t* rank_of_g);
+int launch_duplicate(cudaStream_t st, const uint32_t* offs, SplatAux* aux, int64_t cap, const uint32_t* nv_dev,
+                     int tiles_x, int64_t k_cap, uint32_t* ekey, uint32_t* eval, uint32_t* off_g);
+int launch_tile_ranges(cudaStream_t st, const uint32_t* ekey, int64_t k_cap, const uint32_t* k_dev, int n_tiles,
+                       uint2* ranges);
 int launch_composite(cudaStream_t st, gsb_frame* f, const RasterDev& rc);
 int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc);
 int launch_backward_geom(cudaStream_t st, const gsb_cloud* cloud, gsb_frame* f, const RasterDev& rc, bool full,
@@ -41,8 +42,11 @@ int launch_backward_geom(cudaStream_t st, const gsb_cloud* cloud, gsb_frame* f, 
 int launch_rgb_loss(cudaStream_t st, const float* ren, const float* tgt, int W, int H, double beta, float* gmaps,
                     double* block_sums, double* out3, float* d_image, int64_t* launches);
 size_t loss_block_count(int W, int H);
+int init_loss_constants();
 int launch_pose_iter(cudaStream_t st, void* state, const double* dpose, const double* loss3, double lr_start,
-                     double lr_end, double eps, int budget, CamDev* cam, double* trace_pose, double* trace_loss);
+                     double lr_end, double eps, int budget, CamDev* cam, double* trace_pose, double* trace_loss,
+                     const uint32_t* k_dev, int64_t k_cap);
+int32_t pose_state_take_aborted(void* host_state);
 size_t pose_state_bytes();
 int pose_state_init(void* host_state, const double pose[12]);
 void pose_state_read(const void* host_state, double best_pose[12], double cur_pose[12], double* final_loss,
@@ -122,16 +126,23 @@ struct StageTimer {
   }
 };
 
+// Brackets a stage's launches with CUDA events on the context stream: into
+// the context's event pool (eager launches) or, while a session graph is
+// being captured with profiling on, into that session's per-stage events.
 struct StageScope {
   gsb_ctx* ctx;
-  StageScope(gsb_ctx* c, int stage) : ctx(c) {
-    if (ctx->profiling && ctx->timer) {
+  int stage;
+  StageScope(gsb_ctx* c, int s) : ctx(c), stage(s) {
+    if (ctx->stage_events) {
+      cudaEventRecordWithFlags(ctx->stage_events[stage][0], ctx->stream, cudaEventRecordExternal);
+    } else if (ctx->profiling && ctx->timer) {
       if (ctx->timer->used > 4096) ctx->timer->collect();
       ctx->timer->begin(ctx->stream, stage);
     }
   }
   ~StageScope() {
-    if (ctx->profiling && ctx->timer) ctx->timer->end(ctx->stream);
+    if (ctx->stage_events) cudaEventRecordWithFlags(ctx->stage_events[stage][1], ctx->stream, cudaEventRecordExternal);
+    else if (ctx->profiling && ctx->timer) ctx->timer->end(ctx->stream);
   }
 };
 
@@ -243,119 +254,147 @@ static int read_counters(gsb_ctx* ctx, const uint32_t* dev, uint32_t* host, int 
   return GSB_OK;
 }
 
-// The full forward pass on the device; camera already in f->cam.
-static int render_device(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, const RasterDev& rc) {
+static int tile_bits(int n_tiles) {
+  int bits = 0;
+  while ((1 << bits) < n_tiles) ++bits;
+  return bits;
+}
+
+// Sizes every forward/backward buffer of the frame for (cloud, image size,
+// entry capacity). Any reallocation bumps f->gen (captured graphs hold raw
+// pointers and must be rebuilt).
+static int frame_reserve(gsb_frame* f, const gsb_cloud* cloud, int64_t k_cap) {
+  const int64_t n = std::max<int64_t>(cloud->n, 1);
+  const int64_t np = std::max<int64_t>(cloud->n_pad, 1);
+  const int n_tiles = std::max(f->tiles_x * f->tiles_y, 1);
+  const int64_t npix = std::max<int64_t>((int64_t)f->width * f->height, 1);
+  k_cap = std::max<int64_t>(k_cap, 1024);
+  bool grew = false;
+  GSB_CUDA(f->cam.reserve(sizeof(CamDev), &grew));
+  GSB_CUDA(f->counters.reserve(64, &grew));
+  GSB_CUDA(f->rec_g.reserve(sizeof(SplatRec) * n, &grew));
+  GSB_CUDA(f->rect_g.reserve(sizeof(uint2) * n, &grew));
+  GSB_CUDA(f->cnt_g.reserve(sizeof(uint32_t) * n, &grew));
+  GSB_CUDA(f->depth_g.reserve(sizeof(double) * n, &grew));
+  GSB_CUDA(f->radius_g.reserve(sizeof(double) * n, &grew));
+  GSB_CUDA(f->rank_of_g.reserve(sizeof(int32_t) * n, &grew));
+  GSB_CUDA(f->colj.reserve(sizeof(float) * 9 * np, &grew));
+  GSB_CUDA(f->off_g.reserve(sizeof(uint32_t) * n, &grew));
+  GSB_CUDA(f->vis_idx.reserve(sizeof(uint32_t) * n, &grew));
+  GSB_CUDA(f->cnt_r.reserve(sizeof(uint32_t) * n, &grew));
+  for (int b = 0; b < 2; ++b) {
+    GSB_CUDA(f->dkey[b].reserve(sizeof(uint32_t) * n, &grew));
+    GSB_CUDA(f->dval[b].reserve(sizeof(uint32_t) * n, &grew));
+    GSB_CUDA(f->ekey[b].reserve(sizeof(uint32_t) * k_cap, &grew));
+    GSB_CUDA(f->eval_[b].reserve(sizeof(uint32_t) * k_cap, &grew));
+  }
+  GSB_CUDA(f->rec.reserve(sizeof(SplatRec) * n, &grew));
+  GSB_CUDA(f->aux.reserve(sizeof(SplatAux) * n, &grew));
+  GSB_CUDA(f->scan_tmp.reserve(sizeof(uint32_t) * (scan_words(n) + 64), &grew));
+  const size_t hist = std::max(radix_hist_words(n, 32), radix_hist_words(k_cap, tile_bits(n_tiles)));
+  GSB_CUDA(f->sort_hist.reserve(sizeof(uint32_t) * hist, &grew));
+  GSB_CUDA(f->ranges.reserve(sizeof(uint2) * n_tiles, &grew));
+  GSB_CUDA(f->image.reserve(sizeof(float) * 3 * npix, &grew));
+  GSB_CUDA(f->final_t.reserve(sizeof(float) * npix, &grew));
+  GSB_CUDA(f->pixstate.reserve(sizeof(uint32_t) * npix, &grew));
+  GSB_CUDA(f->d_image.reserve(sizeof(float) * 3 * npix, &grew));
+  GSB_CUDA(f->gmaps.reserve(sizeof(float) * 9 * npix, &grew));
+  GSB_CUDA(f->loss_blocks.reserve(sizeof(double) * 2 * loss_block_count(f->width, f->height), &grew));
+  GSB_CUDA(f->loss_val.reserve(sizeof(double) * 4, &grew));
+  GSB_CUDA(f->partials.reserve(sizeof(float) * kPartial * k_cap, &grew));
+  GSB_CUDA(f->pose_blocks.reserve(sizeof(double) * 6 * ((n + 255) / 256 + 1), &grew));
+  GSB_CUDA(f->d_pose.reserve(sizeof(double) * 6, &grew));
+  if (grew) ++f->gen;
+  f->k_cap = (int64_t)(f->ekey[0].bytes / sizeof(uint32_t));
+  f->k_cap = std::min<int64_t>(f->k_cap, (int64_t)(f->partials.bytes / (sizeof(float) * kPartial)));
+  return GSB_OK;
+}
+
+// The forward pass as a fixed launch sequence (no host synchronisation; live
+// counts V -> counters[0], K -> counters[1] stay on the device). Camera in f->cam.
+static int render_async(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, const RasterDev& rc) {
   cudaStream_t st = ctx->stream;
   const int64_t n = cloud->n;
   const int n_tiles = f->tiles_x * f->tiles_y;
-  const int64_t npix = (int64_t)f->width * f->height;
-  GSB_RESERVE(f->rec_g, sizeof(SplatRec) * std::max<int64_t>(n, 1));
-  GSB_RESERVE(f->rect_g, sizeof(uint2) * std::max<int64_t>(n, 1));
-  GSB_RESERVE(f->cnt_g, sizeof(uint32_t) * std::max<int64_t>(n, 1));
-  GSB_RESERVE(f->depth_g, sizeof(double) * std::max<int64_t>(n, 1));
-  GSB_RESERVE(f->radius_g, sizeof(double) * std::max<int64_t>(n, 1));
-  GSB_RESERVE(f->rank_of_g, sizeof(int32_t) * std::max<int64_t>(n, 1));
-  GSB_RESERVE(f->vis_idx, sizeof(uint32_t) * std::max<int64_t>(n, 1));  // also scan output scratch
-  GSB_RESERVE(f->scan_tmp, sizeof(uint32_t) * (scan_words(std::max<int64_t>(n, 1)) + 4096));
-  GSB_RESERVE(f->counters, 64);
-  GSB_RESERVE(f->ranges, sizeof(uint2) * std::max(n_tiles, 1));
-  GSB_RESERVE(f->image, sizeof(float) * 3 * std::max<int64_t>(npix, 1));
-  GSB_RESERVE(f->final_t, sizeof(float) * std::max<int64_t>(npix, 1));
-  GSB_RESERVE(f->pixstate, sizeof(uint32_t) * std::max<int64_t>(npix, 1));
   uint32_t* counters = f->counters.as<uint32_t>();
-  uint32_t host_cnt[2] = {0, 0};
   {
     StageScope sc(ctx, kStPreprocess);
-    int rc1 = launch_preprocess(st, cloud, f->cam.as<CamDev>(), rc, f);
-    if (rc1) return rc1;
+    if (int r = launch_preprocess(st, cloud, f->cam.as<CamDev>(), rc, f)) return r;
     ctx->launches += n > 0 ? 1 : 0;
   }
-  int64_t nv = 0, k = 0;
   {
     StageScope sc(ctx, kStSort);
-    // 1. compaction (index order); cnt_r holds the scan output until step 3
-    GSB_RESERVE(f->cnt_r, sizeof(uint32_t) * std::max<int64_t>(n, 1));
-    uint32_t* pos = f->cnt_r.as<uint32_t>();
-    int r = scan_exclusive(st, f->cnt_g.as<uint32_t>(), n, true, pos, f->scan_tmp.as<uint32_t>(), counters,
-                           &ctx->launches);
-    if (r) return r;
-  }
-  if (int rr = read_counters(ctx, counters, host_cnt, 1)) return rr;
-  nv = host_cnt[0];
-  f->n_splats = nv;
-  {
-    StageScope sc(ctx, kStSort);
-    GSB_RESERVE(f->dkey[0], sizeof(uint32_t) * std::max<int64_t>(nv, 1));
-    GSB_RESERVE(f->dkey[1], sizeof(uint32_t) * std::max<int64_t>(nv, 1));
-    GSB_RESERVE(f->dval[0], sizeof(uint32_t) * std::max<int64_t>(nv, 1));
-    GSB_RESERVE(f->dval[1], sizeof(uint32_t) * std::max<int64_t>(nv, 1));
-    GSB_RESERVE(f->rec, sizeof(SplatRec) * std::max<int64_t>(nv, 1));
-    GSB_RESERVE(f->aux, sizeof(SplatAux) * std::max<int64_t>(nv, 1));
-    int r = launch_compact(st, f->cnt_g.as<uint32_t>(), f->cnt_r.as<uint32_t>(), f->depth_g.as<double>(), n,
-                           f->vis_idx.as<uint32_t>(), f->dkey[0].as<uint32_t>(), f->dval[0].as<uint32_t>());
-    if (r) return r;
-    ctx->launches += 1;
-    // 2. stable depth sort (FP32 bits) + FP64 tie fix
-    GSB_RESERVE(f->sort_hist, sizeof(uint32_t) * radix_hist_words(std::max<int64_t>(nv, 1), 32));
+    // 1. compaction in index order (visible slot of Gaussian i -> cnt_r[i])
+    if (int r = scan_exclusive(st, f->cnt_g.as<uint32_t>(), n, nullptr, true, f->cnt_r.as<uint32_t>(),
+                               f->scan_tmp.as<uint32_t>(), counters + 0, &ctx->launches))
+      return r;
+    if (int r = launch_compact(st, f->cnt_g.as<uint32_t>(), f->cnt_r.as<uint32_t>(), f->depth_g.as<double>(), n,
+                               f->vis_idx.as<uint32_t>(), f->dkey[0].as<uint32_t>(), f->dval[0].as<uint32_t>()))
+      return r;
+    ctx->launches += n > 0 ? 1 : 0;
+    // 2. stable depth sort (FP32 bits, 4 passes) + FP64 tie fix
     uint32_t* dk[2] = {f->dkey[0].as<uint32_t>(), f->dkey[1].as<uint32_t>()};
     uint32_t* dv[2] = {f->dval[0].as<uint32_t>(), f->dval[1].as<uint32_t>()};
     int sel = 0;
-    r = radix_sort_pairs(st, dk, dv, nv, 32, f->sort_hist.as<uint32_t>(), &sel, &ctx->launches);
-    if (r) return r;
-    r = launch_depth_tie_fix(st, dk[sel], dv[sel], f->vis_idx.as<uint32_t>(), f->depth_g.as<double>(), nv);
-    if (r) return r;
-    ctx->launches += nv > 1 ? 1 : 0;
-    // 3. rank-order records, entry counts -> offsets
-    r = launch_gather_ranks(st, dv[sel], f->vis_idx.as<uint32_t>(), f->rec_g.as<SplatRec>(), f->rect_g.as<uint2>(),
-                            f->cnt_g.as<uint32_t>(), nv, f->rec.as<SplatRec>(), f->aux.as<SplatAux>(),
-                            f->cnt_r.as<uint32_t>(), f->rank_of_g.as<int32_t>());
-    if (r) return r;
-    ctx->launches += nv > 0 ? 1 : 0;
-    GSB_RESERVE(f->scan_tmp, sizeof(uint32_t) * (scan_words(std::max<int64_t>(nv, 1)) + 4096));
-    r = scan_exclusive(st, f->cnt_r.as<uint32_t>(), nv, false, dk[sel ^ 1], f->scan_tmp.as<uint32_t>(), counters + 1,
-                       &ctx->launches);
-    if (r) return r;
-    f->sorted_sel = sel;  // remember where offsets live: dk[sel^1]
-  }
-  if (int rr = read_counters(ctx, counters + 1, host_cnt + 1, 1)) return rr;
-  k = host_cnt[1];
-  f->n_entries = k;
-  {
-    StageScope sc(ctx, kStSort);
-    const int dsel = f->sorted_sel;
-    uint32_t* offs = (dsel ^ 1) ? f->dkey[1].as<uint32_t>() : f->dkey[0].as<uint32_t>();
-    GSB_RESERVE(f->ekey[0], sizeof(uint32_t) * std::max<int64_t>(k, 1));
-    GSB_RESERVE(f->ekey[1], sizeof(uint32_t) * std::max<int64_t>(k, 1));
-    GSB_RESERVE(f->eval_[0], sizeof(uint32_t) * std::max<int64_t>(k, 1));
-    GSB_RESERVE(f->eval_[1], sizeof(uint32_t) * std::max<int64_t>(k, 1));
-    int r = launch_duplicate(st, offs, f->aux.as<SplatAux>(), nv, f->tiles_x, f->ekey[0].as<uint32_t>(),
-                             f->eval_[0].as<uint32_t>());
-    if (r) return r;
-    ctx->launches += nv > 0 ? 1 : 0;
-    int bits = 0;
-    while ((1 << bits) < n_tiles) ++bits;
-    GSB_RESERVE(f->sort_hist, sizeof(uint32_t) * radix_hist_words(std::max<int64_t>(k, 1), bits));
+    if (int r = radix_sort_pairs(st, dk, dv, n, counters + 0, 32, f->sort_hist.as<uint32_t>(), &sel, &ctx->launches))
+      return r;
+    if (int r = launch_depth_tie_fix(st, dk[sel], dv[sel], f->vis_idx.as<uint32_t>(), f->depth_g.as<double>(), n,
+                                     counters + 0))
+      return r;
+    ctx->launches += n > 1 ? 1 : 0;
+    // 3. rank-order records; entry counts -> rank-major offsets (into dk[sel^1])
+    if (int r = launch_gather_ranks(st, dv[sel], f->vis_idx.as<uint32_t>(), f->rec_g.as<SplatRec>(),
+                                    f->rect_g.as<uint2>(), f->cnt_g.as<uint32_t>(), n, counters + 0,
+                                    f->rec.as<SplatRec>(), f->aux.as<SplatAux>(), f->cnt_r.as<uint32_t>(),
+                                    f->rank_of_g.as<int32_t>()))
+      return r;
+    ctx->launches += n > 0 ? 1 : 0;
+    uint32_t* offs = dk[sel ^ 1];
+    if (int r = scan_exclusive(st, f->cnt_r.as<uint32_t>(), n, counters + 0, false, offs, f->scan_tmp.as<uint32_t>(),
+                               counters + 1, &ctx->launches))
+      return r;
+    // 4. duplicate (tile, rank) entries, stable sort by tile, ranges
+    if (int r = launch_duplicate(st, offs, f->aux.as<SplatAux>(), n, counters + 0, f->tiles_x, f->k_cap,
+                                 f->ekey[0].as<uint32_t>(), f->eval_[0].as<uint32_t>(), f->off_g.as<uint32_t>()))
+      return r;
+    ctx->launches += n > 0 ? 1 : 0;
     uint32_t* ek[2] = {f->ekey[0].as<uint32_t>(), f->ekey[1].as<uint32_t>()};
     uint32_t* ev[2] = {f->eval_[0].as<uint32_t>(), f->eval_[1].as<uint32_t>()};
-    int sel = 0;
-    r = radix_sort_pairs(st, ek, ev, k, bits, f->sort_hist.as<uint32_t>(), &sel, &ctx->launches);
-    if (r) return r;
-    f->sorted_sel = sel;
-    r = launch_tile_ranges(st, ek[sel], k, n_tiles, f->ranges.as<uint2>());
-    if (r) return r;
+    int esel = 0;
+    if (int r = radix_sort_pairs(st, ek, ev, f->k_cap, counters + 1, tile_bits(n_tiles), f->sort_hist.as<uint32_t>(),
+                                 &esel, &ctx->launches))
+      return r;
+    f->sorted_sel = esel;
+    if (int r = launch_tile_ranges(st, ek[esel], f->k_cap, counters + 1, n_tiles, f->ranges.as<uint2>())) return r;
     ctx->launches += n_tiles > 0 ? 1 : 0;
   }
   {
     StageScope sc(ctx, kStComposite);
-    int r = launch_composite(st, f, rc);
-    if (r) return r;
+    if (int r = launch_composite(st, f, rc)) return r;
     ctx->launches += n_tiles > 0 ? 1 : 0;
   }
   return GSB_OK;
 }
 
+// Synchronous forward for the host API: runs the async pass, reads (V, K)
+// and re-runs with a larger entry capacity if K overflowed it.
+static int render_sync(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, const RasterDev& rc) {
+  int64_t want = f->k_cap > 0 ? f->k_cap : std::max<int64_t>(3 * cloud->n, 1 << 16);
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    if (int r = frame_reserve(f, cloud, want)) return r;
+    if (int r = render_async(ctx, cloud, f, rc)) return r;
+    uint32_t cnt[2];
+    if (int r = read_counters(ctx, f->counters.as<uint32_t>(), cnt, 2)) return r;
+    f->n_splats = cnt[0];
+    f->n_entries = cnt[1];
+    if ((int64_t)cnt[1] <= f->k_cap) return GSB_OK;
+    want = (int64_t)cnt[1] + (int64_t)cnt[1] / 4 + 4096;
+  }
+  return fail(GSB_ERR_OUT_OF_MEMORY, "entry capacity did not converge");
+}
+
 static int frame_setup(gsb_ctx* ctx, gsb_frame* f, const gsb_cloud* cloud, const gsb_camera* cam,
-                       const double bg[3], const gsb_raster_config* cfg) {
+                       const double bg[3], const gsb_raster_config* cfg, bool upload_camera) {
   if (cam->width <= 0 || cam->height <= 0) return fail(GSB_ERR_INVALID_ARGUMENT, "camera size must be positive");
   f->width = cam->width;
   f->height = cam->height;
@@ -372,11 +411,14 @@ static int frame_setup(gsb_ctx* ctx, gsb_frame* f, const gsb_cloud* cloud, const
   f->valid = false;
   f->has_dimage = false;
   GSB_RESERVE(f->cam, sizeof(CamDev));
-  CamDev cd = make_camdev(cam, kTile);
-  CamDev* h = static_cast<CamDev*>(pinned(ctx, sizeof(CamDev)));
-  if (!h) return fail(GSB_ERR_OUT_OF_MEMORY, "pinned staging");
-  *h = cd;
-  GSB_CUDA(cudaMemcpyAsync(f->cam.p, h, sizeof(CamDev), cudaMemcpyHostToDevice, ctx->stream));
+  if (upload_camera) {
+    CamDev cd = make_camdev(cam, kTile);
+    CamDev* h = static_cast<CamDev*>(pinned(ctx, sizeof(CamDev)));
+    if (!h) return fail(GSB_ERR_OUT_OF_MEMORY, "pinned staging");
+    GSB_CUDA(cudaStreamSynchronize(ctx->stream));  // staging buffer reuse
+    *h = cd;
+    GSB_CUDA(cudaMemcpyAsync(f->cam.p, h, sizeof(CamDev), cudaMemcpyHostToDevice, ctx->stream));
+  }
   return GSB_OK;
 }
 
@@ -410,13 +452,14 @@ static int upload_image(gsb_ctx* ctx, const double* img, int W, int H, float* de
   return GSB_OK;
 }
 
+// Loss on the frame's image (buffers sized by frame_reserve or here).
 static int loss_device(gsb_ctx* ctx, gsb_frame* f, const float* target, double beta, bool want_grad) {
   const int W = f->width, H = f->height;
-  const int64_t P = (int64_t)W * H;
-  GSB_RESERVE(f->gmaps, sizeof(float) * 9 * std::max<int64_t>(P, 1));
+  const int64_t P = std::max<int64_t>((int64_t)W * H, 1);
+  GSB_RESERVE(f->gmaps, sizeof(float) * 9 * P);
   GSB_RESERVE(f->loss_blocks, sizeof(double) * 2 * loss_block_count(W, H));
   GSB_RESERVE(f->loss_val, sizeof(double) * 4);
-  if (want_grad) GSB_RESERVE(f->d_image, sizeof(float) * 3 * std::max<int64_t>(P, 1));
+  if (want_grad) GSB_RESERVE(f->d_image, sizeof(float) * 3 * P);
   StageScope sc(ctx, kStLoss);
   int r = launch_rgb_loss(ctx->stream, f->image.as<float>(), target, W, H, beta, f->gmaps.as<float>(),
                           f->loss_blocks.as<double>(), f->loss_val.as<double>(), want_grad ? f->d_image.as<float>() : nullptr,
@@ -426,22 +469,17 @@ static int loss_device(gsb_ctx* ctx, gsb_frame* f, const float* target, double b
   return GSB_OK;
 }
 
+// Backward pass (buffers sized by frame_reserve).
 static int backward_device(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, bool full, float* grads) {
-  const int64_t k = f->n_entries;
-  GSB_RESERVE(f->partials, sizeof(float) * kPartial * std::max<int64_t>(k, 1));
-  GSB_RESERVE(f->pose_blocks, sizeof(double) * 6 * ((cloud->n + 255) / 256 + 1));
-  GSB_RESERVE(f->d_pose, sizeof(double) * 6);
   const RasterDev rc = make_rasterdev(&f->config);
   {
     StageScope sc(ctx, kStBwdRaster);
-    int r = launch_backward_raster(ctx->stream, f, rc);
-    if (r) return r;
+    if (int r = launch_backward_raster(ctx->stream, f, rc)) return r;
     ctx->launches += f->tiles_x * f->tiles_y > 0 ? 1 : 0;
   }
   {
     StageScope sc(ctx, kStBwdGeom);
-    int r = launch_backward_geom(ctx->stream, cloud, f, rc, full, grads, &ctx->launches);
-    if (r) return r;
+    if (int r = launch_backward_geom(ctx->stream, cloud, f, rc, full, grads, &ctx->launches)) return r;
   }
   return GSB_OK;
 }
@@ -495,6 +533,10 @@ int gsb_ctx_create(int32_t device, gsb_ctx** out) {
     return cuda_fail(e, "cudaStreamCreate");
   }
   c->timer = new StageTimer();
+  if (int r = init_loss_constants()) {
+    gsb_ctx_destroy(c);
+    return r;
+  }
   *out = c;
   return GSB_OK;
 }
@@ -668,7 +710,7 @@ int gsb_frame_destroy(gsb_frame* f) {
   cudaSetDevice(f->ctx->device);
   cudaStreamSynchronize(f->ctx->stream);
   DevBuf* bufs[] = {&f->cam, &f->rec_g, &f->rect_g, &f->cnt_g, &f->depth_g, &f->radius_g, &f->rank_of_g,
-                    &f->vis_idx, &f->dkey[0], &f->dkey[1], &f->dval[0], &f->dval[1], &f->rec, &f->aux,
+                    &f->colj, &f->off_g, &f->vis_idx, &f->dkey[0], &f->dkey[1], &f->dval[0], &f->dval[1], &f->rec, &f->aux,
                     &f->cnt_r, &f->ekey[0], &f->ekey[1], &f->eval_[0], &f->eval_[1], &f->ranges, &f->image,
                     &f->final_t, &f->pixstate, &f->d_image, &f->partials, &f->pose_blocks, &f->d_pose,
                     &f->loss_blocks, &f->loss_val, &f->gmaps, &f->scan_tmp, &f->sort_hist, &f->counters};
@@ -685,9 +727,9 @@ int gsb_render(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, const doub
   gsb_default_raster_config(&dflt);
   if (!cfg) cfg = &dflt;
   if (int r = validate_config(cfg)) return r;
-  if (int r = frame_setup(ctx, f, cloud, cam, bg, cfg)) return r;
+  if (int r = frame_setup(ctx, f, cloud, cam, bg, cfg, true)) return r;
   const RasterDev rc = make_rasterdev(cfg);
-  if (int r = render_device(ctx, cloud, f, rc)) return r;
+  if (int r = render_sync(ctx, cloud, f, rc)) return r;
   f->valid = true;
   if (image_out) return download_image(ctx, f->image.as<float>(), f->width, f->height, image_out);
   return GSB_OK;
@@ -1085,6 +1127,10 @@ int gsb_ctx_timer_stop(gsb_ctx* ctx, double* ms) {
 }  // extern "C"
 
 // ------------------------------------------------------------ sessions
+// A session's pose_descent iteration is one fixed launch sequence, captured
+// once into a CUDA graph and replayed (one cudaGraphLaunch per iteration).
+// The graph is rebuilt when the shared scratch frame's buffers move
+// (frame gen), the entry capacity changes, or profiling is toggled.
 struct gsb_session {
   gsb_ctx* ctx = nullptr;
   gsb_cloud* cloud = nullptr;
@@ -1095,9 +1141,137 @@ struct gsb_session {
   DevBuf camdev;  // CamDev of the current pose
   DevBuf trace;   // pose (12) + loss (1) per iteration
   void* host_state = nullptr;
+  uint32_t* host_counters = nullptr;
   int64_t n_splats = 0, n_entries = 0;
   int32_t stopped = 0;
+  int32_t pending = 0;  // iterations launched since the last status check
+  cudaGraphExec_t exec = nullptr;
+  int64_t graph_launches = 0;  // kernels per replay
+  const gsb_frame* graph_frame = nullptr;
+  uint64_t graph_gen = 0;
+  int64_t graph_kcap = 0;
+  bool graph_profiled = false;
+  cudaEvent_t ev[kNumStages][2] = {};
+  bool have_events = false;
 };
+
+namespace gsb {
+
+static int session_launch_iteration(gsb_ctx* ctx, gsb_session* s, gsb_frame* f) {
+  const gsb_pose_config& cfg = s->cfg;
+  const RasterDev rc = make_rasterdev(&cfg.raster);
+  double* tp = s->trace.as<double>();
+  double* tl = tp + 12 * (size_t)cfg.budget;
+  {
+    StageScope sc(ctx, kStOther);
+    GSB_CUDA(cudaMemcpyAsync(f->cam.p, s->camdev.p, sizeof(CamDev), cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  if (int r = render_async(ctx, s->cloud, f, rc)) return r;
+  if (int r = loss_device(ctx, f, s->target->planes.as<float>(), cfg.beta, true)) return r;
+  if (int r = backward_device(ctx, s->cloud, f, false, nullptr)) return r;
+  StageScope sc(ctx, kStOptim);
+  if (int r = launch_pose_iter(ctx->stream, s->state.p, f->d_pose.as<double>(), f->loss_val.as<double>(),
+                               cfg.cam_lr_start, cfg.cam_lr_end, cfg.pose_converged_eps, cfg.budget,
+                               s->camdev.as<CamDev>(), tp, tl, f->counters.as<uint32_t>() + 1, f->k_cap))
+    return r;
+  ctx->launches += 1;
+  return GSB_OK;
+}
+
+static int session_capture(gsb_ctx* ctx, gsb_session* s, gsb_frame* f) {
+  if (s->exec) {
+    cudaGraphExecDestroy(s->exec);
+    s->exec = nullptr;
+  }
+  if (ctx->profiling && !s->have_events) {
+    for (int k = 0; k < kNumStages; ++k)
+      for (int j = 0; j < 2; ++j) GSB_CUDA(cudaEventCreate(&s->ev[k][j]));
+    s->have_events = true;
+  }
+  const int64_t launches0 = ctx->launches;
+  GSB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  ctx->stage_events = ctx->profiling ? s->ev : nullptr;
+  int r = session_launch_iteration(ctx, s, f);
+  ctx->stage_events = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+  if (r) {
+    if (graph) cudaGraphDestroy(graph);
+    return r;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+  e = cudaGraphInstantiate(&s->exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+  s->graph_launches = ctx->launches - launches0;
+  ctx->launches = launches0;  // counted per replay instead
+  s->graph_frame = f;
+  s->graph_gen = f->gen;
+  s->graph_kcap = f->k_cap;
+  s->graph_profiled = ctx->profiling;
+  return GSB_OK;
+}
+
+static gsb_frame* work_frame(gsb_ctx* ctx) {
+  if (!ctx->work) {
+    ctx->work = new gsb_frame();
+    ctx->work->ctx = ctx;
+  }
+  return ctx->work;
+}
+
+static int session_prepare(gsb_ctx* ctx, gsb_session* s, gsb_frame** out) {
+  gsb_frame* f = work_frame(ctx);
+  if (int r = frame_setup(ctx, f, s->cloud, &s->cam, s->cfg.background, &s->cfg.raster, false)) return r;
+  const int64_t want = f->k_cap > 0 ? f->k_cap : std::max<int64_t>(3 * s->cloud->n, 1 << 16);
+  if (int r = frame_reserve(f, s->cloud, want)) return r;
+  if (!s->exec || s->graph_frame != f || s->graph_gen != f->gen || s->graph_kcap != f->k_cap ||
+      s->graph_profiled != ctx->profiling)
+    if (int r = session_capture(ctx, s, f)) return r;
+  *out = f;
+  return GSB_OK;
+}
+
+static int session_launch(gsb_ctx* ctx, gsb_session* s, int32_t iterations) {
+  gsb_frame* f = nullptr;
+  if (int r = session_prepare(ctx, s, &f)) return r;
+  for (int32_t i = 0; i < iterations; ++i) GSB_CUDA(cudaGraphLaunch(s->exec, ctx->stream));
+  ctx->launches += s->graph_launches * iterations;
+  s->pending += iterations;
+  return GSB_OK;
+}
+
+// Waits for the session's launched iterations; re-runs any the device
+// discarded for an entry-capacity overflow (after growing the capacity).
+static int session_sync(gsb_ctx* ctx, gsb_session* s) {
+  const size_t sb = pose_state_bytes();
+  for (int round = 0; round < 8; ++round) {
+    gsb_frame* f = work_frame(ctx);
+    GSB_CUDA(cudaMemcpyAsync(s->host_state, s->state.p, sb, cudaMemcpyDeviceToHost, ctx->stream));
+    if (f->counters.p)
+      GSB_CUDA(cudaMemcpyAsync(s->host_counters, f->counters.p, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+    GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    pose_state_read(s->host_state, nullptr, nullptr, nullptr, nullptr, nullptr, &s->stopped, nullptr, nullptr, nullptr,
+                    nullptr);
+    const int32_t aborted = pose_state_take_aborted(s->host_state);
+    s->n_splats = s->host_counters[0];
+    s->n_entries = s->host_counters[1];
+    if (aborted == 0) {
+      s->pending = 0;
+      return GSB_OK;
+    }
+    // clear the device-side abort counter, grow the entry capacity, replay
+    GSB_CUDA(cudaMemcpyAsync(s->state.p, s->host_state, sb, cudaMemcpyHostToDevice, ctx->stream));
+    const int64_t k = (int64_t)s->host_counters[1];
+    if (int r = frame_reserve(f, s->cloud, k + k / 4 + 4096)) return r;
+    s->pending = 0;
+    if (int r = session_launch(ctx, s, aborted)) return r;
+  }
+  return fail(GSB_ERR_OUT_OF_MEMORY, "entry capacity did not converge");
+}
+
+}  // namespace gsb
 
 extern "C" {
 
@@ -1123,24 +1297,21 @@ int gsb_session_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* target, const 
     s->cam.t[r] = init_pose[r * 4 + 3];
   }
   const size_t sb = pose_state_bytes();
+  const size_t host_bytes = ((sb + 63) / 64) * 64 + 64 + sizeof(CamDev);
   cudaError_t e = s->state.reserve(sb);
   if (e == cudaSuccess) e = s->camdev.reserve(sizeof(CamDev));
   if (e == cudaSuccess) e = s->trace.reserve(sizeof(double) * 13 * (size_t)cfg->budget);
-  if (e == cudaSuccess) e = cudaMallocHost(&s->host_state, sb);
+  if (e == cudaSuccess) e = cudaMallocHost(&s->host_state, host_bytes);
   if (e != cudaSuccess) {
     gsb_session_destroy(s);
     return cuda_fail(e, "session alloc");
   }
+  char* hb = static_cast<char*>(s->host_state);
+  s->host_counters = reinterpret_cast<uint32_t*>(hb + ((sb + 63) / 64) * 64);
+  CamDev* hcam = reinterpret_cast<CamDev*>(hb + ((sb + 63) / 64) * 64 + 64);
   pose_state_init(s->host_state, init_pose);
-  CamDev cd = make_camdev(&s->cam, kTile);
-  CamDev* h = static_cast<CamDev*>(pinned(ctx, sizeof(CamDev)));
-  if (!h) {
-    gsb_session_destroy(s);
-    return fail(GSB_ERR_OUT_OF_MEMORY, "pinned staging");
-  }
-  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
-  *h = cd;
-  GSB_CUDA(cudaMemcpyAsync(s->camdev.p, h, sizeof(CamDev), cudaMemcpyHostToDevice, ctx->stream));
+  *hcam = make_camdev(&s->cam, kTile);
+  GSB_CUDA(cudaMemcpyAsync(s->camdev.p, hcam, sizeof(CamDev), cudaMemcpyHostToDevice, ctx->stream));
   GSB_CUDA(cudaMemcpyAsync(s->state.p, s->host_state, sb, cudaMemcpyHostToDevice, ctx->stream));
   GSB_CUDA(cudaStreamSynchronize(ctx->stream));
   *out = s;
@@ -1151,6 +1322,10 @@ int gsb_session_destroy(gsb_session* s) {
   if (!s) return GSB_OK;
   cudaSetDevice(s->ctx->device);
   cudaStreamSynchronize(s->ctx->stream);
+  if (s->exec) cudaGraphExecDestroy(s->exec);
+  if (s->have_events)
+    for (int k = 0; k < kNumStages; ++k)
+      for (int j = 0; j < 2; ++j) cudaEventDestroy(s->ev[k][j]);
   s->state.release();
   s->camdev.release();
   s->trace.release();
@@ -1162,39 +1337,34 @@ int gsb_session_destroy(gsb_session* s) {
 int gsb_session_step(gsb_ctx* ctx, gsb_session* s, int32_t iterations) {
   if (int r = ensure_device(ctx)) return r;
   if (!s || s->ctx != ctx) return fail(GSB_ERR_INVALID_ARGUMENT, "session / context mismatch");
-  if (!ctx->work) {
-    ctx->work = new gsb_frame();
-    ctx->work->ctx = ctx;
+  const int32_t chunk = 16;
+  while (iterations > 0 && !s->stopped) {
+    const int32_t now = std::min(iterations, chunk);
+    if (int r = session_launch(ctx, s, now)) return r;
+    if (int r = session_sync(ctx, s)) return r;
+    iterations -= now;
   }
-  gsb_frame* f = ctx->work;
-  const gsb_pose_config& cfg = s->cfg;
-  if (int r = frame_setup(ctx, f, s->cloud, &s->cam, cfg.background, &cfg.raster)) return r;
-  const RasterDev rc = make_rasterdev(&cfg.raster);
-  const size_t sb = pose_state_bytes();
-  double* tp = s->trace.as<double>();
-  double* tl = tp + 12 * (size_t)cfg.budget;
-  for (int it = 0; it < iterations && !s->stopped; ++it) {
-    GSB_CUDA(cudaMemcpyAsync(f->cam.p, s->camdev.p, sizeof(CamDev), cudaMemcpyDeviceToDevice, ctx->stream));
-    if (int r = render_device(ctx, s->cloud, f, rc)) return r;
-    f->valid = true;
-    if (int r = loss_device(ctx, f, s->target->planes.as<float>(), cfg.beta, true)) return r;
-    if (int r = backward_device(ctx, s->cloud, f, false, nullptr)) return r;
-    {
-      StageScope sc(ctx, kStOptim);
-      if (int r = launch_pose_iter(ctx->stream, s->state.p, f->d_pose.as<double>(), f->loss_val.as<double>(),
-                                   cfg.cam_lr_start, cfg.cam_lr_end, cfg.pose_converged_eps, cfg.budget,
-                                   s->camdev.as<CamDev>(), tp, tl))
-        return r;
-      ctx->launches += 1;
-    }
-    GSB_CUDA(cudaMemcpyAsync(s->host_state, s->state.p, sb, cudaMemcpyDeviceToHost, ctx->stream));
-    GSB_CUDA(cudaStreamSynchronize(ctx->stream));
-    pose_state_read(s->host_state, nullptr, nullptr, nullptr, nullptr, nullptr, &s->stopped, nullptr, nullptr,
-                    nullptr, nullptr);
-    s->n_splats = f->n_splats;
-    s->n_entries = f->n_entries;
+  return GSB_OK;
+}
+
+int gsb_session_step_async(gsb_ctx* ctx, gsb_session* s, int32_t iterations) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!s || s->ctx != ctx) return fail(GSB_ERR_INVALID_ARGUMENT, "session / context mismatch");
+  if (iterations <= 0) return GSB_OK;
+  return session_launch(ctx, s, iterations);
+}
+
+int gsb_session_stage_times(gsb_session* s, double* ms_out) {
+  if (!s || !ms_out) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  if (int r = ensure_device(s->ctx)) return r;
+  for (int k = 0; k < kNumStages; ++k) ms_out[k] = 0.0;
+  if (!s->have_events || !s->graph_profiled) return GSB_OK;
+  GSB_CUDA(cudaStreamSynchronize(s->ctx->stream));
+  for (int k = 0; k < kNumStages; ++k) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, s->ev[k][0], s->ev[k][1]) == cudaSuccess) ms_out[k] = t;
   }
-  f->valid = false;  // the scratch frame no longer matches any caller-visible camera
+  cudaGetLastError();  // stages never recorded report cudaErrorInvalidResourceHandle
   return GSB_OK;
 }
 
@@ -1203,8 +1373,7 @@ int gsb_session_read(gsb_session* s, double pose[12], double best_pose[12], doub
   if (!s) return fail(GSB_ERR_INVALID_ARGUMENT, "null session");
   gsb_ctx* ctx = s->ctx;
   if (int r = ensure_device(ctx)) return r;
-  GSB_CUDA(cudaMemcpyAsync(s->host_state, s->state.p, pose_state_bytes(), cudaMemcpyDeviceToHost, ctx->stream));
-  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (int r = session_sync(ctx, s)) return r;  // also re-runs discarded iterations
   pose_state_read(s->host_state, best_pose, pose, final_loss, steps_used, converged, stopped, nullptr, nullptr,
                   nullptr, nullptr);
   return GSB_OK;

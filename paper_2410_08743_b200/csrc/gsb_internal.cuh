@@ -56,6 +56,10 @@ struct __align__(16) SplatAux {
 // symmetric d_conic folded to 3 values: (D00, D01 (=D10), D11).
 constexpr int kPartial = 9;  // d_mu2d(2) d_conic(3) d_color(3) d_opacity(1)
 
+// cnt_g packs the tile count (low 28 bits) and the SH clamp bits (28..30).
+constexpr uint32_t kCntMask = 0x0fffffffu;
+constexpr int kClampShift = 28;
+
 // Parameter planes of a cloud: plane-major [P][n_pad] FP32.
 enum Plane : int {
   kMeanX = 0, kMeanY, kMeanZ, kQuatW, kQuatX, kQuatY, kQuatZ, kScaleX, kScaleY, kScaleZ, kOpacity,
@@ -85,8 +89,9 @@ int cuda_fail(cudaError_t e, const char* what);
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
-  cudaError_t reserve(size_t want) {
+  cudaError_t reserve(size_t want, bool* grew = nullptr) {
     if (want <= bytes) return cudaSuccess;
+    if (grew) *grew = true;
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
@@ -125,6 +130,7 @@ struct gsb_ctx {
   gsb::StageTimer* timer = nullptr;
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
   gsb_frame* work = nullptr;   // scratch forward state shared by sessions
+  cudaEvent_t (*stage_events)[2] = nullptr;  // set while capturing a profiled session graph
 };
 
 struct gsb_cloud {
@@ -167,6 +173,8 @@ struct gsb_frame {
   int32_t width = 0, height = 0, tiles_x = 0, tiles_y = 0;
   uint64_t fingerprint = 0;
   uint64_t cloud_version = 0;
+  int64_t k_cap = 0;      // entry capacity of the K-sized buffers
+  uint64_t gen = 0;       // bumped whenever a buffer is reallocated (invalidates graphs)
   const gsb_cloud* cloud = nullptr;
   gsb_camera camera{};
   gsb_raster_config config{};
@@ -182,6 +190,8 @@ struct gsb_frame {
   gsb::DevBuf depth_g;    // double
   gsb::DevBuf radius_g;   // double (export only)
   gsb::DevBuf rank_of_g;  // int32 rank or -1
+  gsb::DevBuf colj;       // FP32 [9][n_pad] colour/direction Jacobian (clamped rows zero)
+  gsb::DevBuf off_g;      // uint32 entry offset of each visible Gaussian (rank-major stream)
   // visible (V)
   gsb::DevBuf vis_idx;    // uint32 gid, index order
   gsb::DevBuf dkey[2];    // uint32 depth keys (ping-pong)

@@ -222,21 +222,22 @@ __global__ void loss_finalize_kernel(const double* __restrict__ block_sums, int 
   }
 }
 
-static bool g_win_ready = false;
+// gaussian_window (losses.cpp:19-32), FP64 on host, into constant memory of
+// the current device. Called once per context (never inside graph capture).
+int init_loss_constants() {
+  double w[kWin], sum = 0.0;
+  for (int i = 0; i < kWin; ++i) {
+    const double d = i - kHalf;
+    w[i] = exp(-d * d / (2.0 * 1.5 * 1.5));
+    sum += w[i];
+  }
+  for (int i = 0; i < kWin; ++i) w[i] /= sum;
+  GSB_CUDA(cudaMemcpyToSymbol(c_win, w, sizeof w));
+  return GSB_OK;
+}
 
 int launch_rgb_loss(cudaStream_t st, const float* ren, const float* tgt, int W, int H, double beta, float* gmaps,
                     double* block_sums, double* out3, float* d_image, int64_t* launches) {
-  if (!g_win_ready) {  // gaussian_window (losses.cpp:19-32), FP64 on host
-    double w[kWin], sum = 0.0;
-    for (int i = 0; i < kWin; ++i) {
-      const double d = i - kHalf;
-      w[i] = exp(-d * d / (2.0 * 1.5 * 1.5));
-      sum += w[i];
-    }
-    for (int i = 0; i < kWin; ++i) w[i] /= sum;
-    GSB_CUDA(cudaMemcpyToSymbol(c_win, w, sizeof w));
-    g_win_ready = true;
-  }
   const int64_t cnt_valid = (W > 2 * kHalf && H > 2 * kHalf) ? (int64_t)(W - 2 * kHalf) * (H - 2 * kHalf) : 0;
   const int has_ssim = cnt_valid > 0 ? 1 : 0;
   const double scale = has_ssim ? 1.0 / (3.0 * (double)cnt_valid) : 0.0;

@@ -31,6 +31,8 @@ struct PoseState {
   double best_loss, final_loss;
   double applied[6];
   int32_t iter, steps_used, converged, stop;
+  int32_t aborted;  // iterations discarded because the entry capacity overflowed
+  int32_t pad;
 };
 
 struct PoseCtl {
@@ -209,9 +211,14 @@ __device__ void d_write_cam(const PoseState& s, CamDev* cam) {
 
 // One pose_descent iteration tail (after render + loss + backward).
 __global__ void pose_iter_kernel(PoseState* st, const double* __restrict__ dpose, const double* __restrict__ loss3,
-                                 PoseCtl ctl, CamDev* cam, double* trace_pose, double* trace_loss) {
+                                 PoseCtl ctl, CamDev* cam, double* trace_pose, double* trace_loss,
+                                 const uint32_t* __restrict__ k_dev, int64_t k_cap) {
   PoseState s = *st;
   if (s.stop) return;
+  if ((int64_t)*k_dev > k_cap) {  // entry capacity overflow: discard, the host re-runs it
+    st->aborted = s.aborted + 1;
+    return;
+  }
   const int it = s.iter;
   const double loss = loss3[2];
   if (trace_pose) {
@@ -319,9 +326,11 @@ __global__ void __launch_bounds__(256) cloud_adam_kernel(float* __restrict__ par
 
 // ------------------------------------------------------------- host glue
 int launch_pose_iter(cudaStream_t st, void* state, const double* dpose, const double* loss3, double lr_start,
-                     double lr_end, double eps, int budget, CamDev* cam, double* trace_pose, double* trace_loss) {
+                     double lr_end, double eps, int budget, CamDev* cam, double* trace_pose, double* trace_loss,
+                     const uint32_t* k_dev, int64_t k_cap) {
   PoseCtl ctl{lr_start, lr_end, eps, budget, 0};
-  pose_iter_kernel<<<1, 1, 0, st>>>(static_cast<PoseState*>(state), dpose, loss3, ctl, cam, trace_pose, trace_loss);
+  pose_iter_kernel<<<1, 1, 0, st>>>(static_cast<PoseState*>(state), dpose, loss3, ctl, cam, trace_pose, trace_loss,
+                                    k_dev, k_cap);
   GSB_CHECK_LAUNCH("pose_iter_kernel");
   return GSB_OK;
 }
@@ -360,6 +369,12 @@ void pose_state_read(const void* host_state, double best_pose[12], double cur_po
     if (v) v[k] = s->v[k];
   }
   if (step) *step = s->step;
+}
+int32_t pose_state_take_aborted(void* host_state) {
+  PoseState* s = static_cast<PoseState*>(host_state);
+  const int32_t a = s->aborted;
+  s->aborted = 0;
+  return a;
 }
 void pose_state_set_adam(void* host_state, const double m[6], const double v[6], int64_t step) {
   PoseState* s = static_cast<PoseState*>(host_state);

@@ -15,6 +15,8 @@
 // same (FP32-stored) parameters; the depth sort and tile spans — the
 // discrete decisions — therefore match the reference. The per-splat record
 // is then rounded to FP32 for compositing (except mu2d, kept FP64).
+#include <algorithm>
+
 #include "gsb_internal.cuh"
 
 namespace gsb {
@@ -27,37 +29,6 @@ __device__ __forceinline__ double dot3(double a0, double a1, double a2, double b
   return a_(a_(m_(a0, b0), m_(a1, b1)), m_(a2, b2));
 }
 
-// sh.cpp:9-14
-__constant__ double kC1 = 0.4886025119029199;
-__constant__ double kC2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005, -1.0925484305920792,
-                              0.5462742152960396};
-__constant__ double kC3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658, 0.3731763325901154,
-                              -0.4570457994644658, 1.445305721320277, -0.5900435899266435};
-constexpr double kSh0 = 0.28209479177387814;
-
-// sh.cpp:18-40
-__device__ __forceinline__ void sh_basis(double x, double y, double z, int degree, double* out) {
-  out[0] = kSh0;
-  if (degree < 1) return;
-  out[1] = m_(-kC1, y);
-  out[2] = m_(kC1, z);
-  out[3] = m_(-kC1, x);
-  if (degree < 2) return;
-  const double xx = m_(x, x), yy = m_(y, y), zz = m_(z, z);
-  out[4] = m_(m_(kC2[0], x), y);
-  out[5] = m_(m_(kC2[1], y), z);
-  out[6] = m_(kC2[2], s_(s_(m_(2.0, zz), xx), yy));
-  out[7] = m_(m_(kC2[3], x), z);
-  out[8] = m_(kC2[4], s_(xx, yy));
-  if (degree < 3) return;
-  out[9] = m_(m_(kC3[0], y), s_(m_(3.0, xx), yy));
-  out[10] = m_(m_(m_(kC3[1], x), y), z);
-  out[11] = m_(m_(kC3[2], y), s_(s_(m_(4.0, zz), xx), yy));
-  out[12] = m_(m_(kC3[3], z), s_(s_(m_(2.0, zz), m_(3.0, xx)), m_(3.0, yy)));
-  out[13] = m_(m_(kC3[4], x), s_(s_(m_(4.0, zz), xx), yy));
-  out[14] = m_(m_(kC3[5], z), s_(xx, yy));
-  out[15] = m_(m_(kC3[6], x), s_(xx, m_(3.0, yy)));
-}
 
 __device__ __forceinline__ int clamp_tile(double v, int n_tiles) {  // rasterizer.cpp:140-143
   const double hi = n_tiles - 1.0;
@@ -65,11 +36,96 @@ __device__ __forceinline__ int clamp_tile(double v, int n_tiles) {  // rasterize
   return (int)c;
 }
 
+// sh_eval (sh.cpp:66-84) in FP32 — the colour is stored FP32 anyway — plus
+// the colour/direction Jacobian G[c][k] = sum_b coeff[c*cap+b] dY_b/d dir_k
+// with clamped rows zeroed: the d_dir chain of render_backward
+// (rasterizer.cpp:496-511, sh.cpp:42-64, capacity stride as there),
+// precomputed while the SH planes are streamed so the backward never re-reads
+// them. kQuirk: active degree < capacity, where the forward indexes channel c
+// at c*(DEG+1)^2 (sh.cpp:74) but storage / backward use c*(cap+1)^2.
+template <int DEG, bool kQuirk>
+__device__ __forceinline__ void sh_colour(const float* __restrict__ P, int64_t n_pad, int sh_cap, float x, float y,
+                                          float z, float col[3], uint32_t* clamp, float G[9]) {
+  constexpr int NB = (DEG + 1) * (DEG + 1);
+  const int bcap = (sh_cap + 1) * (sh_cap + 1);
+  const float C1 = 0.4886025119029199f;
+  const float C2[5] = {1.0925484305920792f, -1.0925484305920792f, 0.31539156525252005f, -1.0925484305920792f,
+                       0.5462742152960396f};
+  const float C3[7] = {-0.5900435899266435f, 2.890611442640554f, -0.4570457994644658f, 0.3731763325901154f,
+                       -0.4570457994644658f, 1.445305721320277f, -0.5900435899266435f};
+  float B[16], gx[16], gy[16], gz[16];
+  B[0] = 0.28209479177387814f;
+  gx[0] = gy[0] = gz[0] = 0.f;
+  if (DEG >= 1) {
+    B[1] = -C1 * y; B[2] = C1 * z; B[3] = -C1 * x;
+    gx[1] = 0; gy[1] = -C1; gz[1] = 0;
+    gx[2] = 0; gy[2] = 0; gz[2] = C1;
+    gx[3] = -C1; gy[3] = 0; gz[3] = 0;
+  }
+  const float xx = x * x, yy = y * y, zz = z * z;
+  if (DEG >= 2) {
+    B[4] = C2[0] * x * y; B[5] = C2[1] * y * z; B[6] = C2[2] * (2.f * zz - xx - yy);
+    B[7] = C2[3] * x * z; B[8] = C2[4] * (xx - yy);
+    gx[4] = C2[0] * y; gy[4] = C2[0] * x; gz[4] = 0;
+    gx[5] = 0; gy[5] = C2[1] * z; gz[5] = C2[1] * y;
+    gx[6] = C2[2] * (-2.f * x); gy[6] = C2[2] * (-2.f * y); gz[6] = C2[2] * (4.f * z);
+    gx[7] = C2[3] * z; gy[7] = 0; gz[7] = C2[3] * x;
+    gx[8] = C2[4] * (2.f * x); gy[8] = C2[4] * (-2.f * y); gz[8] = 0;
+  }
+  if (DEG >= 3) {
+    B[9] = C3[0] * y * (3.f * xx - yy); B[10] = C3[1] * x * y * z; B[11] = C3[2] * y * (4.f * zz - xx - yy);
+    B[12] = C3[3] * z * (2.f * zz - 3.f * xx - 3.f * yy); B[13] = C3[4] * x * (4.f * zz - xx - yy);
+    B[14] = C3[5] * z * (xx - yy); B[15] = C3[6] * x * (xx - 3.f * yy);
+    gx[9] = C3[0] * (6.f * x * y); gy[9] = C3[0] * (3.f * xx - 3.f * yy); gz[9] = 0;
+    gx[10] = C3[1] * (y * z); gy[10] = C3[1] * (x * z); gz[10] = C3[1] * (x * y);
+    gx[11] = C3[2] * (-2.f * x * y); gy[11] = C3[2] * (4.f * zz - xx - 3.f * yy); gz[11] = C3[2] * (8.f * y * z);
+    gx[12] = C3[3] * (-6.f * x * z); gy[12] = C3[3] * (-6.f * y * z); gz[12] = C3[3] * (6.f * zz - 3.f * xx - 3.f * yy);
+    gx[13] = C3[4] * (4.f * zz - 3.f * xx - yy); gy[13] = C3[4] * (-2.f * x * y); gz[13] = C3[4] * (8.f * x * z);
+    gx[14] = C3[5] * (2.f * x * z); gy[14] = C3[5] * (-2.f * y * z); gz[14] = C3[5] * (xx - yy);
+    gx[15] = C3[6] * (3.f * xx - 3.f * yy); gy[15] = C3[6] * (-6.f * x * y); gz[15] = 0;
+  }
+  uint32_t cl = 0;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    float v = 0.5f, g0 = 0.f, g1 = 0.f, g2 = 0.f;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const float co = P[(int64_t)(kShBase + c * (kQuirk ? NB : bcap) + b) * n_pad];
+      v = fmaf(co, B[b], v);
+      if (!kQuirk) {
+        g0 = fmaf(co, gx[b], g0);
+        g1 = fmaf(co, gy[b], g1);
+        g2 = fmaf(co, gz[b], g2);
+      }
+    }
+    if (kQuirk) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const float co = P[(int64_t)(kShBase + c * bcap + b) * n_pad];
+        g0 = fmaf(co, gx[b], g0);
+        g1 = fmaf(co, gy[b], g1);
+        g2 = fmaf(co, gz[b], g2);
+      }
+    }
+    if (v < 0.f) {
+      cl |= 1u << c;
+      v = 0.f;
+      g0 = g1 = g2 = 0.f;
+    }
+    col[c] = v;
+    G[3 * c] = g0;
+    G[3 * c + 1] = g1;
+    G[3 * c + 2] = g2;
+  }
+  *clamp = cl;
+}
+
+template <int DEG, bool kQuirk>
 __global__ void __launch_bounds__(256) preprocess_kernel(
     const float* __restrict__ params, int64_t n, int64_t n_pad, int sh_cap, int sh_active,
     const CamDev* __restrict__ cam_p, RasterDev rc, SplatRec* __restrict__ rec_g, uint2* __restrict__ rect_g,
     uint32_t* __restrict__ cnt_g, double* __restrict__ depth_g, double* __restrict__ radius_g,
-    int32_t* __restrict__ rank_of_g) {
+    int32_t* __restrict__ rank_of_g, float* __restrict__ colj) {
   __shared__ CamDev cam;
   if (threadIdx.x == 0) cam = *cam_p;
   __syncthreads();
@@ -148,22 +204,10 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
         dx = d_(dx, dn);
         dy = d_(dy, dn);
         dz = d_(dz, dn);
-        const int deg = sh_active < sh_cap ? sh_active : sh_cap;
-        const int nb = (deg + 1) * (deg + 1);
-        double basis[kMaxShCoeffs];
-        sh_basis(dx, dy, dz, deg, basis);
-        float col[3];
+        float col[3], G[9];
         uint32_t clamp = 0;
-        for (int c = 0; c < 3; ++c) {
-          double acc = 0.5;
-          // quirk kept: channel stride (d_active+1)^2 inside the capacity-strided block (sh.cpp:74)
-          for (int b = 0; b < nb; ++b) acc = a_(acc, m_((double)P[(kShBase + c * nb + b) * n_pad], basis[b]));
-          if (acc < 0.0) {
-            clamp |= 1u << c;
-            acc = 0.0;
-          }
-          col[c] = (float)acc;
-        }
+        sh_colour<DEG, kQuirk>(P, n_pad, sh_cap, (float)dx, (float)dy, (float)dz, col, &clamp, G);
+        for (int k = 0; k < 9; ++k) colj[(int64_t)k * n_pad + i] = G[k];
         const double op = d_(1.0, a_(1.0, exp(-(double)P[kOpacity * n_pad])));
         // tile span (rasterizer.cpp:138-146)
         const double tile = (double)kTile;
@@ -171,7 +215,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
         const int tx1 = clamp_tile(floor(d_(a_(u, radius), tile)), cam.tiles_x);
         const int ty0 = clamp_tile(floor(d_(s_(v, radius), tile)), cam.tiles_y);
         const int ty1 = clamp_tile(floor(d_(a_(v, radius), tile)), cam.tiles_y);
-        cnt = (uint32_t)(tx1 - tx0 + 1) * (uint32_t)(ty1 - ty0 + 1);
+        cnt = ((uint32_t)(tx1 - tx0 + 1) * (uint32_t)(ty1 - ty0 + 1)) | (clamp << kClampShift);
         SplatRec rec;
         rec.mu_x = u;
         rec.mu_y = v;
@@ -196,11 +240,25 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
 int launch_preprocess(cudaStream_t st, const gsb_cloud* cloud, const CamDev* cam, const RasterDev& rc,
                       gsb_frame* f) {
   const int64_t n = cloud->n;
-  if (n > 0)
-    preprocess_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-        cloud->params.as<float>(), n, cloud->n_pad, cloud->sh_degree, cloud->active_sh_degree, cam, rc,
-        f->rec_g.as<SplatRec>(), f->rect_g.as<uint2>(), f->cnt_g.as<uint32_t>(), f->depth_g.as<double>(),
-        f->radius_g.as<double>(), f->rank_of_g.as<int32_t>());
+  const int deg = std::min(cloud->active_sh_degree, cloud->sh_degree);
+  const bool quirk = deg < cloud->sh_degree;
+#define GSB_PRE(D, Q)                                                                                          \
+  preprocess_kernel<D, Q><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(                                       \
+      cloud->params.as<float>(), n, cloud->n_pad, cloud->sh_degree, cloud->active_sh_degree, cam, rc,          \
+      f->rec_g.as<SplatRec>(), f->rect_g.as<uint2>(), f->cnt_g.as<uint32_t>(), f->depth_g.as<double>(),        \
+      f->radius_g.as<double>(), f->rank_of_g.as<int32_t>(), f->colj.as<float>())
+  if (n > 0) {
+    switch (deg * 2 + (quirk ? 1 : 0)) {
+      case 0: GSB_PRE(0, false); break;
+      case 1: GSB_PRE(0, true); break;
+      case 2: GSB_PRE(1, false); break;
+      case 3: GSB_PRE(1, true); break;
+      case 4: GSB_PRE(2, false); break;
+      case 5: GSB_PRE(2, true); break;
+      default: GSB_PRE(3, false); break;
+    }
+  }
+#undef GSB_PRE
   GSB_CHECK_LAUNCH("preprocess_kernel");
   return GSB_OK;
 }

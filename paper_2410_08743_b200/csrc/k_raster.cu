@@ -1,7 +1,8 @@
 // k_raster.cu — K3 front-to-back compositing and K4a back-to-front backward
-// raster. One CTA per 16x16 tile, one thread per pixel; splat records are
-// staged through shared memory in batches of 256 (one record per thread per
-// batch, gathered by rank), so each record is read from L2/HBM once per tile.
+// raster. One CTA per 16x16 tile, one thread per pixel (warp w owns tile
+// rows 2w, 2w+1); splat records are staged through shared memory in batches
+// of 256 (one record per thread per batch, gathered by rank), so each record
+// is read from L2/HBM once per tile.
 //
 // K3 restates render's compositing loop (rasterizer.cpp:234-279):
 // integer pixel centres (245), processed counter set before the cutoff test
@@ -13,47 +14,56 @@
 // pixel back-to-front replay from contrib_count-1 with t_before = T/(1-a),
 // clamped channels zeroed, alpha-chain gradients only when a_raw < clamp.
 // The per-(pixel, splat) partials are reduced over the tile's 256 pixels in
-// a fixed order (warp butterfly, then warps 0..7) and written — zero when
-// untouched — to the entry's slot in the rank-major (pre-sort) stream, so
-// K4b reads each splat's partials contiguously and in tile order (phase 2's
-// per-splat order, rasterizer.cpp:410-418). No atomics: deterministic.
+// a fixed order (warp recursive-halving reduce-scatter, then warps 0..7) and
+// written — zero when untouched — to the entry's slot in the rank-major
+// (pre-sort) stream, so K4b reads each splat's partials contiguously and in
+// tile order (phase 2's per-splat order, rasterizer.cpp:410-418). No
+// atomics: deterministic.
+//
+// Both kernels skip a staged splat warp-uniformly when its cutoff ellipse
+// (|dy| <= cutoff * sqrt(Sigma_yy), Sigma = conic^-1, with a safety margin)
+// misses the warp's two pixel rows: every pixel of such a warp would fail the
+// g <= cutoff^2 test, so the result is unchanged.
 #include "gsb_internal.cuh"
 
 namespace gsb {
 
 constexpr int kBatch = 256;
+constexpr int kWarps = kTilePix / 32;
+constexpr unsigned kFull = 0xffffffffu;
 
-struct __align__(16) SmemSplat {
-  float mx, my, ca, cb;   // tile-local mean, conic a, b
-  float cc, op, r, g;     // conic c, opacity, colour r, g
-  float b, pad0, pad1, pad2;
+struct Staged {
+  float4 geo;  // tile-local mean x, y; conic a, b
+  float4 app;  // conic c, opacity, colour r, g
+  float4 ext;  // colour b, ellipse half-height (with margin), -, -
 };
+
+__device__ __forceinline__ void stage_splat(const SplatRec& R, double ox, double oy, float cutoff2, float4* geo,
+                                            float4* app, float4* ext) {
+  const float a = R.conic_a, b = R.conic_b, c = R.conic_c;
+  const float det = a * c - b * b;
+  const float half_h = sqrtf(cutoff2 * a / det) * 1.001f + 1e-3f;  // |dy| bound of g <= cutoff2
+  *geo = make_float4((float)(R.mu_x - ox), (float)(R.mu_y - oy), a, b);
+  *app = make_float4(c, R.opacity, R.col_r, R.col_g);
+  *ext = make_float4(R.col_b, half_h, 0.f, 0.f);
+}
 
 // Mahalanobis power g = d^T conic d. Forward and backward must take the
 // identical cutoff / alpha decisions, so both call exactly this.
-__device__ __forceinline__ float splat_power(const SmemSplat& q, float dx, float dy) {
-  return fmaf(q.ca * dx, dx, fmaf(q.cc * dy, dy, 2.0f * q.cb * dx * dy));
+__device__ __forceinline__ float splat_power(float ca, float cb, float cc, float dx, float dy) {
+  return fmaf(ca * dx, dx, fmaf(cc * dy, dy, 2.0f * cb * dx * dy));
 }
-__device__ __forceinline__ SmemSplat stage_splat(const SplatRec& R, double ox, double oy) {
-  SmemSplat q;
-  q.mx = (float)(R.mu_x - ox);
-  q.my = (float)(R.mu_y - oy);
-  q.ca = R.conic_a;
-  q.cb = R.conic_b;
-  q.cc = R.conic_c;
-  q.op = R.opacity;
-  q.r = R.col_r;
-  q.g = R.col_g;
-  q.b = R.col_b;
-  q.pad0 = q.pad1 = q.pad2 = 0.f;
-  return q;
+
+// Warp-uniform: does the splat's ellipse reach rows [row0, row0+1]?
+__device__ __forceinline__ bool rows_hit(float my, float half_h, float row_c) {
+  return fabsf(row_c - my) <= half_h + 0.5f;
 }
 
 __global__ void __launch_bounds__(kTilePix) composite_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ ranks, const SplatRec* __restrict__ rec,
     const CamDev* __restrict__ cam_p, RasterDev rc, float bg_r, float bg_g, float bg_b, int64_t npix,
     float* __restrict__ image, float* __restrict__ final_t, uint32_t* __restrict__ pixstate) {
-  __shared__ SmemSplat s[kBatch];
+  __shared__ float4 s_geo[kBatch], s_app[kBatch], s_ext[kBatch];
   __shared__ int s_w, s_h, s_tx;
   if (threadIdx.x == 0) {
     s_w = cam_p->width;
@@ -69,6 +79,7 @@ __global__ void __launch_bounds__(kTilePix) composite_kernel(
   const bool inside = x < W && y < H;
   const double ox = (double)(tx * kTile), oy = (double)(ty * kTile);
   const float px = (float)lx, py = (float)ly;
+  const float row_c = (float)(2 * (threadIdx.x >> 5)) + 0.5f;
   const uint2 range = ranges[tile];
   float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
   uint32_t processed = 0;
@@ -76,30 +87,32 @@ __global__ void __launch_bounds__(kTilePix) composite_kernel(
   for (uint32_t base = range.x; base < range.y; base += kBatch) {
     if (__syncthreads_count(done) == kTilePix) break;
     const uint32_t e = base + threadIdx.x;
-    if (e < range.y) {
-      s[threadIdx.x] = stage_splat(rec[ranks[e]], ox, oy);
-    }
+    if (e < range.y) stage_splat(rec[ranks[e]], ox, oy, rc.cutoff2_f, &s_geo[threadIdx.x], &s_app[threadIdx.x], &s_ext[threadIdx.x]);
     __syncthreads();
     const int cnt = min((uint32_t)kBatch, range.y - base);
-    if (!done) {
+    if (!__all_sync(kFull, done)) {
       int k = 0;
       for (; k < cnt; ++k) {
-        const SmemSplat& q = s[k];
-        const float dx = px - q.mx, dy = py - q.my;
-        const float g = splat_power(q, dx, dy);
+        const float4 ge = s_geo[k];
+        const float4 ex = s_ext[k];
+        if (!rows_hit(ge.y, ex.y, row_c)) continue;  // warp-uniform
+        if (done) continue;
+        const float dx = px - ge.x, dy = py - ge.y;
+        const float4 ap = s_app[k];
+        const float g = splat_power(ge.z, ge.w, ap.x, dx, dy);
         if (g > rc.cutoff2_f) continue;
-        const float alpha = fminf(rc.alpha_clamp_f, q.op * __expf(-0.5f * g));
+        const float alpha = fminf(rc.alpha_clamp_f, ap.y * __expf(-0.5f * g));
         const float w = alpha * T;
-        cr = fmaf(q.r, w, cr);
-        cg = fmaf(q.g, w, cg);
-        cb = fmaf(q.b, w, cb);
+        cr = fmaf(ap.z, w, cr);
+        cg = fmaf(ap.w, w, cg);
+        cb = fmaf(ex.x, w, cb);
         T *= (1.0f - alpha);
         if (T < rc.early_term_f) {
           done = true;
-          break;
+          processed = base - range.x + (uint32_t)k + 1u;
         }
       }
-      processed = base - range.x + (done ? (uint32_t)k + 1u : (uint32_t)cnt);
+      if (!done) processed = base - range.x + (uint32_t)cnt;
     }
   }
   if (!inside) return;
@@ -118,21 +131,57 @@ __global__ void __launch_bounds__(kTilePix) composite_kernel(
   pixstate[p] = processed | (of << 29);
 }
 
-__device__ __forceinline__ float warp_sum(float v) {
+// Recursive-halving reduce-scatter of 9 values over a warp (12 shuffles
+// instead of 45): returns the component index this lane ends up owning (or
+// -1) and its warp total in *out. Fixed order, deterministic.
+__device__ __forceinline__ int warp_reduce9(const float v[kPartial], float* out) {
+  const int lane = threadIdx.x & 31;
+  const bool h1 = lane & 16, h2 = lane & 8, h3 = lane & 4, h4 = lane & 2;
+  float w[6];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
+  for (int i = 0; i < 5; ++i) {
+    const float lo = v[i], hi = (i < 4) ? v[5 + i] : 0.f;
+    const float send = h1 ? lo : hi, keep = h1 ? hi : lo;
+    w[i] = keep + __shfl_xor_sync(kFull, send, 16);
+  }
+  w[5] = 0.f;
+  float x[4];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const float lo = w[i], hi = w[3 + i];
+    const float send = h2 ? lo : hi, keep = h2 ? hi : lo;
+    x[i] = keep + __shfl_xor_sync(kFull, send, 8);
+  }
+  x[3] = 0.f;
+  float y[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float lo = x[i], hi = x[2 + i];
+    const float send = h3 ? lo : hi, keep = h3 ? hi : lo;
+    y[i] = keep + __shfl_xor_sync(kFull, send, 4);
+  }
+  float z;
+  {
+    const float send = h4 ? y[0] : y[1], keep = h4 ? y[1] : y[0];
+    z = keep + __shfl_xor_sync(kFull, send, 2);
+  }
+  z += __shfl_xor_sync(kFull, z, 1);
+  const int xi = (h3 ? 2 : 0) + (h4 ? 1 : 0);
+  const int wi = (h2 ? 3 : 0) + xi;
+  const int vi = (h1 ? 5 : 0) + wi;
+  if ((lane & 1) || xi >= 3 || wi >= 5 || vi >= kPartial) return -1;
+  *out = z;
+  return vi;
 }
 
 __global__ void __launch_bounds__(kTilePix) backward_raster_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ ranks, const SplatRec* __restrict__ rec,
     const SplatAux* __restrict__ aux, const CamDev* __restrict__ cam_p, RasterDev rc, float bg_r, float bg_g,
     float bg_b, int64_t npix, const float* __restrict__ d_image, const float* __restrict__ final_t,
-    const uint32_t* __restrict__ pixstate, float* __restrict__ partials) {
-  constexpr int kWarps = kTilePix / 32;
-  __shared__ SmemSplat s[kBatch];
+    const uint32_t* __restrict__ pixstate, float* __restrict__ partials, uint32_t k_cap) {
+  __shared__ float4 s_geo[kBatch], s_app[kBatch], s_ext[kBatch];
   __shared__ uint32_t s_slot[kBatch];
-  __shared__ float s_red[kWarps][kPartial][kBatch / 8 + 1];  // reduced per sub-batch of 32 entries
+  __shared__ float s_red[kWarps][32][kPartial];  // [warp][entry in sub-batch][component]
   __shared__ int s_w, s_h, s_tx;
   __shared__ uint32_t s_maxc[kWarps];
   if (threadIdx.x == 0) {
@@ -140,6 +189,7 @@ __global__ void __launch_bounds__(kTilePix) backward_raster_kernel(
     s_h = cam_p->height;
     s_tx = cam_p->tiles_x;
   }
+  for (int i = threadIdx.x; i < kWarps * 32 * kPartial; i += kTilePix) (&s_red[0][0][0])[i] = 0.f;
   __syncthreads();
   const int W = s_w, H = s_h;
   const int tile = blockIdx.x;
@@ -150,6 +200,7 @@ __global__ void __launch_bounds__(kTilePix) backward_raster_kernel(
   const bool inside = x < W && y < H;
   const double ox = (double)(tx * kTile), oy = (double)(ty * kTile);
   const float px = (float)lx, py = (float)ly;
+  const float row_c = (float)(2 * warp) + 0.5f;
   const uint2 range = ranges[tile];
 
   float dr = 0.f, dg = 0.f, db = 0.f, T = 0.f;
@@ -166,7 +217,7 @@ __global__ void __launch_bounds__(kTilePix) backward_raster_kernel(
     if (dr == 0.f && dg == 0.f && db == 0.f) contrib = 0;  // rasterizer.cpp:372
   }
   float br = bg_r * T, bgg = bg_g * T, bb = bg_b * T;
-  const uint32_t wmax = __reduce_max_sync(0xffffffffu, contrib);
+  const uint32_t wmax = __reduce_max_sync(kFull, contrib);
   if (lane == 0) s_maxc[warp] = wmax;
   __syncthreads();
   uint32_t maxc = 0;
@@ -177,7 +228,7 @@ __global__ void __launch_bounds__(kTilePix) backward_raster_kernel(
   // Batches walk the list from the back; entries past maxc only get zeros.
   const uint32_t nbatch = (len + kBatch - 1) / kBatch;
   for (int bi = (int)nbatch - 1; bi >= 0; --bi) {
-    const uint32_t b0 = (uint32_t)bi * kBatch;                // list-local start
+    const uint32_t b0 = (uint32_t)bi * kBatch;  // list-local start
     const uint32_t cnt = min((uint32_t)kBatch, len - b0);
     __syncthreads();
     if (threadIdx.x < cnt) {
@@ -186,78 +237,78 @@ __global__ void __launch_bounds__(kTilePix) backward_raster_kernel(
       const SplatAux A = aux[r];
       const uint32_t tx0 = A.tx0_ty0 & 0xffffu, ty0 = A.tx0_ty0 >> 16, nx = A.nx_ny & 0xffffu;
       s_slot[threadIdx.x] = A.off + ((uint32_t)ty - ty0) * nx + ((uint32_t)tx - tx0);
-      if (b0 + threadIdx.x < maxc) {
-        s[threadIdx.x] = stage_splat(rec[r], ox, oy);
-      }
+      if (b0 + threadIdx.x < maxc)
+        stage_splat(rec[r], ox, oy, rc.cutoff2_f, &s_geo[threadIdx.x], &s_app[threadIdx.x], &s_ext[threadIdx.x]);
     }
     __syncthreads();
-    const uint32_t active_cnt = b0 < maxc ? min(cnt, maxc - b0) : 0u;
-    // Process entries in sub-batches of 32 (back to front), reducing each
-    // sub-batch's partials into s_red, then flushing them to global.
+    // Sub-batches of 32 entries, back to front; each reduced into s_red, then
+    // flushed (fixed warp order) to the entries' global slots.
     for (int sb = (int)((cnt + 31) / 32) - 1; sb >= 0; --sb) {
       const int k0 = sb * 32;
       const int k1 = min((int)cnt, k0 + 32);
-      for (int k = k1 - 1; k >= k0; --k) {
-        float v[kPartial];
+      if (b0 + (uint32_t)k0 < wmax) {  // this warp has work in the sub-batch
+        for (int k = k1 - 1; k >= k0; --k) {
+          const uint32_t j = b0 + (uint32_t)k;
+          if (j >= wmax) continue;  // warp-uniform
+          const float4 ge = s_geo[k];
+          const float4 ex = s_ext[k];
+          if (!rows_hit(ge.y, ex.y, row_c)) continue;  // warp-uniform
+          float v[kPartial];
 #pragma unroll
-        for (int c = 0; c < kPartial; ++c) v[c] = 0.f;
-        bool hit = false;
-        if ((uint32_t)k < active_cnt && b0 + (uint32_t)k < contrib) {
-          const SmemSplat& q = s[k];
-          const float dx = px - q.mx, dy = py - q.my;
-          const float g = splat_power(q, dx, dy);
-          if (!(g > rc.cutoff2_f)) {
-            const float cx_ = q.ca * dx + q.cb * dy, cy_ = q.cb * dx + q.cc * dy;
-            hit = true;
-            const float G = __expf(-0.5f * g);
-            const float araw = q.op * G;
-            const float alpha = fminf(rc.alpha_clamp_f, araw);
-            const float inv = 1.0f / (1.0f - alpha);
-            const float tb = T * inv;
-            const float wgt = alpha * tb;
-            v[5] = wgt * dr;
-            v[6] = wgt * dg;
-            v[7] = wgt * db;
-            const float dal = dr * (q.r * tb - br * inv) + dg * (q.g * tb - bgg * inv) + db * (q.b * tb - bb * inv);
-            if (araw < rc.alpha_clamp_f) {
-              v[8] = dal * G;
-              const float dgg = dal * (-0.5f * araw);
-              v[0] = -2.0f * dgg * cx_;
-              v[1] = -2.0f * dgg * cy_;
-              v[2] = dgg * dx * dx;
-              v[3] = dgg * dx * dy;
-              v[4] = dgg * dy * dy;
+          for (int c = 0; c < kPartial; ++c) v[c] = 0.f;
+          bool hit = false;
+          if (j < contrib) {
+            const float dx = px - ge.x, dy = py - ge.y;
+            const float4 ap = s_app[k];
+            const float g = splat_power(ge.z, ge.w, ap.x, dx, dy);
+            if (!(g > rc.cutoff2_f)) {
+              hit = true;
+              const float G = __expf(-0.5f * g);
+              const float araw = ap.y * G;
+              const float alpha = fminf(rc.alpha_clamp_f, araw);
+              const float inv = 1.0f / (1.0f - alpha);
+              const float tb = T * inv;
+              const float wgt = alpha * tb;
+              v[5] = wgt * dr;
+              v[6] = wgt * dg;
+              v[7] = wgt * db;
+              const float dal =
+                  dr * (ap.z * tb - br * inv) + dg * (ap.w * tb - bgg * inv) + db * (ex.x * tb - bb * inv);
+              if (araw < rc.alpha_clamp_f) {
+                const float cx_ = ge.z * dx + ge.w * dy, cy_ = ge.w * dx + ap.x * dy;
+                v[8] = dal * G;
+                const float dgg = dal * (-0.5f * araw);
+                v[0] = -2.0f * dgg * cx_;
+                v[1] = -2.0f * dgg * cy_;
+                v[2] = dgg * dx * dx;
+                v[3] = dgg * dx * dy;
+                v[4] = dgg * dy * dy;
+              }
+              T = tb;
+              br = fmaf(ap.z, wgt, br);
+              bgg = fmaf(ap.w, wgt, bgg);
+              bb = fmaf(ex.x, wgt, bb);
             }
-            T = tb;
-            br = fmaf(q.r, wgt, br);
-            bgg = fmaf(q.g, wgt, bgg);
-            bb = fmaf(q.b, wgt, bb);
           }
-        }
-        const int kk = k - k0;
-        if (__any_sync(0xffffffffu, hit)) {
-#pragma unroll
-          for (int c = 0; c < kPartial; ++c) v[c] = warp_sum(v[c]);
-          if (lane == 0) {
-#pragma unroll
-            for (int c = 0; c < kPartial; ++c) s_red[warp][c][kk] = v[c];
+          if (__any_sync(kFull, hit)) {
+            float tot;
+            const int vi = warp_reduce9(v, &tot);
+            if (vi >= 0) s_red[warp][k - k0][vi] = tot;
           }
-        } else if (lane == 0) {
-#pragma unroll
-          for (int c = 0; c < kPartial; ++c) s_red[warp][c][kk] = 0.f;
         }
       }
       __syncthreads();
-      // flush: thread t handles (entry kk = t / 9 ... ) -> 32 entries x 9 comps = 288 values
+      // flush: 32 entries x 9 components, summed over warps 0..7 in order
       for (int idx = threadIdx.x; idx < 32 * kPartial; idx += kTilePix) {
-        const int kk = idx / kPartial, c = idx % kPartial;
+        const int kk = idx / kPartial, c = idx - kk * kPartial;
         const int k = k0 + kk;
-        if (k < k1) {
-          float acc = 0.f;
+        float acc = 0.f;
 #pragma unroll
-          for (int w = 0; w < kWarps; ++w) acc += s_red[w][c][kk];
-          partials[(int64_t)s_slot[k] * kPartial + c] = acc;
+        for (int w = 0; w < kWarps; ++w) {
+          acc += s_red[w][kk][c];
+          s_red[w][kk][c] = 0.f;
         }
+        if (k < k1 && s_slot[k] < k_cap) partials[(int64_t)s_slot[k] * kPartial + c] = acc;
       }
       __syncthreads();
     }
@@ -283,7 +334,8 @@ int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc) {
     backward_raster_kernel<<<n_tiles, kTilePix, 0, st>>>(
         f->ranges.as<uint2>(), f->eval_[f->sorted_sel].as<uint32_t>(), f->rec.as<SplatRec>(), f->aux.as<SplatAux>(),
         f->cam.as<CamDev>(), rc, (float)f->background[0], (float)f->background[1], (float)f->background[2], npix,
-        f->d_image.as<float>(), f->final_t.as<float>(), f->pixstate.as<uint32_t>(), f->partials.as<float>());
+        f->d_image.as<float>(), f->final_t.as<float>(), f->pixstate.as<uint32_t>(), f->partials.as<float>(),
+        (uint32_t)f->k_cap);
   GSB_CHECK_LAUNCH("backward_raster_kernel");
   return GSB_OK;
 }

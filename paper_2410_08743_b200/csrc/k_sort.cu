@@ -15,6 +15,13 @@
 //   5. ranges = [lower_bound(t), lower_bound(t+1)) for every tile.
 // All passes are stable and order preserving, so the tile lists equal the
 // reference's count/prefix/fill output bit for bit on the same FP64 records.
+//
+// Every kernel has a data-independent launch shape (sized by capacities) and
+// reads the live counts (visible splats V, entries K) from device memory, so
+// a whole iteration runs without a host round trip and can be captured in a
+// CUDA graph. Entries beyond the entry capacity are dropped and flagged
+// (K > cap); the pose step then discards the iteration and the host re-runs
+// it with a larger capacity.
 #include "gsb_internal.cuh"
 
 namespace gsb {
@@ -29,6 +36,12 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
+__device__ __forceinline__ int64_t live_count(const uint32_t* n_dev, int64_t cap) {
+  if (!n_dev) return cap;
+  const int64_t v = (int64_t)*n_dev;
+  return v < cap ? v : cap;
+}
+
 template <bool kFlag>
 __device__ __forceinline__ uint32_t scan_load(const uint32_t* in, int64_t i, int64_t n) {
   if (i >= n) return 0u;
@@ -38,12 +51,16 @@ __device__ __forceinline__ uint32_t scan_load(const uint32_t* in, int64_t i, int
 
 // Block sums of 4096-element tiles.
 template <bool kFlag>
-__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_t* __restrict__ in, int64_t n,
+__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_t* __restrict__ in, int64_t cap,
+                                                                    const uint32_t* __restrict__ n_dev,
                                                                     uint32_t* __restrict__ block_sums) {
+  const int64_t n = live_count(n_dev, cap);
   const int64_t base = (int64_t)blockIdx.x * kScanTile;
   uint32_t s = 0;
+  if (base < n) {
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) s += scan_load<kFlag>(in, base + k * kScanThreads + threadIdx.x, n);
+    for (int k = 0; k < kScanItems; ++k) s += scan_load<kFlag>(in, base + k * kScanThreads + threadIdx.x, n);
+  }
   s = __reduce_add_sync(0xffffffffu, s);
   __shared__ uint32_t ws[kScanThreads / 32];
   if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
@@ -65,7 +82,6 @@ __global__ void __launch_bounds__(1024) scan_blocks_kernel(uint32_t* __restrict_
   for (int64_t base = 0; base < nb; base += 1024) {
     const int64_t i = base + threadIdx.x;
     uint32_t v = i < nb ? sums[i] : 0u;
-    // inclusive warp scan
     uint32_t x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -81,7 +97,7 @@ __global__ void __launch_bounds__(1024) scan_blocks_kernel(uint32_t* __restrict_
         uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
         if (threadIdx.x >= o) w += y;
       }
-      wsum[threadIdx.x] = w;  // inclusive
+      wsum[threadIdx.x] = w;
     }
     __syncthreads();
     const uint32_t warp_excl = (threadIdx.x >> 5) ? wsum[(threadIdx.x >> 5) - 1] : 0u;
@@ -100,18 +116,20 @@ __global__ void __launch_bounds__(1024) scan_blocks_kernel(uint32_t* __restrict_
 // Block-local exclusive scan plus block offset. Items are striped
 // (k*256 + tid) for coalescing; the scan order is the global index order.
 template <bool kFlag>
-__global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t* __restrict__ in, int64_t n,
+__global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t* __restrict__ in, int64_t cap,
+                                                                   const uint32_t* __restrict__ n_dev,
                                                                    const uint32_t* __restrict__ block_offs,
                                                                    uint32_t* __restrict__ out) {
-  __shared__ uint32_t tile[kScanTile + kScanTile / 32];
+  const int64_t n = live_count(n_dev, cap);
   const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  if (base >= n) return;
+  __shared__ uint32_t tile[kScanTile + kScanTile / 32];
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
     const int idx = k * kScanThreads + threadIdx.x;
     tile[idx + (idx >> 5)] = scan_load<kFlag>(in, base + idx, n);
   }
   __syncthreads();
-  // thread t owns items [t*16, t*16+16)
   uint32_t local[kScanItems];
   uint32_t s = 0;
 #pragma unroll
@@ -146,21 +164,23 @@ __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t
   }
 }
 
-static size_t scan_scratch_words(int64_t n) { return (size_t)((n + kScanTile - 1) / kScanTile) + 2; }
+static int64_t scan_blocks_for(int64_t cap) { return (cap + kScanTile - 1) / kScanTile; }
+size_t scan_words(int64_t cap) { return (size_t)scan_blocks_for(cap) + 2; }
 
-// Exclusive scan of n u32 values (or of the flags v > 0 when flag) into out.
-// total (device u32*) receives the sum. scratch must hold scan_scratch_words(n).
-int scan_exclusive(cudaStream_t st, const uint32_t* in, int64_t n, bool flag, uint32_t* out, uint32_t* scratch,
-                   uint32_t* total, int64_t* launches) {
-  const int64_t nb = (n + kScanTile - 1) / kScanTile;
+// Exclusive scan of the live prefix (n_dev, capped at cap; n_dev may be
+// NULL = cap) of u32 values — or of the flags v > 0 — into out. *total
+// (device) receives the sum. Launch shape depends on cap only.
+int scan_exclusive(cudaStream_t st, const uint32_t* in, int64_t cap, const uint32_t* n_dev, bool flag, uint32_t* out,
+                   uint32_t* scratch, uint32_t* total, int64_t* launches) {
+  const int64_t nb = scan_blocks_for(cap);
   if (nb > 0) {
-    if (flag) scan_reduce_kernel<true><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, scratch);
-    else scan_reduce_kernel<false><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, scratch);
+    if (flag) scan_reduce_kernel<true><<<(unsigned)nb, kScanThreads, 0, st>>>(in, cap, n_dev, scratch);
+    else scan_reduce_kernel<false><<<(unsigned)nb, kScanThreads, 0, st>>>(in, cap, n_dev, scratch);
   }
   scan_blocks_kernel<<<1, 1024, 0, st>>>(scratch, nb, total);
   if (nb > 0) {
-    if (flag) scan_apply_kernel<true><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, scratch, out);
-    else scan_apply_kernel<false><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, scratch, out);
+    if (flag) scan_apply_kernel<true><<<(unsigned)nb, kScanThreads, 0, st>>>(in, cap, n_dev, scratch, out);
+    else scan_apply_kernel<false><<<(unsigned)nb, kScanThreads, 0, st>>>(in, cap, n_dev, scratch, out);
   }
   *launches += nb > 0 ? 3 : 1;
   GSB_CHECK_LAUNCH("scan_exclusive");
@@ -172,19 +192,23 @@ constexpr int kRadixThreads = 256;
 constexpr int kRadixRounds = 16;
 constexpr int kRadixTile = kRadixThreads * kRadixRounds;  // 4096 items per block
 
-__global__ void __launch_bounds__(kRadixThreads) radix_hist_kernel(const uint32_t* __restrict__ keys, int64_t n,
-                                                                   int shift, int bits,
-                                                                   uint32_t* __restrict__ hist, int64_t nblocks) {
+__global__ void __launch_bounds__(kRadixThreads) radix_hist_kernel(const uint32_t* __restrict__ keys, int64_t cap,
+                                                                   const uint32_t* __restrict__ n_dev, int shift,
+                                                                   int bits, uint32_t* __restrict__ hist,
+                                                                   int64_t nblocks) {
   __shared__ uint32_t h[256];
+  const int64_t n = live_count(n_dev, cap);
   const int ndig = 1 << bits;
   if (threadIdx.x < ndig) h[threadIdx.x] = 0;
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * kRadixTile;
   const uint32_t mask = (uint32_t)ndig - 1u;
+  if (base < n) {
 #pragma unroll 4
-  for (int k = 0; k < kRadixRounds; ++k) {
-    const int64_t i = base + k * kRadixThreads + threadIdx.x;
-    if (i < n) atomicAdd(&h[(keys[i] >> shift) & mask], 1u);
+    for (int k = 0; k < kRadixRounds; ++k) {
+      const int64_t i = base + k * kRadixThreads + threadIdx.x;
+      if (i < n) atomicAdd(&h[(keys[i] >> shift) & mask], 1u);
+    }
   }
   __syncthreads();
   if (threadIdx.x < ndig) hist[(int64_t)threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
@@ -194,12 +218,15 @@ __global__ void __launch_bounds__(kRadixThreads) radix_hist_kernel(const uint32_
 // within a round ranks come from warp match + cross-warp prefix.
 __global__ void __launch_bounds__(kRadixThreads) radix_scatter_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
-    uint32_t* __restrict__ vals_out, int64_t n, int shift, int bits, const uint32_t* __restrict__ offs,
-    int64_t nblocks) {
+    uint32_t* __restrict__ vals_out, int64_t cap, const uint32_t* __restrict__ n_dev, int shift, int bits,
+    const uint32_t* __restrict__ offs, int64_t nblocks) {
   constexpr int kWarps = kRadixThreads / 32;
   __shared__ uint32_t warp_cnt[kWarps][256];
   __shared__ uint32_t warp_off[kWarps][256];
   __shared__ uint32_t digit_run[256];
+  const int64_t n = live_count(n_dev, cap);
+  const int64_t base = (int64_t)blockIdx.x * kRadixTile;
+  if (base >= n) return;
   const int ndig = 1 << bits;
   const uint32_t mask = (uint32_t)ndig - 1u;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -208,7 +235,6 @@ __global__ void __launch_bounds__(kRadixThreads) radix_scatter_kernel(
     for (int w = 0; w < kWarps; ++w) warp_cnt[w][d] = 0;
   }
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * kRadixTile;
   const uint32_t lt = lanemask_lt();
   for (int k = 0; k < kRadixRounds; ++k) {
     const int64_t i = base + k * kRadixThreads + threadIdx.x;
@@ -244,26 +270,30 @@ __global__ void __launch_bounds__(kRadixThreads) radix_scatter_kernel(
   }
 }
 
-// Sorts (keys, vals) by key bits [0, total_bits) stably. Buffers [0] hold the
-// input; returns the index (0/1) of the buffer holding the result.
-int radix_sort_pairs(cudaStream_t st, uint32_t* keys[2], uint32_t* vals[2], int64_t n, int total_bits,
-                     uint32_t* hist, int* result_sel, int64_t* launches) {
+static int radix_passes(int total_bits) { return total_bits <= 0 ? 0 : (total_bits + 7) / 8; }
+
+// Sorts (keys, vals)[0..live) by key bits [0, total_bits) stably. Buffers [0]
+// hold the input; *result_sel receives the buffer index holding the result
+// (fixed by total_bits, hence graph-stable).
+int radix_sort_pairs(cudaStream_t st, uint32_t* keys[2], uint32_t* vals[2], int64_t cap, const uint32_t* n_dev,
+                     int total_bits, uint32_t* hist, int* result_sel, int64_t* launches) {
   int sel = 0;
-  if (n <= 1 || total_bits <= 0) {
+  const int passes = radix_passes(total_bits);
+  if (cap <= 1 || passes == 0) {
     *result_sel = 0;
     return GSB_OK;
   }
-  const int passes = (total_bits + 7) / 8;
   const int bits = (total_bits + passes - 1) / passes;
-  const int64_t nblocks = (n + kRadixTile - 1) / kRadixTile;
+  const int64_t nblocks = (cap + kRadixTile - 1) / kRadixTile;
   const int64_t nh = (int64_t)(1 << bits) * nblocks;
   for (int p = 0; p < passes; ++p) {
     const int shift = p * bits;
-    radix_hist_kernel<<<(unsigned)nblocks, kRadixThreads, 0, st>>>(keys[sel], n, shift, bits, hist, nblocks);
-    int rc = scan_exclusive(st, hist, nh, false, hist, hist + nh, nullptr, launches);
+    radix_hist_kernel<<<(unsigned)nblocks, kRadixThreads, 0, st>>>(keys[sel], cap, n_dev, shift, bits, hist, nblocks);
+    int rc = scan_exclusive(st, hist, nh, nullptr, false, hist, hist + nh, nullptr, launches);
     if (rc) return rc;
     radix_scatter_kernel<<<(unsigned)nblocks, kRadixThreads, 0, st>>>(keys[sel], vals[sel], keys[sel ^ 1],
-                                                                      vals[sel ^ 1], n, shift, bits, hist, nblocks);
+                                                                      vals[sel ^ 1], cap, n_dev, shift, bits, hist,
+                                                                      nblocks);
     *launches += 2;
     sel ^= 1;
   }
@@ -272,15 +302,14 @@ int radix_sort_pairs(cudaStream_t st, uint32_t* keys[2], uint32_t* vals[2], int6
   return GSB_OK;
 }
 
-size_t radix_hist_words(int64_t n, int total_bits) {
-  if (total_bits <= 0) return 16;
-  const int passes = (total_bits + 7) / 8;
+size_t radix_hist_words(int64_t cap, int total_bits) {
+  const int passes = radix_passes(total_bits);
+  if (passes == 0) return 16;
   const int bits = (total_bits + passes - 1) / passes;
-  const int64_t nblocks = (n + kRadixTile - 1) / kRadixTile;
+  const int64_t nblocks = (cap + kRadixTile - 1) / kRadixTile;
   const int64_t nh = (int64_t)(1 << bits) * nblocks;
-  return (size_t)nh + scan_scratch_words(nh) + 16;
+  return (size_t)nh + scan_words(nh) + 16;
 }
-size_t scan_words(int64_t n) { return scan_scratch_words(n); }
 
 // ---------------------------------------------------- compaction + ranks
 // vis_pos = exclusive scan of (cnt_g > 0). Emits visible slot v -> gid and
@@ -300,15 +329,16 @@ __global__ void compact_kernel(const uint32_t* __restrict__ cnt_g, const uint32_
 // equal doubles keep visible-slot order = Gaussian index order).
 __global__ void depth_tie_fix_kernel(const uint32_t* __restrict__ key, uint32_t* __restrict__ val,
                                      const uint32_t* __restrict__ vis_idx, const double* __restrict__ depth_g,
-                                     int64_t n) {
+                                     int64_t cap, const uint32_t* __restrict__ nv_dev) {
+  const int64_t n = live_count(nv_dev, cap);
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const uint32_t k = key[r];
-  if (r > 0 && key[r - 1] == k) return;           // not a run start
-  if (r + 1 >= n || key[r + 1] != k) return;      // singleton
+  if (r > 0 && key[r - 1] == k) return;       // not a run start
+  if (r + 1 >= n || key[r + 1] != k) return;  // singleton
   int64_t end = r + 1;
   while (end < n && key[end] == k) ++end;
-  for (int64_t a = r + 1; a < end; ++a) {         // insertion sort by FP64 depth
+  for (int64_t a = r + 1; a < end; ++a) {     // insertion sort by FP64 depth
     const uint32_t v = val[a];
     const double d = depth_g[vis_idx[v]];
     int64_t b = a - 1;
@@ -323,9 +353,10 @@ __global__ void depth_tie_fix_kernel(const uint32_t* __restrict__ key, uint32_t*
 // Rank-order records: rank r holds visible slot sorted_v[r].
 __global__ void gather_ranks_kernel(const uint32_t* __restrict__ sorted_v, const uint32_t* __restrict__ vis_idx,
                                     const SplatRec* __restrict__ rec_g, const uint2* __restrict__ rect_g,
-                                    const uint32_t* __restrict__ cnt_g, int64_t nv, SplatRec* __restrict__ rec,
-                                    SplatAux* __restrict__ aux, uint32_t* __restrict__ cnt_r,
+                                    const uint32_t* __restrict__ cnt_g, int64_t cap, const uint32_t* __restrict__ nv_dev,
+                                    SplatRec* __restrict__ rec, SplatAux* __restrict__ aux, uint32_t* __restrict__ cnt_r,
                                     int32_t* __restrict__ rank_of_g) {
+  const int64_t nv = live_count(nv_dev, cap);
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nv) return;
   const uint32_t gid = vis_idx[sorted_v[r]];
@@ -338,33 +369,40 @@ __global__ void gather_ranks_kernel(const uint32_t* __restrict__ sorted_v, const
   a.nx_ny = (tx1 - tx0 + 1u) | ((ty1 - ty0 + 1u) << 16);
   a.gid = (int32_t)gid;
   aux[r] = a;
-  cnt_r[r] = cnt_g[gid];
+  cnt_r[r] = cnt_g[gid] & kCntMask;
   rank_of_g[gid] = (int32_t)r;
 }
 
 // Emits (tile, rank) for every tile of every splat, rank-major and row-major
 // inside the rect — the reference fill order (rasterizer.cpp:163-167).
-__global__ void duplicate_kernel(const uint32_t* __restrict__ offs, SplatAux* __restrict__ aux, int64_t nv,
-                                 int tiles_x, uint32_t* __restrict__ ekey, uint32_t* __restrict__ eval) {
+// Entries at or beyond k_cap are dropped (the iteration is then discarded).
+__global__ void duplicate_kernel(const uint32_t* __restrict__ offs, SplatAux* __restrict__ aux, int64_t cap,
+                                 const uint32_t* __restrict__ nv_dev, int tiles_x, int64_t k_cap,
+                                 uint32_t* __restrict__ ekey, uint32_t* __restrict__ eval,
+                                 uint32_t* __restrict__ off_g) {
+  const int64_t nv = live_count(nv_dev, cap);
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nv) return;
   const uint32_t off = offs[r];
-  SplatAux a = aux[r];
+  const SplatAux a = aux[r];
   aux[r].off = off;
+  off_g[a.gid] = off;
   const uint32_t tx0 = a.tx0_ty0 & 0xffffu, ty0 = a.tx0_ty0 >> 16;
   const uint32_t nx = a.nx_ny & 0xffffu, ny = a.nx_ny >> 16;
-  uint32_t j = off;
+  int64_t j = off;
   for (uint32_t y = 0; y < ny; ++y) {
     const uint32_t row = (ty0 + y) * (uint32_t)tiles_x + tx0;
     for (uint32_t x = 0; x < nx; ++x, ++j) {
+      if (j >= k_cap) return;
       ekey[j] = row + x;
       eval[j] = (uint32_t)r;
     }
   }
 }
 
-__global__ void tile_ranges_kernel(const uint32_t* __restrict__ ekey, int64_t k, int n_tiles,
-                                   uint2* __restrict__ ranges) {
+__global__ void tile_ranges_kernel(const uint32_t* __restrict__ ekey, int64_t k_cap, const uint32_t* __restrict__ k_dev,
+                                   int n_tiles, uint2* __restrict__ ranges) {
+  const int64_t k = live_count(k_dev, k_cap);
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_tiles) return;
   auto lower = [&](uint32_t v) {
@@ -380,35 +418,39 @@ __global__ void tile_ranges_kernel(const uint32_t* __restrict__ ekey, int64_t k,
 }
 
 // ------------------------------------------------------------ host glue
-int launch_compact(cudaStream_t st, const uint32_t* cnt_g, const uint32_t* vis_pos, const double* depth_g,
-                   int64_t n, uint32_t* vis_idx, uint32_t* dkey, uint32_t* dval) {
+int launch_compact(cudaStream_t st, const uint32_t* cnt_g, const uint32_t* vis_pos, const double* depth_g, int64_t n,
+                   uint32_t* vis_idx, uint32_t* dkey, uint32_t* dval) {
   if (n > 0) compact_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(cnt_g, vis_pos, depth_g, n, vis_idx, dkey, dval);
   GSB_CHECK_LAUNCH("compact_kernel");
   return GSB_OK;
 }
 int launch_depth_tie_fix(cudaStream_t st, const uint32_t* key, uint32_t* val, const uint32_t* vis_idx,
-                         const double* depth_g, int64_t nv) {
-  if (nv > 1) depth_tie_fix_kernel<<<(unsigned)((nv + 255) / 256), 256, 0, st>>>(key, val, vis_idx, depth_g, nv);
+                         const double* depth_g, int64_t cap, const uint32_t* nv_dev) {
+  if (cap > 1)
+    depth_tie_fix_kernel<<<(unsigned)((cap + 255) / 256), 256, 0, st>>>(key, val, vis_idx, depth_g, cap, nv_dev);
   GSB_CHECK_LAUNCH("depth_tie_fix_kernel");
   return GSB_OK;
 }
 int launch_gather_ranks(cudaStream_t st, const uint32_t* sorted_v, const uint32_t* vis_idx, const SplatRec* rec_g,
-                        const uint2* rect_g, const uint32_t* cnt_g, int64_t nv, SplatRec* rec, SplatAux* aux,
-                        uint32_t* cnt_r, int32_t* rank_of_g) {
-  if (nv > 0)
-    gather_ranks_kernel<<<(unsigned)((nv + 255) / 256), 256, 0, st>>>(sorted_v, vis_idx, rec_g, rect_g, cnt_g, nv, rec,
-                                                                      aux, cnt_r, rank_of_g);
+                        const uint2* rect_g, const uint32_t* cnt_g, int64_t cap, const uint32_t* nv_dev, SplatRec* rec,
+                        SplatAux* aux, uint32_t* cnt_r, int32_t* rank_of_g) {
+  if (cap > 0)
+    gather_ranks_kernel<<<(unsigned)((cap + 255) / 256), 256, 0, st>>>(sorted_v, vis_idx, rec_g, rect_g, cnt_g, cap,
+                                                                       nv_dev, rec, aux, cnt_r, rank_of_g);
   GSB_CHECK_LAUNCH("gather_ranks_kernel");
   return GSB_OK;
 }
-int launch_duplicate(cudaStream_t st, const uint32_t* offs, SplatAux* aux, int64_t nv, int tiles_x, uint32_t* ekey,
-                     uint32_t* eval) {
-  if (nv > 0) duplicate_kernel<<<(unsigned)((nv + 255) / 256), 256, 0, st>>>(offs, aux, nv, tiles_x, ekey, eval);
+int launch_duplicate(cudaStream_t st, const uint32_t* offs, SplatAux* aux, int64_t cap, const uint32_t* nv_dev,
+                     int tiles_x, int64_t k_cap, uint32_t* ekey, uint32_t* eval, uint32_t* off_g) {
+  if (cap > 0)
+    duplicate_kernel<<<(unsigned)((cap + 255) / 256), 256, 0, st>>>(offs, aux, cap, nv_dev, tiles_x, k_cap, ekey, eval,
+                                                                    off_g);
   GSB_CHECK_LAUNCH("duplicate_kernel");
   return GSB_OK;
 }
-int launch_tile_ranges(cudaStream_t st, const uint32_t* ekey, int64_t k, int n_tiles, uint2* ranges) {
-  if (n_tiles > 0) tile_ranges_kernel<<<(n_tiles + 255) / 256, 256, 0, st>>>(ekey, k, n_tiles, ranges);
+int launch_tile_ranges(cudaStream_t st, const uint32_t* ekey, int64_t k_cap, const uint32_t* k_dev, int n_tiles,
+                       uint2* ranges) {
+  if (n_tiles > 0) tile_ranges_kernel<<<(n_tiles + 255) / 256, 256, 0, st>>>(ekey, k_cap, k_dev, n_tiles, ranges);
   GSB_CHECK_LAUNCH("tile_ranges_kernel");
   return GSB_OK;
 }

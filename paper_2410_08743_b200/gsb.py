@@ -164,6 +164,8 @@ def _sigs():
         "gsb_session_step": (C.c_int, [_vp, _vp, i32]),
         "gsb_session_read": (C.c_int, [_vp, _vp, _vp, P(d), P(i32), P(i32), P(i32)]),
         "gsb_session_frame_info": (C.c_int, [_vp, P(FrameInfo)]),
+        "gsb_session_step_async": (C.c_int, [_vp, _vp, i32]),
+        "gsb_session_stage_times": (C.c_int, [_vp, _vp]),
     }
 
 
@@ -465,6 +467,14 @@ class PoseSession:
 
     def step(self, iterations: int = 1):
         _check(lib().gsb_session_step(self.ctx.h, self.h, iterations))
+
+    def step_async(self, iterations: int = 1):
+        _check(lib().gsb_session_step_async(self.ctx.h, self.h, iterations))
+
+    def stage_times(self) -> dict:
+        ms = np.zeros(8)
+        _check(lib().gsb_session_stage_times(self.h, _p(ms)))
+        return {k: float(ms[i]) for i, k in enumerate(Context.STAGES)}
 
     def read(self) -> dict:
         pose, best = np.zeros(12), np.zeros(12)
