@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -24,6 +25,12 @@ size_t scan_words(int64_t n);
 int radix_sort_pairs(cudaStream_t st, uint32_t* keys[2], uint32_t* vals[2], int64_t cap, const uint32_t* n_dev,
                      int total_bits, uint32_t* hist, int* result_sel, int64_t* launches);
 size_t radix_hist_words(int64_t n, int total_bits);
+int scan_onepass(cudaStream_t st, const uint32_t* in, int64_t cap, const uint32_t* n_dev, bool flag, uint32_t* out,
+                 uint32_t* status, uint32_t* total, int64_t* launches);
+size_t scan_onepass_words(int64_t cap);
+int onesweep_sort_pairs(cudaStream_t st, uint32_t* keys[2], uint32_t* vals[2], int64_t cap, const uint32_t* n_dev,
+                        int total_bits, uint32_t* ws, int* result_sel, int64_t* launches);
+size_t onesweep_words(int64_t cap, int total_bits);
 int launch_compact(cudaStream_t st, const uint32_t* cnt_g, const uint32_t* vis_pos, const double* depth_g, int64_t n,
                    uint32_t* vis_idx, uint32_t* dkey, uint32_t* dval);
 int launch_depth_tie_fix(cudaStream_t st, const uint32_t* key, uint32_t* val, const uint32_t* vis_idx,
@@ -254,6 +261,29 @@ static int read_counters(gsb_ctx* ctx, const uint32_t* dev, uint32_t* host, int 
   return GSB_OK;
 }
 
+// K2 primitives: reduce-then-scan scans and hist/scan/scatter LSD passes
+// (default), or single-pass decoupled-lookback scan / Onesweep sort
+// (GSB_SORT=onesweep). Both produce bit-identical results; on B200 at these
+// sizes the whole-wave look-back chains make Onesweep slower (measured
+// 0.48 vs 0.31 ms per sort stage), so it stays opt-in for A/B measurement.
+static bool legacy_sort() {
+  static const bool legacy = [] {
+    const char* e = std::getenv("GSB_SORT");
+    return !(e && std::strcmp(e, "onesweep") == 0);
+  }();
+  return legacy;
+}
+static int scan_any(cudaStream_t st, const uint32_t* in, int64_t cap, const uint32_t* n_dev, bool flag, uint32_t* out,
+                    uint32_t* scratch, uint32_t* total, int64_t* launches) {
+  return legacy_sort() ? scan_exclusive(st, in, cap, n_dev, flag, out, scratch, total, launches)
+                       : scan_onepass(st, in, cap, n_dev, flag, out, scratch, total, launches);
+}
+static int sort_any(cudaStream_t st, uint32_t* keys[2], uint32_t* vals[2], int64_t cap, const uint32_t* n_dev,
+                    int bits, uint32_t* ws, int* sel, int64_t* launches) {
+  return legacy_sort() ? radix_sort_pairs(st, keys, vals, cap, n_dev, bits, ws, sel, launches)
+                       : onesweep_sort_pairs(st, keys, vals, cap, n_dev, bits, ws, sel, launches);
+}
+
 static int tile_bits(int n_tiles) {
   int bits = 0;
   while ((1 << bits) < n_tiles) ++bits;
@@ -290,8 +320,9 @@ static int frame_reserve(gsb_frame* f, const gsb_cloud* cloud, int64_t k_cap) {
   }
   GSB_CUDA(f->rec.reserve(sizeof(SplatRec) * n, &grew));
   GSB_CUDA(f->aux.reserve(sizeof(SplatAux) * n, &grew));
-  GSB_CUDA(f->scan_tmp.reserve(sizeof(uint32_t) * (scan_words(n) + 64), &grew));
-  const size_t hist = std::max(radix_hist_words(n, 32), radix_hist_words(k_cap, tile_bits(n_tiles)));
+  GSB_CUDA(f->scan_tmp.reserve(sizeof(uint32_t) * (std::max(scan_onepass_words(n), scan_words(n)) + 64), &grew));
+  const size_t hist = std::max(std::max(onesweep_words(n, 32), onesweep_words(k_cap, tile_bits(n_tiles))),
+                               std::max(radix_hist_words(n, 32), radix_hist_words(k_cap, tile_bits(n_tiles))));
   GSB_CUDA(f->sort_hist.reserve(sizeof(uint32_t) * hist, &grew));
   GSB_CUDA(f->ranges.reserve(sizeof(uint2) * n_tiles, &grew));
   GSB_CUDA(f->image.reserve(sizeof(float) * 3 * npix, &grew));
@@ -325,8 +356,8 @@ static int render_async(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, cons
   {
     StageScope sc(ctx, kStSort);
     // 1. compaction in index order (visible slot of Gaussian i -> cnt_r[i])
-    if (int r = scan_exclusive(st, f->cnt_g.as<uint32_t>(), n, nullptr, true, f->cnt_r.as<uint32_t>(),
-                               f->scan_tmp.as<uint32_t>(), counters + 0, &ctx->launches))
+    if (int r = scan_any(st, f->cnt_g.as<uint32_t>(), n, nullptr, true, f->cnt_r.as<uint32_t>(),
+                         f->scan_tmp.as<uint32_t>(), counters + 0, &ctx->launches))
       return r;
     if (int r = launch_compact(st, f->cnt_g.as<uint32_t>(), f->cnt_r.as<uint32_t>(), f->depth_g.as<double>(), n,
                                f->vis_idx.as<uint32_t>(), f->dkey[0].as<uint32_t>(), f->dval[0].as<uint32_t>()))
@@ -336,7 +367,7 @@ static int render_async(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, cons
     uint32_t* dk[2] = {f->dkey[0].as<uint32_t>(), f->dkey[1].as<uint32_t>()};
     uint32_t* dv[2] = {f->dval[0].as<uint32_t>(), f->dval[1].as<uint32_t>()};
     int sel = 0;
-    if (int r = radix_sort_pairs(st, dk, dv, n, counters + 0, 32, f->sort_hist.as<uint32_t>(), &sel, &ctx->launches))
+    if (int r = sort_any(st, dk, dv, n, counters + 0, 32, f->sort_hist.as<uint32_t>(), &sel, &ctx->launches))
       return r;
     if (int r = launch_depth_tie_fix(st, dk[sel], dv[sel], f->vis_idx.as<uint32_t>(), f->depth_g.as<double>(), n,
                                      counters + 0))
@@ -350,8 +381,8 @@ static int render_async(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, cons
       return r;
     ctx->launches += n > 0 ? 1 : 0;
     uint32_t* offs = dk[sel ^ 1];
-    if (int r = scan_exclusive(st, f->cnt_r.as<uint32_t>(), n, counters + 0, false, offs, f->scan_tmp.as<uint32_t>(),
-                               counters + 1, &ctx->launches))
+    if (int r = scan_any(st, f->cnt_r.as<uint32_t>(), n, counters + 0, false, offs, f->scan_tmp.as<uint32_t>(),
+                         counters + 1, &ctx->launches))
       return r;
     // 4. duplicate (tile, rank) entries, stable sort by tile, ranges
     if (int r = launch_duplicate(st, offs, f->aux.as<SplatAux>(), n, counters + 0, f->tiles_x, f->k_cap,
@@ -361,8 +392,8 @@ static int render_async(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, cons
     uint32_t* ek[2] = {f->ekey[0].as<uint32_t>(), f->ekey[1].as<uint32_t>()};
     uint32_t* ev[2] = {f->eval_[0].as<uint32_t>(), f->eval_[1].as<uint32_t>()};
     int esel = 0;
-    if (int r = radix_sort_pairs(st, ek, ev, f->k_cap, counters + 1, tile_bits(n_tiles), f->sort_hist.as<uint32_t>(),
-                                 &esel, &ctx->launches))
+    if (int r = sort_any(st, ek, ev, f->k_cap, counters + 1, tile_bits(n_tiles), f->sort_hist.as<uint32_t>(), &esel,
+                         &ctx->launches))
       return r;
     f->sorted_sel = esel;
     if (int r = launch_tile_ranges(st, ek[esel], f->k_cap, counters + 1, n_tiles, f->ranges.as<uint2>())) return r;

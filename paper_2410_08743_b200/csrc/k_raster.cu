@@ -1,51 +1,84 @@
 // k_raster.cu — K3 front-to-back compositing and K4a back-to-front backward
-// raster. One CTA per 16x16 tile, one thread per pixel (warp w owns tile
-// rows 2w, 2w+1); splat records are staged through shared memory in batches
-// of 256 (one record per thread per batch, gathered by rank), so each record
-// is read from L2/HBM once per tile.
+// raster. One 128-thread CTA per 16x16 tile; the four warps own the tile's
+// four 8x8 quadrants and every thread owns two vertically adjacent pixels.
+// Splat records are staged through shared memory in batches of 128 (one
+// record per thread, gathered by rank), so each record is read from L2/HBM
+// once per tile. While staging, each record gets a 4-bit mask of the
+// quadrants its cutoff ellipse's bounding box touches; each warp then
+// compacts (ballot + popc) the batch into its own list and iterates only
+// those entries, so splats that miss a quadrant cost that warp nothing.
 //
 // K3 restates render's compositing loop (rasterizer.cpp:234-279):
 // integer pixel centres (245), processed counter set before the cutoff test
 // (251), hard g > cutoff^2 skip (254), alpha = min(clamp, o e^{-g/2}) (255),
 // break after including the splat once T < early_termination (258), colour
-// clamp at 1 with overflow bits (262-268).
+// clamp at 1 with overflow bits (262-268). The quadrant skip is exact: every
+// pixel outside the bounding box of {g <= cutoff^2} fails the test anyway.
 //
 // K4a restates phase 1 of render_backward (rasterizer.cpp:354-405): per
 // pixel back-to-front replay from contrib_count-1 with t_before = T/(1-a),
 // clamped channels zeroed, alpha-chain gradients only when a_raw < clamp.
-// The per-(pixel, splat) partials are reduced over the tile's 256 pixels in
-// a fixed order (warp recursive-halving reduce-scatter, then warps 0..7) and
-// written — zero when untouched — to the entry's slot in the rank-major
-// (pre-sort) stream, so K4b reads each splat's partials contiguously and in
-// tile order (phase 2's per-splat order, rasterizer.cpp:410-418). No
-// atomics: deterministic.
-//
-// Both kernels skip a staged splat warp-uniformly when its cutoff ellipse
-// (|dy| <= cutoff * sqrt(Sigma_yy), Sigma = conic^-1, with a safety margin)
-// misses the warp's two pixel rows: every pixel of such a warp would fail the
-// g <= cutoff^2 test, so the result is unchanged.
+// Per-(pixel, splat) partials are reduced over the tile's 256 pixels in a
+// fixed order (the thread's two pixels, a warp recursive-halving
+// reduce-scatter, then warps 0..3) and written — zero when untouched — to
+// the entry's slot in the rank-major (pre-sort) stream, so K4b reads each
+// splat's partials contiguously and in tile order (phase 2's per-splat
+// order, rasterizer.cpp:410-418). No atomics: deterministic.
 #include "gsb_internal.cuh"
 
 namespace gsb {
 
-constexpr int kBatch = 256;
-constexpr int kWarps = kTilePix / 32;
+constexpr int kThreads = 128;          // 2 pixels per thread
+constexpr int kBatch = kThreads;       // records staged per batch
+constexpr int kWarps = kThreads / 32;  // 4 warps = 4 quadrants of 8x8
 constexpr unsigned kFull = 0xffffffffu;
 
-struct Staged {
-  float4 geo;  // tile-local mean x, y; conic a, b
-  float4 app;  // conic c, opacity, colour r, g
-  float4 ext;  // colour b, ellipse half-height (with margin), -, -
-};
+__device__ __forceinline__ uint32_t lanemask_lt_() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
 
-__device__ __forceinline__ void stage_splat(const SplatRec& R, double ox, double oy, float cutoff2, float4* geo,
-                                            float4* app, float4* ext) {
+// Stages one record (tile-local mean, conic, opacity, colour) and returns the
+// mask of quadrants whose rectangle meets the bounding box of the cutoff
+// ellipse: |dx| <= sqrt(cutoff2 Sigma_xx), |dy| <= sqrt(cutoff2 Sigma_yy),
+// Sigma = conic^-1 (with a safety margin against FP32 rounding of g).
+__device__ __forceinline__ uint32_t stage_splat(const SplatRec& R, double ox, double oy, float cutoff2, float4* geo,
+                                                float4* app, float* col_b) {
   const float a = R.conic_a, b = R.conic_b, c = R.conic_c;
   const float det = a * c - b * b;
-  const float half_h = sqrtf(cutoff2 * a / det) * 1.001f + 1e-3f;  // |dy| bound of g <= cutoff2
-  *geo = make_float4((float)(R.mu_x - ox), (float)(R.mu_y - oy), a, b);
+  const float hw = sqrtf(cutoff2 * c / det) * 1.001f + 1e-2f;
+  const float hh = sqrtf(cutoff2 * a / det) * 1.001f + 1e-2f;
+  const float mx = (float)(R.mu_x - ox), my = (float)(R.mu_y - oy);
+  *geo = make_float4(mx, my, a, b);
   *app = make_float4(c, R.opacity, R.col_r, R.col_g);
-  *ext = make_float4(R.col_b, half_h, 0.f, 0.f);
+  *col_b = R.col_b;
+  if (!(det > 0.f) || !(hw < 1e30f) || !(hh < 1e30f)) return 0xfu;  // degenerate in FP32: test every pixel
+  uint32_t mask = 0;
+  const bool x0 = mx - hw <= 7.0f, x1 = mx + hw >= 8.0f;   // quadrant columns [0,7], [8,15]
+  const bool y0 = my - hh <= 7.0f, y1 = my + hh >= 8.0f;
+  const bool xin = mx + hw >= 0.0f && mx - hw <= 15.0f, yin = my + hh >= 0.0f && my - hh <= 15.0f;
+  if (!(xin && yin)) return 0u;
+  if (x0 && y0) mask |= 1u;
+  if (x1 && y0) mask |= 2u;
+  if (x0 && y1) mask |= 4u;
+  if (x1 && y1) mask |= 8u;
+  return mask;
+}
+
+// exp(-g/2) and 1/x via the MUFU approximations with flush-to-zero: the
+// arguments never reach the denormal range here (g <= cutoff^2, 1 - alpha >=
+// 1 - alpha_clamp), so the non-FTZ fix-up code around MUFU is dead weight.
+// Forward and backward use the same helper, so their decisions agree.
+__device__ __forceinline__ float exp_neg_half(float g) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(g * -0.7213475204444817f));
+  return y;
+}
+__device__ __forceinline__ float rcp_fast(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 // Mahalanobis power g = d^T conic d. Forward and backward must take the
@@ -54,16 +87,79 @@ __device__ __forceinline__ float splat_power(float ca, float cb, float cc, float
   return fmaf(ca * dx, dx, fmaf(cc * dy, dy, 2.0f * cb * dx * dy));
 }
 
-// Warp-uniform: does the splat's ellipse reach rows [row0, row0+1]?
-__device__ __forceinline__ bool rows_hit(float my, float half_h, float row_c) {
-  return fabsf(row_c - my) <= half_h + 0.5f;
+// Warp-cooperative compaction of the batch entries whose mask has this
+// warp's bit; writes indices (ascending) to list, returns the count.
+__device__ __forceinline__ int build_list(const uint8_t* s_mask, int cnt, int warp, uint8_t* list) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt_();
+  int n = 0;
+#pragma unroll
+  for (int c = 0; c < kBatch / 32; ++c) {
+    const int e = c * 32 + lane;
+    const bool mine = e < cnt && ((s_mask[e] >> warp) & 1u);
+    const uint32_t bits = __ballot_sync(kFull, mine);
+    if (mine) list[n + __popc(bits & lt)] = (uint8_t)e;
+    n += __popc(bits);
+  }
+  __syncwarp();
+  return n;
 }
 
-__global__ void __launch_bounds__(kTilePix) composite_kernel(
+struct PixFwd {
+  float T, r, g, b;
+  uint32_t processed;
+  bool done;
+};
+
+__device__ __forceinline__ void composite_one(PixFwd& p, const float4& ge, const float4& ap, float col_b, float dx,
+                                              float dy, const RasterDev& rc, uint32_t idx1) {
+  if (p.done) return;
+  const float g = splat_power(ge.z, ge.w, ap.x, dx, dy);
+  if (g > rc.cutoff2_f) return;
+  const float alpha = fminf(rc.alpha_clamp_f, ap.y * exp_neg_half(g));
+  const float w = alpha * p.T;
+  p.r = fmaf(ap.z, w, p.r);
+  p.g = fmaf(ap.w, w, p.g);
+  p.b = fmaf(col_b, w, p.b);
+  p.T *= (1.0f - alpha);
+  if (p.T < rc.early_term_f) {
+    p.done = true;
+    p.processed = idx1;
+  }
+}
+
+__device__ __forceinline__ void write_pixel(const PixFwd& p, int x, int y, int W, int H, float bg_r, float bg_g,
+                                            float bg_b, int64_t npix, float* image, float* final_t,
+                                            uint32_t* pixstate) {
+  if (x >= W || y >= H) return;
+  float cr = fmaf(bg_r, p.T, p.r), cg = fmaf(bg_g, p.T, p.g), cb = fmaf(bg_b, p.T, p.b);
+  uint32_t of = 0;
+  if (cr > 1.0f) { cr = 1.0f; of |= 1u; }
+  if (cg > 1.0f) { cg = 1.0f; of |= 2u; }
+  if (cb > 1.0f) { cb = 1.0f; of |= 4u; }
+  const int64_t q = (int64_t)y * W + x;
+  image[q] = cr;
+  image[npix + q] = cg;
+  image[2 * npix + q] = cb;
+  final_t[q] = p.T;
+  pixstate[q] = p.processed | (of << 29);
+}
+
+// Quadrant layout: warp w -> quadrant (w & 1, w >> 1); lane l -> column
+// 8 (w & 1) + (l & 7), rows 8 (w >> 1) + 2 (l >> 3) and +1.
+__device__ __forceinline__ void pixel_coords(int warp, int lane, int* lx, int* ly) {
+  *lx = (warp & 1) * 8 + (lane & 7);
+  *ly = (warp >> 1) * 8 + (lane >> 3) * 2;
+}
+
+__global__ void __launch_bounds__(kThreads) composite_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ ranks, const SplatRec* __restrict__ rec,
     const CamDev* __restrict__ cam_p, RasterDev rc, float bg_r, float bg_g, float bg_b, int64_t npix,
     float* __restrict__ image, float* __restrict__ final_t, uint32_t* __restrict__ pixstate) {
-  __shared__ float4 s_geo[kBatch], s_app[kBatch], s_ext[kBatch];
+  __shared__ float4 s_geo[kBatch], s_app[kBatch];
+  __shared__ float s_colb[kBatch];
+  __shared__ uint8_t s_mask[kBatch];
+  __shared__ uint8_t s_list[kWarps][kBatch];
   __shared__ int s_w, s_h, s_tx;
   if (threadIdx.x == 0) {
     s_w = cam_p->width;
@@ -74,61 +170,42 @@ __global__ void __launch_bounds__(kTilePix) composite_kernel(
   const int W = s_w, H = s_h;
   const int tile = blockIdx.x;
   const int tx = tile % s_tx, ty = tile / s_tx;
-  const int lx = threadIdx.x & (kTile - 1), ly = threadIdx.x / kTile;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int lx, ly;
+  pixel_coords(warp, lane, &lx, &ly);
   const int x = tx * kTile + lx, y = ty * kTile + ly;
-  const bool inside = x < W && y < H;
   const double ox = (double)(tx * kTile), oy = (double)(ty * kTile);
   const float px = (float)lx, py = (float)ly;
-  const float row_c = (float)(2 * (threadIdx.x >> 5)) + 0.5f;
   const uint2 range = ranges[tile];
-  float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
-  uint32_t processed = 0;
-  bool done = !inside;
+  PixFwd a{1.f, 0.f, 0.f, 0.f, 0u, !(x < W && y < H)};
+  PixFwd b{1.f, 0.f, 0.f, 0.f, 0u, !(x < W && y + 1 < H)};
   for (uint32_t base = range.x; base < range.y; base += kBatch) {
-    if (__syncthreads_count(done) == kTilePix) break;
+    if (__syncthreads_count(a.done && b.done) == kThreads) break;
     const uint32_t e = base + threadIdx.x;
-    if (e < range.y) stage_splat(rec[ranks[e]], ox, oy, rc.cutoff2_f, &s_geo[threadIdx.x], &s_app[threadIdx.x], &s_ext[threadIdx.x]);
-    __syncthreads();
     const int cnt = min((uint32_t)kBatch, range.y - base);
-    if (!__all_sync(kFull, done)) {
-      int k = 0;
-      for (; k < cnt; ++k) {
+    if (threadIdx.x < cnt)
+      s_mask[threadIdx.x] = (uint8_t)stage_splat(rec[ranks[e]], ox, oy, rc.cutoff2_f, &s_geo[threadIdx.x],
+                                                 &s_app[threadIdx.x], &s_colb[threadIdx.x]);
+    __syncthreads();
+    const uint32_t list0 = base - range.x;
+    if (!__all_sync(kFull, a.done && b.done)) {
+      const int n = build_list(s_mask, cnt, warp, s_list[warp]);
+      for (int i = 0; i < n; ++i) {
+        const int k = s_list[warp][i];
         const float4 ge = s_geo[k];
-        const float4 ex = s_ext[k];
-        if (!rows_hit(ge.y, ex.y, row_c)) continue;  // warp-uniform
-        if (done) continue;
-        const float dx = px - ge.x, dy = py - ge.y;
         const float4 ap = s_app[k];
-        const float g = splat_power(ge.z, ge.w, ap.x, dx, dy);
-        if (g > rc.cutoff2_f) continue;
-        const float alpha = fminf(rc.alpha_clamp_f, ap.y * __expf(-0.5f * g));
-        const float w = alpha * T;
-        cr = fmaf(ap.z, w, cr);
-        cg = fmaf(ap.w, w, cg);
-        cb = fmaf(ex.x, w, cb);
-        T *= (1.0f - alpha);
-        if (T < rc.early_term_f) {
-          done = true;
-          processed = base - range.x + (uint32_t)k + 1u;
-        }
+        const float cb = s_colb[k];
+        const float dx = px - ge.x, dy = py - ge.y;
+        composite_one(a, ge, ap, cb, dx, dy, rc, list0 + k + 1u);
+        composite_one(b, ge, ap, cb, dx, dy + 1.0f, rc, list0 + k + 1u);
+        if (__all_sync(kFull, a.done && b.done)) break;
       }
-      if (!done) processed = base - range.x + (uint32_t)cnt;
     }
+    if (!a.done) a.processed = list0 + (uint32_t)cnt;
+    if (!b.done) b.processed = list0 + (uint32_t)cnt;
   }
-  if (!inside) return;
-  cr = fmaf(bg_r, T, cr);
-  cg = fmaf(bg_g, T, cg);
-  cb = fmaf(bg_b, T, cb);
-  uint32_t of = 0;
-  if (cr > 1.0f) { cr = 1.0f; of |= 1u; }
-  if (cg > 1.0f) { cg = 1.0f; of |= 2u; }
-  if (cb > 1.0f) { cb = 1.0f; of |= 4u; }
-  const int64_t p = (int64_t)y * W + x;
-  image[p] = cr;
-  image[npix + p] = cg;
-  image[2 * npix + p] = cb;
-  final_t[p] = T;
-  pixstate[p] = processed | (of << 29);
+  write_pixel(a, x, y, W, H, bg_r, bg_g, bg_b, npix, image, final_t, pixstate);
+  write_pixel(b, x, y + 1, W, H, bg_r, bg_g, bg_b, npix, image, final_t, pixstate);
 }
 
 // Recursive-halving reduce-scatter of 9 values over a warp (12 shuffles
@@ -174,14 +251,76 @@ __device__ __forceinline__ int warp_reduce9(const float v[kPartial], float* out)
   return vi;
 }
 
-__global__ void __launch_bounds__(kTilePix) backward_raster_kernel(
+struct PixBwd {
+  float dr, dg, db, T, br, bg, bb;
+  uint32_t contrib;
+};
+
+__device__ __forceinline__ void load_pixel_bwd(PixBwd& p, int x, int y, int W, int H, int64_t npix, float bg_r,
+                                               float bg_g, float bg_b, const float* d_image, const float* final_t,
+                                               const uint32_t* pixstate) {
+  p.dr = p.dg = p.db = p.T = 0.f;
+  p.contrib = 0;
+  if (x < W && y < H) {
+    const int64_t q = (int64_t)y * W + x;
+    const uint32_t ps = pixstate[q];
+    const uint32_t of = ps >> 29;
+    p.dr = (of & 1u) ? 0.f : d_image[q];
+    p.dg = (of & 2u) ? 0.f : d_image[npix + q];
+    p.db = (of & 4u) ? 0.f : d_image[2 * npix + q];
+    p.T = final_t[q];
+    p.contrib = ps & 0x1fffffffu;
+    if (p.dr == 0.f && p.dg == 0.f && p.db == 0.f) p.contrib = 0;  // rasterizer.cpp:372
+  }
+  p.br = bg_r * p.T;
+  p.bg = bg_g * p.T;
+  p.bb = bg_b * p.T;
+}
+
+// One (pixel, splat) replay step of phase 1; accumulates into v.
+__device__ __forceinline__ bool backward_one(PixBwd& p, const float4& ge, const float4& ap, float col_b, float dx,
+                                             float dy, const RasterDev& rc, uint32_t j, float v[kPartial]) {
+  if (j >= p.contrib) return false;
+  const float g = splat_power(ge.z, ge.w, ap.x, dx, dy);
+  if (g > rc.cutoff2_f) return false;
+  const float G = exp_neg_half(g);
+  const float araw = ap.y * G;
+  const float alpha = fminf(rc.alpha_clamp_f, araw);
+  const float inv = rcp_fast(1.0f - alpha);
+  const float tb = p.T * inv;
+  const float wgt = alpha * tb;
+  v[5] = fmaf(wgt, p.dr, v[5]);
+  v[6] = fmaf(wgt, p.dg, v[6]);
+  v[7] = fmaf(wgt, p.db, v[7]);
+  const float dal = p.dr * (ap.z * tb - p.br * inv) + p.dg * (ap.w * tb - p.bg * inv) + p.db * (col_b * tb - p.bb * inv);
+  if (araw < rc.alpha_clamp_f) {
+    const float cx_ = ge.z * dx + ge.w * dy, cy_ = ge.w * dx + ap.x * dy;
+    v[8] = fmaf(dal, G, v[8]);
+    const float dgg = dal * (-0.5f * araw);
+    v[0] = fmaf(-2.0f * dgg, cx_, v[0]);
+    v[1] = fmaf(-2.0f * dgg, cy_, v[1]);
+    v[2] = fmaf(dgg * dx, dx, v[2]);
+    v[3] = fmaf(dgg * dx, dy, v[3]);
+    v[4] = fmaf(dgg * dy, dy, v[4]);
+  }
+  p.T = tb;
+  p.br = fmaf(ap.z, wgt, p.br);
+  p.bg = fmaf(ap.w, wgt, p.bg);
+  p.bb = fmaf(col_b, wgt, p.bb);
+  return true;
+}
+
+__global__ void __launch_bounds__(kThreads, 8) backward_raster_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ ranks, const SplatRec* __restrict__ rec,
     const SplatAux* __restrict__ aux, const CamDev* __restrict__ cam_p, RasterDev rc, float bg_r, float bg_g,
     float bg_b, int64_t npix, const float* __restrict__ d_image, const float* __restrict__ final_t,
     const uint32_t* __restrict__ pixstate, float* __restrict__ partials, uint32_t k_cap) {
-  __shared__ float4 s_geo[kBatch], s_app[kBatch], s_ext[kBatch];
+  __shared__ float4 s_geo[kBatch], s_app[kBatch];
+  __shared__ float s_colb[kBatch];
   __shared__ uint32_t s_slot[kBatch];
-  __shared__ float s_red[kWarps][32][kPartial];  // [warp][entry in sub-batch][component]
+  __shared__ uint8_t s_mask[kBatch];
+  __shared__ uint8_t s_list[kWarps][kBatch];
+  __shared__ float s_red[kWarps][kBatch][kPartial];  // [warp][entry in batch][component]
   __shared__ int s_w, s_h, s_tx;
   __shared__ uint32_t s_maxc[kWarps];
   if (threadIdx.x == 0) {
@@ -189,35 +328,23 @@ __global__ void __launch_bounds__(kTilePix) backward_raster_kernel(
     s_h = cam_p->height;
     s_tx = cam_p->tiles_x;
   }
-  for (int i = threadIdx.x; i < kWarps * 32 * kPartial; i += kTilePix) (&s_red[0][0][0])[i] = 0.f;
+  for (int i = threadIdx.x; i < kWarps * kBatch * kPartial; i += kThreads) (&s_red[0][0][0])[i] = 0.f;
   __syncthreads();
   const int W = s_w, H = s_h;
   const int tile = blockIdx.x;
   const int tx = tile % s_tx, ty = tile / s_tx;
-  const int lx = threadIdx.x & (kTile - 1), ly = threadIdx.x / kTile;
-  const int x = tx * kTile + lx, y = ty * kTile + ly;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool inside = x < W && y < H;
+  int lx, ly;
+  pixel_coords(warp, lane, &lx, &ly);
+  const int x = tx * kTile + lx, y = ty * kTile + ly;
   const double ox = (double)(tx * kTile), oy = (double)(ty * kTile);
   const float px = (float)lx, py = (float)ly;
-  const float row_c = (float)(2 * warp) + 0.5f;
   const uint2 range = ranges[tile];
 
-  float dr = 0.f, dg = 0.f, db = 0.f, T = 0.f;
-  uint32_t contrib = 0;
-  if (inside) {
-    const int64_t p = (int64_t)y * W + x;
-    const uint32_t ps = pixstate[p];
-    const uint32_t of = ps >> 29;
-    dr = (of & 1u) ? 0.f : d_image[p];
-    dg = (of & 2u) ? 0.f : d_image[npix + p];
-    db = (of & 4u) ? 0.f : d_image[2 * npix + p];
-    T = final_t[p];
-    contrib = ps & 0x1fffffffu;
-    if (dr == 0.f && dg == 0.f && db == 0.f) contrib = 0;  // rasterizer.cpp:372
-  }
-  float br = bg_r * T, bgg = bg_g * T, bb = bg_b * T;
-  const uint32_t wmax = __reduce_max_sync(kFull, contrib);
+  PixBwd a, b;
+  load_pixel_bwd(a, x, y, W, H, npix, bg_r, bg_g, bg_b, d_image, final_t, pixstate);
+  load_pixel_bwd(b, x, y + 1, W, H, npix, bg_r, bg_g, bg_b, d_image, final_t, pixstate);
+  const uint32_t wmax = __reduce_max_sync(kFull, max(a.contrib, b.contrib));
   if (lane == 0) s_maxc[warp] = wmax;
   __syncthreads();
   uint32_t maxc = 0;
@@ -229,89 +356,55 @@ __global__ void __launch_bounds__(kTilePix) backward_raster_kernel(
   const uint32_t nbatch = (len + kBatch - 1) / kBatch;
   for (int bi = (int)nbatch - 1; bi >= 0; --bi) {
     const uint32_t b0 = (uint32_t)bi * kBatch;  // list-local start
-    const uint32_t cnt = min((uint32_t)kBatch, len - b0);
-    __syncthreads();
+    const int cnt = (int)min((uint32_t)kBatch, len - b0);
     if (threadIdx.x < cnt) {
       const uint32_t e = range.x + b0 + threadIdx.x;
       const uint32_t r = ranks[e];
       const SplatAux A = aux[r];
       const uint32_t tx0 = A.tx0_ty0 & 0xffffu, ty0 = A.tx0_ty0 >> 16, nx = A.nx_ny & 0xffffu;
       s_slot[threadIdx.x] = A.off + ((uint32_t)ty - ty0) * nx + ((uint32_t)tx - tx0);
-      if (b0 + threadIdx.x < maxc)
-        stage_splat(rec[r], ox, oy, rc.cutoff2_f, &s_geo[threadIdx.x], &s_app[threadIdx.x], &s_ext[threadIdx.x]);
+      s_mask[threadIdx.x] =
+          b0 + threadIdx.x < maxc
+              ? (uint8_t)stage_splat(rec[r], ox, oy, rc.cutoff2_f, &s_geo[threadIdx.x], &s_app[threadIdx.x],
+                                     &s_colb[threadIdx.x])
+              : (uint8_t)0;
     }
     __syncthreads();
-    // Sub-batches of 32 entries, back to front; each reduced into s_red, then
-    // flushed (fixed warp order) to the entries' global slots.
-    for (int sb = (int)((cnt + 31) / 32) - 1; sb >= 0; --sb) {
-      const int k0 = sb * 32;
-      const int k1 = min((int)cnt, k0 + 32);
-      if (b0 + (uint32_t)k0 < wmax) {  // this warp has work in the sub-batch
-        for (int k = k1 - 1; k >= k0; --k) {
-          const uint32_t j = b0 + (uint32_t)k;
-          if (j >= wmax) continue;  // warp-uniform
-          const float4 ge = s_geo[k];
-          const float4 ex = s_ext[k];
-          if (!rows_hit(ge.y, ex.y, row_c)) continue;  // warp-uniform
-          float v[kPartial];
+    if (b0 < wmax) {  // this warp has pixels that replay entries of this batch
+      const int n = build_list(s_mask, cnt, warp, s_list[warp]);
+      for (int i = n - 1; i >= 0; --i) {  // back to front
+        const int k = s_list[warp][i];
+        const uint32_t j = b0 + (uint32_t)k;
+        if (j >= wmax) continue;  // warp-uniform
+        const float4 ge = s_geo[k];
+        const float4 ap = s_app[k];
+        const float cb = s_colb[k];
+        float v[kPartial];
 #pragma unroll
-          for (int c = 0; c < kPartial; ++c) v[c] = 0.f;
-          bool hit = false;
-          if (j < contrib) {
-            const float dx = px - ge.x, dy = py - ge.y;
-            const float4 ap = s_app[k];
-            const float g = splat_power(ge.z, ge.w, ap.x, dx, dy);
-            if (!(g > rc.cutoff2_f)) {
-              hit = true;
-              const float G = __expf(-0.5f * g);
-              const float araw = ap.y * G;
-              const float alpha = fminf(rc.alpha_clamp_f, araw);
-              const float inv = 1.0f / (1.0f - alpha);
-              const float tb = T * inv;
-              const float wgt = alpha * tb;
-              v[5] = wgt * dr;
-              v[6] = wgt * dg;
-              v[7] = wgt * db;
-              const float dal =
-                  dr * (ap.z * tb - br * inv) + dg * (ap.w * tb - bgg * inv) + db * (ex.x * tb - bb * inv);
-              if (araw < rc.alpha_clamp_f) {
-                const float cx_ = ge.z * dx + ge.w * dy, cy_ = ge.w * dx + ap.x * dy;
-                v[8] = dal * G;
-                const float dgg = dal * (-0.5f * araw);
-                v[0] = -2.0f * dgg * cx_;
-                v[1] = -2.0f * dgg * cy_;
-                v[2] = dgg * dx * dx;
-                v[3] = dgg * dx * dy;
-                v[4] = dgg * dy * dy;
-              }
-              T = tb;
-              br = fmaf(ap.z, wgt, br);
-              bgg = fmaf(ap.w, wgt, bgg);
-              bb = fmaf(ex.x, wgt, bb);
-            }
-          }
-          if (__any_sync(kFull, hit)) {
-            float tot;
-            const int vi = warp_reduce9(v, &tot);
-            if (vi >= 0) s_red[warp][k - k0][vi] = tot;
-          }
+        for (int c = 0; c < kPartial; ++c) v[c] = 0.f;
+        const float dx = px - ge.x, dy = py - ge.y;
+        const bool ha = backward_one(a, ge, ap, cb, dx, dy, rc, j, v);
+        const bool hb = backward_one(b, ge, ap, cb, dx, dy + 1.0f, rc, j, v);
+        if (__any_sync(kFull, ha || hb)) {
+          float tot;
+          const int vi = warp_reduce9(v, &tot);
+          if (vi >= 0) s_red[warp][k][vi] = tot;
         }
       }
-      __syncthreads();
-      // flush: 32 entries x 9 components, summed over warps 0..7 in order
-      for (int idx = threadIdx.x; idx < 32 * kPartial; idx += kTilePix) {
-        const int kk = idx / kPartial, c = idx - kk * kPartial;
-        const int k = k0 + kk;
-        float acc = 0.f;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
-          acc += s_red[w][kk][c];
-          s_red[w][kk][c] = 0.f;
-        }
-        if (k < k1 && s_slot[k] < k_cap) partials[(int64_t)s_slot[k] * kPartial + c] = acc;
-      }
-      __syncthreads();
     }
+    __syncthreads();
+    // flush: batch entries x 9 components, summed over warps 0..3 in order
+    for (int idx = threadIdx.x; idx < cnt * kPartial; idx += kThreads) {
+      const int k = idx / kPartial, c = idx - k * kPartial;
+      float acc = 0.f;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        acc += s_red[w][k][c];
+        s_red[w][k][c] = 0.f;
+      }
+      if (s_slot[k] < k_cap) partials[(int64_t)s_slot[k] * kPartial + c] = acc;
+    }
+    __syncthreads();
   }
 }
 
@@ -319,7 +412,7 @@ int launch_composite(cudaStream_t st, gsb_frame* f, const RasterDev& rc) {
   const int n_tiles = f->tiles_x * f->tiles_y;
   const int64_t npix = (int64_t)f->width * f->height;
   if (n_tiles > 0)
-    composite_kernel<<<n_tiles, kTilePix, 0, st>>>(
+    composite_kernel<<<n_tiles, kThreads, 0, st>>>(
         f->ranges.as<uint2>(), f->eval_[f->sorted_sel].as<uint32_t>(), f->rec.as<SplatRec>(), f->cam.as<CamDev>(), rc,
         (float)f->background[0], (float)f->background[1], (float)f->background[2], npix, f->image.as<float>(),
         f->final_t.as<float>(), f->pixstate.as<uint32_t>());
@@ -331,7 +424,7 @@ int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc) {
   const int n_tiles = f->tiles_x * f->tiles_y;
   const int64_t npix = (int64_t)f->width * f->height;
   if (n_tiles > 0)
-    backward_raster_kernel<<<n_tiles, kTilePix, 0, st>>>(
+    backward_raster_kernel<<<n_tiles, kThreads, 0, st>>>(
         f->ranges.as<uint2>(), f->eval_[f->sorted_sel].as<uint32_t>(), f->rec.as<SplatRec>(), f->aux.as<SplatAux>(),
         f->cam.as<CamDev>(), rc, (float)f->background[0], (float)f->background[1], (float)f->background[2], npix,
         f->d_image.as<float>(), f->final_t.as<float>(), f->pixstate.as<uint32_t>(), f->partials.as<float>(),

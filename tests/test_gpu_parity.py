@@ -116,6 +116,31 @@ def test_binning_bit_exact_on_device_records(G, ctx):
     assert np.array_equal(d["tile_ranges"], ref.tile_ranges)
 
 
+def test_binning_bit_exact_c2_scale(G, ctx):
+    """C2 shape (300k Gaussians, 1008x756, forward-facing): the device's
+    depth order, tile lists and ranges equal rasterizer.cpp:127-168 re-run on
+    the device's own FP64 records, across hundreds of 4096-item sort tiles
+    (exercises the decoupled look-back)."""
+    hc, poses = synth_scene(2, 300_000, 1008, kind=1, cams=2, scale_offset=math.log(500 / 300_000) / 3)
+    cam = O.make_camera(0.75 * 1008, 0.75 * 1008, 503.5, 377.5, 1008, 756, *O.pose_split(poses[0]))
+    cloud = to_dev(G, ctx, hc)
+    d = G.render(ctx, cloud, dev_cam(G, cam), want_image=False).download()
+    n = hc.n
+    keep = np.zeros(n, np.uint8)
+    keep[d["splat_gaussian"]] = 1
+    mu2d = np.zeros((n, 2))
+    mu2d[d["splat_gaussian"]] = d["splat_mu2d"]
+    rad = np.zeros(n)
+    rad[d["splat_gaussian"]] = d["splat_radius"]
+    dep = np.zeros(n)
+    dep[d["splat_gaussian"]] = d["splat_depth"]
+    sg, lists, ranges = O.bin_records(keep, mu2d, rad, dep, 1008, 756)
+    assert len(d["splat_gaussian"]) > 200_000 and len(lists) > 500_000
+    assert np.array_equal(sg, d["splat_gaussian"])
+    assert np.array_equal(lists, d["tile_lists"])
+    assert np.array_equal(ranges, d["tile_ranges"])
+
+
 def test_render_c1_scene_image(G, ctx):
     """C1 (10k Gaussians, 256x256): max-abs over pixels without an FP32
     decision flip (cutoff / early-termination) <= 1e-5; flips are rare."""
