@@ -65,7 +65,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -260,6 +260,16 @@ def run_ours(args, ws, rank, local):
     return out
 
 
+def ncu_traffic(stage):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the stage's
+    kernel from the committed ncu --set full capture (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(p)).get(stage, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
 def roofline(stage, ms, fi, work, peaks, clk):
     """Dominant-stage roofline (SURVEY §8d units)."""
     V, K = fi.n_splats, fi.n_entries
@@ -279,7 +289,8 @@ def roofline(stage, ms, fi, work, peaks, clk):
         peak = fp32_peak_tflops(148, clk_mhz)
         achieved = flops / (ms / 1e3) / 1e12
         return {"stage": stage, "bound": "fp32", "achieved": round(achieved, 3), "peak": round(peak, 2),
-                "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": ncu_traffic(stage),
+                "traffic_unit": "DRAM bytes per launch (ncu, profiles/ncu_traffic.json)",
                 "peak_source": "nominal FP32 = 148 SM x 128 lanes x 2 x sm_max_mhz (no FP32 entry in "
                                "MEASURED_PEAKS.json)",
                 "frac_at_measured_clock": round(achieved / fp32_peak_tflops(148, clk["sm_mhz"]), 4)
@@ -289,7 +300,7 @@ def roofline(stage, ms, fi, work, peaks, clk):
         b = bytes_per[stage]
         achieved = b / (ms / 1e3) / 1e9
         return {"stage": stage, "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(achieved / hbm_peak, 4), "traffic": None, "peak_source": hbm_src,
+                "frac": round(achieved / hbm_peak, 4), "traffic": ncu_traffic(stage), "peak_source": hbm_src,
                 "algorithmic": f"{b} bytes per launch (SURVEY §8d)", "ms_per_launch": round(ms, 4)}
     return {"stage": stage, "bound": "fp32", "achieved": None, "peak": None, "unit": "TFLOP/s", "frac": None,
             "traffic": None, "note": "work counts unavailable (cpu baseline skipped)", "ms_per_launch": round(ms, 4)}
@@ -359,7 +370,7 @@ def run_reference(args, ws, rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-iters", type=int, default=100)
