@@ -50,6 +50,7 @@ int launch_rgb_loss(cudaStream_t st, const float* ren, const float* tgt, int W, 
                     double* block_sums, double* out3, float* d_image, int64_t* launches);
 size_t loss_block_count(int W, int H);
 int init_loss_constants();
+int init_preprocess_attributes();
 int launch_pose_iter(cudaStream_t st, void* state, const double* dpose, const double* loss3, double lr_start,
                      double lr_end, double eps, int budget, CamDev* cam, double* trace_pose, double* trace_loss,
                      const uint32_t* k_dev, int64_t k_cap);
@@ -304,12 +305,12 @@ static int frame_reserve(gsb_frame* f, const gsb_cloud* cloud, int64_t k_cap) {
   GSB_CUDA(f->counters.reserve(64, &grew));
   GSB_CUDA(f->rec_g.reserve(sizeof(SplatRec) * n, &grew));
   GSB_CUDA(f->rect_g.reserve(sizeof(uint2) * n, &grew));
-  GSB_CUDA(f->cnt_g.reserve(sizeof(uint32_t) * n, &grew));
+  GSB_CUDA(f->cnt_g.reserve(sizeof(uint32_t) * np, &grew));  // n_pad: TMA-staged by 16 B
   GSB_CUDA(f->depth_g.reserve(sizeof(double) * n, &grew));
   GSB_CUDA(f->radius_g.reserve(sizeof(double) * n, &grew));
   GSB_CUDA(f->rank_of_g.reserve(sizeof(int32_t) * n, &grew));
   GSB_CUDA(f->colj.reserve(sizeof(float) * 9 * np, &grew));
-  GSB_CUDA(f->off_g.reserve(sizeof(uint32_t) * n, &grew));
+  GSB_CUDA(f->off_g.reserve(sizeof(uint32_t) * np, &grew));
   GSB_CUDA(f->vis_idx.reserve(sizeof(uint32_t) * n, &grew));
   GSB_CUDA(f->cnt_r.reserve(sizeof(uint32_t) * n, &grew));
   for (int b = 0; b < 2; ++b) {
@@ -565,6 +566,10 @@ int gsb_ctx_create(int32_t device, gsb_ctx** out) {
   }
   c->timer = new StageTimer();
   if (int r = init_loss_constants()) {
+    gsb_ctx_destroy(c);
+    return r;
+  }
+  if (int r = init_preprocess_attributes()) {
     gsb_ctx_destroy(c);
     return r;
   }

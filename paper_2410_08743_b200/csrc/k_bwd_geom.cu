@@ -44,39 +44,64 @@ __device__ __forceinline__ void sh_basis_d(double x, double y, double z, int deg
   B[15] = kBC3[6] * x * (xx - 3.0 * yy);
 }
 
+// The CTA's 256-Gaussian segments of the 11 geometry/opacity planes, the 9
+// colour-Jacobian planes, the tile counts and the entry offsets are staged
+// into shared memory by TMA bulk copies (one elected thread, one mbarrier).
+constexpr int kGeomBlock = 256;
+constexpr int kGeomPlanes = kOpacity + 1;  // means, quat, log-scale, opacity
+
 template <bool kFull>
-__global__ void __launch_bounds__(256, 2) backward_geom_kernel(
-    const float* __restrict__ params, int64_t n, int64_t n_pad, int sh_cap, int sh_active,
+__global__ void __launch_bounds__(kGeomBlock, 2) backward_geom_kernel(
+    const float* __restrict__ params, int64_t n, int64_t n_pad_g, int sh_cap, int sh_active,
     const CamDev* __restrict__ cam_p, RasterDev rc, const uint32_t* __restrict__ cnt_g,
     const uint32_t* __restrict__ off_g, const float* __restrict__ colj, const float* __restrict__ partials,
     int64_t k_cap, float* __restrict__ grads, double* __restrict__ pose_blocks) {
+  __shared__ __align__(128) float s_par[kGeomPlanes * kGeomBlock];
+  __shared__ __align__(128) float s_colj[9 * kGeomBlock];
+  __shared__ __align__(128) uint32_t s_cnt[kGeomBlock], s_off[kGeomBlock];
   __shared__ CamDev cam;
   __shared__ double s_pose[8][6];
-  if (threadIdx.x == 0) cam = *cam_p;
+  __shared__ __align__(8) uint64_t bar;
+  const int64_t i0 = (int64_t)blockIdx.x * kGeomBlock;
+  if (threadIdx.x == 0) {
+    cam = *cam_p;
+    mbar_init(&bar, 1);
+    const int64_t here = n - i0 < kGeomBlock ? n - i0 : kGeomBlock;
+    const uint32_t bytes = (uint32_t)(((here * 4) + 15) & ~(int64_t)15);
+    // cnt_g / off_g are sized to whole 256-blocks (frame_reserve), colj to n_pad
+    mbar_arrive_expect_tx(&bar, bytes * (kGeomPlanes + 9 + 2));
+    for (int p = 0; p < kGeomPlanes; ++p) tma_load_1d(s_par + p * kGeomBlock, params + p * n_pad_g + i0, bytes, &bar);
+    for (int p = 0; p < 9; ++p) tma_load_1d(s_colj + p * kGeomBlock, colj + p * n_pad_g + i0, bytes, &bar);
+    tma_load_1d(s_cnt, cnt_g + i0, bytes, &bar);
+    tma_load_1d(s_off, off_g + i0, bytes, &bar);
+  }
   __syncthreads();
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  mbar_wait(&bar, 0);
+  const int64_t i = i0 + threadIdx.x;
   const int bcap = (sh_cap + 1) * (sh_cap + 1);
   const int nplanes = kShBase + 3 * bcap;
   double pc0 = 0, pc1 = 0, pc2 = 0, pc3 = 0, pc4 = 0, pc5 = 0;
-  const uint32_t craw = i < n ? cnt_g[i] : 0u;
+  const uint32_t craw = i < n ? s_cnt[threadIdx.x] : 0u;
   const uint32_t cnt = craw & kCntMask;
   if (kFull && i < n && cnt == 0u) {
-    for (int p = 0; p < nplanes + 2; ++p) grads[(int64_t)p * n_pad + i] = 0.f;
+    for (int p = 0; p < nplanes + 2; ++p) grads[(int64_t)p * n_pad_g + i] = 0.f;
   }
   // (off + cnt > k_cap only when the entry capacity overflowed: the iteration
   // is discarded by the pose step and re-run, so skip the splat.)
-  if (i < n && cnt > 0u && (int64_t)off_g[i] + cnt <= k_cap) {
+  const uint32_t off = s_off[threadIdx.x];
+  if (i < n && cnt > 0u && (int64_t)off + cnt <= k_cap) {
     const uint32_t clamp = craw >> kClampShift;
     // phase 2: ordered sum of this splat's entry partials (tile order)
     double acc[kPartial];
 #pragma unroll
     for (int c = 0; c < kPartial; ++c) acc[c] = 0.0;
-    const float* pp = partials + (int64_t)off_g[i] * kPartial;
+    const float* pp = partials + (int64_t)off * kPartial;
     for (uint32_t j = 0; j < cnt; ++j) {
 #pragma unroll
       for (int c = 0; c < kPartial; ++c) acc[c] += (double)pp[j * kPartial + c];
     }
-    const float* P = params + i;
+    const float* P = s_par + threadIdx.x;
+    constexpr int64_t n_pad = kGeomBlock;  // plane stride of the staged copy
     const double mean0 = P[kMeanX * n_pad], mean1 = P[kMeanY * n_pad], mean2 = P[kMeanZ * n_pad];
     const double* Rc = cam.R;
     double mc[3];
@@ -158,9 +183,9 @@ __global__ void __launch_bounds__(256, 2) backward_geom_kernel(
     double dd0 = 0, dd1 = 0, dd2 = 0;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      dd0 += dcol[c] * (double)colj[(int64_t)(3 * c + 0) * n_pad + i];
-      dd1 += dcol[c] * (double)colj[(int64_t)(3 * c + 1) * n_pad + i];
-      dd2 += dcol[c] * (double)colj[(int64_t)(3 * c + 2) * n_pad + i];
+      dd0 += dcol[c] * (double)s_colj[(3 * c + 0) * kGeomBlock + threadIdx.x];
+      dd1 += dcol[c] * (double)s_colj[(3 * c + 1) * kGeomBlock + threadIdx.x];
+      dd2 += dcol[c] * (double)s_colj[(3 * c + 2) * kGeomBlock + threadIdx.x];
     }
     const double pd = dir0 * dd0 + dir1 * dd1 + dir2 * dd2;
     const double dtg0 = (dd0 - dir0 * pd) / dist, dtg1 = (dd1 - dir1 * pd) / dist, dtg2 = (dd2 - dir2 * pd) / dist;
@@ -183,7 +208,7 @@ __global__ void __launch_bounds__(256, 2) backward_geom_kernel(
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         const double dtga = a == 0 ? dtg0 : (a == 1 ? dtg1 : dtg2);
-        grads[(int64_t)(kMeanX + a) * n_pad + i] = (float)(Rc[a] * dmc[0] + Rc[3 + a] * dmc[1] + Rc[6 + a] * dmc[2] + dtga);
+        grads[(int64_t)(kMeanX + a) * n_pad_g + i] = (float)(Rc[a] * dmc[0] + Rc[3 + a] * dmc[1] + Rc[6 + a] * dmc[2] + dtga);
       }
       // d_Sigma = m^T dcov m (symmetric)
       double dS[9];
@@ -206,7 +231,7 @@ __global__ void __launch_bounds__(256, 2) backward_geom_kernel(
 #pragma unroll
         for (int a = 0; a < 3; ++a)
           rtr += Rg[a * 3 + k] * (dS[a * 3] * Rg[k] + dS[a * 3 + 1] * Rg[3 + k] + dS[a * 3 + 2] * Rg[6 + k]);
-        grads[(int64_t)(kScaleX + k) * n_pad + i] = (float)(2.0 * scs[k] * rtr * scs[k]);
+        grads[(int64_t)(kScaleX + k) * n_pad_g + i] = (float)(2.0 * scs[k] * rtr * scs[k]);
       }
       // quat_rotation_jacobian (scene.cpp:56-88): d_q_k = sum_j <dRg, 2 U_j> (delta_jk - q_j q_k)/|q|
       const double q[4] = {w, x, y, zq};
@@ -227,7 +252,7 @@ __global__ void __launch_bounds__(256, 2) backward_geom_kernel(
         double s = 0.0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) s += dU[j] * ((((j == k) ? 1.0 : 0.0) - q[j] * q[k]) / qn);
-        grads[(int64_t)(kQuatW + k) * n_pad + i] = (float)s;
+        grads[(int64_t)(kQuatW + k) * n_pad_g + i] = (float)s;
       }
       // SH coefficients: d_sh[c][b] = d_colour_c Y_b(dir) for active bands of unclamped channels
       const int deg = sh_active < sh_cap ? sh_active : sh_cap;
@@ -237,12 +262,12 @@ __global__ void __launch_bounds__(256, 2) backward_geom_kernel(
       for (int c = 0; c < 3; ++c) {
         const bool clamped = (clamp >> c) & 1u;
         for (int b = 0; b < bcap; ++b)
-          grads[(int64_t)(kShBase + c * bcap + b) * n_pad + i] = (!clamped && b < nb) ? (float)(dcol[c] * Bv[b]) : 0.f;
+          grads[(int64_t)(kShBase + c * bcap + b) * n_pad_g + i] = (!clamped && b < nb) ? (float)(dcol[c] * Bv[b]) : 0.f;
       }
       const double o = 1.0 / (1.0 + exp(-(double)P[kOpacity * n_pad]));
-      grads[(int64_t)kOpacity * n_pad + i] = (float)(acc[8] * o * (1.0 - o));
-      grads[(int64_t)nplanes * n_pad + i] = (float)dmu2x;
-      grads[(int64_t)(nplanes + 1) * n_pad + i] = (float)dmu2y;
+      grads[(int64_t)kOpacity * n_pad_g + i] = (float)(acc[8] * o * (1.0 - o));
+      grads[(int64_t)nplanes * n_pad_g + i] = (float)dmu2x;
+      grads[(int64_t)(nplanes + 1) * n_pad_g + i] = (float)dmu2y;
     }
   }
   // deterministic block reduction of the pose contributions

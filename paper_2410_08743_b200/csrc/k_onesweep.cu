@@ -62,9 +62,9 @@ __device__ __forceinline__ uint32_t look_back(const uint32_t* status, int64_t ti
 // ------------------------------------------------------------- scan
 // status: [1 ticket][ntiles] words, zeroed before the launch.
 template <bool kFlag>
-__global__ void __launch_bounds__(kOsThreads) scan_onepass_kernel(const uint32_t* __restrict__ in, int64_t cap,
+__global__ void __launch_bounds__(kOsThreads) scan_onepass_kernel(const uint32_t* in, int64_t cap,
                                                                    const uint32_t* __restrict__ n_dev,
-                                                                   uint32_t* __restrict__ out, uint32_t* status,
+                                                                   uint32_t* out, uint32_t* status,
                                                                    uint32_t* __restrict__ total) {
   __shared__ uint32_t s_tile_idx, s_prefix;
   __shared__ uint32_t s_warp[kOsThreads / 32];

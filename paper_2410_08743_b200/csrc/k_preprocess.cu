@@ -120,19 +120,38 @@ __device__ __forceinline__ void sh_colour(const float* __restrict__ P, int64_t n
   *clamp = cl;
 }
 
+// The CTA's 256-Gaussian segment of every parameter plane is staged into
+// shared memory with one TMA bulk copy per plane (issued by one thread,
+// completing on an mbarrier), so all ~59 KB are in flight at once; the
+// per-thread reads below then come from shared memory (stride kPreBlock).
+constexpr int kPreBlock = 256;
+
 template <int DEG, bool kQuirk>
-__global__ void __launch_bounds__(256) preprocess_kernel(
-    const float* __restrict__ params, int64_t n, int64_t n_pad, int sh_cap, int sh_active,
+__global__ void __launch_bounds__(kPreBlock) preprocess_kernel(
+    const float* __restrict__ params, int64_t n, int64_t n_pad_g, int sh_cap, int sh_active,
     const CamDev* __restrict__ cam_p, RasterDev rc, SplatRec* __restrict__ rec_g, uint2* __restrict__ rect_g,
     uint32_t* __restrict__ cnt_g, double* __restrict__ depth_g, double* __restrict__ radius_g,
     int32_t* __restrict__ rank_of_g, float* __restrict__ colj) {
+  extern __shared__ __align__(128) float s_par[];  // [planes][kPreBlock]
   __shared__ CamDev cam;
-  if (threadIdx.x == 0) cam = *cam_p;
+  __shared__ __align__(8) uint64_t bar;
+  const int nplanes = kShBase + 3 * (sh_cap + 1) * (sh_cap + 1);
+  const int64_t i0 = (int64_t)blockIdx.x * kPreBlock;
+  if (threadIdx.x == 0) {
+    cam = *cam_p;
+    mbar_init(&bar, 1);
+    const int64_t cnt_here = n - i0 < kPreBlock ? n - i0 : kPreBlock;
+    const uint32_t bytes = (uint32_t)(((cnt_here * 4) + 15) & ~(int64_t)15);  // n_pad covers the round-up
+    mbar_arrive_expect_tx(&bar, bytes * (uint32_t)nplanes);
+    for (int p = 0; p < nplanes; ++p) tma_load_1d(s_par + p * kPreBlock, params + p * n_pad_g + i0, bytes, &bar);
+  }
   __syncthreads();
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  mbar_wait(&bar, 0);
+  const int64_t i = i0 + threadIdx.x;
   if (i >= n) return;
   rank_of_g[i] = -1;
-  const float* P = params + i;
+  const float* P = s_par + threadIdx.x;
+  constexpr int64_t n_pad = kPreBlock;  // plane stride of the staged copy
   const double mx = P[kMeanX * n_pad], my = P[kMeanY * n_pad], mz = P[kMeanZ * n_pad];
   // Se3Pose::act: rotation * p + translation (lie.hpp:38)
   const double cx = a_(dot3(cam.R[0], cam.R[1], cam.R[2], mx, my, mz), cam.t[0]);
@@ -207,7 +226,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
         float col[3], G[9];
         uint32_t clamp = 0;
         sh_colour<DEG, kQuirk>(P, n_pad, sh_cap, (float)dx, (float)dy, (float)dz, col, &clamp, G);
-        for (int k = 0; k < 9; ++k) colj[(int64_t)k * n_pad + i] = G[k];
+        for (int k = 0; k < 9; ++k) colj[(int64_t)k * n_pad_g + i] = G[k];
         const double op = d_(1.0, a_(1.0, exp(-(double)P[kOpacity * n_pad])));
         // tile span (rasterizer.cpp:138-146)
         const double tile = (double)kTile;
@@ -242,8 +261,9 @@ int launch_preprocess(cudaStream_t st, const gsb_cloud* cloud, const CamDev* cam
   const int64_t n = cloud->n;
   const int deg = std::min(cloud->active_sh_degree, cloud->sh_degree);
   const bool quirk = deg < cloud->sh_degree;
+  const size_t smem = sizeof(float) * kPreBlock * num_planes(cloud->sh_degree);
 #define GSB_PRE(D, Q)                                                                                          \
-  preprocess_kernel<D, Q><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(                                       \
+  preprocess_kernel<D, Q><<<(unsigned)((n + kPreBlock - 1) / kPreBlock), kPreBlock, smem, st>>>(              \
       cloud->params.as<float>(), n, cloud->n_pad, cloud->sh_degree, cloud->active_sh_degree, cam, rc,          \
       f->rec_g.as<SplatRec>(), f->rect_g.as<uint2>(), f->cnt_g.as<uint32_t>(), f->depth_g.as<double>(),        \
       f->radius_g.as<double>(), f->rank_of_g.as<int32_t>(), f->colj.as<float>())
@@ -260,6 +280,23 @@ int launch_preprocess(cudaStream_t st, const gsb_cloud* cloud, const CamDev* cam
   }
 #undef GSB_PRE
   GSB_CHECK_LAUNCH("preprocess_kernel");
+  return GSB_OK;
+}
+
+// Opt every instantiation into the dynamic shared memory its staging needs
+// (59 KB at SH-3). Called once per context, outside any graph capture.
+int init_preprocess_attributes() {
+  const int smem = (int)(sizeof(float) * kPreBlock * num_planes(3));
+#define GSB_ATTR(D, Q) \
+  GSB_CUDA(cudaFuncSetAttribute(preprocess_kernel<D, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))
+  GSB_ATTR(0, false);
+  GSB_ATTR(0, true);
+  GSB_ATTR(1, false);
+  GSB_ATTR(1, true);
+  GSB_ATTR(2, false);
+  GSB_ATTR(2, true);
+  GSB_ATTR(3, false);
+#undef GSB_ATTR
   return GSB_OK;
 }
 

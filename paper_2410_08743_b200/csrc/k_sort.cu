@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(1024) scan_blocks_kernel(uint32_t* __restrict_
 // Block-local exclusive scan plus block offset. Items are striped
 // (k*256 + tid) for coalescing; the scan order is the global index order.
 template <bool kFlag>
-__global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t* __restrict__ in, int64_t cap,
+__global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t* in, int64_t cap,
                                                                    const uint32_t* __restrict__ n_dev,
                                                                    const uint32_t* __restrict__ block_offs,
                                                                    uint32_t* __restrict__ out) {
@@ -203,26 +203,73 @@ __global__ void __launch_bounds__(kRadixThreads) radix_hist_kernel(const uint32_
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * kRadixTile;
   const uint32_t mask = (uint32_t)ndig - 1u;
+  const uint32_t lane = threadIdx.x & 31;
   if (base < n) {
 #pragma unroll 4
     for (int k = 0; k < kRadixRounds; ++k) {
+      // warp-aggregated: one shared atomic per distinct digit per warp (tile
+      // keys arrive in long runs of equal digits)
       const int64_t i = base + k * kRadixThreads + threadIdx.x;
-      if (i < n) atomicAdd(&h[(keys[i] >> shift) & mask], 1u);
+      const bool valid = i < n;
+      const uint32_t dig = valid ? (keys[i] >> shift) & mask : 0x100u + lane;
+      const uint32_t peers = __match_any_sync(0xffffffffu, dig);
+      if (valid && (peers & ((1u << lane) - 1u)) == 0u) atomicAdd(&h[dig], (uint32_t)__popc(peers));
     }
   }
   __syncthreads();
   if (threadIdx.x < ndig) hist[(int64_t)threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
 }
 
-// Stable scatter: items are processed in rounds of 256 in global order;
-// within a round ranks come from warp match + cross-warp prefix.
+// Exclusive scan of a small array (radix histograms, <= ~1M words) in one
+// CTA: each thread scans a contiguous chunk, chunk totals are scanned across
+// the block. One launch instead of reduce / scan / apply.
+__global__ void __launch_bounds__(1024) scan_small_kernel(uint32_t* __restrict__ a, int64_t n) {
+  __shared__ uint32_t s_tot[1024];
+  __shared__ uint32_t s_w[32];
+  const int64_t chunk = (n + 1023) / 1024;
+  const int64_t b = (int64_t)threadIdx.x * chunk, e = b + chunk < n ? b + chunk : n;
+  uint32_t t = 0;
+  for (int64_t i = b; i < e; ++i) t += a[i];
+  uint32_t x = t;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) >= o) x += y;
+  }
+  if ((threadIdx.x & 31) == 31) s_w[threadIdx.x >> 5] = x;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t w = s_w[threadIdx.x];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (threadIdx.x >= o) w += y;
+    }
+    s_w[threadIdx.x] = w;
+  }
+  __syncthreads();
+  uint32_t run = ((threadIdx.x >> 5) ? s_w[(threadIdx.x >> 5) - 1] : 0u) + x - t;
+  for (int64_t i = b; i < e; ++i) {
+    const uint32_t v = a[i];
+    a[i] = run;
+    run += v;
+  }
+  (void)s_tot;
+}
+
+// Stable scatter: items are processed in rounds of 512 in global order (two
+// items per thread: sub-round s covers items s*256 + tid); ranks come from
+// warp match_any, then a cross-(sub-round, warp) prefix per digit — 16
+// virtual warps, two barriers per 512 items.
 __global__ void __launch_bounds__(kRadixThreads) radix_scatter_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, int64_t cap, const uint32_t* __restrict__ n_dev, int shift, int bits,
     const uint32_t* __restrict__ offs, int64_t nblocks) {
   constexpr int kWarps = kRadixThreads / 32;
-  __shared__ uint32_t warp_cnt[kWarps][256];
-  __shared__ uint32_t warp_off[kWarps][256];
+  constexpr int kSubs = 2;
+  constexpr int kV = kWarps * kSubs;  // virtual warps per round
+  __shared__ uint32_t warp_cnt[kV][256];
+  __shared__ uint32_t warp_off[kV][256];
   __shared__ uint32_t digit_run[256];
   const int64_t n = live_count(n_dev, cap);
   const int64_t base = (int64_t)blockIdx.x * kRadixTile;
@@ -232,28 +279,34 @@ __global__ void __launch_bounds__(kRadixThreads) radix_scatter_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int d = threadIdx.x; d < 256; d += kRadixThreads) {
     digit_run[d] = d < ndig ? offs[(int64_t)d * nblocks + blockIdx.x] : 0u;
-    for (int w = 0; w < kWarps; ++w) warp_cnt[w][d] = 0;
+    for (int w = 0; w < kV; ++w) warp_cnt[w][d] = 0;
   }
   __syncthreads();
   const uint32_t lt = lanemask_lt();
-  for (int k = 0; k < kRadixRounds; ++k) {
-    const int64_t i = base + k * kRadixThreads + threadIdx.x;
-    if (base + k * kRadixThreads >= n) break;  // uniform across the block
-    const bool valid = i < n;
-    uint32_t key = 0, val = 0, dig = 0x100u + lane;  // invalid lanes get unique sentinels
-    if (valid) {
-      key = keys_in[i];
-      val = vals_in[i];
-      dig = (key >> shift) & mask;
+  for (int k = 0; k < kRadixRounds / kSubs; ++k) {
+    const int64_t r0 = base + (int64_t)k * kSubs * kRadixThreads;
+    if (r0 >= n) break;  // uniform across the block
+    uint32_t key[kSubs], val[kSubs], dig[kSubs], rank[kSubs];
+    bool valid[kSubs];
+#pragma unroll
+    for (int s = 0; s < kSubs; ++s) {
+      const int64_t i = r0 + s * kRadixThreads + threadIdx.x;
+      valid[s] = i < n;
+      key[s] = valid[s] ? keys_in[i] : 0u;
+      val[s] = valid[s] ? vals_in[i] : 0u;
+      dig[s] = valid[s] ? (key[s] >> shift) & mask : 0x100u + lane;  // invalid lanes: unique sentinels
     }
-    const uint32_t peers = __match_any_sync(0xffffffffu, dig);
-    const uint32_t rank = __popc(peers & lt);
-    if (valid && rank == 0) warp_cnt[warp][dig] = __popc(peers);
+#pragma unroll
+    for (int s = 0; s < kSubs; ++s) {
+      const uint32_t peers = __match_any_sync(0xffffffffu, dig[s]);
+      rank[s] = __popc(peers & lt);
+      if (valid[s] && rank[s] == 0) warp_cnt[s * kWarps + warp][dig[s]] = __popc(peers);
+    }
     __syncthreads();
     for (int d = threadIdx.x; d < ndig; d += kRadixThreads) {
       uint32_t run = digit_run[d];
 #pragma unroll
-      for (int w = 0; w < kWarps; ++w) {
+      for (int w = 0; w < kV; ++w) {
         const uint32_t c = warp_cnt[w][d];
         warp_off[w][d] = run;
         run += c;
@@ -262,15 +315,19 @@ __global__ void __launch_bounds__(kRadixThreads) radix_scatter_kernel(
       digit_run[d] = run;
     }
     __syncthreads();
-    if (valid) {
-      const uint32_t pos = warp_off[warp][dig] + rank;
-      keys_out[pos] = key;
-      vals_out[pos] = val;
+#pragma unroll
+    for (int s = 0; s < kSubs; ++s) {
+      if (!valid[s]) continue;
+      const uint32_t pos = warp_off[s * kWarps + warp][dig[s]] + rank[s];
+      keys_out[pos] = key[s];
+      vals_out[pos] = val[s];
     }
   }
 }
 
 static int radix_passes(int total_bits) { return total_bits <= 0 ? 0 : (total_bits + 7) / 8; }
+int scan_onepass(cudaStream_t st, const uint32_t* in, int64_t cap, const uint32_t* n_dev, bool flag, uint32_t* out,
+                 uint32_t* status, uint32_t* total, int64_t* launches);
 
 // Sorts (keys, vals)[0..live) by key bits [0, total_bits) stably. Buffers [0]
 // hold the input; *result_sel receives the buffer index holding the result
@@ -289,7 +346,8 @@ int radix_sort_pairs(cudaStream_t st, uint32_t* keys[2], uint32_t* vals[2], int6
   for (int p = 0; p < passes; ++p) {
     const int shift = p * bits;
     radix_hist_kernel<<<(unsigned)nblocks, kRadixThreads, 0, st>>>(keys[sel], cap, n_dev, shift, bits, hist, nblocks);
-    int rc = scan_exclusive(st, hist, nh, nullptr, false, hist, hist + nh, nullptr, launches);
+    // few tiles -> short look-back: the single-pass scan wins for histograms
+    int rc = scan_onepass(st, hist, nh, nullptr, false, hist, hist + nh, nullptr, launches);
     if (rc) return rc;
     radix_scatter_kernel<<<(unsigned)nblocks, kRadixThreads, 0, st>>>(keys[sel], vals[sel], keys[sel ^ 1],
                                                                       vals[sel ^ 1], cap, n_dev, shift, bits, hist,
