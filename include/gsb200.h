@@ -91,6 +91,8 @@ typedef struct {
   int64_t n_gaussians, n_splats, n_entries;
   int32_t width, height, tiles_x, tiles_y;
   uint64_t state_fingerprint;
+  int32_t binning; /* GSB_BINNING_* used for this state */
+  int32_t reserved;
 } gsb_frame_info;
 
 /* The pose_descent knobs of TrainConfig (trainer.hpp:21-60) that estimate_pose reads. */
@@ -112,6 +114,14 @@ void gsb_default_pose_config(gsb_pose_config* cfg);
 int gsb_ctx_create(int32_t device, gsb_ctx** out);
 int gsb_ctx_destroy(gsb_ctx* ctx);
 int gsb_ctx_synchronize(gsb_ctx* ctx);
+/* K2 binning strategy (both give the reference's tile lists bit for bit,
+ * rasterizer.cpp:127-168). TILE_LOCAL (default): per-tile (depth, gid) sort
+ * in shared memory, falling back to GLOBAL for a frame once any tile holds
+ * more than 8192 entries. GLOBAL: global stable depth sort + rank-major
+ * duplication + stable tile sort. */
+#define GSB_BINNING_TILE_LOCAL 0
+#define GSB_BINNING_GLOBAL 1
+int gsb_ctx_set_binning(gsb_ctx* ctx, int32_t mode);
 /* Device time of the kernels launched on the context stream since the last
  * reset, split by stage (ms): preprocess, sort/bin, composite, loss,
  * backward raster, backward geometry, optimizer. Enabled by

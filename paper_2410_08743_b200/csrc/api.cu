@@ -42,6 +42,9 @@ int launch_duplicate(cudaStream_t st, const uint32_t* offs, SplatAux* aux, int64
                      int tiles_x, int64_t k_cap, uint32_t* ekey, uint32_t* eval, uint32_t* off_g);
 int launch_tile_ranges(cudaStream_t st, const uint32_t* ekey, int64_t k_cap, const uint32_t* k_dev, int n_tiles,
                        uint2* ranges);
+int launch_tile_bin(cudaStream_t st, gsb_frame* f, int64_t n, int64_t* launches);
+size_t bin_hist_words(int64_t n, int n_tiles);
+int init_bin_attributes();
 int launch_composite(cudaStream_t st, gsb_frame* f, const RasterDev& rc);
 int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc);
 int launch_backward_geom(cudaStream_t st, const gsb_cloud* cloud, gsb_frame* f, const RasterDev& rc, bool full,
@@ -54,7 +57,7 @@ int init_preprocess_attributes();
 int launch_pose_iter(cudaStream_t st, void* state, const double* dpose, const double* loss3, double lr_start,
                      double lr_end, double eps, int budget, CamDev* cam, double* trace_pose, double* trace_loss,
                      const uint32_t* k_dev, int64_t k_cap);
-int32_t pose_state_take_aborted(void* host_state);
+int32_t pose_state_take_aborted(void* host_state, uint32_t* k_max, uint32_t* tile_ovf);
 size_t pose_state_bytes();
 int pose_state_init(void* host_state, const double pose[12]);
 void pose_state_read(const void* host_state, double best_pose[12], double cur_pose[12], double* final_loss,
@@ -303,6 +306,10 @@ static int frame_reserve(gsb_frame* f, const gsb_cloud* cloud, int64_t k_cap) {
   bool grew = false;
   GSB_CUDA(f->cam.reserve(sizeof(CamDev), &grew));
   GSB_CUDA(f->counters.reserve(64, &grew));
+  GSB_CUDA(f->aux_g.reserve(sizeof(SplatAux) * n, &grew));
+  GSB_CUDA(f->tile_hist.reserve(sizeof(uint32_t) * bin_hist_words(n, n_tiles), &grew));
+  GSB_CUDA(f->tile_scan.reserve(sizeof(uint32_t) * scan_onepass_words(bin_hist_words(n, n_tiles)), &grew));
+  GSB_CUDA(f->tile_big.reserve(sizeof(uint32_t) * n_tiles, &grew));
   GSB_CUDA(f->rec_g.reserve(sizeof(SplatRec) * n, &grew));
   GSB_CUDA(f->rect_g.reserve(sizeof(uint2) * n, &grew));
   GSB_CUDA(f->cnt_g.reserve(sizeof(uint32_t) * np, &grew));  // n_pad: TMA-staged by 16 B
@@ -319,6 +326,8 @@ static int frame_reserve(gsb_frame* f, const gsb_cloud* cloud, int64_t k_cap) {
     GSB_CUDA(f->ekey[b].reserve(sizeof(uint32_t) * k_cap, &grew));
     GSB_CUDA(f->eval_[b].reserve(sizeof(uint32_t) * k_cap, &grew));
   }
+  GSB_CUDA(f->ent_key.reserve(sizeof(uint64_t) * k_cap, &grew));
+  GSB_CUDA(f->ent_gid.reserve(sizeof(uint32_t) * k_cap, &grew));
   GSB_CUDA(f->rec.reserve(sizeof(SplatRec) * n, &grew));
   GSB_CUDA(f->aux.reserve(sizeof(SplatAux) * n, &grew));
   GSB_CUDA(f->scan_tmp.reserve(sizeof(uint32_t) * (std::max(scan_onepass_words(n), scan_words(n)) + 64), &grew));
@@ -339,66 +348,86 @@ static int frame_reserve(gsb_frame* f, const gsb_cloud* cloud, int64_t k_cap) {
   if (grew) ++f->gen;
   f->k_cap = (int64_t)(f->ekey[0].bytes / sizeof(uint32_t));
   f->k_cap = std::min<int64_t>(f->k_cap, (int64_t)(f->partials.bytes / (sizeof(float) * kPartial)));
+  f->k_cap = std::min<int64_t>(f->k_cap, (int64_t)(f->ent_key.bytes / sizeof(uint64_t)));
+  f->k_cap = std::min<int64_t>(f->k_cap, (int64_t)(f->ent_gid.bytes / sizeof(uint32_t)));
+  f->k_cap = std::min<int64_t>(f->k_cap, 0xffffffffll);
+  return GSB_OK;
+}
+
+// Global depth order (reference rank order): compaction in index order, stable
+// depth sort (FP32 bits, 4 passes) + FP64 tie fix, rank-order records. Leaves
+// the rank-major entry offsets in *offs_out (a depth-key ping-pong buffer).
+static int rank_order_async(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, uint32_t** offs_out) {
+  cudaStream_t st = ctx->stream;
+  const int64_t n = cloud->n;
+  uint32_t* counters = f->counters.as<uint32_t>();
+  if (int r = scan_any(st, f->cnt_g.as<uint32_t>(), n, nullptr, true, f->cnt_r.as<uint32_t>(),
+                       f->scan_tmp.as<uint32_t>(), counters + 0, &ctx->launches))
+    return r;
+  if (int r = launch_compact(st, f->cnt_g.as<uint32_t>(), f->cnt_r.as<uint32_t>(), f->depth_g.as<double>(), n,
+                             f->vis_idx.as<uint32_t>(), f->dkey[0].as<uint32_t>(), f->dval[0].as<uint32_t>()))
+    return r;
+  ctx->launches += n > 0 ? 1 : 0;
+  uint32_t* dk[2] = {f->dkey[0].as<uint32_t>(), f->dkey[1].as<uint32_t>()};
+  uint32_t* dv[2] = {f->dval[0].as<uint32_t>(), f->dval[1].as<uint32_t>()};
+  int sel = 0;
+  if (int r = sort_any(st, dk, dv, n, counters + 0, 32, f->sort_hist.as<uint32_t>(), &sel, &ctx->launches)) return r;
+  if (int r = launch_depth_tie_fix(st, dk[sel], dv[sel], f->vis_idx.as<uint32_t>(), f->depth_g.as<double>(), n,
+                                   counters + 0))
+    return r;
+  ctx->launches += n > 1 ? 1 : 0;
+  if (int r = launch_gather_ranks(st, dv[sel], f->vis_idx.as<uint32_t>(), f->rec_g.as<SplatRec>(),
+                                  f->rect_g.as<uint2>(), f->cnt_g.as<uint32_t>(), n, counters + 0,
+                                  f->rec.as<SplatRec>(), f->aux.as<SplatAux>(), f->cnt_r.as<uint32_t>(),
+                                  f->rank_of_g.as<int32_t>()))
+    return r;
+  ctx->launches += n > 0 ? 1 : 0;
+  *offs_out = dk[sel ^ 1];
   return GSB_OK;
 }
 
 // The forward pass as a fixed launch sequence (no host synchronisation; live
-// counts V -> counters[0], K -> counters[1] stay on the device). Camera in f->cam.
+// counts V -> counters[0], K -> counters[1] stay on the device, counters[2]
+// flags a tile too large for tile-local binning). Camera in f->cam.
 static int render_async(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, const RasterDev& rc) {
   cudaStream_t st = ctx->stream;
   const int64_t n = cloud->n;
   const int n_tiles = f->tiles_x * f->tiles_y;
   uint32_t* counters = f->counters.as<uint32_t>();
+  const bool tile_local = f->binning == kBinTileLocal;
   {
     StageScope sc(ctx, kStPreprocess);
+    GSB_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(uint32_t), st));
     if (int r = launch_preprocess(st, cloud, f->cam.as<CamDev>(), rc, f)) return r;
     ctx->launches += n > 0 ? 1 : 0;
   }
   {
     StageScope sc(ctx, kStSort);
-    // 1. compaction in index order (visible slot of Gaussian i -> cnt_r[i])
-    if (int r = scan_any(st, f->cnt_g.as<uint32_t>(), n, nullptr, true, f->cnt_r.as<uint32_t>(),
-                         f->scan_tmp.as<uint32_t>(), counters + 0, &ctx->launches))
-      return r;
-    if (int r = launch_compact(st, f->cnt_g.as<uint32_t>(), f->cnt_r.as<uint32_t>(), f->depth_g.as<double>(), n,
-                               f->vis_idx.as<uint32_t>(), f->dkey[0].as<uint32_t>(), f->dval[0].as<uint32_t>()))
-      return r;
-    ctx->launches += n > 0 ? 1 : 0;
-    // 2. stable depth sort (FP32 bits, 4 passes) + FP64 tie fix
-    uint32_t* dk[2] = {f->dkey[0].as<uint32_t>(), f->dkey[1].as<uint32_t>()};
-    uint32_t* dv[2] = {f->dval[0].as<uint32_t>(), f->dval[1].as<uint32_t>()};
-    int sel = 0;
-    if (int r = sort_any(st, dk, dv, n, counters + 0, 32, f->sort_hist.as<uint32_t>(), &sel, &ctx->launches))
-      return r;
-    if (int r = launch_depth_tie_fix(st, dk[sel], dv[sel], f->vis_idx.as<uint32_t>(), f->depth_g.as<double>(), n,
-                                     counters + 0))
-      return r;
-    ctx->launches += n > 1 ? 1 : 0;
-    // 3. rank-order records; entry counts -> rank-major offsets (into dk[sel^1])
-    if (int r = launch_gather_ranks(st, dv[sel], f->vis_idx.as<uint32_t>(), f->rec_g.as<SplatRec>(),
-                                    f->rect_g.as<uint2>(), f->cnt_g.as<uint32_t>(), n, counters + 0,
-                                    f->rec.as<SplatRec>(), f->aux.as<SplatAux>(), f->cnt_r.as<uint32_t>(),
-                                    f->rank_of_g.as<int32_t>()))
-      return r;
-    ctx->launches += n > 0 ? 1 : 0;
-    uint32_t* offs = dk[sel ^ 1];
-    if (int r = scan_any(st, f->cnt_r.as<uint32_t>(), n, counters + 0, false, offs, f->scan_tmp.as<uint32_t>(),
-                         counters + 1, &ctx->launches))
-      return r;
-    // 4. duplicate (tile, rank) entries, stable sort by tile, ranges
-    if (int r = launch_duplicate(st, offs, f->aux.as<SplatAux>(), n, counters + 0, f->tiles_x, f->k_cap,
-                                 f->ekey[0].as<uint32_t>(), f->eval_[0].as<uint32_t>(), f->off_g.as<uint32_t>()))
-      return r;
-    ctx->launches += n > 0 ? 1 : 0;
-    uint32_t* ek[2] = {f->ekey[0].as<uint32_t>(), f->ekey[1].as<uint32_t>()};
-    uint32_t* ev[2] = {f->eval_[0].as<uint32_t>(), f->eval_[1].as<uint32_t>()};
-    int esel = 0;
-    if (int r = sort_any(st, ek, ev, f->k_cap, counters + 1, tile_bits(n_tiles), f->sort_hist.as<uint32_t>(), &esel,
-                         &ctx->launches))
-      return r;
-    f->sorted_sel = esel;
-    if (int r = launch_tile_ranges(st, ek[esel], f->k_cap, counters + 1, n_tiles, f->ranges.as<uint2>())) return r;
-    ctx->launches += n_tiles > 0 ? 1 : 0;
+    if (tile_local) {
+      // tile ranges from the preprocess counts, scatter, per-tile (depth, gid) sort
+      if (int r = launch_tile_bin(st, f, n, &ctx->launches)) return r;
+    } else {
+      uint32_t* offs = nullptr;
+      if (int r = rank_order_async(ctx, cloud, f, &offs)) return r;
+      if (int r = scan_any(st, f->cnt_r.as<uint32_t>(), n, counters + 0, false, offs, f->scan_tmp.as<uint32_t>(),
+                           counters + 1, &ctx->launches))
+        return r;
+      // duplicate (tile, rank) entries, stable sort by tile, ranges
+      if (int r = launch_duplicate(st, offs, f->aux.as<SplatAux>(), n, counters + 0, f->tiles_x, f->k_cap,
+                                   f->ekey[0].as<uint32_t>(), f->eval_[0].as<uint32_t>(), f->off_g.as<uint32_t>()))
+        return r;
+      ctx->launches += n > 0 ? 1 : 0;
+      uint32_t* ek[2] = {f->ekey[0].as<uint32_t>(), f->ekey[1].as<uint32_t>()};
+      uint32_t* ev[2] = {f->eval_[0].as<uint32_t>(), f->eval_[1].as<uint32_t>()};
+      int esel = 0;
+      if (int r = sort_any(st, ek, ev, f->k_cap, counters + 1, tile_bits(n_tiles), f->sort_hist.as<uint32_t>(),
+                           &esel, &ctx->launches))
+        return r;
+      f->sorted_sel = esel;
+      if (int r = launch_tile_ranges(st, ek[esel], f->k_cap, counters + 1, n_tiles, f->ranges.as<uint2>())) return r;
+      ctx->launches += n_tiles > 0 ? 1 : 0;
+    }
+    f->ranks_valid = !tile_local;
   }
   {
     StageScope sc(ctx, kStComposite);
@@ -408,6 +437,14 @@ static int render_async(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, cons
   return GSB_OK;
 }
 
+// A tile held more entries than the per-tile sort takes: this frame uses the
+// global binning path from now on (buffers unchanged; graphs are rebuilt).
+static void fall_back_to_global(gsb_frame* f) {
+  f->fallback_global = true;
+  f->binning = kBinGlobal;
+  ++f->gen;
+}
+
 // Synchronous forward for the host API: runs the async pass, reads (V, K)
 // and re-runs with a larger entry capacity if K overflowed it.
 static int render_sync(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, const RasterDev& rc) {
@@ -415,10 +452,14 @@ static int render_sync(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, const
   for (int attempt = 0; attempt < 4; ++attempt) {
     if (int r = frame_reserve(f, cloud, want)) return r;
     if (int r = render_async(ctx, cloud, f, rc)) return r;
-    uint32_t cnt[2];
-    if (int r = read_counters(ctx, f->counters.as<uint32_t>(), cnt, 2)) return r;
+    uint32_t cnt[3];
+    if (int r = read_counters(ctx, f->counters.as<uint32_t>(), cnt, 3)) return r;
     f->n_splats = cnt[0];
     f->n_entries = cnt[1];
+    if (cnt[2] != 0u) {
+      fall_back_to_global(f);
+      continue;
+    }
     if ((int64_t)cnt[1] <= f->k_cap) return GSB_OK;
     want = (int64_t)cnt[1] + (int64_t)cnt[1] / 4 + 4096;
   }
@@ -435,6 +476,13 @@ static int frame_setup(gsb_ctx* ctx, gsb_frame* f, const gsb_cloud* cloud, const
   if (f->tiles_x > 65535 || f->tiles_y > 65535) return fail(GSB_ERR_INVALID_ARGUMENT, "image too large");
   f->camera = *cam;
   f->config = *cfg;
+  const bool local_ok = (int64_t)f->tiles_x * f->tiles_y <= kBinMaxTiles;  // per-tile counters fit shared memory
+  const int binning =
+      (ctx->binning == kBinGlobal || f->fallback_global || !local_ok) ? kBinGlobal : kBinTileLocal;
+  if (binning != f->binning) {
+    f->binning = binning;
+    ++f->gen;
+  }
   for (int c = 0; c < 3; ++c) f->background[c] = bg ? bg[c] : 0.0;
   f->n_gaussians = cloud->n;
   f->cloud = cloud;
@@ -573,6 +621,10 @@ int gsb_ctx_create(int32_t device, gsb_ctx** out) {
     gsb_ctx_destroy(c);
     return r;
   }
+  if (int r = init_bin_attributes()) {
+    gsb_ctx_destroy(c);
+    return r;
+  }
   *out = c;
   return GSB_OK;
 }
@@ -595,6 +647,14 @@ int gsb_ctx_destroy(gsb_ctx* ctx) {
 int gsb_ctx_synchronize(gsb_ctx* ctx) {
   if (int r = ensure_device(ctx)) return r;
   GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return GSB_OK;
+}
+
+int gsb_ctx_set_binning(gsb_ctx* ctx, int32_t mode) {
+  if (int r = ensure_device(ctx)) return r;
+  if (mode != GSB_BINNING_TILE_LOCAL && mode != GSB_BINNING_GLOBAL)
+    return fail(GSB_ERR_INVALID_ARGUMENT, "unknown binning mode");
+  ctx->binning = mode == GSB_BINNING_GLOBAL ? kBinGlobal : kBinTileLocal;
   return GSB_OK;
 }
 
@@ -781,6 +841,8 @@ int gsb_frame_get_info(gsb_frame* f, gsb_frame_info* info) {
   info->tiles_x = f->tiles_x;
   info->tiles_y = f->tiles_y;
   info->state_fingerprint = f->fingerprint;
+  info->binning = f->binning == kBinGlobal ? GSB_BINNING_GLOBAL : GSB_BINNING_TILE_LOCAL;
+  info->reserved = 0;
   return GSB_OK;
 }
 
@@ -799,6 +861,13 @@ int gsb_frame_download(gsb_frame* f, double* image, double* accum_t, double* fin
   std::vector<uint32_t> ps(P);
   GSB_CUDA(cudaMemcpyAsync(ft.data(), f->final_t.p, sizeof(float) * P, cudaMemcpyDeviceToHost, ctx->stream));
   GSB_CUDA(cudaMemcpyAsync(ps.data(), f->pixstate.p, sizeof(uint32_t) * P, cudaMemcpyDeviceToHost, ctx->stream));
+  if (!f->ranks_valid && f->cloud) {
+    // tile-local frames never build the global rank order; materialise it
+    // (the reference's ProjectedSplat order) for the export
+    uint32_t* offs = nullptr;
+    if (int r = rank_order_async(ctx, f->cloud, f, &offs)) return r;
+    f->ranks_valid = true;
+  }
   std::vector<SplatRec> rec(V);
   std::vector<SplatAux> aux(V);
   if (V > 0) {
@@ -812,12 +881,18 @@ int gsb_frame_download(gsb_frame* f, double* image, double* accum_t, double* fin
     GSB_CUDA(cudaMemcpyAsync(radius_g.data(), f->radius_g.p, sizeof(double) * f->n_gaussians,
                              cudaMemcpyDeviceToHost, ctx->stream));
   }
-  if (tile_lists && K > 0)
-    GSB_CUDA(cudaMemcpyAsync(tile_lists, f->eval_[f->sorted_sel].p, sizeof(uint32_t) * K, cudaMemcpyDeviceToHost,
-                             ctx->stream));
+  std::vector<int32_t> rank_of(f->binning == kBinTileLocal && tile_lists ? f->n_gaussians : 0);
+  if (tile_lists && K > 0) {
+    GSB_CUDA(cudaMemcpyAsync(tile_lists, f->list(), sizeof(uint32_t) * K, cudaMemcpyDeviceToHost, ctx->stream));
+    if (!rank_of.empty())
+      GSB_CUDA(cudaMemcpyAsync(rank_of.data(), f->rank_of_g.p, sizeof(int32_t) * rank_of.size(),
+                               cudaMemcpyDeviceToHost, ctx->stream));
+  }
   if (tile_ranges && T > 0)
     GSB_CUDA(cudaMemcpyAsync(tile_ranges, f->ranges.p, sizeof(uint2) * T, cudaMemcpyDeviceToHost, ctx->stream));
   GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (!rank_of.empty())  // tile-local lists hold gids: export them as ranks
+    for (int64_t e = 0; e < K; ++e) tile_lists[e] = rank_of[(uint32_t)tile_lists[e]];
   for (int64_t p = 0; p < P; ++p) {
     if (final_t) final_t[p] = ft[p];
     if (accum_t) accum_t[p] = 1.0 - (double)ft[p];  // rasterizer.cpp:271-273
@@ -1285,22 +1360,25 @@ static int session_sync(gsb_ctx* ctx, gsb_session* s) {
     gsb_frame* f = work_frame(ctx);
     GSB_CUDA(cudaMemcpyAsync(s->host_state, s->state.p, sb, cudaMemcpyDeviceToHost, ctx->stream));
     if (f->counters.p)
-      GSB_CUDA(cudaMemcpyAsync(s->host_counters, f->counters.p, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+      GSB_CUDA(cudaMemcpyAsync(s->host_counters, f->counters.p, 3 * sizeof(uint32_t), cudaMemcpyDeviceToHost,
                                ctx->stream));
     GSB_CUDA(cudaStreamSynchronize(ctx->stream));
     pose_state_read(s->host_state, nullptr, nullptr, nullptr, nullptr, nullptr, &s->stopped, nullptr, nullptr, nullptr,
                     nullptr);
-    const int32_t aborted = pose_state_take_aborted(s->host_state);
+    uint32_t abort_k = 0, abort_tile = 0;
+    const int32_t aborted = pose_state_take_aborted(s->host_state, &abort_k, &abort_tile);
     s->n_splats = s->host_counters[0];
     s->n_entries = s->host_counters[1];
     if (aborted == 0) {
       s->pending = 0;
       return GSB_OK;
     }
-    // clear the device-side abort counter, grow the entry capacity, replay
+    // clear the device-side abort counter, grow the entry capacity (or leave
+    // tile-local binning), replay
     GSB_CUDA(cudaMemcpyAsync(s->state.p, s->host_state, sb, cudaMemcpyHostToDevice, ctx->stream));
-    const int64_t k = (int64_t)s->host_counters[1];
-    if (int r = frame_reserve(f, s->cloud, k + k / 4 + 4096)) return r;
+    if (abort_tile != 0u) fall_back_to_global(f);
+    const int64_t k = std::max<int64_t>(abort_k, s->host_counters[1]);
+    if (int r = frame_reserve(f, s->cloud, std::max<int64_t>(f->k_cap, k + k / 4 + 4096))) return r;
     s->pending = 0;
     if (int r = session_launch(ctx, s, aborted)) return r;
   }
@@ -1425,6 +1503,7 @@ int gsb_session_frame_info(gsb_session* s, gsb_frame_info* info) {
   info->height = s->cam.height;
   info->tiles_x = (s->cam.width + kTile - 1) / kTile;
   info->tiles_y = (s->cam.height + kTile - 1) / kTile;
+  if (s->ctx->work) info->binning = s->ctx->work->binning == kBinGlobal ? GSB_BINNING_GLOBAL : GSB_BINNING_TILE_LOCAL;
   return GSB_OK;
 }
 

@@ -143,6 +143,18 @@ struct DevBuf {
   }
 };
 
+// K2 binning modes. Tile-local (default): per-tile entry counts and entry
+// slots come out of preprocess, entries are scattered into their tile's
+// range, and each tile's list is sorted by (FP64 depth, gid) in shared memory
+// (k_bin.cu). Global: compaction + global stable depth sort + rank-major
+// duplication + stable tile sort (k_sort.cu) — used when some tile holds more
+// entries than the per-tile sort's capacity, and to materialise the
+// reference's rank order for the splat-list export.
+enum Binning : int { kBinTileLocal = 0, kBinGlobal = 1 };
+constexpr int kTileSortSmall = 2048;  // entries per tile sorted by the 256-thread CTA (49 KB shared)
+constexpr int kTileSortLarge = 8192;  // ... by the 512-thread persistent CTA (161 KB shared)
+constexpr int kBinMaxTiles = 16384;   // per-tile counters held in shared memory (else global binning)
+
 // Stage ids for the per-stage device timers (bench roofline attribution).
 enum Stage : int {
   kStPreprocess = 0, kStSort, kStComposite, kStLoss, kStBwdRaster, kStBwdGeom, kStOptim, kStOther, kNumStages
@@ -166,6 +178,7 @@ struct gsb_ctx {
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
   gsb_frame* work = nullptr;   // scratch forward state shared by sessions
   cudaEvent_t (*stage_events)[2] = nullptr;  // set while capturing a profiled session graph
+  int binning = 0;             // gsb::Binning preference (gsb_ctx_set_binning)
 };
 
 struct gsb_cloud {
@@ -255,5 +268,25 @@ struct gsb_frame {
   // scan / sort scratch
   gsb::DevBuf scan_tmp;
   gsb::DevBuf sort_hist;
-  gsb::DevBuf counters;   // uint32/uint64 device counters
+  gsb::DevBuf counters;   // uint32 device counters: V, K, tile overflow flag
+  // tile-local binning
+  int binning = gsb::kBinTileLocal;
+  bool fallback_global = false;  // a tile overflowed the per-tile sort: stay global
+  gsb::DevBuf aux_g;      // SplatAux per Gaussian (slot base, tile rect)
+  gsb::DevBuf tile_hist;  // uint32 [tiles][chunks] entry counts -> run offsets (+ total)
+  gsb::DevBuf tile_scan;  // look-back scan status words
+  gsb::DevBuf tile_big;   // uint32 tiles for the large per-tile sort (count in counters[3])
+  gsb::DevBuf ent_key;    // uint64 (FP64 depth high word << 32 | gid) per entry, tile grouped
+  gsb::DevBuf ent_gid;    // uint32 gid per entry -> depth-sorted tile lists
+  bool ranks_valid = false;  // rank-order arrays (rec, aux, rank_of_g) hold this frame
+  // what the raster kernels read: tile lists of record ids, records, aux
+  const uint32_t* list() const {
+    return binning == gsb::kBinTileLocal ? ent_gid.as<uint32_t>() : eval_[sorted_sel].as<uint32_t>();
+  }
+  const gsb::SplatRec* list_rec() const {
+    return binning == gsb::kBinTileLocal ? rec_g.as<gsb::SplatRec>() : rec.as<gsb::SplatRec>();
+  }
+  const gsb::SplatAux* list_aux() const {
+    return binning == gsb::kBinTileLocal ? aux_g.as<gsb::SplatAux>() : aux.as<gsb::SplatAux>();
+  }
 };

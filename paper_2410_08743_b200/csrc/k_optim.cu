@@ -31,7 +31,9 @@ struct PoseState {
   double best_loss, final_loss;
   double applied[6];
   int32_t iter, steps_used, converged, stop;
-  int32_t aborted;  // iterations discarded because the entry capacity overflowed
+  int32_t aborted;         // iterations discarded (entry capacity / per-tile sort overflow)
+  uint32_t abort_k_max;    // largest K seen by a discarded iteration
+  uint32_t abort_tile_ovf; // a discarded iteration had a tile beyond the per-tile sort
   int32_t pad;
 };
 
@@ -215,8 +217,12 @@ __global__ void pose_iter_kernel(PoseState* st, const double* __restrict__ dpose
                                  const uint32_t* __restrict__ k_dev, int64_t k_cap) {
   PoseState s = *st;
   if (s.stop) return;
-  if ((int64_t)*k_dev > k_cap) {  // entry capacity overflow: discard, the host re-runs it
+  // k_dev = {K, tile overflow flag}: the entry capacity or the per-tile sort
+  // overflowed — discard the iteration; the host fixes the cause and re-runs it
+  if ((int64_t)k_dev[0] > k_cap || k_dev[1] != 0u) {
     st->aborted = s.aborted + 1;
+    st->abort_k_max = max(s.abort_k_max, k_dev[0]);
+    st->abort_tile_ovf = s.abort_tile_ovf | k_dev[1];
     return;
   }
   const int it = s.iter;
@@ -370,10 +376,14 @@ void pose_state_read(const void* host_state, double best_pose[12], double cur_po
   }
   if (step) *step = s->step;
 }
-int32_t pose_state_take_aborted(void* host_state) {
+int32_t pose_state_take_aborted(void* host_state, uint32_t* k_max, uint32_t* tile_ovf) {
   PoseState* s = static_cast<PoseState*>(host_state);
   const int32_t a = s->aborted;
+  *k_max = s->abort_k_max;
+  *tile_ovf = s->abort_tile_ovf;
   s->aborted = 0;
+  s->abort_k_max = 0;
+  s->abort_tile_ovf = 0;
   return a;
 }
 void pose_state_set_adam(void* host_state, const double m[6], const double v[6], int64_t step) {

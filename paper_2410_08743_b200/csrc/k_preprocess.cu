@@ -131,7 +131,8 @@ __global__ void __launch_bounds__(kPreBlock) preprocess_kernel(
     const float* __restrict__ params, int64_t n, int64_t n_pad_g, int sh_cap, int sh_active,
     const CamDev* __restrict__ cam_p, RasterDev rc, SplatRec* __restrict__ rec_g, uint2* __restrict__ rect_g,
     uint32_t* __restrict__ cnt_g, double* __restrict__ depth_g, double* __restrict__ radius_g,
-    int32_t* __restrict__ rank_of_g, float* __restrict__ colj) {
+    int32_t* __restrict__ rank_of_g, float* __restrict__ colj, uint32_t* __restrict__ counters,
+    bool tile_local, SplatAux* __restrict__ aux_g, uint32_t* __restrict__ off_g) {
   extern __shared__ __align__(128) float s_par[];  // [planes][kPreBlock]
   __shared__ CamDev cam;
   __shared__ __align__(8) uint64_t bar;
@@ -148,112 +149,147 @@ __global__ void __launch_bounds__(kPreBlock) preprocess_kernel(
   __syncthreads();
   mbar_wait(&bar, 0);
   const int64_t i = i0 + threadIdx.x;
-  if (i >= n) return;
-  rank_of_g[i] = -1;
-  const float* P = s_par + threadIdx.x;
-  constexpr int64_t n_pad = kPreBlock;  // plane stride of the staged copy
-  const double mx = P[kMeanX * n_pad], my = P[kMeanY * n_pad], mz = P[kMeanZ * n_pad];
-  // Se3Pose::act: rotation * p + translation (lie.hpp:38)
-  const double cx = a_(dot3(cam.R[0], cam.R[1], cam.R[2], mx, my, mz), cam.t[0]);
-  const double cy = a_(dot3(cam.R[3], cam.R[4], cam.R[5], mx, my, mz), cam.t[1]);
-  const double cz = a_(dot3(cam.R[6], cam.R[7], cam.R[8], mx, my, mz), cam.t[2]);
   uint32_t cnt = 0;
-  if (cz > rc.z_near) {
-    // project (rasterizer.cpp:185-190)
-    const double u = a_(d_(m_(cam.fx, cx), cz), cam.cx);
-    const double v = a_(d_(m_(cam.fy, cy), cz), cam.cy);
-    if (isfinite(u) && isfinite(v)) {
-      // covariance3d: R(q) diag(s) (R(q) diag(s))^T
-      const double qw = P[kQuatW * n_pad], qx = P[kQuatX * n_pad], qy = P[kQuatY * n_pad], qz = P[kQuatZ * n_pad];
-      const double qn = __dsqrt_rn(a_(a_(a_(m_(qw, qw), m_(qx, qx)), m_(qy, qy)), m_(qz, qz)));
-      const double w = d_(qw, qn), x = d_(qx, qn), y = d_(qy, qn), z = d_(qz, qn);
-      double Rg[9];
-      Rg[0] = s_(1.0, m_(2.0, a_(m_(y, y), m_(z, z))));
-      Rg[1] = m_(2.0, s_(m_(x, y), m_(w, z)));
-      Rg[2] = m_(2.0, a_(m_(x, z), m_(w, y)));
-      Rg[3] = m_(2.0, a_(m_(x, y), m_(w, z)));
-      Rg[4] = s_(1.0, m_(2.0, a_(m_(x, x), m_(z, z))));
-      Rg[5] = m_(2.0, s_(m_(y, z), m_(w, x)));
-      Rg[6] = m_(2.0, s_(m_(x, z), m_(w, y)));
-      Rg[7] = m_(2.0, a_(m_(y, z), m_(w, x)));
-      Rg[8] = s_(1.0, m_(2.0, a_(m_(x, x), m_(y, y))));
-      const double sx = exp((double)P[kScaleX * n_pad]), sy = exp((double)P[kScaleY * n_pad]),
-                   sz = exp((double)P[kScaleZ * n_pad]);
-      double M[9];
-      for (int r = 0; r < 3; ++r) {
-        M[r * 3 + 0] = m_(Rg[r * 3 + 0], sx);
-        M[r * 3 + 1] = m_(Rg[r * 3 + 1], sy);
-        M[r * 3 + 2] = m_(Rg[r * 3 + 2], sz);
-      }
-      double S[9];
-      for (int r = 0; r < 3; ++r)
-        for (int c = 0; c < 3; ++c) S[r * 3 + c] = dot3(M[r * 3], M[r * 3 + 1], M[r * 3 + 2], M[c * 3], M[c * 3 + 1], M[c * 3 + 2]);
-      // projection_jacobian (rasterizer.cpp:31-39)
-      const double iz = d_(1.0, cz);
-      const double iz2 = m_(iz, iz);
-      const double J00 = m_(cam.fx, iz), J02 = m_(m_(-cam.fx, cx), iz2);
-      const double J11 = m_(cam.fy, iz), J12 = m_(m_(-cam.fy, cy), iz2);
-      // m = J R (2x3); row0 = J00*R0 + 0*R1 + J02*R2
-      double m[6];
-      for (int c = 0; c < 3; ++c) {
-        m[c] = a_(a_(m_(J00, cam.R[c]), m_(0.0, cam.R[3 + c])), m_(J02, cam.R[6 + c]));
-        m[3 + c] = a_(a_(m_(0.0, cam.R[c]), m_(J11, cam.R[3 + c])), m_(J12, cam.R[6 + c]));
-      }
-      double ms[6];
-      for (int r = 0; r < 2; ++r)
-        for (int c = 0; c < 3; ++c) ms[r * 3 + c] = dot3(m[r * 3], m[r * 3 + 1], m[r * 3 + 2], S[c], S[3 + c], S[6 + c]);
-      double cov[4];
-      for (int r = 0; r < 2; ++r)
-        for (int c = 0; c < 2; ++c) cov[r * 2 + c] = dot3(ms[r * 3], ms[r * 3 + 1], ms[r * 3 + 2], m[c * 3], m[c * 3 + 1], m[c * 3 + 2]);
-      cov[0] = a_(cov[0], rc.dilation);
-      cov[3] = a_(cov[3], rc.dilation);
-      // max_eigenvalue_2x2 + radius
-      const double mid = m_(0.5, a_(cov[0], cov[3]));
-      const double diff = m_(0.5, s_(cov[0], cov[3]));
-      const double lmax = a_(mid, __dsqrt_rn(a_(m_(diff, diff), m_(cov[1], cov[2]))));
-      const double radius = m_(rc.cutoff_sigma, __dsqrt_rn(lmax));
-      if (radius > 0.0 && isfinite(radius) && !(a_(u, radius) < 0.0) && !(s_(u, radius) > cam.width - 1) &&
-          !(a_(v, radius) < 0.0) && !(s_(v, radius) > cam.height - 1)) {
-        // invert_spd2
-        const double det = s_(m_(cov[0], cov[3]), m_(cov[1], cov[2]));
-        const double ca = d_(cov[3], det), cb = d_(-cov[1], det), cc2 = d_(-cov[2], det), cd = d_(cov[0], det);
-        // colour: sh_eval at dir = normalize(mean - center)
-        double dx = s_(mx, cam.center[0]), dy = s_(my, cam.center[1]), dz = s_(mz, cam.center[2]);
-        const double dn = __dsqrt_rn(a_(a_(m_(dx, dx), m_(dy, dy)), m_(dz, dz)));
-        dx = d_(dx, dn);
-        dy = d_(dy, dn);
-        dz = d_(dz, dn);
-        float col[3], G[9];
-        uint32_t clamp = 0;
-        sh_colour<DEG, kQuirk>(P, n_pad, sh_cap, (float)dx, (float)dy, (float)dz, col, &clamp, G);
-        for (int k = 0; k < 9; ++k) colj[(int64_t)k * n_pad_g + i] = G[k];
-        const double op = d_(1.0, a_(1.0, exp(-(double)P[kOpacity * n_pad])));
-        // tile span (rasterizer.cpp:138-146)
-        const double tile = (double)kTile;
-        const int tx0 = clamp_tile(floor(d_(s_(u, radius), tile)), cam.tiles_x);
-        const int tx1 = clamp_tile(floor(d_(a_(u, radius), tile)), cam.tiles_x);
-        const int ty0 = clamp_tile(floor(d_(s_(v, radius), tile)), cam.tiles_y);
-        const int ty1 = clamp_tile(floor(d_(a_(v, radius), tile)), cam.tiles_y);
-        cnt = ((uint32_t)(tx1 - tx0 + 1) * (uint32_t)(ty1 - ty0 + 1)) | (clamp << kClampShift);
-        SplatRec rec;
-        rec.mu_x = u;
-        rec.mu_y = v;
-        rec.conic_a = (float)ca;
-        rec.conic_b = (float)(0.5 * (cb + cc2));
-        rec.conic_c = (float)cd;
-        rec.opacity = (float)op;
-        rec.col_r = col[0];
-        rec.col_g = col[1];
-        rec.col_b = col[2];
-        rec.clamp_bits = clamp;
-        rec_g[i] = rec;
-        rect_g[i] = make_uint2((uint32_t)tx0 | ((uint32_t)tx1 << 16), (uint32_t)ty0 | ((uint32_t)ty1 << 16));
-        depth_g[i] = cz;
-        radius_g[i] = radius;
+  uint32_t rect_x = 0, rect_y = 0;  // tx0 | tx1 << 16, ty0 | ty1 << 16
+  if (i < n) {
+    rank_of_g[i] = -1;
+    const float* P = s_par + threadIdx.x;
+    constexpr int64_t n_pad = kPreBlock;  // plane stride of the staged copy
+    const double mx = P[kMeanX * n_pad], my = P[kMeanY * n_pad], mz = P[kMeanZ * n_pad];
+    // Se3Pose::act: rotation * p + translation (lie.hpp:38)
+    const double cx = a_(dot3(cam.R[0], cam.R[1], cam.R[2], mx, my, mz), cam.t[0]);
+    const double cy = a_(dot3(cam.R[3], cam.R[4], cam.R[5], mx, my, mz), cam.t[1]);
+    const double cz = a_(dot3(cam.R[6], cam.R[7], cam.R[8], mx, my, mz), cam.t[2]);
+    if (cz > rc.z_near) {
+      // project (rasterizer.cpp:185-190)
+      const double u = a_(d_(m_(cam.fx, cx), cz), cam.cx);
+      const double v = a_(d_(m_(cam.fy, cy), cz), cam.cy);
+      if (isfinite(u) && isfinite(v)) {
+        // covariance3d: R(q) diag(s) (R(q) diag(s))^T
+        const double qw = P[kQuatW * n_pad], qx = P[kQuatX * n_pad], qy = P[kQuatY * n_pad], qz = P[kQuatZ * n_pad];
+        const double qn = __dsqrt_rn(a_(a_(a_(m_(qw, qw), m_(qx, qx)), m_(qy, qy)), m_(qz, qz)));
+        const double w = d_(qw, qn), x = d_(qx, qn), y = d_(qy, qn), z = d_(qz, qn);
+        double Rg[9];
+        Rg[0] = s_(1.0, m_(2.0, a_(m_(y, y), m_(z, z))));
+        Rg[1] = m_(2.0, s_(m_(x, y), m_(w, z)));
+        Rg[2] = m_(2.0, a_(m_(x, z), m_(w, y)));
+        Rg[3] = m_(2.0, a_(m_(x, y), m_(w, z)));
+        Rg[4] = s_(1.0, m_(2.0, a_(m_(x, x), m_(z, z))));
+        Rg[5] = m_(2.0, s_(m_(y, z), m_(w, x)));
+        Rg[6] = m_(2.0, s_(m_(x, z), m_(w, y)));
+        Rg[7] = m_(2.0, a_(m_(y, z), m_(w, x)));
+        Rg[8] = s_(1.0, m_(2.0, a_(m_(x, x), m_(y, y))));
+        const double sx = exp((double)P[kScaleX * n_pad]), sy = exp((double)P[kScaleY * n_pad]),
+                     sz = exp((double)P[kScaleZ * n_pad]);
+        double M[9];
+        for (int r = 0; r < 3; ++r) {
+          M[r * 3 + 0] = m_(Rg[r * 3 + 0], sx);
+          M[r * 3 + 1] = m_(Rg[r * 3 + 1], sy);
+          M[r * 3 + 2] = m_(Rg[r * 3 + 2], sz);
+        }
+        double S[9];
+        for (int r = 0; r < 3; ++r)
+          for (int c = 0; c < 3; ++c) S[r * 3 + c] = dot3(M[r * 3], M[r * 3 + 1], M[r * 3 + 2], M[c * 3], M[c * 3 + 1], M[c * 3 + 2]);
+        // projection_jacobian (rasterizer.cpp:31-39)
+        const double iz = d_(1.0, cz);
+        const double iz2 = m_(iz, iz);
+        const double J00 = m_(cam.fx, iz), J02 = m_(m_(-cam.fx, cx), iz2);
+        const double J11 = m_(cam.fy, iz), J12 = m_(m_(-cam.fy, cy), iz2);
+        // m = J R (2x3); row0 = J00*R0 + 0*R1 + J02*R2
+        double m[6];
+        for (int c = 0; c < 3; ++c) {
+          m[c] = a_(a_(m_(J00, cam.R[c]), m_(0.0, cam.R[3 + c])), m_(J02, cam.R[6 + c]));
+          m[3 + c] = a_(a_(m_(0.0, cam.R[c]), m_(J11, cam.R[3 + c])), m_(J12, cam.R[6 + c]));
+        }
+        double ms[6];
+        for (int r = 0; r < 2; ++r)
+          for (int c = 0; c < 3; ++c) ms[r * 3 + c] = dot3(m[r * 3], m[r * 3 + 1], m[r * 3 + 2], S[c], S[3 + c], S[6 + c]);
+        double cov[4];
+        for (int r = 0; r < 2; ++r)
+          for (int c = 0; c < 2; ++c) cov[r * 2 + c] = dot3(ms[r * 3], ms[r * 3 + 1], ms[r * 3 + 2], m[c * 3], m[c * 3 + 1], m[c * 3 + 2]);
+        cov[0] = a_(cov[0], rc.dilation);
+        cov[3] = a_(cov[3], rc.dilation);
+        // max_eigenvalue_2x2 + radius
+        const double mid = m_(0.5, a_(cov[0], cov[3]));
+        const double diff = m_(0.5, s_(cov[0], cov[3]));
+        const double lmax = a_(mid, __dsqrt_rn(a_(m_(diff, diff), m_(cov[1], cov[2]))));
+        const double radius = m_(rc.cutoff_sigma, __dsqrt_rn(lmax));
+        if (radius > 0.0 && isfinite(radius) && !(a_(u, radius) < 0.0) && !(s_(u, radius) > cam.width - 1) &&
+            !(a_(v, radius) < 0.0) && !(s_(v, radius) > cam.height - 1)) {
+          // invert_spd2
+          const double det = s_(m_(cov[0], cov[3]), m_(cov[1], cov[2]));
+          const double ca = d_(cov[3], det), cb = d_(-cov[1], det), cc2 = d_(-cov[2], det), cd = d_(cov[0], det);
+          // colour: sh_eval at dir = normalize(mean - center)
+          double dx = s_(mx, cam.center[0]), dy = s_(my, cam.center[1]), dz = s_(mz, cam.center[2]);
+          const double dn = __dsqrt_rn(a_(a_(m_(dx, dx), m_(dy, dy)), m_(dz, dz)));
+          dx = d_(dx, dn);
+          dy = d_(dy, dn);
+          dz = d_(dz, dn);
+          float col[3], G[9];
+          uint32_t clamp = 0;
+          sh_colour<DEG, kQuirk>(P, n_pad, sh_cap, (float)dx, (float)dy, (float)dz, col, &clamp, G);
+          for (int k = 0; k < 9; ++k) colj[(int64_t)k * n_pad_g + i] = G[k];
+          const double op = d_(1.0, a_(1.0, exp(-(double)P[kOpacity * n_pad])));
+          // tile span (rasterizer.cpp:138-146)
+          const double tile = (double)kTile;
+          const int tx0 = clamp_tile(floor(d_(s_(u, radius), tile)), cam.tiles_x);
+          const int tx1 = clamp_tile(floor(d_(a_(u, radius), tile)), cam.tiles_x);
+          const int ty0 = clamp_tile(floor(d_(s_(v, radius), tile)), cam.tiles_y);
+          const int ty1 = clamp_tile(floor(d_(a_(v, radius), tile)), cam.tiles_y);
+          cnt = ((uint32_t)(tx1 - tx0 + 1) * (uint32_t)(ty1 - ty0 + 1)) | (clamp << kClampShift);
+          SplatRec rec;
+          rec.mu_x = u;
+          rec.mu_y = v;
+          rec.conic_a = (float)ca;
+          rec.conic_b = (float)(0.5 * (cb + cc2));
+          rec.conic_c = (float)cd;
+          rec.opacity = (float)op;
+          rec.col_r = col[0];
+          rec.col_g = col[1];
+          rec.col_b = col[2];
+          rec.clamp_bits = clamp;
+          rec_g[i] = rec;
+          rect_x = (uint32_t)tx0 | ((uint32_t)tx1 << 16);
+          rect_y = (uint32_t)ty0 | ((uint32_t)ty1 << 16);
+          rect_g[i] = make_uint2(rect_x, rect_y);
+          depth_g[i] = cz;
+          radius_g[i] = radius;
+        }
       }
     }
+    cnt_g[i] = cnt;
   }
-  cnt_g[i] = cnt;
+  if (tile_local) {
+    // Tile-local binning (k_bin.cu): reserve this splat's entry slots with one
+    // atomic per warp (slot order is free — every consumer indexes them by
+    // (gid, tile) — so the result stays deterministic) and count V.
+    const uint32_t c = cnt & kCntMask, lane = threadIdx.x & 31u;
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (uint32_t)o) x += y;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, x, 31);
+    const uint32_t vis = __popc(__ballot_sync(0xffffffffu, c > 0u));
+    uint32_t base = 0;
+    if (lane == 0 && tot) {
+      base = atomicAdd(counters + 1, tot);
+      atomicAdd(counters + 0, vis);
+    }
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (c) {
+      const uint32_t off = base + x - c;
+      const uint32_t tx0 = rect_x & 0xffffu, tx1 = rect_x >> 16, ty0 = rect_y & 0xffffu, ty1 = rect_y >> 16;
+      SplatAux a;
+      a.off = off;
+      a.tx0_ty0 = tx0 | (ty0 << 16);
+      a.nx_ny = (tx1 - tx0 + 1u) | ((ty1 - ty0 + 1u) << 16);
+      a.gid = (int32_t)i;
+      aux_g[i] = a;
+      off_g[i] = off;
+    }
+  }
 }
 
 int launch_preprocess(cudaStream_t st, const gsb_cloud* cloud, const CamDev* cam, const RasterDev& rc,
@@ -261,12 +297,15 @@ int launch_preprocess(cudaStream_t st, const gsb_cloud* cloud, const CamDev* cam
   const int64_t n = cloud->n;
   const int deg = std::min(cloud->active_sh_degree, cloud->sh_degree);
   const bool quirk = deg < cloud->sh_degree;
+  const bool tile_local = f->binning == kBinTileLocal;
   const size_t smem = sizeof(float) * kPreBlock * num_planes(cloud->sh_degree);
 #define GSB_PRE(D, Q)                                                                                          \
   preprocess_kernel<D, Q><<<(unsigned)((n + kPreBlock - 1) / kPreBlock), kPreBlock, smem, st>>>(              \
       cloud->params.as<float>(), n, cloud->n_pad, cloud->sh_degree, cloud->active_sh_degree, cam, rc,          \
       f->rec_g.as<SplatRec>(), f->rect_g.as<uint2>(), f->cnt_g.as<uint32_t>(), f->depth_g.as<double>(),        \
-      f->radius_g.as<double>(), f->rank_of_g.as<int32_t>(), f->colj.as<float>())
+      f->radius_g.as<double>(), f->rank_of_g.as<int32_t>(), f->colj.as<float>(),                              \
+      f->counters.as<uint32_t>(), tile_local,    \
+      f->aux_g.as<SplatAux>(), f->off_g.as<uint32_t>())
   if (n > 0) {
     switch (deg * 2 + (quirk ? 1 : 0)) {
       case 0: GSB_PRE(0, false); break;

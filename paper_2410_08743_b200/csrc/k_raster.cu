@@ -413,7 +413,7 @@ int launch_composite(cudaStream_t st, gsb_frame* f, const RasterDev& rc) {
   const int64_t npix = (int64_t)f->width * f->height;
   if (n_tiles > 0)
     composite_kernel<<<n_tiles, kThreads, 0, st>>>(
-        f->ranges.as<uint2>(), f->eval_[f->sorted_sel].as<uint32_t>(), f->rec.as<SplatRec>(), f->cam.as<CamDev>(), rc,
+        f->ranges.as<uint2>(), f->list(), f->list_rec(), f->cam.as<CamDev>(), rc,
         (float)f->background[0], (float)f->background[1], (float)f->background[2], npix, f->image.as<float>(),
         f->final_t.as<float>(), f->pixstate.as<uint32_t>());
   GSB_CHECK_LAUNCH("composite_kernel");
@@ -425,7 +425,7 @@ int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc) {
   const int64_t npix = (int64_t)f->width * f->height;
   if (n_tiles > 0)
     backward_raster_kernel<<<n_tiles, kThreads, 0, st>>>(
-        f->ranges.as<uint2>(), f->eval_[f->sorted_sel].as<uint32_t>(), f->rec.as<SplatRec>(), f->aux.as<SplatAux>(),
+        f->ranges.as<uint2>(), f->list(), f->list_rec(), f->list_aux(),
         f->cam.as<CamDev>(), rc, (float)f->background[0], (float)f->background[1], (float)f->background[2], npix,
         f->d_image.as<float>(), f->final_t.as<float>(), f->pixstate.as<uint32_t>(), f->partials.as<float>(),
         (uint32_t)f->k_cap);

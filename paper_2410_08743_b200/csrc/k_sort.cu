@@ -23,6 +23,7 @@
 // (K > cap); the pose step then discards the iteration and the host re-runs
 // it with a larger capacity.
 #include "gsb_internal.cuh"
+#include <cstdlib>
 
 namespace gsb {
 
@@ -347,7 +348,9 @@ int radix_sort_pairs(cudaStream_t st, uint32_t* keys[2], uint32_t* vals[2], int6
     const int shift = p * bits;
     radix_hist_kernel<<<(unsigned)nblocks, kRadixThreads, 0, st>>>(keys[sel], cap, n_dev, shift, bits, hist, nblocks);
     // few tiles -> short look-back: the single-pass scan wins for histograms
-    int rc = scan_onepass(st, hist, nh, nullptr, false, hist, hist + nh, nullptr, launches);
+    static const bool legacy = [] { const char* e = std::getenv("GSB_HIST_SCAN"); return e && e[0] == 'l'; }();
+    int rc = legacy ? scan_exclusive(st, hist, nh, nullptr, false, hist, hist + nh, nullptr, launches)
+                    : scan_onepass(st, hist, nh, nullptr, false, hist, hist + nh, nullptr, launches);
     if (rc) return rc;
     radix_scatter_kernel<<<(unsigned)nblocks, kRadixThreads, 0, st>>>(keys[sel], vals[sel], keys[sel ^ 1],
                                                                       vals[sel ^ 1], cap, n_dev, shift, bits, hist,

@@ -89,7 +89,7 @@ class PoseAdam(C.Structure):
 class FrameInfo(C.Structure):
     _fields_ = [("n_gaussians", C.c_int64), ("n_splats", C.c_int64), ("n_entries", C.c_int64),
                 ("width", C.c_int32), ("height", C.c_int32), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32),
-                ("state_fingerprint", C.c_uint64)]
+                ("state_fingerprint", C.c_uint64), ("binning", C.c_int32), ("reserved", C.c_int32)]
 
 
 class PoseConfig(C.Structure):
@@ -125,6 +125,7 @@ def _sigs():
         "gsb_ctx_destroy": (C.c_int, [_vp]),
         "gsb_ctx_synchronize": (C.c_int, [_vp]),
         "gsb_ctx_set_profiling": (C.c_int, [_vp, i32]),
+        "gsb_ctx_set_binning": (C.c_int, [_vp, i32]),
         "gsb_ctx_stage_times": (C.c_int, [_vp, _vp, _vp, i32]),
         "gsb_ctx_launch_count": (i64, [_vp]),
         "gsb_cloud_create": (C.c_int, [_vp, i64, i32, P(_vp)]),
@@ -218,6 +219,13 @@ class Context:
 
     def synchronize(self):
         _check(lib().gsb_ctx_synchronize(self.h))
+
+    BINNING_TILE_LOCAL = 0
+    BINNING_GLOBAL = 1
+
+    def set_binning(self, mode: int):
+        """K2 strategy: BINNING_TILE_LOCAL (default) or BINNING_GLOBAL."""
+        _check(lib().gsb_ctx_set_binning(self.h, int(mode)))
 
     def set_profiling(self, on: bool):
         _check(lib().gsb_ctx_set_profiling(self.h, 1 if on else 0))

@@ -85,13 +85,22 @@ def test_render_matches_oracle_conditioned(G, ctx, seed):
     assert np.all(d["accum_transmittance"] + d["final_transmittance"] == 1.0)
 
 
-def test_binning_bit_exact_on_device_records(G, ctx):
+@pytest.fixture(params=["tile_local", "global"])
+def binning(request, G, ctx):
+    mode = G.Context.BINNING_TILE_LOCAL if request.param == "tile_local" else G.Context.BINNING_GLOBAL
+    ctx.set_binning(mode)
+    yield mode
+    ctx.set_binning(G.Context.BINNING_TILE_LOCAL)
+
+
+def test_binning_bit_exact_on_device_records(G, ctx, binning):
     """rasterizer.cpp:127-168 re-run on the GPU's own FP64 records must give
     the device tile lists / ranges bit for bit (C1-sized scene)."""
     hc, poses = synth_scene(99, 10000, 256, scale_offset=math.log(500 / 10000) / 3)
     cam = O.synth_camera(256, 256, poses[0])
     cloud = to_dev(G, ctx, hc)
     out = G.render(ctx, cloud, dev_cam(G, cam))
+    assert out.info().binning == binning
     d = out.download()
     n = hc.n
     keep = np.zeros(n, np.uint8)
@@ -116,7 +125,7 @@ def test_binning_bit_exact_on_device_records(G, ctx):
     assert np.array_equal(d["tile_ranges"], ref.tile_ranges)
 
 
-def test_binning_bit_exact_c2_scale(G, ctx):
+def test_binning_bit_exact_c2_scale(G, ctx, binning):
     """C2 shape (300k Gaussians, 1008x756, forward-facing): the device's
     depth order, tile lists and ranges equal rasterizer.cpp:127-168 re-run on
     the device's own FP64 records, across hundreds of 4096-item sort tiles
@@ -190,6 +199,44 @@ def test_repeat_render_bit_identical(G, ctx):
     b = G.render(ctx, cloud, dev_cam(G, ocam), bg).download()
     for k in ("image", "final_transmittance", "contrib_count", "tile_lists", "tile_ranges"):
         assert a[k].tobytes() == b[k].tobytes()
+
+
+def crowded_tile_scene(n, z_levels=None, seed=5):
+    """n small Gaussians projecting into the top-left 16x16 tile of a 64x64
+    image (identity pose): one tile list of ~n entries. z_levels quantises the
+    depths so most entries tie on depth (ties resolve by Gaussian index)."""
+    r = np.random.default_rng(seed)
+    z = r.uniform(2.0, 4.0, n) if z_levels is None else r.choice(np.asarray(z_levels, np.float64), n)
+    u, v = r.uniform(5.0, 11.0, n), r.uniform(5.0, 11.0, n)
+    fx = 40.0
+    means = np.stack([(u - 0.5) * z / fx, (v - 0.5) * z / fx, z], axis=1)
+    rot = r.normal(size=(n, 4))
+    rot /= np.linalg.norm(rot, axis=1, keepdims=True)
+    hc = O.HostCloud(means, rot, np.full((n, 3), math.log(0.002)) + r.uniform(-0.3, 0.3, (n, 3)),
+                     r.uniform(-4.0, -1.0, n), r.uniform(-0.5, 0.5, (n, 3, 1)), 0, 0)
+    cam = O.make_camera(fx, fx, 0.5, 0.5, 64, 64, np.eye(3), np.zeros(3))
+    return hc.as_float32_exact(), cam
+
+
+@pytest.mark.parametrize("n,z_levels,expect", [(1500, None, 0), (1500, [2.0, 3.0], 0), (6000, None, 0),
+                                                (6000, [2.0, 2.5, 3.0], 0), (20000, None, 1)])
+def test_crowded_tile_lists_bit_exact(G, ctx, n, z_levels, expect):
+    """Per-tile sort paths: small CTA (<= 2048 entries), large CTA (<= 8192,
+    incl. massive exact depth ties), and the fallback to global binning for a
+    tile beyond 8192 entries — tile lists equal the reference's each time."""
+    hc, cam = crowded_tile_scene(n, z_levels)
+    cloud = to_dev(G, ctx, hc)
+    out = G.render(ctx, cloud, dev_cam(G, cam), (0.1, 0.2, 0.3))
+    assert out.info().binning == expect
+    d = out.download()
+    ref = O.render(hc, cam, (0.1, 0.2, 0.3))
+    r0 = ref.tile_ranges.reshape(-1, 2)[0]
+    assert r0[1] - r0[0] > n * 0.9
+    assert np.array_equal(d["splat_gaussian"], ref.splat_gaussian)
+    assert np.array_equal(d["tile_lists"], ref.tile_lists)
+    assert np.array_equal(d["tile_ranges"], ref.tile_ranges)
+    assert np.array_equal(d["contrib_count"], ref.contrib_count)
+    assert np.max(np.abs(d["image"] - ref.image)) < 1e-4
 
 
 # -------------------------------------------------------------------- loss
