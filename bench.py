@@ -137,16 +137,15 @@ def run_ours(args, ws, rank, local):
     budget = max(100, args.warmup + 2 * args.steps + 4)
     cfg = gsb.PoseConfig.default(budget=budget, pose_converged_eps=0.0)
     sessions = [gsb.PoseSession(ctx, cloud, images[v], intr, init[v], cfg) for v in views]
+    batch = gsb.PoseBatch(ctx, sessions)
 
     def step():
-        for s in sessions:
-            s.step_async(1)  # one CUDA-graph replay per view; no host round trip
+        batch.step_async(1)  # one CUDA-graph replay advances every view one iteration; no host round trip
 
     for _ in range(args.warmup):
         step()
     ctx.synchronize()
-    for s in sessions:
-        s.read()  # re-runs any iteration discarded for entry-capacity growth
+    batch.sync()  # re-runs any iteration discarded for entry-capacity growth
     if dist:
         dist.barrier()
     clocks = ClockSampler(local)
@@ -160,10 +159,9 @@ def run_ours(args, ws, rank, local):
     wall_s = time.perf_counter() - t0
     launches = ctx.launch_count() - launches0
     clk = clocks.stop()
-    for s in sessions:
-        s.read()
-    # Attribution pass: the same steps again with per-stage CUDA events
-    # recorded inside every session graph, read back after each step.
+    batch.sync()
+    # Attribution pass: the same steps again, sessions one after another, with
+    # per-stage CUDA events recorded inside every session graph.
     ctx.set_profiling(True)
     for s in sessions:
         s.step_async(1)  # rebuilds the graphs with event nodes (untimed)
@@ -190,7 +188,9 @@ def run_ours(args, ws, rank, local):
     fi = sessions[0].frame_info()
     res = sessions[0].read()
 
-    # ---- e2e: gsb_estimate_pose from host FP64 images (the user-facing call)
+    batch.close()
+    # ---- e2e: gsb_estimate_poses from host FP64 images (the user-facing call
+    # for C3's independent views: one call per GPU over its views)
     e2e_iters = args.e2e_iters
     e2e_cfg = gsb.PoseConfig.default(budget=e2e_iters, pose_converged_eps=0.0)
     if dist:
@@ -198,13 +198,14 @@ def run_ours(args, ws, rank, local):
     ctx.synchronize()
     t0 = time.perf_counter()
     h2d = d2h = 0
+    imgs = []
     for v in views:
-        img = gsb.Image(ctx, host_targets[v])                 # H2D of the view's frame
-        out = gsb.estimate_pose(ctx, cloud, img, intr, init[v], e2e_cfg)
+        imgs.append(gsb.Image(ctx, host_targets[v]))          # H2D of the view's frame
         h2d += host_targets[v].size * 4 + 12 * 8            # FP32 planes uploaded + pose
-        d2h += 12 * 8 + 8 + 8                                 # pose, loss, steps/flags
-        assert out["steps"] == e2e_iters
-        del img
+        d2h += 12 * 8 + 8 + 4                                 # pose, loss, steps
+    out = gsb.estimate_poses(ctx, cloud, imgs, intr, init[views], e2e_cfg)
+    assert all(int(k) == e2e_iters for k in out["steps"])
+    del imgs
     ctx.synchronize()
     e2e_s = time.perf_counter() - t0
     if dist:
@@ -239,8 +240,8 @@ def run_ours(args, ws, rank, local):
                        "parallelism": f"views sharded over {ws} GPU(s), no collective"},
             "e2e": {"value": round(e2e_value, 3), "unit": "iters/s", "h2d_bytes_per_step": int(h2d * ws / e2e_iters),
                     "d2h_bytes_per_step": int(d2h * ws / e2e_iters),
-                    "how": f"gsb_estimate_pose per view from host FP64 HWC image, {e2e_iters} iterations; "
-                           "bytes per iteration-of-all-views"},
+                    "how": f"gsb_estimate_poses over the GPU's views from host FP64 HWC images, {e2e_iters} "
+                           "iterations; bytes per iteration-of-all-views"},
             "gpu_launches": int(launches),
             "clocks": clk,
             "roofline": roof,

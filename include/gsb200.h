@@ -248,6 +248,26 @@ int gsb_session_read(gsb_session* s, double pose[12], double best_pose[12], doub
 /* Forward-state sizes of the session's last iteration (V, K) for work accounting. */
 int gsb_session_frame_info(gsb_session* s, gsb_frame_info* info);
 
+/* ---- pose batch: several sessions advanced by one graph replay ----
+ * Config C3 (independent views of one cloud). Each session gets a private
+ * forward state for the batch's lifetime; one replay runs one pose_descent
+ * iteration of every session, the sessions' launch sequences being parallel
+ * branches of one CUDA graph. Per-session results are identical to stepping
+ * the sessions one by one. No reference counterpart: the reference runs
+ * estimate_pose once per view (pipelines.cpp:218-222). */
+typedef struct gsb_pose_batch gsb_pose_batch;
+int gsb_pose_batch_create(gsb_ctx* ctx, gsb_session* const* sessions, int32_t count, gsb_pose_batch** out);
+int gsb_pose_batch_destroy(gsb_pose_batch* b);
+int gsb_pose_batch_step(gsb_ctx* ctx, gsb_pose_batch* b, int32_t iterations);
+int gsb_pose_batch_step_async(gsb_ctx* ctx, gsb_pose_batch* b, int32_t iterations);
+/* waits for the batch; re-runs any iteration a session discarded (capacity growth) */
+int gsb_pose_batch_sync(gsb_ctx* ctx, gsb_pose_batch* b);
+/* estimate_pose for `count` views of one cloud as one pose batch: init_poses /
+ * poses_out are count x 12 (best pose per view); final_losses, steps_used optional. */
+int gsb_estimate_poses(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* const* targets, const double intr[4],
+                       const double* init_poses, int32_t count, const gsb_pose_config* cfg, double* poses_out,
+                       double* final_losses, int32_t* steps_used);
+
 #ifdef __cplusplus
 }
 #endif

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -159,6 +160,19 @@ struct StageScope {
 
 // --------------------------------------------------------------- helpers
 static int cuda_fail_or_ok(cudaError_t e) { return e == cudaSuccess ? GSB_OK : cuda_fail(e, "cudaMemcpy"); }
+
+// GSB_DEBUG=1: host-side events (graph captures, buffer growth, discarded
+// iterations, binning fallbacks) on stderr, for diagnosing e2e overheads.
+static bool debug_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("GSB_DEBUG");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+static double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
 
 static int ensure_device(gsb_ctx* ctx) {
   if (!ctx) return fail(GSB_ERR_INVALID_ARGUMENT, "null context");
@@ -345,7 +359,10 @@ static int frame_reserve(gsb_frame* f, const gsb_cloud* cloud, int64_t k_cap) {
   GSB_CUDA(f->partials.reserve(sizeof(float) * kPartial * k_cap, &grew));
   GSB_CUDA(f->pose_blocks.reserve(sizeof(double) * 6 * ((n + 255) / 256 + 1), &grew));
   GSB_CUDA(f->d_pose.reserve(sizeof(double) * 6, &grew));
-  if (grew) ++f->gen;
+  if (grew) {
+    ++f->gen;
+    if (debug_on()) std::fprintf(stderr, "[gsb] frame_reserve grew (k_cap request %lld)\n", (long long)k_cap);
+  }
   f->k_cap = (int64_t)(f->ekey[0].bytes / sizeof(uint32_t));
   f->k_cap = std::min<int64_t>(f->k_cap, (int64_t)(f->partials.bytes / (sizeof(float) * kPartial)));
   f->k_cap = std::min<int64_t>(f->k_cap, (int64_t)(f->ent_key.bytes / sizeof(uint64_t)));
@@ -637,6 +654,7 @@ int gsb_ctx_destroy(gsb_ctx* ctx) {
   if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
   delete ctx->timer;
   if (ctx->work) gsb_frame_destroy(ctx->work);
+  for (gsb_frame* f : ctx->frame_pool) gsb_frame_destroy(f);
   if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
   if (ctx->ev_stop) cudaEventDestroy(ctx->ev_stop);
   cudaStreamDestroy(ctx->stream);
@@ -809,7 +827,8 @@ int gsb_frame_destroy(gsb_frame* f) {
                     &f->colj, &f->off_g, &f->vis_idx, &f->dkey[0], &f->dkey[1], &f->dval[0], &f->dval[1], &f->rec, &f->aux,
                     &f->cnt_r, &f->ekey[0], &f->ekey[1], &f->eval_[0], &f->eval_[1], &f->ranges, &f->image,
                     &f->final_t, &f->pixstate, &f->d_image, &f->partials, &f->pose_blocks, &f->d_pose,
-                    &f->loss_blocks, &f->loss_val, &f->gmaps, &f->scan_tmp, &f->sort_hist, &f->counters};
+                    &f->loss_blocks, &f->loss_val, &f->gmaps, &f->scan_tmp, &f->sort_hist, &f->counters,
+                    &f->aux_g, &f->tile_hist, &f->tile_scan, &f->tile_big, &f->ent_key, &f->ent_gid};
   for (DevBuf* b : bufs) b->release();
   delete f;
   return GSB_OK;
@@ -1264,6 +1283,25 @@ struct gsb_session {
   bool graph_profiled = false;
   cudaEvent_t ev[kNumStages][2] = {};
   bool have_events = false;
+  gsb_frame* own = nullptr;      // private forward state while the session is in a pose batch
+  gsb_pose_batch* batch = nullptr;
+};
+
+// A pose batch advances several sessions by one pose_descent iteration per
+// graph replay: each session's launch sequence is a parallel branch of one
+// CUDA graph (fork/join over side streams), on its own forward state, so the
+// branches fill each other's wave tails and serial single-block kernels.
+struct gsb_pose_batch {
+  gsb_ctx* ctx = nullptr;
+  std::vector<gsb_session*> sessions;
+  std::vector<cudaStream_t> streams;
+  std::vector<cudaEvent_t> joins;
+  cudaEvent_t fork = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<uint64_t> graph_gen;
+  std::vector<int64_t> graph_kcap;
+  std::vector<int> graph_binning;
+  int64_t graph_launches = 0;
 };
 
 namespace gsb {
@@ -1290,6 +1328,7 @@ static int session_launch_iteration(gsb_ctx* ctx, gsb_session* s, gsb_frame* f) 
 }
 
 static int session_capture(gsb_ctx* ctx, gsb_session* s, gsb_frame* f) {
+  const double t_dbg = debug_on() ? now_ms() : 0.0;
   if (s->exec) {
     cudaGraphExecDestroy(s->exec);
     s->exec = nullptr;
@@ -1320,6 +1359,9 @@ static int session_capture(gsb_ctx* ctx, gsb_session* s, gsb_frame* f) {
   s->graph_gen = f->gen;
   s->graph_kcap = f->k_cap;
   s->graph_profiled = ctx->profiling;
+  if (debug_on())
+    std::fprintf(stderr, "[gsb] session graph captured: %lld kernels, %.2f ms (binning %d, k_cap %lld)\n",
+                 (long long)s->graph_launches, now_ms() - t_dbg, f->binning, (long long)f->k_cap);
   return GSB_OK;
 }
 
@@ -1331,11 +1373,21 @@ static gsb_frame* work_frame(gsb_ctx* ctx) {
   return ctx->work;
 }
 
-static int session_prepare(gsb_ctx* ctx, gsb_session* s, gsb_frame** out) {
-  gsb_frame* f = work_frame(ctx);
+static gsb_frame* session_frame(gsb_ctx* ctx, gsb_session* s) { return s->own ? s->own : work_frame(ctx); }
+
+// Frame set-up + buffer sizing for one session iteration (no capture).
+static int session_frame_ready(gsb_ctx* ctx, gsb_session* s, gsb_frame** out) {
+  gsb_frame* f = session_frame(ctx, s);
   if (int r = frame_setup(ctx, f, s->cloud, &s->cam, s->cfg.background, &s->cfg.raster, false)) return r;
   const int64_t want = f->k_cap > 0 ? f->k_cap : std::max<int64_t>(3 * s->cloud->n, 1 << 16);
   if (int r = frame_reserve(f, s->cloud, want)) return r;
+  *out = f;
+  return GSB_OK;
+}
+
+static int session_prepare(gsb_ctx* ctx, gsb_session* s, gsb_frame** out) {
+  gsb_frame* f = nullptr;
+  if (int r = session_frame_ready(ctx, s, &f)) return r;
   if (!s->exec || s->graph_frame != f || s->graph_gen != f->gen || s->graph_kcap != f->k_cap ||
       s->graph_profiled != ctx->profiling)
     if (int r = session_capture(ctx, s, f)) return r;
@@ -1357,7 +1409,7 @@ static int session_launch(gsb_ctx* ctx, gsb_session* s, int32_t iterations) {
 static int session_sync(gsb_ctx* ctx, gsb_session* s) {
   const size_t sb = pose_state_bytes();
   for (int round = 0; round < 8; ++round) {
-    gsb_frame* f = work_frame(ctx);
+    gsb_frame* f = session_frame(ctx, s);
     GSB_CUDA(cudaMemcpyAsync(s->host_state, s->state.p, sb, cudaMemcpyDeviceToHost, ctx->stream));
     if (f->counters.p)
       GSB_CUDA(cudaMemcpyAsync(s->host_counters, f->counters.p, 3 * sizeof(uint32_t), cudaMemcpyDeviceToHost,
@@ -1373,6 +1425,9 @@ static int session_sync(gsb_ctx* ctx, gsb_session* s) {
       s->pending = 0;
       return GSB_OK;
     }
+    if (debug_on())
+      std::fprintf(stderr, "[gsb] %d iteration(s) discarded: K %u (cap %lld), tile overflow %u\n", aborted, abort_k,
+                   (long long)f->k_cap, abort_tile);
     // clear the device-side abort counter, grow the entry capacity (or leave
     // tile-local binning), replay
     GSB_CUDA(cudaMemcpyAsync(s->state.p, s->host_state, sb, cudaMemcpyHostToDevice, ctx->stream));
@@ -1436,7 +1491,24 @@ int gsb_session_destroy(gsb_session* s) {
   if (!s) return GSB_OK;
   cudaSetDevice(s->ctx->device);
   cudaStreamSynchronize(s->ctx->stream);
+  if (gsb_pose_batch* b = s->batch) {  // leave the batch: its graph is rebuilt without this branch
+    for (size_t i = 0; i < b->sessions.size(); ++i)
+      if (b->sessions[i] == s) {
+        cudaStreamDestroy(b->streams[i]);
+        cudaEventDestroy(b->joins[i]);
+        b->sessions.erase(b->sessions.begin() + i);
+        b->streams.erase(b->streams.begin() + i);
+        b->joins.erase(b->joins.begin() + i);
+        b->graph_gen.erase(b->graph_gen.begin() + i);
+        b->graph_kcap.erase(b->graph_kcap.begin() + i);
+        b->graph_binning.erase(b->graph_binning.begin() + i);
+        break;
+      }
+    if (b->exec) cudaGraphExecDestroy(b->exec);
+    b->exec = nullptr;
+  }
   if (s->exec) cudaGraphExecDestroy(s->exec);
+  if (s->own) s->ctx->frame_pool.push_back(s->own);
   if (s->have_events)
     for (int k = 0; k < kNumStages; ++k)
       for (int j = 0; j < 2; ++j) cudaEventDestroy(s->ev[k][j]);
@@ -1503,7 +1575,7 @@ int gsb_session_frame_info(gsb_session* s, gsb_frame_info* info) {
   info->height = s->cam.height;
   info->tiles_x = (s->cam.width + kTile - 1) / kTile;
   info->tiles_y = (s->cam.height + kTile - 1) / kTile;
-  if (s->ctx->work) info->binning = s->ctx->work->binning == kBinGlobal ? GSB_BINNING_GLOBAL : GSB_BINNING_TILE_LOCAL;
+  if (gsb_frame* f = session_frame(s->ctx, s)) info->binning = f->binning == kBinGlobal ? GSB_BINNING_GLOBAL : GSB_BINNING_TILE_LOCAL;
   return GSB_OK;
 }
 
@@ -1527,6 +1599,204 @@ int gsb_estimate_pose(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* target, const d
                                      cudaMemcpyDeviceToHost));
   }
   gsb_session_destroy(s);
+  return r;
+}
+
+}  // extern "C"
+
+namespace gsb {
+
+static void batch_drop_graph(gsb_pose_batch* b) {
+  if (b->exec) cudaGraphExecDestroy(b->exec);
+  b->exec = nullptr;
+}
+
+// One graph: fork -> one branch per session (its own stream while capturing)
+// -> join. ctx->stream is pointed at the branch stream while a session's
+// launch sequence is recorded, so the launch code is the single-session code.
+static int batch_capture(gsb_ctx* ctx, gsb_pose_batch* b) {
+  batch_drop_graph(b);
+  const size_t n = b->sessions.size();
+  std::vector<gsb_frame*> frames(n);
+  for (size_t i = 0; i < n; ++i)
+    if (int r = session_frame_ready(ctx, b->sessions[i], &frames[i])) return r;
+  const double t_dbg = debug_on() ? now_ms() : 0.0;
+  const int64_t launches0 = ctx->launches;
+  cudaStream_t main = ctx->stream;
+  const bool profiling = ctx->profiling;  // per-stage events are per session graph, not per batch
+  ctx->profiling = false;
+  GSB_CUDA(cudaStreamBeginCapture(main, cudaStreamCaptureModeThreadLocal));
+  int r = GSB_OK;
+  cudaError_t e = cudaEventRecord(b->fork, main);
+  for (size_t i = 0; i < n && !r && e == cudaSuccess; ++i) {
+    e = cudaStreamWaitEvent(b->streams[i], b->fork, 0);
+    if (e != cudaSuccess) break;
+    ctx->stream = b->streams[i];
+    r = session_launch_iteration(ctx, b->sessions[i], frames[i]);
+    ctx->stream = main;
+    if (!r) e = cudaEventRecord(b->joins[i], b->streams[i]);
+    if (!r && e == cudaSuccess) e = cudaStreamWaitEvent(main, b->joins[i], 0);
+  }
+  ctx->stream = main;
+  ctx->profiling = profiling;
+  cudaGraph_t graph = nullptr;
+  cudaError_t e2 = cudaStreamEndCapture(main, &graph);
+  if (r || e != cudaSuccess || e2 != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    ctx->launches = launches0;
+    if (r) return r;
+    return cuda_fail(e != cudaSuccess ? e : e2, "pose batch capture");
+  }
+  e = cudaGraphInstantiate(&b->exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate (pose batch)");
+  b->graph_launches = ctx->launches - launches0;
+  ctx->launches = launches0;
+  for (size_t i = 0; i < n; ++i) {
+    b->graph_gen[i] = frames[i]->gen;
+    b->graph_kcap[i] = frames[i]->k_cap;
+    b->graph_binning[i] = frames[i]->binning;
+  }
+  if (debug_on())
+    std::fprintf(stderr, "[gsb] pose batch graph captured: %zu sessions, %lld kernels, %.2f ms\n", n,
+                 (long long)b->graph_launches, now_ms() - t_dbg);
+  return GSB_OK;
+}
+
+static int batch_prepare(gsb_ctx* ctx, gsb_pose_batch* b) {
+  bool stale = b->exec == nullptr;
+  for (size_t i = 0; i < b->sessions.size() && !stale; ++i) {
+    const gsb_frame* f = b->sessions[i]->own;
+    stale = f->gen != b->graph_gen[i] || f->k_cap != b->graph_kcap[i] || f->binning != b->graph_binning[i];
+  }
+  return stale ? batch_capture(ctx, b) : GSB_OK;
+}
+
+}  // namespace gsb
+
+extern "C" {
+
+int gsb_pose_batch_create(gsb_ctx* ctx, gsb_session* const* sessions, int32_t count, gsb_pose_batch** out) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!sessions || count <= 0 || !out) return fail(GSB_ERR_INVALID_ARGUMENT, "empty pose batch");
+  for (int32_t i = 0; i < count; ++i) {
+    if (!sessions[i] || sessions[i]->ctx != ctx) return fail(GSB_ERR_INVALID_ARGUMENT, "session / context mismatch");
+    if (sessions[i]->batch) return fail(GSB_ERR_INVALID_ARGUMENT, "session already belongs to a pose batch");
+    for (int32_t j = 0; j < i; ++j)
+      if (sessions[j] == sessions[i]) return fail(GSB_ERR_INVALID_ARGUMENT, "session listed twice");
+  }
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  gsb_pose_batch* b = new gsb_pose_batch();
+  b->ctx = ctx;
+  cudaError_t e = cudaEventCreateWithFlags(&b->fork, cudaEventDisableTiming);
+  for (int32_t i = 0; i < count && e == cudaSuccess; ++i) {
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev = nullptr;
+    e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (e == cudaSuccess) b->streams.push_back(st);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) b->joins.push_back(ev);
+  }
+  if (e != cudaSuccess) {
+    gsb_pose_batch_destroy(b);
+    return cuda_fail(e, "pose batch streams");
+  }
+  for (int32_t i = 0; i < count; ++i) {
+    gsb_session* s = sessions[i];
+    if (!ctx->frame_pool.empty()) {
+      s->own = ctx->frame_pool.back();
+      ctx->frame_pool.pop_back();
+    } else {
+      s->own = new gsb_frame();
+      s->own->ctx = ctx;
+    }
+    s->batch = b;
+    b->sessions.push_back(s);
+  }
+  b->graph_gen.assign(count, 0);
+  b->graph_kcap.assign(count, 0);
+  b->graph_binning.assign(count, -1);
+  *out = b;
+  return GSB_OK;
+}
+
+int gsb_pose_batch_destroy(gsb_pose_batch* b) {
+  if (!b) return GSB_OK;
+  gsb_ctx* ctx = b->ctx;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  batch_drop_graph(b);
+  for (gsb_session* s : b->sessions) {
+    if (s->exec && s->graph_frame == s->own) {  // its single-session graph points at the private frame
+      cudaGraphExecDestroy(s->exec);
+      s->exec = nullptr;
+    }
+    if (s->own) ctx->frame_pool.push_back(s->own);  // keeps its sized buffers for the next batch
+    s->own = nullptr;
+    s->batch = nullptr;
+  }
+  for (cudaStream_t st : b->streams) cudaStreamDestroy(st);
+  for (cudaEvent_t ev : b->joins) cudaEventDestroy(ev);
+  if (b->fork) cudaEventDestroy(b->fork);
+  delete b;
+  return GSB_OK;
+}
+
+int gsb_pose_batch_step_async(gsb_ctx* ctx, gsb_pose_batch* b, int32_t iterations) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!b || b->ctx != ctx) return fail(GSB_ERR_INVALID_ARGUMENT, "pose batch / context mismatch");
+  if (iterations <= 0) return GSB_OK;
+  if (int r = batch_prepare(ctx, b)) return r;
+  for (int32_t i = 0; i < iterations; ++i) GSB_CUDA(cudaGraphLaunch(b->exec, ctx->stream));
+  ctx->launches += b->graph_launches * iterations;
+  for (gsb_session* s : b->sessions) s->pending += iterations;
+  return GSB_OK;
+}
+
+int gsb_pose_batch_sync(gsb_ctx* ctx, gsb_pose_batch* b) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!b || b->ctx != ctx) return fail(GSB_ERR_INVALID_ARGUMENT, "pose batch / context mismatch");
+  for (gsb_session* s : b->sessions)
+    if (int r = session_sync(ctx, s)) return r;  // re-runs discarded iterations on the session's own graph
+  return GSB_OK;
+}
+
+int gsb_pose_batch_step(gsb_ctx* ctx, gsb_pose_batch* b, int32_t iterations) {
+  const int32_t chunk = 16;
+  while (iterations > 0) {
+    bool all_stopped = true;
+    for (gsb_session* s : b->sessions) all_stopped = all_stopped && s->stopped;
+    if (all_stopped) break;
+    const int32_t now = std::min(iterations, chunk);
+    if (int r = gsb_pose_batch_step_async(ctx, b, now)) return r;
+    if (int r = gsb_pose_batch_sync(ctx, b)) return r;
+    iterations -= now;
+  }
+  return GSB_OK;
+}
+
+// C3's call: pose_descent for `count` independent views of one cloud
+// (pipelines.cpp:218-222 per view), advanced together as one pose batch.
+int gsb_estimate_poses(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* const* targets, const double intr[4],
+                       const double* init_poses, int32_t count, const gsb_pose_config* cfg, double* poses_out,
+                       double* final_losses, int32_t* steps_used) {
+  if (!targets || !init_poses || !poses_out || count <= 0) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  std::vector<gsb_session*> ss(count, nullptr);
+  int r = GSB_OK;
+  for (int32_t i = 0; i < count && !r; ++i)
+    r = gsb_session_create(ctx, cloud, targets[i], intr, init_poses + 12 * (size_t)i, cfg, &ss[i]);
+  gsb_pose_batch* b = nullptr;
+  if (!r) r = gsb_pose_batch_create(ctx, ss.data(), count, &b);
+  if (!r) r = gsb_pose_batch_step(ctx, b, cfg->budget);
+  for (int32_t i = 0; i < count && !r; ++i) {
+    int32_t su = 0;
+    r = gsb_session_read(ss[i], nullptr, poses_out + 12 * (size_t)i, final_losses ? final_losses + i : nullptr, &su,
+                         nullptr, nullptr);
+    if (!r && steps_used) steps_used[i] = su;
+  }
+  if (b) gsb_pose_batch_destroy(b);
+  for (gsb_session* s : ss)
+    if (s) gsb_session_destroy(s);
   return r;
 }
 

@@ -179,6 +179,7 @@ struct gsb_ctx {
   gsb_frame* work = nullptr;   // scratch forward state shared by sessions
   cudaEvent_t (*stage_events)[2] = nullptr;  // set while capturing a profiled session graph
   int binning = 0;             // gsb::Binning preference (gsb_ctx_set_binning)
+  std::vector<gsb_frame*> frame_pool;  // sized forward states returned by pose batches, reused
 };
 
 struct gsb_cloud {

@@ -167,6 +167,12 @@ def _sigs():
         "gsb_session_frame_info": (C.c_int, [_vp, P(FrameInfo)]),
         "gsb_session_step_async": (C.c_int, [_vp, _vp, i32]),
         "gsb_session_stage_times": (C.c_int, [_vp, _vp]),
+        "gsb_pose_batch_create": (C.c_int, [_vp, _vp, i32, P(_vp)]),
+        "gsb_pose_batch_destroy": (C.c_int, [_vp]),
+        "gsb_pose_batch_step": (C.c_int, [_vp, _vp, i32]),
+        "gsb_pose_batch_step_async": (C.c_int, [_vp, _vp, i32]),
+        "gsb_pose_batch_sync": (C.c_int, [_vp, _vp]),
+        "gsb_estimate_poses": (C.c_int, [_vp, _vp, _vp, _vp, _vp, i32, P(PoseConfig), _vp, _vp, _vp]),
     }
 
 
@@ -347,7 +353,7 @@ class Grads:
     def __init__(self, ctx: Context, cloud: Cloud):
         h = _vp()
         _check(lib().gsb_grads_create(ctx.h, cloud.h, C.byref(h)))
-        self.h, self.n, self.sh_degree = h, cloud.n, cloud.sh_degree
+        self.h, self.ctx, self.n, self.sh_degree = h, ctx, cloud.n, cloud.sh_degree
 
     def __del__(self):
         try:
@@ -373,7 +379,7 @@ class Image:
         img = np.ascontiguousarray(img, np.float64)
         h = _vp()
         _check(lib().gsb_image_create(ctx.h, _p(img), img.shape[1], img.shape[0], C.byref(h)))
-        self.h, self.width, self.height = h, img.shape[1], img.shape[0]
+        self.h, self.ctx, self.width, self.height = h, ctx, img.shape[1], img.shape[0]
 
     def __del__(self):
         try:
@@ -495,6 +501,51 @@ class PoseSession:
         fi = FrameInfo()
         _check(lib().gsb_session_frame_info(self.h, C.byref(fi)))
         return fi
+
+
+class PoseBatch:
+    """Several sessions advanced by one CUDA-graph replay per iteration (gsb_pose_batch)."""
+
+    def __init__(self, ctx: Context, sessions):
+        self.sessions = list(sessions)
+        arr = (_vp * len(self.sessions))(*[s.h for s in self.sessions])
+        h = _vp()
+        _check(lib().gsb_pose_batch_create(ctx.h, arr, len(self.sessions), C.byref(h)))
+        self.h, self.ctx = h, ctx
+
+    def close(self):
+        if self.h:
+            lib().gsb_pose_batch_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def step(self, iterations: int = 1):
+        _check(lib().gsb_pose_batch_step(self.ctx.h, self.h, iterations))
+
+    def step_async(self, iterations: int = 1):
+        _check(lib().gsb_pose_batch_step_async(self.ctx.h, self.h, iterations))
+
+    def sync(self):
+        _check(lib().gsb_pose_batch_sync(self.ctx.h, self.h))
+
+
+def estimate_poses(ctx: Context, cloud: Cloud, targets, intr, init_poses, config: PoseConfig | None = None):
+    """estimate_pose for several views of one cloud at once (gsb_estimate_poses)."""
+    cfg = config or PoseConfig.default()
+    intr = np.ascontiguousarray(intr, np.float64)
+    init = np.ascontiguousarray(init_poses, np.float64).reshape(-1, 12)
+    n = init.shape[0]
+    assert len(targets) == n
+    arr = (_vp * n)(*[t.h for t in targets])
+    out, fl, su = np.zeros((n, 12)), np.zeros(n), np.zeros(n, np.int32)
+    _check(lib().gsb_estimate_poses(ctx.h, cloud.h, arr, _p(intr), _p(init), n, C.byref(cfg), _p(out), _p(fl),
+                                    _p(su)))
+    return dict(pose=out, final_loss=fl, steps=su)
 
 
 def synth_poses(seed: int, n: int, sh_degree: int, kind: int, cameras: int, orbit_radius=2.5,

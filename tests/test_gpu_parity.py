@@ -373,6 +373,71 @@ def test_estimate_pose_trajectory_matches_oracle(G, ctx):
     assert np.max(np.abs(res["trace_loss"] - ref["trace_loss"])) < 1e-4
 
 
+def test_pose_batch_bitwise_equals_sequential_sessions(G, ctx):
+    """A pose batch (sessions as parallel graph branches, private forward
+    states) gives bit-identical per-view trajectories to stepping each
+    session alone, and each view still tracks the oracle."""
+    rng = O.make_rng(99)
+    hc = O.synth_cloud(2000, 3, rng).as_float32_exact()
+    poses = O.synth_poses(0, 6, rng)
+    cloud = to_dev(G, ctx, hc)
+    noise = O.make_rng(1002)
+    cams = [O.synth_camera(96, 80, poses[v]) for v in range(5)]
+    targets = [O.render(hc, c).image for c in cams]
+    inits = [O.perturb_pose(poses[v], 15.0, 0.15, noise) for v in range(5)]
+    intr = [cams[0].fx, cams[0].fy, cams[0].cx, cams[0].cy]
+    cfg = G.PoseConfig.default(budget=40, pose_converged_eps=0.0)
+    imgs = [G.Image(ctx, t) for t in targets]
+    seq = []
+    for v in range(5):
+        s = G.PoseSession(ctx, cloud, imgs[v], intr, inits[v], cfg)
+        s.step(40)
+        seq.append(s.read())
+        del s
+    sessions = [G.PoseSession(ctx, cloud, imgs[v], intr, inits[v], cfg) for v in range(5)]
+    batch = G.PoseBatch(ctx, sessions)
+    for _ in range(4):
+        batch.step_async(10)
+    batch.sync()
+    for v in range(5):
+        r = sessions[v].read()
+        assert r["steps"] == seq[v]["steps"] == 40
+        assert np.array_equal(r["pose"], seq[v]["pose"]), v
+        assert np.array_equal(r["best_pose"], seq[v]["best_pose"]), v
+        assert r["final_loss"] == seq[v]["final_loss"]
+    batch.close()
+    # the one-call form
+    res = G.estimate_poses(ctx, cloud, imgs, intr, np.stack(inits), cfg)
+    for v in range(5):
+        assert np.array_equal(res["pose"][v], seq[v]["best_pose"]), v
+        assert res["steps"][v] == 40
+    # view 0 against the oracle's pose_descent
+    ref = O.estimate_pose(hc, targets[0], *intr, inits[0], budget=40, pose_converged_eps=0.0)
+    r, d = O.abs_pose_error(res["pose"][0], ref["pose"])
+    assert r < 0.1 and d < 1e-3, (r, d)
+
+
+def test_pose_batch_capacity_growth(G, ctx):
+    """Sessions of a batch start with a tiny entry capacity on their private
+    forward states: discarded iterations are re-run and results still equal
+    the sequential ones."""
+    rng = O.make_rng(7)
+    hc = O.synth_cloud(4000, 1, rng).as_float32_exact()
+    hc.log_scales += 0.7  # large footprints -> many tile entries
+    poses = O.synth_poses(1, 3, rng)
+    cloud = to_dev(G, ctx, hc)
+    cams = [O.synth_camera(128, 96, poses[v]) for v in range(3)]
+    imgs = [G.Image(ctx, O.render(hc, c).image) for c in cams]
+    noise = O.make_rng(5)
+    inits = [O.perturb_pose(poses[v], 5.0, 0.05, noise) for v in range(3)]
+    intr = [cams[0].fx, cams[0].fy, cams[0].cx, cams[0].cy]
+    cfg = G.PoseConfig.default(budget=12, pose_converged_eps=0.0)
+    seq = [G.estimate_pose(ctx, cloud, imgs[v], intr, inits[v], cfg) for v in range(3)]
+    res = G.estimate_poses(ctx, cloud, imgs, intr, np.stack(inits), cfg)
+    for v in range(3):
+        assert np.array_equal(res["pose"][v], seq[v]["pose"]), v
+
+
 @pytest.mark.slow
 def test_estimate_pose_acceptance_criterion(G, ctx):
     """tests/acceptance.cpp:74-100 on the device: >= 18/20 trials converge."""
