@@ -19,6 +19,7 @@ OBJ = os.path.join(PKG, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr"]
+FLAGS += os.environ.get("GSB_NVCC_EXTRA", "").split()  # experiment knobs (e.g. -DGSB_BWD_MIN_BLOCKS=8)
 
 
 def sources():
