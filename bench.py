@@ -215,6 +215,7 @@ def run_ours(args, ws, rank, local):
         e2e_s = float(t.item())
     e2e_value = VIEWS_PER_GPU * ws * e2e_iters / e2e_s
 
+    joint = None if args.no_joint else run_joint(args, ws, rank, local, dist)
     out = None
     if rank == 0:
         # roofline for the dominant stage
@@ -251,6 +252,8 @@ def run_ours(args, ws, rank, local):
             "profiled_ms_per_step": round(prof_ms / args.steps, 4),
             "pose_check": {"view": int(views[0]), "final_loss": res["final_loss"], "steps": res["steps"]},
         }
+        if joint is not None:
+            out["joint_c4"] = joint
         if cpu is not None:
             out["cpu_baseline"] = cpu
         if work is not None:
@@ -259,6 +262,60 @@ def run_ours(args, ws, rank, local):
         dist.barrier()
         dist.destroy_process_group()
     return out
+
+
+# ------------------------------------------------ C4: joint DP (secondary)
+C4_N, C4_VIEWS, C4_SEED = 300_000, 20, 4
+
+
+def run_joint(args, ws, rank, local, dist):
+    """Config C4: joint reconstruction + pose refinement on 20 LLFF-shaped
+    views (300k Gaussians SH3, 1008x756), data parallel: one view per GPU per
+    step, NCCL all-reduce of the gradient planes inside the step graph.
+    Returns steps/s and views/s (whole job, max-over-ranks device time)."""
+    from paper_2410_08743_b200 import gsb
+    ctx = gsb.Context(local)
+    comm = None
+    if ws > 1:
+        uid = [gsb.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = gsb.Comm(ctx, uid[0], rank, ws)
+    gt_cloud = gsb.Cloud(ctx, C4_N, SH_DEGREE)
+    gt_cloud.synth(C4_SEED, log_scale_offset(C4_N))
+    gt = gsb.synth_poses(C4_SEED, C4_N, SH_DEGREE, 1, C4_VIEWS)
+    intr = gsb.synth_intrinsics(WIDTH, HEIGHT)
+    targets = [gsb.Image(ctx, gsb.render(ctx, gt_cloud, gsb.Camera.from_pose12(*intr, WIDTH, HEIGHT, p)).image)
+               for p in gt]
+    noise = gsb.PoseRng(55)
+    init = np.stack([gsb.perturb_pose_tangent(p, 0.05, noise) for p in gt])
+    cloud = gsb.Cloud(ctx, C4_N, SH_DEGREE)
+    cloud.synth(C4_SEED, log_scale_offset(C4_N))
+    cloud.jitter(700, 0.05, 0.3)  # tests/test_trainer.cpp:598-601
+    iters = args.warmup + args.steps
+    cfg = gsb.JointConfig.default(iterations=max(iters, 1000), sh_degree=SH_DEGREE, sh_degree_interval=0)
+    j = gsb.JointOptimizer(ctx, cloud, targets, intr, init, cfg, 800, local_views=1, comm=comm)
+    j.step(args.warmup)
+    if dist:
+        dist.barrier()
+    ctx.timer_start()
+    j.step(args.steps)
+    ms = ctx.timer_stop()
+    if dist:
+        import torch
+        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    res = j.read()
+    j.close()
+    if comm:
+        comm.close()
+    return {"workload": f"C4 joint reconstruction + pose refinement: {C4_N} Gaussians SH3, {C4_VIEWS} views "
+                        f"{WIDTH}x{HEIGHT}, 1 view/GPU/step, densify off",
+            "steps_per_s": round(args.steps / (ms / 1e3), 3), "views_per_s": round(ws * args.steps / (ms / 1e3), 3),
+            "ms_per_step": round(ms / args.steps, 4),
+            "parallelism": f"data parallel over {ws} GPU(s): NCCL all-reduce of {(11 + 48 + 2)} FP32 gradient "
+                           "planes per step" if ws > 1 else "1 GPU (no collective)",
+            "final_total_loss": float(res["trace_total"][-1]) if len(res["trace_total"]) else None}
 
 
 def ncu_traffic(stage):
@@ -377,6 +434,7 @@ def main():
     ap.add_argument("--e2e-iters", type=int, default=100)
     ap.add_argument("--cpu-iters", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-joint", action="store_true", help="skip the secondary C4 joint-DP measurement")
     args = ap.parse_args()
     ws, rank, local = dist_env()
     if args.warmup < 3 and args.impl == "ours":

@@ -16,6 +16,9 @@
  *   gsb_estimate_pose     <- gsopt::estimate_pose     include/gsopt/trainer.hpp:170-171
  *                            (pose_descent, src/pipelines.cpp:58-92, device resident)
  *   gsb_cloud_*           <- GaussianCloud            include/gsopt/scene.hpp:22-46
+ *   gsb_joint_*           <- gsopt::joint_optimize    include/gsopt/trainer.hpp:155-163
+ *                            (src/pipelines.cpp:96-216, densification off), data parallel
+ *                            over training views with an NCCL all-reduce (gsb_comm_*)
  *
  * Status codes: 0 = OK; reference ErrorCode value + 1 (core.hpp:35-47) for
  * the reference's own failure modes; >= 100 for CUDA / argument / memory
@@ -155,6 +158,11 @@ int gsb_cloud_synth(gsb_cloud* cloud, uint64_t seed, double log_scale_offset);
  * kind: 0 orbit, 1 forward-facing, 2 random-walk. poses: cameras*12 row-major [R|t]. */
 int gsb_synth_poses(uint64_t seed, int64_t n, int32_t sh_degree, int32_t kind, int32_t cameras,
                     double orbit_radius, double orbit_arc, double* poses);
+/* perturb_pose_tangent (eval.cpp:148-152), same rng convention as gsb_perturb_pose. */
+int gsb_perturb_pose_tangent(const double pose[12], double sigma, uint64_t* rng_state, double out[12]);
+/* Joint-test initial cloud (tests/test_trainer.cpp:598-601): means += mean_sigma
+ * * normal3, then log-scales += log_scale_range * uniform(-1, 1) per Gaussian. */
+int gsb_cloud_jitter(gsb_cloud* cloud, uint64_t seed, double mean_sigma, double log_scale_range);
 /* perturb_pose (eval.cpp:130-146) with a caller-held rng state (init with seed). */
 int gsb_perturb_pose(const double pose[12], double rot_deg, double trans, uint64_t* rng_state,
                      double out[12]);
@@ -267,6 +275,51 @@ int gsb_pose_batch_sync(gsb_ctx* ctx, gsb_pose_batch* b);
 int gsb_estimate_poses(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* const* targets, const double intr[4],
                        const double* init_poses, int32_t count, const gsb_pose_config* cfg, double* poses_out,
                        double* final_losses, int32_t* steps_used);
+
+/* ---- communicator: NCCL over NVLink for data-parallel training ----
+ * libnccl.so.2 is loaded at run time (dlopen); without it gsb_comm_* return
+ * GSB_ERR_NO_DEVICE. One rank per GPU. The 128-byte unique id is created on
+ * rank 0 and distributed by the caller (e.g. torch.distributed broadcast). */
+typedef struct gsb_comm gsb_comm;
+int gsb_comm_unique_id(uint8_t id_out[128]);
+int gsb_comm_create(gsb_ctx* ctx, const uint8_t id[128], int32_t rank, int32_t world, gsb_comm** out);
+int gsb_comm_destroy(gsb_comm* c);
+/* in-place sum over ranks of n device floats (stream ordered on ctx) */
+int gsb_comm_allreduce_f32(gsb_comm* c, float* dev_buf, int64_t n);
+
+/* ---- joint reconstruction + pose refinement (joint_optimize) ----
+ * The TrainConfig fields joint_optimize reads (trainer.hpp:21-60,
+ * losses.hpp:15-19); densification is not part of this loop. */
+typedef struct {
+  int32_t iterations;
+  double cam_lr_start, cam_lr_end, pos_lr_start, pos_lr_end;
+  double rot_lr, scale_lr, opacity_lr, sh_dc_lr, sh_rest_lr;
+  int32_t opacity_l1_steps, sh_degree, sh_degree_interval, optimize_poses;
+  double beta, aniso_ratio, opacity_l1_weight;
+  double background[3];
+  gsb_raster_config raster;
+} gsb_joint_config;
+void gsb_default_joint_config(gsb_joint_config* c);
+/* The training-view sequence of joint_optimize (pipelines.cpp:122-129: epoch
+ * permutations shuffled in place from Rng(seed)); step t of a data-parallel
+ * run with S slots per step uses seq[t*S .. t*S+S-1], rank r the slots
+ * r*local .. r*local+local-1. Host only. */
+int gsb_joint_schedule(uint64_t seed, int32_t n_views, int64_t count, int32_t* seq_out);
+/* One step = `local` views rendered on this rank (local * world slots in
+ * all); the Adam gradient is the slots' mean plus the regularisers, then each
+ * slot's pose step in slot order. local = world = 1 is joint_optimize's loop.
+ * The cloud is optimised in place; targets stay owned by the caller.
+ * comm may be NULL (single rank). */
+typedef struct gsb_joint gsb_joint;
+int gsb_joint_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* const* targets, int32_t n_views,
+                     const double intr[4], const double* init_poses, const gsb_joint_config* cfg,
+                     uint64_t seed, int32_t local_views, gsb_comm* comm, gsb_joint** out);
+int gsb_joint_destroy(gsb_joint* j);
+/* runs `steps` steps (blocking); GSB_ERR_DIVERGED at a non-finite total loss */
+int gsb_joint_step(gsb_ctx* ctx, gsb_joint* j, int32_t steps);
+/* poses_out n_views x 12 (optional), steps done, per-step total / L1 traces
+ * (iterations entries each, optional) */
+int gsb_joint_read(gsb_joint* j, double* poses_out, int64_t* steps_done, double* trace_total, double* trace_l1);
 
 #ifdef __cplusplus
 }

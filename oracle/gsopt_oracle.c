@@ -1409,6 +1409,148 @@ int32_t orc_estimate_pose(const orc_cloud* cloud, const double* image, double fx
   return steps_used;
 }
 
+/* pipelines.cpp:122-129: the training-view sequence. `order` starts as iota
+ * and is re-shuffled IN PLACE (Fisher-Yates from the back with
+ * rng.uniform_int(0, i)) at the start of every epoch; the sequence is the
+ * concatenation of the epoch orders. seq receives `count` view indices. */
+void orc_joint_schedule(orc_rng* rng, int32_t n_views, int64_t count, int32_t* seq) {
+  int32_t* order = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n_views > 0 ? n_views : 1));
+  for (int32_t i = 0; i < n_views; ++i) order[i] = i;
+  for (int64_t k = 0; k < count; ++k) {
+    if (k % n_views == 0) {
+      for (int32_t i = n_views - 1; i > 0; --i) {
+        const int32_t j = (int32_t)orc_rng_uniform_int(rng, 0, i);
+        const int32_t tmp = order[i];
+        order[i] = order[j];
+        order[j] = tmp;
+      }
+    }
+    seq[k] = order[k % n_views];
+  }
+  free(order);
+}
+
+/* pipelines.cpp:96-216 (joint_optimize) with densification off and without
+ * the ground-truth pose statistics, generalised to `slots` training views per
+ * step (the data-parallel semantics of the B200 build): step t
+ * renders views seq[t*slots .. t*slots+slots-1] (orc_joint_schedule), the
+ * Adam gradient is the MEAN of the slots' render gradients plus the
+ * regularisers (anisotropy 217-244, opacity L1 246-257, both added once, on
+ * the pre-step parameters), and the slots' pose steps are applied in slot
+ * order with each view's own PoseAdam. slots == 1 is the reference loop
+ * exactly. Returns 0, or 10 (ErrorCode::diverged + 1) at a non-finite total
+ * loss (160-162). trace_total / trace_l1 (iterations, nullable) receive the
+ * step's mean total loss and mean L1. poses: n_views x 12, updated in place. */
+int32_t orc_joint_optimize(orc_cloud* cloud, const double* const* images, int32_t n_views, double fx, double fy,
+                           double cx, double cy, int32_t w, int32_t h, double* poses, const orc_joint_cfg* cfg,
+                           int32_t slots, orc_rng* rng, double* trace_total, double* trace_l1) {
+  const int64_t n = cloud->n;
+  const int32_t iters = cfg->iterations;
+  int32_t* seq = (int32_t*)malloc(sizeof(int32_t) * ((size_t)iters * slots + 1));
+  orc_joint_schedule(rng, n_views, (int64_t)iters * slots, seq);
+  orc_adam_state st[5];
+  memset(st, 0, sizeof st);
+  orc_pose_adam* pad = (orc_pose_adam*)calloc((size_t)n_views, sizeof(orc_pose_adam));
+  double* d_image = (double*)malloc(sizeof(double) * (size_t)w * h * 3);
+  double* dpose = (double*)malloc(sizeof(double) * 6 * (size_t)slots);
+  orc_grads acc;
+  orc_grads_alloc(&acc, cloud);
+  const int basis = sh_count(cloud->sh_degree);
+  int32_t status = 0;
+  for (int32_t t = 0; t < iters && status == 0; ++t) {
+    if (cfg->sh_degree_interval > 0 && t > 0 && t % cfg->sh_degree_interval == 0) {
+      const int32_t a = cloud->active_sh_degree + 1;
+      cloud->active_sh_degree = a < cfg->sh_degree ? a : cfg->sh_degree;
+    }
+    memset(acc.d_means, 0, sizeof(double) * 3 * n);
+    memset(acc.d_rotations, 0, sizeof(double) * 4 * n);
+    memset(acc.d_log_scales, 0, sizeof(double) * 3 * n);
+    memset(acc.d_opacity_logits, 0, sizeof(double) * n);
+    memset(acc.d_sh, 0, sizeof(double) * 3 * basis * n);
+    double rgb_sum = 0.0, l1_sum = 0.0;
+    for (int32_t s = 0; s < slots; ++s) {
+      const int32_t v = seq[(int64_t)t * slots + s];
+      orc_camera cam;
+      cam.fx = fx; cam.fy = fy; cam.cx = cx; cam.cy = cy; cam.width = w; cam.height = h;
+      for (int r = 0; r < 3; ++r) {
+        for (int c = 0; c < 3; ++c) cam.R[r * 3 + c] = poses[12 * v + r * 4 + c];
+        cam.t[r] = poses[12 * v + r * 4 + 3];
+      }
+      orc_render_out* out = orc_render(cloud, &cam, cfg->background, &cfg->raster);
+      l1_sum += orc_rgb_loss(out->image, images[v], w, h, 0.0, NULL);
+      rgb_sum += orc_rgb_loss(out->image, images[v], w, h, cfg->beta, d_image);
+      orc_grads g;
+      orc_render_backward(cloud, &cam, out, d_image, w, h, &g);
+      const double inv = 1.0 / (double)slots;
+      for (int64_t k = 0; k < 3 * n; ++k) acc.d_means[k] += g.d_means[k] * inv;
+      for (int64_t k = 0; k < 4 * n; ++k) acc.d_rotations[k] += g.d_rotations[k] * inv;
+      for (int64_t k = 0; k < 3 * n; ++k) acc.d_log_scales[k] += g.d_log_scales[k] * inv;
+      for (int64_t k = 0; k < n; ++k) acc.d_opacity_logits[k] += g.d_opacity_logits[k] * inv;
+      for (int64_t k = 0; k < 3 * basis * n; ++k) acc.d_sh[k] += g.d_sh[k] * inv;
+      memcpy(dpose + 6 * s, g.d_pose, sizeof(double) * 6);
+      orc_grads_free(&g);
+      orc_render_free(out);
+    }
+    /* regularisers on the pre-step parameters (pipelines.cpp:144-157) */
+    double* d_aniso = (double*)malloc(sizeof(double) * (3 * n + 1));
+    const double aniso = orc_anisotropy_loss(cloud->log_scales, n, cfg->aniso_ratio, d_aniso);
+    for (int64_t k = 0; k < 3 * n; ++k) acc.d_log_scales[k] += d_aniso[k];
+    free(d_aniso);
+    double op_l1 = 0.0;
+    if (t < cfg->opacity_l1_steps && cfg->opacity_l1_weight > 0.0) {
+      double* ops = (double*)malloc(sizeof(double) * (n + 1));
+      double* d_ops = (double*)malloc(sizeof(double) * (n + 1));
+      for (int64_t i = 0; i < n; ++i) ops[i] = sigmoid(cloud->opacity_logits[i]);
+      op_l1 = orc_opacity_l1(ops, n, d_ops);
+      for (int64_t i = 0; i < n; ++i)
+        acc.d_opacity_logits[i] += cfg->opacity_l1_weight * d_ops[i] * ops[i] * (1.0 - ops[i]);
+      free(ops);
+      free(d_ops);
+    }
+    const double total = rgb_sum / slots + aniso + cfg->opacity_l1_weight * op_l1;
+    if (trace_total) trace_total[t] = total;
+    if (trace_l1) trace_l1[t] = l1_sum / slots;
+    if (!isfinite(total)) {
+      status = 10;
+      break;
+    }
+    double lrs[6];
+    lrs[0] = orc_schedule(1, cfg->pos_lr_start, cfg->pos_lr_end, t, iters);
+    lrs[1] = cfg->rot_lr;
+    lrs[2] = cfg->scale_lr;
+    lrs[3] = cfg->opacity_lr;
+    lrs[4] = cfg->sh_dc_lr;
+    lrs[5] = cfg->sh_rest_lr;
+    orc_cloud_adam_step(cloud, &acc, st, lrs);
+    if (cfg->optimize_poses) {
+      const double cam_lr = orc_schedule(0, cfg->cam_lr_start, cfg->cam_lr_end, t, iters);
+      for (int32_t s = 0; s < slots; ++s) {
+        const int32_t v = seq[(int64_t)t * slots + s];
+        double R[9], tt[3], Rn[9], tn[3], applied[6];
+        for (int r = 0; r < 3; ++r) {
+          for (int c = 0; c < 3; ++c) R[r * 3 + c] = poses[12 * v + r * 4 + c];
+          tt[r] = poses[12 * v + r * 4 + 3];
+        }
+        orc_pose_step(R, tt, dpose + 6 * s, cam_lr, &pad[v], Rn, tn, applied);
+        for (int r = 0; r < 3; ++r) {
+          for (int c = 0; c < 3; ++c) poses[12 * v + r * 4 + c] = Rn[r * 3 + c];
+          poses[12 * v + r * 4 + 3] = tn[r];
+        }
+      }
+    }
+  }
+  orc_grads_free(&acc);
+  for (int k = 0; k < 5; ++k) {
+    free(st[k].m);
+    free(st[k].v);
+  }
+  free(pad);
+  free(d_image);
+  free(dpose);
+  free(seq);
+  return status;
+}
+
 /* ----------------------------------------------------------------- synth */
 void orc_cloud_alloc(orc_cloud* c, int64_t n, int32_t sh_degree) { /* scene.cpp:14-24 */
   const int basis = sh_count(sh_degree);

@@ -172,6 +172,23 @@ int32_t orc_estimate_pose(const orc_cloud* cloud, const double* image, double fx
                           double R_out[9], double t_out[3], double* final_loss, int32_t* converged,
                           double* trace_pose, double* trace_loss, double* trace_dpose);
 
+/* pipelines.cpp:122-129 epoch shuffles -> view sequence (count entries) */
+void orc_joint_schedule(orc_rng* rng, int32_t n_views, int64_t count, int32_t* seq);
+/* TrainConfig fields joint_optimize reads (trainer.hpp:21-60, losses.hpp:15-19) */
+typedef struct {
+  int32_t iterations;
+  double cam_lr_start, cam_lr_end, pos_lr_start, pos_lr_end, rot_lr, scale_lr, opacity_lr, sh_dc_lr, sh_rest_lr;
+  int32_t opacity_l1_steps, sh_degree, sh_degree_interval, optimize_poses;
+  double beta, aniso_ratio, opacity_l1_weight;
+  double background[3];
+  orc_raster_config raster;
+} orc_joint_cfg;
+/* pipelines.cpp:96-216 without densify / gt stats; `slots` views per step
+ * (1 = the reference loop). Returns 0 or 10 (diverged). */
+int32_t orc_joint_optimize(orc_cloud* cloud, const double* const* images, int32_t n_views, double fx, double fy,
+                           double cx, double cy, int32_t w, int32_t h, double* poses, const orc_joint_cfg* cfg,
+                           int32_t slots, orc_rng* rng, double* trace_total, double* trace_l1);
+
 /* synth.cpp:33-101 + eval.cpp:122-152 */
 void orc_synth_cloud(orc_cloud* cloud, int64_t n, int32_t sh_degree, orc_rng* rng);
 void orc_look_at(const double eye[3], const double target[3], double R[9], double t[3]);

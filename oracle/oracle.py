@@ -78,6 +78,17 @@ class PoseAdam(C.Structure):
     _fields_ = [("m", C.c_double * 6), ("v", C.c_double * 6), ("step", C.c_int64)]
 
 
+class JointCfg(C.Structure):
+    """orc_joint_cfg: the TrainConfig fields joint_optimize reads (trainer.hpp:21-60, losses.hpp:15-19)."""
+    _fields_ = [("iterations", C.c_int32), ("cam_lr_start", C.c_double), ("cam_lr_end", C.c_double),
+                ("pos_lr_start", C.c_double), ("pos_lr_end", C.c_double), ("rot_lr", C.c_double),
+                ("scale_lr", C.c_double), ("opacity_lr", C.c_double), ("sh_dc_lr", C.c_double),
+                ("sh_rest_lr", C.c_double), ("opacity_l1_steps", C.c_int32), ("sh_degree", C.c_int32),
+                ("sh_degree_interval", C.c_int32), ("optimize_poses", C.c_int32), ("beta", C.c_double),
+                ("aniso_ratio", C.c_double), ("opacity_l1_weight", C.c_double), ("background", C.c_double * 3),
+                ("raster", RasterConfig)]
+
+
 class PoseCfg(C.Structure):
     _fields_ = [("cam_lr_start", C.c_double), ("cam_lr_end", C.c_double), ("beta", C.c_double),
                 ("pose_converged_eps", C.c_double), ("background", C.c_double * 3), ("raster", RasterConfig)]
@@ -140,6 +151,10 @@ def lib():
             "orc_cloud_free": (None, [P(Cloud)]),
             "orc_num_threads": (C.c_int, []),
             "orc_count_work": (None, [P(RenderOut), vp, vp]),
+            "orc_joint_schedule": (None, [P(Rng), i32, i64, vp]),
+            "orc_cloud_adam_step": (None, [P(Cloud), P(Grads), vp, vp]),
+            "orc_joint_optimize": (i32, [P(Cloud), vp, i32, d, d, d, d, i32, i32, vp, P(JointCfg), i32, P(Rng),
+                                         vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -493,6 +508,72 @@ def estimate_pose(cloud: HostCloud, image, fx, fy, cx, cy, init12, budget=1000, 
                                     C.cast(C.byref(conv), C.c_void_p), _p(tp), _p(tl), _p(td))
     return dict(pose=pose_join(Ro, to), steps=steps, final_loss=fl.value, converged=bool(conv.value),
                 trace_pose=tp[:steps], trace_loss=tl[:steps], trace_dpose=td[:steps])
+
+
+class CloudAdam:
+    """cloud_adam_step (pipelines.cpp:18-41) over a persistent FP64 cloud and
+    its five AdamStates (trainer.hpp:69-78): step(grads, lrs) updates in place."""
+
+    def __init__(self, cloud: HostCloud):
+        self.view = cloud.copy().c()
+        self.states = (C.c_byte * (5 * 32))()  # 5 x {double* m, *v; int64 n, step}
+
+    def step(self, g: dict, lrs):
+        n = self.view.s.n
+        bufs = [np.ascontiguousarray(g[k], np.float64).reshape(-1)
+                for k in ("d_means", "d_rotations", "d_log_scales", "d_opacity_logits", "d_sh")]
+        og = Grads()
+        og.n, og.sh_len = n, bufs[4].size
+        P = C.POINTER(C.c_double)
+        og.d_means, og.d_rotations, og.d_log_scales, og.d_opacity_logits, og.d_sh = [b.ctypes.data_as(P) for b in bufs]
+        lrs = np.ascontiguousarray(lrs, np.float64)
+        lib().orc_cloud_adam_step(self.view.ref(), C.byref(og), C.cast(self.states, C.c_void_p), _p(lrs))
+
+    def cloud(self) -> HostCloud:
+        hc = self.view.hc
+        return HostCloud(*[b.reshape(a.shape).copy() for b, a in zip(self.view.bufs, (
+            hc.means, hc.rotations, hc.log_scales, hc.opacity_logits, hc.sh))], hc.sh_degree, hc.active_sh_degree)
+
+
+def joint_config(iterations, **kw) -> JointCfg:
+    """TrainConfig defaults (trainer.hpp:21-60, losses.hpp:15-19) with overrides."""
+    c = JointCfg()
+    c.iterations = iterations
+    c.cam_lr_start, c.cam_lr_end, c.pos_lr_start, c.pos_lr_end = 1e-2, 1e-4, 1.6e-2, 1.6e-4
+    c.rot_lr, c.scale_lr, c.opacity_lr, c.sh_dc_lr, c.sh_rest_lr = 1e-3, 5e-3, 5e-2, 2.5e-3, 2.5e-3 / 20.0
+    c.opacity_l1_steps, c.sh_degree, c.sh_degree_interval, c.optimize_poses = 10000, 3, 1000, 1
+    c.beta, c.aniso_ratio, c.opacity_l1_weight = 0.2, 10.0, 0.01
+    c.raster = default_raster_config()
+    for k, v in kw.items():
+        if k == "background":
+            for i in range(3):
+                c.background[i] = v[i]
+        else:
+            setattr(c, k, v)
+    return c
+
+
+def joint_schedule(rng: Rng, n_views: int, count: int) -> np.ndarray:
+    """pipelines.cpp:122-129 view sequence (epoch shuffles in place)."""
+    out = np.zeros(count, np.int32)
+    lib().orc_joint_schedule(C.byref(rng), n_views, count, _p(out))
+    return out
+
+
+def joint_optimize(cloud: HostCloud, images, intr, width, height, poses, cfg: JointCfg, slots: int, rng: Rng):
+    """pipelines.cpp:96-216 (densify off), `slots` views per step. Returns
+    (status, cloud, poses, trace_total, trace_l1); cloud/poses are new arrays."""
+    cv = cloud.copy().c()
+    imgs = [np.ascontiguousarray(im, np.float64) for im in images]
+    ptrs = (C.c_void_p * len(imgs))(*[im.ctypes.data for im in imgs])
+    P = np.ascontiguousarray(np.asarray(poses, np.float64).reshape(-1, 12)).copy()
+    tt, tl = np.zeros(cfg.iterations), np.zeros(cfg.iterations)
+    st = lib().orc_joint_optimize(cv.ref(), C.cast(ptrs, C.c_void_p), len(imgs), intr[0], intr[1], intr[2],
+                                  intr[3], width, height, _p(P), C.byref(cfg), slots, C.byref(rng), _p(tt), _p(tl))
+    out = HostCloud(*[b.reshape(a.shape) for b, a in zip(cv.bufs, (cloud.means, cloud.rotations, cloud.log_scales,
+                                                                   cloud.opacity_logits, cloud.sh))],
+                    cloud.sh_degree, cv.s.active_sh_degree)
+    return st, out, P, tt, tl
 
 
 # --------------------------------------------------------------- gradcheck

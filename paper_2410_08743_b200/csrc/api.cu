@@ -7,6 +7,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <dlfcn.h>
+#include <nccl.h>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -68,6 +70,23 @@ void pose_state_set_adam(void* host_state, const double m[6], const double v[6],
 int launch_pose_step(cudaStream_t st, void* states, const double* dpose, double lr, int nb);
 int launch_adam_f64(cudaStream_t st, double* p, const double* g, double* m, double* v, int64_t n, double lr,
                     int64_t step);
+int launch_joint_slot_begin(cudaStream_t st, const void* js, const int32_t* seq, const JointCtl& ctl, int b,
+                            const CamDev* cams, CamDev* frame_cam, const float* const* targets, float* tbuf,
+                            int64_t n3p);
+int launch_joint_slot_end(cudaStream_t st, const JointCtl& ctl, int b, const double* d_pose, const double* loss3,
+                          const uint32_t* counters, int64_t k_cap, double* xchg);
+int launch_joint_sum(cudaStream_t st, float* g0, const float* rest, int64_t len, int nrest, int64_t stride);
+int64_t joint_adam_blocks(int64_t n);
+int launch_joint_adam(cudaStream_t st, float* params, const float* grads, float* m, float* v, int64_t n,
+                      int64_t n_pad, const void* js, const JointCtl& ctl, const double* xchg, double* red_blocks);
+int launch_joint_finalize(cudaStream_t st, void* js, const int32_t* seq, const JointCtl& ctl, const double* xchg,
+                          const double* red_blocks, int64_t nblocks, void* poses, CamDev* cams, double* trace_total,
+                          double* trace_l1);
+size_t joint_state_bytes();
+size_t joint_xchg_doubles();
+void joint_state_read(const void* host, int64_t* t, int32_t* diverged, int32_t* aborted, double* k_max,
+                      int32_t* tile);
+void joint_state_clear_abort(void* host);
 int launch_cloud_adam(cudaStream_t st, float* params, const float* grads, float* m, float* v, int64_t n,
                       int64_t n_pad, int sh_degree, const double lrs[6], const int64_t steps[5]);
 
@@ -1798,6 +1817,459 @@ int gsb_estimate_poses(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* const* targets
   for (gsb_session* s : ss)
     if (s) gsb_session_destroy(s);
   return r;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ NCCL (dlopen)
+namespace gsb {
+
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+// libnccl.so.2 is resolved at run time: the library (and every non-DP path)
+// loads without it; a process that already loaded NCCL (e.g. torch's) shares it.
+static NcclApi& nccl() {
+  static NcclApi api;
+  if (api.tried) return api;
+  api.tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return api;
+  api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+  api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+  api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
+  api.group_start = reinterpret_cast<decltype(api.group_start)>(dlsym(h, "ncclGroupStart"));
+  api.group_end = reinterpret_cast<decltype(api.group_end)>(dlsym(h, "ncclGroupEnd"));
+  api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+  api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+  api.ok = api.get_unique_id && api.comm_init_rank && api.all_reduce && api.group_start && api.group_end &&
+           api.comm_destroy && api.error_string;
+  return api;
+}
+
+static int nccl_fail(ncclResult_t r, const char* what) {
+  return fail(GSB_ERR_CUDA + 4, std::string(what) + ": " + (nccl().error_string ? nccl().error_string(r) : "nccl"));
+}
+
+}  // namespace gsb
+
+struct gsb_comm {
+  gsb_ctx* ctx = nullptr;
+  ncclComm_t comm = nullptr;
+  int32_t rank = 0, world = 1;
+};
+
+extern "C" {
+
+int gsb_comm_unique_id(uint8_t id_out[128]) {
+  if (!id_out) return fail(GSB_ERR_INVALID_ARGUMENT, "null id");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  if (!nccl().ok) return fail(GSB_ERR_NO_DEVICE, "libnccl.so.2 not loadable");
+  ncclUniqueId id;
+  if (ncclResult_t r = nccl().get_unique_id(&id)) return nccl_fail(r, "ncclGetUniqueId");
+  std::memcpy(id_out, &id, sizeof id);
+  return GSB_OK;
+}
+
+int gsb_comm_create(gsb_ctx* ctx, const uint8_t id[128], int32_t rank, int32_t world, gsb_comm** out) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!id || !out || world < 1 || rank < 0 || rank >= world) return fail(GSB_ERR_INVALID_ARGUMENT, "bad comm args");
+  if (!nccl().ok) return fail(GSB_ERR_NO_DEVICE, "libnccl.so.2 not loadable");
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof uid);
+  gsb_comm* c = new gsb_comm();
+  c->ctx = ctx;
+  c->rank = rank;
+  c->world = world;
+  if (ncclResult_t r = nccl().comm_init_rank(&c->comm, world, uid, rank)) {
+    delete c;
+    return nccl_fail(r, "ncclCommInitRank");
+  }
+  *out = c;
+  return GSB_OK;
+}
+
+int gsb_comm_destroy(gsb_comm* c) {
+  if (!c) return GSB_OK;
+  cudaSetDevice(c->ctx->device);
+  cudaStreamSynchronize(c->ctx->stream);
+  if (c->comm) nccl().comm_destroy(c->comm);
+  delete c;
+  return GSB_OK;
+}
+
+int gsb_comm_allreduce_f32(gsb_comm* c, float* dev_buf, int64_t n) {
+  if (!c) return fail(GSB_ERR_INVALID_ARGUMENT, "null comm");
+  if (int r = ensure_device(c->ctx)) return r;
+  if (n <= 0) return GSB_OK;
+  if (ncclResult_t r = nccl().all_reduce(dev_buf, dev_buf, (size_t)n, ncclFloat32, ncclSum, c->comm, c->ctx->stream))
+    return nccl_fail(r, "ncclAllReduce");
+  GSB_CUDA(cudaStreamSynchronize(c->ctx->stream));
+  return GSB_OK;
+}
+
+void gsb_default_joint_config(gsb_joint_config* c) {  // trainer.hpp:21-60, losses.hpp:15-19
+  c->iterations = 30000;
+  c->cam_lr_start = 1e-2;
+  c->cam_lr_end = 1e-4;
+  c->pos_lr_start = 1.6e-2;
+  c->pos_lr_end = 1.6e-4;
+  c->rot_lr = 1e-3;
+  c->scale_lr = 5e-3;
+  c->opacity_lr = 5e-2;
+  c->sh_dc_lr = 2.5e-3;
+  c->sh_rest_lr = 2.5e-3 / 20.0;
+  c->opacity_l1_steps = 10000;
+  c->sh_degree = 3;
+  c->sh_degree_interval = 1000;
+  c->optimize_poses = 1;
+  c->beta = 0.2;
+  c->aniso_ratio = 10.0;
+  c->opacity_l1_weight = 0.01;
+  c->background[0] = c->background[1] = c->background[2] = 0.0;
+  gsb_default_raster_config(&c->raster);
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------- joint loop
+// joint_optimize (pipelines.cpp:96-216, densification off) on the device:
+// one CUDA graph per step covers the rank's `local` slots (camera + target
+// selection, render, loss, full backward), the slot sum, the NCCL
+// all-reduce of the gradient planes and of the FP64 exchange slots (d_pose,
+// losses, overflow flags), the Adam step with the regularisers and the pose
+// steps. Every rank sees identical reduced bytes, so replicas stay bitwise
+// in sync without broadcasting parameters.
+struct gsb_joint {
+  gsb_ctx* ctx = nullptr;
+  gsb_cloud* cloud = nullptr;
+  gsb_comm* comm = nullptr;
+  gsb_joint_config cfg{};
+  JointCtl ctl{};
+  int32_t n_views = 0, local = 1, world = 1, rank = 0;
+  gsb_camera cam{};  // intrinsics + size (pose per view lives on the device)
+  std::vector<gsb_frame*> frames;
+  DevBuf grads, adam_m, adam_v, state, seq, poses, cams, tptrs, tbuf, xchg, red, trace_total, trace_l1;
+  int64_t glen = 0;  // floats per gradient copy ((planes + 2) * n_pad)
+  void* host_state = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int64_t graph_launches = 0;
+  std::vector<uint64_t> graph_gen;
+  std::vector<int64_t> graph_kcap;
+  int graph_active = -1;
+  int64_t t = 0;  // steps completed as of the last sync
+  int64_t sh_grown_t = -1;  // step at which the active SH degree last grew
+};
+
+namespace gsb {
+
+static int joint_launch_step(gsb_ctx* ctx, gsb_joint* j) {
+  cudaStream_t st = ctx->stream;
+  const RasterDev rc = make_rasterdev(&j->cfg.raster);
+  const int64_t P = (int64_t)j->cam.width * j->cam.height;
+  const size_t xbytes = sizeof(double) * joint_xchg_doubles() * (size_t)j->ctl.slots;
+  GSB_CUDA(cudaMemsetAsync(j->xchg.p, 0, xbytes, st));
+  for (int b = 0; b < j->local; ++b) {
+    gsb_frame* f = j->frames[b];
+    float* tb = j->tbuf.as<float>() + (size_t)b * 3 * P;
+    float* gb = j->grads.as<float>() + (size_t)b * j->glen;
+    if (int r = launch_joint_slot_begin(st, j->state.p, j->seq.as<int32_t>(), j->ctl, b, j->cams.as<CamDev>(),
+                                        f->cam.as<CamDev>(), j->tptrs.as<const float*>(), tb, 3 * P))
+      return r;
+    if (int r = render_async(ctx, j->cloud, f, rc)) return r;
+    if (int r = loss_device(ctx, f, tb, j->cfg.beta, true)) return r;
+    if (int r = backward_device(ctx, j->cloud, f, true, gb)) return r;
+    if (int r = launch_joint_slot_end(st, j->ctl, b, f->d_pose.as<double>(), f->loss_val.as<double>(),
+                                      f->counters.as<uint32_t>(), f->k_cap, j->xchg.as<double>()))
+      return r;
+    ctx->launches += 2;
+  }
+  if (j->local > 1) {
+    if (int r = launch_joint_sum(st, j->grads.as<float>(), j->grads.as<float>() + j->glen, j->glen, j->local - 1,
+                                 j->glen))
+      return r;
+    ctx->launches += 1;
+  }
+  if (j->comm && j->world > 1) {  // gradient planes (FP32) and exchange slots (FP64), one NCCL group
+    NcclApi& nc = nccl();
+    if (ncclResult_t r = nc.group_start()) return nccl_fail(r, "ncclGroupStart");
+    ncclResult_t r1 = nc.all_reduce(j->grads.p, j->grads.p, (size_t)j->glen, ncclFloat32, ncclSum, j->comm->comm, st);
+    ncclResult_t r2 = nc.all_reduce(j->xchg.p, j->xchg.p, joint_xchg_doubles() * (size_t)j->ctl.slots, ncclFloat64,
+                                    ncclSum, j->comm->comm, st);
+    ncclResult_t r3 = nc.group_end();
+    if (r1 || r2 || r3) return nccl_fail(r1 ? r1 : (r2 ? r2 : r3), "ncclAllReduce (joint)");
+  }
+  const int64_t nb = joint_adam_blocks(j->cloud->n);
+  if (int r = launch_joint_adam(st, j->cloud->params.as<float>(), j->grads.as<float>(), j->adam_m.as<float>(),
+                                j->adam_v.as<float>(), j->cloud->n, j->cloud->n_pad, j->state.p, j->ctl,
+                                j->xchg.as<double>(), j->red.as<double>()))
+    return r;
+  if (int r = launch_joint_finalize(st, j->state.p, j->seq.as<int32_t>(), j->ctl, j->xchg.as<double>(),
+                                    j->red.as<double>(), nb, j->poses.p, j->cams.as<CamDev>(),
+                                    j->trace_total.as<double>(), j->trace_l1.as<double>()))
+    return r;
+  ctx->launches += 2;
+  return GSB_OK;
+}
+
+static int joint_frames_ready(gsb_ctx* ctx, gsb_joint* j) {
+  for (gsb_frame* f : j->frames) {
+    if (int r = frame_setup(ctx, f, j->cloud, &j->cam, j->cfg.background, &j->cfg.raster, false)) return r;
+    const int64_t want = f->k_cap > 0 ? f->k_cap : std::max<int64_t>(3 * j->cloud->n, 1 << 16);
+    if (int r = frame_reserve(f, j->cloud, want)) return r;
+  }
+  return GSB_OK;
+}
+
+static int joint_prepare(gsb_ctx* ctx, gsb_joint* j) {
+  if (int r = joint_frames_ready(ctx, j)) return r;
+  bool stale = !j->exec || j->graph_active != j->cloud->active_sh_degree;
+  for (size_t b = 0; b < j->frames.size() && !stale; ++b)
+    stale = j->frames[b]->gen != j->graph_gen[b] || j->frames[b]->k_cap != j->graph_kcap[b];
+  if (!stale) return GSB_OK;
+  if (j->exec) cudaGraphExecDestroy(j->exec);
+  j->exec = nullptr;
+  const bool profiling = ctx->profiling;
+  ctx->profiling = false;
+  const int64_t launches0 = ctx->launches;
+  GSB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  int r = joint_launch_step(ctx, j);
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+  ctx->profiling = profiling;
+  if (r || e != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    ctx->launches = launches0;
+    return r ? r : cuda_fail(e, "joint capture");
+  }
+  e = cudaGraphInstantiate(&j->exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate (joint)");
+  j->graph_launches = ctx->launches - launches0;
+  ctx->launches = launches0;
+  for (size_t b = 0; b < j->frames.size(); ++b) {
+    j->graph_gen[b] = j->frames[b]->gen;
+    j->graph_kcap[b] = j->frames[b]->k_cap;
+  }
+  j->graph_active = j->cloud->active_sh_degree;
+  if (debug_on()) std::fprintf(stderr, "[gsb] joint graph captured: %lld kernels\n", (long long)j->graph_launches);
+  return GSB_OK;
+}
+
+// Launches `k` replays, waits, re-runs steps discarded for entry-capacity
+// growth (every rank sees the same discard count through the exchange slots).
+static int joint_run(gsb_ctx* ctx, gsb_joint* j, int64_t k) {
+  const size_t sb = joint_state_bytes();
+  for (int round = 0; round < 8 && k > 0; ++round) {
+    if (int r = joint_prepare(ctx, j)) return r;
+    for (int64_t i = 0; i < k; ++i) GSB_CUDA(cudaGraphLaunch(j->exec, ctx->stream));
+    ctx->launches += j->graph_launches * k;
+    ++j->cloud->version;
+    GSB_CUDA(cudaMemcpyAsync(j->host_state, j->state.p, sb, cudaMemcpyDeviceToHost, ctx->stream));
+    GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    int64_t t = 0;
+    int32_t div = 0, aborted = 0, tile = 0;
+    double kmax = 0.0;
+    joint_state_read(j->host_state, &t, &div, &aborted, &kmax, &tile);
+    j->t = t;
+    if (div) return fail(GSB_ERR_DIVERGED, "joint_optimize: non-finite loss at step " + std::to_string(div - 1));
+    if (aborted == 0) return GSB_OK;
+    if (debug_on()) std::fprintf(stderr, "[gsb] joint: %d step(s) discarded (K %.0f, tile overflow %d)\n", aborted, kmax, tile);
+    joint_state_clear_abort(j->host_state);
+    GSB_CUDA(cudaMemcpyAsync(j->state.p, j->host_state, sb, cudaMemcpyHostToDevice, ctx->stream));
+    for (gsb_frame* f : j->frames) {
+      if (tile) fall_back_to_global(f);
+      if (int r = frame_reserve(f, j->cloud, std::max<int64_t>(f->k_cap, (int64_t)kmax + (int64_t)kmax / 4 + 4096)))
+        return r;
+    }
+    k = aborted;
+  }
+  return k > 0 ? fail(GSB_ERR_OUT_OF_MEMORY, "joint: entry capacity did not converge") : GSB_OK;
+}
+
+}  // namespace gsb
+
+extern "C" {
+
+int gsb_joint_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* const* targets, int32_t n_views,
+                     const double intr[4], const double* init_poses, const gsb_joint_config* cfg, uint64_t seed,
+                     int32_t local_views, gsb_comm* comm, gsb_joint** out) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!cloud || !targets || !intr || !init_poses || !cfg || !out) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  if (n_views < 2) return fail(GSB_ERR_INVALID_CONFIG, "joint_optimize: need >= 2 images");  // pipelines.cpp:101
+  if (local_views < 1 || cfg->iterations < 0) return fail(GSB_ERR_INVALID_CONFIG, "bad joint config");
+  if (int r = validate_config(&cfg->raster)) return r;
+  if (comm && comm->ctx != ctx) return fail(GSB_ERR_INVALID_ARGUMENT, "comm / context mismatch");
+  const int W = targets[0]->width, H = targets[0]->height;
+  for (int32_t v = 0; v < n_views; ++v)
+    if (!targets[v] || targets[v]->width != W || targets[v]->height != H)
+      return fail(GSB_ERR_DIMENSION_MISMATCH, "joint_optimize: target sizes differ");
+  gsb_joint* j = new gsb_joint();
+  j->ctx = ctx;
+  j->cloud = cloud;
+  j->comm = comm;
+  j->cfg = *cfg;
+  j->n_views = n_views;
+  j->local = local_views;
+  j->world = comm ? comm->world : 1;
+  j->rank = comm ? comm->rank : 0;
+  j->cam.fx = intr[0];
+  j->cam.fy = intr[1];
+  j->cam.cx = intr[2];
+  j->cam.cy = intr[3];
+  j->cam.width = W;
+  j->cam.height = H;
+  for (int k = 0; k < 9; ++k) j->cam.R[k] = (k % 4 == 0) ? 1.0 : 0.0;
+  const int slots = j->local * j->world;
+  const int np = num_planes(cloud->sh_degree);
+  JointCtl& c = j->ctl;
+  c.iterations = cfg->iterations;
+  c.slots = slots;
+  c.slot0 = j->rank * j->local;
+  c.local = j->local;
+  c.n_views = n_views;
+  c.opacity_l1_steps = cfg->opacity_l1_steps;
+  c.optimize_poses = cfg->optimize_poses;
+  c.nplanes = np;
+  c.basis = (cloud->sh_degree + 1) * (cloud->sh_degree + 1);
+  c.pos_lr_start = cfg->pos_lr_start;
+  c.pos_lr_end = cfg->pos_lr_end;
+  c.rot_lr = cfg->rot_lr;
+  c.scale_lr = cfg->scale_lr;
+  c.opacity_lr = cfg->opacity_lr;
+  c.sh_dc_lr = cfg->sh_dc_lr;
+  c.sh_rest_lr = cfg->sh_rest_lr;
+  c.cam_lr_start = cfg->cam_lr_start;
+  c.cam_lr_end = cfg->cam_lr_end;
+  c.aniso_ratio = cfg->aniso_ratio;
+  c.opacity_l1_weight = cfg->opacity_l1_weight;
+  c.inv_slots = 1.0 / (double)slots;
+  j->glen = (int64_t)(np + 2) * cloud->n_pad;
+  const int64_t P = (int64_t)W * H;
+  const int64_t iters = std::max(cfg->iterations, 1);
+  const int64_t nb = joint_adam_blocks(std::max<int64_t>(cloud->n, 1));
+  const size_t sb = joint_state_bytes();
+  cudaError_t e = j->grads.reserve(sizeof(float) * j->glen * j->local);
+  if (e == cudaSuccess) e = j->adam_m.reserve(sizeof(float) * np * cloud->n_pad);
+  if (e == cudaSuccess) e = j->adam_v.reserve(sizeof(float) * np * cloud->n_pad);
+  if (e == cudaSuccess) e = j->state.reserve(sb);
+  if (e == cudaSuccess) e = j->seq.reserve(sizeof(int32_t) * iters * slots);
+  if (e == cudaSuccess) e = j->poses.reserve(pose_state_bytes() * n_views);
+  if (e == cudaSuccess) e = j->cams.reserve(sizeof(CamDev) * n_views);
+  if (e == cudaSuccess) e = j->tptrs.reserve(sizeof(float*) * n_views);
+  if (e == cudaSuccess) e = j->tbuf.reserve(sizeof(float) * 3 * P * j->local);
+  if (e == cudaSuccess) e = j->xchg.reserve(sizeof(double) * joint_xchg_doubles() * slots);
+  if (e == cudaSuccess) e = j->red.reserve(sizeof(double) * 2 * nb);
+  if (e == cudaSuccess) e = j->trace_total.reserve(sizeof(double) * iters);
+  if (e == cudaSuccess) e = j->trace_l1.reserve(sizeof(double) * iters);
+  if (e == cudaSuccess) e = cudaMallocHost(&j->host_state, std::max<size_t>(sb, 64));
+  if (e != cudaSuccess) {
+    gsb_joint_destroy(j);
+    return cuda_fail(e, "joint alloc");
+  }
+  // host-side initial state: schedule, per-view PoseState + CamDev, target pointers
+  std::vector<int32_t> seq((size_t)iters * slots);
+  if (int r = gsb_joint_schedule(seed, n_views, (int64_t)seq.size(), seq.data())) {
+    gsb_joint_destroy(j);
+    return r;
+  }
+  std::vector<char> ps(pose_state_bytes() * n_views);
+  std::vector<CamDev> cams(n_views);
+  std::vector<const float*> tp(n_views);
+  for (int32_t v = 0; v < n_views; ++v) {
+    pose_state_init(ps.data() + pose_state_bytes() * v, init_poses + 12 * (size_t)v);
+    gsb_camera cv = j->cam;
+    for (int r = 0; r < 3; ++r) {
+      for (int k = 0; k < 3; ++k) cv.R[r * 3 + k] = init_poses[12 * (size_t)v + r * 4 + k];
+      cv.t[r] = init_poses[12 * (size_t)v + r * 4 + 3];
+    }
+    cams[v] = make_camdev(&cv, kTile);
+    tp[v] = targets[v]->planes.as<float>();
+  }
+  std::memset(j->host_state, 0, sb);
+  cudaStream_t st = ctx->stream;
+  GSB_CUDA(cudaMemcpyAsync(j->seq.p, seq.data(), sizeof(int32_t) * seq.size(), cudaMemcpyHostToDevice, st));
+  GSB_CUDA(cudaMemcpyAsync(j->poses.p, ps.data(), ps.size(), cudaMemcpyHostToDevice, st));
+  GSB_CUDA(cudaMemcpyAsync(j->cams.p, cams.data(), sizeof(CamDev) * n_views, cudaMemcpyHostToDevice, st));
+  GSB_CUDA(cudaMemcpyAsync(j->tptrs.p, tp.data(), sizeof(float*) * n_views, cudaMemcpyHostToDevice, st));
+  GSB_CUDA(cudaMemcpyAsync(j->state.p, j->host_state, sb, cudaMemcpyHostToDevice, st));
+  GSB_CUDA(cudaMemsetAsync(j->adam_m.p, 0, sizeof(float) * np * cloud->n_pad, st));
+  GSB_CUDA(cudaMemsetAsync(j->adam_v.p, 0, sizeof(float) * np * cloud->n_pad, st));
+  GSB_CUDA(cudaMemsetAsync(j->grads.p, 0, sizeof(float) * j->glen * j->local, st));
+  GSB_CUDA(cudaStreamSynchronize(st));
+  for (int b = 0; b < j->local; ++b) {
+    gsb_frame* f = new gsb_frame();
+    f->ctx = ctx;
+    j->frames.push_back(f);
+  }
+  j->graph_gen.assign(j->local, 0);
+  j->graph_kcap.assign(j->local, 0);
+  *out = j;
+  return GSB_OK;
+}
+
+int gsb_joint_destroy(gsb_joint* j) {
+  if (!j) return GSB_OK;
+  cudaSetDevice(j->ctx->device);
+  cudaStreamSynchronize(j->ctx->stream);
+  if (j->exec) cudaGraphExecDestroy(j->exec);
+  for (gsb_frame* f : j->frames) gsb_frame_destroy(f);
+  DevBuf* bufs[] = {&j->grads, &j->adam_m, &j->adam_v, &j->state, &j->seq, &j->poses, &j->cams, &j->tptrs,
+                    &j->tbuf, &j->xchg, &j->red, &j->trace_total, &j->trace_l1};
+  for (DevBuf* b : bufs) b->release();
+  if (j->host_state) cudaFreeHost(j->host_state);
+  delete j;
+  return GSB_OK;
+}
+
+int gsb_joint_step(gsb_ctx* ctx, gsb_joint* j, int32_t steps) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!j || j->ctx != ctx) return fail(GSB_ERR_INVALID_ARGUMENT, "joint / context mismatch");
+  int64_t left = std::min<int64_t>(steps, (int64_t)j->cfg.iterations - j->t);
+  const int interval = j->cfg.sh_degree_interval;
+  while (left > 0) {
+    // SH degree growth at the start of step t (pipelines.cpp:130-133): chunks end on growth steps
+    if (interval > 0 && j->t > 0 && j->t % interval == 0 && j->sh_grown_t != j->t) {
+      j->cloud->active_sh_degree = std::min(j->cloud->active_sh_degree + 1, j->cfg.sh_degree);
+      j->sh_grown_t = j->t;
+    }
+    int64_t chunk = std::min<int64_t>(left, 16);
+    if (interval > 0) chunk = std::min<int64_t>(chunk, interval - (j->t % interval));
+    const int64_t t0 = j->t;
+    if (int r = joint_run(ctx, j, chunk)) return r;
+    left -= j->t - t0;
+    if (j->t == t0) return fail(GSB_ERR_CUDA, "joint: no progress");
+  }
+  return GSB_OK;
+}
+
+int gsb_joint_read(gsb_joint* j, double* poses_out, int64_t* steps_done, double* trace_total, double* trace_l1) {
+  if (!j) return fail(GSB_ERR_INVALID_ARGUMENT, "null joint");
+  gsb_ctx* ctx = j->ctx;
+  if (int r = ensure_device(ctx)) return r;
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (steps_done) *steps_done = j->t;
+  if (poses_out) {
+    std::vector<char> ps(pose_state_bytes() * j->n_views);
+    GSB_CUDA(cudaMemcpy(ps.data(), j->poses.p, ps.size(), cudaMemcpyDeviceToHost));
+    for (int32_t v = 0; v < j->n_views; ++v)
+      pose_state_read(ps.data() + pose_state_bytes() * v, nullptr, poses_out + 12 * (size_t)v, nullptr, nullptr,
+                      nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+  }
+  const size_t nt = (size_t)std::max<int64_t>(j->t, 0);
+  if (trace_total && nt) GSB_CUDA(cudaMemcpy(trace_total, j->trace_total.p, sizeof(double) * nt, cudaMemcpyDeviceToHost));
+  if (trace_l1 && nt) GSB_CUDA(cudaMemcpy(trace_l1, j->trace_l1.p, sizeof(double) * nt, cudaMemcpyDeviceToHost));
+  return GSB_OK;
 }
 
 }  // extern "C"

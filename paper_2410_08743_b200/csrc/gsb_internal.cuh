@@ -162,6 +162,13 @@ enum Stage : int {
 
 struct StageTimer;  // defined in api.cu
 
+// Joint-loop constants passed by value to the joint kernels (k_optim.cu).
+struct JointCtl {
+  int32_t iterations, slots, slot0, local, n_views, opacity_l1_steps, optimize_poses, nplanes, basis;
+  double pos_lr_start, pos_lr_end, rot_lr, scale_lr, opacity_lr, sh_dc_lr, sh_rest_lr, cam_lr_start, cam_lr_end;
+  double aniso_ratio, opacity_l1_weight, inv_slots;
+};
+
 }  // namespace gsb
 
 // ------------------------------------------------------------- C structs

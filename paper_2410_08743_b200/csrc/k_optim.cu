@@ -17,6 +17,7 @@
 // bits changed.
 #include "gsb_internal.cuh"
 
+#include <algorithm>
 #include <cmath>
 
 namespace gsb {
@@ -328,6 +329,314 @@ __global__ void __launch_bounds__(256) cloud_adam_kernel(float* __restrict__ par
     const float nn = sqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
     for (int k = 0; k < 4; ++k) params[(int64_t)(kQuatW + k) * n_pad + i] = q[k] / nn;
   }
+}
+
+// ------------------------------------------------------------ joint loop
+// joint_optimize (pipelines.cpp:96-216) as a device-resident step: `slots`
+// training views per step (data parallel: `local` of them on this rank, the
+// rest on the other ranks), the Adam gradient is the mean of the slots'
+// render gradients plus the anisotropy / opacity-L1 regularisers evaluated
+// once on the pre-step parameters (losses.cpp:217-257, pipelines.cpp:144-157),
+// then the slots' pose steps in slot order (176-180). The step counter, the
+// learning-rate schedules and Adam's bias corrections live on the device, so
+// one CUDA graph replays every step. See DESIGN.md §7.
+
+// Exchange slot (FP64, summed over ranks = gathered): d_pose, L1, SSIM,
+// rgb loss, overflow flag, K seen, tile overflow.
+constexpr int kXchgW = 12;
+enum XchgField : int { kXPose = 0, kXL1 = 6, kXSsim = 7, kXRgb = 8, kXOvf = 9, kXK = 10, kXTile = 11 };
+
+struct JointDev {
+  int64_t t;          // steps completed
+  int64_t adam_step;  // CloudAdam / AdamState step (== t unless steps were discarded)
+  int32_t diverged;   // 1 + the step whose total loss was non-finite (0: none)
+  int32_t aborted;    // steps discarded for capacity growth since the host last looked
+  double abort_k_max;
+  int32_t abort_tile;
+  int32_t pad;
+};
+
+// schedule (trainer.cpp:30-38): kind 0 cosine, 1 exponential
+__device__ double d_schedule(int kind, double start, double end, int64_t step, int64_t total) {
+  if (total <= 0) return end;
+  double s = (double)step / (double)total;
+  s = s < 0.0 ? 0.0 : (s > 1.0 ? 1.0 : s);
+  if (kind == 0) return end + (start - end) * 0.5 * (1.0 + cos(M_PI * s));
+  return start * pow(end / start, s);
+}
+
+// Slot b of this rank: camera of the scheduled view into the frame, target
+// planes into the frame's target buffer (3 P floats).
+__global__ void joint_slot_begin_kernel(const JointDev* __restrict__ js, const int32_t* __restrict__ seq, JointCtl ctl,
+                                        int b, const CamDev* __restrict__ cams, CamDev* __restrict__ frame_cam,
+                                        const float* const* __restrict__ targets, float* __restrict__ tbuf,
+                                        int64_t n3p) {
+  const int64_t t = js->t < ctl.iterations ? js->t : ctl.iterations - 1;
+  const int v = seq[t * ctl.slots + ctl.slot0 + b];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *frame_cam = cams[v];
+  const float4* src = reinterpret_cast<const float4*>(targets[v]);
+  float4* dst = reinterpret_cast<float4*>(tbuf);
+  const int64_t n4 = n3p >> 2;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+  for (int64_t i = (n4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n3p;
+       i += (int64_t)gridDim.x * blockDim.x)
+    tbuf[i] = targets[v][i];
+}
+
+// Slot b's results into the exchange buffer (zeroed at step start).
+__global__ void joint_slot_end_kernel(JointCtl ctl, int b, const double* __restrict__ d_pose,
+                                      const double* __restrict__ loss3, const uint32_t* __restrict__ counters,
+                                      int64_t k_cap, double* __restrict__ xchg) {
+  double* x = xchg + (int64_t)(ctl.slot0 + b) * kXchgW;
+  for (int k = 0; k < 6; ++k) x[kXPose + k] = d_pose[k];
+  x[kXL1] = loss3[0];
+  x[kXSsim] = loss3[1];
+  x[kXRgb] = loss3[2];
+  const bool ovf = (int64_t)counters[1] > k_cap || counters[2] != 0u;
+  x[kXOvf] = ovf ? 1.0 : 0.0;
+  x[kXK] = (double)counters[1];
+  x[kXTile] = counters[2] != 0u ? 1.0 : 0.0;
+}
+
+// grads[0] += grads[1..local-1] in slot order (local batches on one rank).
+__global__ void joint_sum_kernel(float* __restrict__ g0, const float* __restrict__ rest, int64_t len, int nrest,
+                                 int64_t stride) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= len) return;
+  float acc = g0[i];
+  for (int b = 0; b < nrest; ++b) acc += rest[(int64_t)b * stride + i];
+  g0[i] = acc;
+}
+
+__device__ __forceinline__ bool joint_step_discarded(const double* xchg, int slots) {
+  for (int s = 0; s < slots; ++s)
+    if (xchg[(int64_t)s * kXchgW + kXOvf] != 0.0) return true;
+  return false;
+}
+
+// cloud_adam_step (pipelines.cpp:18-41) on the averaged gradient plus the
+// regularisers, one thread per Gaussian over the FP32 planes; block partial
+// sums (aniso loss, opacity sum) for the step's total loss. Skipped when the
+// step is discarded (some slot overflowed its entry capacity) or has already
+// run out of iterations.
+constexpr int kJointBlock = 256;
+__global__ void __launch_bounds__(kJointBlock) joint_adam_kernel(float* __restrict__ params,
+                                                               const float* __restrict__ grads, float* __restrict__ m,
+                                                               float* __restrict__ v, int64_t n, int64_t n_pad,
+                                                               const JointDev* __restrict__ js, JointCtl ctl,
+                                                               const double* __restrict__ xchg,
+                                                               double* __restrict__ red_blocks) {
+  __shared__ float s_lr[6], s_bc1, s_bc2;
+  __shared__ int s_skip, s_opl1;
+  __shared__ double s_red[kJointBlock / 32][2];
+  if (threadIdx.x == 0) {
+    const int64_t t = js->t;
+    s_skip = (t >= ctl.iterations || js->diverged || joint_step_discarded(xchg, ctl.slots)) ? 1 : 0;
+    s_opl1 = (t < ctl.opacity_l1_steps && ctl.opacity_l1_weight > 0.0) ? 1 : 0;
+    const double st = (double)(js->adam_step + 1);
+    s_bc1 = (float)(1.0 - pow(kB1, st));
+    s_bc2 = (float)(1.0 - pow(kB2, st));
+    s_lr[0] = (float)d_schedule(1, ctl.pos_lr_start, ctl.pos_lr_end, t, ctl.iterations);
+    s_lr[1] = (float)ctl.rot_lr;
+    s_lr[2] = (float)ctl.scale_lr;
+    s_lr[3] = (float)ctl.opacity_lr;
+    s_lr[4] = (float)ctl.sh_dc_lr;
+    s_lr[5] = (float)ctl.sh_rest_lr;
+  }
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double aniso = 0.0, opsum = 0.0;
+  if (i < n) {
+    const double inv_n = 1.0 / (double)n;
+    // anisotropy_loss (losses.cpp:217-244) on the pre-step log-scales
+    double sc[3];
+    for (int k = 0; k < 3; ++k) sc[k] = exp((double)params[(int64_t)(kScaleX + k) * n_pad + i]);
+    int amax = 0, amin = 0;
+    for (int k = 1; k < 3; ++k) {
+      if (sc[k] > sc[amax]) amax = k;
+      if (sc[k] < sc[amin]) amin = k;
+    }
+    const double r = sc[amax] / sc[amin];
+    double dls[3] = {0.0, 0.0, 0.0};
+    if (r > ctl.aniso_ratio) {
+      aniso = (r - ctl.aniso_ratio) * inv_n;
+      dls[amax] += inv_n / sc[amin] * sc[amax];
+      dls[amin] += -inv_n * sc[amax] / (sc[amin] * sc[amin]) * sc[amin];
+    }
+    // opacity_l1 (losses.cpp:246-257) through the sigmoid (pipelines.cpp:148-157)
+    const double o = 1.0 / (1.0 + exp(-(double)params[(int64_t)kOpacity * n_pad + i]));
+    opsum = o * inv_n;
+    const double dop = s_opl1 ? ctl.opacity_l1_weight * inv_n * o * (1.0 - o) : 0.0;
+    if (!s_skip) {
+      const float inv_s = (float)ctl.inv_slots;
+      bool quat_moved = false;
+      float q[4];
+      for (int p = 0; p < ctl.nplanes; ++p) {
+        const int64_t k = (int64_t)p * n_pad + i;
+        float lr;
+        if (p < kQuatW) lr = s_lr[0];
+        else if (p < kScaleX) lr = s_lr[1];
+        else if (p < kOpacity) lr = s_lr[2];
+        else if (p == kOpacity) lr = s_lr[3];
+        else lr = ((p - kShBase) % ctl.basis == 0) ? s_lr[4] : s_lr[5];
+        float gi = grads[k] * inv_s;
+        if (p >= kScaleX && p < kOpacity) gi = (float)((double)gi + dls[p - kScaleX]);
+        if (p == kOpacity) gi = (float)((double)gi + dop);
+        const float mi = 0.9f * m[k] + 0.1f * gi;
+        const float vi = 0.999f * v[k] + 0.001f * gi * gi;
+        m[k] = mi;
+        v[k] = vi;
+        const float old = params[k];
+        const float nw = old - lr * (mi / s_bc1) / (sqrtf(vi / s_bc2) + 1e-15f);
+        params[k] = nw;
+        if (p >= kQuatW && p < kScaleX) {
+          q[p - kQuatW] = nw;
+          quat_moved = quat_moved || (nw != old);
+        }
+      }
+      if (quat_moved) {  // pipelines.cpp:36-40
+        const float nn = sqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+        for (int k = 0; k < 4; ++k) params[(int64_t)(kQuatW + k) * n_pad + i] = q[k] / nn;
+      }
+    }
+  }
+  // fixed-order block reduction of (aniso, opacity sum)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    aniso += __shfl_xor_sync(0xffffffffu, aniso, o);
+    opsum += __shfl_xor_sync(0xffffffffu, opsum, o);
+  }
+  if (lane == 0) {
+    s_red[warp][0] = aniso;
+    s_red[warp][1] = opsum;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < kJointBlock / 32; ++w) {
+      a += s_red[w][0];
+      b += s_red[w][1];
+    }
+    red_blocks[2 * blockIdx.x] = a;
+    red_blocks[2 * blockIdx.x + 1] = b;
+  }
+}
+
+// Step tail: total loss trace and divergence check (pipelines.cpp:159-162),
+// the slots' pose steps in slot order with each view's PoseAdam and the
+// cosine camera schedule (176-180), step counters. One block.
+__global__ void joint_finalize_kernel(JointDev* __restrict__ js, const int32_t* __restrict__ seq, JointCtl ctl,
+                                      const double* __restrict__ xchg, const double* __restrict__ red_blocks,
+                                      int64_t nblocks, PoseState* __restrict__ poses, CamDev* __restrict__ cams,
+                                      double* __restrict__ trace_total, double* __restrict__ trace_l1) {
+  __shared__ double s_a[256], s_b[256];
+  double a = 0.0, b = 0.0;
+  for (int64_t k = threadIdx.x; k < nblocks; k += 256) {
+    a += red_blocks[2 * k];
+    b += red_blocks[2 * k + 1];
+  }
+  s_a[threadIdx.x] = a;
+  s_b[threadIdx.x] = b;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  JointDev j = *js;
+  if (j.t >= ctl.iterations || j.diverged) return;
+  if (joint_step_discarded(xchg, ctl.slots)) {  // the host grows the capacity and replays this step
+    j.aborted += 1;
+    for (int s = 0; s < ctl.slots; ++s) {
+      j.abort_k_max = fmax(j.abort_k_max, xchg[(int64_t)s * kXchgW + kXK]);
+      if (xchg[(int64_t)s * kXchgW + kXTile] != 0.0) j.abort_tile = 1;
+    }
+    *js = j;
+    return;
+  }
+  double aniso = 0.0, opsum = 0.0;
+  for (int k = 0; k < 256; ++k) {
+    aniso += s_a[k];
+    opsum += s_b[k];
+  }
+  double rgb = 0.0, l1 = 0.0;
+  for (int s = 0; s < ctl.slots; ++s) {
+    rgb += xchg[(int64_t)s * kXchgW + kXRgb];
+    l1 += xchg[(int64_t)s * kXchgW + kXL1];
+  }
+  const bool opl1 = j.t < ctl.opacity_l1_steps && ctl.opacity_l1_weight > 0.0;
+  const double total = rgb * ctl.inv_slots + aniso + ctl.opacity_l1_weight * (opl1 ? opsum : 0.0);
+  if (trace_total) trace_total[j.t] = total;
+  if (trace_l1) trace_l1[j.t] = l1 * ctl.inv_slots;
+  if (!isfinite(total)) j.diverged = (int32_t)(j.t + 1);
+  if (ctl.optimize_poses) {
+    const double lr = d_schedule(0, ctl.cam_lr_start, ctl.cam_lr_end, j.t, ctl.iterations);
+    for (int s = 0; s < ctl.slots; ++s) {
+      const int v = seq[j.t * ctl.slots + s];
+      PoseState p = poses[v];
+      d_pose_step(p, xchg + (int64_t)s * kXchgW + kXPose, lr);
+      poses[v] = p;
+      d_write_cam(p, &cams[v]);
+    }
+  }
+  j.t += 1;
+  j.adam_step += 1;
+  *js = j;
+}
+
+int launch_joint_slot_begin(cudaStream_t st, const void* js, const int32_t* seq, const JointCtl& ctl, int b,
+                            const CamDev* cams, CamDev* frame_cam, const float* const* targets, float* tbuf,
+                            int64_t n3p) {
+  const int64_t blocks = std::min<int64_t>((n3p / 4 + 255) / 256 + 1, 4 * 148);
+  joint_slot_begin_kernel<<<(unsigned)blocks, 256, 0, st>>>(static_cast<const JointDev*>(js), seq, ctl, b, cams,
+                                                            frame_cam, targets, tbuf, n3p);
+  GSB_CHECK_LAUNCH("joint_slot_begin_kernel");
+  return GSB_OK;
+}
+int launch_joint_slot_end(cudaStream_t st, const JointCtl& ctl, int b, const double* d_pose, const double* loss3,
+                          const uint32_t* counters, int64_t k_cap, double* xchg) {
+  joint_slot_end_kernel<<<1, 1, 0, st>>>(ctl, b, d_pose, loss3, counters, k_cap, xchg);
+  GSB_CHECK_LAUNCH("joint_slot_end_kernel");
+  return GSB_OK;
+}
+int launch_joint_sum(cudaStream_t st, float* g0, const float* rest, int64_t len, int nrest, int64_t stride) {
+  if (nrest > 0 && len > 0)
+    joint_sum_kernel<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(g0, rest, len, nrest, stride);
+  GSB_CHECK_LAUNCH("joint_sum_kernel");
+  return GSB_OK;
+}
+int64_t joint_adam_blocks(int64_t n) { return (n + kJointBlock - 1) / kJointBlock; }
+int launch_joint_adam(cudaStream_t st, float* params, const float* grads, float* m, float* v, int64_t n,
+                      int64_t n_pad, const void* js, const JointCtl& ctl, const double* xchg, double* red_blocks) {
+  const int64_t nb = joint_adam_blocks(n);
+  if (nb > 0)
+    joint_adam_kernel<<<(unsigned)nb, kJointBlock, 0, st>>>(params, grads, m, v, n, n_pad,
+                                                            static_cast<const JointDev*>(js), ctl, xchg, red_blocks);
+  GSB_CHECK_LAUNCH("joint_adam_kernel");
+  return GSB_OK;
+}
+int launch_joint_finalize(cudaStream_t st, void* js, const int32_t* seq, const JointCtl& ctl, const double* xchg,
+                          const double* red_blocks, int64_t nblocks, void* poses, CamDev* cams, double* trace_total,
+                          double* trace_l1) {
+  joint_finalize_kernel<<<1, 256, 0, st>>>(static_cast<JointDev*>(js), seq, ctl, xchg, red_blocks, nblocks,
+                                           static_cast<PoseState*>(poses), cams, trace_total, trace_l1);
+  GSB_CHECK_LAUNCH("joint_finalize_kernel");
+  return GSB_OK;
+}
+size_t joint_state_bytes() { return sizeof(JointDev); }
+size_t joint_xchg_doubles() { return kXchgW; }
+void joint_state_read(const void* host, int64_t* t, int32_t* diverged, int32_t* aborted, double* k_max,
+                      int32_t* tile) {
+  const JointDev* j = static_cast<const JointDev*>(host);
+  if (t) *t = j->t;
+  if (diverged) *diverged = j->diverged;
+  if (aborted) *aborted = j->aborted;
+  if (k_max) *k_max = j->abort_k_max;
+  if (tile) *tile = j->abort_tile;
+}
+void joint_state_clear_abort(void* host) {
+  JointDev* j = static_cast<JointDev*>(host);
+  j->aborted = 0;
+  j->abort_k_max = 0.0;
+  j->abort_tile = 0;
 }
 
 // ------------------------------------------------------------- host glue

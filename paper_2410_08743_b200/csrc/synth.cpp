@@ -4,6 +4,7 @@
 // only; nothing here is on the hot path. Vec3(rng(), rng(), rng())
 // constructor arguments are drawn right to left, matching a GCC x86-64
 // build of the reference.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <vector>
@@ -121,9 +122,97 @@ void so3_exp(const double w[3], double R[9]) {
   for (int k = 0; k < 9; ++k) R[k] = ((k % 4 == 0) ? 1.0 : 0.0) + a * W[k] + b * W2[k];
 }
 
+// se3_exp (lie.cpp:117-129): rotation as so3_exp, translation V(omega) v
+void se3_exp(const double tau[6], double R[9], double t[3]) {
+  const double* w = tau + 3;
+  so3_exp(w, R);
+  const double th = std::sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+  const double t2 = th * th;
+  double b, d;
+  if (th < 1e-8) {
+    b = 0.5 - t2 / 24.0;
+  } else {
+    const double hs = std::sin(0.5 * th);
+    b = 2.0 * hs * hs / t2;
+  }
+  d = th < 1e-2 ? 1.0 / 6.0 - t2 / 120.0 + t2 * t2 / 5040.0 : (th - std::sin(th)) / (t2 * th);
+  const double W[9] = {0.0, -w[2], w[1], w[2], 0.0, -w[0], -w[1], w[0], 0.0};
+  double W2[9], V[9];
+  mat3_mul(W, W, W2);
+  for (int k = 0; k < 9; ++k) V[k] = ((k % 4 == 0) ? 1.0 : 0.0) + b * W[k] + d * W2[k];
+  mat3_vec(V, tau, t);
+}
+
 }  // namespace
 
 extern "C" {
+
+// pipelines.cpp:122-129: `order` starts as iota and is shuffled in place at
+// every epoch start (j = rng.uniform_int(0, i) for i = n-1 .. 1).
+int gsb_joint_schedule(uint64_t seed, int32_t n_views, int64_t count, int32_t* seq_out) {
+  if (n_views <= 0 || count < 0 || (count > 0 && !seq_out))
+    return gsb::fail(GSB_ERR_INVALID_ARGUMENT, "bad joint schedule arguments");
+  Rng rng(seed);
+  std::vector<int32_t> order(n_views);
+  for (int32_t i = 0; i < n_views; ++i) order[i] = i;
+  for (int64_t k = 0; k < count; ++k) {
+    if (k % n_views == 0)
+      for (int32_t i = n_views - 1; i > 0; --i) {
+        const int32_t j = (int32_t)(rng.next() % (uint64_t)(i + 1));  // core.hpp:78-80
+        std::swap(order[i], order[j]);
+      }
+    seq_out[k] = order[k % n_views];
+  }
+  return GSB_OK;
+}
+
+// perturb_pose_tangent (eval.cpp:148-152): Exp(sigma * N(0, I_6)) * pose
+int gsb_perturb_pose_tangent(const double pose[12], double sigma, uint64_t* rng_state, double out[12]) {
+  if (!pose || !rng_state || !out) return gsb::fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  Rng rng(1);
+  rng.s = *rng_state ? *rng_state : 0x9e3779b97f4a7c15ull;
+  double tau[6];
+  for (int k = 0; k < 6; ++k) tau[k] = sigma * rng.normal();
+  *rng_state = rng.s;
+  double Re[9], te[3], R[9], t[3], Rn[9], tn[3];
+  se3_exp(tau, Re, te);
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c) R[r * 3 + c] = pose[r * 4 + c];
+    t[r] = pose[r * 4 + 3];
+  }
+  mat3_mul(Re, R, Rn);
+  mat3_vec(Re, t, tn);
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c) out[r * 4 + c] = Rn[r * 3 + c];
+    out[r * 4 + 3] = tn[r] + te[r];
+  }
+  return GSB_OK;
+}
+
+// Initial cloud of the joint tests (tests/test_trainer.cpp:598-601): means +=
+// mean_sigma * normal3 (GCC draws z, y, x), then per Gaussian log-scales +=
+// log_scale_range * uniform(-1, 1) (one draw for all three axes).
+int gsb_cloud_jitter(gsb_cloud* cloud, uint64_t seed, double mean_sigma, double log_scale_range) {
+  if (!cloud) return gsb::fail(GSB_ERR_INVALID_ARGUMENT, "null cloud");
+  const int64_t n = cloud->n;
+  const int basis = (cloud->sh_degree + 1) * (cloud->sh_degree + 1);
+  std::vector<double> means(3 * n), rot(4 * n), ls(3 * n), op(n), sh((size_t)3 * basis * n);
+  if (int r = gsb_cloud_download(cloud, means.data(), rot.data(), ls.data(), op.data(), sh.data())) return r;
+  Rng rng(seed);
+  for (int64_t i = 0; i < n; ++i) {
+    const double z = rng.normal(), y = rng.normal(), x = rng.normal();
+    means[3 * i] += mean_sigma * x;
+    means[3 * i + 1] += mean_sigma * y;
+    means[3 * i + 2] += mean_sigma * z;
+  }
+  if (log_scale_range != 0.0)
+    for (int64_t i = 0; i < n; ++i) {
+      const double u = log_scale_range * rng.uniform(-1.0, 1.0);
+      for (int k = 0; k < 3; ++k) ls[3 * i + k] += u;
+    }
+  return gsb_cloud_upload(cloud, means.data(), rot.data(), ls.data(), op.data(), sh.data(), cloud->active_sh_degree);
+}
+
 
 int gsb_cloud_synth(gsb_cloud* cloud, uint64_t seed, double log_scale_offset) {
   if (!cloud) return gsb::fail(GSB_ERR_INVALID_ARGUMENT, "null cloud");

@@ -113,6 +113,29 @@ _lib = None
 _vp = C.c_void_p
 
 
+class JointConfig(C.Structure):
+    """gsb_joint_config: the TrainConfig fields joint_optimize reads (trainer.hpp:21-60)."""
+    _fields_ = [("iterations", C.c_int32), ("cam_lr_start", C.c_double), ("cam_lr_end", C.c_double),
+                ("pos_lr_start", C.c_double), ("pos_lr_end", C.c_double), ("rot_lr", C.c_double),
+                ("scale_lr", C.c_double), ("opacity_lr", C.c_double), ("sh_dc_lr", C.c_double),
+                ("sh_rest_lr", C.c_double), ("opacity_l1_steps", C.c_int32), ("sh_degree", C.c_int32),
+                ("sh_degree_interval", C.c_int32), ("optimize_poses", C.c_int32), ("beta", C.c_double),
+                ("aniso_ratio", C.c_double), ("opacity_l1_weight", C.c_double), ("background", C.c_double * 3),
+                ("raster", RasterConfig)]
+
+    @staticmethod
+    def default(**kw) -> "JointConfig":
+        c = JointConfig()
+        lib().gsb_default_joint_config(C.byref(c))
+        for k, v in kw.items():
+            if k == "background":
+                for i in range(3):
+                    c.background[i] = v[i]
+            else:
+                setattr(c, k, v)
+        return c
+
+
 def _sigs():
     P = C.POINTER
     d, i32, i64, u32, u64 = C.c_double, C.c_int32, C.c_int64, C.c_uint32, C.c_uint64
@@ -173,6 +196,18 @@ def _sigs():
         "gsb_pose_batch_step_async": (C.c_int, [_vp, _vp, i32]),
         "gsb_pose_batch_sync": (C.c_int, [_vp, _vp]),
         "gsb_estimate_poses": (C.c_int, [_vp, _vp, _vp, _vp, _vp, i32, P(PoseConfig), _vp, _vp, _vp]),
+        "gsb_comm_unique_id": (C.c_int, [_vp]),
+        "gsb_comm_create": (C.c_int, [_vp, _vp, i32, i32, P(_vp)]),
+        "gsb_comm_destroy": (C.c_int, [_vp]),
+        "gsb_comm_allreduce_f32": (C.c_int, [_vp, _vp, i64]),
+        "gsb_default_joint_config": (None, [P(JointConfig)]),
+        "gsb_joint_schedule": (C.c_int, [u64, i32, i64, _vp]),
+        "gsb_joint_create": (C.c_int, [_vp, _vp, _vp, i32, _vp, _vp, P(JointConfig), u64, i32, _vp, P(_vp)]),
+        "gsb_joint_destroy": (C.c_int, [_vp]),
+        "gsb_joint_step": (C.c_int, [_vp, _vp, i32]),
+        "gsb_joint_read": (C.c_int, [_vp, _vp, P(i64), _vp, _vp]),
+        "gsb_perturb_pose_tangent": (C.c_int, [_vp, d, P(u64), _vp]),
+        "gsb_cloud_jitter": (C.c_int, [_vp, u64, d, d]),
     }
 
 
@@ -289,6 +324,10 @@ class Cloud:
         out = [np.zeros((n, 3)), np.zeros((n, 4)), np.zeros((n, 3)), np.zeros(n), np.zeros((n, 3, b))]
         _check(lib().gsb_cloud_download(self.h, *[_p(a) for a in out]))
         return out
+
+    def jitter(self, seed: int, mean_sigma: float, log_scale_range: float = 0.0):
+        """tests/test_trainer.cpp:598-601 initial-cloud jitter (gsb_cloud_jitter)."""
+        _check(lib().gsb_cloud_jitter(self.h, seed, mean_sigma, log_scale_range))
 
     def synth(self, seed: int, log_scale_offset: float = 0.0):
         _check(lib().gsb_cloud_synth(self.h, seed, log_scale_offset))
@@ -546,6 +585,86 @@ def estimate_poses(ctx: Context, cloud: Cloud, targets, intr, init_poses, config
     _check(lib().gsb_estimate_poses(ctx.h, cloud.h, arr, _p(intr), _p(init), n, C.byref(cfg), _p(out), _p(fl),
                                     _p(su)))
     return dict(pose=out, final_loss=fl, steps=su)
+
+
+class Comm:
+    """NCCL communicator for data-parallel joint training (gsb_comm). Rank 0
+    creates the unique id; the caller distributes it (e.g. torch.distributed)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _check(lib().gsb_comm_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, ctx: Context, uid: bytes, rank: int, world: int):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = _vp()
+        _check(lib().gsb_comm_create(ctx.h, buf, rank, world, C.byref(h)))
+        self.h, self.ctx, self.rank, self.world = h, ctx, rank, world
+
+    def close(self):
+        if self.h:
+            lib().gsb_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def joint_schedule(seed: int, n_views: int, count: int) -> np.ndarray:
+    """joint_optimize's training-view sequence (pipelines.cpp:122-129)."""
+    out = np.zeros(count, np.int32)
+    _check(lib().gsb_joint_schedule(seed, n_views, count, _p(out)))
+    return out
+
+
+class JointOptimizer:
+    """joint_optimize (pipelines.cpp:96-216, densification off) on the device,
+    `local_views` views per rank per step, data parallel over `comm`."""
+
+    def __init__(self, ctx: Context, cloud: Cloud, targets, intr, init_poses, config: JointConfig, seed: int,
+                 local_views: int = 1, comm: Comm | None = None):
+        self.cfg = config
+        intr = np.ascontiguousarray(intr, np.float64)
+        init = np.ascontiguousarray(init_poses, np.float64).reshape(-1, 12)
+        self.n_views = init.shape[0]
+        arr = (_vp * self.n_views)(*[t.h for t in targets])
+        h = _vp()
+        _check(lib().gsb_joint_create(ctx.h, cloud.h, arr, self.n_views, _p(intr), _p(init), C.byref(config), seed,
+                                      local_views, comm.h if comm else None, C.byref(h)))
+        self.h, self.ctx, self._keep = h, ctx, (cloud, list(targets), comm)
+
+    def close(self):
+        if self.h:
+            lib().gsb_joint_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def step(self, steps: int = 1):
+        _check(lib().gsb_joint_step(self.ctx.h, self.h, steps))
+
+    def read(self) -> dict:
+        poses = np.zeros((self.n_views, 12))
+        done = C.c_int64()
+        tt, tl = np.zeros(max(self.cfg.iterations, 1)), np.zeros(max(self.cfg.iterations, 1))
+        _check(lib().gsb_joint_read(self.h, _p(poses), C.byref(done), _p(tt), _p(tl)))
+        return dict(poses=poses, steps=done.value, trace_total=tt[:done.value], trace_l1=tl[:done.value])
+
+
+def perturb_pose_tangent(pose12, sigma, state: "PoseRng"):
+    p = np.ascontiguousarray(pose12, np.float64).reshape(12)
+    out = np.zeros(12)
+    _check(lib().gsb_perturb_pose_tangent(_p(p), sigma, C.byref(state.state), _p(out)))
+    return out
 
 
 def synth_poses(seed: int, n: int, sh_degree: int, kind: int, cameras: int, orbit_radius=2.5,
