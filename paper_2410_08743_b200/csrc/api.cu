@@ -22,6 +22,8 @@ namespace gsb {
 
 // kernels (k_*.cu)
 int launch_preprocess(cudaStream_t st, const gsb_cloud* cloud, const CamDev* cam, const RasterDev& rc, gsb_frame* f);
+int launch_preprocess_multi(cudaStream_t st, const gsb_cloud* cloud, const RasterDev& rc, const CamDev* const* cams,
+                            gsb_frame* const* frames, int nviews);
 int scan_exclusive(cudaStream_t st, const uint32_t* in, int64_t cap, const uint32_t* n_dev, bool flag, uint32_t* out,
                    uint32_t* scratch, uint32_t* total, int64_t* launches);
 size_t scan_words(int64_t n);
@@ -425,18 +427,27 @@ static int rank_order_async(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, 
 // The forward pass as a fixed launch sequence (no host synchronisation; live
 // counts V -> counters[0], K -> counters[1] stay on the device, counters[2]
 // flags a tile too large for tile-local binning). Camera in f->cam.
+static int render_post(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, const RasterDev& rc);
+
 static int render_async(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, const RasterDev& rc) {
+  cudaStream_t st = ctx->stream;
+  const int64_t n = cloud->n;
+  {
+    StageScope sc(ctx, kStPreprocess);
+    GSB_CUDA(cudaMemsetAsync(f->counters.p, 0, 4 * sizeof(uint32_t), st));
+    if (int r = launch_preprocess(st, cloud, f->cam.as<CamDev>(), rc, f)) return r;
+    ctx->launches += n > 0 ? 1 : 0;
+  }
+  return render_post(ctx, cloud, f, rc);
+}
+
+// Everything of the forward pass after K1 (binning + compositing).
+static int render_post(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, const RasterDev& rc) {
   cudaStream_t st = ctx->stream;
   const int64_t n = cloud->n;
   const int n_tiles = f->tiles_x * f->tiles_y;
   uint32_t* counters = f->counters.as<uint32_t>();
   const bool tile_local = f->binning == kBinTileLocal;
-  {
-    StageScope sc(ctx, kStPreprocess);
-    GSB_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(uint32_t), st));
-    if (int r = launch_preprocess(st, cloud, f->cam.as<CamDev>(), rc, f)) return r;
-    ctx->launches += n > 0 ? 1 : 0;
-  }
   {
     StageScope sc(ctx, kStSort);
     if (tile_local) {
@@ -1325,16 +1336,23 @@ struct gsb_pose_batch {
 
 namespace gsb {
 
-static int session_launch_iteration(gsb_ctx* ctx, gsb_session* s, gsb_frame* f) {
+// One pose_descent iteration of the session on forward state f. pre_done:
+// K1 already ran for this iteration (a pose batch's shared multi-view launch,
+// which also copied the camera into f).
+static int session_launch_iteration(gsb_ctx* ctx, gsb_session* s, gsb_frame* f, bool pre_done = false) {
   const gsb_pose_config& cfg = s->cfg;
   const RasterDev rc = make_rasterdev(&cfg.raster);
   double* tp = s->trace.as<double>();
   double* tl = tp + 12 * (size_t)cfg.budget;
-  {
-    StageScope sc(ctx, kStOther);
-    GSB_CUDA(cudaMemcpyAsync(f->cam.p, s->camdev.p, sizeof(CamDev), cudaMemcpyDeviceToDevice, ctx->stream));
+  if (pre_done) {
+    if (int r = render_post(ctx, s->cloud, f, rc)) return r;
+  } else {
+    {
+      StageScope sc(ctx, kStOther);
+      GSB_CUDA(cudaMemcpyAsync(f->cam.p, s->camdev.p, sizeof(CamDev), cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    if (int r = render_async(ctx, s->cloud, f, rc)) return r;
   }
-  if (int r = render_async(ctx, s->cloud, f, rc)) return r;
   if (int r = loss_device(ctx, f, s->target->planes.as<float>(), cfg.beta, true)) return r;
   if (int r = backward_device(ctx, s->cloud, f, false, nullptr)) return r;
   StageScope sc(ctx, kStOptim);
@@ -1646,12 +1664,38 @@ static int batch_capture(gsb_ctx* ctx, gsb_pose_batch* b) {
   ctx->profiling = false;
   GSB_CUDA(cudaStreamBeginCapture(main, cudaStreamCaptureModeThreadLocal));
   int r = GSB_OK;
-  cudaError_t e = cudaEventRecord(b->fork, main);
+  cudaError_t e = cudaSuccess;
+  // K1 for every session of one cloud in one launch (the cloud is read once);
+  // sessions on other clouds run their own K1 inside their branch.
+  std::vector<char> shared(n, 0);
+  {
+    std::vector<const CamDev*> cams;
+    std::vector<gsb_frame*> fr;
+    const gsb_cloud* c0 = b->sessions[0]->cloud;
+    bool same_cfg = true;
+    for (size_t i = 0; i < n; ++i)
+      same_cfg = same_cfg && std::memcmp(&b->sessions[i]->cfg.raster, &b->sessions[0]->cfg.raster,
+                                         sizeof(gsb_raster_config)) == 0;
+    for (size_t i = 0; i < n && same_cfg; ++i)
+      if (b->sessions[i]->cloud == c0) {
+        shared[i] = 1;
+        cams.push_back(b->sessions[i]->camdev.as<CamDev>());
+        fr.push_back(frames[i]);
+        e = cudaMemsetAsync(frames[i]->counters.p, 0, 4 * sizeof(uint32_t), main);
+        if (e != cudaSuccess) break;
+      }
+    if (e == cudaSuccess && !fr.empty()) {
+      r = launch_preprocess_multi(main, c0, make_rasterdev(&b->sessions[0]->cfg.raster), cams.data(), fr.data(),
+                                  (int)fr.size());
+      ctx->launches += (int64_t)((fr.size() + 15) / 16);
+    }
+  }
+  if (!r && e == cudaSuccess) e = cudaEventRecord(b->fork, main);
   for (size_t i = 0; i < n && !r && e == cudaSuccess; ++i) {
     e = cudaStreamWaitEvent(b->streams[i], b->fork, 0);
     if (e != cudaSuccess) break;
     ctx->stream = b->streams[i];
-    r = session_launch_iteration(ctx, b->sessions[i], frames[i]);
+    r = session_launch_iteration(ctx, b->sessions[i], frames[i], shared[i] != 0);
     ctx->stream = main;
     if (!r) e = cudaEventRecord(b->joins[i], b->streams[i]);
     if (!r && e == cudaSuccess) e = cudaStreamWaitEvent(main, b->joins[i], 0);

@@ -126,186 +126,262 @@ __device__ __forceinline__ void sh_colour(const float* __restrict__ P, int64_t n
 // per-thread reads below then come from shared memory (stride kPreBlock).
 constexpr int kPreBlock = 256;
 
+// Per-view outputs of K1 (one forward state).
+struct PreOut {
+  const CamDev* cam_src;  // camera of this iteration (device resident)
+  CamDev* cam_dst;        // copied into the forward state by block 0 (multi-view launch only)
+  SplatRec* rec_g;
+  uint2* rect_g;
+  uint32_t* cnt_g;
+  double* depth_g;
+  double* radius_g;
+  int32_t* rank_of_g;
+  float* colj;
+  uint32_t* counters;
+  SplatAux* aux_g;
+  uint32_t* off_g;
+  int64_t n_pad_out;  // plane stride of colj
+  int32_t tile_local;
+  int32_t pad;
+};
+constexpr int kMaxPreViews = 16;
+struct PreViews {
+  PreOut v[kMaxPreViews];
+};
+
+// View-independent per-Gaussian geometry: mean, the 3D covariance
+// R(q) diag(s)^2 R(q)^T (scene.cpp:90-94, symmetric: 6 entries) and the
+// opacity sigmoid — evaluated once and reused by every view of a launch.
+struct GaussGeom {
+  double mx, my, mz;
+  double S00, S01, S02, S11, S12, S22;
+  double op;
+};
+
+__device__ __forceinline__ GaussGeom gauss_geom(const float* P, int64_t n_pad) {
+  GaussGeom g;
+  g.mx = P[kMeanX * n_pad];
+  g.my = P[kMeanY * n_pad];
+  g.mz = P[kMeanZ * n_pad];
+  const double qw = P[kQuatW * n_pad], qx = P[kQuatX * n_pad], qy = P[kQuatY * n_pad], qz = P[kQuatZ * n_pad];
+  const double qn = __dsqrt_rn(a_(a_(a_(m_(qw, qw), m_(qx, qx)), m_(qy, qy)), m_(qz, qz)));
+  const double w = d_(qw, qn), x = d_(qx, qn), y = d_(qy, qn), z = d_(qz, qn);
+  double Rg[9];
+  Rg[0] = s_(1.0, m_(2.0, a_(m_(y, y), m_(z, z))));
+  Rg[1] = m_(2.0, s_(m_(x, y), m_(w, z)));
+  Rg[2] = m_(2.0, a_(m_(x, z), m_(w, y)));
+  Rg[3] = m_(2.0, a_(m_(x, y), m_(w, z)));
+  Rg[4] = s_(1.0, m_(2.0, a_(m_(x, x), m_(z, z))));
+  Rg[5] = m_(2.0, s_(m_(y, z), m_(w, x)));
+  Rg[6] = m_(2.0, s_(m_(x, z), m_(w, y)));
+  Rg[7] = m_(2.0, a_(m_(y, z), m_(w, x)));
+  Rg[8] = s_(1.0, m_(2.0, a_(m_(x, x), m_(y, y))));
+  const double sx = exp((double)P[kScaleX * n_pad]), sy = exp((double)P[kScaleY * n_pad]),
+               sz = exp((double)P[kScaleZ * n_pad]);
+  double M[9];
+  for (int r = 0; r < 3; ++r) {
+    M[r * 3 + 0] = m_(Rg[r * 3 + 0], sx);
+    M[r * 3 + 1] = m_(Rg[r * 3 + 1], sy);
+    M[r * 3 + 2] = m_(Rg[r * 3 + 2], sz);
+  }
+  // S[r][c] = <M_r, M_c>; exactly symmetric (the products commute)
+  g.S00 = dot3(M[0], M[1], M[2], M[0], M[1], M[2]);
+  g.S01 = dot3(M[0], M[1], M[2], M[3], M[4], M[5]);
+  g.S02 = dot3(M[0], M[1], M[2], M[6], M[7], M[8]);
+  g.S11 = dot3(M[3], M[4], M[5], M[3], M[4], M[5]);
+  g.S12 = dot3(M[3], M[4], M[5], M[6], M[7], M[8]);
+  g.S22 = dot3(M[6], M[7], M[8], M[6], M[7], M[8]);
+  g.op = d_(1.0, a_(1.0, exp(-(double)P[kOpacity * n_pad])));
+  return g;
+}
+
+// One Gaussian seen from one camera: rasterizer.cpp:95-125 + 138-146.
+// Returns the packed tile count | clamp bits (0 = culled) and the tile rect.
 template <int DEG, bool kQuirk>
-__global__ void __launch_bounds__(kPreBlock) preprocess_kernel(
-    const float* __restrict__ params, int64_t n, int64_t n_pad_g, int sh_cap, int sh_active,
-    const CamDev* __restrict__ cam_p, RasterDev rc, SplatRec* __restrict__ rec_g, uint2* __restrict__ rect_g,
-    uint32_t* __restrict__ cnt_g, double* __restrict__ depth_g, double* __restrict__ radius_g,
-    int32_t* __restrict__ rank_of_g, float* __restrict__ colj, uint32_t* __restrict__ counters,
-    bool tile_local, SplatAux* __restrict__ aux_g, uint32_t* __restrict__ off_g) {
+__device__ __forceinline__ uint32_t project_one(const float* P, int64_t n_pad, int sh_cap, const GaussGeom& g,
+                                                const CamDev& cam, const RasterDev& rc, int64_t i,
+                                                const PreOut& o, uint32_t* rect_x, uint32_t* rect_y) {
+  // Se3Pose::act: rotation * p + translation (lie.hpp:38)
+  const double cx = a_(dot3(cam.R[0], cam.R[1], cam.R[2], g.mx, g.my, g.mz), cam.t[0]);
+  const double cy = a_(dot3(cam.R[3], cam.R[4], cam.R[5], g.mx, g.my, g.mz), cam.t[1]);
+  const double cz = a_(dot3(cam.R[6], cam.R[7], cam.R[8], g.mx, g.my, g.mz), cam.t[2]);
+  if (!(cz > rc.z_near)) return 0u;
+  // project (rasterizer.cpp:185-190)
+  const double u = a_(d_(m_(cam.fx, cx), cz), cam.cx);
+  const double v = a_(d_(m_(cam.fy, cy), cz), cam.cy);
+  if (!(isfinite(u) && isfinite(v))) return 0u;
+  const double S[9] = {g.S00, g.S01, g.S02, g.S01, g.S11, g.S12, g.S02, g.S12, g.S22};
+  // projection_jacobian (rasterizer.cpp:31-39)
+  const double iz = d_(1.0, cz);
+  const double iz2 = m_(iz, iz);
+  const double J00 = m_(cam.fx, iz), J02 = m_(m_(-cam.fx, cx), iz2);
+  const double J11 = m_(cam.fy, iz), J12 = m_(m_(-cam.fy, cy), iz2);
+  // m = J R (2x3); row0 = J00*R0 + 0*R1 + J02*R2
+  double m[6];
+  for (int c = 0; c < 3; ++c) {
+    m[c] = a_(a_(m_(J00, cam.R[c]), m_(0.0, cam.R[3 + c])), m_(J02, cam.R[6 + c]));
+    m[3 + c] = a_(a_(m_(0.0, cam.R[c]), m_(J11, cam.R[3 + c])), m_(J12, cam.R[6 + c]));
+  }
+  double ms[6];
+  for (int r = 0; r < 2; ++r)
+    for (int c = 0; c < 3; ++c) ms[r * 3 + c] = dot3(m[r * 3], m[r * 3 + 1], m[r * 3 + 2], S[c], S[3 + c], S[6 + c]);
+  double cov[4];
+  for (int r = 0; r < 2; ++r)
+    for (int c = 0; c < 2; ++c) cov[r * 2 + c] = dot3(ms[r * 3], ms[r * 3 + 1], ms[r * 3 + 2], m[c * 3], m[c * 3 + 1], m[c * 3 + 2]);
+  cov[0] = a_(cov[0], rc.dilation);
+  cov[3] = a_(cov[3], rc.dilation);
+  // max_eigenvalue_2x2 + radius
+  const double mid = m_(0.5, a_(cov[0], cov[3]));
+  const double diff = m_(0.5, s_(cov[0], cov[3]));
+  const double lmax = a_(mid, __dsqrt_rn(a_(m_(diff, diff), m_(cov[1], cov[2]))));
+  const double radius = m_(rc.cutoff_sigma, __dsqrt_rn(lmax));
+  if (!(radius > 0.0 && isfinite(radius) && !(a_(u, radius) < 0.0) && !(s_(u, radius) > cam.width - 1) &&
+        !(a_(v, radius) < 0.0) && !(s_(v, radius) > cam.height - 1)))
+    return 0u;
+  // invert_spd2
+  const double det = s_(m_(cov[0], cov[3]), m_(cov[1], cov[2]));
+  const double ca = d_(cov[3], det), cb = d_(-cov[1], det), cc2 = d_(-cov[2], det), cd = d_(cov[0], det);
+  // colour: sh_eval at dir = normalize(mean - center)
+  double dx = s_(g.mx, cam.center[0]), dy = s_(g.my, cam.center[1]), dz = s_(g.mz, cam.center[2]);
+  const double dn = __dsqrt_rn(a_(a_(m_(dx, dx), m_(dy, dy)), m_(dz, dz)));
+  dx = d_(dx, dn);
+  dy = d_(dy, dn);
+  dz = d_(dz, dn);
+  float col[3], G[9];
+  uint32_t clamp = 0;
+  sh_colour<DEG, kQuirk>(P, n_pad, sh_cap, (float)dx, (float)dy, (float)dz, col, &clamp, G);
+  for (int k = 0; k < 9; ++k) o.colj[(int64_t)k * o.n_pad_out + i] = G[k];
+  // tile span (rasterizer.cpp:138-146)
+  const double tile = (double)kTile;
+  const int tx0 = clamp_tile(floor(d_(s_(u, radius), tile)), cam.tiles_x);
+  const int tx1 = clamp_tile(floor(d_(a_(u, radius), tile)), cam.tiles_x);
+  const int ty0 = clamp_tile(floor(d_(s_(v, radius), tile)), cam.tiles_y);
+  const int ty1 = clamp_tile(floor(d_(a_(v, radius), tile)), cam.tiles_y);
+  SplatRec rec;
+  rec.mu_x = u;
+  rec.mu_y = v;
+  rec.conic_a = (float)ca;
+  rec.conic_b = (float)(0.5 * (cb + cc2));
+  rec.conic_c = (float)cd;
+  rec.opacity = (float)g.op;
+  rec.col_r = col[0];
+  rec.col_g = col[1];
+  rec.col_b = col[2];
+  rec.clamp_bits = clamp;
+  o.rec_g[i] = rec;
+  *rect_x = (uint32_t)tx0 | ((uint32_t)tx1 << 16);
+  *rect_y = (uint32_t)ty0 | ((uint32_t)ty1 << 16);
+  o.rect_g[i] = make_uint2(*rect_x, *rect_y);
+  o.depth_g[i] = cz;
+  o.radius_g[i] = radius;
+  return ((uint32_t)(tx1 - tx0 + 1) * (uint32_t)(ty1 - ty0 + 1)) | (clamp << kClampShift);
+}
+
+// Tile-local binning (k_bin.cu): reserve the splat's entry slots with one
+// atomic per warp (slot order is free — every consumer indexes them by
+// (gid, tile) — so the result stays deterministic) and count V.
+__device__ __forceinline__ void reserve_slots(const PreOut& o, int64_t i, uint32_t cnt, uint32_t rect_x,
+                                              uint32_t rect_y) {
+  const uint32_t c = cnt & kCntMask, lane = threadIdx.x & 31u;
+  uint32_t x = c;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
+    if (lane >= (uint32_t)off) x += y;
+  }
+  const uint32_t tot = __shfl_sync(0xffffffffu, x, 31);
+  const uint32_t vis = __popc(__ballot_sync(0xffffffffu, c > 0u));
+  uint32_t base = 0;
+  if (lane == 0 && tot) {
+    base = atomicAdd(o.counters + 1, tot);
+    atomicAdd(o.counters + 0, vis);
+  }
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (c) {
+    const uint32_t off = base + x - c;
+    const uint32_t tx0 = rect_x & 0xffffu, tx1 = rect_x >> 16, ty0 = rect_y & 0xffffu, ty1 = rect_y >> 16;
+    SplatAux a;
+    a.off = off;
+    a.tx0_ty0 = tx0 | (ty0 << 16);
+    a.nx_ny = (tx1 - tx0 + 1u) | ((ty1 - ty0 + 1u) << 16);
+    a.gid = (int32_t)i;
+    o.aux_g[i] = a;
+    o.off_g[i] = off;
+  }
+}
+
+// K1 over `nviews` cameras at once: the CTA's 256-Gaussian segment of every
+// parameter plane is staged into shared memory with one TMA bulk copy per
+// plane (issued by one thread, completing on an mbarrier), the
+// view-independent geometry is evaluated once, and each view's projection,
+// colour and tile rect follow from the same staged parameters — the cloud is
+// read from HBM once per launch instead of once per view.
+template <int DEG, bool kQuirk>
+__global__ void __launch_bounds__(kPreBlock) preprocess_kernel(const float* __restrict__ params, int64_t n,
+                                                               int64_t n_pad_g, int sh_cap, RasterDev rc,
+                                                               int nviews, const __grid_constant__ PreViews views) {
   extern __shared__ __align__(128) float s_par[];  // [planes][kPreBlock]
-  __shared__ CamDev cam;
+  __shared__ CamDev s_cam[kMaxPreViews];
   __shared__ __align__(8) uint64_t bar;
   const int nplanes = kShBase + 3 * (sh_cap + 1) * (sh_cap + 1);
   const int64_t i0 = (int64_t)blockIdx.x * kPreBlock;
   if (threadIdx.x == 0) {
-    cam = *cam_p;
     mbar_init(&bar, 1);
     const int64_t cnt_here = n - i0 < kPreBlock ? n - i0 : kPreBlock;
     const uint32_t bytes = (uint32_t)(((cnt_here * 4) + 15) & ~(int64_t)15);  // n_pad covers the round-up
     mbar_arrive_expect_tx(&bar, bytes * (uint32_t)nplanes);
     for (int p = 0; p < nplanes; ++p) tma_load_1d(s_par + p * kPreBlock, params + p * n_pad_g + i0, bytes, &bar);
   }
+  for (int v = threadIdx.x; v < nviews; v += kPreBlock) {
+    s_cam[v] = *views.v[v].cam_src;
+    if (blockIdx.x == 0 && views.v[v].cam_dst) *views.v[v].cam_dst = s_cam[v];
+  }
   __syncthreads();
   mbar_wait(&bar, 0);
   const int64_t i = i0 + threadIdx.x;
-  uint32_t cnt = 0;
-  uint32_t rect_x = 0, rect_y = 0;  // tx0 | tx1 << 16, ty0 | ty1 << 16
-  if (i < n) {
-    rank_of_g[i] = -1;
-    const float* P = s_par + threadIdx.x;
-    constexpr int64_t n_pad = kPreBlock;  // plane stride of the staged copy
-    const double mx = P[kMeanX * n_pad], my = P[kMeanY * n_pad], mz = P[kMeanZ * n_pad];
-    // Se3Pose::act: rotation * p + translation (lie.hpp:38)
-    const double cx = a_(dot3(cam.R[0], cam.R[1], cam.R[2], mx, my, mz), cam.t[0]);
-    const double cy = a_(dot3(cam.R[3], cam.R[4], cam.R[5], mx, my, mz), cam.t[1]);
-    const double cz = a_(dot3(cam.R[6], cam.R[7], cam.R[8], mx, my, mz), cam.t[2]);
-    if (cz > rc.z_near) {
-      // project (rasterizer.cpp:185-190)
-      const double u = a_(d_(m_(cam.fx, cx), cz), cam.cx);
-      const double v = a_(d_(m_(cam.fy, cy), cz), cam.cy);
-      if (isfinite(u) && isfinite(v)) {
-        // covariance3d: R(q) diag(s) (R(q) diag(s))^T
-        const double qw = P[kQuatW * n_pad], qx = P[kQuatX * n_pad], qy = P[kQuatY * n_pad], qz = P[kQuatZ * n_pad];
-        const double qn = __dsqrt_rn(a_(a_(a_(m_(qw, qw), m_(qx, qx)), m_(qy, qy)), m_(qz, qz)));
-        const double w = d_(qw, qn), x = d_(qx, qn), y = d_(qy, qn), z = d_(qz, qn);
-        double Rg[9];
-        Rg[0] = s_(1.0, m_(2.0, a_(m_(y, y), m_(z, z))));
-        Rg[1] = m_(2.0, s_(m_(x, y), m_(w, z)));
-        Rg[2] = m_(2.0, a_(m_(x, z), m_(w, y)));
-        Rg[3] = m_(2.0, a_(m_(x, y), m_(w, z)));
-        Rg[4] = s_(1.0, m_(2.0, a_(m_(x, x), m_(z, z))));
-        Rg[5] = m_(2.0, s_(m_(y, z), m_(w, x)));
-        Rg[6] = m_(2.0, s_(m_(x, z), m_(w, y)));
-        Rg[7] = m_(2.0, a_(m_(y, z), m_(w, x)));
-        Rg[8] = s_(1.0, m_(2.0, a_(m_(x, x), m_(y, y))));
-        const double sx = exp((double)P[kScaleX * n_pad]), sy = exp((double)P[kScaleY * n_pad]),
-                     sz = exp((double)P[kScaleZ * n_pad]);
-        double M[9];
-        for (int r = 0; r < 3; ++r) {
-          M[r * 3 + 0] = m_(Rg[r * 3 + 0], sx);
-          M[r * 3 + 1] = m_(Rg[r * 3 + 1], sy);
-          M[r * 3 + 2] = m_(Rg[r * 3 + 2], sz);
-        }
-        double S[9];
-        for (int r = 0; r < 3; ++r)
-          for (int c = 0; c < 3; ++c) S[r * 3 + c] = dot3(M[r * 3], M[r * 3 + 1], M[r * 3 + 2], M[c * 3], M[c * 3 + 1], M[c * 3 + 2]);
-        // projection_jacobian (rasterizer.cpp:31-39)
-        const double iz = d_(1.0, cz);
-        const double iz2 = m_(iz, iz);
-        const double J00 = m_(cam.fx, iz), J02 = m_(m_(-cam.fx, cx), iz2);
-        const double J11 = m_(cam.fy, iz), J12 = m_(m_(-cam.fy, cy), iz2);
-        // m = J R (2x3); row0 = J00*R0 + 0*R1 + J02*R2
-        double m[6];
-        for (int c = 0; c < 3; ++c) {
-          m[c] = a_(a_(m_(J00, cam.R[c]), m_(0.0, cam.R[3 + c])), m_(J02, cam.R[6 + c]));
-          m[3 + c] = a_(a_(m_(0.0, cam.R[c]), m_(J11, cam.R[3 + c])), m_(J12, cam.R[6 + c]));
-        }
-        double ms[6];
-        for (int r = 0; r < 2; ++r)
-          for (int c = 0; c < 3; ++c) ms[r * 3 + c] = dot3(m[r * 3], m[r * 3 + 1], m[r * 3 + 2], S[c], S[3 + c], S[6 + c]);
-        double cov[4];
-        for (int r = 0; r < 2; ++r)
-          for (int c = 0; c < 2; ++c) cov[r * 2 + c] = dot3(ms[r * 3], ms[r * 3 + 1], ms[r * 3 + 2], m[c * 3], m[c * 3 + 1], m[c * 3 + 2]);
-        cov[0] = a_(cov[0], rc.dilation);
-        cov[3] = a_(cov[3], rc.dilation);
-        // max_eigenvalue_2x2 + radius
-        const double mid = m_(0.5, a_(cov[0], cov[3]));
-        const double diff = m_(0.5, s_(cov[0], cov[3]));
-        const double lmax = a_(mid, __dsqrt_rn(a_(m_(diff, diff), m_(cov[1], cov[2]))));
-        const double radius = m_(rc.cutoff_sigma, __dsqrt_rn(lmax));
-        if (radius > 0.0 && isfinite(radius) && !(a_(u, radius) < 0.0) && !(s_(u, radius) > cam.width - 1) &&
-            !(a_(v, radius) < 0.0) && !(s_(v, radius) > cam.height - 1)) {
-          // invert_spd2
-          const double det = s_(m_(cov[0], cov[3]), m_(cov[1], cov[2]));
-          const double ca = d_(cov[3], det), cb = d_(-cov[1], det), cc2 = d_(-cov[2], det), cd = d_(cov[0], det);
-          // colour: sh_eval at dir = normalize(mean - center)
-          double dx = s_(mx, cam.center[0]), dy = s_(my, cam.center[1]), dz = s_(mz, cam.center[2]);
-          const double dn = __dsqrt_rn(a_(a_(m_(dx, dx), m_(dy, dy)), m_(dz, dz)));
-          dx = d_(dx, dn);
-          dy = d_(dy, dn);
-          dz = d_(dz, dn);
-          float col[3], G[9];
-          uint32_t clamp = 0;
-          sh_colour<DEG, kQuirk>(P, n_pad, sh_cap, (float)dx, (float)dy, (float)dz, col, &clamp, G);
-          for (int k = 0; k < 9; ++k) colj[(int64_t)k * n_pad_g + i] = G[k];
-          const double op = d_(1.0, a_(1.0, exp(-(double)P[kOpacity * n_pad])));
-          // tile span (rasterizer.cpp:138-146)
-          const double tile = (double)kTile;
-          const int tx0 = clamp_tile(floor(d_(s_(u, radius), tile)), cam.tiles_x);
-          const int tx1 = clamp_tile(floor(d_(a_(u, radius), tile)), cam.tiles_x);
-          const int ty0 = clamp_tile(floor(d_(s_(v, radius), tile)), cam.tiles_y);
-          const int ty1 = clamp_tile(floor(d_(a_(v, radius), tile)), cam.tiles_y);
-          cnt = ((uint32_t)(tx1 - tx0 + 1) * (uint32_t)(ty1 - ty0 + 1)) | (clamp << kClampShift);
-          SplatRec rec;
-          rec.mu_x = u;
-          rec.mu_y = v;
-          rec.conic_a = (float)ca;
-          rec.conic_b = (float)(0.5 * (cb + cc2));
-          rec.conic_c = (float)cd;
-          rec.opacity = (float)op;
-          rec.col_r = col[0];
-          rec.col_g = col[1];
-          rec.col_b = col[2];
-          rec.clamp_bits = clamp;
-          rec_g[i] = rec;
-          rect_x = (uint32_t)tx0 | ((uint32_t)tx1 << 16);
-          rect_y = (uint32_t)ty0 | ((uint32_t)ty1 << 16);
-          rect_g[i] = make_uint2(rect_x, rect_y);
-          depth_g[i] = cz;
-          radius_g[i] = radius;
-        }
-      }
+  const float* P = s_par + threadIdx.x;
+  constexpr int64_t n_pad = kPreBlock;  // plane stride of the staged copy
+  GaussGeom g{};
+  if (i < n) g = gauss_geom(P, n_pad);
+  for (int v = 0; v < nviews; ++v) {
+    const PreOut& o = views.v[v];
+    uint32_t cnt = 0, rect_x = 0, rect_y = 0;
+    if (i < n) {
+      o.rank_of_g[i] = -1;
+      cnt = project_one<DEG, kQuirk>(P, n_pad, sh_cap, g, s_cam[v], rc, i, o, &rect_x, &rect_y);
+      o.cnt_g[i] = cnt;
     }
-    cnt_g[i] = cnt;
-  }
-  if (tile_local) {
-    // Tile-local binning (k_bin.cu): reserve this splat's entry slots with one
-    // atomic per warp (slot order is free — every consumer indexes them by
-    // (gid, tile) — so the result stays deterministic) and count V.
-    const uint32_t c = cnt & kCntMask, lane = threadIdx.x & 31u;
-    uint32_t x = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= (uint32_t)o) x += y;
-    }
-    const uint32_t tot = __shfl_sync(0xffffffffu, x, 31);
-    const uint32_t vis = __popc(__ballot_sync(0xffffffffu, c > 0u));
-    uint32_t base = 0;
-    if (lane == 0 && tot) {
-      base = atomicAdd(counters + 1, tot);
-      atomicAdd(counters + 0, vis);
-    }
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (c) {
-      const uint32_t off = base + x - c;
-      const uint32_t tx0 = rect_x & 0xffffu, tx1 = rect_x >> 16, ty0 = rect_y & 0xffffu, ty1 = rect_y >> 16;
-      SplatAux a;
-      a.off = off;
-      a.tx0_ty0 = tx0 | (ty0 << 16);
-      a.nx_ny = (tx1 - tx0 + 1u) | ((ty1 - ty0 + 1u) << 16);
-      a.gid = (int32_t)i;
-      aux_g[i] = a;
-      off_g[i] = off;
-    }
+    if (o.tile_local) reserve_slots(o, i, cnt, rect_x, rect_y);
   }
 }
 
-int launch_preprocess(cudaStream_t st, const gsb_cloud* cloud, const CamDev* cam, const RasterDev& rc,
-                      gsb_frame* f) {
+static PreOut pre_out(const CamDev* cam_src, CamDev* cam_dst, gsb_frame* f, int64_t n_pad) {
+  PreOut o{};
+  o.cam_src = cam_src;
+  o.cam_dst = cam_dst;
+  o.rec_g = f->rec_g.as<SplatRec>();
+  o.rect_g = f->rect_g.as<uint2>();
+  o.cnt_g = f->cnt_g.as<uint32_t>();
+  o.depth_g = f->depth_g.as<double>();
+  o.radius_g = f->radius_g.as<double>();
+  o.rank_of_g = f->rank_of_g.as<int32_t>();
+  o.colj = f->colj.as<float>();
+  o.counters = f->counters.as<uint32_t>();
+  o.aux_g = f->aux_g.as<SplatAux>();
+  o.off_g = f->off_g.as<uint32_t>();
+  o.n_pad_out = n_pad;
+  o.tile_local = f->binning == kBinTileLocal ? 1 : 0;
+  return o;
+}
+
+static int launch_pre(cudaStream_t st, const gsb_cloud* cloud, const RasterDev& rc, int nviews, const PreViews& pv) {
   const int64_t n = cloud->n;
   const int deg = std::min(cloud->active_sh_degree, cloud->sh_degree);
   const bool quirk = deg < cloud->sh_degree;
-  const bool tile_local = f->binning == kBinTileLocal;
   const size_t smem = sizeof(float) * kPreBlock * num_planes(cloud->sh_degree);
-#define GSB_PRE(D, Q)                                                                                          \
-  preprocess_kernel<D, Q><<<(unsigned)((n + kPreBlock - 1) / kPreBlock), kPreBlock, smem, st>>>(              \
-      cloud->params.as<float>(), n, cloud->n_pad, cloud->sh_degree, cloud->active_sh_degree, cam, rc,          \
-      f->rec_g.as<SplatRec>(), f->rect_g.as<uint2>(), f->cnt_g.as<uint32_t>(), f->depth_g.as<double>(),        \
-      f->radius_g.as<double>(), f->rank_of_g.as<int32_t>(), f->colj.as<float>(),                              \
-      f->counters.as<uint32_t>(), tile_local,    \
-      f->aux_g.as<SplatAux>(), f->off_g.as<uint32_t>())
+#define GSB_PRE(D, Q)                                                                             \
+  preprocess_kernel<D, Q><<<(unsigned)((n + kPreBlock - 1) / kPreBlock), kPreBlock, smem, st>>>( \
+      cloud->params.as<float>(), n, cloud->n_pad, cloud->sh_degree, rc, nviews, pv)
   if (n > 0) {
     switch (deg * 2 + (quirk ? 1 : 0)) {
       case 0: GSB_PRE(0, false); break;
@@ -319,6 +395,27 @@ int launch_preprocess(cudaStream_t st, const gsb_cloud* cloud, const CamDev* cam
   }
 #undef GSB_PRE
   GSB_CHECK_LAUNCH("preprocess_kernel");
+  return GSB_OK;
+}
+
+int launch_preprocess(cudaStream_t st, const gsb_cloud* cloud, const CamDev* cam, const RasterDev& rc,
+                      gsb_frame* f) {
+  PreViews pv{};
+  pv.v[0] = pre_out(cam, nullptr, f, cloud->n_pad);
+  return launch_pre(st, cloud, rc, 1, pv);
+}
+
+// One launch for several forward states of the same cloud (pose batches):
+// cams[k] is view k's camera, copied into frames[k]->cam by the kernel.
+int launch_preprocess_multi(cudaStream_t st, const gsb_cloud* cloud, const RasterDev& rc, const CamDev* const* cams,
+                            gsb_frame* const* frames, int nviews) {
+  for (int v0 = 0; v0 < nviews; v0 += kMaxPreViews) {
+    PreViews pv{};
+    const int nv = std::min(kMaxPreViews, nviews - v0);
+    for (int k = 0; k < nv; ++k)
+      pv.v[k] = pre_out(cams[v0 + k], frames[v0 + k]->cam.as<CamDev>(), frames[v0 + k], cloud->n_pad);
+    if (int r = launch_pre(st, cloud, rc, nv, pv)) return r;
+  }
   return GSB_OK;
 }
 

@@ -9,6 +9,8 @@ own magnitude, so an entry whose gradient is at rounding-noise level (FP32 vs
 FP64) can move by up to lr per step in either direction; those entries are
 why the parameter bound is a quantile rather than a max.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -122,6 +124,9 @@ def test_joint_chunked_steps_and_single_rank_comm(G, ctx):
     assert np.array_equal(a["poses"], b["poses"]) and np.array_equal(a["trace_total"], b["trace_total"])
     for x, y in zip(da, db):
         assert np.array_equal(x, y)
+    # single-host loopback bootstrap: no interface probing on the test box
+    os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
+    os.environ.setdefault("NCCL_IB_DISABLE", "1")
     try:
         uid = G.Comm.unique_id()
     except G.GsbError:
