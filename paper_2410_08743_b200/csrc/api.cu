@@ -51,7 +51,7 @@ int launch_tile_bin(cudaStream_t st, gsb_frame* f, int64_t n, int64_t* launches)
 size_t bin_hist_words(int64_t n, int n_tiles);
 int init_bin_attributes();
 int launch_composite(cudaStream_t st, gsb_frame* f, const RasterDev& rc);
-int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc);
+int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc, bool pose_only);
 int launch_backward_geom(cudaStream_t st, const gsb_cloud* cloud, gsb_frame* f, const RasterDev& rc, bool full,
                          float* grads, int64_t* launches);
 int launch_rgb_loss(cudaStream_t st, const float* ren, const float* tgt, int W, int H, double beta, float* gmaps,
@@ -601,7 +601,7 @@ static int backward_device(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, b
   const RasterDev rc = make_rasterdev(&f->config);
   {
     StageScope sc(ctx, kStBwdRaster);
-    if (int r = launch_backward_raster(ctx->stream, f, rc)) return r;
+    if (int r = launch_backward_raster(ctx->stream, f, rc, !full)) return r;
     ctx->launches += f->tiles_x * f->tiles_y > 0 ? 1 : 0;
   }
   {

@@ -91,14 +91,24 @@ __global__ void __launch_bounds__(kGeomBlock, 2) backward_geom_kernel(
   const uint32_t off = s_off[threadIdx.x];
   if (i < n && cnt > 0u && (int64_t)off + cnt <= k_cap) {
     const uint32_t clamp = craw >> kClampShift;
-    // phase 2: ordered sum of this splat's entry partials (tile order)
+    // phase 2: ordered sum of this splat's entry partials (tile order); the
+    // pose-only backward stores 8 per entry (no opacity), two 16-B loads
     double acc[kPartial];
 #pragma unroll
     for (int c = 0; c < kPartial; ++c) acc[c] = 0.0;
-    const float* pp = partials + (int64_t)off * kPartial;
-    for (uint32_t j = 0; j < cnt; ++j) {
+    if (kFull) {
+      const float* pp = partials + (int64_t)off * kPartial;
+      for (uint32_t j = 0; j < cnt; ++j) {
 #pragma unroll
-      for (int c = 0; c < kPartial; ++c) acc[c] += (double)pp[j * kPartial + c];
+        for (int c = 0; c < kPartial; ++c) acc[c] += (double)pp[j * kPartial + c];
+      }
+    } else {
+      const float4* pp = reinterpret_cast<const float4*>(partials) + (int64_t)off * 2;
+      for (uint32_t j = 0; j < cnt; ++j) {
+        const float4 lo = pp[2 * j], hi = pp[2 * j + 1];
+        acc[0] += (double)lo.x; acc[1] += (double)lo.y; acc[2] += (double)lo.z; acc[3] += (double)lo.w;
+        acc[4] += (double)hi.x; acc[5] += (double)hi.y; acc[6] += (double)hi.z; acc[7] += (double)hi.w;
+      }
     }
     const float* P = s_par + threadIdx.x;
     constexpr int64_t n_pad = kGeomBlock;  // plane stride of the staged copy

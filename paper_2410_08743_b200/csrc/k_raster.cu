@@ -325,6 +325,36 @@ __device__ __forceinline__ int warp_reduce9(const float v[kPartial], float* out)
   return vi;
 }
 
+// Pose-only backward: 8 components (the opacity partial has no consumer),
+// reduce-scatter xor 16 / 8 / 4 (4 + 2 + 1 shuffles) then a plain xor 2 / 1
+// sum: 9 shuffles. Lanes with (lane & 3) == 0 end owning component
+// 4 b4 + 2 b3 + b2 (b_k = bit k of lane).
+__device__ __forceinline__ int warp_reduce8(const float v[8], float* out) {
+  const int lane = threadIdx.x & 31;
+  const bool h1 = lane & 16, h2 = lane & 8, h3 = lane & 4;
+  float w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = h1 ? v[i] : v[4 + i], keep = h1 ? v[4 + i] : v[i];
+    w[i] = keep + __shfl_xor_sync(kFull, send, 16);
+  }
+  float x[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = h2 ? w[i] : w[2 + i], keep = h2 ? w[2 + i] : w[i];
+    x[i] = keep + __shfl_xor_sync(kFull, send, 8);
+  }
+  float z;
+  {
+    const float send = h3 ? x[0] : x[1], keep = h3 ? x[1] : x[0];
+    z = keep + __shfl_xor_sync(kFull, send, 4);
+  }
+  z += __shfl_xor_sync(kFull, z, 2);
+  z += __shfl_xor_sync(kFull, z, 1);
+  *out = z;
+  return (lane & 3) ? -1 : (h1 ? 4 : 0) + (h2 ? 2 : 0) + (h3 ? 1 : 0);
+}
+
 struct PixBwd {
   float dr, dg, db, T, br, bg, bb;
   uint32_t contrib;
@@ -351,9 +381,11 @@ __device__ __forceinline__ void load_pixel_bwd(PixBwd& p, int x, int y, int W, i
   p.bb = bg_b * p.T;
 }
 
-// One (pixel, splat) replay step of phase 1; accumulates into v.
+// One (pixel, splat) replay step of phase 1; accumulates into v (NC = 8:
+// no opacity partial).
+template <int NC>
 __device__ __forceinline__ bool backward_one(PixBwd& p, const float4& ge, const float4& ap, float col_b, float dx,
-                                             float dy, const RasterDev& rc, uint32_t j, float v[kPartial]) {
+                                             float dy, const RasterDev& rc, uint32_t j, float v[NC]) {
   if (j >= p.contrib) return false;
   const float g = splat_power(ge.z, ge.w, ap.x, dx, dy);
   if (g > rc.cutoff2_f) return false;
@@ -369,7 +401,7 @@ __device__ __forceinline__ bool backward_one(PixBwd& p, const float4& ge, const 
   const float dal = p.dr * (ap.z * tb - p.br * inv) + p.dg * (ap.w * tb - p.bg * inv) + p.db * (col_b * tb - p.bb * inv);
   if (araw < rc.alpha_clamp_f) {
     const float cx_ = ge.z * dx + ge.w * dy, cy_ = ge.w * dx + ap.x * dy;
-    v[8] = fmaf(dal, G, v[8]);
+    if (NC > 8) v[NC - 1] = fmaf(dal, G, v[NC - 1]);
     const float dgg = dal * (-0.5f * araw);
     v[0] = fmaf(-2.0f * dgg, cx_, v[0]);
     v[1] = fmaf(-2.0f * dgg, cy_, v[1]);
@@ -384,6 +416,7 @@ __device__ __forceinline__ bool backward_one(PixBwd& p, const float4& ge, const 
   return true;
 }
 
+template <int NC>
 __global__ void __launch_bounds__(kThreads, 8) backward_raster_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ ranks, const SplatRec* __restrict__ rec,
     const SplatAux* __restrict__ aux, const CamDev* __restrict__ cam_p, RasterDev rc, float bg_r, float bg_g,
@@ -394,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 8) backward_raster_kernel(
   __shared__ uint32_t s_slot[kBatch];
   __shared__ uint8_t s_mask[kBatch];
   __shared__ uint8_t s_list[kWarps][kBatch];
-  __shared__ float s_red[kWarps][kBatch][kPartial];  // [warp][entry in batch][component]
+  __shared__ float s_red[kWarps][kBatch][NC];  // [warp][entry in batch][component]
   __shared__ int s_w, s_h, s_tx;
   __shared__ uint32_t s_maxc[kWarps];
   if (threadIdx.x == 0) {
@@ -402,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, 8) backward_raster_kernel(
     s_h = cam_p->height;
     s_tx = cam_p->tiles_x;
   }
-  for (int i = threadIdx.x; i < kWarps * kBatch * kPartial; i += kThreads) (&s_red[0][0][0])[i] = 0.f;
+  for (int i = threadIdx.x; i < kWarps * kBatch * NC; i += kThreads) (&s_red[0][0][0])[i] = 0.f;
   __syncthreads();
   const int W = s_w, H = s_h;
   const int tile = blockIdx.x;
@@ -453,30 +486,30 @@ __global__ void __launch_bounds__(kThreads, 8) backward_raster_kernel(
         const float4 ge = s_geo[k];
         const float4 ap = s_app[k];
         const float cb = s_colb[k];
-        float v[kPartial];
+        float v[NC];
 #pragma unroll
-        for (int c = 0; c < kPartial; ++c) v[c] = 0.f;
+        for (int c = 0; c < NC; ++c) v[c] = 0.f;
         const float dx = px - ge.x, dy = py - ge.y;
-        const bool ha = backward_one(a, ge, ap, cb, dx, dy, rc, j, v);
-        const bool hb = backward_one(b, ge, ap, cb, dx, dy + 1.0f, rc, j, v);
+        const bool ha = backward_one<NC>(a, ge, ap, cb, dx, dy, rc, j, v);
+        const bool hb = backward_one<NC>(b, ge, ap, cb, dx, dy + 1.0f, rc, j, v);
         if (__any_sync(kFull, ha || hb)) {
           float tot;
-          const int vi = warp_reduce9(v, &tot);
+          const int vi = NC == 8 ? warp_reduce8(v, &tot) : warp_reduce9(v, &tot);
           if (vi >= 0) s_red[warp][k][vi] = tot;
         }
       }
     }
     __syncthreads();
     // flush: batch entries x 9 components, summed over warps 0..3 in order
-    for (int idx = threadIdx.x; idx < cnt * kPartial; idx += kThreads) {
-      const int k = idx / kPartial, c = idx - k * kPartial;
+    for (int idx = threadIdx.x; idx < cnt * NC; idx += kThreads) {
+      const int k = idx / NC, c = idx - k * NC;
       float acc = 0.f;
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) {
         acc += s_red[w][k][c];
         s_red[w][k][c] = 0.f;
       }
-      if (s_slot[k] < k_cap) partials[(int64_t)s_slot[k] * kPartial + c] = acc;
+      if (s_slot[k] < k_cap) partials[(int64_t)s_slot[k] * NC + c] = acc;
     }
     __syncthreads();
   }
@@ -494,11 +527,12 @@ int launch_composite(cudaStream_t st, gsb_frame* f, const RasterDev& rc) {
   return GSB_OK;
 }
 
-int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc) {
+// pose_only: 8 partials per entry (no opacity); else the full 9.
+int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc, bool pose_only) {
   const int n_tiles = f->tiles_x * f->tiles_y;
   const int64_t npix = (int64_t)f->width * f->height;
   if (n_tiles > 0)
-    backward_raster_kernel<<<n_tiles, kThreads, 0, st>>>(
+    (pose_only ? backward_raster_kernel<8> : backward_raster_kernel<kPartial>)<<<n_tiles, kThreads, 0, st>>>(
         f->ranges.as<uint2>(), f->list(), f->list_rec(), f->list_aux(),
         f->cam.as<CamDev>(), rc, (float)f->background[0], (float)f->background[1], (float)f->background[2], npix,
         f->d_image.as<float>(), f->final_t.as<float>(), f->pixstate.as<uint32_t>(), f->partials.as<float>(),
