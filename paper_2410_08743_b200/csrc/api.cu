@@ -58,6 +58,7 @@ int launch_rgb_loss(cudaStream_t st, const float* ren, const float* tgt, int W, 
                     double* block_sums, double* out3, float* d_image, int64_t* launches);
 size_t loss_block_count(int W, int H);
 int init_loss_constants();
+int init_loss_attributes();
 int init_preprocess_attributes();
 int launch_pose_iter(cudaStream_t st, void* state, const double* dpose, const double* loss3, double lr_start,
                      double lr_end, double eps, int budget, CamDev* cam, double* trace_pose, double* trace_loss,
@@ -661,6 +662,10 @@ int gsb_ctx_create(int32_t device, gsb_ctx** out) {
   }
   c->timer = new StageTimer();
   if (int r = init_loss_constants()) {
+    gsb_ctx_destroy(c);
+    return r;
+  }
+  if (int r = init_loss_attributes()) {
     gsb_ctx_destroy(c);
     return r;
   }

@@ -10,7 +10,9 @@
 // expressions of the reference are kept so identical images give exactly
 // zero loss and gradient.
 //
-// Two tiled kernels (16x16 outputs + 5 px halo staged in shared memory):
+// Two tiled kernels (32x32 outputs + 5 px halo staged in shared memory,
+// register-blocked separable passes: each thread computes 4 consecutive
+// outputs from 14 inputs held in registers):
 //   loss_maps:  5 forward convolutions -> SSIM map sum, L1 sum, g maps;
 //   loss_grad:  3 back-convolutions + L1 sign term -> d_image.
 // Per-block partial sums are reduced in a fixed order (deterministic).
@@ -18,10 +20,14 @@
 
 namespace gsb {
 
-constexpr int kLT = 16;             // output tile
 constexpr int kHalf = 5;
 constexpr int kWin = 11;
-constexpr int kLI = kLT + 2 * kHalf;  // 26 staged rows/cols
+// Register-blocked tiles: 32x32 outputs per 256-thread CTA, every thread
+// producing R = 4 consecutive outputs per pass (the 14 inputs they share are
+// loaded once into registers), 42x42 staged inputs.
+constexpr int kTW = 32, kTH = 32, kR = 4;
+constexpr int kSW = kTW + 2 * kHalf, kSH = kTH + 2 * kHalf;  // 42 x 42
+constexpr int kThr = 256;
 __constant__ double c_win[kWin];
 
 __device__ __forceinline__ double m_(double a, double b) { return __dmul_rn(a, b); }
@@ -42,65 +48,110 @@ __device__ __forceinline__ double blk_reduce_sum(double v, double* s_tmp) {
   return t;  // valid in thread 0
 }
 
-__global__ void __launch_bounds__(256) loss_maps_kernel(const float* __restrict__ ren, const float* __restrict__ tgt,
-                                                        int W, int H, double scale, float* __restrict__ gmaps,
-                                                        double* __restrict__ block_sums) {
-  __shared__ double sa[kLI][kLI + 1], sb[kLI][kLI + 1];
-  __shared__ double hq[5][kLI][kLT + 1];
-  __shared__ double s_tmp[8];
-  const int64_t P = (int64_t)W * H;
-  const int bx = blockIdx.x * kLT, by = blockIdx.y * kLT;
-  const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
-  const int x = bx + lx, y = by + ly;
-  const bool in_img = x < W && y < H;
-  const bool valid = x >= kHalf && x < W - kHalf && y >= kHalf && y < H - kHalf;
-  double l1 = 0.0, ss = 0.0;
-  for (int c = 0; c < 3; ++c) {
-    const float* A = ren + c * P;
-    const float* B = tgt + c * P;
-    for (int idx = threadIdx.x; idx < kLI * kLI; idx += 256) {
-      const int r = idx / kLI, q = idx % kLI;
-      const int gx = bx - kHalf + q, gy = by - kHalf + r;
-      const bool ok = gx >= 0 && gx < W && gy >= 0 && gy < H;
-      sa[r][q] = ok ? (double)A[(int64_t)gy * W + gx] : 0.0;
-      sb[r][q] = ok ? (double)B[(int64_t)gy * W + gx] : 0.0;
-    }
-    __syncthreads();
-    // horizontal pass over 26 rows x 16 cols
-    for (int idx = threadIdx.x; idx < kLI * kLT; idx += 256) {
-      const int r = idx / kLT, q = idx % kLT;
-      double h0 = 0, h1 = 0, h2 = 0, h3 = 0, h4 = 0;
+// Stages a (kSH x kSW) window of NM FP32 planes starting at (gx0, gy0),
+// zero outside the image (conv_window's zero padding, losses.cpp:37-63).
+// All of a thread's loads are issued before its first shared store, so the
+// ~7 x NM global loads per thread are in flight together.
+template <int NM>
+__device__ __forceinline__ void stage_planes(float (*dst)[kSH][kSW + 1], const float* const* src, int W, int H,
+                                             int gx0, int gy0) {
+  constexpr int kIt = (kSH * kSW + kThr - 1) / kThr;
+  float v[kIt][NM];
 #pragma unroll
-      for (int k = 0; k < kWin; ++k) {
-        const double w = c_win[k];
-        const double a = sa[r][q + k], b = sb[r][q + k];
-        h0 += w * a;
-        h1 += w * b;
-        h2 += w * (a * a);
-        h3 += w * (b * b);
-        h4 += w * (a * b);
+  for (int it = 0; it < kIt; ++it) {
+    const int idx = it * kThr + threadIdx.x;
+    const int r = idx / kSW, q = idx - r * kSW;
+    const int gx = gx0 + q, gy = gy0 + r;
+    const bool ok = idx < kSH * kSW && gx >= 0 && gx < W && gy >= 0 && gy < H;
+    const int64_t p = ok ? (int64_t)gy * W + gx : 0;
+#pragma unroll
+    for (int m = 0; m < NM; ++m) v[it][m] = ok ? __ldg(src[m] + p) : 0.f;
+  }
+#pragma unroll
+  for (int it = 0; it < kIt; ++it) {
+    const int idx = it * kThr + threadIdx.x;
+    if (idx < kSH * kSW) {
+      const int r = idx / kSW, q = idx - r * kSW;
+#pragma unroll
+      for (int m = 0; m < NM; ++m) dst[m][r][q] = v[it][m];
+    }
+  }
+}
+
+// Horizontal pass of the five SSIM statistics (a, b, a^2, b^2, ab) over the
+// staged rows: task = (row, 4-column group); 42 rows x 8 groups = 336 tasks.
+__device__ __forceinline__ void hpass5(const float (*st)[kSH][kSW + 1], double (*hq)[kSH][kTW + 1]) {
+  for (int task = threadIdx.x; task < kSH * (kTW / kR); task += kThr) {
+    const int r = task / (kTW / kR), q0 = (task - r * (kTW / kR)) * kR;
+    double x[kR + kWin - 1], y[kR + kWin - 1];
+#pragma unroll
+    for (int k = 0; k < kR + kWin - 1; ++k) {
+      x[k] = st[0][r][q0 + k];
+      y[k] = st[1][r][q0 + k];
+    }
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+      double acc[kR];
+#pragma unroll
+      for (int j = 0; j < kR; ++j) acc[j] = 0.0;
+#pragma unroll
+      for (int k = 0; k < kR + kWin - 1; ++k) {
+        const double f = m == 0 ? x[k] : m == 1 ? y[k] : m == 2 ? x[k] * x[k] : m == 3 ? y[k] * y[k] : x[k] * y[k];
+#pragma unroll
+        for (int j = 0; j < kR; ++j)
+          if (k - j >= 0 && k - j < kWin) acc[j] = fma(c_win[k - j], f, acc[j]);
       }
-      hq[0][r][q] = h0;
-      hq[1][r][q] = h1;
-      hq[2][r][q] = h2;
-      hq[3][r][q] = h3;
-      hq[4][r][q] = h4;
-    }
-    __syncthreads();
-    if (in_img) {
-      const double a = sa[ly + kHalf][lx + kHalf], b = sb[ly + kHalf][lx + kHalf];
-      l1 += fabs(a - b);
-      if (valid) {
-        double ma = 0, mb = 0, eaa = 0, ebb = 0, eab = 0;
 #pragma unroll
-        for (int k = 0; k < kWin; ++k) {
-          const double w = c_win[k];
-          ma += w * hq[0][ly + k][lx];
-          mb += w * hq[1][ly + k][lx];
-          eaa += w * hq[2][ly + k][lx];
-          ebb += w * hq[3][ly + k][lx];
-          eab += w * hq[4][ly + k][lx];
-        }
+      for (int j = 0; j < kR; ++j) hq[m][r][q0 + j] = acc[j];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThr) loss_maps_kernel(const float* __restrict__ ren, const float* __restrict__ tgt,
+                                                         int W, int H, double scale, float* __restrict__ gmaps,
+                                                         double* __restrict__ block_sums) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float(*st)[kSH][kSW + 1] = reinterpret_cast<float(*)[kSH][kSW + 1]>(smem_raw);
+  double(*hq)[kSH][kTW + 1] =
+      reinterpret_cast<double(*)[kSH][kTW + 1]>(smem_raw + sizeof(float) * 2 * kSH * (kSW + 1) + 8);
+  __shared__ double s_tmp[kThr / 32];
+  const int64_t P = (int64_t)W * H;
+  const int bx = blockIdx.x * kTW, by = blockIdx.y * kTH;
+  // vertical task: column c, rows 4 rg .. 4 rg + 3
+  const int c = threadIdx.x & (kTW - 1), rg = threadIdx.x / kTW;
+  const int x = bx + c;
+  double l1 = 0.0, ss = 0.0;
+  for (int ch = 0; ch < 3; ++ch) {
+    const float* src[2] = {ren + ch * P, tgt + ch * P};
+    stage_planes<2>(st, src, W, H, bx - kHalf, by - kHalf);
+    __syncthreads();
+    hpass5(st, hq);
+    __syncthreads();
+    double mv[5][kR];
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+      double acc[kR];
+#pragma unroll
+      for (int j = 0; j < kR; ++j) acc[j] = 0.0;
+#pragma unroll
+      for (int k = 0; k < kR + kWin - 1; ++k) {
+        const double f = hq[m][rg * kR + k][c];
+#pragma unroll
+        for (int j = 0; j < kR; ++j)
+          if (k - j >= 0 && k - j < kWin) acc[j] = fma(c_win[k - j], f, acc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < kR; ++j) mv[m][j] = acc[j];
+    }
+#pragma unroll
+    for (int j = 0; j < kR; ++j) {
+      const int y = by + rg * kR + j;
+      if (x >= W || y >= H) continue;
+      const double a = st[0][rg * kR + j + kHalf][c + kHalf], b = st[1][rg * kR + j + kHalf][c + kHalf];
+      l1 += fabs(a - b);
+      const int64_t p = (int64_t)y * W + x;
+      if (x >= kHalf && x < W - kHalf && y >= kHalf && y < H - kHalf) {
+        const double ma = mv[0][j], mb = mv[1][j], eaa = mv[2][j], ebb = mv[3][j], eab = mv[4][j];
         // Pointwise SSIM terms with explicitly rounded (unfused) arithmetic in
         // the reference's expression order, so identical inputs cancel exactly
         // (a1 == b1, a2 == b2, s == 1 and a zero gradient; losses.cpp:112-131).
@@ -113,15 +164,13 @@ __global__ void __launch_bounds__(256) loss_maps_kernel(const float* __restrict_
         ss += s;
         const double gmu = d_(m_(scale, a_(m_(m_(2.0, mb), s_(a2, a1)), m_(m_(m_(2.0, ma), s), s_(b1, b2)))), b12);
         const double qv = d_(a1, b12);
-        const int64_t p = (int64_t)y * W + x;
-        gmaps[(3 * c + 0) * P + p] = (float)gmu;
-        gmaps[(3 * c + 1) * P + p] = (float)m_(-m_(scale, qv), d_(a2, b2));
-        gmaps[(3 * c + 2) * P + p] = (float)m_(2.0, m_(scale, qv));
+        gmaps[(3 * ch + 0) * P + p] = (float)gmu;
+        gmaps[(3 * ch + 1) * P + p] = (float)m_(-m_(scale, qv), d_(a2, b2));
+        gmaps[(3 * ch + 2) * P + p] = (float)m_(2.0, m_(scale, qv));
       } else {
-        const int64_t p = (int64_t)y * W + x;
-        gmaps[(3 * c + 0) * P + p] = 0.f;
-        gmaps[(3 * c + 1) * P + p] = 0.f;
-        gmaps[(3 * c + 2) * P + p] = 0.f;
+        gmaps[(3 * ch + 0) * P + p] = 0.f;
+        gmaps[(3 * ch + 1) * P + p] = 0.f;
+        gmaps[(3 * ch + 2) * P + p] = 0.f;
       }
     }
     __syncthreads();
@@ -129,70 +178,81 @@ __global__ void __launch_bounds__(256) loss_maps_kernel(const float* __restrict_
   const double t1 = blk_reduce_sum(l1, s_tmp);
   const double t2 = blk_reduce_sum(ss, s_tmp);
   if (threadIdx.x == 0) {
-    const int b = blockIdx.y * gridDim.x + blockIdx.x;
-    block_sums[2 * b] = t1;
-    block_sums[2 * b + 1] = t2;
+    const int bidx = blockIdx.y * gridDim.x + blockIdx.x;
+    block_sums[2 * bidx] = t1;
+    block_sums[2 * bidx + 1] = t2;
   }
 }
 
-__global__ void __launch_bounds__(256) loss_grad_kernel(const float* __restrict__ ren, const float* __restrict__ tgt,
-                                                        const float* __restrict__ gmaps, int W, int H, double beta,
-                                                        double l1_norm, int has_ssim, float* __restrict__ d_image) {
-  __shared__ float sg[3][kLI][kLI + 1];
-  __shared__ double hq[3][kLI][kLT + 1];
-  const int64_t P = (int64_t)W * H;
-  const int bx = blockIdx.x * kLT, by = blockIdx.y * kLT;
-  const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
-  const int x = bx + lx, y = by + ly;
-  const bool in_img = x < W && y < H;
-  for (int c = 0; c < 3; ++c) {
-    if (has_ssim) {
-      for (int idx = threadIdx.x; idx < kLI * kLI; idx += 256) {
-        const int r = idx / kLI, q = idx % kLI;
-        const int gx = bx - kHalf + q, gy = by - kHalf + r;
-        const bool ok = gx >= 0 && gx < W && gy >= 0 && gy < H;
-        const int64_t p = (int64_t)gy * W + gx;
-        sg[0][r][q] = ok ? gmaps[(3 * c + 0) * P + p] : 0.f;
-        sg[1][r][q] = ok ? gmaps[(3 * c + 1) * P + p] : 0.f;
-        sg[2][r][q] = ok ? gmaps[(3 * c + 2) * P + p] : 0.f;
-      }
-      __syncthreads();
-      for (int idx = threadIdx.x; idx < kLI * kLT; idx += 256) {
-        const int r = idx / kLT, q = idx % kLT;
-        double h0 = 0, h1 = 0, h2 = 0;
+// Horizontal pass of the three gradient maps (back-convolution, losses.cpp:144-151).
+__device__ __forceinline__ void hpass3(const float (*st)[kSH][kSW + 1], double (*hq)[kSH][kTW + 1]) {
+  for (int task = threadIdx.x; task < kSH * (kTW / kR); task += kThr) {
+    const int r = task / (kTW / kR), q0 = (task - r * (kTW / kR)) * kR;
 #pragma unroll
-        for (int k = 0; k < kWin; ++k) {
-          const double w = c_win[k];
-          h0 += w * (double)sg[0][r][q + k];
-          h1 += w * (double)sg[1][r][q + k];
-          h2 += w * (double)sg[2][r][q + k];
-        }
-        hq[0][r][q] = h0;
-        hq[1][r][q] = h1;
-        hq[2][r][q] = h2;
+    for (int m = 0; m < 3; ++m) {
+      double acc[kR];
+#pragma unroll
+      for (int j = 0; j < kR; ++j) acc[j] = 0.0;
+#pragma unroll
+      for (int k = 0; k < kR + kWin - 1; ++k) {
+        const double f = st[m][r][q0 + k];
+#pragma unroll
+        for (int j = 0; j < kR; ++j)
+          if (k - j >= 0 && k - j < kWin) acc[j] = fma(c_win[k - j], f, acc[j]);
       }
-      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < kR; ++j) hq[m][r][q0 + j] = acc[j];
     }
-    if (in_img) {
+  }
+}
+
+__global__ void __launch_bounds__(kThr) loss_grad_kernel(const float* __restrict__ ren, const float* __restrict__ tgt,
+                                                         const float* __restrict__ gmaps, int W, int H, double beta,
+                                                         double l1_norm, int has_ssim, float* __restrict__ d_image) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float(*st)[kSH][kSW + 1] = reinterpret_cast<float(*)[kSH][kSW + 1]>(smem_raw);
+  double(*hq)[kSH][kTW + 1] =
+      reinterpret_cast<double(*)[kSH][kTW + 1]>(smem_raw + sizeof(float) * 3 * kSH * (kSW + 1) + 8);
+  const int64_t P = (int64_t)W * H;
+  const int bx = blockIdx.x * kTW, by = blockIdx.y * kTH;
+  const int c = threadIdx.x & (kTW - 1), rg = threadIdx.x / kTW;
+  const int x = bx + c;
+  for (int ch = 0; ch < 3; ++ch) {
+    double cv[3][kR];
+    if (has_ssim) {
+      const float* src[3] = {gmaps + (3 * ch + 0) * P, gmaps + (3 * ch + 1) * P, gmaps + (3 * ch + 2) * P};
+      stage_planes<3>(st, src, W, H, bx - kHalf, by - kHalf);
+      __syncthreads();
+      hpass3(st, hq);
+      __syncthreads();
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        double acc[kR];
+#pragma unroll
+        for (int j = 0; j < kR; ++j) acc[j] = 0.0;
+#pragma unroll
+        for (int k = 0; k < kR + kWin - 1; ++k) {
+          const double f = hq[m][rg * kR + k][c];
+#pragma unroll
+          for (int j = 0; j < kR; ++j)
+            if (k - j >= 0 && k - j < kWin) acc[j] = fma(c_win[k - j], f, acc[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < kR; ++j) cv[m][j] = acc[j];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kR; ++j) {
+      const int y = by + rg * kR + j;
+      if (x >= W || y >= H) continue;
       const int64_t p = (int64_t)y * W + x;
-      const double a = ren[c * P + p], b = tgt[c * P + p];
+      const double a = ren[ch * P + p], b = tgt[ch * P + p];
       const double diff = a - b;
       const double dl1 = diff == 0.0 ? 0.0 : (diff > 0.0 ? l1_norm : -l1_norm);
-      double dss = 0.0;
-      if (has_ssim) {
-        double cm = 0, ce = 0, cx = 0;
-#pragma unroll
-        for (int k = 0; k < kWin; ++k) {
-          const double w = c_win[k];
-          cm += w * hq[0][ly + k][lx];
-          ce += w * hq[1][ly + k][lx];
-          cx += w * hq[2][ly + k][lx];
-        }
-        dss = a_(a_(cm, m_(m_(2.0, a), ce)), m_(b, cx));
-      }
-      d_image[c * P + p] = (float)s_(m_(1.0 - beta, dl1), m_(beta, dss));
+      const double dss = has_ssim ? a_(a_(cv[0][j], m_(m_(2.0, a), cv[1][j])), m_(b, cv[2][j])) : 0.0;
+      d_image[ch * P + p] = (float)s_(m_(1.0 - beta, dl1), m_(beta, dss));
     }
-    __syncthreads();
+    if (has_ssim) __syncthreads();
   }
 }
 
@@ -236,21 +296,31 @@ int init_loss_constants() {
   return GSB_OK;
 }
 
+constexpr size_t kMapsSmem = sizeof(float) * 2 * kSH * (kSW + 1) + 8 + sizeof(double) * 5 * kSH * (kTW + 1);
+constexpr size_t kGradSmem = sizeof(float) * 3 * kSH * (kSW + 1) + 8 + sizeof(double) * 3 * kSH * (kTW + 1);
+
+int init_loss_attributes() {
+  GSB_CUDA(cudaFuncSetAttribute(loss_maps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMapsSmem));
+  GSB_CUDA(cudaFuncSetAttribute(loss_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGradSmem));
+  return GSB_OK;
+}
+
 int launch_rgb_loss(cudaStream_t st, const float* ren, const float* tgt, int W, int H, double beta, float* gmaps,
                     double* block_sums, double* out3, float* d_image, int64_t* launches) {
   const int64_t cnt_valid = (W > 2 * kHalf && H > 2 * kHalf) ? (int64_t)(W - 2 * kHalf) * (H - 2 * kHalf) : 0;
   const int has_ssim = cnt_valid > 0 ? 1 : 0;
   const double scale = has_ssim ? 1.0 / (3.0 * (double)cnt_valid) : 0.0;
   const double l1_norm = 1.0 / (3.0 * (double)W * (double)H);
-  dim3 grid((W + kLT - 1) / kLT, (H + kLT - 1) / kLT);
-  loss_maps_kernel<<<grid, 256, 0, st>>>(ren, tgt, W, H, scale, gmaps, block_sums);
-  if (d_image) loss_grad_kernel<<<grid, 256, 0, st>>>(ren, tgt, gmaps, W, H, beta, l1_norm, has_ssim, d_image);
+  dim3 grid((W + kTW - 1) / kTW, (H + kTH - 1) / kTH);
+  loss_maps_kernel<<<grid, kThr, kMapsSmem, st>>>(ren, tgt, W, H, scale, gmaps, block_sums);
+  if (d_image)
+    loss_grad_kernel<<<grid, kThr, kGradSmem, st>>>(ren, tgt, gmaps, W, H, beta, l1_norm, has_ssim, d_image);
   loss_finalize_kernel<<<1, 256, 0, st>>>(block_sums, (int)(grid.x * grid.y), l1_norm, scale, has_ssim, beta, out3);
   *launches += d_image ? 3 : 2;
   GSB_CHECK_LAUNCH("rgb_loss kernels");
   return GSB_OK;
 }
 
-size_t loss_block_count(int W, int H) { return (size_t)((W + kLT - 1) / kLT) * ((H + kLT - 1) / kLT); }
+size_t loss_block_count(int W, int H) { return (size_t)((W + kTW - 1) / kTW) * ((H + kTH - 1) / kTH); }
 
 }  // namespace gsb

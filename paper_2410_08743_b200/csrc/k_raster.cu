@@ -416,8 +416,11 @@ __device__ __forceinline__ bool backward_one(PixBwd& p, const float4& ge, const 
   return true;
 }
 
+#ifndef GSB_BWD_MIN_BLOCKS
+#define GSB_BWD_MIN_BLOCKS 8
+#endif
 template <int NC>
-__global__ void __launch_bounds__(kThreads, 8) backward_raster_kernel(
+__global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ ranks, const SplatRec* __restrict__ rec,
     const SplatAux* __restrict__ aux, const CamDev* __restrict__ cam_p, RasterDev rc, float bg_r, float bg_g,
     float bg_b, int64_t npix, const float* __restrict__ d_image, const float* __restrict__ final_t,
