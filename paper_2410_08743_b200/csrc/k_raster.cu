@@ -146,6 +146,16 @@ __device__ __forceinline__ int build_lists(const uint16_t* s_mask, int cnt, int 
   return max(max(n[0], n[1]), max(n[2], n[3]));
 }
 
+// A splat record as the raster loops read it from shared memory: one base
+// address per entry (tile-local mean, conic, opacity, colour; entry slot).
+struct __align__(16) StagedSplat {
+  float4 geo;  // mx, my, conic a, conic b
+  float4 app;  // conic c, opacity, colour r, g
+  float col_b;
+  uint32_t slot;
+  uint32_t pad[2];
+};
+
 struct PixFwd {
   float T, r, g, b;
   uint32_t processed;
@@ -190,8 +200,7 @@ __global__ void __launch_bounds__(kThreads) composite_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ ranks, const SplatRec* __restrict__ rec,
     const CamDev* __restrict__ cam_p, RasterDev rc, float bg_r, float bg_g, float bg_b, int64_t npix,
     float* __restrict__ image, float* __restrict__ final_t, uint32_t* __restrict__ pixstate) {
-  __shared__ float4 s_geo[kBatch], s_app[kBatch];
-  __shared__ float s_colb[kBatch];
+  __shared__ StagedSplat s_sp[kBatch];
   __shared__ uint16_t s_mask[kBatch];
   __shared__ uint8_t s_list[kWarps][kSubs][kBatch];
   __shared__ int s_w, s_h, s_tx;
@@ -219,8 +228,8 @@ __global__ void __launch_bounds__(kThreads) composite_kernel(
     const uint32_t e = base + threadIdx.x;
     const int cnt = min((uint32_t)kBatch, range.y - base);
     if (threadIdx.x < cnt)
-      s_mask[threadIdx.x] = (uint16_t)stage_splat(rec[ranks[e]], ox, oy, rc.cutoff2_f, &s_geo[threadIdx.x],
-                                                  &s_app[threadIdx.x], &s_colb[threadIdx.x]);
+      s_mask[threadIdx.x] = (uint16_t)stage_splat(rec[ranks[e]], ox, oy, rc.cutoff2_f, &s_sp[threadIdx.x].geo,
+                                                  &s_sp[threadIdx.x].app, &s_sp[threadIdx.x].col_b);
     __syncthreads();
     const uint32_t list0 = base - range.x;
     // a finished sub-warp lists nothing (its region's pixels are all terminated)
@@ -233,9 +242,10 @@ __global__ void __launch_bounds__(kThreads) composite_kernel(
     for (int it = 0; it < nmax; ++it) {
       if (it < mine) {
         const int k = s_list[warp][sub][it];
-        const float4 ge = s_geo[k];
-        const float4 ap = s_app[k];
-        const float cb = s_colb[k];
+        const StagedSplat& S = s_sp[k];
+        const float4 ge = S.geo;
+        const float4 ap = S.app;
+        const float cb = S.col_b;
         const float dx = px - ge.x, dy = py - ge.y;
         composite_one(a, ge, ap, cb, dx, dy, rc, list0 + k + 1u);
         composite_one(b, ge, ap, cb, dx, dy + 1.0f, rc, list0 + k + 1u);
@@ -355,8 +365,11 @@ __device__ __forceinline__ int warp_reduce8(const float v[8], float* out) {
   return (lane & 3) ? -1 : (h1 ? 4 : 0) + (h2 ? 2 : 0) + (h3 ? 1 : 0);
 }
 
+// Backward pixel state. Bd = sum_c d_pix[c] * behind[c]: the replay only
+// ever needs the behind colour dotted with the pixel's upstream gradient
+// (rasterizer.cpp:386-390), so one scalar replaces the three channels.
 struct PixBwd {
-  float dr, dg, db, T, br, bg, bb;
+  float dr, dg, db, T, Bd;
   uint32_t contrib;
 };
 
@@ -376,9 +389,7 @@ __device__ __forceinline__ void load_pixel_bwd(PixBwd& p, int x, int y, int W, i
     p.contrib = ps & 0x1fffffffu;
     if (p.dr == 0.f && p.dg == 0.f && p.db == 0.f) p.contrib = 0;  // rasterizer.cpp:372
   }
-  p.br = bg_r * p.T;
-  p.bg = bg_g * p.T;
-  p.bb = bg_b * p.T;
+  p.Bd = p.T * (p.dr * bg_r + p.dg * bg_g + p.db * bg_b);
 }
 
 // One (pixel, splat) replay step of phase 1; accumulates into v (NC = 8:
@@ -398,7 +409,9 @@ __device__ __forceinline__ bool backward_one(PixBwd& p, const float4& ge, const 
   v[5] = fmaf(wgt, p.dr, v[5]);
   v[6] = fmaf(wgt, p.dg, v[6]);
   v[7] = fmaf(wgt, p.db, v[7]);
-  const float dal = p.dr * (ap.z * tb - p.br * inv) + p.dg * (ap.w * tb - p.bg * inv) + p.db * (col_b * tb - p.bb * inv);
+  // d_alpha = sum_c d_c (c_c t_before - behind_c / (1 - alpha))
+  const float dc = fmaf(p.dr, ap.z, fmaf(p.dg, ap.w, p.db * col_b));
+  const float dal = fmaf(tb, dc, -inv * p.Bd);
   if (araw < rc.alpha_clamp_f) {
     const float cx_ = ge.z * dx + ge.w * dy, cy_ = ge.w * dx + ap.x * dy;
     if (NC > 8) v[NC - 1] = fmaf(dal, G, v[NC - 1]);
@@ -410,9 +423,7 @@ __device__ __forceinline__ bool backward_one(PixBwd& p, const float4& ge, const 
     v[4] = fmaf(dgg * dy, dy, v[4]);
   }
   p.T = tb;
-  p.br = fmaf(ap.z, wgt, p.br);
-  p.bg = fmaf(ap.w, wgt, p.bg);
-  p.bb = fmaf(col_b, wgt, p.bb);
+  p.Bd = fmaf(wgt, dc, p.Bd);  // behind += colour * weight
   return true;
 }
 
@@ -425,9 +436,7 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
     const SplatAux* __restrict__ aux, const CamDev* __restrict__ cam_p, RasterDev rc, float bg_r, float bg_g,
     float bg_b, int64_t npix, const float* __restrict__ d_image, const float* __restrict__ final_t,
     const uint32_t* __restrict__ pixstate, float* __restrict__ partials, uint32_t k_cap) {
-  __shared__ float4 s_geo[kBatch], s_app[kBatch];
-  __shared__ float s_colb[kBatch];
-  __shared__ uint32_t s_slot[kBatch];
+  __shared__ StagedSplat s_sp[kBatch];
   __shared__ uint8_t s_mask[kBatch];
   __shared__ uint8_t s_list[kWarps][kBatch];
   __shared__ float s_red[kWarps][kBatch][NC];  // [warp][entry in batch][component]
@@ -472,11 +481,11 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
       const uint32_t r = ranks[e];
       const SplatAux A = aux[r];
       const uint32_t tx0 = A.tx0_ty0 & 0xffffu, ty0 = A.tx0_ty0 >> 16, nx = A.nx_ny & 0xffffu;
-      s_slot[threadIdx.x] = A.off + ((uint32_t)ty - ty0) * nx + ((uint32_t)tx - tx0);
+      StagedSplat& S = s_sp[threadIdx.x];
+      S.slot = A.off + ((uint32_t)ty - ty0) * nx + ((uint32_t)tx - tx0);
       s_mask[threadIdx.x] =
           b0 + threadIdx.x < maxc
-              ? (uint8_t)quad_mask(stage_splat(rec[r], ox, oy, rc.cutoff2_f, &s_geo[threadIdx.x],
-                                               &s_app[threadIdx.x], &s_colb[threadIdx.x]))
+              ? (uint8_t)quad_mask(stage_splat(rec[r], ox, oy, rc.cutoff2_f, &S.geo, &S.app, &S.col_b))
               : (uint8_t)0;
     }
     __syncthreads();
@@ -486,9 +495,10 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
         const int k = s_list[warp][i];
         const uint32_t j = b0 + (uint32_t)k;
         if (j >= wmax) continue;  // warp-uniform
-        const float4 ge = s_geo[k];
-        const float4 ap = s_app[k];
-        const float cb = s_colb[k];
+        const StagedSplat& S = s_sp[k];
+        const float4 ge = S.geo;
+        const float4 ap = S.app;
+        const float cb = S.col_b;
         float v[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) v[c] = 0.f;
@@ -512,7 +522,8 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
         acc += s_red[w][k][c];
         s_red[w][k][c] = 0.f;
       }
-      if (s_slot[k] < k_cap) partials[(int64_t)s_slot[k] * NC + c] = acc;
+      const uint32_t slot = s_sp[k].slot;
+      if (slot < k_cap) partials[(int64_t)slot * NC + c] = acc;
     }
     __syncthreads();
   }
