@@ -179,6 +179,36 @@ __device__ __forceinline__ void composite_one(PixFwd& p, const float4& ge, const
   }
 }
 
+// Both pixels of a lane for one splat, branch free (alpha = 0 is an exact
+// no-op for a pixel that is done or outside the cutoff).
+__device__ __forceinline__ void composite_pair(PixFwd& a, PixFwd& b, const float4& ge, const float4& ap, float col_b,
+                                               float dx, float dy, const RasterDev& rc, uint32_t idx1) {
+  const float ga = splat_power(ge.z, ge.w, ap.x, dx, dy);
+  const float gb = splat_power(ge.z, ge.w, ap.x, dx, dy + 1.0f);
+  const bool ha = !a.done && ga <= rc.cutoff2_f;
+  const bool hb = !b.done && gb <= rc.cutoff2_f;
+  if (!(ha || hb)) return;
+  const float al_a = ha ? fminf(rc.alpha_clamp_f, ap.y * exp_neg_half(ga)) : 0.f;
+  const float al_b = hb ? fminf(rc.alpha_clamp_f, ap.y * exp_neg_half(gb)) : 0.f;
+  const float wa = al_a * a.T, wb = al_b * b.T;
+  a.r = fmaf(ap.z, wa, a.r);
+  a.g = fmaf(ap.w, wa, a.g);
+  a.b = fmaf(col_b, wa, a.b);
+  b.r = fmaf(ap.z, wb, b.r);
+  b.g = fmaf(ap.w, wb, b.g);
+  b.b = fmaf(col_b, wb, b.b);
+  a.T *= (1.0f - al_a);
+  b.T *= (1.0f - al_b);
+  if (ha && a.T < rc.early_term_f) {
+    a.done = true;
+    a.processed = idx1;
+  }
+  if (hb && b.T < rc.early_term_f) {
+    b.done = true;
+    b.processed = idx1;
+  }
+}
+
 __device__ __forceinline__ void write_pixel(const PixFwd& p, int x, int y, int W, int H, float bg_r, float bg_g,
                                             float bg_b, int64_t npix, float* image, float* final_t,
                                             uint32_t* pixstate) {
@@ -247,8 +277,7 @@ __global__ void __launch_bounds__(kThreads) composite_kernel(
         const float4 ap = S.app;
         const float cb = S.col_b;
         const float dx = px - ge.x, dy = py - ge.y;
-        composite_one(a, ge, ap, cb, dx, dy, rc, list0 + k + 1u);
-        composite_one(b, ge, ap, cb, dx, dy + 1.0f, rc, list0 + k + 1u);
+        composite_pair(a, b, ge, ap, cb, dx, dy, rc, list0 + k + 1u);
       }
       // a sub-warp whose 16 pixels have all terminated stops early
       if (__all_sync(kFull, (a.done && b.done) || it + 1 >= mine)) break;
@@ -427,6 +456,52 @@ __device__ __forceinline__ bool backward_one(PixBwd& p, const float4& ge, const 
   return true;
 }
 
+// Both pixels of a lane for one splat, branch free: a pixel that is past its
+// contrib count or outside the cutoff gets alpha_raw = 0, which makes every
+// update below an exact no-op (inv = 1, weight 0, d_alpha chain times 0), so
+// the two independent chains interleave without divergent branches.
+template <int NC>
+__device__ __forceinline__ bool backward_pair(PixBwd& a, PixBwd& b, const float4& ge, const float4& ap, float col_b,
+                                              float dx, float dy, const RasterDev& rc, uint32_t j, float v[NC]) {
+  const float ga = splat_power(ge.z, ge.w, ap.x, dx, dy);
+  const float gb = splat_power(ge.z, ge.w, ap.x, dx, dy + 1.0f);
+  const bool ha = j < a.contrib && ga <= rc.cutoff2_f;
+  const bool hb = j < b.contrib && gb <= rc.cutoff2_f;
+  if (!(ha || hb)) return false;
+  const float Ga = exp_neg_half(ga), Gb = exp_neg_half(gb);
+  const float ra = ha ? ap.y * Ga : 0.f, rb = hb ? ap.y * Gb : 0.f;  // alpha_raw
+  const float al_a = fminf(rc.alpha_clamp_f, ra), al_b = fminf(rc.alpha_clamp_f, rb);
+  const float ia = rcp_fast(1.0f - al_a), ib = rcp_fast(1.0f - al_b);
+  const float ta = a.T * ia, tb = b.T * ib;  // t_before
+  const float wa = al_a * ta, wb = al_b * tb;
+  v[5] = fmaf(wa, a.dr, fmaf(wb, b.dr, v[5]));
+  v[6] = fmaf(wa, a.dg, fmaf(wb, b.dg, v[6]));
+  v[7] = fmaf(wa, a.db, fmaf(wb, b.db, v[7]));
+  const float dca = fmaf(a.dr, ap.z, fmaf(a.dg, ap.w, a.db * col_b));
+  const float dcb = fmaf(b.dr, ap.z, fmaf(b.dg, ap.w, b.db * col_b));
+  const float dala = fmaf(ta, dca, -ia * a.Bd), dalb = fmaf(tb, dcb, -ib * b.Bd);
+  // alpha-chain gradients only where alpha_raw < clamp (rasterizer.cpp:392)
+  const float ka = ra < rc.alpha_clamp_f ? dala * (-0.5f * ra) : 0.f;
+  const float kb = rb < rc.alpha_clamp_f ? dalb * (-0.5f * rb) : 0.f;
+  if (NC > 8) {
+    v[NC - 1] = fmaf(ra < rc.alpha_clamp_f ? dala : 0.f, Ga * (ha ? 1.f : 0.f),
+                     fmaf(rb < rc.alpha_clamp_f ? dalb : 0.f, Gb * (hb ? 1.f : 0.f), v[NC - 1]));
+  }
+  const float dyb = dy + 1.0f;
+  const float cxa = ge.z * dx + ge.w * dy, cya = ge.w * dx + ap.x * dy;
+  const float cxb = ge.z * dx + ge.w * dyb, cyb = ge.w * dx + ap.x * dyb;
+  v[0] = fmaf(-2.0f * ka, cxa, fmaf(-2.0f * kb, cxb, v[0]));
+  v[1] = fmaf(-2.0f * ka, cya, fmaf(-2.0f * kb, cyb, v[1]));
+  v[2] = fmaf(ka * dx, dx, fmaf(kb * dx, dx, v[2]));
+  v[3] = fmaf(ka * dx, dy, fmaf(kb * dx, dyb, v[3]));
+  v[4] = fmaf(ka * dy, dy, fmaf(kb * dyb, dyb, v[4]));
+  a.T = ta;
+  b.T = tb;
+  a.Bd = fmaf(wa, dca, a.Bd);
+  b.Bd = fmaf(wb, dcb, b.Bd);
+  return true;
+}
+
 #ifndef GSB_BWD_MIN_BLOCKS
 #define GSB_BWD_MIN_BLOCKS 8
 #endif
@@ -503,9 +578,8 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
 #pragma unroll
         for (int c = 0; c < NC; ++c) v[c] = 0.f;
         const float dx = px - ge.x, dy = py - ge.y;
-        const bool ha = backward_one<NC>(a, ge, ap, cb, dx, dy, rc, j, v);
-        const bool hb = backward_one<NC>(b, ge, ap, cb, dx, dy + 1.0f, rc, j, v);
-        if (__any_sync(kFull, ha || hb)) {
+        const bool hit = backward_pair<NC>(a, b, ge, ap, cb, dx, dy, rc, j, v);
+        if (__any_sync(kFull, hit)) {
           float tot;
           const int vi = NC == 8 ? warp_reduce8(v, &tot) : warp_reduce9(v, &tot);
           if (vi >= 0) s_red[warp][k][vi] = tot;
