@@ -193,6 +193,10 @@ def run_ours(args, ws, rank, local):
     # for C3's independent views: one call per GPU over its views)
     e2e_iters = args.e2e_iters
     e2e_cfg = gsb.PoseConfig.default(budget=e2e_iters, pose_converged_eps=0.0)
+    # one untimed warm-up call (first-call allocations, graph instantiation)
+    warm = [gsb.Image(ctx, host_targets[v]) for v in views]
+    gsb.estimate_poses(ctx, cloud, warm, intr, init[views], gsb.PoseConfig.default(budget=4, pose_converged_eps=0.0))
+    del warm
     if dist:
         dist.barrier()
     ctx.synchronize()

@@ -35,7 +35,10 @@ int scan_onepass(cudaStream_t st, const uint32_t* in, int64_t cap, const uint32_
                  uint32_t* status, uint32_t* total, int64_t* launches);
 
 constexpr int kBinThreads = 512;
-constexpr int kBinChunk = 4096;  // Gaussians per counting CTA
+#ifndef GSB_BIN_CHUNK
+#define GSB_BIN_CHUNK 4096
+#endif
+constexpr int kBinChunk = GSB_BIN_CHUNK;  // Gaussians per counting CTA
 
 int64_t bin_chunks(int64_t n) { return std::max<int64_t>((n + kBinChunk - 1) / kBinChunk, 1); }
 

@@ -298,19 +298,28 @@ __global__ void __launch_bounds__(kGeomBlock, 2) backward_geom_kernel(
   }
 }
 
-__global__ void pose_reduce_kernel(const double* __restrict__ blocks, int64_t nb, double* __restrict__ out) {
+// Fixed-order reduction of the per-block pose partials: each thread sums a
+// strided subset in order, then a fixed binary tree in shared memory (same
+// association every launch: deterministic), 6 components at once.
+__global__ void __launch_bounds__(256) pose_reduce_kernel(const double* __restrict__ blocks, int64_t nb,
+                                                          double* __restrict__ out) {
   __shared__ double s[6][256];
-  for (int k = 0; k < 6; ++k) {
-    double t = 0.0;
-    for (int64_t b = threadIdx.x; b < nb; b += 256) t += blocks[b * 6 + k];
-    s[k][threadIdx.x] = t;
+  double t[6] = {0, 0, 0, 0, 0, 0};
+  for (int64_t b = threadIdx.x; b < nb; b += 256) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) t[k] += blocks[b * 6 + k];
   }
+#pragma unroll
+  for (int k = 0; k < 6; ++k) s[k][threadIdx.x] = t[k];
   __syncthreads();
-  if (threadIdx.x < 6) {
-    double t = 0.0;
-    for (int j = 0; j < 256; ++j) t += s[threadIdx.x][j];
-    out[threadIdx.x] = t;
+  for (int h = 128; h > 0; h >>= 1) {
+    if (threadIdx.x < h) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) s[k][threadIdx.x] += s[k][threadIdx.x + h];
+    }
+    __syncthreads();
   }
+  if (threadIdx.x < 6) out[threadIdx.x] = s[threadIdx.x][0];
 }
 
 int launch_backward_geom(cudaStream_t st, const gsb_cloud* cloud, gsb_frame* f, const RasterDev& rc, bool full,

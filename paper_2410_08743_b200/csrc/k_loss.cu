@@ -257,8 +257,9 @@ __global__ void __launch_bounds__(kThr) loss_grad_kernel(const float* __restrict
 }
 
 // Fixed-order reduction of the block partials; out = {l1_mean, ssim_mean, loss}.
-__global__ void loss_finalize_kernel(const double* __restrict__ block_sums, int nb, double l1_norm, double scale,
-                                     int has_ssim, double beta, double* __restrict__ out) {
+__global__ void __launch_bounds__(256) loss_finalize_kernel(const double* __restrict__ block_sums, int nb,
+                                                            double l1_norm, double scale, int has_ssim, double beta,
+                                                            double* __restrict__ out) {
   __shared__ double s1[256], s2[256];
   double a = 0.0, b = 0.0;
   for (int i = threadIdx.x; i < nb; i += 256) {
@@ -268,14 +269,16 @@ __global__ void loss_finalize_kernel(const double* __restrict__ block_sums, int 
   s1[threadIdx.x] = a;
   s2[threadIdx.x] = b;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double ta = 0.0, tb = 0.0;
-    for (int i = 0; i < 256; ++i) {
-      ta += s1[i];
-      tb += s2[i];
+  for (int h = 128; h > 0; h >>= 1) {  // fixed binary tree: deterministic
+    if (threadIdx.x < h) {
+      s1[threadIdx.x] += s1[threadIdx.x + h];
+      s2[threadIdx.x] += s2[threadIdx.x + h];
     }
-    const double l1 = ta * l1_norm;
-    const double ssim = has_ssim ? tb * scale : 1.0;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double l1 = s1[0] * l1_norm;
+    const double ssim = has_ssim ? s2[0] * scale : 1.0;
     out[0] = l1;
     out[1] = ssim;
     out[2] = (1.0 - beta) * l1 + beta * (1.0 - ssim);
