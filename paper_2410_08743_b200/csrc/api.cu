@@ -1420,6 +1420,7 @@ static gsb_frame* session_frame(gsb_ctx* ctx, gsb_session* s) { return s->own ? 
 // Frame set-up + buffer sizing for one session iteration (no capture).
 static int session_frame_ready(gsb_ctx* ctx, gsb_session* s, gsb_frame** out) {
   gsb_frame* f = session_frame(ctx, s);
+  f->lean = true;  // never exported (not reachable through gsb_frame_download)
   if (int r = frame_setup(ctx, f, s->cloud, &s->cam, s->cfg.background, &s->cfg.raster, false)) return r;
   const int64_t want = f->k_cap > 0 ? f->k_cap : std::max<int64_t>(3 * s->cloud->n, 1 << 16);
   if (int r = frame_reserve(f, s->cloud, want)) return r;
@@ -2073,6 +2074,7 @@ static int joint_launch_step(gsb_ctx* ctx, gsb_joint* j) {
 
 static int joint_frames_ready(gsb_ctx* ctx, gsb_joint* j) {
   for (gsb_frame* f : j->frames) {
+    f->lean = true;
     if (int r = frame_setup(ctx, f, j->cloud, &j->cam, j->cfg.background, &j->cfg.raster, false)) return r;
     const int64_t want = f->k_cap > 0 ? f->k_cap : std::max<int64_t>(3 * j->cloud->n, 1 << 16);
     if (int r = frame_reserve(f, j->cloud, want)) return r;

@@ -237,6 +237,7 @@ struct gsb_frame {
   double background[3] = {0, 0, 0};
   bool valid = false;
   bool has_dimage = false;
+  bool lean = false;      // internal state (sessions, joint): skip the export-only K1 outputs
   // device camera / config
   gsb::DevBuf cam;        // CamDev
   // per Gaussian (n)

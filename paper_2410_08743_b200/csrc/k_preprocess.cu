@@ -142,6 +142,8 @@ struct PreOut {
   uint32_t* off_g;
   int64_t n_pad_out;  // plane stride of colj
   int32_t tile_local;
+  int32_t write_rect;    // tile rect (global binning / export)
+  int32_t write_export;  // radius, rank_of_g = -1 (RenderOutput export only)
   int32_t pad;
 };
 constexpr int kMaxPreViews = 16;
@@ -271,9 +273,9 @@ __device__ __forceinline__ uint32_t project_one(const float* P, int64_t n_pad, i
   o.rec_g[i] = rec;
   *rect_x = (uint32_t)tx0 | ((uint32_t)tx1 << 16);
   *rect_y = (uint32_t)ty0 | ((uint32_t)ty1 << 16);
-  o.rect_g[i] = make_uint2(*rect_x, *rect_y);
+  if (o.write_rect) o.rect_g[i] = make_uint2(*rect_x, *rect_y);
   o.depth_g[i] = cz;
-  o.radius_g[i] = radius;
+  if (o.write_export) o.radius_g[i] = radius;
   return ((uint32_t)(tx1 - tx0 + 1) * (uint32_t)(ty1 - ty0 + 1)) | (clamp << kClampShift);
 }
 
@@ -347,7 +349,7 @@ __global__ void __launch_bounds__(kPreBlock) preprocess_kernel(const float* __re
     const PreOut& o = views.v[v];
     uint32_t cnt = 0, rect_x = 0, rect_y = 0;
     if (i < n) {
-      o.rank_of_g[i] = -1;
+      if (o.write_export) o.rank_of_g[i] = -1;
       cnt = project_one<DEG, kQuirk>(P, n_pad, sh_cap, g, s_cam[v], rc, i, o, &rect_x, &rect_y);
       o.cnt_g[i] = cnt;
     }
@@ -371,6 +373,8 @@ static PreOut pre_out(const CamDev* cam_src, CamDev* cam_dst, gsb_frame* f, int6
   o.off_g = f->off_g.as<uint32_t>();
   o.n_pad_out = n_pad;
   o.tile_local = f->binning == kBinTileLocal ? 1 : 0;
+  o.write_export = f->lean ? 0 : 1;
+  o.write_rect = (!f->lean || f->binning != kBinTileLocal) ? 1 : 0;
   return o;
 }
 
