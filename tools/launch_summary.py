@@ -16,7 +16,7 @@ def main(path):
             continue
         v = float(r[vi].replace(",", ""))
         unit = r[ui]
-        us = v / 1000.0 if unit == "nsecond" else v * 1000.0 if unit == "msecond" else v
+        us = v / 1000.0 if unit in ("nsecond", "ns") else v * 1000.0 if unit in ("msecond", "ms") else v
         tot[r[ki]] += us
         cnt[r[ki]] += 1
     s = sum(tot.values())
