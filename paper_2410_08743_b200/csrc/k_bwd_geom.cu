@@ -48,9 +48,15 @@ __device__ __forceinline__ void sh_basis_d(double x, double y, double z, int deg
 // colour-Jacobian planes, the tile counts and the entry offsets are staged
 // into shared memory by TMA bulk copies (one elected thread, one mbarrier).
 constexpr int kGeomBlock = 256;
+#ifndef GSB_POSE_CHAIN_T
+#define GSB_POSE_CHAIN_T float
+#endif
 constexpr int kGeomPlanes = kOpacity + 1;  // means, quat, log-scale, opacity
 
-template <bool kFull>
+// R: arithmetic type of the per-splat chain — double for the full gradient
+// bundle (joint_optimize's parameter gradients), float for the pose-only
+// path (the 6-vector itself is accumulated in FP64 either way).
+template <bool kFull, typename R>
 __global__ void __launch_bounds__(kGeomBlock, 2) backward_geom_kernel(
     const float* __restrict__ params, int64_t n, int64_t n_pad_g, int sh_cap, int sh_active,
     const CamDev* __restrict__ cam_p, RasterDev rc, const uint32_t* __restrict__ cnt_g,
@@ -112,62 +118,64 @@ __global__ void __launch_bounds__(kGeomBlock, 2) backward_geom_kernel(
     }
     const float* P = s_par + threadIdx.x;
     constexpr int64_t n_pad = kGeomBlock;  // plane stride of the staged copy
-    const double mean0 = P[kMeanX * n_pad], mean1 = P[kMeanY * n_pad], mean2 = P[kMeanZ * n_pad];
-    const double* Rc = cam.R;
-    double mc[3];
+    const R mean0 = P[kMeanX * n_pad], mean1 = P[kMeanY * n_pad], mean2 = P[kMeanZ * n_pad];
+    R Rc[9];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) mc[a] = Rc[a * 3] * mean0 + Rc[a * 3 + 1] * mean1 + Rc[a * 3 + 2] * mean2 + cam.t[a];
-    const double iz = 1.0 / mc[2], iz2 = iz * iz, iz3 = iz2 * iz;
-    const double fx = cam.fx, fy = cam.fy;
-    const double J00 = fx * iz, J02 = -fx * mc[0] * iz2, J11 = fy * iz, J12 = -fy * mc[1] * iz2;
-    double m[6];
+    for (int k = 0; k < 9; ++k) Rc[k] = (R)cam.R[k];
+    R mc[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) mc[a] = Rc[a * 3] * mean0 + Rc[a * 3 + 1] * mean1 + Rc[a * 3 + 2] * mean2 + (R)cam.t[a];
+    const R iz = R(1.0) / mc[2], iz2 = iz * iz, iz3 = iz2 * iz;
+    const R fx = (R)cam.fx, fy = (R)cam.fy;
+    const R J00 = fx * iz, J02 = -fx * mc[0] * iz2, J11 = fy * iz, J12 = -fy * mc[1] * iz2;
+    R m[6];
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
       m[b] = J00 * Rc[b] + J02 * Rc[6 + b];
       m[3 + b] = J11 * Rc[3 + b] + J12 * Rc[6 + b];
     }
-    const double sc0 = exp((double)P[kScaleX * n_pad]), sc1 = exp((double)P[kScaleY * n_pad]),
-                 sc2 = exp((double)P[kScaleZ * n_pad]);
-    const double qr0 = P[kQuatW * n_pad], qr1 = P[kQuatX * n_pad], qr2 = P[kQuatY * n_pad], qr3 = P[kQuatZ * n_pad];
-    const double qn = sqrt(qr0 * qr0 + qr1 * qr1 + qr2 * qr2 + qr3 * qr3);
-    const double w = qr0 / qn, x = qr1 / qn, y = qr2 / qn, zq = qr3 / qn;
-    const double Rg[9] = {1 - 2 * (y * y + zq * zq), 2 * (x * y - w * zq), 2 * (x * zq + w * y),
+    const R sc0 = exp((R)P[kScaleX * n_pad]), sc1 = exp((R)P[kScaleY * n_pad]),
+                 sc2 = exp((R)P[kScaleZ * n_pad]);
+    const R qr0 = P[kQuatW * n_pad], qr1 = P[kQuatX * n_pad], qr2 = P[kQuatY * n_pad], qr3 = P[kQuatZ * n_pad];
+    const R qn = sqrt(qr0 * qr0 + qr1 * qr1 + qr2 * qr2 + qr3 * qr3);
+    const R w = qr0 / qn, x = qr1 / qn, y = qr2 / qn, zq = qr3 / qn;
+    const R Rg[9] = {1 - 2 * (y * y + zq * zq), 2 * (x * y - w * zq), 2 * (x * zq + w * y),
                           2 * (x * y + w * zq), 1 - 2 * (x * x + zq * zq), 2 * (y * zq - w * x),
                           2 * (x * zq - w * y), 2 * (y * zq + w * x), 1 - 2 * (x * x + y * y)};
-    const double s2[3] = {sc0 * sc0, sc1 * sc1, sc2 * sc2};
-    double Sg[6];  // symmetric Sigma: 00 01 02 11 12 22
+    const R s2[3] = {sc0 * sc0, sc1 * sc1, sc2 * sc2};
+    R Sg[6];  // symmetric Sigma: 00 01 02 11 12 22
     Sg[0] = Rg[0] * Rg[0] * s2[0] + Rg[1] * Rg[1] * s2[1] + Rg[2] * Rg[2] * s2[2];
     Sg[1] = Rg[0] * Rg[3] * s2[0] + Rg[1] * Rg[4] * s2[1] + Rg[2] * Rg[5] * s2[2];
     Sg[2] = Rg[0] * Rg[6] * s2[0] + Rg[1] * Rg[7] * s2[1] + Rg[2] * Rg[8] * s2[2];
     Sg[3] = Rg[3] * Rg[3] * s2[0] + Rg[4] * Rg[4] * s2[1] + Rg[5] * Rg[5] * s2[2];
     Sg[4] = Rg[3] * Rg[6] * s2[0] + Rg[4] * Rg[7] * s2[1] + Rg[5] * Rg[8] * s2[2];
     Sg[5] = Rg[6] * Rg[6] * s2[0] + Rg[7] * Rg[7] * s2[1] + Rg[8] * Rg[8] * s2[2];
-    auto S = [&](int r, int c) -> double {
+    auto S = [&](int r, int c) -> R {
       const int a = r < c ? r : c, b = r < c ? c : r;
       return Sg[a == 0 ? b : (a == 1 ? 2 + b : 5)];
     };
     // cov2d = m Sigma m^T + dilation; conic = cov2d^-1 (same expressions as K1)
-    double ms[6];
+    R ms[6];
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
       for (int b = 0; b < 3; ++b) ms[a * 3 + b] = m[a * 3] * S(0, b) + m[a * 3 + 1] * S(1, b) + m[a * 3 + 2] * S(2, b);
-    const double c00 = ms[0] * m[0] + ms[1] * m[1] + ms[2] * m[2] + rc.dilation;
-    const double c01 = ms[0] * m[3] + ms[1] * m[4] + ms[2] * m[5];
-    const double c11 = ms[3] * m[3] + ms[4] * m[4] + ms[5] * m[5] + rc.dilation;
-    const double det = c00 * c11 - c01 * c01;
-    const double C0 = c11 / det, C1 = -c01 / det, C3 = c00 / det;
+    const R c00 = ms[0] * m[0] + ms[1] * m[1] + ms[2] * m[2] + (R)rc.dilation;
+    const R c01 = ms[0] * m[3] + ms[1] * m[4] + ms[2] * m[5];
+    const R c11 = ms[3] * m[3] + ms[4] * m[4] + ms[5] * m[5] + (R)rc.dilation;
+    const R det = c00 * c11 - c01 * c01;
+    const R C0 = c11 / det, C1 = -c01 / det, C3 = c00 / det;
     // d_cov2d = -(C D C), D symmetric = [[D00, D01], [D01, D11]]
-    const double D00 = acc[2], D01 = acc[3], D11 = acc[4];
-    const double E0 = C0 * D00 + C1 * D01, E1 = C0 * D01 + C1 * D11;  // (C D) row 0
-    const double E2 = C1 * D00 + C3 * D01, E3 = C1 * D01 + C3 * D11;  // (C D) row 1
-    const double dc00 = -(E0 * C0 + E1 * C1), dc01 = -(E0 * C1 + E1 * C3), dc11 = -(E2 * C1 + E3 * C3);
+    const R D00 = acc[2], D01 = acc[3], D11 = acc[4];
+    const R E0 = C0 * D00 + C1 * D01, E1 = C0 * D01 + C1 * D11;  // (C D) row 0
+    const R E2 = C1 * D00 + C3 * D01, E3 = C1 * D01 + C3 * D11;  // (C D) row 1
+    const R dc00 = -(E0 * C0 + E1 * C1), dc01 = -(E0 * C1 + E1 * C3), dc11 = -(E2 * C1 + E3 * C3);
     // d_m = 2 dcov m Sigma (2x3)
-    double t0[3], t1[3], dm[6];
+    R t0[3], t1[3], dm[6];
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
-      t0[b] = 2.0 * (dc00 * m[b] + dc01 * m[3 + b]);
-      t1[b] = 2.0 * (dc01 * m[b] + dc11 * m[3 + b]);
+      t0[b] = R(2.0) * (dc00 * m[b] + dc01 * m[3 + b]);
+      t1[b] = R(2.0) * (dc01 * m[b] + dc11 * m[3 + b]);
     }
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
@@ -175,30 +183,30 @@ __global__ void __launch_bounds__(kGeomBlock, 2) backward_geom_kernel(
       dm[3 + b] = t1[0] * S(0, b) + t1[1] * S(1, b) + t1[2] * S(2, b);
     }
     // d_jac = d_m R^T (only columns 0 and 2 of row 0, 1 and 2 of row 1 matter)
-    const double dj00 = dm[0] * Rc[0] + dm[1] * Rc[1] + dm[2] * Rc[2];
-    const double dj02 = dm[0] * Rc[6] + dm[1] * Rc[7] + dm[2] * Rc[8];
-    const double dj11 = dm[3] * Rc[3] + dm[4] * Rc[4] + dm[5] * Rc[5];
-    const double dj12 = dm[3] * Rc[6] + dm[4] * Rc[7] + dm[5] * Rc[8];
-    const double dmu2x = acc[0], dmu2y = acc[1];
-    double dmc[3];
+    const R dj00 = dm[0] * Rc[0] + dm[1] * Rc[1] + dm[2] * Rc[2];
+    const R dj02 = dm[0] * Rc[6] + dm[1] * Rc[7] + dm[2] * Rc[8];
+    const R dj11 = dm[3] * Rc[3] + dm[4] * Rc[4] + dm[5] * Rc[5];
+    const R dj12 = dm[3] * Rc[6] + dm[4] * Rc[7] + dm[5] * Rc[8];
+    const R dmu2x = acc[0], dmu2y = acc[1];
+    R dmc[3];
     dmc[0] = dj02 * (-fx * iz2) + dmu2x * fx * iz;
     dmc[1] = dj12 * (-fy * iz2) + dmu2y * fy * iz;
-    dmc[2] = dj00 * (-fx * iz2) + dj11 * (-fy * iz2) + dj02 * (2.0 * fx * mc[0] * iz3) +
-             dj12 * (2.0 * fy * mc[1] * iz3) - dmu2x * fx * mc[0] * iz2 - dmu2y * fy * mc[1] * iz2;
+    dmc[2] = dj00 * (-fx * iz2) + dj11 * (-fy * iz2) + dj02 * (R(2.0) * fx * mc[0] * iz3) +
+             dj12 * (R(2.0) * fy * mc[1] * iz3) - dmu2x * fx * mc[0] * iz2 - dmu2y * fy * mc[1] * iz2;
     // colour chain: d_dir = G^T d_colour, projected and scaled by 1/dist
-    const double tg0 = mean0 - cam.center[0], tg1 = mean1 - cam.center[1], tg2 = mean2 - cam.center[2];
-    const double dist = sqrt(tg0 * tg0 + tg1 * tg1 + tg2 * tg2);
-    const double dir0 = tg0 / dist, dir1 = tg1 / dist, dir2 = tg2 / dist;
-    const double dcol[3] = {acc[5], acc[6], acc[7]};
-    double dd0 = 0, dd1 = 0, dd2 = 0;
+    const R tg0 = mean0 - (R)cam.center[0], tg1 = mean1 - (R)cam.center[1], tg2 = mean2 - (R)cam.center[2];
+    const R dist = sqrt(tg0 * tg0 + tg1 * tg1 + tg2 * tg2);
+    const R dir0 = tg0 / dist, dir1 = tg1 / dist, dir2 = tg2 / dist;
+    const R dcol[3] = {(R)acc[5], (R)acc[6], (R)acc[7]};
+    R dd0 = 0, dd1 = 0, dd2 = 0;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      dd0 += dcol[c] * (double)s_colj[(3 * c + 0) * kGeomBlock + threadIdx.x];
-      dd1 += dcol[c] * (double)s_colj[(3 * c + 1) * kGeomBlock + threadIdx.x];
-      dd2 += dcol[c] * (double)s_colj[(3 * c + 2) * kGeomBlock + threadIdx.x];
+      dd0 += dcol[c] * (R)s_colj[(3 * c + 0) * kGeomBlock + threadIdx.x];
+      dd1 += dcol[c] * (R)s_colj[(3 * c + 1) * kGeomBlock + threadIdx.x];
+      dd2 += dcol[c] * (R)s_colj[(3 * c + 2) * kGeomBlock + threadIdx.x];
     }
-    const double pd = dir0 * dd0 + dir1 * dd1 + dir2 * dd2;
-    const double dtg0 = (dd0 - dir0 * pd) / dist, dtg1 = (dd1 - dir1 * pd) / dist, dtg2 = (dd2 - dir2 * pd) / dist;
+    const R pd = dir0 * dd0 + dir1 * dd1 + dir2 * dd2;
+    const R dtg0 = (dd0 - dir0 * pd) / dist, dtg1 = (dd1 - dir1 * pd) / dist, dtg2 = (dd2 - dir2 * pd) / dist;
     // pose tangent (rasterizer.cpp:523-533); d_R_c = J^T d_m has rows
     // J00 dm0, J11 dm1, J02 dm0 + J12 dm1.
     pc0 = dmc[0] + (Rc[0] * dtg0 + Rc[1] * dtg1 + Rc[2] * dtg2);
@@ -209,7 +217,7 @@ __global__ void __launch_bounds__(kGeomBlock, 2) backward_geom_kernel(
     pc5 = mc[0] * dmc[1] - mc[1] * dmc[0];
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
-      const double r0 = J00 * dm[b], r1 = J11 * dm[3 + b], r2 = J02 * dm[b] + J12 * dm[3 + b];
+      const R r0 = J00 * dm[b], r1 = J11 * dm[3 + b], r2 = J02 * dm[b] + J12 * dm[3 + b];
       pc3 += -r1 * Rc[6 + b] + r2 * Rc[3 + b];
       pc4 += r0 * Rc[6 + b] - r2 * Rc[b];
       pc5 += -r0 * Rc[3 + b] + r1 * Rc[b];
@@ -328,12 +336,12 @@ int launch_backward_geom(cudaStream_t st, const gsb_cloud* cloud, gsb_frame* f, 
   const int64_t nb = (n + 255) / 256;
   if (nb > 0) {
     if (full)
-      backward_geom_kernel<true><<<(unsigned)nb, 256, 0, st>>>(
+      backward_geom_kernel<true, double><<<(unsigned)nb, 256, 0, st>>>(
           cloud->params.as<float>(), n, cloud->n_pad, cloud->sh_degree, cloud->active_sh_degree, f->cam.as<CamDev>(),
           rc, f->cnt_g.as<uint32_t>(), f->off_g.as<uint32_t>(), f->colj.as<float>(), f->partials.as<float>(), f->k_cap, grads,
           f->pose_blocks.as<double>());
     else
-      backward_geom_kernel<false><<<(unsigned)nb, 256, 0, st>>>(
+      backward_geom_kernel<false, GSB_POSE_CHAIN_T><<<(unsigned)nb, 256, 0, st>>>(
           cloud->params.as<float>(), n, cloud->n_pad, cloud->sh_degree, cloud->active_sh_degree, f->cam.as<CamDev>(),
           rc, f->cnt_g.as<uint32_t>(), f->off_g.as<uint32_t>(), f->colj.as<float>(), f->partials.as<float>(), f->k_cap, nullptr,
           f->pose_blocks.as<double>());

@@ -273,9 +273,11 @@ def test_backward_matches_oracle(G, ctx, seed):
     assert rel_err(g["d_opacity_logits"], gr.d_opacity_logits) < 1e-3
     assert rel_err(g["d_sh"], gr.d_sh) < 1e-3
     assert rel_err(g["d_mu2d"], gr.d_mu2d) < 1e-3
-    # pose-only path gives the same pose gradient (separately compiled kernel)
+    # pose-only path (8 partials per entry, FP32 per-splat chain, FP64 6-vector
+    # accumulation) agrees with the oracle and with the FP64-chain full path
     _, dp2 = G.render_backward(ctx, cloud, cam, out, d_img, pose_only=True)
-    assert np.max(np.abs(dp2 - dp)) <= 1e-12 * np.max(np.abs(dp))
+    assert rel_err(dp2, gr.d_pose) < 1e-3
+    assert np.max(np.abs(dp2 - dp)) <= 1e-5 * np.max(np.abs(dp))
 
 
 def test_backward_invariants(G, ctx):
