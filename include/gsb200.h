@@ -158,6 +158,11 @@ int gsb_cloud_synth(gsb_cloud* cloud, uint64_t seed, double log_scale_offset);
  * kind: 0 orbit, 1 forward-facing, 2 random-walk. poses: cameras*12 row-major [R|t]. */
 int gsb_synth_poses(uint64_t seed, int64_t n, int32_t sh_degree, int32_t kind, int32_t cameras,
                     double orbit_radius, double orbit_arc, double* poses);
+/* Rng helpers on a caller-held xorshift64* state (core.hpp:58-102): the split
+ * children's normal3 draws of densify_and_prune (children x 3, GCC draw
+ * order) and one epoch shuffle of pipelines.cpp:123-129. Host only. */
+int gsb_rng_child_normals(uint64_t* rng_state, int64_t children, double* out);
+int gsb_rng_shuffle(uint64_t* rng_state, int32_t n, int32_t* order);
 /* perturb_pose_tangent (eval.cpp:148-152), same rng convention as gsb_perturb_pose. */
 int gsb_perturb_pose_tangent(const double pose[12], double sigma, uint64_t* rng_state, double out[12]);
 /* Joint-test initial cloud (tests/test_trainer.cpp:598-601): means += mean_sigma
@@ -276,6 +281,15 @@ int gsb_estimate_poses(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* const* targets
                        const double* init_poses, int32_t count, const gsb_pose_config* cfg, double* poses_out,
                        double* final_losses, int32_t* steps_used);
 
+/* ---- densify_and_prune (trainer.hpp:130-133, trainer.cpp:144-239) ----
+ * grad_sum / count: the GradAccum arrays (host, cloud n entries). The cloud is
+ * rebuilt on the device (its size changes); adam (optional) is remapped like
+ * CloudAdam::remap. rng_state: the run's Rng (split children draw normal3).
+ * report = {cloned, split, pruned}. */
+int gsb_densify_and_prune(gsb_ctx* ctx, gsb_cloud* cloud, const double* grad_sum, const int32_t* count,
+                          double grad_threshold, double densify_size_ratio, int32_t n_target, double prune_opacity,
+                          uint64_t* rng_state, gsb_adam* adam, int32_t report[3]);
+
 /* ---- communicator: NCCL over NVLink for data-parallel training ----
  * libnccl.so.2 is loaded at run time (dlopen); without it gsb_comm_* return
  * GSB_ERR_NO_DEVICE. One rank per GPU. The 128-byte unique id is created on
@@ -298,6 +312,11 @@ typedef struct {
   double beta, aniso_ratio, opacity_l1_weight;
   double background[3];
   gsb_raster_config raster;
+  /* densification (trainer.hpp:35-42): after step t when densify_start <= t <=
+   * densify_stop, t > 0 and (t - densify_start) % densify_interval == 0;
+   * densify_interval <= 0 disables it */
+  int32_t densify_interval, densify_start, densify_stop, n_target;
+  double grad_threshold, densify_size_ratio, prune_opacity;
 } gsb_joint_config;
 void gsb_default_joint_config(gsb_joint_config* c);
 /* The training-view sequence of joint_optimize (pipelines.cpp:122-129: epoch
@@ -320,6 +339,8 @@ int gsb_joint_step(gsb_ctx* ctx, gsb_joint* j, int32_t steps);
 /* poses_out n_views x 12 (optional), steps done, per-step total / L1 traces
  * (iterations entries each, optional) */
 int gsb_joint_read(gsb_joint* j, double* poses_out, int64_t* steps_done, double* trace_total, double* trace_l1);
+/* current cloud size, densify_and_prune events so far, last event's {cloned, split, pruned} */
+int gsb_joint_info(gsb_joint* j, int64_t* n_gaussians, int32_t* densify_events, int32_t last_report[3]);
 
 #ifdef __cplusplus
 }

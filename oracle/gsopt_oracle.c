@@ -1409,6 +1409,150 @@ int32_t orc_estimate_pose(const orc_cloud* cloud, const double* image, double fx
   return steps_used;
 }
 
+/* trainer.cpp:134-142 (GradAccum::add) for one view: visible splats only. */
+void orc_grad_accum_add(const orc_render_out* out, const orc_grads* g, int32_t image_max_dim, double* grad_sum,
+                        int32_t* count) {
+  const double norm_scale = 0.5 * (double)image_max_dim;
+  for (int64_t s = 0; s < out->n_splats; ++s) {
+    const int32_t i = out->splats[s].gaussian;
+    const double x = g->d_mu2d[2 * i], y = g->d_mu2d[2 * i + 1];
+    grad_sum[i] += sqrt(x * x + y * y) * norm_scale;
+    count[i] += 1;
+  }
+}
+
+static int cmp_desc(const void* a, const void* b) {
+  const double x = *(const double*)a, y = *(const double*)b;
+  return x > y ? -1 : (x < y ? 1 : 0);
+}
+
+/* trainer.cpp:144-239 (densify_and_prune): clone small / split large
+ * Gaussians whose mean normalised screen gradient reaches grad_threshold
+ * (kept originals first, then clones and split children in index order,
+ * children drawn rot * (scale .* normal3) with log-scale - ln 1.6), then prune
+ * to opacity > max(prune_opacity, (n_target+1)-th largest opacity). `out` is
+ * allocated here (free with orc_cloud_free); *final_source (out->n entries,
+ * -1 = fresh) with orc_free. report = {cloned, split, pruned}. */
+void orc_densify_and_prune(const orc_cloud* cloud, const double* grad_sum, const int32_t* count,
+                           double grad_threshold, double size_ratio, int32_t n_target, double prune_opacity,
+                           orc_rng* rng, orc_cloud* out, int32_t** final_source, int32_t report[3]) {
+  const int64_t n = cloud->n;
+  const int basis = sh_count(cloud->sh_degree);
+  const int64_t shs = 3 * basis;
+  report[0] = report[1] = report[2] = 0;
+  double lo[3] = {cloud->means[0], cloud->means[1], cloud->means[2]}, hi[3] = {lo[0], lo[1], lo[2]};
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = fmin(lo[k], cloud->means[3 * i + k]);
+      hi[k] = fmax(hi[k], cloud->means[3 * i + k]);
+    }
+  const double dx = hi[0] - lo[0], dy = hi[1] - lo[1], dz = hi[2] - lo[2];
+  const double extent = sqrt(dx * dx + dy * dy + dz * dz);
+  const double size_threshold = size_ratio * fmax(extent, 1e-6);
+  uint8_t* action = (uint8_t*)calloc((size_t)n + 1, 1); /* 0 keep, 1 clone, 2 split */
+  int64_t extra = 0, kept = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (count[i] > 0) {
+      const double avg = grad_sum[i] / (double)count[i];
+      if (!(avg < grad_threshold)) {
+        double mx = exp(cloud->log_scales[3 * i]);
+        mx = fmax(mx, exp(cloud->log_scales[3 * i + 1]));
+        mx = fmax(mx, exp(cloud->log_scales[3 * i + 2]));
+        action[i] = mx <= size_threshold ? 1 : 2;
+      }
+    }
+    kept += action[i] != 2;
+    extra += action[i] == 1 ? 1 : (action[i] == 2 ? 2 : 0);
+  }
+  const int64_t total = kept + extra;
+  orc_cloud nx;
+  orc_cloud_alloc(&nx, total, cloud->sh_degree);
+  nx.active_sh_degree = cloud->active_sh_degree;
+  int32_t* src = (int32_t*)malloc(sizeof(int32_t) * (size_t)(total + 1));
+  int64_t j = 0;
+  #define ORC_APPEND(I, FRESH)                                                              \
+    do {                                                                                    \
+      memcpy(nx.rotations + 4 * j, cloud->rotations + 4 * (I), 4 * sizeof(double));         \
+      nx.opacity_logits[j] = cloud->opacity_logits[I];                                      \
+      memcpy(nx.sh + shs * j, cloud->sh + shs * (I), (size_t)shs * sizeof(double));         \
+      src[j] = (FRESH) ? -1 : (int32_t)(I);                                                 \
+    } while (0)
+  for (int64_t i = 0; i < n; ++i) {
+    if (action[i] == 2) continue;
+    memcpy(nx.means + 3 * j, cloud->means + 3 * i, 3 * sizeof(double));
+    memcpy(nx.log_scales + 3 * j, cloud->log_scales + 3 * i, 3 * sizeof(double));
+    ORC_APPEND(i, 0);
+    ++j;
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    if (action[i] == 1) {
+      memcpy(nx.means + 3 * j, cloud->means + 3 * i, 3 * sizeof(double));
+      memcpy(nx.log_scales + 3 * j, cloud->log_scales + 3 * i, 3 * sizeof(double));
+      ORC_APPEND(i, 1);
+      ++j;
+      ++report[0];
+    } else if (action[i] == 2) {
+      double R[9];
+      orc_quat_to_rotation(cloud->rotations + 4 * i, R);
+      const double sc[3] = {exp(cloud->log_scales[3 * i]), exp(cloud->log_scales[3 * i + 1]),
+                            exp(cloud->log_scales[3 * i + 2])};
+      for (int c = 0; c < 2; ++c) {
+        double nrm[3];
+        nrm[2] = orc_rng_normal(rng); /* Vec3(normal(), normal(), normal()): GCC draws right to left */
+        nrm[1] = orc_rng_normal(rng);
+        nrm[0] = orc_rng_normal(rng);
+        const double v[3] = {sc[0] * nrm[0], sc[1] * nrm[1], sc[2] * nrm[2]};
+        double smp[3];
+        mat3_vec(R, v, smp);
+        for (int k = 0; k < 3; ++k) {
+          nx.means[3 * j + k] = cloud->means[3 * i + k] + smp[k];
+          nx.log_scales[3 * j + k] = cloud->log_scales[3 * i + k] - log(1.6);
+        }
+        ORC_APPEND(i, 1);
+        ++j;
+      }
+      ++report[1];
+    }
+  }
+  #undef ORC_APPEND
+  double* op = (double*)malloc(sizeof(double) * (size_t)(total + 1));
+  for (int64_t i = 0; i < total; ++i) op[i] = sigmoid(nx.opacity_logits[i]);
+  double threshold = prune_opacity;
+  if (total > n_target) {
+    double* sorted = (double*)malloc(sizeof(double) * (size_t)total);
+    memcpy(sorted, op, sizeof(double) * (size_t)total);
+    qsort(sorted, (size_t)total, sizeof(double), cmp_desc);
+    threshold = fmax(threshold, sorted[n_target]); /* (n_target+1)-th largest */
+    free(sorted);
+  }
+  int64_t m = 0;
+  for (int64_t i = 0; i < total; ++i) m += op[i] > threshold;
+  orc_cloud_alloc(out, m, cloud->sh_degree);
+  out->active_sh_degree = cloud->active_sh_degree;
+  int32_t* fs = (int32_t*)malloc(sizeof(int32_t) * (size_t)(m + 1));
+  int64_t q = 0;
+  for (int64_t i = 0; i < total; ++i) {
+    if (!(op[i] > threshold)) {
+      ++report[2];
+      continue;
+    }
+    memcpy(out->means + 3 * q, nx.means + 3 * i, 3 * sizeof(double));
+    memcpy(out->rotations + 4 * q, nx.rotations + 4 * i, 4 * sizeof(double));
+    memcpy(out->log_scales + 3 * q, nx.log_scales + 3 * i, 3 * sizeof(double));
+    out->opacity_logits[q] = nx.opacity_logits[i];
+    memcpy(out->sh + shs * q, nx.sh + shs * i, (size_t)shs * sizeof(double));
+    fs[q] = src[i];
+    ++q;
+  }
+  *final_source = fs;
+  free(op);
+  free(src);
+  free(action);
+  orc_cloud_free(&nx);
+}
+
+void orc_free(void* p) { free(p); }
+
 /* pipelines.cpp:122-129: the training-view sequence. `order` starts as iota
  * and is re-shuffled IN PLACE (Fisher-Yates from the back with
  * rng.uniform_int(0, i)) at the start of every epoch; the sequence is the
@@ -1430,46 +1574,87 @@ void orc_joint_schedule(orc_rng* rng, int32_t n_views, int64_t count, int32_t* s
   free(order);
 }
 
-/* pipelines.cpp:96-216 (joint_optimize) with densification off and without
- * the ground-truth pose statistics, generalised to `slots` training views per
- * step (the data-parallel semantics of the B200 build): step t
- * renders views seq[t*slots .. t*slots+slots-1] (orc_joint_schedule), the
- * Adam gradient is the MEAN of the slots' render gradients plus the
- * regularisers (anisotropy 217-244, opacity L1 246-257, both added once, on
- * the pre-step parameters), and the slots' pose steps are applied in slot
- * order with each view's own PoseAdam. slots == 1 is the reference loop
- * exactly. Returns 0, or 10 (ErrorCode::diverged + 1) at a non-finite total
- * loss (160-162). trace_total / trace_l1 (iterations, nullable) receive the
- * step's mean total loss and mean L1. poses: n_views x 12, updated in place. */
+/* Epoch-shuffle state of pipelines.cpp:122-129, consumed lazily so that its
+ * draws interleave with densify_and_prune's exactly as in the reference. */
+typedef struct {
+  int32_t n, *order;
+  int64_t next; /* next slot index to produce */
+} orc_sched;
+
+static int32_t sched_slot(orc_sched* sc, orc_rng* rng) {
+  const int64_t k = sc->next++;
+  if (k % sc->n == 0)
+    for (int32_t i = sc->n - 1; i > 0; --i) {
+      const int32_t j = (int32_t)orc_rng_uniform_int(rng, 0, i);
+      const int32_t tmp = sc->order[i];
+      sc->order[i] = sc->order[j];
+      sc->order[j] = tmp;
+    }
+  return sc->order[k % sc->n];
+}
+
+/* CloudAdam::remap (trainer.cpp:101-132) for one flat AdamState of `width`
+ * entries per Gaussian. */
+static void adam_remap(orc_adam_state* s, const int32_t* src, int64_t n_new, int64_t width) {
+  if (!s->m) return;
+  double* m = (double*)calloc((size_t)(n_new * width + 1), sizeof(double));
+  double* v = (double*)calloc((size_t)(n_new * width + 1), sizeof(double));
+  for (int64_t j = 0; j < n_new; ++j) {
+    if (src[j] < 0) continue;
+    memcpy(m + j * width, s->m + (int64_t)src[j] * width, sizeof(double) * (size_t)width);
+    memcpy(v + j * width, s->v + (int64_t)src[j] * width, sizeof(double) * (size_t)width);
+  }
+  free(s->m);
+  free(s->v);
+  s->m = m;
+  s->v = v;
+  s->n = n_new * width;
+}
+
+/* pipelines.cpp:96-216 (joint_optimize) without the ground-truth pose
+ * statistics, generalised to `slots` training views per step (the
+ * data-parallel semantics of the B200 build): step t renders the
+ * next `slots` views of the epoch-shuffle sequence, the Adam gradient is the
+ * MEAN of the slots' render gradients plus the regularisers (anisotropy
+ * 217-244, opacity L1 246-257, both added once, on the pre-step parameters),
+ * GradAccum adds every slot's view (trainer.cpp:134-142), the slots' pose
+ * steps are applied in slot order with each view's own PoseAdam, and
+ * densify_and_prune runs after step t when t is a densification step
+ * (182-186). slots == 1 is the reference loop exactly. Returns 0, or 10
+ * (ErrorCode::diverged + 1) at a non-finite total loss (160-162).
+ * trace_total / trace_l1 (iterations, nullable) receive the step's mean total
+ * loss and mean L1. poses: n_views x 12, updated in place. */
 int32_t orc_joint_optimize(orc_cloud* cloud, const double* const* images, int32_t n_views, double fx, double fy,
                            double cx, double cy, int32_t w, int32_t h, double* poses, const orc_joint_cfg* cfg,
                            int32_t slots, orc_rng* rng, double* trace_total, double* trace_l1) {
-  const int64_t n = cloud->n;
   const int32_t iters = cfg->iterations;
-  int32_t* seq = (int32_t*)malloc(sizeof(int32_t) * ((size_t)iters * slots + 1));
-  orc_joint_schedule(rng, n_views, (int64_t)iters * slots, seq);
+  orc_sched sc;
+  sc.n = n_views;
+  sc.next = 0;
+  sc.order = (int32_t*)malloc(sizeof(int32_t) * (size_t)n_views);
+  for (int32_t i = 0; i < n_views; ++i) sc.order[i] = i;
+  int32_t* vs = (int32_t*)malloc(sizeof(int32_t) * (size_t)slots);
   orc_adam_state st[5];
   memset(st, 0, sizeof st);
   orc_pose_adam* pad = (orc_pose_adam*)calloc((size_t)n_views, sizeof(orc_pose_adam));
   double* d_image = (double*)malloc(sizeof(double) * (size_t)w * h * 3);
   double* dpose = (double*)malloc(sizeof(double) * 6 * (size_t)slots);
-  orc_grads acc;
-  orc_grads_alloc(&acc, cloud);
-  const int basis = sh_count(cloud->sh_degree);
+  double* acc_sum = (double*)calloc((size_t)cloud->n + 1, sizeof(double));
+  int32_t* acc_cnt = (int32_t*)calloc((size_t)cloud->n + 1, sizeof(int32_t));
   int32_t status = 0;
   for (int32_t t = 0; t < iters && status == 0; ++t) {
+    const int64_t n = cloud->n;
+    const int basis = sh_count(cloud->sh_degree);
+    for (int32_t s = 0; s < slots; ++s) vs[s] = sched_slot(&sc, rng);
     if (cfg->sh_degree_interval > 0 && t > 0 && t % cfg->sh_degree_interval == 0) {
       const int32_t a = cloud->active_sh_degree + 1;
       cloud->active_sh_degree = a < cfg->sh_degree ? a : cfg->sh_degree;
     }
-    memset(acc.d_means, 0, sizeof(double) * 3 * n);
-    memset(acc.d_rotations, 0, sizeof(double) * 4 * n);
-    memset(acc.d_log_scales, 0, sizeof(double) * 3 * n);
-    memset(acc.d_opacity_logits, 0, sizeof(double) * n);
-    memset(acc.d_sh, 0, sizeof(double) * 3 * basis * n);
+    orc_grads acc;
+    orc_grads_alloc(&acc, cloud);
     double rgb_sum = 0.0, l1_sum = 0.0;
     for (int32_t s = 0; s < slots; ++s) {
-      const int32_t v = seq[(int64_t)t * slots + s];
+      const int32_t v = vs[s];
       orc_camera cam;
       cam.fx = fx; cam.fy = fy; cam.cx = cx; cam.cy = cy; cam.width = w; cam.height = h;
       for (int r = 0; r < 3; ++r) {
@@ -1488,6 +1673,7 @@ int32_t orc_joint_optimize(orc_cloud* cloud, const double* const* images, int32_
       for (int64_t k = 0; k < n; ++k) acc.d_opacity_logits[k] += g.d_opacity_logits[k] * inv;
       for (int64_t k = 0; k < 3 * basis * n; ++k) acc.d_sh[k] += g.d_sh[k] * inv;
       memcpy(dpose + 6 * s, g.d_pose, sizeof(double) * 6);
+      orc_grad_accum_add(out, &g, w > h ? w : h, acc_sum, acc_cnt);
       orc_grads_free(&g);
       orc_render_free(out);
     }
@@ -1512,6 +1698,7 @@ int32_t orc_joint_optimize(orc_cloud* cloud, const double* const* images, int32_
     if (trace_l1) trace_l1[t] = l1_sum / slots;
     if (!isfinite(total)) {
       status = 10;
+      orc_grads_free(&acc);
       break;
     }
     double lrs[6];
@@ -1522,10 +1709,11 @@ int32_t orc_joint_optimize(orc_cloud* cloud, const double* const* images, int32_
     lrs[4] = cfg->sh_dc_lr;
     lrs[5] = cfg->sh_rest_lr;
     orc_cloud_adam_step(cloud, &acc, st, lrs);
+    orc_grads_free(&acc);
     if (cfg->optimize_poses) {
       const double cam_lr = orc_schedule(0, cfg->cam_lr_start, cfg->cam_lr_end, t, iters);
       for (int32_t s = 0; s < slots; ++s) {
-        const int32_t v = seq[(int64_t)t * slots + s];
+        const int32_t v = vs[s];
         double R[9], tt[3], Rn[9], tn[3], applied[6];
         for (int r = 0; r < 3; ++r) {
           for (int c = 0; c < 3; ++c) R[r * 3 + c] = poses[12 * v + r * 4 + c];
@@ -1538,8 +1726,28 @@ int32_t orc_joint_optimize(orc_cloud* cloud, const double* const* images, int32_
         }
       }
     }
+    if (cfg->densify_interval > 0 && t >= cfg->densify_start && t <= cfg->densify_stop && t > 0 &&
+        (t - cfg->densify_start) % cfg->densify_interval == 0) {
+      orc_cloud out;
+      int32_t* src = NULL;
+      int32_t rep[3];
+      orc_densify_and_prune(cloud, acc_sum, acc_cnt, cfg->grad_threshold, cfg->densify_size_ratio, cfg->n_target,
+                            cfg->prune_opacity, rng, &out, &src, rep);
+      const int64_t nn = out.n, bw = 3 * (int64_t)sh_count(cloud->sh_degree);
+      adam_remap(&st[0], src, nn, 3);
+      adam_remap(&st[1], src, nn, 4);
+      adam_remap(&st[2], src, nn, 3);
+      adam_remap(&st[3], src, nn, 1);
+      adam_remap(&st[4], src, nn, bw);
+      free(src);
+      orc_cloud_free(cloud);
+      *cloud = out;
+      free(acc_sum);
+      free(acc_cnt);
+      acc_sum = (double*)calloc((size_t)nn + 1, sizeof(double));
+      acc_cnt = (int32_t*)calloc((size_t)nn + 1, sizeof(int32_t));
+    }
   }
-  orc_grads_free(&acc);
   for (int k = 0; k < 5; ++k) {
     free(st[k].m);
     free(st[k].v);
@@ -1547,7 +1755,10 @@ int32_t orc_joint_optimize(orc_cloud* cloud, const double* const* images, int32_
   free(pad);
   free(d_image);
   free(dpose);
-  free(seq);
+  free(vs);
+  free(sc.order);
+  free(acc_sum);
+  free(acc_cnt);
   return status;
 }
 

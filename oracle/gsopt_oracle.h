@@ -172,6 +172,15 @@ int32_t orc_estimate_pose(const orc_cloud* cloud, const double* image, double fx
                           double R_out[9], double t_out[3], double* final_loss, int32_t* converged,
                           double* trace_pose, double* trace_loss, double* trace_dpose);
 
+/* trainer.cpp:134-142 GradAccum::add for one rendered view */
+void orc_grad_accum_add(const orc_render_out* out, const orc_grads* g, int32_t image_max_dim, double* grad_sum,
+                        int32_t* count);
+/* trainer.cpp:144-239; `out` allocated inside (orc_cloud_free), *final_source
+ * (out->n, -1 = fresh) freed with orc_free; report = {cloned, split, pruned} */
+void orc_densify_and_prune(const orc_cloud* cloud, const double* grad_sum, const int32_t* count,
+                           double grad_threshold, double size_ratio, int32_t n_target, double prune_opacity,
+                           orc_rng* rng, orc_cloud* out, int32_t** final_source, int32_t report[3]);
+void orc_free(void* p);
 /* pipelines.cpp:122-129 epoch shuffles -> view sequence (count entries) */
 void orc_joint_schedule(orc_rng* rng, int32_t n_views, int64_t count, int32_t* seq);
 /* TrainConfig fields joint_optimize reads (trainer.hpp:21-60, losses.hpp:15-19) */
@@ -182,9 +191,13 @@ typedef struct {
   double beta, aniso_ratio, opacity_l1_weight;
   double background[3];
   orc_raster_config raster;
+  /* densification (trainer.hpp:35-42); densify_interval <= 0 disables */
+  int32_t densify_interval, densify_start, densify_stop, n_target;
+  double grad_threshold, densify_size_ratio, prune_opacity;
 } orc_joint_cfg;
-/* pipelines.cpp:96-216 without densify / gt stats; `slots` views per step
- * (1 = the reference loop). Returns 0 or 10 (diverged). */
+/* pipelines.cpp:96-216 without gt stats; `slots` views per step (1 = the
+ * reference loop). The cloud may change size (densify_and_prune): it is
+ * reallocated in place (orc_cloud_alloc'ed memory). Returns 0 or 10 (diverged). */
 int32_t orc_joint_optimize(orc_cloud* cloud, const double* const* images, int32_t n_views, double fx, double fy,
                            double cx, double cy, int32_t w, int32_t h, double* poses, const orc_joint_cfg* cfg,
                            int32_t slots, orc_rng* rng, double* trace_total, double* trace_l1);

@@ -86,7 +86,9 @@ class JointCfg(C.Structure):
                 ("sh_rest_lr", C.c_double), ("opacity_l1_steps", C.c_int32), ("sh_degree", C.c_int32),
                 ("sh_degree_interval", C.c_int32), ("optimize_poses", C.c_int32), ("beta", C.c_double),
                 ("aniso_ratio", C.c_double), ("opacity_l1_weight", C.c_double), ("background", C.c_double * 3),
-                ("raster", RasterConfig)]
+                ("raster", RasterConfig), ("densify_interval", C.c_int32), ("densify_start", C.c_int32),
+                ("densify_stop", C.c_int32), ("n_target", C.c_int32), ("grad_threshold", C.c_double),
+                ("densify_size_ratio", C.c_double), ("prune_opacity", C.c_double)]
 
 
 class PoseCfg(C.Structure):
@@ -153,6 +155,8 @@ def lib():
             "orc_count_work": (None, [P(RenderOut), vp, vp]),
             "orc_joint_schedule": (None, [P(Rng), i32, i64, vp]),
             "orc_cloud_adam_step": (None, [P(Cloud), P(Grads), vp, vp]),
+            "orc_densify_and_prune": (None, [P(Cloud), vp, vp, d, d, i32, d, P(Rng), P(Cloud), vp, vp]),
+            "orc_free": (None, [vp]),
             "orc_joint_optimize": (i32, [P(Cloud), vp, i32, d, d, d, d, i32, i32, vp, P(JointCfg), i32, P(Rng),
                                          vp, vp]),
         }
@@ -535,6 +539,24 @@ class CloudAdam:
             hc.means, hc.rotations, hc.log_scales, hc.opacity_logits, hc.sh))], hc.sh_degree, hc.active_sh_degree)
 
 
+def densify_and_prune(cloud: HostCloud, grad_sum, count, grad_threshold=2e-4, size_ratio=0.01, n_target=256000,
+                      prune_opacity=0.005, rng: Rng | None = None):
+    """trainer.cpp:144-239. Returns (new HostCloud, final_source int32[n'], (cloned, split, pruned))."""
+    cv = cloud.c()
+    gs = np.ascontiguousarray(grad_sum, np.float64)
+    ct = np.ascontiguousarray(count, np.int32)
+    out = Cloud()
+    fs = C.POINTER(C.c_int32)()
+    rep = np.zeros(3, np.int32)
+    lib().orc_densify_and_prune(cv.ref(), _p(gs), _p(ct), grad_threshold, size_ratio, n_target, prune_opacity,
+                                C.byref(rng), C.byref(out), C.cast(C.byref(fs), C.c_void_p), _p(rep))
+    res = _from_c_cloud(out)
+    src = np.ctypeslib.as_array(fs, shape=(max(out.n, 1),))[:out.n].copy() if out.n else np.zeros(0, np.int32)
+    lib().orc_free(C.cast(fs, C.c_void_p))
+    lib().orc_cloud_free(C.byref(out))
+    return res, src, tuple(int(x) for x in rep)
+
+
 def joint_config(iterations, **kw) -> JointCfg:
     """TrainConfig defaults (trainer.hpp:21-60, losses.hpp:15-19) with overrides."""
     c = JointCfg()
@@ -544,6 +566,8 @@ def joint_config(iterations, **kw) -> JointCfg:
     c.opacity_l1_steps, c.sh_degree, c.sh_degree_interval, c.optimize_poses = 10000, 3, 1000, 1
     c.beta, c.aniso_ratio, c.opacity_l1_weight = 0.2, 10.0, 0.01
     c.raster = default_raster_config()
+    c.densify_interval, c.densify_start, c.densify_stop, c.n_target = 100, 500, 15000, 256000
+    c.grad_threshold, c.densify_size_ratio, c.prune_opacity = 2e-4, 0.01, 0.005
     for k, v in kw.items():
         if k == "background":
             for i in range(3):
@@ -560,19 +584,31 @@ def joint_schedule(rng: Rng, n_views: int, count: int) -> np.ndarray:
     return out
 
 
+def _alloc_c_cloud(hc: HostCloud) -> Cloud:
+    """A malloc-backed copy (orc_cloud_alloc) the oracle may reallocate."""
+    cc = Cloud()
+    lib().orc_cloud_alloc(C.byref(cc), hc.n, hc.sh_degree)
+    cc.active_sh_degree = hc.active_sh_degree
+    for name, arr in (("means", hc.means), ("rotations", hc.rotations), ("log_scales", hc.log_scales),
+                      ("opacity_logits", hc.opacity_logits), ("sh", hc.sh)):
+        a = np.ascontiguousarray(arr, np.float64).reshape(-1)
+        if a.size:
+            C.memmove(getattr(cc, name), a.ctypes.data, a.nbytes)
+    return cc
+
+
 def joint_optimize(cloud: HostCloud, images, intr, width, height, poses, cfg: JointCfg, slots: int, rng: Rng):
-    """pipelines.cpp:96-216 (densify off), `slots` views per step. Returns
+    """pipelines.cpp:96-216 (+ densify_and_prune), `slots` views per step. Returns
     (status, cloud, poses, trace_total, trace_l1); cloud/poses are new arrays."""
-    cv = cloud.copy().c()
+    cc = _alloc_c_cloud(cloud)
     imgs = [np.ascontiguousarray(im, np.float64) for im in images]
     ptrs = (C.c_void_p * len(imgs))(*[im.ctypes.data for im in imgs])
     P = np.ascontiguousarray(np.asarray(poses, np.float64).reshape(-1, 12)).copy()
     tt, tl = np.zeros(cfg.iterations), np.zeros(cfg.iterations)
-    st = lib().orc_joint_optimize(cv.ref(), C.cast(ptrs, C.c_void_p), len(imgs), intr[0], intr[1], intr[2],
+    st = lib().orc_joint_optimize(C.byref(cc), C.cast(ptrs, C.c_void_p), len(imgs), intr[0], intr[1], intr[2],
                                   intr[3], width, height, _p(P), C.byref(cfg), slots, C.byref(rng), _p(tt), _p(tl))
-    out = HostCloud(*[b.reshape(a.shape) for b, a in zip(cv.bufs, (cloud.means, cloud.rotations, cloud.log_scales,
-                                                                   cloud.opacity_logits, cloud.sh))],
-                    cloud.sh_degree, cv.s.active_sh_degree)
+    out = _from_c_cloud(cc)
+    lib().orc_cloud_free(C.byref(cc))
     return st, out, P, tt, tl
 
 

@@ -90,6 +90,26 @@ size_t joint_xchg_doubles();
 void joint_state_read(const void* host, int64_t* t, int32_t* diverged, int32_t* aborted, double* k_max,
                       int32_t* tile);
 void joint_state_clear_abort(void* host);
+int launch_grad_accum(cudaStream_t st, const float* grads, int nplanes, int64_t n_pad, int64_t n,
+                      const uint32_t* cnt_g, double scale, double* gsum, int32_t* gcnt);
+int densify_bbox_blocks();
+int launch_densify_bbox(cudaStream_t st, const float* params, int64_t n, int64_t n_pad, float* out);
+int launch_densify_action(cudaStream_t st, const float* params, int64_t n, int64_t n_pad, const double* gsum,
+                          const int32_t* gcnt, double grad_threshold, double size_threshold, uint32_t* keep,
+                          uint32_t* extra, uint32_t* split);
+int launch_densify_build(cudaStream_t st, const float* params, int64_t n, int64_t n_pad, int nplanes,
+                         const uint32_t* keep, const uint32_t* keep_pos, const uint32_t* extra,
+                         const uint32_t* extra_pos, const uint32_t* split_rank, const double* normals,
+                         uint32_t n_keep, float* out, int64_t n_pad_o, int32_t* src_o);
+int launch_densify_logit_keys(cudaStream_t st, const float* params, int64_t n, int64_t n_pad, uint32_t* keys,
+                              uint32_t* vals);
+int launch_densify_prune_flag(cudaStream_t st, const float* params, int64_t n, int64_t n_pad, double threshold,
+                              uint32_t* flag);
+int launch_densify_gather(cudaStream_t st, const float* in, int64_t n, int64_t n_pad_i, int nplanes,
+                          const uint32_t* flag, const uint32_t* pos, const int32_t* src_i, float* out,
+                          int64_t n_pad_o, int32_t* src_o);
+int launch_densify_adam_remap(cudaStream_t st, const float* m, const float* v, int64_t n_pad_i, int nplanes,
+                              const int32_t* src, int64_t n_o, int64_t n_pad_o, float* m_o, float* v_o);
 int launch_cloud_adam(cudaStream_t st, float* params, const float* grads, float* m, float* v, int64_t n,
                       int64_t n_pad, int sh_degree, const double lrs[6], const int64_t steps[5]);
 
@@ -1871,6 +1891,197 @@ int gsb_estimate_poses(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* const* targets
 
 }  // extern "C"
 
+
+// ------------------------------------------------------ densify_and_prune
+namespace gsb {
+
+static int64_t pad_n(int64_t n) { return std::max<int64_t>(32, (n + 31) / 32 * 32); }
+
+struct DensifyParams {
+  double grad_threshold, size_ratio, prune_opacity;
+  int32_t n_target;
+};
+
+// trainer.cpp:144-239 on the device (k_densify.cu); d_gsum / d_gcnt are the
+// GradAccum arrays (device, cloud->n). Rebuilds cloud->params (new n, n_pad)
+// and remaps the Adam moment planes (m, v: [planes][n_pad], may be null).
+static int densify_device(gsb_ctx* ctx, gsb_cloud* cloud, const double* d_gsum, const int32_t* d_gcnt,
+                          const DensifyParams& p, uint64_t* rng_state, DevBuf* adam_m, DevBuf* adam_v,
+                          int32_t report[3]) {
+  cudaStream_t st = ctx->stream;
+  const int64_t n = cloud->n, np = cloud->n_pad;
+  const int nplanes = num_planes(cloud->sh_degree);
+  report[0] = report[1] = report[2] = 0;
+  if (n == 0) return GSB_OK;
+  // bounding box -> extent -> size threshold (trainer.cpp:148-155), exact
+  DevBuf bb;
+  GSB_CUDA(bb.reserve(sizeof(float) * 6 * densify_bbox_blocks()));
+  if (int r = launch_densify_bbox(st, cloud->params.as<float>(), n, np, bb.as<float>())) return r;
+  std::vector<float> hb(6 * densify_bbox_blocks());
+  GSB_CUDA(cudaMemcpyAsync(hb.data(), bb.p, sizeof(float) * hb.size(), cudaMemcpyDeviceToHost, st));
+  GSB_CUDA(cudaStreamSynchronize(st));
+  double lo[3], hi[3];
+  for (int k = 0; k < 3; ++k) {
+    lo[k] = hb[k];
+    hi[k] = hb[3 + k];
+    for (int b = 1; b < densify_bbox_blocks(); ++b) {
+      lo[k] = std::min(lo[k], (double)hb[6 * b + k]);
+      hi[k] = std::max(hi[k], (double)hb[6 * b + 3 + k]);
+    }
+  }
+  const double dx = hi[0] - lo[0], dy = hi[1] - lo[1], dz = hi[2] - lo[2];
+  const double extent = std::sqrt(dx * dx + dy * dy + dz * dz);
+  const double size_threshold = p.size_ratio * std::max(extent, 1e-6);
+  // actions + positions
+  DevBuf keep, extra, split, keep_pos, extra_pos, split_rank, tmp, tot;
+  GSB_CUDA(keep.reserve(sizeof(uint32_t) * n));
+  GSB_CUDA(extra.reserve(sizeof(uint32_t) * n));
+  GSB_CUDA(split.reserve(sizeof(uint32_t) * n));
+  GSB_CUDA(keep_pos.reserve(sizeof(uint32_t) * n));
+  GSB_CUDA(extra_pos.reserve(sizeof(uint32_t) * n));
+  GSB_CUDA(split_rank.reserve(sizeof(uint32_t) * n));
+  GSB_CUDA(tmp.reserve(sizeof(uint32_t) * (scan_onepass_words(n) + 64)));
+  GSB_CUDA(tot.reserve(sizeof(uint32_t) * 4));
+  if (int r = launch_densify_action(st, cloud->params.as<float>(), n, np, d_gsum, d_gcnt, p.grad_threshold,
+                                    size_threshold, keep.as<uint32_t>(), extra.as<uint32_t>(), split.as<uint32_t>()))
+    return r;
+  int64_t launches = 0;
+  uint32_t* t = tot.as<uint32_t>();
+  if (int r = scan_onepass(st, keep.as<uint32_t>(), n, nullptr, false, keep_pos.as<uint32_t>(), tmp.as<uint32_t>(),
+                           t + 0, &launches))
+    return r;
+  if (int r = scan_onepass(st, extra.as<uint32_t>(), n, nullptr, false, extra_pos.as<uint32_t>(), tmp.as<uint32_t>(),
+                           t + 1, &launches))
+    return r;
+  if (int r = scan_onepass(st, split.as<uint32_t>(), n, nullptr, false, split_rank.as<uint32_t>(),
+                           tmp.as<uint32_t>(), t + 2, &launches))
+    return r;
+  uint32_t ht[3];
+  GSB_CUDA(cudaMemcpyAsync(ht, t, sizeof ht, cudaMemcpyDeviceToHost, st));
+  GSB_CUDA(cudaStreamSynchronize(st));
+  const uint32_t n_keep = ht[0], n_extra = ht[1], n_split = ht[2];
+  report[1] = (int32_t)n_split;
+  report[0] = (int32_t)(n_extra - 2 * n_split);
+  // split children's normals from the run's Rng, in the reference's draw order
+  std::vector<double> nh(6 * (size_t)n_split + 1);
+  if (int r = gsb_rng_child_normals(rng_state, 2 * (int64_t)n_split, nh.data())) return r;
+  DevBuf normals;
+  GSB_CUDA(normals.reserve(sizeof(double) * nh.size()));
+  GSB_CUDA(cudaMemcpyAsync(normals.p, nh.data(), sizeof(double) * nh.size(), cudaMemcpyHostToDevice, st));
+  // post-densify population
+  const int64_t total = (int64_t)n_keep + n_extra, np_t = pad_n(total);
+  DevBuf next, src_next;
+  GSB_CUDA(next.reserve(sizeof(float) * nplanes * np_t));
+  GSB_CUDA(src_next.reserve(sizeof(int32_t) * std::max<int64_t>(total, 1)));
+  GSB_CUDA(cudaMemsetAsync(next.p, 0, sizeof(float) * nplanes * np_t, st));
+  if (int r = launch_densify_build(st, cloud->params.as<float>(), n, np, nplanes, keep.as<uint32_t>(),
+                                   keep_pos.as<uint32_t>(), extra.as<uint32_t>(), extra_pos.as<uint32_t>(),
+                                   split_rank.as<uint32_t>(), normals.as<double>(), n_keep, next.as<float>(), np_t,
+                                   src_next.as<int32_t>()))
+    return r;
+  // prune threshold: max(prune_opacity, (n_target+1)-th largest opacity)
+  double threshold = p.prune_opacity;
+  if (total > p.n_target && p.n_target >= 0) {
+    DevBuf kv[2][2], hist;
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) GSB_CUDA(kv[a][b].reserve(sizeof(uint32_t) * total));
+    GSB_CUDA(hist.reserve(sizeof(uint32_t) * (radix_hist_words(total, 32) + 64)));
+    if (int r = launch_densify_logit_keys(st, next.as<float>(), total, np_t, kv[0][0].as<uint32_t>(),
+                                          kv[1][0].as<uint32_t>()))
+      return r;
+    uint32_t* keys[2] = {kv[0][0].as<uint32_t>(), kv[0][1].as<uint32_t>()};
+    uint32_t* vals[2] = {kv[1][0].as<uint32_t>(), kv[1][1].as<uint32_t>()};
+    int sel = 0;
+    if (int r = radix_sort_pairs(st, keys, vals, total, nullptr, 32, hist.as<uint32_t>(), &sel, &launches)) return r;
+    uint32_t kbits = 0;  // ascending: the (n_target+1)-th largest sits at total - 1 - n_target
+    GSB_CUDA(cudaMemcpyAsync(&kbits, keys[sel] + (total - 1 - p.n_target), sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                             st));
+    GSB_CUDA(cudaStreamSynchronize(st));
+    const uint32_t b = (kbits & 0x80000000u) ? (kbits & 0x7fffffffu) : ~kbits;
+    float logit;
+    std::memcpy(&logit, &b, sizeof logit);
+    threshold = std::max(threshold, 1.0 / (1.0 + std::exp(-(double)logit)));
+  }
+  DevBuf flag, pos;
+  GSB_CUDA(flag.reserve(sizeof(uint32_t) * total));
+  GSB_CUDA(pos.reserve(sizeof(uint32_t) * total));
+  if (int r = launch_densify_prune_flag(st, next.as<float>(), total, np_t, threshold, flag.as<uint32_t>())) return r;
+  GSB_CUDA(tmp.reserve(sizeof(uint32_t) * (scan_onepass_words(total) + 64)));
+  if (int r = scan_onepass(st, flag.as<uint32_t>(), total, nullptr, false, pos.as<uint32_t>(), tmp.as<uint32_t>(),
+                           t + 3, &launches))
+    return r;
+  uint32_t m = 0;
+  GSB_CUDA(cudaMemcpyAsync(&m, t + 3, sizeof m, cudaMemcpyDeviceToHost, st));
+  GSB_CUDA(cudaStreamSynchronize(st));
+  report[2] = (int32_t)(total - m);
+  const int64_t np_m = pad_n(m);
+  DevBuf fin, src_fin;
+  GSB_CUDA(fin.reserve(sizeof(float) * nplanes * np_m));
+  GSB_CUDA(src_fin.reserve(sizeof(int32_t) * std::max<int64_t>(m, 1)));
+  GSB_CUDA(cudaMemsetAsync(fin.p, 0, sizeof(float) * nplanes * np_m, st));
+  if (int r = launch_densify_gather(st, next.as<float>(), total, np_t, nplanes, flag.as<uint32_t>(),
+                                    pos.as<uint32_t>(), src_next.as<int32_t>(), fin.as<float>(), np_m,
+                                    src_fin.as<int32_t>()))
+    return r;
+  if (adam_m && adam_v && adam_m->p && adam_v->p) {
+    DevBuf mo, vo;
+    GSB_CUDA(mo.reserve(sizeof(float) * nplanes * np_m));
+    GSB_CUDA(vo.reserve(sizeof(float) * nplanes * np_m));
+    GSB_CUDA(cudaMemsetAsync(mo.p, 0, sizeof(float) * nplanes * np_m, st));
+    GSB_CUDA(cudaMemsetAsync(vo.p, 0, sizeof(float) * nplanes * np_m, st));
+    if (int r = launch_densify_adam_remap(st, adam_m->as<float>(), adam_v->as<float>(), np, nplanes,
+                                          src_fin.as<int32_t>(), m, np_m, mo.as<float>(), vo.as<float>()))
+      return r;
+    GSB_CUDA(cudaStreamSynchronize(st));
+    std::swap(*adam_m, mo);
+    std::swap(*adam_v, vo);
+    mo.release();
+    vo.release();
+  }
+  GSB_CUDA(cudaStreamSynchronize(st));
+  std::swap(cloud->params, fin);
+  fin.release();
+  cloud->n = m;
+  cloud->n_pad = np_m;
+  ++cloud->version;
+  ctx->launches += launches + 7;
+  DevBuf* tmps[] = {&bb, &keep, &extra, &split, &keep_pos, &extra_pos, &split_rank, &tmp, &tot, &normals, &next,
+                    &src_next, &flag, &pos, &src_fin};
+  for (DevBuf* b : tmps) b->release();
+  return GSB_OK;
+}
+
+}  // namespace gsb
+
+extern "C" {
+
+int gsb_densify_and_prune(gsb_ctx* ctx, gsb_cloud* cloud, const double* grad_sum, const int32_t* count,
+                          double grad_threshold, double densify_size_ratio, int32_t n_target, double prune_opacity,
+                          uint64_t* rng_state, gsb_adam* adam, int32_t report[3]) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!cloud || !grad_sum || !count || !rng_state || !report) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  if (adam && (adam->n != cloud->n || adam->n_pad != cloud->n_pad))
+    return fail(GSB_ERR_DIMENSION_MISMATCH, "adam state does not match the cloud");
+  const int64_t n = cloud->n;
+  DevBuf gs, gc;
+  GSB_CUDA(gs.reserve(sizeof(double) * std::max<int64_t>(n, 1)));
+  GSB_CUDA(gc.reserve(sizeof(int32_t) * std::max<int64_t>(n, 1)));
+  GSB_CUDA(cudaMemcpyAsync(gs.p, grad_sum, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  GSB_CUDA(cudaMemcpyAsync(gc.p, count, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  DensifyParams p{grad_threshold, densify_size_ratio, prune_opacity, n_target};
+  int r = densify_device(ctx, cloud, gs.as<double>(), gc.as<int32_t>(), p, rng_state, adam ? &adam->m : nullptr,
+                         adam ? &adam->v : nullptr, report);
+  if (!r && adam) {
+    adam->n = cloud->n;
+    adam->n_pad = cloud->n_pad;
+  }
+  gs.release();
+  gc.release();
+  return r;
+}
+
+}  // extern "C"
+
 // ------------------------------------------------------------ NCCL (dlopen)
 namespace gsb {
 
@@ -1988,6 +2199,13 @@ void gsb_default_joint_config(gsb_joint_config* c) {  // trainer.hpp:21-60, loss
   c->opacity_l1_weight = 0.01;
   c->background[0] = c->background[1] = c->background[2] = 0.0;
   gsb_default_raster_config(&c->raster);
+  c->densify_interval = 100;
+  c->densify_start = 500;
+  c->densify_stop = 15000;
+  c->n_target = 256000;
+  c->grad_threshold = 2e-4;
+  c->densify_size_ratio = 0.01;
+  c->prune_opacity = 0.005;
 }
 
 }  // extern "C"
@@ -2019,9 +2237,66 @@ struct gsb_joint {
   int graph_active = -1;
   int64_t t = 0;  // steps completed as of the last sync
   int64_t sh_grown_t = -1;  // step at which the active SH degree last grew
+  // training-view sequence, produced lazily so its shuffles interleave with
+  // densify_and_prune's draws from the same Rng (pipelines.cpp:123-129, 182-186)
+  uint64_t rng_state = 0;
+  std::vector<int32_t> order;
+  int64_t seq_next = 0;
+  // GradAccum (trainer.cpp:134-142) on the device + densification bookkeeping
+  DevBuf acc_sum, acc_cnt;
+  const void* graph_params = nullptr;
+  int64_t graph_n = -1;
+  int32_t densify_report[3] = {0, 0, 0};
+  int32_t densify_events = 0;
 };
 
 namespace gsb {
+
+static bool joint_densify_due(const gsb_joint* j, int64_t t) {  // after step t (pipelines.cpp:182-183)
+  const gsb_joint_config& c = j->cfg;
+  return c.densify_interval > 0 && t >= c.densify_start && t <= c.densify_stop && t > 0 &&
+         (t - c.densify_start) % c.densify_interval == 0;
+}
+
+// Extends the device view sequence to `upto` slots (epoch shuffles drawn now,
+// i.e. before any later densify draws, as in the reference loop).
+static int joint_sched_extend(gsb_ctx* ctx, gsb_joint* j, int64_t upto) {
+  const int64_t cap = (int64_t)std::max(j->cfg.iterations, 1) * j->ctl.slots;
+  upto = std::min(upto, cap);
+  if (upto <= j->seq_next) return GSB_OK;
+  std::vector<int32_t> add;
+  add.reserve((size_t)(upto - j->seq_next));
+  for (int64_t k = j->seq_next; k < upto; ++k) {
+    if (k % j->n_views == 0)
+      if (int r = gsb_rng_shuffle(&j->rng_state, j->n_views, j->order.data())) return r;
+    add.push_back(j->order[k % j->n_views]);
+  }
+  GSB_CUDA(cudaMemcpyAsync(j->seq.as<int32_t>() + j->seq_next, add.data(), sizeof(int32_t) * add.size(),
+                           cudaMemcpyHostToDevice, ctx->stream));
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));  // host staging vector
+  j->seq_next = upto;
+  return GSB_OK;
+}
+
+static bool joint_accumulates(const gsb_joint* j) { return j->cfg.densify_interval > 0; }
+
+// Per-Gaussian buffers sized by the cloud (after creation and after every
+// densify_and_prune): gradient copies, reduction blocks, GradAccum.
+static int joint_size_buffers(gsb_ctx* ctx, gsb_joint* j) {
+  const int64_t n = std::max<int64_t>(j->cloud->n, 1);
+  const int np = num_planes(j->cloud->sh_degree);
+  j->glen = (int64_t)(np + 2) * j->cloud->n_pad;
+  GSB_CUDA(j->grads.reserve(sizeof(float) * j->glen * j->local));
+  GSB_CUDA(j->red.reserve(sizeof(double) * 2 * joint_adam_blocks(n)));
+  GSB_CUDA(cudaMemsetAsync(j->grads.p, 0, sizeof(float) * j->glen * j->local, ctx->stream));
+  if (joint_accumulates(j)) {
+    GSB_CUDA(j->acc_sum.reserve(sizeof(double) * n));
+    GSB_CUDA(j->acc_cnt.reserve(sizeof(int32_t) * n));
+    GSB_CUDA(cudaMemsetAsync(j->acc_sum.p, 0, sizeof(double) * n, ctx->stream));
+    GSB_CUDA(cudaMemsetAsync(j->acc_cnt.p, 0, sizeof(int32_t) * n, ctx->stream));
+  }
+  return GSB_OK;
+}
 
 static int joint_launch_step(gsb_ctx* ctx, gsb_joint* j) {
   cudaStream_t st = ctx->stream;
@@ -2039,6 +2314,13 @@ static int joint_launch_step(gsb_ctx* ctx, gsb_joint* j) {
     if (int r = render_async(ctx, j->cloud, f, rc)) return r;
     if (int r = loss_device(ctx, f, tb, j->cfg.beta, true)) return r;
     if (int r = backward_device(ctx, j->cloud, f, true, gb)) return r;
+    if (joint_accumulates(j)) {  // GradAccum::add for this view (trainer.cpp:134-142)
+      if (int r = launch_grad_accum(st, gb, num_planes(j->cloud->sh_degree), j->cloud->n_pad, j->cloud->n,
+                                    f->cnt_g.as<uint32_t>(), 0.5 * std::max(j->cam.width, j->cam.height),
+                                    j->acc_sum.as<double>(), j->acc_cnt.as<int32_t>()))
+        return r;
+      ctx->launches += 1;
+    }
     if (int r = launch_joint_slot_end(st, j->ctl, b, f->d_pose.as<double>(), f->loss_val.as<double>(),
                                       f->counters.as<uint32_t>(), f->k_cap, j->xchg.as<double>()))
       return r;
@@ -2084,7 +2366,8 @@ static int joint_frames_ready(gsb_ctx* ctx, gsb_joint* j) {
 
 static int joint_prepare(gsb_ctx* ctx, gsb_joint* j) {
   if (int r = joint_frames_ready(ctx, j)) return r;
-  bool stale = !j->exec || j->graph_active != j->cloud->active_sh_degree;
+  bool stale = !j->exec || j->graph_active != j->cloud->active_sh_degree || j->graph_params != j->cloud->params.p ||
+               j->graph_n != j->cloud->n;
   for (size_t b = 0; b < j->frames.size() && !stale; ++b)
     stale = j->frames[b]->gen != j->graph_gen[b] || j->frames[b]->k_cap != j->graph_kcap[b];
   if (!stale) return GSB_OK;
@@ -2113,6 +2396,8 @@ static int joint_prepare(gsb_ctx* ctx, gsb_joint* j) {
     j->graph_kcap[b] = j->frames[b]->k_cap;
   }
   j->graph_active = j->cloud->active_sh_degree;
+  j->graph_params = j->cloud->params.p;
+  j->graph_n = j->cloud->n;
   if (debug_on()) std::fprintf(stderr, "[gsb] joint graph captured: %lld kernels\n", (long long)j->graph_launches);
   return GSB_OK;
 }
@@ -2210,8 +2495,7 @@ int gsb_joint_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* const* targets, 
   const int64_t iters = std::max(cfg->iterations, 1);
   const int64_t nb = joint_adam_blocks(std::max<int64_t>(cloud->n, 1));
   const size_t sb = joint_state_bytes();
-  cudaError_t e = j->grads.reserve(sizeof(float) * j->glen * j->local);
-  if (e == cudaSuccess) e = j->adam_m.reserve(sizeof(float) * np * cloud->n_pad);
+  cudaError_t e = j->adam_m.reserve(sizeof(float) * np * cloud->n_pad);
   if (e == cudaSuccess) e = j->adam_v.reserve(sizeof(float) * np * cloud->n_pad);
   if (e == cudaSuccess) e = j->state.reserve(sb);
   if (e == cudaSuccess) e = j->seq.reserve(sizeof(int32_t) * iters * slots);
@@ -2220,7 +2504,6 @@ int gsb_joint_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* const* targets, 
   if (e == cudaSuccess) e = j->tptrs.reserve(sizeof(float*) * n_views);
   if (e == cudaSuccess) e = j->tbuf.reserve(sizeof(float) * 3 * P * j->local);
   if (e == cudaSuccess) e = j->xchg.reserve(sizeof(double) * joint_xchg_doubles() * slots);
-  if (e == cudaSuccess) e = j->red.reserve(sizeof(double) * 2 * nb);
   if (e == cudaSuccess) e = j->trace_total.reserve(sizeof(double) * iters);
   if (e == cudaSuccess) e = j->trace_l1.reserve(sizeof(double) * iters);
   if (e == cudaSuccess) e = cudaMallocHost(&j->host_state, std::max<size_t>(sb, 64));
@@ -2228,12 +2511,16 @@ int gsb_joint_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* const* targets, 
     gsb_joint_destroy(j);
     return cuda_fail(e, "joint alloc");
   }
-  // host-side initial state: schedule, per-view PoseState + CamDev, target pointers
-  std::vector<int32_t> seq((size_t)iters * slots);
-  if (int r = gsb_joint_schedule(seed, n_views, (int64_t)seq.size(), seq.data())) {
+  (void)nb;
+  if (int r = joint_size_buffers(ctx, j)) {
     gsb_joint_destroy(j);
     return r;
   }
+  // host-side initial state: the Rng of the view sequence (extended lazily),
+  // per-view PoseState + CamDev, target pointers
+  j->rng_state = seed ? seed : 0x9e3779b97f4a7c15ull;
+  j->order.resize(n_views);
+  for (int32_t v = 0; v < n_views; ++v) j->order[v] = v;
   std::vector<char> ps(pose_state_bytes() * n_views);
   std::vector<CamDev> cams(n_views);
   std::vector<const float*> tp(n_views);
@@ -2249,14 +2536,12 @@ int gsb_joint_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* const* targets, 
   }
   std::memset(j->host_state, 0, sb);
   cudaStream_t st = ctx->stream;
-  GSB_CUDA(cudaMemcpyAsync(j->seq.p, seq.data(), sizeof(int32_t) * seq.size(), cudaMemcpyHostToDevice, st));
   GSB_CUDA(cudaMemcpyAsync(j->poses.p, ps.data(), ps.size(), cudaMemcpyHostToDevice, st));
   GSB_CUDA(cudaMemcpyAsync(j->cams.p, cams.data(), sizeof(CamDev) * n_views, cudaMemcpyHostToDevice, st));
   GSB_CUDA(cudaMemcpyAsync(j->tptrs.p, tp.data(), sizeof(float*) * n_views, cudaMemcpyHostToDevice, st));
   GSB_CUDA(cudaMemcpyAsync(j->state.p, j->host_state, sb, cudaMemcpyHostToDevice, st));
   GSB_CUDA(cudaMemsetAsync(j->adam_m.p, 0, sizeof(float) * np * cloud->n_pad, st));
   GSB_CUDA(cudaMemsetAsync(j->adam_v.p, 0, sizeof(float) * np * cloud->n_pad, st));
-  GSB_CUDA(cudaMemsetAsync(j->grads.p, 0, sizeof(float) * j->glen * j->local, st));
   GSB_CUDA(cudaStreamSynchronize(st));
   for (int b = 0; b < j->local; ++b) {
     gsb_frame* f = new gsb_frame();
@@ -2276,7 +2561,7 @@ int gsb_joint_destroy(gsb_joint* j) {
   if (j->exec) cudaGraphExecDestroy(j->exec);
   for (gsb_frame* f : j->frames) gsb_frame_destroy(f);
   DevBuf* bufs[] = {&j->grads, &j->adam_m, &j->adam_v, &j->state, &j->seq, &j->poses, &j->cams, &j->tptrs,
-                    &j->tbuf, &j->xchg, &j->red, &j->trace_total, &j->trace_l1};
+                    &j->tbuf, &j->xchg, &j->red, &j->trace_total, &j->trace_l1, &j->acc_sum, &j->acc_cnt};
   for (DevBuf* b : bufs) b->release();
   if (j->host_state) cudaFreeHost(j->host_state);
   delete j;
@@ -2296,11 +2581,50 @@ int gsb_joint_step(gsb_ctx* ctx, gsb_joint* j, int32_t steps) {
     }
     int64_t chunk = std::min<int64_t>(left, 16);
     if (interval > 0) chunk = std::min<int64_t>(chunk, interval - (j->t % interval));
+    for (int64_t k = 0; k < chunk; ++k)  // densification after step t ends the chunk
+      if (joint_densify_due(j, j->t + k)) {
+        chunk = k + 1;
+        break;
+      }
+    if (int r = joint_sched_extend(ctx, j, (j->t + chunk) * j->ctl.slots)) return r;
     const int64_t t0 = j->t;
     if (int r = joint_run(ctx, j, chunk)) return r;
     left -= j->t - t0;
     if (j->t == t0) return fail(GSB_ERR_CUDA, "joint: no progress");
+    if (j->t - t0 == chunk && joint_densify_due(j, j->t - 1)) {
+      // densify_and_prune (pipelines.cpp:182-186): GradAccum summed over ranks,
+      // then the identical rebuild on every replica (same Rng)
+      if (j->comm && j->world > 1) {
+        NcclApi& nc = nccl();
+        if (ncclResult_t r = nc.group_start()) return nccl_fail(r, "ncclGroupStart");
+        ncclResult_t r1 = nc.all_reduce(j->acc_sum.p, j->acc_sum.p, (size_t)j->cloud->n, ncclFloat64, ncclSum,
+                                        j->comm->comm, ctx->stream);
+        ncclResult_t r2 = nc.all_reduce(j->acc_cnt.p, j->acc_cnt.p, (size_t)j->cloud->n, ncclInt32, ncclSum,
+                                        j->comm->comm, ctx->stream);
+        ncclResult_t r3 = nc.group_end();
+        if (r1 || r2 || r3) return nccl_fail(r1 ? r1 : (r2 ? r2 : r3), "ncclAllReduce (GradAccum)");
+      }
+      DensifyParams dp{j->cfg.grad_threshold, j->cfg.densify_size_ratio, j->cfg.prune_opacity, j->cfg.n_target};
+      if (int r = densify_device(ctx, j->cloud, j->acc_sum.as<double>(), j->acc_cnt.as<int32_t>(), dp, &j->rng_state,
+                                 &j->adam_m, &j->adam_v, j->densify_report))
+        return r;
+      ++j->densify_events;
+      if (int r = joint_size_buffers(ctx, j)) return r;
+      if (debug_on())
+        std::fprintf(stderr, "[gsb] joint densify after step %lld: cloned %d split %d pruned %d -> n %lld\n",
+                     (long long)(j->t - 1), j->densify_report[0], j->densify_report[1], j->densify_report[2],
+                     (long long)j->cloud->n);
+    }
   }
+  return GSB_OK;
+}
+
+int gsb_joint_info(gsb_joint* j, int64_t* n_gaussians, int32_t* densify_events, int32_t last_report[3]) {
+  if (!j) return fail(GSB_ERR_INVALID_ARGUMENT, "null joint");
+  if (n_gaussians) *n_gaussians = j->cloud->n;
+  if (densify_events) *densify_events = j->densify_events;
+  if (last_report)
+    for (int k = 0; k < 3; ++k) last_report[k] = j->densify_report[k];
   return GSB_OK;
 }
 

@@ -166,6 +166,35 @@ int gsb_joint_schedule(uint64_t seed, int32_t n_views, int64_t count, int32_t* s
   return GSB_OK;
 }
 
+// The split children's normals of densify_and_prune (trainer.cpp:215-219):
+// per child one rng->normal3(), whose Vec3(normal(), normal(), normal())
+// arguments a GCC build draws right to left. out: children x 3 (x, y, z).
+int gsb_rng_child_normals(uint64_t* rng_state, int64_t children, double* out) {
+  if (!rng_state || children < 0 || (children > 0 && !out)) return gsb::fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  Rng rng(1);
+  rng.s = *rng_state ? *rng_state : 0x9e3779b97f4a7c15ull;
+  for (int64_t c = 0; c < children; ++c) {
+    out[3 * c + 2] = rng.normal();
+    out[3 * c + 1] = rng.normal();
+    out[3 * c + 0] = rng.normal();
+  }
+  *rng_state = rng.s;
+  return GSB_OK;
+}
+
+// Epoch shuffle of pipelines.cpp:123-129 on a caller-held order and rng state.
+int gsb_rng_shuffle(uint64_t* rng_state, int32_t n, int32_t* order) {
+  if (!rng_state || n < 0 || (n > 0 && !order)) return gsb::fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  Rng rng(1);
+  rng.s = *rng_state ? *rng_state : 0x9e3779b97f4a7c15ull;
+  for (int32_t i = n - 1; i > 0; --i) {
+    const int32_t j = (int32_t)(rng.next() % (uint64_t)(i + 1));
+    std::swap(order[i], order[j]);
+  }
+  *rng_state = rng.s;
+  return GSB_OK;
+}
+
 // perturb_pose_tangent (eval.cpp:148-152): Exp(sigma * N(0, I_6)) * pose
 int gsb_perturb_pose_tangent(const double pose[12], double sigma, uint64_t* rng_state, double out[12]) {
   if (!pose || !rng_state || !out) return gsb::fail(GSB_ERR_INVALID_ARGUMENT, "null argument");

@@ -121,7 +121,9 @@ class JointConfig(C.Structure):
                 ("sh_rest_lr", C.c_double), ("opacity_l1_steps", C.c_int32), ("sh_degree", C.c_int32),
                 ("sh_degree_interval", C.c_int32), ("optimize_poses", C.c_int32), ("beta", C.c_double),
                 ("aniso_ratio", C.c_double), ("opacity_l1_weight", C.c_double), ("background", C.c_double * 3),
-                ("raster", RasterConfig)]
+                ("raster", RasterConfig), ("densify_interval", C.c_int32), ("densify_start", C.c_int32),
+                ("densify_stop", C.c_int32), ("n_target", C.c_int32), ("grad_threshold", C.c_double),
+                ("densify_size_ratio", C.c_double), ("prune_opacity", C.c_double)]
 
     @staticmethod
     def default(**kw) -> "JointConfig":
@@ -206,8 +208,12 @@ def _sigs():
         "gsb_joint_destroy": (C.c_int, [_vp]),
         "gsb_joint_step": (C.c_int, [_vp, _vp, i32]),
         "gsb_joint_read": (C.c_int, [_vp, _vp, P(i64), _vp, _vp]),
+        "gsb_joint_info": (C.c_int, [_vp, P(i64), P(i32), _vp]),
         "gsb_perturb_pose_tangent": (C.c_int, [_vp, d, P(u64), _vp]),
         "gsb_cloud_jitter": (C.c_int, [_vp, u64, d, d]),
+        "gsb_densify_and_prune": (C.c_int, [_vp, _vp, _vp, _vp, d, d, i32, d, P(u64), _vp, _vp]),
+        "gsb_rng_child_normals": (C.c_int, [P(u64), i64, _vp]),
+        "gsb_rng_shuffle": (C.c_int, [P(u64), i32, _vp]),
     }
 
 
@@ -324,6 +330,12 @@ class Cloud:
         out = [np.zeros((n, 3)), np.zeros((n, 4)), np.zeros((n, 3)), np.zeros(n), np.zeros((n, 3, b))]
         _check(lib().gsb_cloud_download(self.h, *[_p(a) for a in out]))
         return out
+
+    def refresh(self):
+        """Re-reads the size (changed by densify_and_prune on the device)."""
+        n, dd, ad = C.c_int64(), C.c_int32(), C.c_int32()
+        _check(lib().gsb_cloud_info(self.h, C.byref(n), C.byref(dd), C.byref(ad)))
+        self.n = n.value
 
     def jitter(self, seed: int, mean_sigma: float, log_scale_range: float = 0.0):
         """tests/test_trainer.cpp:598-601 initial-cloud jitter (gsb_cloud_jitter)."""
@@ -657,7 +669,24 @@ class JointOptimizer:
         done = C.c_int64()
         tt, tl = np.zeros(max(self.cfg.iterations, 1)), np.zeros(max(self.cfg.iterations, 1))
         _check(lib().gsb_joint_read(self.h, _p(poses), C.byref(done), _p(tt), _p(tl)))
-        return dict(poses=poses, steps=done.value, trace_total=tt[:done.value], trace_l1=tl[:done.value])
+        n, ev, rep = C.c_int64(), C.c_int32(), np.zeros(3, np.int32)
+        _check(lib().gsb_joint_info(self.h, C.byref(n), C.byref(ev), _p(rep)))
+        self._keep[0].refresh()
+        return dict(poses=poses, steps=done.value, trace_total=tt[:done.value], trace_l1=tl[:done.value],
+                    n_gaussians=n.value, densify_events=ev.value, densify_report=tuple(int(x) for x in rep))
+
+
+def densify_and_prune(ctx: Context, cloud: Cloud, grad_sum, count, grad_threshold=2e-4, densify_size_ratio=0.01,
+                      n_target=256000, prune_opacity=0.005, rng: "PoseRng" = None, adam_handle=None):
+    """gsopt::densify_and_prune (trainer.hpp:130-133) on the device; returns
+    (cloned, split, pruned). The cloud's size changes in place."""
+    gs = np.ascontiguousarray(grad_sum, np.float64)
+    ct = np.ascontiguousarray(count, np.int32)
+    rep = np.zeros(3, np.int32)
+    _check(lib().gsb_densify_and_prune(ctx.h, cloud.h, _p(gs), _p(ct), grad_threshold, densify_size_ratio, n_target,
+                                       prune_opacity, C.byref(rng.state), adam_handle, _p(rep)))
+    cloud.refresh()
+    return tuple(int(x) for x in rep)
 
 
 def perturb_pose_tangent(pose12, sigma, state: "PoseRng"):

@@ -164,3 +164,57 @@ def test_joint_capacity_growth_replays_steps(G, ctx):
     assert res["steps"] == iters
     rel = np.abs(res["trace_total"] - tt) / np.maximum(np.abs(tt), 1e-12)
     assert np.max(rel) < 1e-3
+
+
+def test_densify_and_prune_matches_oracle(G, ctx):
+    """gsb_densify_and_prune vs the oracle's trainer.cpp:144-239 on identical
+    inputs (cloud, GradAccum arrays, Rng): same population, order, clone /
+    split / prune counts, the split children equal to the reference's doubles
+    rounded to FP32, same Rng state afterwards."""
+    rng = O.make_rng(21)
+    hc = O.synth_cloud(3000, 2, rng).as_float32_exact()
+    r = np.random.default_rng(5)
+    count = r.integers(0, 4, hc.n).astype(np.int32)
+    grad_sum = np.abs(r.normal(0.0, 4e-4, hc.n)) * np.maximum(count, 1)
+    for n_target in (100000, 3500):
+        cloud = G.Cloud.from_host(ctx, hc.means, hc.rotations, hc.log_scales, hc.opacity_logits, hc.sh, 2)
+        grng = G.PoseRng(99)
+        rep = G.densify_and_prune(ctx, cloud, grad_sum, count, 2e-4, 0.01, n_target, 0.005, grng)
+        orng = O.make_rng(99)
+        want, src, orep = O.densify_and_prune(hc, grad_sum, count, 2e-4, 0.01, n_target, 0.005, orng)
+        assert rep == orep, (rep, orep)
+        assert cloud.n == want.n
+        m, q, ls, op, sh = cloud.download()
+        f32 = lambda a: np.asarray(a, np.float64).astype(np.float32).astype(np.float64)
+        assert np.array_equal(q, want.rotations) and np.array_equal(op, want.opacity_logits)
+        assert np.array_equal(sh, want.sh)
+        assert np.max(np.abs(m - f32(want.means))) <= 1e-7 * max(1.0, np.max(np.abs(want.means)))
+        assert np.max(np.abs(ls - f32(want.log_scales))) <= 1e-6
+        assert grng.state.value == orng.state  # the same draws were consumed
+    assert rep[2] > 0  # the n_target case pruned
+
+
+def test_joint_with_densification(G, ctx):
+    """joint_optimize with densify_and_prune every 3 steps (GradAccum on the
+    device, Rng shared with the epoch shuffles): the population follows the
+    oracle's and the loss trace tracks it."""
+    hc, imgs, intr, init, _ = joint_scene(seed=9, n=300)
+    iters = 8
+    kw = dict(sh_degree=1, sh_degree_interval=0, densify_interval=3, densify_start=3, n_target=420,
+              grad_threshold=1e-5)
+    ocfg = O.joint_config(iters, **kw)
+    st, cl, P, tt, tl = O.joint_optimize(hc, imgs, intr, 48, 40, init, ocfg, 1, O.make_rng(13))
+    assert st == 0 and cl.n != hc.n
+    cfg = G.JointConfig.default(iterations=iters, **kw)
+    cloud = G.Cloud.from_host(ctx, hc.means, hc.rotations, hc.log_scales, hc.opacity_logits, hc.sh, hc.sh_degree,
+                              hc.active_sh_degree)
+    targets = [G.Image(ctx, im) for im in imgs]
+    j = G.JointOptimizer(ctx, cloud, targets, intr, init, cfg, 13)
+    j.step(iters)
+    res = j.read()
+    j.close()
+    assert res["steps"] == iters and res["densify_events"] == 2
+    assert abs(res["n_gaussians"] - cl.n) <= max(2, cl.n // 100), (res["n_gaussians"], cl.n)
+    rel = np.abs(res["trace_total"] - tt) / np.maximum(np.abs(tt), 1e-12)
+    assert np.max(rel[:4]) < 1e-3  # before / at the first densification
+    assert np.max(rel) < 2e-2, rel
