@@ -16,6 +16,8 @@
  *   gsb_estimate_pose     <- gsopt::estimate_pose     include/gsopt/trainer.hpp:170-171
  *                            (pose_descent, src/pipelines.cpp:58-92, device resident)
  *   gsb_cloud_*           <- GaussianCloud            include/gsopt/scene.hpp:22-46
+ *   gsb_cloud_{load,save}_ply <- load/save_cloud_ply  include/gsopt/scene_io.hpp (src/ply.cpp:29-148)
+ *   gsb_densify_and_prune <- gsopt::densify_and_prune include/gsopt/trainer.hpp:130-133
  *   gsb_joint_*           <- gsopt::joint_optimize    include/gsopt/trainer.hpp:155-163
  *                            (src/pipelines.cpp:96-216, densification off), data parallel
  *                            over training views with an NCCL all-reduce (gsb_comm_*)
@@ -149,6 +151,12 @@ int gsb_cloud_download(gsb_cloud* cloud, double* means, double* rotations, doubl
                        double* opacity_logits, double* sh);
 int gsb_cloud_info(gsb_cloud* cloud, int64_t* n, int32_t* sh_degree, int32_t* active_sh_degree);
 int gsb_cloud_set_active_sh_degree(gsb_cloud* cloud, int32_t active_sh_degree);
+/* 3DGS PLY I/O straight to / from the device layout: load_cloud_ply
+ * (src/ply.cpp:62-148; the SH degree follows the f_rest count, active = it)
+ * and save_cloud_ply (29-60; higher bands zero-padded to degree 3). Bad files
+ * return GSB_ERR_CORRUPT_FILE. */
+int gsb_cloud_load_ply(gsb_ctx* ctx, const char* path, gsb_cloud** out);
+int gsb_cloud_save_ply(gsb_cloud* cloud, const char* path);
 /* Fills the cloud with the synth.cpp:45-62 draw sequence (GCC argument order)
  * from seed, plus log_scale_offset added to every log-scale (SURVEY §8d
  * density matching). Host generator, then one upload. */

@@ -214,6 +214,8 @@ def _sigs():
         "gsb_densify_and_prune": (C.c_int, [_vp, _vp, _vp, _vp, d, d, i32, d, P(u64), _vp, _vp]),
         "gsb_rng_child_normals": (C.c_int, [P(u64), i64, _vp]),
         "gsb_rng_shuffle": (C.c_int, [P(u64), i32, _vp]),
+        "gsb_cloud_load_ply": (C.c_int, [_vp, C.c_char_p, P(_vp)]),
+        "gsb_cloud_save_ply": (C.c_int, [_vp, C.c_char_p]),
     }
 
 
@@ -330,6 +332,22 @@ class Cloud:
         out = [np.zeros((n, 3)), np.zeros((n, 4)), np.zeros((n, 3)), np.zeros(n), np.zeros((n, 3, b))]
         _check(lib().gsb_cloud_download(self.h, *[_p(a) for a in out]))
         return out
+
+    @staticmethod
+    def load_ply(ctx: Context, path: str) -> "Cloud":
+        """load_cloud_ply (src/ply.cpp:62-148) straight into the device layout."""
+        h = _vp()
+        _check(lib().gsb_cloud_load_ply(ctx.h, os.fsencode(path), C.byref(h)))
+        c = Cloud.__new__(Cloud)
+        c.h, c.ctx = h, ctx
+        n, dd, ad = C.c_int64(), C.c_int32(), C.c_int32()
+        _check(lib().gsb_cloud_info(h, C.byref(n), C.byref(dd), C.byref(ad)))
+        c.n, c.sh_degree = n.value, dd.value
+        return c
+
+    def save_ply(self, path: str):
+        """save_cloud_ply (src/ply.cpp:29-60)."""
+        _check(lib().gsb_cloud_save_ply(self.h, os.fsencode(path)))
 
     def refresh(self):
         """Re-reads the size (changed by densify_and_prune on the device)."""
