@@ -32,7 +32,7 @@ sys.path.insert(0, ROOT)
 N_GAUSS = 1_000_000
 WIDTH, HEIGHT = 1008, 756
 TOTAL_VIEWS = 64            # C3: 64 independent views
-VIEWS_PER_GPU = 8           # weak scaling: 8 views per rank (64 at 8 GPUs)
+VIEWS_PER_GPU = int(os.environ.get("GSB_BENCH_VIEWS_PER_GPU", "8"))  # weak scaling: 8 per rank (64 at 8 GPUs)
 SCENE_SEED = 3
 NOISE_SEED = 1002
 SH_DEGREE = 3
