@@ -48,6 +48,9 @@ __device__ __forceinline__ void sh_basis_d(double x, double y, double z, int deg
 // colour-Jacobian planes, the tile counts and the entry offsets are staged
 // into shared memory by TMA bulk copies (one elected thread, one mbarrier).
 constexpr int kGeomBlock = 256;
+#ifndef GSB_GEOM_POSE_MIN_BLOCKS
+#define GSB_GEOM_POSE_MIN_BLOCKS 4  // 64 registers: occupancy over a few spilled bytes (measured)
+#endif
 #ifndef GSB_POSE_CHAIN_T
 #define GSB_POSE_CHAIN_T float
 #endif
@@ -57,7 +60,7 @@ constexpr int kGeomPlanes = kOpacity + 1;  // means, quat, log-scale, opacity
 // bundle (joint_optimize's parameter gradients), float for the pose-only
 // path (the 6-vector itself is accumulated in FP64 either way).
 template <bool kFull, typename R>
-__global__ void __launch_bounds__(kGeomBlock, 2) backward_geom_kernel(
+__global__ void __launch_bounds__(kGeomBlock, (kFull ? 2 : GSB_GEOM_POSE_MIN_BLOCKS)) backward_geom_kernel(
     const float* __restrict__ params, int64_t n, int64_t n_pad_g, int sh_cap, int sh_active,
     const CamDev* __restrict__ cam_p, RasterDev rc, const uint32_t* __restrict__ cnt_g,
     const uint32_t* __restrict__ off_g, const float* __restrict__ colj, const float* __restrict__ partials,

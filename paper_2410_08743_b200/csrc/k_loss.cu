@@ -107,7 +107,10 @@ __device__ __forceinline__ void hpass5(const float (*st)[kSH][kSW + 1], double (
   }
 }
 
-__global__ void __launch_bounds__(kThr) loss_maps_kernel(const float* __restrict__ ren, const float* __restrict__ tgt,
+#ifndef GSB_LOSS_MIN_BLOCKS
+#define GSB_LOSS_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(kThr, GSB_LOSS_MIN_BLOCKS) loss_maps_kernel(const float* __restrict__ ren, const float* __restrict__ tgt,
                                                          int W, int H, double scale, float* __restrict__ gmaps,
                                                          double* __restrict__ block_sums) {
   extern __shared__ __align__(16) unsigned char smem_raw[];

@@ -125,6 +125,9 @@ __device__ __forceinline__ void sh_colour(const float* __restrict__ P, int64_t n
 // completing on an mbarrier), so all ~59 KB are in flight at once; the
 // per-thread reads below then come from shared memory (stride kPreBlock).
 constexpr int kPreBlock = 256;
+#ifndef GSB_PRE_MIN_BLOCKS
+#define GSB_PRE_MIN_BLOCKS 1
+#endif
 
 // Per-view outputs of K1 (one forward state).
 struct PreOut {
@@ -319,7 +322,7 @@ __device__ __forceinline__ void reserve_slots(const PreOut& o, int64_t i, uint32
 // colour and tile rect follow from the same staged parameters — the cloud is
 // read from HBM once per launch instead of once per view.
 template <int DEG, bool kQuirk>
-__global__ void __launch_bounds__(kPreBlock) preprocess_kernel(const float* __restrict__ params, int64_t n,
+__global__ void __launch_bounds__(kPreBlock, GSB_PRE_MIN_BLOCKS) preprocess_kernel(const float* __restrict__ params, int64_t n,
                                                                int64_t n_pad_g, int sh_cap, RasterDev rc,
                                                                int nviews, const __grid_constant__ PreViews views) {
   extern __shared__ __align__(128) float s_par[];  // [planes][kPreBlock]
