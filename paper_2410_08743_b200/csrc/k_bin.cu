@@ -51,12 +51,20 @@ __global__ void __launch_bounds__(kBinThreads) tile_count_kernel(const uint32_t*
   for (int t = threadIdx.x; t < n_tiles; t += kBinThreads) s_cnt[t] = 0;
   __syncthreads();
   const int64_t g0 = (int64_t)blockIdx.x * kBinChunk;
-  for (int k = threadIdx.x; k < kBinChunk; k += kBinThreads) {
-    const int64_t i = g0 + k;
-    if (i >= n || (cnt_g[i] & kCntMask) == 0u) continue;
-    const SplatAux a = aux_g[i];
-    const uint32_t tx0 = a.tx0_ty0 & 0xffffu, ty0 = a.tx0_ty0 >> 16;
-    const uint32_t nx = a.nx_ny & 0xffffu, ny = a.nx_ny >> 16;
+  constexpr int kPer = kBinChunk / kBinThreads;  // Gaussians per thread: loads issued together
+  uint32_t c[kPer];
+  SplatAux a[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int64_t i = g0 + u * kBinThreads + threadIdx.x;
+    c[u] = i < n ? (cnt_g[i] & kCntMask) : 0u;
+    if (c[u]) a[u] = aux_g[i];
+  }
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    if (!c[u]) continue;
+    const uint32_t tx0 = a[u].tx0_ty0 & 0xffffu, ty0 = a[u].tx0_ty0 >> 16;
+    const uint32_t nx = a[u].nx_ny & 0xffffu, ny = a[u].nx_ny >> 16;
     for (uint32_t y = 0; y < ny; ++y) {
       const uint32_t row = (ty0 + y) * (uint32_t)tiles_x + tx0;
       for (uint32_t x = 0; x < nx; ++x) atomicAdd(s_cnt + row + x, 1u);
@@ -94,15 +102,26 @@ __global__ void __launch_bounds__(kBinThreads) tile_scatter_kernel(const uint32_
   for (int t = threadIdx.x; t < n_tiles; t += kBinThreads) s_cur[t] = offs[(int64_t)t * nchunks + blockIdx.x];
   __syncthreads();
   const int64_t g0 = (int64_t)blockIdx.x * kBinChunk;
-  for (int k = threadIdx.x; k < kBinChunk; k += kBinThreads) {
-    const int64_t i = g0 + k;
-    if (i >= n || (cnt_g[i] & kCntMask) == 0u) continue;
-    const SplatAux a = aux_g[i];
-    // depth > z_near > 0: the FP64 bit pattern orders like the value
-    const unsigned long long key =
-        ((unsigned long long)(uint32_t)__double2hiint(depth_g[i]) << 32) | (unsigned long long)(uint32_t)i;
-    const uint32_t tx0 = a.tx0_ty0 & 0xffffu, ty0 = a.tx0_ty0 >> 16;
-    const uint32_t nx = a.nx_ny & 0xffffu, ny = a.nx_ny >> 16;
+  constexpr int kPer = kBinChunk / kBinThreads;  // Gaussians per thread: loads issued together
+  uint32_t c[kPer];
+  SplatAux a[kPer];
+  uint32_t dh[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int64_t i = g0 + u * kBinThreads + threadIdx.x;
+    c[u] = i < n ? (cnt_g[i] & kCntMask) : 0u;
+    if (c[u]) {
+      a[u] = aux_g[i];
+      dh[u] = (uint32_t)__double2hiint(depth_g[i]);  // depth > z_near > 0: bits order like the value
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    if (!c[u]) continue;
+    const int64_t i = g0 + u * kBinThreads + threadIdx.x;
+    const unsigned long long key = ((unsigned long long)dh[u] << 32) | (unsigned long long)(uint32_t)i;
+    const uint32_t tx0 = a[u].tx0_ty0 & 0xffffu, ty0 = a[u].tx0_ty0 >> 16;
+    const uint32_t nx = a[u].nx_ny & 0xffffu, ny = a[u].nx_ny >> 16;
     for (uint32_t y = 0; y < ny; ++y) {
       const uint32_t row = (ty0 + y) * (uint32_t)tiles_x + tx0;
       for (uint32_t x = 0; x < nx; ++x) {

@@ -107,10 +107,12 @@ __device__ __forceinline__ void hpass5(const float (*st)[kSH][kSW + 1], double (
   }
 }
 
-#ifndef GSB_LOSS_MIN_BLOCKS
-#define GSB_LOSS_MIN_BLOCKS 1
+#ifdef GSB_LOSS_MIN_BLOCKS
+#define GSB_LOSS_BOUNDS __launch_bounds__(kThr, GSB_LOSS_MIN_BLOCKS)
+#else
+#define GSB_LOSS_BOUNDS __launch_bounds__(kThr)
 #endif
-__global__ void __launch_bounds__(kThr, GSB_LOSS_MIN_BLOCKS) loss_maps_kernel(const float* __restrict__ ren, const float* __restrict__ tgt,
+__global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, const float* __restrict__ tgt,
                                                          int W, int H, double scale, float* __restrict__ gmaps,
                                                          double* __restrict__ block_sums) {
   extern __shared__ __align__(16) unsigned char smem_raw[];

@@ -125,8 +125,12 @@ __device__ __forceinline__ void sh_colour(const float* __restrict__ P, int64_t n
 // completing on an mbarrier), so all ~59 KB are in flight at once; the
 // per-thread reads below then come from shared memory (stride kPreBlock).
 constexpr int kPreBlock = 256;
-#ifndef GSB_PRE_MIN_BLOCKS
-#define GSB_PRE_MIN_BLOCKS 1
+// (an explicit minBlocks of 1 lets ptxas spend 138 registers -> 1 CTA/SM;
+// the default form keeps 124 and 2 CTAs/SM)
+#ifdef GSB_PRE_MIN_BLOCKS
+#define GSB_PRE_BOUNDS __launch_bounds__(kPreBlock, GSB_PRE_MIN_BLOCKS)
+#else
+#define GSB_PRE_BOUNDS __launch_bounds__(kPreBlock)
 #endif
 
 // Per-view outputs of K1 (one forward state).
@@ -322,7 +326,7 @@ __device__ __forceinline__ void reserve_slots(const PreOut& o, int64_t i, uint32
 // colour and tile rect follow from the same staged parameters — the cloud is
 // read from HBM once per launch instead of once per view.
 template <int DEG, bool kQuirk>
-__global__ void __launch_bounds__(kPreBlock, GSB_PRE_MIN_BLOCKS) preprocess_kernel(const float* __restrict__ params, int64_t n,
+__global__ void GSB_PRE_BOUNDS preprocess_kernel(const float* __restrict__ params, int64_t n,
                                                                int64_t n_pad_g, int sh_cap, RasterDev rc,
                                                                int nviews, const __grid_constant__ PreViews views) {
   extern __shared__ __align__(128) float s_par[];  // [planes][kPreBlock]
