@@ -209,6 +209,17 @@ int gsb_image_destroy(gsb_image* image);
 int gsb_frame_rgb_loss(gsb_ctx* ctx, gsb_frame* frame, gsb_image* target, double beta,
                        double* loss_out);
 
+/* masked_rgb_loss (losses.cpp:273-289): mask = host uint8 H*W; GSB_ERR_EMPTY_MASK
+ * when no pixel is set (masked_l1's empty_mask). d_rendered optional. */
+int gsb_masked_rgb_loss(gsb_ctx* ctx, const double* rendered, const double* target, int32_t width,
+                        int32_t height, const uint8_t* mask, double beta, double* loss_out,
+                        double* d_rendered);
+/* Same on the frame's image with its own transmittance_mask(accum, threshold)
+ * (losses.cpp:259-263, accum = 1 - final transmittance); the gradient stays in
+ * the frame. masked_out: pixels that passed (0 -> GSB_ERR_EMPTY_MASK). */
+int gsb_frame_masked_rgb_loss(gsb_ctx* ctx, gsb_frame* frame, gsb_image* target, double beta,
+                              double threshold, double* loss_out, int64_t* masked_out);
+
 /* ---- backward (render_backward, rasterizer.cpp:336-540) ---- */
 int gsb_grads_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_grads** out);
 int gsb_grads_destroy(gsb_grads* grads);
@@ -349,6 +360,47 @@ int gsb_joint_step(gsb_ctx* ctx, gsb_joint* j, int32_t steps);
 int gsb_joint_read(gsb_joint* j, double* poses_out, int64_t* steps_done, double* trace_total, double* trace_l1);
 /* current cloud size, densify_and_prune events so far, last event's {cloned, split, pruned} */
 int gsb_joint_info(gsb_joint* j, int64_t* n_gaussians, int32_t* densify_events, int32_t last_report[3]);
+
+/* ---- bootstrap path (pipelines.cpp:224-312, scene.cpp:115-243) ----
+ * RGB-D frames -> per-frame clouds -> relative poses -> an initial trajectory.
+ * The TrainConfig knobs these read (trainer.hpp:21-60, losses.hpp:19). */
+typedef struct {
+  int32_t per_frame_fit_steps, relpose_steps, unproject_points;
+  double pos_lr_start, pos_lr_end, rot_lr, scale_lr, opacity_lr, sh_dc_lr, sh_rest_lr;
+  double relpose_lr_start, relpose_lr_end;
+  double beta, mask_threshold;
+  double background[3];
+  gsb_raster_config raster;
+} gsb_bootstrap_config;
+void gsb_default_bootstrap_config(gsb_bootstrap_config* cfg);
+/* unproject (scene.cpp:209-243): every ceil(valid / max_points)-th valid pixel
+ * (valid != 0, finite, > 0; row-major) lifted to world by world_to_cam^-1.
+ * points_out / colors_out: max_points * 3. GSB_ERR_NO_VALID_DEPTH if none. */
+int gsb_unproject(const double* depth, const uint8_t* valid, int32_t width, int32_t height,
+                  const double* frame_hwc, const double intr[4], const double world_to_cam[12],
+                  int32_t max_points, double* points_out, double* colors_out, int64_t* n_out);
+/* init_from_points (scene.cpp:182-207): log-scale = log(max(mean 3-NN distance,
+ * 1e-7)) (kNN on the device), identity rotation, opacity logit(0.1), SH DC
+ * from colour, active degree 0. GSB_ERR_DEGENERATE_CLOUD below 4 points. */
+int gsb_init_from_points(gsb_ctx* ctx, const double* points, const double* colors, int64_t n,
+                         int32_t sh_degree, gsb_cloud** out);
+/* fit_frame_gaussians (pipelines.cpp:224-250): SH-0 cloud from the frame at the
+ * identity pose, per_frame_fit_steps of render -> rgb_loss -> backward -> Adam. */
+int gsb_fit_frame_gaussians(gsb_ctx* ctx, const double* frame_hwc, const double* depth,
+                            const uint8_t* valid, int32_t width, int32_t height, const double intr[4],
+                            const gsb_bootstrap_config* cfg, gsb_cloud** out);
+/* estimate_relative_pose (pipelines.cpp:252-290): masked pose-only descent from
+ * the identity; best-loss pose, ok = 0 (identity) once the mask empties. */
+int gsb_estimate_relative_pose(gsb_ctx* ctx, gsb_cloud* cloud, const double* frame_next_hwc,
+                               int32_t width, int32_t height, const double intr[4],
+                               const gsb_bootstrap_config* cfg, double pose_out[12], int32_t* ok,
+                               double* final_loss);
+/* bootstrap_trajectory (pipelines.cpp:292-312): poses_out n_frames x 12
+ * world_to_cam (frame 0 = identity), pair_ok n_frames - 1 (optional). */
+int gsb_bootstrap_trajectory(gsb_ctx* ctx, const double* const* frames, const double* const* depths,
+                             const uint8_t* const* valids, int32_t n_frames, int32_t width,
+                             int32_t height, const double intr[4], const gsb_bootstrap_config* cfg,
+                             double* poses_out, int32_t* pair_ok);
 
 #ifdef __cplusplus
 }

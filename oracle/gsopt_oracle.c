@@ -1109,13 +1109,18 @@ static void conv_window(const double* src, int width, int height, double* dst, d
   }
 }
 /* losses.cpp:74-155 (mask == nullptr path) */
-double orc_ssim(const double* a, const double* b, int32_t width, int32_t height, double* d_a) {
+/* losses.cpp:74-155 (ssim_core): mask (nullable) selects the valid-window
+ * pixels that enter the mean */
+static double ssim_core_m(const double* a, const double* b, int32_t width, int32_t height, const uint8_t* mask,
+                          double* d_a) {
   const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
   const int x0 = KHALF, x1 = width - KHALF, y0 = KHALF, y1 = height - KHALF;
   const size_t P = (size_t)width * height;
   if (d_a) memset(d_a, 0, sizeof(double) * P * 3);
   int64_t count = 0;
-  if (x1 > x0 && y1 > y0) count = (int64_t)(x1 - x0) * (y1 - y0);
+  if (x1 > x0 && y1 > y0)
+    for (int y = y0; y < y1; ++y)
+      for (int x = x0; x < x1; ++x) count += (!mask || mask[(size_t)y * width + x]) ? 1 : 0;
   if (count == 0) return 1.0;
   const double scale = 1.0 / (3.0 * (double)count);
   double total = 0.0;
@@ -1145,6 +1150,7 @@ double orc_ssim(const double* a, const double* b, int32_t width, int32_t height,
     for (int y = y0; y < y1; ++y) {
       for (int x = x0; x < x1; ++x) {
         const size_t p = (size_t)y * width + x;
+        if (mask && !mask[p]) continue;
         const double ma = mu_a[p], mb = mu_b[p];
         const double va = e_aa[p] - ma * ma;
         const double vb = e_bb[p] - mb * mb;
@@ -1171,6 +1177,51 @@ double orc_ssim(const double* a, const double* b, int32_t width, int32_t height,
   }
   free(buf);
   return total * scale;
+}
+double orc_ssim(const double* a, const double* b, int32_t width, int32_t height, double* d_a) {
+  return ssim_core_m(a, b, width, height, NULL, d_a);
+}
+/* losses.cpp:158-192 with a mask: masked pixels only, norm over their count */
+static double l1_core_m(const double* r, const double* t, int32_t w, int32_t h, const uint8_t* mask, double* d,
+                        int64_t* count_out) {
+  const int64_t P = (int64_t)w * h;
+  int64_t count = 0;
+  for (int64_t p = 0; p < P; ++p) count += mask[p] != 0;
+  *count_out = count;
+  if (d) memset(d, 0, sizeof(double) * P * 3);
+  if (count == 0) return 0.0;
+  const double norm = 1.0 / (3.0 * (double)count);
+  double total = 0.0;
+  for (int64_t p = 0; p < P; ++p) {
+    if (!mask[p]) continue;
+    for (int c = 0; c < 3; ++c) {
+      double diff = r[p * 3 + c] - t[p * 3 + c];
+      total += fabs(diff);
+      if (d && diff != 0.0) d[p * 3 + c] = diff > 0.0 ? norm : -norm;
+    }
+  }
+  return total * norm;
+}
+/* losses.cpp:259-263 */
+void orc_transmittance_mask(const double* accum, int64_t n, double threshold, uint8_t* mask) {
+  for (int64_t i = 0; i < n; ++i) mask[i] = accum[i] > threshold ? 1 : 0;
+}
+/* losses.cpp:273-289; returns the loss, *status = 5 (empty_mask + 1) when no pixel passes */
+double orc_masked_rgb_loss(const double* rendered, const double* target, int32_t w, int32_t h, const uint8_t* mask,
+                           double beta, double* d_rendered, int32_t* status) {
+  const size_t n = (size_t)w * h * 3;
+  double* d_l1 = d_rendered ? (double*)malloc(sizeof(double) * n) : NULL;
+  double* d_ss = d_rendered ? (double*)malloc(sizeof(double) * n) : NULL;
+  int64_t cnt = 0;
+  double l1 = l1_core_m(rendered, target, w, h, mask, d_l1, &cnt);
+  *status = cnt == 0 ? 5 : 0;
+  double s = cnt ? ssim_core_m(rendered, target, w, h, mask, d_ss) : 1.0;
+  double loss = (1.0 - beta) * l1 + beta * (1.0 - s);
+  if (d_rendered)
+    for (size_t i = 0; i < n; ++i) d_rendered[i] = cnt ? (1.0 - beta) * d_l1[i] - beta * d_ss[i] : 0.0;
+  free(d_l1);
+  free(d_ss);
+  return loss;
 }
 /* losses.cpp:158-192 */
 static double l1_core(const double* r, const double* t, int32_t w, int32_t h, double* d) {
@@ -1760,6 +1811,225 @@ int32_t orc_joint_optimize(orc_cloud* cloud, const double* const* images, int32_
   free(acc_sum);
   free(acc_cnt);
   return status;
+}
+
+/* ------------------------------------------------------------ bootstrap */
+/* scene.cpp:209-243: valid pixels (valid != 0, finite, d > 0) in row-major
+ * order, every ceil(count / max_points)-th one lifted to cam_to_world (d * ray).
+ * points / colors: caller buffers of max_points * 3. Returns the number of
+ * points, -1 for no valid depth (ErrorCode::no_valid_depth). */
+int64_t orc_unproject(const double* depth, const uint8_t* valid, int32_t w, int32_t h, const double* frame,
+                      double fx, double fy, double cx, double cy, const double R[9], const double t[3],
+                      int32_t max_points, double* points, double* colors) {
+  int64_t count = 0;
+  for (int64_t p = 0; p < (int64_t)w * h; ++p)
+    if (valid[p] && isfinite(depth[p]) && depth[p] > 0.0) ++count;
+  if (count == 0) return -1;
+  const int64_t stride = (count + max_points - 1) / max_points;
+  /* cam_to_world = (R^T, -R^T t) */
+  double Rt[9], ti[3];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) Rt[i * 3 + j] = R[j * 3 + i];
+  mat3_vec(Rt, t, ti);
+  for (int k = 0; k < 3; ++k) ti[k] = -ti[k];
+  int64_t idx = 0, out = 0;
+  for (int64_t p = 0; p < (int64_t)w * h; ++p) {
+    if (!(valid[p] && isfinite(depth[p]) && depth[p] > 0.0)) continue;
+    if (idx % stride == 0) {
+      const int x = (int)(p % w), y = (int)(p / w);
+      const double d = depth[p];
+      const double ray[3] = {(x - cx) / fx, (y - cy) / fy, 1.0};
+      const double q[3] = {d * ray[0], d * ray[1], d * ray[2]};
+      double wpt[3];
+      mat3_vec(Rt, q, wpt);
+      for (int k = 0; k < 3; ++k) {
+        points[3 * out + k] = wpt[k] + ti[k];
+        colors[3 * out + k] = frame[p * 3 + k];
+      }
+      ++out;
+    }
+    ++idx;
+  }
+  return out;
+}
+
+/* scene.cpp:115-180: mean distance to the k nearest other points (exact;
+ * restated as brute force, which selects the same k distances). */
+void orc_mean_knn_distance(const double* pts, int64_t n, int k, double* out) {
+  double best[8];
+  for (int64_t i = 0; i < n; ++i) {
+    for (int b = 0; b < k; ++b) best[b] = INFINITY;
+    for (int64_t j = 0; j < n; ++j) {
+      if (j == i) continue;
+      const double dx = pts[3 * j] - pts[3 * i], dy = pts[3 * j + 1] - pts[3 * i + 1],
+                   dz = pts[3 * j + 2] - pts[3 * i + 2];
+      const double d = sqrt(dx * dx + dy * dy + dz * dz);
+      if (d < best[k - 1]) {
+        best[k - 1] = d;
+        for (int b = k - 1; b > 0 && best[b] < best[b - 1]; --b) {
+          const double tmp = best[b];
+          best[b] = best[b - 1];
+          best[b - 1] = tmp;
+        }
+      }
+    }
+    double sum = 0.0;
+    for (int b = 0; b < k; ++b) sum += best[b];
+    out[i] = sum / k;
+  }
+}
+
+/* scene.cpp:182-207 */
+void orc_init_from_points(const double* pts, const double* cols, int64_t n, int32_t sh_degree, orc_cloud* out) {
+  double* nn = (double*)malloc(sizeof(double) * (size_t)(n + 1));
+  orc_mean_knn_distance(pts, n, 3, nn);
+  orc_cloud_alloc(out, n, sh_degree);
+  out->active_sh_degree = 0;
+  const int basis = sh_count(sh_degree);
+  const double op = log(0.1 / (1.0 - 0.1)); /* logit(0.1), core.hpp:113 */
+  for (int64_t i = 0; i < n; ++i) {
+    for (int k = 0; k < 3; ++k) out->means[3 * i + k] = pts[3 * i + k];
+    out->rotations[4 * i] = 1.0;
+    out->rotations[4 * i + 1] = out->rotations[4 * i + 2] = out->rotations[4 * i + 3] = 0.0;
+    const double sc = log(fmax(nn[i], 1e-7));
+    for (int k = 0; k < 3; ++k) out->log_scales[3 * i + k] = sc;
+    out->opacity_logits[i] = op;
+    for (int c = 0; c < 3; ++c) out->sh[(size_t)i * 3 * basis + c * basis] = (cols[3 * i + c] - 0.5) / 0.28209479177387814;
+  }
+  free(nn);
+}
+
+/* pipelines.cpp:224-250: unproject at the identity pose, SH-0 cloud, steps of
+ * render -> rgb_loss -> render_backward -> cloud_adam_step (position lr
+ * exponential over the fit). Returns 0, or -1 (no valid depth). */
+int32_t orc_fit_frame_gaussians(const double* frame, const double* depth, const uint8_t* valid, int32_t w, int32_t h,
+                                double fx, double fy, double cx, double cy, const orc_fit_cfg* cfg, orc_cloud* out) {
+  const double I[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, z[3] = {0, 0, 0};
+  double* pts = (double*)malloc(sizeof(double) * 3 * (size_t)cfg->unproject_points);
+  double* cols = (double*)malloc(sizeof(double) * 3 * (size_t)cfg->unproject_points);
+  const int64_t np = orc_unproject(depth, valid, w, h, frame, fx, fy, cx, cy, I, z, cfg->unproject_points, pts, cols);
+  if (np < 0) {
+    free(pts);
+    free(cols);
+    return -1;
+  }
+  orc_init_from_points(pts, cols, np, 0, out);
+  free(pts);
+  free(cols);
+  orc_adam_state st[5];
+  memset(st, 0, sizeof st);
+  orc_camera cam;
+  cam.fx = fx; cam.fy = fy; cam.cx = cx; cam.cy = cy; cam.width = w; cam.height = h;
+  memcpy(cam.R, I, sizeof I);
+  memcpy(cam.t, z, sizeof z);
+  double* d_image = (double*)malloc(sizeof(double) * (size_t)w * h * 3);
+  for (int32_t t = 0; t < cfg->steps; ++t) {
+    orc_render_out* ro = orc_render(out, &cam, cfg->background, &cfg->raster);
+    orc_rgb_loss(ro->image, frame, w, h, cfg->beta, d_image);
+    orc_grads g;
+    orc_render_backward(out, &cam, ro, d_image, w, h, &g);
+    const double lrs[6] = {orc_schedule(1, cfg->pos_lr_start, cfg->pos_lr_end, t, cfg->steps), cfg->rot_lr,
+                           cfg->scale_lr, cfg->opacity_lr, cfg->sh_dc_lr, cfg->sh_rest_lr};
+    orc_cloud_adam_step(out, &g, st, lrs);
+    orc_grads_free(&g);
+    orc_render_free(ro);
+  }
+  for (int k = 0; k < 5; ++k) {
+    free(st[k].m);
+    free(st[k].v);
+  }
+  free(d_image);
+  return 0;
+}
+
+/* pipelines.cpp:252-290: transmittance-masked pose-only descent from the
+ * identity; failure (ok = 0, identity) once the mask empties; lr halves
+ * whenever fewer than 5% of the pixels pass. Returns ok. */
+int32_t orc_estimate_relative_pose(const orc_cloud* cloud, const double* frame, int32_t w, int32_t h, double fx,
+                                   double fy, double cx, double cy, const orc_relpose_cfg* cfg, double R_out[9],
+                                   double t_out[3], double* final_loss) {
+  const double I[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+  double R[9], t[3] = {0, 0, 0};
+  memcpy(R, I, sizeof R);
+  memcpy(R_out, I, sizeof R);
+  memset(t_out, 0, sizeof(double) * 3);
+  *final_loss = 0.0;
+  orc_pose_adam adam;
+  memset(&adam, 0, sizeof adam);
+  double best = INFINITY, lr_scale = 1.0;
+  const size_t P = (size_t)w * h;
+  uint8_t* mask = (uint8_t*)malloc(P);
+  double* d_image = (double*)malloc(sizeof(double) * P * 3);
+  int32_t ok = 1;
+  for (int32_t it = 0; it < cfg->steps; ++it) {
+    orc_camera cam;
+    cam.fx = fx; cam.fy = fy; cam.cx = cx; cam.cy = cy; cam.width = w; cam.height = h;
+    memcpy(cam.R, R, sizeof R);
+    memcpy(cam.t, t, sizeof t);
+    orc_render_out* ro = orc_render(cloud, &cam, cfg->background, &cfg->raster);
+    orc_transmittance_mask(ro->accum_transmittance, (int64_t)P, cfg->mask_threshold, mask);
+    size_t masked = 0;
+    for (size_t p = 0; p < P; ++p) masked += mask[p];
+    if (masked == 0) {
+      memcpy(R_out, I, sizeof R);
+      memset(t_out, 0, sizeof(double) * 3);
+      ok = 0;
+      orc_render_free(ro);
+      break;
+    }
+    if ((double)masked < 0.05 * (double)P) lr_scale *= 0.5;
+    int32_t st = 0;
+    const double loss = orc_masked_rgb_loss(ro->image, frame, w, h, mask, cfg->beta, d_image, &st);
+    if (loss < best) {
+      best = loss;
+      memcpy(R_out, R, sizeof R);
+      memcpy(t_out, t, sizeof t);
+      *final_loss = loss;
+    }
+    orc_grads g;
+    orc_render_backward(cloud, &cam, ro, d_image, w, h, &g);
+    const double lr = lr_scale * orc_schedule(0, cfg->lr_start, cfg->lr_end, it, cfg->steps);
+    double Rn[9], tn[3], applied[6];
+    orc_pose_step(R, t, g.d_pose, lr, &adam, Rn, tn, applied);
+    memcpy(R, Rn, sizeof R);
+    memcpy(t, tn, sizeof t);
+    orc_grads_free(&g);
+    orc_render_free(ro);
+  }
+  free(mask);
+  free(d_image);
+  return ok;
+}
+
+/* pipelines.cpp:292-312: per consecutive pair, fit frame t, estimate the
+ * relative pose into frame t+1, compose (lie.hpp:48-53). poses: n x 12. */
+int32_t orc_bootstrap_trajectory(const double* const* frames, const double* const* depths,
+                                 const uint8_t* const* valids, int32_t n, int32_t w, int32_t h, double fx, double fy,
+                                 double cx, double cy, const orc_fit_cfg* fit, const orc_relpose_cfg* rel,
+                                 double* poses, int32_t* pair_ok) {
+  double R[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, t[3] = {0, 0, 0};
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c) poses[r * 4 + c] = R[r * 3 + c];
+    poses[r * 4 + 3] = t[r];
+  }
+  for (int32_t f = 0; f + 1 < n; ++f) {
+    orc_cloud cl;
+    if (orc_fit_frame_gaussians(frames[f], depths[f], valids[f], w, h, fx, fy, cx, cy, fit, &cl) != 0) return -1;
+    double Rr[9], tr[3], fl;
+    pair_ok[f] = orc_estimate_relative_pose(&cl, frames[f + 1], w, h, fx, fy, cx, cy, rel, Rr, tr, &fl);
+    orc_cloud_free(&cl);
+    double Rn[9], tn[3];
+    mat3_mul(Rr, R, Rn);
+    mat3_vec(Rr, t, tn);
+    for (int k = 0; k < 3; ++k) tn[k] += tr[k];
+    memcpy(R, Rn, sizeof R);
+    memcpy(t, tn, sizeof t);
+    for (int r = 0; r < 3; ++r) {
+      for (int c = 0; c < 3; ++c) poses[12 * (f + 1) + r * 4 + c] = R[r * 3 + c];
+      poses[12 * (f + 1) + r * 4 + 3] = t[r];
+    }
+  }
+  return 0;
 }
 
 /* ----------------------------------------------------------------- synth */

@@ -202,6 +202,37 @@ int32_t orc_joint_optimize(orc_cloud* cloud, const double* const* images, int32_
                            double cx, double cy, int32_t w, int32_t h, double* poses, const orc_joint_cfg* cfg,
                            int32_t slots, orc_rng* rng, double* trace_total, double* trace_l1);
 
+/* ---- bootstrap path (pipelines.cpp:224-312, losses.cpp:259-289, scene.cpp:115-243) ---- */
+void orc_transmittance_mask(const double* accum, int64_t n, double threshold, uint8_t* mask);
+double orc_masked_rgb_loss(const double* rendered, const double* target, int32_t w, int32_t h, const uint8_t* mask,
+                           double beta, double* d_rendered, int32_t* status);
+int64_t orc_unproject(const double* depth, const uint8_t* valid, int32_t w, int32_t h, const double* frame,
+                      double fx, double fy, double cx, double cy, const double R[9], const double t[3],
+                      int32_t max_points, double* points, double* colors);
+void orc_mean_knn_distance(const double* pts, int64_t n, int k, double* out);
+void orc_init_from_points(const double* pts, const double* cols, int64_t n, int32_t sh_degree, orc_cloud* out);
+typedef struct {
+  int32_t steps, unproject_points;
+  double pos_lr_start, pos_lr_end, rot_lr, scale_lr, opacity_lr, sh_dc_lr, sh_rest_lr, beta;
+  double background[3];
+  orc_raster_config raster;
+} orc_fit_cfg;
+typedef struct {
+  int32_t steps;
+  double lr_start, lr_end, beta, mask_threshold;
+  double background[3];
+  orc_raster_config raster;
+} orc_relpose_cfg;
+int32_t orc_fit_frame_gaussians(const double* frame, const double* depth, const uint8_t* valid, int32_t w, int32_t h,
+                                double fx, double fy, double cx, double cy, const orc_fit_cfg* cfg, orc_cloud* out);
+int32_t orc_estimate_relative_pose(const orc_cloud* cloud, const double* frame, int32_t w, int32_t h, double fx,
+                                   double fy, double cx, double cy, const orc_relpose_cfg* cfg, double R_out[9],
+                                   double t_out[3], double* final_loss);
+int32_t orc_bootstrap_trajectory(const double* const* frames, const double* const* depths,
+                                 const uint8_t* const* valids, int32_t n, int32_t w, int32_t h, double fx, double fy,
+                                 double cx, double cy, const orc_fit_cfg* fit, const orc_relpose_cfg* rel,
+                                 double* poses, int32_t* pair_ok);
+
 /* synth.cpp:33-101 + eval.cpp:122-152 */
 void orc_synth_cloud(orc_cloud* cloud, int64_t n, int32_t sh_degree, orc_rng* rng);
 void orc_look_at(const double eye[3], const double target[3], double R[9], double t[3]);

@@ -91,6 +91,18 @@ class JointCfg(C.Structure):
                 ("densify_size_ratio", C.c_double), ("prune_opacity", C.c_double)]
 
 
+class FitCfg(C.Structure):
+    _fields_ = [("steps", C.c_int32), ("unproject_points", C.c_int32), ("pos_lr_start", C.c_double),
+                ("pos_lr_end", C.c_double), ("rot_lr", C.c_double), ("scale_lr", C.c_double),
+                ("opacity_lr", C.c_double), ("sh_dc_lr", C.c_double), ("sh_rest_lr", C.c_double),
+                ("beta", C.c_double), ("background", C.c_double * 3), ("raster", RasterConfig)]
+
+
+class RelposeCfg(C.Structure):
+    _fields_ = [("steps", C.c_int32), ("lr_start", C.c_double), ("lr_end", C.c_double), ("beta", C.c_double),
+                ("mask_threshold", C.c_double), ("background", C.c_double * 3), ("raster", RasterConfig)]
+
+
 class PoseCfg(C.Structure):
     _fields_ = [("cam_lr_start", C.c_double), ("cam_lr_end", C.c_double), ("beta", C.c_double),
                 ("pose_converged_eps", C.c_double), ("background", C.c_double * 3), ("raster", RasterConfig)]
@@ -157,6 +169,15 @@ def lib():
             "orc_cloud_adam_step": (None, [P(Cloud), P(Grads), vp, vp]),
             "orc_densify_and_prune": (None, [P(Cloud), vp, vp, d, d, i32, d, P(Rng), P(Cloud), vp, vp]),
             "orc_free": (None, [vp]),
+            "orc_transmittance_mask": (None, [vp, i64, d, vp]),
+            "orc_masked_rgb_loss": (d, [vp, vp, i32, i32, vp, d, vp, P(i32)]),
+            "orc_unproject": (i64, [vp, vp, i32, i32, vp, d, d, d, d, vp, vp, i32, vp, vp]),
+            "orc_mean_knn_distance": (None, [vp, i64, C.c_int, vp]),
+            "orc_init_from_points": (None, [vp, vp, i64, i32, P(Cloud)]),
+            "orc_fit_frame_gaussians": (i32, [vp, vp, vp, i32, i32, d, d, d, d, P(FitCfg), P(Cloud)]),
+            "orc_estimate_relative_pose": (i32, [P(Cloud), vp, i32, i32, d, d, d, d, P(RelposeCfg), vp, vp, P(d)]),
+            "orc_bootstrap_trajectory": (i32, [vp, vp, vp, i32, i32, i32, d, d, d, d, P(FitCfg), P(RelposeCfg), vp,
+                                               vp]),
             "orc_joint_optimize": (i32, [P(Cloud), vp, i32, d, d, d, d, i32, i32, vp, P(JointCfg), i32, P(Rng),
                                          vp, vp]),
         }
@@ -610,6 +631,121 @@ def joint_optimize(cloud: HostCloud, images, intr, width, height, poses, cfg: Jo
     out = _from_c_cloud(cc)
     lib().orc_cloud_free(C.byref(cc))
     return st, out, P, tt, tl
+
+
+# ---------------------------------------------------------- bootstrap
+def fit_config(steps=100, unproject_points=50000, **kw) -> FitCfg:
+    """TrainConfig defaults of fit_frame_gaussians (trainer.hpp:21-60)."""
+    c = FitCfg()
+    c.steps, c.unproject_points = steps, unproject_points
+    c.pos_lr_start, c.pos_lr_end, c.rot_lr, c.scale_lr = 1.6e-2, 1.6e-4, 1e-3, 5e-3
+    c.opacity_lr, c.sh_dc_lr, c.sh_rest_lr, c.beta = 5e-2, 2.5e-3, 2.5e-3 / 20.0, 0.2
+    c.raster = default_raster_config()
+    for k, v in kw.items():
+        if k == "background":
+            for i in range(3):
+                c.background[i] = v[i]
+        else:
+            setattr(c, k, v)
+    return c
+
+
+def relpose_config(steps=200, **kw) -> RelposeCfg:
+    """TrainConfig / LossConfig defaults of estimate_relative_pose (trainer.hpp:43-45, losses.hpp:19)."""
+    c = RelposeCfg()
+    c.steps, c.lr_start, c.lr_end, c.beta, c.mask_threshold = steps, 1e-3, 1e-4, 0.2, 0.99
+    c.raster = default_raster_config()
+    for k, v in kw.items():
+        if k == "background":
+            for i in range(3):
+                c.background[i] = v[i]
+        else:
+            setattr(c, k, v)
+    return c
+
+
+def masked_rgb_loss(rendered, target, mask, beta=0.2, want_grad=True):
+    """losses.cpp:273-289; raises OracleError(5) on an empty mask."""
+    r = np.ascontiguousarray(rendered, np.float64)
+    t = np.ascontiguousarray(target, np.float64)
+    m = np.ascontiguousarray(mask, np.uint8).reshape(-1)
+    d = np.zeros_like(r) if want_grad else None
+    st = C.c_int32()
+    loss = lib().orc_masked_rgb_loss(_p(r), _p(t), r.shape[1], r.shape[0], _p(m), beta,
+                                     _p(d) if d is not None else None, C.byref(st))
+    if st.value:
+        raise OracleError(st.value, "masked_l1: no pixel passes the mask")
+    return (loss, d) if want_grad else loss
+
+
+def unproject(depth, valid, frame, intr, R, t, max_points):
+    dep = np.ascontiguousarray(depth, np.float64)
+    val = np.ascontiguousarray(valid, np.uint8)
+    img = np.ascontiguousarray(frame, np.float64)
+    H, W = dep.shape
+    pts, cols = np.zeros((max_points, 3)), np.zeros((max_points, 3))
+    Rm = np.ascontiguousarray(R, np.float64).reshape(9)
+    tv = np.ascontiguousarray(t, np.float64).reshape(3)
+    n = lib().orc_unproject(_p(dep), _p(val), W, H, _p(img), intr[0], intr[1], intr[2], intr[3], _p(Rm), _p(tv),
+                            max_points, _p(pts), _p(cols))
+    if n < 0:
+        raise OracleError(3, "unproject: empty validity mask")
+    return pts[:n].copy(), cols[:n].copy()
+
+
+def mean_knn_distance(points, k=3):
+    p = np.ascontiguousarray(points, np.float64)
+    out = np.zeros(p.shape[0])
+    lib().orc_mean_knn_distance(_p(p), p.shape[0], k, _p(out))
+    return out
+
+
+def init_from_points(points, colors, sh_degree=0) -> HostCloud:
+    p = np.ascontiguousarray(points, np.float64)
+    c = np.ascontiguousarray(colors, np.float64)
+    out = Cloud()
+    lib().orc_init_from_points(_p(p), _p(c), p.shape[0], sh_degree, C.byref(out))
+    res = _from_c_cloud(out)
+    lib().orc_cloud_free(C.byref(out))
+    return res
+
+
+def fit_frame_gaussians(frame, depth, valid, intr, cfg: FitCfg) -> HostCloud:
+    img = np.ascontiguousarray(frame, np.float64)
+    dep = np.ascontiguousarray(depth, np.float64)
+    val = np.ascontiguousarray(valid, np.uint8)
+    out = Cloud()
+    st = lib().orc_fit_frame_gaussians(_p(img), _p(dep), _p(val), img.shape[1], img.shape[0], intr[0], intr[1],
+                                       intr[2], intr[3], C.byref(cfg), C.byref(out))
+    if st:
+        raise OracleError(3, "unproject: empty validity mask")
+    res = _from_c_cloud(out)
+    lib().orc_cloud_free(C.byref(out))
+    return res
+
+
+def estimate_relative_pose(cloud: HostCloud, frame_next, intr, cfg: RelposeCfg):
+    """-> (pose12, ok, final_loss)."""
+    cv = cloud.c()
+    img = np.ascontiguousarray(frame_next, np.float64)
+    R, t, fl = np.zeros(9), np.zeros(3), C.c_double()
+    ok = lib().orc_estimate_relative_pose(cv.ref(), _p(img), img.shape[1], img.shape[0], intr[0], intr[1], intr[2],
+                                          intr[3], C.byref(cfg), _p(R), _p(t), C.byref(fl))
+    return pose_join(R.reshape(3, 3), t), bool(ok), fl.value
+
+
+def bootstrap_trajectory(frames, depths, valids, intr, fit: FitCfg, rel: RelposeCfg):
+    n = len(frames)
+    fr = [np.ascontiguousarray(f, np.float64) for f in frames]
+    de = [np.ascontiguousarray(d, np.float64) for d in depths]
+    va = [np.ascontiguousarray(v, np.uint8) for v in valids]
+    arr = lambda xs: C.cast((C.c_void_p * n)(*[x.ctypes.data for x in xs]), C.c_void_p)  # noqa: E731
+    poses, ok = np.zeros((n, 12)), np.zeros(max(n - 1, 1), np.int32)
+    st = lib().orc_bootstrap_trajectory(arr(fr), arr(de), arr(va), n, fr[0].shape[1], fr[0].shape[0], intr[0],
+                                        intr[1], intr[2], intr[3], C.byref(fit), C.byref(rel), _p(poses), _p(ok))
+    if st:
+        raise OracleError(3, "unproject: empty validity mask")
+    return poses, ok[:n - 1].astype(bool)
 
 
 # --------------------------------------------------------------- gradcheck

@@ -55,7 +55,8 @@ int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc, b
 int launch_backward_geom(cudaStream_t st, const gsb_cloud* cloud, gsb_frame* f, const RasterDev& rc, bool full,
                          float* grads, int64_t* launches);
 int launch_rgb_loss(cudaStream_t st, const float* ren, const float* tgt, int W, int H, double beta, float* gmaps,
-                    double* block_sums, double* out3, float* d_image, int64_t* launches);
+                    double* block_sums, double* out3, float* d_image, int64_t* launches, const float* mask_t = nullptr,
+                    double mask_thr = 0.0, void* mask_ws = nullptr);
 size_t loss_block_count(int W, int H);
 int init_loss_constants();
 int init_loss_attributes();
@@ -601,17 +602,20 @@ static int upload_image(gsb_ctx* ctx, const double* img, int W, int H, float* de
 }
 
 // Loss on the frame's image (buffers sized by frame_reserve or here).
-static int loss_device(gsb_ctx* ctx, gsb_frame* f, const float* target, double beta, bool want_grad) {
+// mask_t (nullable): masked_rgb_loss on accum = 1 - mask_t > mask_thr.
+static int loss_device(gsb_ctx* ctx, gsb_frame* f, const float* target, double beta, bool want_grad,
+                       const float* mask_t = nullptr, double mask_thr = 0.0) {
   const int W = f->width, H = f->height;
   const int64_t P = std::max<int64_t>((int64_t)W * H, 1);
   GSB_RESERVE(f->gmaps, sizeof(float) * 9 * P);
   GSB_RESERVE(f->loss_blocks, sizeof(double) * 2 * loss_block_count(W, H));
   GSB_RESERVE(f->loss_val, sizeof(double) * 4);
+  if (mask_t) GSB_RESERVE(f->mask_ws, 64);
   if (want_grad) GSB_RESERVE(f->d_image, sizeof(float) * 3 * P);
   StageScope sc(ctx, kStLoss);
   int r = launch_rgb_loss(ctx->stream, f->image.as<float>(), target, W, H, beta, f->gmaps.as<float>(),
                           f->loss_blocks.as<double>(), f->loss_val.as<double>(), want_grad ? f->d_image.as<float>() : nullptr,
-                          &ctx->launches);
+                          &ctx->launches, mask_t, mask_thr, mask_t ? f->mask_ws.p : nullptr);
   if (r) return r;
   if (want_grad) f->has_dimage = true;
   return GSB_OK;
@@ -882,7 +886,7 @@ int gsb_frame_destroy(gsb_frame* f) {
                     &f->colj, &f->off_g, &f->vis_idx, &f->dkey[0], &f->dkey[1], &f->dval[0], &f->dval[1], &f->rec, &f->aux,
                     &f->cnt_r, &f->ekey[0], &f->ekey[1], &f->eval_[0], &f->eval_[1], &f->ranges, &f->image,
                     &f->final_t, &f->pixstate, &f->d_image, &f->partials, &f->pose_blocks, &f->d_pose,
-                    &f->loss_blocks, &f->loss_val, &f->gmaps, &f->scan_tmp, &f->sort_hist, &f->counters,
+                    &f->loss_blocks, &f->loss_val, &f->mask_ws, &f->gmaps, &f->scan_tmp, &f->sort_hist, &f->counters,
                     &f->aux_g, &f->tile_hist, &f->tile_scan, &f->tile_big, &f->ent_key, &f->ent_gid};
   for (DevBuf* b : bufs) b->release();
   delete f;
@@ -1069,6 +1073,69 @@ int gsb_frame_rgb_loss(gsb_ctx* ctx, gsb_frame* f, gsb_image* target, double bet
     GSB_CUDA(cudaStreamSynchronize(ctx->stream));
     *loss_out = out3[2];
   }
+  return GSB_OK;
+}
+
+// masked_rgb_loss (losses.cpp:273-289) on host FP64 images and a host mask.
+// The mask enters the device loss as a transmittance plane (0 where set, 1
+// elsewhere) with threshold 0.5, i.e. through the same kernels as the
+// frame-resident variant below.
+int gsb_masked_rgb_loss(gsb_ctx* ctx, const double* rendered, const double* target, int32_t W, int32_t H,
+                        const uint8_t* mask, double beta, double* loss_out, double* d_rendered) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!rendered || !target || !mask || W <= 0 || H <= 0) return fail(GSB_ERR_INVALID_ARGUMENT, "bad images / mask");
+  const int64_t P = (int64_t)W * H;
+  int64_t count = 0;
+  for (int64_t p = 0; p < P; ++p) count += mask[p] != 0;
+  if (count == 0) return fail(GSB_ERR_EMPTY_MASK, "masked_l1: no pixel passes the mask");
+  static thread_local gsb_frame* work = nullptr;
+  static thread_local DevBuf tgt, mplane;
+  if (!work || work->ctx != ctx) {
+    work = new gsb_frame();
+    work->ctx = ctx;
+  }
+  work->width = W;
+  work->height = H;
+  GSB_RESERVE(work->image, sizeof(float) * 3 * P);
+  GSB_RESERVE(tgt, sizeof(float) * 3 * P);
+  GSB_RESERVE(mplane, sizeof(float) * P);
+  if (int r = upload_image(ctx, rendered, W, H, work->image.as<float>())) return r;
+  if (int r = upload_image(ctx, target, W, H, tgt.as<float>())) return r;
+  std::vector<float> mt(P);
+  for (int64_t p = 0; p < P; ++p) mt[p] = mask[p] ? 0.f : 1.f;
+  GSB_CUDA(cudaMemcpyAsync(mplane.p, mt.data(), sizeof(float) * P, cudaMemcpyHostToDevice, ctx->stream));
+  if (int r = loss_device(ctx, work, tgt.as<float>(), beta, d_rendered != nullptr, mplane.as<float>(), 0.5)) return r;
+  double out3[4];
+  GSB_CUDA(cudaMemcpyAsync(out3, work->loss_val.p, sizeof(double) * 3, cudaMemcpyDeviceToHost, ctx->stream));
+  if (d_rendered)
+    if (int r = download_image(ctx, work->d_image.as<float>(), W, H, d_rendered)) return r;
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (loss_out) *loss_out = out3[2];
+  return GSB_OK;
+}
+
+// masked_rgb_loss of the frame's image with the frame's own transmittance
+// mask (transmittance_mask(accum, threshold), losses.cpp:259-263); the
+// gradient stays in the frame. GSB_ERR_EMPTY_MASK (masked_out = 0) when no
+// pixel passes, like masked_l1's empty_mask.
+int gsb_frame_masked_rgb_loss(gsb_ctx* ctx, gsb_frame* f, gsb_image* target, double beta, double threshold,
+                              double* loss_out, int64_t* masked_out) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!f || !f->valid || !target) return fail(GSB_ERR_INVALID_ARGUMENT, "frame / target missing");
+  if (target->width != f->width || target->height != f->height)
+    return fail(GSB_ERR_DIMENSION_MISMATCH, "masked_rgb_loss: image shapes differ");
+  if (int r = loss_device(ctx, f, target->planes.as<float>(), beta, true, f->final_t.as<float>(), threshold)) return r;
+  double out3[4];
+  uint64_t counts[2];
+  GSB_CUDA(cudaMemcpyAsync(out3, f->loss_val.p, sizeof(double) * 3, cudaMemcpyDeviceToHost, ctx->stream));
+  GSB_CUDA(cudaMemcpyAsync(counts, f->mask_ws.p, sizeof(counts), cudaMemcpyDeviceToHost, ctx->stream));
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (masked_out) *masked_out = (int64_t)counts[0];
+  if (counts[0] == 0) {
+    f->has_dimage = false;
+    return fail(GSB_ERR_EMPTY_MASK, "masked_l1: no pixel passes the mask");
+  }
+  if (loss_out) *loss_out = out3[2];
   return GSB_OK;
 }
 

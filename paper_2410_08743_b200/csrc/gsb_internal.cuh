@@ -273,6 +273,7 @@ struct gsb_frame {
   // loss
   gsb::DevBuf loss_blocks;// double [blocks][2]
   gsb::DevBuf loss_val;   // double[2] (l1, ssim)
+  gsb::DevBuf mask_ws;    // masked_rgb_loss counts + norms (2 u64 + 4 doubles)
   gsb::DevBuf gmaps;      // FP32 [9][P] ssim gradient maps
   // scan / sort scratch
   gsb::DevBuf scan_tmp;

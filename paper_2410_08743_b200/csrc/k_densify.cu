@@ -183,12 +183,60 @@ __global__ void densify_adam_remap_kernel(const float* __restrict__ m, const flo
   }
 }
 
+// mean_knn_distance (scene.cpp:115-180) for k = 3, brute force over shared
+// memory tiles (the exact k nearest distances, like the reference's grid
+// search), FP64 with explicit rounding: sqrt(dx^2 + dy^2 + dz^2).
+constexpr int kKnnTile = 256;
+__global__ void __launch_bounds__(kKnnTile) knn3_mean_kernel(const double* __restrict__ pts, int64_t n,
+                                                             double* __restrict__ out) {
+  __shared__ double s[3][kKnnTile];
+  const int64_t i = (int64_t)blockIdx.x * kKnnTile + threadIdx.x;
+  double px = 0, py = 0, pz = 0;
+  if (i < n) {
+    px = pts[3 * i];
+    py = pts[3 * i + 1];
+    pz = pts[3 * i + 2];
+  }
+  double b0 = INFINITY, b1 = INFINITY, b2 = INFINITY;
+  for (int64_t t0 = 0; t0 < n; t0 += kKnnTile) {
+    const int64_t j = t0 + threadIdx.x;
+    __syncthreads();
+    for (int k = 0; k < 3; ++k) s[k][threadIdx.x] = j < n ? pts[3 * j + k] : 0.0;
+    __syncthreads();
+    const int m = (int)min((int64_t)kKnnTile, n - t0);
+    for (int q = 0; q < m; ++q) {
+      if (t0 + q == i) continue;
+      const double dx = s_(s[0][q], px), dy = s_(s[1][q], py), dz = s_(s[2][q], pz);
+      const double d = sqrt(a_(a_(m_(dx, dx), m_(dy, dy)), m_(dz, dz)));
+      if (d < b2) {  // insertion into the sorted best three
+        if (d < b1) {
+          b2 = b1;
+          if (d < b0) {
+            b1 = b0;
+            b0 = d;
+          } else {
+            b1 = d;
+          }
+        } else {
+          b2 = d;
+        }
+      }
+    }
+  }
+  if (i < n) out[i] = a_(a_(b0, b1), b2) / 3.0;
+}
+
 static unsigned grid_of(int64_t n) { return (unsigned)std::max<int64_t>((n + kDenBlock - 1) / kDenBlock, 1); }
 
 int launch_grad_accum(cudaStream_t st, const float* grads, int nplanes, int64_t n_pad, int64_t n,
                       const uint32_t* cnt_g, double scale, double* gsum, int32_t* gcnt) {
   if (n > 0) grad_accum_kernel<<<grid_of(n), kDenBlock, 0, st>>>(grads, nplanes, n_pad, n, cnt_g, scale, gsum, gcnt);
   GSB_CHECK_LAUNCH("grad_accum_kernel");
+  return GSB_OK;
+}
+int launch_knn3_mean(cudaStream_t st, const double* pts, int64_t n, double* out) {
+  if (n > 0) knn3_mean_kernel<<<(unsigned)((n + kKnnTile - 1) / kKnnTile), kKnnTile, 0, st>>>(pts, n, out);
+  GSB_CHECK_LAUNCH("knn3_mean_kernel");
   return GSB_OK;
 }
 int densify_bbox_blocks() { return 148; }

@@ -30,6 +30,18 @@ constexpr int kSW = kTW + 2 * kHalf, kSH = kTH + 2 * kHalf;  // 42 x 42
 constexpr int kThr = 256;
 __constant__ double c_win[kWin];
 
+// Transmittance mask of masked_rgb_loss (losses.cpp:259-289): pixel p takes
+// part iff accum = 1 - final_T > thr; norms (device) = {L1 norm, SSIM scale,
+// masked count, masked valid-window count} from mask_count / mask_norms.
+struct MaskArgs {
+  const float* final_t;  // nullptr: unmasked rgb_loss (host norms)
+  double thr;
+  const double* norms;
+};
+__device__ __forceinline__ bool mask_at(const MaskArgs& m, int64_t p) {
+  return !m.final_t || (1.0 - (double)m.final_t[p]) > m.thr;
+}
+
 __device__ __forceinline__ double m_(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double a_(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double s_(double a, double b) { return __dsub_rn(a, b); }
@@ -114,7 +126,8 @@ __device__ __forceinline__ void hpass5(const float (*st)[kSH][kSW + 1], double (
 #endif
 __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, const float* __restrict__ tgt,
                                                          int W, int H, double scale, float* __restrict__ gmaps,
-                                                         double* __restrict__ block_sums) {
+                                                         double* __restrict__ block_sums, MaskArgs mk) {
+  if (mk.final_t) scale = mk.norms[1];
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float(*st)[kSH][kSW + 1] = reinterpret_cast<float(*)[kSH][kSW + 1]>(smem_raw);
   double(*hq)[kSH][kTW + 1] =
@@ -153,9 +166,10 @@ __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, 
       const int y = by + rg * kR + j;
       if (x >= W || y >= H) continue;
       const double a = st[0][rg * kR + j + kHalf][c + kHalf], b = st[1][rg * kR + j + kHalf][c + kHalf];
-      l1 += fabs(a - b);
       const int64_t p = (int64_t)y * W + x;
-      if (x >= kHalf && x < W - kHalf && y >= kHalf && y < H - kHalf) {
+      const bool in_mask = mask_at(mk, p);
+      if (in_mask) l1 += fabs(a - b);
+      if (in_mask && x >= kHalf && x < W - kHalf && y >= kHalf && y < H - kHalf) {
         const double ma = mv[0][j], mb = mv[1][j], eaa = mv[2][j], ebb = mv[3][j], eab = mv[4][j];
         // Pointwise SSIM terms with explicitly rounded (unfused) arithmetic in
         // the reference's expression order, so identical inputs cancel exactly
@@ -213,7 +227,12 @@ __device__ __forceinline__ void hpass3(const float (*st)[kSH][kSW + 1], double (
 
 __global__ void __launch_bounds__(kThr) loss_grad_kernel(const float* __restrict__ ren, const float* __restrict__ tgt,
                                                          const float* __restrict__ gmaps, int W, int H, double beta,
-                                                         double l1_norm, int has_ssim, float* __restrict__ d_image) {
+                                                         double l1_norm, int has_ssim, float* __restrict__ d_image,
+                                                         MaskArgs mk) {
+  if (mk.final_t) {
+    l1_norm = mk.norms[0];
+    has_ssim = mk.norms[3] > 0.0 ? has_ssim : 0;
+  }
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float(*st)[kSH][kSW + 1] = reinterpret_cast<float(*)[kSH][kSW + 1]>(smem_raw);
   double(*hq)[kSH][kTW + 1] =
@@ -253,7 +272,7 @@ __global__ void __launch_bounds__(kThr) loss_grad_kernel(const float* __restrict
       const int64_t p = (int64_t)y * W + x;
       const double a = ren[ch * P + p], b = tgt[ch * P + p];
       const double diff = a - b;
-      const double dl1 = diff == 0.0 ? 0.0 : (diff > 0.0 ? l1_norm : -l1_norm);
+      const double dl1 = (diff == 0.0 || !mask_at(mk, p)) ? 0.0 : (diff > 0.0 ? l1_norm : -l1_norm);
       const double dss = has_ssim ? a_(a_(cv[0][j], m_(m_(2.0, a), cv[1][j])), m_(b, cv[2][j])) : 0.0;
       d_image[ch * P + p] = (float)s_(m_(1.0 - beta, dl1), m_(beta, dss));
     }
@@ -264,7 +283,12 @@ __global__ void __launch_bounds__(kThr) loss_grad_kernel(const float* __restrict
 // Fixed-order reduction of the block partials; out = {l1_mean, ssim_mean, loss}.
 __global__ void __launch_bounds__(256) loss_finalize_kernel(const double* __restrict__ block_sums, int nb,
                                                             double l1_norm, double scale, int has_ssim, double beta,
-                                                            double* __restrict__ out) {
+                                                            double* __restrict__ out, MaskArgs mk) {
+  if (mk.final_t) {
+    l1_norm = mk.norms[0];
+    scale = mk.norms[1];
+    has_ssim = mk.norms[3] > 0.0 ? has_ssim : 0;
+  }
   __shared__ double s1[256], s2[256];
   double a = 0.0, b = 0.0;
   for (int i = threadIdx.x; i < nb; i += 256) {
@@ -290,6 +314,34 @@ __global__ void __launch_bounds__(256) loss_finalize_kernel(const double* __rest
   }
 }
 
+// Masked pixel counts (integer atomics: exact) for masked_rgb_loss.
+__global__ void mask_count_kernel(const float* __restrict__ final_t, int W, int H, double thr,
+                                  unsigned long long* __restrict__ counts) {
+  unsigned long long c1 = 0, c2 = 0;
+  const int64_t P = (int64_t)W * H;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+    if (!((1.0 - (double)final_t[p]) > thr)) continue;
+    const int x = (int)(p % W), y = (int)(p / W);
+    ++c1;
+    if (x >= kHalf && x < W - kHalf && y >= kHalf && y < H - kHalf) ++c2;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+    c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(counts, c1);
+    atomicAdd(counts + 1, c2);
+  }
+}
+__global__ void mask_norms_kernel(const unsigned long long* __restrict__ counts, double* __restrict__ norms) {
+  const double c1 = (double)counts[0], c2 = (double)counts[1];
+  norms[0] = c1 > 0.0 ? 1.0 / (3.0 * c1) : 0.0;
+  norms[1] = c2 > 0.0 ? 1.0 / (3.0 * c2) : 0.0;
+  norms[2] = c1;
+  norms[3] = c2;
+}
+
 // gaussian_window (losses.cpp:19-32), FP64 on host, into constant memory of
 // the current device. Called once per context (never inside graph capture).
 int init_loss_constants() {
@@ -313,17 +365,32 @@ int init_loss_attributes() {
   return GSB_OK;
 }
 
+// mask_t (nullable): final transmittance of the rendered frame; then the loss
+// is masked_rgb_loss with accum = 1 - T > mask_thr, and mask_ws (>= 48 bytes of
+// device scratch) receives the counts and norms ({l1 norm, ssim scale, count,
+// valid count} as doubles at offset 16).
 int launch_rgb_loss(cudaStream_t st, const float* ren, const float* tgt, int W, int H, double beta, float* gmaps,
-                    double* block_sums, double* out3, float* d_image, int64_t* launches) {
+                    double* block_sums, double* out3, float* d_image, int64_t* launches, const float* mask_t,
+                    double mask_thr, void* mask_ws) {
+  MaskArgs mk{mask_t, mask_thr, nullptr};
+  if (mask_t) {
+    unsigned long long* cnt = static_cast<unsigned long long*>(mask_ws);
+    mk.norms = reinterpret_cast<const double*>(cnt + 2);
+    GSB_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), st));
+    mask_count_kernel<<<148, 256, 0, st>>>(mask_t, W, H, mask_thr, cnt);
+    mask_norms_kernel<<<1, 1, 0, st>>>(cnt, reinterpret_cast<double*>(cnt + 2));
+    *launches += 2;
+  }
   const int64_t cnt_valid = (W > 2 * kHalf && H > 2 * kHalf) ? (int64_t)(W - 2 * kHalf) * (H - 2 * kHalf) : 0;
   const int has_ssim = cnt_valid > 0 ? 1 : 0;
   const double scale = has_ssim ? 1.0 / (3.0 * (double)cnt_valid) : 0.0;
   const double l1_norm = 1.0 / (3.0 * (double)W * (double)H);
   dim3 grid((W + kTW - 1) / kTW, (H + kTH - 1) / kTH);
-  loss_maps_kernel<<<grid, kThr, kMapsSmem, st>>>(ren, tgt, W, H, scale, gmaps, block_sums);
+  loss_maps_kernel<<<grid, kThr, kMapsSmem, st>>>(ren, tgt, W, H, scale, gmaps, block_sums, mk);
   if (d_image)
-    loss_grad_kernel<<<grid, kThr, kGradSmem, st>>>(ren, tgt, gmaps, W, H, beta, l1_norm, has_ssim, d_image);
-  loss_finalize_kernel<<<1, 256, 0, st>>>(block_sums, (int)(grid.x * grid.y), l1_norm, scale, has_ssim, beta, out3);
+    loss_grad_kernel<<<grid, kThr, kGradSmem, st>>>(ren, tgt, gmaps, W, H, beta, l1_norm, has_ssim, d_image, mk);
+  loss_finalize_kernel<<<1, 256, 0, st>>>(block_sums, (int)(grid.x * grid.y), l1_norm, scale, has_ssim, beta, out3,
+                                          mk);
   *launches += d_image ? 3 : 2;
   GSB_CHECK_LAUNCH("rgb_loss kernels");
   return GSB_OK;

@@ -21,6 +21,9 @@ LIB_PATH = os.path.join(PKG_DIR, "libgsb200.so")
 
 # include/gsb200.h status codes
 OK = 0
+ERR_DEGENERATE_CLOUD = 2
+ERR_NO_VALID_DEPTH = 3
+ERR_EMPTY_MASK = 5
 ERR_STATE_MISMATCH = 6
 ERR_DIMENSION_MISMATCH = 4
 ERR_DIVERGED = 10
@@ -138,6 +141,29 @@ class JointConfig(C.Structure):
         return c
 
 
+class BootstrapConfig(C.Structure):
+    """gsb_bootstrap_config: the TrainConfig / LossConfig knobs of the bootstrap path
+    (trainer.hpp:21-60, losses.hpp:19)."""
+    _fields_ = [("per_frame_fit_steps", C.c_int32), ("relpose_steps", C.c_int32), ("unproject_points", C.c_int32),
+                ("pos_lr_start", C.c_double), ("pos_lr_end", C.c_double), ("rot_lr", C.c_double),
+                ("scale_lr", C.c_double), ("opacity_lr", C.c_double), ("sh_dc_lr", C.c_double),
+                ("sh_rest_lr", C.c_double), ("relpose_lr_start", C.c_double), ("relpose_lr_end", C.c_double),
+                ("beta", C.c_double), ("mask_threshold", C.c_double), ("background", C.c_double * 3),
+                ("raster", RasterConfig)]
+
+    @staticmethod
+    def default(**kw) -> "BootstrapConfig":
+        c = BootstrapConfig()
+        lib().gsb_default_bootstrap_config(C.byref(c))
+        for k, v in kw.items():
+            if k == "background":
+                for i in range(3):
+                    c.background[i] = v[i]
+            else:
+                setattr(c, k, v)
+        return c
+
+
 def _sigs():
     P = C.POINTER
     d, i32, i64, u32, u64 = C.c_double, C.c_int32, C.c_int64, C.c_uint32, C.c_uint64
@@ -216,6 +242,16 @@ def _sigs():
         "gsb_rng_shuffle": (C.c_int, [P(u64), i32, _vp]),
         "gsb_cloud_load_ply": (C.c_int, [_vp, C.c_char_p, P(_vp)]),
         "gsb_cloud_save_ply": (C.c_int, [_vp, C.c_char_p]),
+        "gsb_masked_rgb_loss": (C.c_int, [_vp, _vp, _vp, i32, i32, _vp, d, P(d), _vp]),
+        "gsb_frame_masked_rgb_loss": (C.c_int, [_vp, _vp, _vp, d, d, P(d), P(i64)]),
+        "gsb_default_bootstrap_config": (None, [P(BootstrapConfig)]),
+        "gsb_unproject": (C.c_int, [_vp, _vp, i32, i32, _vp, _vp, _vp, i32, _vp, _vp, P(i64)]),
+        "gsb_init_from_points": (C.c_int, [_vp, _vp, _vp, i64, i32, P(_vp)]),
+        "gsb_fit_frame_gaussians": (C.c_int, [_vp, _vp, _vp, _vp, i32, i32, _vp, P(BootstrapConfig), P(_vp)]),
+        "gsb_estimate_relative_pose": (C.c_int, [_vp, _vp, _vp, i32, i32, _vp, P(BootstrapConfig), _vp, P(i32),
+                                                 P(d)]),
+        "gsb_bootstrap_trajectory": (C.c_int, [_vp, _vp, _vp, _vp, i32, i32, i32, _vp, P(BootstrapConfig), _vp,
+                                               _vp]),
     }
 
 
@@ -338,6 +374,10 @@ class Cloud:
         """load_cloud_ply (src/ply.cpp:62-148) straight into the device layout."""
         h = _vp()
         _check(lib().gsb_cloud_load_ply(ctx.h, os.fsencode(path), C.byref(h)))
+        return Cloud._wrap(ctx, h)
+
+    @staticmethod
+    def _wrap(ctx: Context, h) -> "Cloud":
         c = Cloud.__new__(Cloud)
         c.h, c.ctx = h, ctx
         n, dd, ad = C.c_int64(), C.c_int32(), C.c_int32()
@@ -737,3 +777,96 @@ class PoseRng:
 def synth_intrinsics(width: int, height: int):
     """synth.cpp:64-71: fx = fy = 0.75 W, c = (dim - 1) / 2."""
     return np.array([0.75 * width, 0.75 * width, 0.5 * (width - 1), 0.5 * (height - 1)])
+
+
+# ------------------------------------------------------- bootstrap path
+def masked_rgb_loss(ctx: Context, rendered: np.ndarray, target: np.ndarray, mask: np.ndarray, beta: float = 0.2,
+                    want_grad=True):
+    """gsopt::masked_rgb_loss (losses.cpp:273-289); mask: (H, W) or (H*W,) of 0/1."""
+    r = np.ascontiguousarray(rendered, np.float64)
+    t = np.ascontiguousarray(target, np.float64)
+    if r.shape != t.shape:
+        raise GsbError(ERR_DIMENSION_MISMATCH, "masked_rgb_loss: image shapes differ")
+    m = np.ascontiguousarray(mask, np.uint8).reshape(-1)
+    if m.size != r.shape[0] * r.shape[1]:
+        raise GsbError(ERR_DIMENSION_MISMATCH, "masked_l1: mask size mismatch")
+    loss = C.c_double()
+    d = np.zeros_like(r) if want_grad else None
+    _check(lib().gsb_masked_rgb_loss(ctx.h, _p(r), _p(t), r.shape[1], r.shape[0], _p(m), beta, C.byref(loss),
+                                     _p(d)))
+    return (loss.value, d) if want_grad else loss.value
+
+
+def frame_masked_rgb_loss(ctx: Context, frame: Frame, target: Image, beta: float, threshold: float):
+    """masked_rgb_loss(out.image, target, transmittance_mask(out.accum_transmittance, threshold))
+    on the device; returns (loss, masked pixel count)."""
+    loss, cnt = C.c_double(), C.c_int64()
+    _check(lib().gsb_frame_masked_rgb_loss(ctx.h, frame.h, target.h, beta, threshold, C.byref(loss),
+                                           C.byref(cnt)))
+    return loss.value, cnt.value
+
+
+def unproject(depth: np.ndarray, valid: np.ndarray, frame: np.ndarray, intr, world_to_cam12, max_points: int):
+    """gsopt::unproject (scene.cpp:209-243) -> (points (n,3), colors (n,3))."""
+    dep = np.ascontiguousarray(depth, np.float64)
+    val = np.ascontiguousarray(valid, np.uint8)
+    img = np.ascontiguousarray(frame, np.float64)
+    H, W = dep.shape
+    i4 = np.ascontiguousarray(intr, np.float64)
+    pose = np.ascontiguousarray(world_to_cam12, np.float64).reshape(12)
+    pts, cols, n = np.zeros((max(max_points, 1), 3)), np.zeros((max(max_points, 1), 3)), C.c_int64()
+    _check(lib().gsb_unproject(_p(dep), _p(val), W, H, _p(img), _p(i4), _p(pose), max_points, _p(pts), _p(cols),
+                               C.byref(n)))
+    return pts[:n.value].copy(), cols[:n.value].copy()
+
+
+def init_from_points(ctx: Context, points, colors, sh_degree: int = 0) -> Cloud:
+    """gsopt::init_from_points (scene.cpp:182-207), kNN scales computed on the device."""
+    p = np.ascontiguousarray(points, np.float64)
+    c = np.ascontiguousarray(colors, np.float64)
+    if p.shape != c.shape:
+        raise GsbError(ERR_DIMENSION_MISMATCH, "init_from_points: points/colors size mismatch")
+    h = _vp()
+    _check(lib().gsb_init_from_points(ctx.h, _p(p), _p(c), p.shape[0], sh_degree, C.byref(h)))
+    return Cloud._wrap(ctx, h)
+
+
+def fit_frame_gaussians(ctx: Context, frame, depth, valid, intr, config: BootstrapConfig | None = None) -> Cloud:
+    """gsopt::fit_frame_gaussians (pipelines.cpp:224-250)."""
+    cfg = config or BootstrapConfig.default()
+    img = np.ascontiguousarray(frame, np.float64)
+    dep = np.ascontiguousarray(depth, np.float64)
+    val = np.ascontiguousarray(valid, np.uint8)
+    i4 = np.ascontiguousarray(intr, np.float64)
+    h = _vp()
+    _check(lib().gsb_fit_frame_gaussians(ctx.h, _p(img), _p(dep), _p(val), img.shape[1], img.shape[0], _p(i4),
+                                         C.byref(cfg), C.byref(h)))
+    return Cloud._wrap(ctx, h)
+
+
+def estimate_relative_pose(ctx: Context, cloud: Cloud, frame_next, intr, config: BootstrapConfig | None = None):
+    """gsopt::estimate_relative_pose (pipelines.cpp:252-290) -> (pose12, ok, final_loss)."""
+    cfg = config or BootstrapConfig.default()
+    img = np.ascontiguousarray(frame_next, np.float64)
+    i4 = np.ascontiguousarray(intr, np.float64)
+    pose, ok, fl = np.zeros(12), C.c_int32(), C.c_double()
+    _check(lib().gsb_estimate_relative_pose(ctx.h, cloud.h, _p(img), img.shape[1], img.shape[0], _p(i4),
+                                            C.byref(cfg), _p(pose), C.byref(ok), C.byref(fl)))
+    return pose, bool(ok.value), fl.value
+
+
+def bootstrap_trajectory(ctx: Context, frames, depths, valids, intr, config: BootstrapConfig | None = None):
+    """gsopt::bootstrap_trajectory (pipelines.cpp:292-312) -> (world_to_cam (n,12), pair_ok (n-1,))."""
+    cfg = config or BootstrapConfig.default()
+    n = len(frames)
+    if n < 2 or len(depths) != n or len(valids) != n:
+        raise GsbError(ERR_INVALID_CONFIG, "bootstrap_trajectory: need >= 2 frames with depths")
+    fr = [np.ascontiguousarray(f, np.float64) for f in frames]
+    de = [np.ascontiguousarray(d, np.float64) for d in depths]
+    va = [np.ascontiguousarray(v, np.uint8) for v in valids]
+    arr = lambda xs: (C.c_void_p * n)(*[x.ctypes.data for x in xs])  # noqa: E731
+    i4 = np.ascontiguousarray(intr, np.float64)
+    poses, ok = np.zeros((n, 12)), np.zeros(n - 1, np.int32)
+    _check(lib().gsb_bootstrap_trajectory(ctx.h, arr(fr), arr(de), arr(va), n, fr[0].shape[1], fr[0].shape[0],
+                                          _p(i4), C.byref(cfg), _p(poses), _p(ok)))
+    return poses, ok.astype(bool)
