@@ -296,7 +296,8 @@ def run_joint(args, ws, rank, local, dist):
     cloud.synth(C4_SEED, log_scale_offset(C4_N))
     cloud.jitter(700, 0.05, 0.3)  # tests/test_trainer.cpp:598-601
     iters = args.warmup + args.steps
-    cfg = gsb.JointConfig.default(iterations=max(iters, 1000), sh_degree=SH_DEGREE, sh_degree_interval=0)
+    cfg = gsb.JointConfig.default(iterations=max(iters, 1000), sh_degree=SH_DEGREE, sh_degree_interval=0,
+                                  densify_interval=0)
     j = gsb.JointOptimizer(ctx, cloud, targets, intr, init, cfg, 800, local_views=1, comm=comm)
     j.step(args.warmup)
     if dist:

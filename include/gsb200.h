@@ -361,6 +361,26 @@ int gsb_joint_read(gsb_joint* j, double* poses_out, int64_t* steps_done, double*
 /* current cloud size, densify_and_prune events so far, last event's {cloned, split, pruned} */
 int gsb_joint_info(gsb_joint* j, int64_t* n_gaussians, int32_t* densify_events, int32_t last_report[3]);
 
+/* ---- small on-disk formats (host only; scene_io.cpp, image.cpp:105-141) ----
+ * f32map: "f32map W H scale\n" + W*H little-endian floats (values * scale on
+ * load). Pass values/depth = NULL to query the size first. */
+int gsb_load_float_map(const char* path, float* values, int64_t capacity, int32_t* width,
+                       int32_t* height);
+int gsb_save_float_map(const float* values, int32_t width, int32_t height, const char* path,
+                       double scale);
+/* f32map as load_scene's depth (scene_io.cpp:203-215): valid = finite && > 0. */
+int gsb_load_depth_map(const char* path, double* depth, uint8_t* valid, int64_t capacity,
+                       int32_t* width, int32_t* height);
+/* {"poses": [[12 numbers: row-major R|t world_to_cam], ...]} (scene_io.cpp:64-79),
+ * 17 significant digits (lossless). poses = NULL queries n. */
+int gsb_save_poses_json(const double* poses, int32_t n, const char* path);
+int gsb_load_poses_json(const char* path, double* poses, int32_t capacity, int32_t* n);
+/* cameras.json (load_cameras_json, scene_io.cpp:254-279): GSB_ERR_MISSING_INTRINSICS
+ * if fx/fy/cx/cy/width/height/frames is absent. poses / names optional. */
+int gsb_load_cameras_json(const char* path, double intr[4], int32_t size[2], double* poses,
+                          int32_t capacity, int32_t* n_frames, int32_t* has_poses, char* names,
+                          int64_t names_capacity);
+
 /* ---- bootstrap path (pipelines.cpp:224-312, scene.cpp:115-243) ----
  * RGB-D frames -> per-frame clouds -> relative poses -> an initial trajectory.
  * The TrainConfig knobs these read (trainer.hpp:21-60, losses.hpp:19). */

@@ -25,6 +25,8 @@ ERR_DEGENERATE_CLOUD = 2
 ERR_NO_VALID_DEPTH = 3
 ERR_EMPTY_MASK = 5
 ERR_STATE_MISMATCH = 6
+ERR_MISSING_INTRINSICS = 7
+ERR_CORRUPT_FILE = 9
 ERR_DIMENSION_MISMATCH = 4
 ERR_DIVERGED = 10
 ERR_INVALID_CONFIG = 11
@@ -242,6 +244,12 @@ def _sigs():
         "gsb_rng_shuffle": (C.c_int, [P(u64), i32, _vp]),
         "gsb_cloud_load_ply": (C.c_int, [_vp, C.c_char_p, P(_vp)]),
         "gsb_cloud_save_ply": (C.c_int, [_vp, C.c_char_p]),
+        "gsb_load_float_map": (C.c_int, [C.c_char_p, _vp, i64, P(i32), P(i32)]),
+        "gsb_save_float_map": (C.c_int, [_vp, i32, i32, C.c_char_p, d]),
+        "gsb_load_depth_map": (C.c_int, [C.c_char_p, _vp, _vp, i64, P(i32), P(i32)]),
+        "gsb_save_poses_json": (C.c_int, [_vp, i32, C.c_char_p]),
+        "gsb_load_poses_json": (C.c_int, [C.c_char_p, _vp, i32, P(i32)]),
+        "gsb_load_cameras_json": (C.c_int, [C.c_char_p, _vp, _vp, _vp, i32, P(i32), P(i32), C.c_char_p, i64]),
         "gsb_masked_rgb_loss": (C.c_int, [_vp, _vp, _vp, i32, i32, _vp, d, P(d), _vp]),
         "gsb_frame_masked_rgb_loss": (C.c_int, [_vp, _vp, _vp, d, d, P(d), P(i64)]),
         "gsb_default_bootstrap_config": (None, [P(BootstrapConfig)]),
@@ -870,3 +878,58 @@ def bootstrap_trajectory(ctx: Context, frames, depths, valids, intr, config: Boo
     _check(lib().gsb_bootstrap_trajectory(ctx.h, arr(fr), arr(de), arr(va), n, fr[0].shape[1], fr[0].shape[0],
                                           _p(i4), C.byref(cfg), _p(poses), _p(ok)))
     return poses, ok.astype(bool)
+
+
+# ------------------------------------------------------- on-disk formats
+def load_float_map(path: str) -> np.ndarray:
+    """load_float_map (image.cpp:105-126) -> float32 (H, W)."""
+    w, h = C.c_int32(), C.c_int32()
+    _check(lib().gsb_load_float_map(os.fsencode(path), None, 0, C.byref(w), C.byref(h)))
+    out = np.zeros((h.value, w.value), np.float32)
+    _check(lib().gsb_load_float_map(os.fsencode(path), _p(out), out.size, C.byref(w), C.byref(h)))
+    return out
+
+
+def save_float_map(values, path: str, scale: float = 1.0):
+    """save_float_map (image.cpp:128-141); values (H, W)."""
+    v = np.ascontiguousarray(values, np.float32)
+    _check(lib().gsb_save_float_map(_p(v), v.shape[1], v.shape[0], os.fsencode(path), scale))
+
+
+def load_depth_map(path: str):
+    """depth/<stem>.f32 as load_scene reads it -> (depth FP64 (H, W), valid uint8 (H, W))."""
+    w, h = C.c_int32(), C.c_int32()
+    _check(lib().gsb_load_depth_map(os.fsencode(path), None, None, 0, C.byref(w), C.byref(h)))
+    dep, val = np.zeros((h.value, w.value)), np.zeros((h.value, w.value), np.uint8)
+    _check(lib().gsb_load_depth_map(os.fsencode(path), _p(dep), _p(val), dep.size, C.byref(w), C.byref(h)))
+    return dep, val
+
+
+def save_poses_json(poses, path: str):
+    """save_poses_json (scene_io.cpp:64-68); poses (n, 12) row-major [R|t]."""
+    P_ = np.ascontiguousarray(np.asarray(poses, np.float64).reshape(-1, 12))
+    _check(lib().gsb_save_poses_json(_p(P_), P_.shape[0], os.fsencode(path)))
+
+
+def load_poses_json(path: str) -> np.ndarray:
+    """load_poses_json (scene_io.cpp:70-79) -> (n, 12)."""
+    n = C.c_int32()
+    _check(lib().gsb_load_poses_json(os.fsencode(path), None, 0, C.byref(n)))
+    out = np.zeros((n.value, 12))
+    _check(lib().gsb_load_poses_json(os.fsencode(path), _p(out), n.value, C.byref(n)))
+    return out
+
+
+def load_cameras_json(path: str) -> dict:
+    """load_cameras_json (scene_io.cpp:254-279) -> dict(intrinsics, width, height, poses, names, has_poses)."""
+    intr, size, n, hp = np.zeros(4), np.zeros(2, np.int32), C.c_int32(), C.c_int32()
+    _check(lib().gsb_load_cameras_json(os.fsencode(path), _p(intr), _p(size), None, 0, C.byref(n), C.byref(hp),
+                                       None, 0))
+    poses = np.zeros((n.value, 12))
+    cap = max(os.path.getsize(path) + 1, 1)
+    names = C.create_string_buffer(cap)
+    _check(lib().gsb_load_cameras_json(os.fsencode(path), _p(intr), _p(size), _p(poses), n.value, C.byref(n),
+                                       C.byref(hp), names, cap))
+    nm = names.value.decode()
+    return dict(intrinsics=intr, width=int(size[0]), height=int(size[1]), poses=poses,
+                names=nm.split("\n") if n.value else [], has_poses=bool(hp.value))
