@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "gsb_internal.cuh"
@@ -571,6 +572,27 @@ static int frame_setup(gsb_ctx* ctx, gsb_frame* f, const gsb_cloud* cloud, const
   return GSB_OK;
 }
 
+// Host-side (de)interleave of an image between the caller's FP64 HWC buffer
+// and the pinned FP32 planes, split over the host cores for frame-sized
+// images (it is the e2e path's only O(pixels) host work).
+template <typename F>
+static void host_parallel(size_t n, F fn) {
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const size_t chunks = n < (size_t)1 << 16 ? 1 : std::min<size_t>(hw, (n + 65535) / 65536);
+  if (chunks <= 1) {
+    fn((size_t)0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const size_t step = (n + chunks - 1) / chunks;
+  for (size_t c = 1; c < chunks; ++c) {
+    const size_t b = c * step, e = std::min(n, b + step);
+    if (b < e) th.emplace_back([=, &fn] { fn(b, e); });
+  }
+  fn((size_t)0, std::min(n, step));
+  for (auto& t : th) t.join();
+}
+
 // planar FP32 [3][P] -> interleaved FP64 host
 static int download_image(gsb_ctx* ctx, const float* dev_planes, int W, int H, double* out) {
   const size_t P = (size_t)W * H;
@@ -578,11 +600,13 @@ static int download_image(gsb_ctx* ctx, const float* dev_planes, int W, int H, d
   if (!h) return fail(GSB_ERR_OUT_OF_MEMORY, "pinned staging");
   GSB_CUDA(cudaMemcpyAsync(h, dev_planes, sizeof(float) * 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
   GSB_CUDA(cudaStreamSynchronize(ctx->stream));
-  for (size_t p = 0; p < P; ++p) {
-    out[3 * p] = h[p];
-    out[3 * p + 1] = h[P + p];
-    out[3 * p + 2] = h[2 * P + p];
-  }
+  host_parallel(P, [&](size_t b, size_t e) {
+    for (size_t p = b; p < e; ++p) {
+      out[3 * p] = h[p];
+      out[3 * p + 1] = h[P + p];
+      out[3 * p + 2] = h[2 * P + p];
+    }
+  });
   return GSB_OK;
 }
 // interleaved FP64 host -> planar FP32 device
@@ -591,11 +615,17 @@ static int upload_image(gsb_ctx* ctx, const double* img, int W, int H, float* de
   float* h = static_cast<float*>(pinned(ctx, sizeof(float) * 3 * P));
   if (!h) return fail(GSB_ERR_OUT_OF_MEMORY, "pinned staging");
   GSB_CUDA(cudaStreamSynchronize(ctx->stream));  // staging buffer reuse
-  for (size_t p = 0; p < P; ++p) {
-    h[p] = (float)img[3 * p];
-    h[P + p] = (float)img[3 * p + 1];
-    h[2 * P + p] = (float)img[3 * p + 2];
-  }
+  const double t0 = debug_on() ? now_ms() : 0.0;
+  host_parallel(P, [&](size_t b, size_t e) {
+    for (size_t p = b; p < e; ++p) {
+      h[p] = (float)img[3 * p];
+      h[P + p] = (float)img[3 * p + 1];
+      h[2 * P + p] = (float)img[3 * p + 2];
+    }
+  });
+  if (debug_on())
+    std::fprintf(stderr, "[gsb] upload_image: convert %.2f ms (%u threads)\n", now_ms() - t0,
+                 std::thread::hardware_concurrency());
   GSB_CUDA(cudaMemcpyAsync(dev_planes, h, sizeof(float) * 3 * P, cudaMemcpyHostToDevice, ctx->stream));
   GSB_CUDA(cudaStreamSynchronize(ctx->stream));
   return GSB_OK;
@@ -714,6 +744,8 @@ int gsb_ctx_destroy(gsb_ctx* ctx) {
   delete ctx->timer;
   if (ctx->work) gsb_frame_destroy(ctx->work);
   for (gsb_frame* f : ctx->frame_pool) gsb_frame_destroy(f);
+  for (DevBuf& b : ctx->image_pool) b.release();
+  ctx->image_pool.clear();
   if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
   if (ctx->ev_stop) cudaEventDestroy(ctx->ev_stop);
   cudaStreamDestroy(ctx->stream);
@@ -1011,12 +1043,23 @@ int gsb_image_create(gsb_ctx* ctx, const double* img, int32_t W, int32_t H, gsb_
   im->ctx = ctx;
   im->width = W;
   im->height = H;
-  cudaError_t e = im->planes.reserve(sizeof(float) * 3 * (size_t)W * H);
+  const double t0 = debug_on() ? now_ms() : 0.0;
+  const size_t need = sizeof(float) * 3 * (size_t)W * H;
+  for (size_t i = 0; i < ctx->image_pool.size(); ++i)  // a destroyed image's planes of a fitting size
+    if (ctx->image_pool[i].bytes >= need && ctx->image_pool[i].bytes <= 2 * need + 4096) {
+      im->planes = ctx->image_pool[i];
+      ctx->image_pool.erase(ctx->image_pool.begin() + (ptrdiff_t)i);
+      break;
+    }
+  cudaError_t e = im->planes.reserve(need);
   if (e != cudaSuccess) {
     delete im;
     return cuda_fail(e, "image alloc");
   }
-  if (int r = upload_image(ctx, img, W, H, im->planes.as<float>())) {
+  const double t1 = debug_on() ? now_ms() : 0.0;
+  const int ru = upload_image(ctx, img, W, H, im->planes.as<float>());
+  if (debug_on()) std::fprintf(stderr, "[gsb] image_create: alloc %.2f upload %.2f ms\n", t1 - t0, now_ms() - t1);
+  if (int r = ru) {
     im->planes.release();
     delete im;
     return r;
@@ -1029,6 +1072,10 @@ int gsb_image_destroy(gsb_image* im) {
   if (!im) return GSB_OK;
   cudaSetDevice(im->ctx->device);
   cudaStreamSynchronize(im->ctx->stream);
+  if (im->planes.p && im->ctx->image_pool.size() < 64) {  // keep the planes for the next image of this size
+    im->ctx->image_pool.push_back(im->planes);
+    im->planes = DevBuf();
+  }
   im->planes.release();
   delete im;
   return GSB_OK;
@@ -1939,20 +1986,30 @@ int gsb_estimate_poses(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* const* targets
   if (!targets || !init_poses || !poses_out || count <= 0) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
   std::vector<gsb_session*> ss(count, nullptr);
   int r = GSB_OK;
+  double t[6] = {debug_on() ? now_ms() : 0.0};
   for (int32_t i = 0; i < count && !r; ++i)
     r = gsb_session_create(ctx, cloud, targets[i], intr, init_poses + 12 * (size_t)i, cfg, &ss[i]);
+  if (debug_on()) t[1] = now_ms();
   gsb_pose_batch* b = nullptr;
   if (!r) r = gsb_pose_batch_create(ctx, ss.data(), count, &b);
+  if (debug_on()) t[2] = now_ms();
   if (!r) r = gsb_pose_batch_step(ctx, b, cfg->budget);
+  if (debug_on()) t[3] = now_ms();
   for (int32_t i = 0; i < count && !r; ++i) {
     int32_t su = 0;
     r = gsb_session_read(ss[i], nullptr, poses_out + 12 * (size_t)i, final_losses ? final_losses + i : nullptr, &su,
                          nullptr, nullptr);
     if (!r && steps_used) steps_used[i] = su;
   }
+  if (debug_on()) t[4] = now_ms();
   if (b) gsb_pose_batch_destroy(b);
   for (gsb_session* s : ss)
     if (s) gsb_session_destroy(s);
+  if (debug_on()) {
+    t[5] = now_ms();
+    std::fprintf(stderr, "[gsb] estimate_poses: create %.2f batch %.2f step %.2f read %.2f destroy %.2f ms\n",
+                 t[1] - t[0], t[2] - t[1], t[3] - t[2], t[4] - t[3], t[5] - t[4]);
+  }
   return r;
 }
 

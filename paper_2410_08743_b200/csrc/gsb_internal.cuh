@@ -187,6 +187,7 @@ struct gsb_ctx {
   cudaEvent_t (*stage_events)[2] = nullptr;  // set while capturing a profiled session graph
   int binning = 0;             // gsb::Binning preference (gsb_ctx_set_binning)
   std::vector<gsb_frame*> frame_pool;  // sized forward states returned by pose batches, reused
+  std::vector<gsb::DevBuf> image_pool;  // target-image planes of destroyed gsb_images, reused by size
 };
 
 struct gsb_cloud {

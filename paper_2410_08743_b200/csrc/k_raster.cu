@@ -156,6 +156,20 @@ struct __align__(16) StagedSplat {
   uint32_t pad[2];
 };
 
+// Shared-window loads from a 32-bit shared address computed once per kernel
+// (otherwise the generic->shared conversion is rematerialised in the inner
+// loops under register pressure: S2R SR_CgaCtaId + LEA per entry).
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float lds_f1(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+
 struct PixFwd {
   float T, r, g, b;
   uint32_t processed;
@@ -502,6 +516,9 @@ __device__ __forceinline__ bool backward_pair(PixBwd& a, PixBwd& b, const float4
   return true;
 }
 
+#ifndef GSB_LDS_ASM
+#define GSB_LDS_ASM 1
+#endif
 #ifndef GSB_BWD_MIN_BLOCKS
 #define GSB_BWD_MIN_BLOCKS 8
 #endif
@@ -534,6 +551,7 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
   const double ox = (double)(tx * kTile), oy = (double)(ty * kTile);
   const float px = (float)lx, py = (float)ly;
   const uint2 range = ranges[tile];
+  const uint32_t sp_base = (uint32_t)__cvta_generic_to_shared(s_sp);
 
   PixBwd a, b;
   load_pixel_bwd(a, x, y, W, H, npix, bg_r, bg_g, bg_b, d_image, final_t, pixstate);
@@ -570,10 +588,17 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
         const int k = s_list[warp][i];
         const uint32_t j = b0 + (uint32_t)k;
         if (j >= wmax) continue;  // warp-uniform
-        const StagedSplat& S = s_sp[k];
-        const float4 ge = S.geo;
-        const float4 ap = S.app;
-        const float cb = S.col_b;
+#if GSB_LDS_ASM
+        const uint32_t sa = sp_base + (uint32_t)k * (uint32_t)sizeof(StagedSplat);
+        const float4 ge = lds_f4(sa);
+        const float4 ap = lds_f4(sa + 16u);
+        const float cb = lds_f1(sa + 32u);
+#else
+        const float4 ge = s_sp[k].geo;
+        const float4 ap = s_sp[k].app;
+        const float cb = s_sp[k].col_b;
+        (void)sp_base;
+#endif
         float v[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) v[c] = 0.f;
