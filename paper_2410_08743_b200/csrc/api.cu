@@ -393,6 +393,7 @@ static int frame_reserve(gsb_frame* f, const gsb_cloud* cloud, int64_t k_cap) {
                                std::max(radix_hist_words(n, 32), radix_hist_words(k_cap, tile_bits(n_tiles))));
   GSB_CUDA(f->sort_hist.reserve(sizeof(uint32_t) * hist, &grew));
   GSB_CUDA(f->ranges.reserve(sizeof(uint2) * n_tiles, &grew));
+  GSB_CUDA(f->tile_cut.reserve(sizeof(double2) * n_tiles, &grew));
   GSB_CUDA(f->image.reserve(sizeof(float) * 3 * npix, &grew));
   GSB_CUDA(f->final_t.reserve(sizeof(float) * npix, &grew));
   GSB_CUDA(f->pixstate.reserve(sizeof(uint32_t) * npix, &grew));
@@ -916,7 +917,7 @@ int gsb_frame_destroy(gsb_frame* f) {
   cudaStreamSynchronize(f->ctx->stream);
   DevBuf* bufs[] = {&f->cam, &f->rec_g, &f->rect_g, &f->cnt_g, &f->depth_g, &f->radius_g, &f->rank_of_g,
                     &f->colj, &f->off_g, &f->vis_idx, &f->dkey[0], &f->dkey[1], &f->dval[0], &f->dval[1], &f->rec, &f->aux,
-                    &f->cnt_r, &f->ekey[0], &f->ekey[1], &f->eval_[0], &f->eval_[1], &f->ranges, &f->image,
+                    &f->cnt_r, &f->ekey[0], &f->ekey[1], &f->eval_[0], &f->eval_[1], &f->ranges, &f->tile_cut, &f->image,
                     &f->final_t, &f->pixstate, &f->d_image, &f->partials, &f->pose_blocks, &f->d_pose,
                     &f->loss_blocks, &f->loss_val, &f->mask_ws, &f->gmaps, &f->scan_tmp, &f->sort_hist, &f->counters,
                     &f->aux_g, &f->tile_hist, &f->tile_scan, &f->tile_big, &f->ent_key, &f->ent_gid};

@@ -268,7 +268,8 @@ struct gsb_frame {
   gsb::DevBuf pixstate;   // uint32 contrib | overflow << 29
   gsb::DevBuf d_image;    // FP32 planes [3][P]
   // backward
-  gsb::DevBuf partials;   // float [K][9] at pre-sort positions
+  gsb::DevBuf partials;   // float [K][9] at pre-sort positions (live entries only)
+  gsb::DevBuf tile_cut;   // double2 per tile: (FP64 depth, gid) of the last replayed entry, depth -1 if none
   gsb::DevBuf pose_blocks;// double [blocks][6]
   gsb::DevBuf d_pose;     // double[6]
   // loss

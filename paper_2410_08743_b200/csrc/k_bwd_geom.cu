@@ -56,6 +56,16 @@ constexpr int kGeomBlock = 256;
 #endif
 constexpr int kGeomPlanes = kOpacity + 1;  // means, quat, log-scale, opacity
 
+// Where K4b finds each splat's tile rect (tile-local binning: aux_g; global:
+// rect_g) and the per-tile cut K4a wrote (k_raster.cu).
+struct EntryCut {
+  const double2* tile_cut;
+  const double* depth_g;
+  const SplatAux* aux_g;
+  const uint2* rect_g;
+  int32_t tiles_x;
+};
+
 // R: arithmetic type of the per-splat chain — double for the full gradient
 // bundle (joint_optimize's parameter gradients), float for the pose-only
 // path (the 6-vector itself is accumulated in FP64 either way).
@@ -64,10 +74,12 @@ __global__ void __launch_bounds__(kGeomBlock, (kFull ? 2 : GSB_GEOM_POSE_MIN_BLO
     const float* __restrict__ params, int64_t n, int64_t n_pad_g, int sh_cap, int sh_active,
     const CamDev* __restrict__ cam_p, RasterDev rc, const uint32_t* __restrict__ cnt_g,
     const uint32_t* __restrict__ off_g, const float* __restrict__ colj, const float* __restrict__ partials,
-    int64_t k_cap, float* __restrict__ grads, double* __restrict__ pose_blocks) {
+    int64_t k_cap, const EntryCut cutd, float* __restrict__ grads, double* __restrict__ pose_blocks) {
   __shared__ __align__(128) float s_par[kGeomPlanes * kGeomBlock];
   __shared__ __align__(128) float s_colj[9 * kGeomBlock];
   __shared__ __align__(128) uint32_t s_cnt[kGeomBlock], s_off[kGeomBlock];
+  __shared__ __align__(128) uint4 s_rect[kGeomBlock];  // SplatAux (tile-local) or uint2 rect pairs (global)
+  __shared__ __align__(128) double s_dep[kGeomBlock];
   __shared__ CamDev cam;
   __shared__ double s_pose[8][6];
   __shared__ __align__(8) uint64_t bar;
@@ -77,8 +89,15 @@ __global__ void __launch_bounds__(kGeomBlock, (kFull ? 2 : GSB_GEOM_POSE_MIN_BLO
     mbar_init(&bar, 1);
     const int64_t here = n - i0 < kGeomBlock ? n - i0 : kGeomBlock;
     const uint32_t bytes = (uint32_t)(((here * 4) + 15) & ~(int64_t)15);
+    const uint32_t b8 = (uint32_t)(((here * 8) + 15) & ~(int64_t)15);
+    const uint32_t brect = cutd.aux_g ? (uint32_t)(here * 16) : b8;
     // cnt_g / off_g are sized to whole 256-blocks (frame_reserve), colj to n_pad
-    mbar_arrive_expect_tx(&bar, bytes * (kGeomPlanes + 9 + 2));
+    mbar_arrive_expect_tx(&bar, bytes * (kGeomPlanes + 9 + 2) + b8 + brect);
+    tma_load_1d(s_dep, cutd.depth_g + i0, b8, &bar);
+    if (cutd.aux_g)
+      tma_load_1d(s_rect, cutd.aux_g + i0, brect, &bar);
+    else
+      tma_load_1d(s_rect, cutd.rect_g + i0, brect, &bar);
     for (int p = 0; p < kGeomPlanes; ++p) tma_load_1d(s_par + p * kGeomBlock, params + p * n_pad_g + i0, bytes, &bar);
     for (int p = 0; p < 9; ++p) tma_load_1d(s_colj + p * kGeomBlock, colj + p * n_pad_g + i0, bytes, &bar);
     tma_load_1d(s_cnt, cnt_g + i0, bytes, &bar);
@@ -102,21 +121,45 @@ __global__ void __launch_bounds__(kGeomBlock, (kFull ? 2 : GSB_GEOM_POSE_MIN_BLO
     const uint32_t clamp = craw >> kClampShift;
     // phase 2: ordered sum of this splat's entry partials (tile order); the
     // pose-only backward stores 8 per entry (no opacity), two 16-B loads
+    // Entries past their tile's cut were replayed by no pixel (zero partials,
+    // never stored by K4a): skipping them leaves every sum bit-identical.
     double acc[kPartial];
 #pragma unroll
     for (int c = 0; c < kPartial; ++c) acc[c] = 0.0;
-    if (kFull) {
-      const float* pp = partials + (int64_t)off * kPartial;
-      for (uint32_t j = 0; j < cnt; ++j) {
-#pragma unroll
-        for (int c = 0; c < kPartial; ++c) acc[c] += (double)pp[j * kPartial + c];
-      }
+    uint32_t tx0, ty0, nx;
+    if (cutd.aux_g) {
+      const uint4 A = s_rect[threadIdx.x];  // SplatAux {off, tx0_ty0, nx_ny, gid}
+      tx0 = A.y & 0xffffu; ty0 = A.y >> 16; nx = A.z & 0xffffu;
     } else {
-      const float4* pp = reinterpret_cast<const float4*>(partials) + (int64_t)off * 2;
-      for (uint32_t j = 0; j < cnt; ++j) {
-        const float4 lo = pp[2 * j], hi = pp[2 * j + 1];
-        acc[0] += (double)lo.x; acc[1] += (double)lo.y; acc[2] += (double)lo.z; acc[3] += (double)lo.w;
-        acc[4] += (double)hi.x; acc[5] += (double)hi.y; acc[6] += (double)hi.z; acc[7] += (double)hi.w;
+      const uint2 rc2 = reinterpret_cast<const uint2*>(s_rect)[threadIdx.x];
+      tx0 = rc2.x & 0xffffu; ty0 = rc2.y & 0xffffu; nx = (rc2.x >> 16) - tx0 + 1u;
+    }
+    const double dep = s_dep[threadIdx.x], gidd = (double)i;
+    const double2* cutrow = cutd.tile_cut + (int64_t)ty0 * cutd.tiles_x + tx0;
+    uint32_t jx = 0;
+    // 32 entries at a time: the cut loads are independent, then only the
+    // live entries' partials are loaded (in tile order).
+    for (uint32_t j0 = 0; j0 < cnt; j0 += 32) {
+      const uint32_t m = cnt - j0 < 32u ? cnt - j0 : 32u;
+      uint32_t live = 0;
+      for (uint32_t u = 0; u < m; ++u) {
+        const double2 ct = __ldg(cutrow + jx);
+        if (dep < ct.x || (dep == ct.x && gidd <= ct.y)) live |= 1u << u;
+        if (++jx == nx) { jx = 0; cutrow += cutd.tiles_x; }
+      }
+      while (live) {
+        const uint32_t j = j0 + (uint32_t)(__ffs(live) - 1);
+        live &= live - 1u;
+        if (kFull) {
+          const float* pp = partials + ((int64_t)off + j) * kPartial;
+#pragma unroll
+          for (int c = 0; c < kPartial; ++c) acc[c] += (double)pp[c];
+        } else {
+          const float4* pp = reinterpret_cast<const float4*>(partials) + ((int64_t)off + j) * 2;
+          const float4 lo = pp[0], hi = pp[1];
+          acc[0] += (double)lo.x; acc[1] += (double)lo.y; acc[2] += (double)lo.z; acc[3] += (double)lo.w;
+          acc[4] += (double)hi.x; acc[5] += (double)hi.y; acc[6] += (double)hi.z; acc[7] += (double)hi.w;
+        }
       }
     }
     const float* P = s_par + threadIdx.x;
@@ -336,17 +379,23 @@ __global__ void __launch_bounds__(256) pose_reduce_kernel(const double* __restri
 int launch_backward_geom(cudaStream_t st, const gsb_cloud* cloud, gsb_frame* f, const RasterDev& rc, bool full,
                          float* grads, int64_t* launches) {
   const int64_t n = cloud->n;
+  EntryCut cutd;
+  cutd.tile_cut = f->tile_cut.as<double2>();
+  cutd.depth_g = f->depth_g.as<double>();
+  cutd.aux_g = f->binning == kBinTileLocal ? f->aux_g.as<SplatAux>() : nullptr;
+  cutd.rect_g = f->rect_g.as<uint2>();
+  cutd.tiles_x = f->tiles_x;
   const int64_t nb = (n + 255) / 256;
   if (nb > 0) {
     if (full)
       backward_geom_kernel<true, double><<<(unsigned)nb, 256, 0, st>>>(
           cloud->params.as<float>(), n, cloud->n_pad, cloud->sh_degree, cloud->active_sh_degree, f->cam.as<CamDev>(),
-          rc, f->cnt_g.as<uint32_t>(), f->off_g.as<uint32_t>(), f->colj.as<float>(), f->partials.as<float>(), f->k_cap, grads,
+          rc, f->cnt_g.as<uint32_t>(), f->off_g.as<uint32_t>(), f->colj.as<float>(), f->partials.as<float>(), f->k_cap, cutd, grads,
           f->pose_blocks.as<double>());
     else
       backward_geom_kernel<false, GSB_POSE_CHAIN_T><<<(unsigned)nb, 256, 0, st>>>(
           cloud->params.as<float>(), n, cloud->n_pad, cloud->sh_degree, cloud->active_sh_degree, f->cam.as<CamDev>(),
-          rc, f->cnt_g.as<uint32_t>(), f->off_g.as<uint32_t>(), f->colj.as<float>(), f->partials.as<float>(), f->k_cap, nullptr,
+          rc, f->cnt_g.as<uint32_t>(), f->off_g.as<uint32_t>(), f->colj.as<float>(), f->partials.as<float>(), f->k_cap, cutd, nullptr,
           f->pose_blocks.as<double>());
   }
   pose_reduce_kernel<<<1, 256, 0, st>>>(f->pose_blocks.as<double>(), nb, f->d_pose.as<double>());

@@ -527,7 +527,8 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ ranks, const SplatRec* __restrict__ rec,
     const SplatAux* __restrict__ aux, const CamDev* __restrict__ cam_p, RasterDev rc, float bg_r, float bg_g,
     float bg_b, int64_t npix, const float* __restrict__ d_image, const float* __restrict__ final_t,
-    const uint32_t* __restrict__ pixstate, float* __restrict__ partials, uint32_t k_cap) {
+    const uint32_t* __restrict__ pixstate, const double* __restrict__ depth_g, double2* __restrict__ tile_cut,
+    float* __restrict__ partials, uint32_t k_cap) {
   __shared__ StagedSplat s_sp[kBatch];
   __shared__ uint8_t s_mask[kBatch];
   __shared__ uint8_t s_list[kWarps][kBatch];
@@ -562,9 +563,21 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
   uint32_t maxc = 0;
 #pragma unroll
   for (int w = 0; w < kWarps; ++w) maxc = max(maxc, s_maxc[w]);
-  const uint32_t len = range.y - range.x;
+  // Entries at list positions >= maxc are replayed by no pixel: their
+  // partials are zero and are neither computed nor stored. K4b skips them by
+  // comparing its (FP64 depth, gid) with the tile's cut — the key of entry
+  // maxc - 1 (tile lists are sorted by exactly that key).
+  if (threadIdx.x == 0) {
+    double2 cut = make_double2(-1.0, 0.0);
+    if (maxc > 0) {
+      const int32_t gid = aux[ranks[range.x + maxc - 1]].gid;
+      cut = make_double2(depth_g[gid], (double)gid);
+    }
+    tile_cut[tile] = cut;
+  }
+  const uint32_t len = min(range.y - range.x, maxc);
 
-  // Batches walk the list from the back; entries past maxc only get zeros.
+  // Batches walk the live part of the list from the back.
   const uint32_t nbatch = (len + kBatch - 1) / kBatch;
   for (int bi = (int)nbatch - 1; bi >= 0; --bi) {
     const uint32_t b0 = (uint32_t)bi * kBatch;  // list-local start
@@ -576,10 +589,7 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
       const uint32_t tx0 = A.tx0_ty0 & 0xffffu, ty0 = A.tx0_ty0 >> 16, nx = A.nx_ny & 0xffffu;
       StagedSplat& S = s_sp[threadIdx.x];
       S.slot = A.off + ((uint32_t)ty - ty0) * nx + ((uint32_t)tx - tx0);
-      s_mask[threadIdx.x] =
-          b0 + threadIdx.x < maxc
-              ? (uint8_t)quad_mask(stage_splat(rec[r], ox, oy, rc.cutoff2_f, &S.geo, &S.app, &S.col_b))
-              : (uint8_t)0;
+      s_mask[threadIdx.x] = (uint8_t)quad_mask(stage_splat(rec[r], ox, oy, rc.cutoff2_f, &S.geo, &S.app, &S.col_b));
     }
     __syncthreads();
     if (b0 < wmax) {  // this warp has pixels that replay entries of this batch
@@ -648,8 +658,8 @@ int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc, b
     (pose_only ? backward_raster_kernel<8> : backward_raster_kernel<kPartial>)<<<n_tiles, kThreads, 0, st>>>(
         f->ranges.as<uint2>(), f->list(), f->list_rec(), f->list_aux(),
         f->cam.as<CamDev>(), rc, (float)f->background[0], (float)f->background[1], (float)f->background[2], npix,
-        f->d_image.as<float>(), f->final_t.as<float>(), f->pixstate.as<uint32_t>(), f->partials.as<float>(),
-        (uint32_t)f->k_cap);
+        f->d_image.as<float>(), f->final_t.as<float>(), f->pixstate.as<uint32_t>(), f->depth_g.as<double>(),
+        f->tile_cut.as<double2>(), f->partials.as<float>(), (uint32_t)f->k_cap);
   GSB_CHECK_LAUNCH("backward_raster_kernel");
   return GSB_OK;
 }
