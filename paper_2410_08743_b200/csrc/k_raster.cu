@@ -435,62 +435,25 @@ __device__ __forceinline__ void load_pixel_bwd(PixBwd& p, int x, int y, int W, i
   p.Bd = p.T * (p.dr * bg_r + p.dg * bg_g + p.db * bg_b);
 }
 
-// One (pixel, splat) replay step of phase 1; accumulates into v (NC = 8:
-// no opacity partial).
+// Both pixels of a lane for one splat (one replay step of phase 1), branch
+// free: a pixel that is past its contrib count or outside the cutoff (ha/hb
+// false) gets alpha_raw = 0, which makes every update below an exact no-op
+// (inv = 1, weight 0, d_alpha chain times 0), so the two chains interleave
+// and lanes without a hit need no separate path. Writes v (NC = 8: no
+// opacity partial).
 template <int NC>
-__device__ __forceinline__ bool backward_one(PixBwd& p, const float4& ge, const float4& ap, float col_b, float dx,
-                                             float dy, const RasterDev& rc, uint32_t j, float v[NC]) {
-  if (j >= p.contrib) return false;
-  const float g = splat_power(ge.z, ge.w, ap.x, dx, dy);
-  if (g > rc.cutoff2_f) return false;
-  const float G = exp_neg_half(g);
-  const float araw = ap.y * G;
-  const float alpha = fminf(rc.alpha_clamp_f, araw);
-  const float inv = rcp_fast(1.0f - alpha);
-  const float tb = p.T * inv;
-  const float wgt = alpha * tb;
-  v[5] = fmaf(wgt, p.dr, v[5]);
-  v[6] = fmaf(wgt, p.dg, v[6]);
-  v[7] = fmaf(wgt, p.db, v[7]);
-  // d_alpha = sum_c d_c (c_c t_before - behind_c / (1 - alpha))
-  const float dc = fmaf(p.dr, ap.z, fmaf(p.dg, ap.w, p.db * col_b));
-  const float dal = fmaf(tb, dc, -inv * p.Bd);
-  if (araw < rc.alpha_clamp_f) {
-    const float cx_ = ge.z * dx + ge.w * dy, cy_ = ge.w * dx + ap.x * dy;
-    if (NC > 8) v[NC - 1] = fmaf(dal, G, v[NC - 1]);
-    const float dgg = dal * (-0.5f * araw);
-    v[0] = fmaf(-2.0f * dgg, cx_, v[0]);
-    v[1] = fmaf(-2.0f * dgg, cy_, v[1]);
-    v[2] = fmaf(dgg * dx, dx, v[2]);
-    v[3] = fmaf(dgg * dx, dy, v[3]);
-    v[4] = fmaf(dgg * dy, dy, v[4]);
-  }
-  p.T = tb;
-  p.Bd = fmaf(wgt, dc, p.Bd);  // behind += colour * weight
-  return true;
-}
-
-// Both pixels of a lane for one splat, branch free: a pixel that is past its
-// contrib count or outside the cutoff gets alpha_raw = 0, which makes every
-// update below an exact no-op (inv = 1, weight 0, d_alpha chain times 0), so
-// the two independent chains interleave without divergent branches.
-template <int NC>
-__device__ __forceinline__ bool backward_pair(PixBwd& a, PixBwd& b, const float4& ge, const float4& ap, float col_b,
-                                              float dx, float dy, const RasterDev& rc, uint32_t j, float v[NC]) {
-  const float ga = splat_power(ge.z, ge.w, ap.x, dx, dy);
-  const float gb = splat_power(ge.z, ge.w, ap.x, dx, dy + 1.0f);
-  const bool ha = j < a.contrib && ga <= rc.cutoff2_f;
-  const bool hb = j < b.contrib && gb <= rc.cutoff2_f;
-  if (!(ha || hb)) return false;
+__device__ __forceinline__ void backward_pair(PixBwd& a, PixBwd& b, const float4& ge, const float4& ap, float col_b,
+                                              float dx, float dy, float ga, float gb, bool ha, bool hb,
+                                              const RasterDev& rc, float v[NC]) {
   const float Ga = exp_neg_half(ga), Gb = exp_neg_half(gb);
   const float ra = ha ? ap.y * Ga : 0.f, rb = hb ? ap.y * Gb : 0.f;  // alpha_raw
   const float al_a = fminf(rc.alpha_clamp_f, ra), al_b = fminf(rc.alpha_clamp_f, rb);
   const float ia = rcp_fast(1.0f - al_a), ib = rcp_fast(1.0f - al_b);
   const float ta = a.T * ia, tb = b.T * ib;  // t_before
   const float wa = al_a * ta, wb = al_b * tb;
-  v[5] = fmaf(wa, a.dr, fmaf(wb, b.dr, v[5]));
-  v[6] = fmaf(wa, a.dg, fmaf(wb, b.dg, v[6]));
-  v[7] = fmaf(wa, a.db, fmaf(wb, b.db, v[7]));
+  v[5] = fmaf(wa, a.dr, wb * b.dr);
+  v[6] = fmaf(wa, a.dg, wb * b.dg);
+  v[7] = fmaf(wa, a.db, wb * b.db);
   const float dca = fmaf(a.dr, ap.z, fmaf(a.dg, ap.w, a.db * col_b));
   const float dcb = fmaf(b.dr, ap.z, fmaf(b.dg, ap.w, b.db * col_b));
   const float dala = fmaf(ta, dca, -ia * a.Bd), dalb = fmaf(tb, dcb, -ib * b.Bd);
@@ -499,21 +462,22 @@ __device__ __forceinline__ bool backward_pair(PixBwd& a, PixBwd& b, const float4
   const float kb = rb < rc.alpha_clamp_f ? dalb * (-0.5f * rb) : 0.f;
   if (NC > 8) {
     v[NC - 1] = fmaf(ra < rc.alpha_clamp_f ? dala : 0.f, Ga * (ha ? 1.f : 0.f),
-                     fmaf(rb < rc.alpha_clamp_f ? dalb : 0.f, Gb * (hb ? 1.f : 0.f), v[NC - 1]));
+                     (rb < rc.alpha_clamp_f ? dalb : 0.f) * (Gb * (hb ? 1.f : 0.f)));
   }
-  const float dyb = dy + 1.0f;
-  const float cxa = ge.z * dx + ge.w * dy, cya = ge.w * dx + ap.x * dy;
-  const float cxb = ge.z * dx + ge.w * dyb, cyb = ge.w * dx + ap.x * dyb;
-  v[0] = fmaf(-2.0f * ka, cxa, fmaf(-2.0f * kb, cxb, v[0]));
-  v[1] = fmaf(-2.0f * ka, cya, fmaf(-2.0f * kb, cyb, v[1]));
-  v[2] = fmaf(ka * dx, dx, fmaf(kb * dx, dx, v[2]));
-  v[3] = fmaf(ka * dx, dy, fmaf(kb * dx, dyb, v[3]));
-  v[4] = fmaf(ka * dy, dy, fmaf(kb * dyb, dyb, v[4]));
+  // pixel b sits at dy + 1: with s = ka + kb the pair's sums factor as
+  // conic.d_a s + conic.(0, 1) kb, dx^2 s, dx (dy s + kb), dy^2 s + (2 dy + 1) kb;
+  // components 0 and 1 leave out the factor -2 (applied exactly at the flush)
+  const float sk = ka + kb;
+  const float cxa = fmaf(ge.z, dx, ge.w * dy), cya = fmaf(ge.w, dx, ap.x * dy);
+  v[0] = fmaf(sk, cxa, kb * ge.w);
+  v[1] = fmaf(sk, cya, kb * ap.x);
+  v[2] = (sk * dx) * dx;
+  v[3] = dx * fmaf(sk, dy, kb);
+  v[4] = fmaf(sk * dy, dy, kb * (dy + dy + 1.0f));
   a.T = ta;
   b.T = tb;
   a.Bd = fmaf(wa, dca, a.Bd);
   b.Bd = fmaf(wb, dcb, b.Bd);
-  return true;
 }
 
 #ifndef GSB_LDS_ASM
@@ -609,16 +573,17 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
         const float cb = s_sp[k].col_b;
         (void)sp_base;
 #endif
-        float v[NC];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) v[c] = 0.f;
         const float dx = px - ge.x, dy = py - ge.y;
-        const bool hit = backward_pair<NC>(a, b, ge, ap, cb, dx, dy, rc, j, v);
-        if (__any_sync(kFull, hit)) {
-          float tot;
-          const int vi = NC == 8 ? warp_reduce8(v, &tot) : warp_reduce9(v, &tot);
-          if (vi >= 0) s_red[warp][k][vi] = tot;
-        }
+        const float ga = splat_power(ge.z, ge.w, ap.x, dx, dy);
+        const float gb = splat_power(ge.z, ge.w, ap.x, dx, dy + 1.0f);
+        const bool ha = j < a.contrib && ga <= rc.cutoff2_f;
+        const bool hb = j < b.contrib && gb <= rc.cutoff2_f;
+        if (!__any_sync(kFull, ha || hb)) continue;  // s_red stays zero for this entry
+        float v[NC];
+        backward_pair<NC>(a, b, ge, ap, cb, dx, dy, ga, gb, ha, hb, rc, v);
+        float tot;
+        const int vi = NC == 8 ? warp_reduce8(v, &tot) : warp_reduce9(v, &tot);
+        if (vi >= 0) s_red[warp][k][vi] = tot;
       }
     }
     __syncthreads();
@@ -631,6 +596,7 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
         acc += s_red[w][k][c];
         s_red[w][k][c] = 0.f;
       }
+      if (c < 2) acc *= -2.0f;  // d_mu2d = -2 dg (conic d) (rasterizer.cpp:396)
       const uint32_t slot = s_sp[k].slot;
       if (slot < k_cap) partials[(int64_t)slot * NC + c] = acc;
     }
