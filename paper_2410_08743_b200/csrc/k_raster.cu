@@ -604,6 +604,190 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
   }
 }
 
+// ---- K4a, pose-only variant on half-quadrant lists: each warp still owns
+// an 8x8 quadrant (same pixel layout as above), but its two 16-lane halves
+// (rows 0-3 and 4-7 of the quadrant) walk their own lists of the batch
+// entries whose cutoff-ellipse box reaches their 8x4 half, so one warp step
+// serves two entries and a splat costs a half nothing unless it reaches it.
+// Per-entry partials: a 16-lane reduce-scatter (8 shuffles serve both halves'
+// entries) and a fixed-order add into the warp's shared slot (half 0 before
+// half 1 within a step; steps in list order) — deterministic.
+__device__ __forceinline__ uint32_t half_mask(uint32_t m16) {
+  uint32_t r = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int by = 2 * (q >> 1) + h, bx = 2 * (q & 1);
+      if ((m16 >> (4 * by + bx)) & 3u) r |= 1u << (2 * q + h);
+    }
+  return r;
+}
+
+// Lists of batch entries (list-local position < lim) reaching half 0 / 1 of
+// warp w's quadrant, ascending; returns both counts.
+__device__ __forceinline__ void build_half_lists(const uint8_t* s_mask, int cnt, int warp, uint32_t lim,
+                                                 uint8_t (*list)[kBatch], int* n0, int* n1) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt_();
+  int c0 = 0, c1 = 0;
+#pragma unroll
+  for (int c = 0; c < kBatch / 32; ++c) {
+    const int e = c * 32 + lane;
+    const uint32_t m = (e < cnt && (uint32_t)e < lim) ? (s_mask[e] >> (2 * warp)) : 0u;
+    const bool t0 = m & 1u, t1 = m & 2u;
+    const uint32_t b0 = __ballot_sync(kFull, t0), b1 = __ballot_sync(kFull, t1);
+    if (t0) list[0][c0 + __popc(b0 & lt)] = (uint8_t)e;
+    if (t1) list[1][c1 + __popc(b1 & lt)] = (uint8_t)e;
+    c0 += __popc(b0);
+    c1 += __popc(b1);
+  }
+  __syncwarp();
+  *n0 = c0;
+  *n1 = c1;
+}
+
+// 8 values over each 16-lane half: xor 8 / 4 / 2 reduce-scatter (4 + 2 + 1
+// shuffles) and a plain xor-1 sum; even lanes end owning component
+// 4 b3 + 2 b2 + b1 (b_k = bit k of the lane) of their half's sum.
+__device__ __forceinline__ int half_reduce8(const float v[8], float* out) {
+  const int lane = threadIdx.x & 31;
+  const bool h1 = lane & 8, h2 = lane & 4, h3 = lane & 2;
+  float w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = h1 ? v[i] : v[4 + i], keep = h1 ? v[4 + i] : v[i];
+    w[i] = keep + __shfl_xor_sync(kFull, send, 8);
+  }
+  float x[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = h2 ? w[i] : w[2 + i], keep = h2 ? w[2 + i] : w[i];
+    x[i] = keep + __shfl_xor_sync(kFull, send, 4);
+  }
+  float z;
+  {
+    const float send = h3 ? x[0] : x[1], keep = h3 ? x[1] : x[0];
+    z = keep + __shfl_xor_sync(kFull, send, 2);
+  }
+  z += __shfl_xor_sync(kFull, z, 1);
+  *out = z;
+  return (lane & 1) ? -1 : (h1 ? 4 : 0) + (h2 ? 2 : 0) + (h3 ? 1 : 0);
+}
+
+__global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_half_kernel(
+    const uint2* __restrict__ ranges, const uint32_t* __restrict__ ranks, const SplatRec* __restrict__ rec,
+    const SplatAux* __restrict__ aux, const CamDev* __restrict__ cam_p, RasterDev rc, float bg_r, float bg_g,
+    float bg_b, int64_t npix, const float* __restrict__ d_image, const float* __restrict__ final_t,
+    const uint32_t* __restrict__ pixstate, const double* __restrict__ depth_g, double2* __restrict__ tile_cut,
+    float* __restrict__ partials, uint32_t k_cap) {
+  constexpr int NC = 8;
+  __shared__ StagedSplat s_sp[kBatch];
+  __shared__ uint8_t s_mask[kBatch];
+  __shared__ uint8_t s_list[kWarps][2][kBatch];
+  __shared__ float s_red[kWarps][kBatch][NC];  // [warp][entry in batch][component]
+  __shared__ int s_w, s_h, s_tx;
+  __shared__ uint32_t s_maxc[kWarps];
+  if (threadIdx.x == 0) {
+    s_w = cam_p->width;
+    s_h = cam_p->height;
+    s_tx = cam_p->tiles_x;
+  }
+  for (int i = threadIdx.x; i < kWarps * kBatch * NC; i += kThreads) (&s_red[0][0][0])[i] = 0.f;
+  __syncthreads();
+  const int W = s_w, H = s_h;
+  const int tile = blockIdx.x;
+  const int tx = tile % s_tx, ty = tile / s_tx;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, half = lane >> 4;
+  int lx, ly;
+  quad_pixel_coords(warp, lane, &lx, &ly);
+  const int x = tx * kTile + lx, y = ty * kTile + ly;
+  const double ox = (double)(tx * kTile), oy = (double)(ty * kTile);
+  const float px = (float)lx, py = (float)ly;
+  const uint2 range = ranges[tile];
+  const uint32_t sp_base = (uint32_t)__cvta_generic_to_shared(s_sp);
+
+  PixBwd a, b;
+  load_pixel_bwd(a, x, y, W, H, npix, bg_r, bg_g, bg_b, d_image, final_t, pixstate);
+  load_pixel_bwd(b, x, y + 1, W, H, npix, bg_r, bg_g, bg_b, d_image, final_t, pixstate);
+  const uint32_t wmax = __reduce_max_sync(kFull, max(a.contrib, b.contrib));
+  if (lane == 0) s_maxc[warp] = wmax;
+  __syncthreads();
+  uint32_t maxc = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) maxc = max(maxc, s_maxc[w]);
+  // entries at list positions >= maxc: see backward_raster_kernel
+  if (threadIdx.x == 0) {
+    double2 cut = make_double2(-1.0, 0.0);
+    if (maxc > 0) {
+      const int32_t gid = aux[ranks[range.x + maxc - 1]].gid;
+      cut = make_double2(depth_g[gid], (double)gid);
+    }
+    tile_cut[tile] = cut;
+  }
+  const uint32_t len = min(range.y - range.x, maxc);
+  const uint32_t nbatch = (len + kBatch - 1) / kBatch;
+  for (int bi = (int)nbatch - 1; bi >= 0; --bi) {
+    const uint32_t b0 = (uint32_t)bi * kBatch;  // list-local start
+    const int cnt = (int)min((uint32_t)kBatch, len - b0);
+    if (threadIdx.x < cnt) {
+      const uint32_t e = range.x + b0 + threadIdx.x;
+      const uint32_t r = ranks[e];
+      const SplatAux A = aux[r];
+      const uint32_t tx0 = A.tx0_ty0 & 0xffffu, ty0 = A.tx0_ty0 >> 16, nx = A.nx_ny & 0xffffu;
+      StagedSplat& S = s_sp[threadIdx.x];
+      S.slot = A.off + ((uint32_t)ty - ty0) * nx + ((uint32_t)tx - tx0);
+      s_mask[threadIdx.x] = (uint8_t)half_mask(stage_splat(rec[r], ox, oy, rc.cutoff2_f, &S.geo, &S.app, &S.col_b));
+    }
+    __syncthreads();
+    if (b0 < wmax) {  // this warp has pixels that replay entries of this batch
+      int n0, n1;
+      build_half_lists(s_mask, cnt, warp, wmax - b0, s_list[warp], &n0, &n1);
+      const int mine = half ? n1 : n0;
+      const int nmax = max(n0, n1);
+      const uint8_t* my_list = s_list[warp][half];
+      for (int it = 0; it < nmax; ++it) {  // each half back to front
+        const bool act = it < mine;
+        const int k = act ? my_list[mine - 1 - it] : 0;
+        const uint32_t j = b0 + (uint32_t)k;
+        const uint32_t sa = sp_base + (uint32_t)k * (uint32_t)sizeof(StagedSplat);
+        const float4 ge = lds_f4(sa);
+        const float4 ap = lds_f4(sa + 16u);
+        const float dx = px - ge.x, dy = py - ge.y;
+        const float ga = splat_power(ge.z, ge.w, ap.x, dx, dy);
+        const float gb = splat_power(ge.z, ge.w, ap.x, dx, dy + 1.0f);
+        const bool ha = act && j < a.contrib && ga <= rc.cutoff2_f;
+        const bool hb = act && j < b.contrib && gb <= rc.cutoff2_f;
+        if (!__any_sync(kFull, ha || hb)) continue;  // neither half's entry touched: zero partials
+        const float cb = lds_f1(sa + 32u);
+        float v[NC];
+        backward_pair<NC>(a, b, ge, ap, cb, dx, dy, ga, gb, ha, hb, rc, v);
+        float tot;
+        const int vi = half_reduce8(v, &tot);
+        // both halves may hold the same entry in this step: half 0 adds first
+        if (vi >= 0 && act && half == 0) s_red[warp][k][vi] += tot;
+        __syncwarp();
+        if (vi >= 0 && act && half == 1) s_red[warp][k][vi] += tot;
+      }
+    }
+    __syncthreads();
+    // flush: batch entries x 8 components, summed over warps 0..3 in order
+    for (int idx = threadIdx.x; idx < cnt * NC; idx += kThreads) {
+      const int k = idx / NC, c = idx - k * NC;
+      float acc = 0.f;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        acc += s_red[w][k][c];
+        s_red[w][k][c] = 0.f;
+      }
+      if (c < 2) acc *= -2.0f;  // d_mu2d = -2 dg (conic d) (rasterizer.cpp:396)
+      const uint32_t slot = s_sp[k].slot;
+      if (slot < k_cap) partials[(int64_t)slot * NC + c] = acc;
+    }
+    __syncthreads();
+  }
+}
+
 int launch_composite(cudaStream_t st, gsb_frame* f, const RasterDev& rc) {
   const int n_tiles = f->tiles_x * f->tiles_y;
   const int64_t npix = (int64_t)f->width * f->height;
@@ -617,11 +801,15 @@ int launch_composite(cudaStream_t st, gsb_frame* f, const RasterDev& rc) {
 }
 
 // pose_only: 8 partials per entry (no opacity); else the full 9.
+#ifndef GSB_BWD_HALF
+#define GSB_BWD_HALF 1
+#endif
 int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc, bool pose_only) {
   const int n_tiles = f->tiles_x * f->tiles_y;
   const int64_t npix = (int64_t)f->width * f->height;
   if (n_tiles > 0)
-    (pose_only ? backward_raster_kernel<8> : backward_raster_kernel<kPartial>)<<<n_tiles, kThreads, 0, st>>>(
+    (pose_only ? (GSB_BWD_HALF ? backward_raster_half_kernel : backward_raster_kernel<8>)
+               : backward_raster_kernel<kPartial>)<<<n_tiles, kThreads, 0, st>>>(
         f->ranges.as<uint2>(), f->list(), f->list_rec(), f->list_aux(),
         f->cam.as<CamDev>(), rc, (float)f->background[0], (float)f->background[1], (float)f->background[2], npix,
         f->d_image.as<float>(), f->final_t.as<float>(), f->pixstate.as<uint32_t>(), f->depth_g.as<double>(),
