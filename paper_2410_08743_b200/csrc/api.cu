@@ -742,6 +742,8 @@ int gsb_ctx_destroy(gsb_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   ctx->scratch_small.release();
   if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
+  for (auto& pb : ctx->pinned_pool) cudaFreeHost(pb.first);
+  ctx->pinned_pool.clear();
   delete ctx->timer;
   if (ctx->work) gsb_frame_destroy(ctx->work);
   for (gsb_frame* f : ctx->frame_pool) gsb_frame_destroy(f);
@@ -1440,7 +1442,8 @@ struct gsb_session {
   DevBuf state;   // PoseState
   DevBuf camdev;  // CamDev of the current pose
   DevBuf trace;   // pose (12) + loss (1) per iteration
-  void* host_state = nullptr;
+  void* host_state = nullptr;  // pinned, from / back to ctx->pinned_pool
+  size_t host_state_bytes = 0;
   uint32_t* host_counters = nullptr;
   int64_t n_splats = 0, n_entries = 0;
   int32_t stopped = 0;
@@ -1648,7 +1651,21 @@ int gsb_session_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* target, const 
   cudaError_t e = s->state.reserve(sb);
   if (e == cudaSuccess) e = s->camdev.reserve(sizeof(CamDev));
   if (e == cudaSuccess) e = s->trace.reserve(sizeof(double) * 13 * (size_t)cfg->budget);
-  if (e == cudaSuccess) e = cudaMallocHost(&s->host_state, host_bytes);
+  // pinned status block from the context's pool (cudaMallocHost / cudaFreeHost
+  // cost up to hundreds of ms per call under load)
+  if (e == cudaSuccess) {
+    for (size_t i = 0; i < ctx->pinned_pool.size(); ++i)
+      if (ctx->pinned_pool[i].second >= host_bytes) {
+        s->host_state = ctx->pinned_pool[i].first;
+        s->host_state_bytes = ctx->pinned_pool[i].second;
+        ctx->pinned_pool.erase(ctx->pinned_pool.begin() + i);
+        break;
+      }
+    if (!s->host_state) {
+      e = cudaMallocHost(&s->host_state, host_bytes);
+      if (e == cudaSuccess) s->host_state_bytes = host_bytes;
+    }
+  }
   if (e != cudaSuccess) {
     gsb_session_destroy(s);
     return cuda_fail(e, "session alloc");
@@ -1693,7 +1710,7 @@ int gsb_session_destroy(gsb_session* s) {
   s->state.release();
   s->camdev.release();
   s->trace.release();
-  if (s->host_state) cudaFreeHost(s->host_state);
+  if (s->host_state) s->ctx->pinned_pool.emplace_back(s->host_state, s->host_state_bytes);
   delete s;
   return GSB_OK;
 }

@@ -188,6 +188,7 @@ struct gsb_ctx {
   int binning = 0;             // gsb::Binning preference (gsb_ctx_set_binning)
   std::vector<gsb_frame*> frame_pool;  // sized forward states returned by pose batches, reused
   std::vector<gsb::DevBuf> image_pool;  // target-image planes of destroyed gsb_images, reused by size
+  std::vector<std::pair<void*, size_t>> pinned_pool;  // pinned session status blocks, reused
 };
 
 struct gsb_cloud {

@@ -15,7 +15,7 @@ intr = gsb.synth_intrinsics(bench.WIDTH, bench.HEIGHT)
 views = list(range(8))
 hosts = [gsb.render(ctx, cloud, gsb.Camera.from_pose12(*intr, bench.WIDTH, bench.HEIGHT, gt[v])).image for v in views]
 cfg = gsb.PoseConfig.default(budget=100, pose_converged_eps=0.0)
-for rep in range(3):
+for rep in range(5):
     ctx.synchronize()
     t0 = time.perf_counter()
     imgs = [gsb.Image(ctx, h) for h in hosts]
