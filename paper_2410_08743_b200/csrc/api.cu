@@ -611,11 +611,29 @@ static int download_image(gsb_ctx* ctx, const float* dev_planes, int W, int H, d
   return GSB_OK;
 }
 // interleaved FP64 host -> planar FP32 device
+// Host FP64 HWC image -> device FP32 planes, stream ordered on ctx->stream.
+// Two pinned staging slots alternate: the conversion of the next image
+// overlaps the DMA of the previous one, and the call returns without waiting
+// for its own copy (only for the copy that last used the slot it takes).
 static int upload_image(gsb_ctx* ctx, const double* img, int W, int H, float* dev_planes) {
   const size_t P = (size_t)W * H;
-  float* h = static_cast<float*>(pinned(ctx, sizeof(float) * 3 * P));
-  if (!h) return fail(GSB_ERR_OUT_OF_MEMORY, "pinned staging");
-  GSB_CUDA(cudaStreamSynchronize(ctx->stream));  // staging buffer reuse
+  const size_t bytes = sizeof(float) * 3 * P;
+  const int k = ctx->up_next;
+  ctx->up_next ^= 1;
+  if (ctx->up_ev[k]) {
+    GSB_CUDA(cudaEventSynchronize(ctx->up_ev[k]));  // the slot's previous copy has landed
+  } else {
+    GSB_CUDA(cudaEventCreateWithFlags(&ctx->up_ev[k], cudaEventDisableTiming));
+  }
+  if (bytes > ctx->up_bytes[k]) {
+    if (ctx->up_buf[k]) cudaFreeHost(ctx->up_buf[k]);
+    ctx->up_buf[k] = nullptr;
+    ctx->up_bytes[k] = 0;
+    const size_t cap = bytes + bytes / 4 + 4096;
+    if (cudaMallocHost(&ctx->up_buf[k], cap) != cudaSuccess) return fail(GSB_ERR_OUT_OF_MEMORY, "pinned staging");
+    ctx->up_bytes[k] = cap;
+  }
+  float* h = static_cast<float*>(ctx->up_buf[k]);
   const double t0 = debug_on() ? now_ms() : 0.0;
   host_parallel(P, [&](size_t b, size_t e) {
     for (size_t p = b; p < e; ++p) {
@@ -627,8 +645,8 @@ static int upload_image(gsb_ctx* ctx, const double* img, int W, int H, float* de
   if (debug_on())
     std::fprintf(stderr, "[gsb] upload_image: convert %.2f ms (%u threads)\n", now_ms() - t0,
                  std::thread::hardware_concurrency());
-  GSB_CUDA(cudaMemcpyAsync(dev_planes, h, sizeof(float) * 3 * P, cudaMemcpyHostToDevice, ctx->stream));
-  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  GSB_CUDA(cudaMemcpyAsync(dev_planes, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  GSB_CUDA(cudaEventRecord(ctx->up_ev[k], ctx->stream));
   return GSB_OK;
 }
 
@@ -743,6 +761,10 @@ int gsb_ctx_destroy(gsb_ctx* ctx) {
   ctx->scratch_small.release();
   if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
   for (auto& pb : ctx->pinned_pool) cudaFreeHost(pb.first);
+  for (int k = 0; k < 2; ++k) {
+    if (ctx->up_buf[k]) cudaFreeHost(ctx->up_buf[k]);
+    if (ctx->up_ev[k]) cudaEventDestroy(ctx->up_ev[k]);
+  }
   ctx->pinned_pool.clear();
   delete ctx->timer;
   if (ctx->work) gsb_frame_destroy(ctx->work);

@@ -189,6 +189,10 @@ struct gsb_ctx {
   std::vector<gsb_frame*> frame_pool;  // sized forward states returned by pose batches, reused
   std::vector<gsb::DevBuf> image_pool;  // target-image planes of destroyed gsb_images, reused by size
   std::vector<std::pair<void*, size_t>> pinned_pool;  // pinned session status blocks, reused
+  void* up_buf[2] = {nullptr, nullptr};  // pinned image-upload staging slots (alternating)
+  size_t up_bytes[2] = {0, 0};
+  cudaEvent_t up_ev[2] = {nullptr, nullptr};  // last copy out of each slot
+  int up_next = 0;
 };
 
 struct gsb_cloud {
