@@ -25,13 +25,15 @@
 // K4a restates phase 1 of render_backward (rasterizer.cpp:354-405): per
 // pixel back-to-front replay from contrib_count-1 with t_before = T/(1-a),
 // clamped channels zeroed, alpha-chain gradients only when a_raw < clamp.
-// Per-(pixel, splat) partials are reduced in a fixed order: the lane's two
-// pixels, an 8-lane recursive-halving reduce-scatter inside each sub-warp
-// (10 shuffles serve the four sub-warps' splats at once), the four sub-warps
-// of a warp in sub-warp order, then warps 0..3 — and written (zero when
-// untouched) to the entry's slot in the splat-major entry stream, so K4b
+// Each warp owns an 8x8 quadrant (two pixels per lane). Per-(pixel, splat)
+// partials are reduced in a fixed order: the lane's two pixels, a warp (full
+// gradient) or 16-lane half (pose-only: each half walks its own 8x4 list)
+// recursive-halving reduce-scatter, ordered adds per warp, then warps 0..3 —
+// and written to the entry's slot in the splat-major entry stream, so K4b
 // reads each splat's partials contiguously and in tile order (phase 2's
-// per-splat order, rasterizer.cpp:410-418). No atomics: deterministic.
+// per-splat order, rasterizer.cpp:410-418). Entries at list positions no
+// pixel replays are not written; K4b skips them through the per-tile cut.
+// No atomics: deterministic.
 #include "gsb_internal.cuh"
 
 namespace gsb {
