@@ -280,6 +280,35 @@ def test_backward_matches_oracle(G, ctx, seed):
     assert np.max(np.abs(dp2 - dp)) <= 1e-5 * np.max(np.abs(dp))
 
 
+def test_backward_global_binning_bitwise_equals_tile_local(G, ctx):
+    """Both binning paths build the same tile lists, and K4b finds each
+    splat's tile rect (aux_g vs rect_g) and the per-tile cut of the entries
+    no pixel replays the same way: full gradients and the pose-only d_pose
+    must be bit-identical (C1-sized scene, the loss gradient as d_image)."""
+    hc, poses = synth_scene(99, 10000, 256, scale_offset=math.log(500 / 10000) / 3)
+    ocam = O.synth_camera(256, 256, poses[1])
+    cloud = to_dev(G, ctx, hc)
+    cam = dev_cam(G, ocam)
+    target = O.render(hc, O.synth_camera(256, 256, poses[0])).image
+    res = {}
+    for mode in (G.Context.BINNING_TILE_LOCAL, G.Context.BINNING_GLOBAL):
+        ctx.set_binning(mode)
+        try:
+            out = G.render(ctx, cloud, cam)
+            assert out.info().binning == mode
+            _, d_img = G.rgb_loss(ctx, out.image, target, 0.2)
+            g, dp = G.render_backward(ctx, cloud, cam, out, d_img)
+            _, dpo = G.render_backward(ctx, cloud, cam, out, d_img, pose_only=True)
+            res[mode] = (g, dp, dpo)
+        finally:
+            ctx.set_binning(G.Context.BINNING_TILE_LOCAL)
+    (g0, dp0, dpo0), (g1, dp1, dpo1) = res[G.Context.BINNING_TILE_LOCAL], res[G.Context.BINNING_GLOBAL]
+    assert np.any(dp0 != 0)
+    assert dp0.tobytes() == dp1.tobytes() and dpo0.tobytes() == dpo1.tobytes()
+    for k in g0:
+        assert g0[k].tobytes() == g1[k].tobytes(), k
+
+
 def test_backward_invariants(G, ctx):
     hc, ocam, bg, rng = scene(58, 8, 32, conditioned=False)
     cloud = to_dev(G, ctx, hc)
