@@ -225,7 +225,14 @@ __device__ __forceinline__ void hpass3(const float (*st)[kSH][kSW + 1], double (
   }
 }
 
-__global__ void __launch_bounds__(kThr) loss_grad_kernel(const float* __restrict__ ren, const float* __restrict__ tgt,
+// 4 CTAs/SM (64 registers, 48 B of spills; 55 KB shared each): the kernel is
+// load-latency bound, and in a pose batch the extra resident CTAs of the
+// other branches fill in (measured: batch +3.8 % over the default 2 CTAs/SM)
+#ifndef GSB_LOSS_GRAD_MIN_BLOCKS
+#define GSB_LOSS_GRAD_MIN_BLOCKS 4
+#endif
+#define GSB_LOSS_GRAD_BOUNDS __launch_bounds__(kThr, GSB_LOSS_GRAD_MIN_BLOCKS)
+__global__ void GSB_LOSS_GRAD_BOUNDS loss_grad_kernel(const float* __restrict__ ren, const float* __restrict__ tgt,
                                                          const float* __restrict__ gmaps, int W, int H, double beta,
                                                          double l1_norm, int has_ssim, float* __restrict__ d_image,
                                                          MaskArgs mk) {
