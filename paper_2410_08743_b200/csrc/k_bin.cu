@@ -92,7 +92,12 @@ __global__ void tile_ranges_from_scan_kernel(const uint32_t* __restrict__ offs, 
 
 // 4. Scatter (depth high word, gid) — one 8-byte store per entry — into the
 // CTA's run of every tile.
-__global__ void __launch_bounds__(kBinThreads) tile_scatter_kernel(const uint32_t* __restrict__ cnt_g,
+#ifdef GSB_SCATTER_MIN_BLOCKS
+#define GSB_SCATTER_BOUNDS __launch_bounds__(kBinThreads, GSB_SCATTER_MIN_BLOCKS)
+#else
+#define GSB_SCATTER_BOUNDS __launch_bounds__(kBinThreads)
+#endif
+__global__ void GSB_SCATTER_BOUNDS tile_scatter_kernel(const uint32_t* __restrict__ cnt_g,
                                                                    const SplatAux* __restrict__ aux_g,
                                                                    const double* __restrict__ depth_g, int64_t n,
                                                                    int n_tiles, int tiles_x, int64_t nchunks,

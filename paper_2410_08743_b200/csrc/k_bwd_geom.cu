@@ -49,7 +49,7 @@ __device__ __forceinline__ void sh_basis_d(double x, double y, double z, int deg
 // into shared memory by TMA bulk copies (one elected thread, one mbarrier).
 constexpr int kGeomBlock = 256;
 #ifndef GSB_GEOM_POSE_MIN_BLOCKS
-#define GSB_GEOM_POSE_MIN_BLOCKS 4  // 64 registers: occupancy over a few spilled bytes (measured)
+#define GSB_GEOM_POSE_MIN_BLOCKS 5  // 48 registers: occupancy over ~100 spilled bytes (measured: 4 -> 5 CTAs/SM, 0.087 -> 0.085 ms)
 #endif
 #ifndef GSB_POSE_CHAIN_T
 #define GSB_POSE_CHAIN_T float

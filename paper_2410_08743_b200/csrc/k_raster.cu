@@ -242,7 +242,12 @@ __device__ __forceinline__ void write_pixel(const PixFwd& p, int x, int y, int W
   pixstate[q] = p.processed | (of << 29);
 }
 
-__global__ void __launch_bounds__(kThreads) composite_kernel(
+#ifdef GSB_COMP_MIN_BLOCKS  // (an explicit minimum of 1 changes ptxas's register choice: leave it unset)
+#define GSB_COMP_BOUNDS __launch_bounds__(kThreads, GSB_COMP_MIN_BLOCKS)
+#else
+#define GSB_COMP_BOUNDS __launch_bounds__(kThreads)
+#endif
+__global__ void GSB_COMP_BOUNDS composite_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ ranks, const SplatRec* __restrict__ rec,
     const CamDev* __restrict__ cam_p, RasterDev rc, float bg_r, float bg_g, float bg_b, int64_t npix,
     float* __restrict__ image, float* __restrict__ final_t, uint32_t* __restrict__ pixstate) {
