@@ -45,6 +45,25 @@ __device__ __forceinline__ uint32_t ld_status(const uint32_t* p) {
   return v;
 }
 
+// Warp-wide variant for the scan (called by a full warp): reads the status
+// of the 32 nearest predecessors at once, waits until all of them are
+// published, and sums aggregates down to the nearest inclusive prefix; the
+// serial chain across tiles is then one step per 32 tiles instead of one.
+__device__ __forceinline__ uint32_t look_back_warp(const uint32_t* status, int64_t tile) {
+  const int lane = threadIdx.x & 31;
+  uint32_t excl = 0;
+  for (int64_t top = tile - 1;; top -= 32) {
+    const int64_t t = top - lane;  // lane 0 = nearest predecessor
+    uint32_t s = t >= 0 ? ld_status(status + t) : kStPre;  // before tile 0: prefix 0
+    while (__any_sync(0xffffffffu, (s & ~kStCount) == 0u))
+      if ((s & ~kStCount) == 0u) s = ld_status(status + t);
+    const uint32_t pre = __ballot_sync(0xffffffffu, (s & kStPre) != 0u);
+    const int stop = pre ? __ffs(pre) - 1 : 31;  // include lanes 0..stop
+    excl += __reduce_add_sync(0xffffffffu, lane <= stop ? (s & kStCount) : 0u);
+    if (pre) return excl;
+  }
+}
+
 // Exclusive prefix of this tile's aggregate over all earlier tiles (one
 // thread; walks back until an inclusive prefix is found).
 __device__ __forceinline__ uint32_t look_back(const uint32_t* status, int64_t tile, int64_t stride) {
@@ -106,24 +125,32 @@ __global__ void __launch_bounds__(kOsThreads) scan_onepass_kernel(const uint32_t
   }
   if ((threadIdx.x & 31) == 31) s_warp[threadIdx.x >> 5] = x;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {  // warp 0: publish, then a warp-wide look-back
+    const int lane = threadIdx.x;
     uint32_t agg = 0;
-    for (int w = 0; w < kOsThreads / 32; ++w) {
-      const uint32_t c = s_warp[w];
-      s_warp[w] = agg;
-      agg += c;
+    if (lane == 0) {
+      for (int w = 0; w < kOsThreads / 32; ++w) {
+        const uint32_t c = s_warp[w];
+        s_warp[w] = agg;
+        agg += c;
+      }
     }
+    agg = __shfl_sync(0xffffffffu, agg, 0);
     uint32_t* st = status + 1;
     if (tile == 0) {
-      st_status(st, kStPre | agg);
-      s_prefix = 0;
+      if (lane == 0) {
+        st_status(st, kStPre | agg);
+        s_prefix = 0;
+      }
     } else {
-      st_status(st + tile, kStAgg | agg);
-      const uint32_t excl = look_back(st, tile, 1);
-      st_status(st + tile, kStPre | (excl + agg));
-      s_prefix = excl;
+      if (lane == 0) st_status(st + tile, kStAgg | agg);
+      const uint32_t excl = look_back_warp(st, tile);
+      if (lane == 0) {
+        st_status(st + tile, kStPre | (excl + agg));
+        s_prefix = excl;
+      }
     }
-    if (tile == ntiles - 1 && total) *total = s_prefix + agg;
+    if (lane == 0 && tile == ntiles - 1 && total) *total = s_prefix + agg;
   }
   __syncthreads();
   uint32_t run = s_prefix + s_warp[threadIdx.x >> 5] + x - sum;
