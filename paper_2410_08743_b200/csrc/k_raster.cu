@@ -682,13 +682,51 @@ __device__ __forceinline__ int half_reduce8(const float v[8], float* out) {
   return (lane & 1) ? -1 : (h1 ? 4 : 0) + (h2 ? 2 : 0) + (h3 ? 1 : 0);
 }
 
+// 9 values (full gradient: + the opacity partial) over each 16-lane half:
+// uneven reduce-scatter 9 -> 5 -> 3 -> 2 -> 1 (5 + 3 + 2 + 1 shuffles); the
+// lane with bits (b3 b2 b1 b0) ends owning component 5 b3 + 3 b2 + 2 b1 + b0
+// when that index chain stays in range (each component exactly once).
+__device__ __forceinline__ int half_reduce9(const float v[9], float* out) {
+  const int lane = threadIdx.x & 31;
+  const bool h8 = lane & 8, h4 = lane & 4, h2 = lane & 2, h1 = lane & 1;
+  float w[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    const float lo = v[i], hi = i < 4 ? v[5 + i] : 0.f;
+    const float send = h8 ? lo : hi, keep = h8 ? hi : lo;
+    w[i] = keep + __shfl_xor_sync(kFull, send, 8);
+  }
+  float x[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const float lo = w[i], hi = i < 2 ? w[3 + i] : 0.f;
+    const float send = h4 ? lo : hi, keep = h4 ? hi : lo;
+    x[i] = keep + __shfl_xor_sync(kFull, send, 4);
+  }
+  float y[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float lo = x[i], hi = i < 1 ? x[2] : 0.f;
+    const float send = h2 ? lo : hi, keep = h2 ? hi : lo;
+    y[i] = keep + __shfl_xor_sync(kFull, send, 2);
+  }
+  float z;
+  {
+    const float send = h1 ? y[0] : y[1], keep = h1 ? y[1] : y[0];
+    z = keep + __shfl_xor_sync(kFull, send, 1);
+  }
+  const int xi = (h2 ? 2 : 0) + (h1 ? 1 : 0), wi = (h4 ? 3 : 0) + xi, vi = (h8 ? 5 : 0) + wi;
+  *out = z;
+  return (xi < 3 && wi < 5 && vi < 9) ? vi : -1;
+}
+
+template <int NC>
 __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_half_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ ranks, const SplatRec* __restrict__ rec,
     const SplatAux* __restrict__ aux, const CamDev* __restrict__ cam_p, RasterDev rc, float bg_r, float bg_g,
     float bg_b, int64_t npix, const float* __restrict__ d_image, const float* __restrict__ final_t,
     const uint32_t* __restrict__ pixstate, const double* __restrict__ depth_g, double2* __restrict__ tile_cut,
     float* __restrict__ partials, uint32_t k_cap) {
-  constexpr int NC = 8;
   __shared__ StagedSplat s_sp[kBatch];
   __shared__ uint8_t s_mask[kBatch];
   __shared__ uint8_t s_list[kWarps][2][kBatch];
@@ -770,7 +808,7 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
         float v[NC];
         backward_pair<NC>(a, b, ge, ap, cb, dx, dy, ga, gb, ha, hb, rc, v);
         float tot;
-        const int vi = half_reduce8(v, &tot);
+        const int vi = NC == 8 ? half_reduce8(v, &tot) : half_reduce9(v, &tot);
         // both halves may hold the same entry in this step: half 0 adds first
         if (vi >= 0 && act && half == 0) s_red[warp][k][vi] += tot;
         __syncwarp();
@@ -811,12 +849,16 @@ int launch_composite(cudaStream_t st, gsb_frame* f, const RasterDev& rc) {
 #ifndef GSB_BWD_HALF
 #define GSB_BWD_HALF 1
 #endif
+#ifndef GSB_BWD_HALF_FULL
+#define GSB_BWD_HALF_FULL 0  // the 9-component half variant measured slower for C4 (0.881 -> 0.903 ms per joint step)
+#endif
 int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc, bool pose_only) {
   const int n_tiles = f->tiles_x * f->tiles_y;
   const int64_t npix = (int64_t)f->width * f->height;
   if (n_tiles > 0)
-    (pose_only ? (GSB_BWD_HALF ? backward_raster_half_kernel : backward_raster_kernel<8>)
-               : backward_raster_kernel<kPartial>)<<<n_tiles, kThreads, 0, st>>>(
+    (pose_only ? (GSB_BWD_HALF ? backward_raster_half_kernel<8> : backward_raster_kernel<8>)
+               : (GSB_BWD_HALF_FULL ? backward_raster_half_kernel<kPartial> : backward_raster_kernel<kPartial>))
+        <<<n_tiles, kThreads, 0, st>>>(
         f->ranges.as<uint2>(), f->list(), f->list_rec(), f->list_aux(),
         f->cam.as<CamDev>(), rc, (float)f->background[0], (float)f->background[1], (float)f->background[2], npix,
         f->d_image.as<float>(), f->final_t.as<float>(), f->pixstate.as<uint32_t>(), f->depth_g.as<double>(),
