@@ -172,28 +172,14 @@ __device__ __forceinline__ float lds_f1(uint32_t a) {
   return v;
 }
 
+// Pixel state of the forward pass; bit 31 of `processed` = done (the pixel
+// terminated, or lies outside the image and is never written).
+constexpr uint32_t kDone = 0x80000000u;
 struct PixFwd {
   float T, r, g, b;
   uint32_t processed;
-  bool done;
 };
-
-__device__ __forceinline__ void composite_one(PixFwd& p, const float4& ge, const float4& ap, float col_b, float dx,
-                                              float dy, const RasterDev& rc, uint32_t idx1) {
-  if (p.done) return;
-  const float g = splat_power(ge.z, ge.w, ap.x, dx, dy);
-  if (g > rc.cutoff2_f) return;
-  const float alpha = fminf(rc.alpha_clamp_f, ap.y * exp_neg_half(g));
-  const float w = alpha * p.T;
-  p.r = fmaf(ap.z, w, p.r);
-  p.g = fmaf(ap.w, w, p.g);
-  p.b = fmaf(col_b, w, p.b);
-  p.T *= (1.0f - alpha);
-  if (p.T < rc.early_term_f) {
-    p.done = true;
-    p.processed = idx1;
-  }
-}
+__device__ __forceinline__ bool pix_done(const PixFwd& p, const RasterDev&) { return (int32_t)p.processed < 0; }
 
 // Both pixels of a lane for one splat, branch free (alpha = 0 is an exact
 // no-op for a pixel that is done or outside the cutoff).
@@ -201,8 +187,8 @@ __device__ __forceinline__ void composite_pair(PixFwd& a, PixFwd& b, const float
                                                float dx, float dy, const RasterDev& rc, uint32_t idx1) {
   const float ga = splat_power(ge.z, ge.w, ap.x, dx, dy);
   const float gb = splat_power(ge.z, ge.w, ap.x, dx, dy + 1.0f);
-  const bool ha = !a.done && ga <= rc.cutoff2_f;
-  const bool hb = !b.done && gb <= rc.cutoff2_f;
+  const bool ha = !pix_done(a, rc) && ga <= rc.cutoff2_f;
+  const bool hb = !pix_done(b, rc) && gb <= rc.cutoff2_f;
   if (!(ha || hb)) return;
   const float al_a = ha ? fminf(rc.alpha_clamp_f, ap.y * exp_neg_half(ga)) : 0.f;
   const float al_b = hb ? fminf(rc.alpha_clamp_f, ap.y * exp_neg_half(gb)) : 0.f;
@@ -215,14 +201,8 @@ __device__ __forceinline__ void composite_pair(PixFwd& a, PixFwd& b, const float
   b.b = fmaf(col_b, wb, b.b);
   a.T *= (1.0f - al_a);
   b.T *= (1.0f - al_b);
-  if (ha && a.T < rc.early_term_f) {
-    a.done = true;
-    a.processed = idx1;
-  }
-  if (hb && b.T < rc.early_term_f) {
-    b.done = true;
-    b.processed = idx1;
-  }
+  if (ha && a.T < rc.early_term_f) a.processed = idx1 | kDone;
+  if (hb && b.T < rc.early_term_f) b.processed = idx1 | kDone;
 }
 
 __device__ __forceinline__ void write_pixel(const PixFwd& p, int x, int y, int W, int H, float bg_r, float bg_g,
@@ -239,7 +219,7 @@ __device__ __forceinline__ void write_pixel(const PixFwd& p, int x, int y, int W
   image[npix + q] = cg;
   image[2 * npix + q] = cb;
   final_t[q] = p.T;
-  pixstate[q] = p.processed | (of << 29);
+  pixstate[q] = (p.processed & ~kDone) | (of << 29);
 }
 
 #ifdef GSB_COMP_MIN_BLOCKS  // (an explicit minimum of 1 changes ptxas's register choice: leave it unset)
@@ -272,10 +252,10 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
   const double ox = (double)(tx * kTile), oy = (double)(ty * kTile);
   const float px = (float)lx, py = (float)ly;
   const uint2 range = ranges[tile];
-  PixFwd a{1.f, 0.f, 0.f, 0.f, 0u, !(x < W && y < H)};
-  PixFwd b{1.f, 0.f, 0.f, 0.f, 0u, !(x < W && y + 1 < H)};
+  PixFwd a{1.f, 0.f, 0.f, 0.f, (x < W && y < H) ? 0u : kDone};
+  PixFwd b{1.f, 0.f, 0.f, 0.f, (x < W && y + 1 < H) ? 0u : kDone};
   for (uint32_t base = range.x; base < range.y; base += kBatch) {
-    if (__syncthreads_count(a.done && b.done) == kThreads) break;
+    if (__syncthreads_count(pix_done(a, rc) && pix_done(b, rc)) == kThreads) break;
     const uint32_t e = base + threadIdx.x;
     const int cnt = min((uint32_t)kBatch, range.y - base);
     if (threadIdx.x < cnt)
@@ -285,7 +265,7 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
     const uint32_t list0 = base - range.x;
     // a finished sub-warp lists nothing (its region's pixels are all terminated)
     uint32_t lim[kSubs];
-    const uint32_t live = __ballot_sync(kFull, !(a.done && b.done));
+    const uint32_t live = __ballot_sync(kFull, !(pix_done(a, rc) && pix_done(b, rc)));
 #pragma unroll
     for (int s = 0; s < kSubs; ++s) lim[s] = ((live >> (8 * s)) & 0xffu) ? 0xffffffffu : 0u;
     int mine = 0;
@@ -301,11 +281,11 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
         composite_pair(a, b, ge, ap, cb, dx, dy, rc, list0 + k + 1u);
       }
       // a sub-warp whose 16 pixels have all terminated stops early
-      if (__all_sync(kFull, (a.done && b.done) || it + 1 >= mine)) break;
+      if (__all_sync(kFull, (pix_done(a, rc) && pix_done(b, rc)) || it + 1 >= mine)) break;
     }
     (void)sub_mask;
-    if (!a.done) a.processed = list0 + (uint32_t)cnt;
-    if (!b.done) b.processed = list0 + (uint32_t)cnt;
+    if (!pix_done(a, rc)) a.processed = list0 + (uint32_t)cnt;
+    if (!pix_done(b, rc)) b.processed = list0 + (uint32_t)cnt;
   }
   write_pixel(a, x, y, W, H, bg_r, bg_g, bg_b, npix, image, final_t, pixstate);
   write_pixel(b, x, y + 1, W, H, bg_r, bg_g, bg_b, npix, image, final_t, pixstate);
