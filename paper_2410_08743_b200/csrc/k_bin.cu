@@ -378,8 +378,11 @@ __device__ void sort_tile(TileSortSmem<CAP, NT, NB>& S, uint2 r, const unsigned 
   __syncthreads();
 }
 
-constexpr int kSortThreads = 256, kSortLargeThreads = 1024;
-using SmallSmem = TileSortSmem<kTileSortSmall, kSortThreads, 2048>;
+#ifndef GSB_SORT_SMALL_THREADS
+#define GSB_SORT_SMALL_THREADS 512
+#endif
+constexpr int kSortThreads = GSB_SORT_SMALL_THREADS, kSortLargeThreads = 1024;
+using SmallSmem = TileSortSmem<kTileSortSmall, kSortThreads, (kTileSortSmall > 2048 ? kTileSortSmall : 2048)>;
 using LargeSmem = TileSortSmem<kTileSortLarge, kSortLargeThreads, 4096>;
 static_assert(2 * (sizeof(LargeSmem) + 128 + 1024) <= 228 * 1024, "two large-sort CTAs per SM");
 
