@@ -472,14 +472,8 @@ __global__ void __launch_bounds__(kJointBlock) joint_adam_kernel(float* __restri
       const float inv_s = (float)ctl.inv_slots;
       bool quat_moved = false;
       float q[4];
-      for (int p = 0; p < ctl.nplanes; ++p) {
+      auto step = [&](int p, float lr) {
         const int64_t k = (int64_t)p * n_pad + i;
-        float lr;
-        if (p < kQuatW) lr = s_lr[0];
-        else if (p < kScaleX) lr = s_lr[1];
-        else if (p < kOpacity) lr = s_lr[2];
-        else if (p == kOpacity) lr = s_lr[3];
-        else lr = ((p - kShBase) % ctl.basis == 0) ? s_lr[4] : s_lr[5];
         float gi = grads[k] * inv_s;
         if (p >= kScaleX && p < kOpacity) gi = (float)((double)gi + dls[p - kScaleX]);
         if (p == kOpacity) gi = (float)((double)gi + dop);
@@ -494,6 +488,18 @@ __global__ void __launch_bounds__(kJointBlock) joint_adam_kernel(float* __restri
           q[p - kQuatW] = nw;
           quat_moved = quat_moved || (nw != old);
         }
+      };
+      // geometry / opacity planes (fixed count, unrolled)
+#pragma unroll
+      for (int p = 0; p < kShBase; ++p)
+        step(p, p < kQuatW ? s_lr[0] : p < kScaleX ? s_lr[1] : p < kOpacity ? s_lr[2] : s_lr[3]);
+      // SH planes c * basis + b: DC band at b == 0 (pipelines.cpp:33); unrolled
+      // so that several planes' loads are in flight per thread
+      for (int c = 0; c < 3; ++c) {
+        const int p0 = kShBase + c * ctl.basis;
+        step(p0, s_lr[4]);
+#pragma unroll 4
+        for (int b = 1; b < ctl.basis; ++b) step(p0 + b, s_lr[5]);
       }
       if (quat_moved) {  // pipelines.cpp:36-40
         const float nn = sqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
