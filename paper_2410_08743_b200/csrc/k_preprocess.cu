@@ -126,8 +126,12 @@ __device__ __forceinline__ void sh_colour(const float* __restrict__ P, int64_t n
 // per-thread reads below then come from shared memory (stride kPreBlock).
 constexpr int kPreBlock = 256;
 // (an explicit minBlocks of 1 lets ptxas spend 138 registers -> 1 CTA/SM;
-// the default form keeps 124 and 2 CTAs/SM)
-#ifdef GSB_PRE_MIN_BLOCKS
+// the default form keeps 124 and 2 CTAs/SM; 3 CTAs/SM = 80 registers with
+// ~100 B spilled measured best: K1 0.107 -> 0.101 ms, pose batch +0.9 %)
+#ifndef GSB_PRE_MIN_BLOCKS
+#define GSB_PRE_MIN_BLOCKS 3
+#endif
+#if GSB_PRE_MIN_BLOCKS > 1
 #define GSB_PRE_BOUNDS __launch_bounds__(kPreBlock, GSB_PRE_MIN_BLOCKS)
 #else
 #define GSB_PRE_BOUNDS __launch_bounds__(kPreBlock)
