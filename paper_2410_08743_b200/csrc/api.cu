@@ -66,6 +66,7 @@ int launch_pose_iter(cudaStream_t st, void* state, const double* dpose, const do
                      double lr_end, double eps, int budget, CamDev* cam, double* trace_pose, double* trace_loss,
                      const uint32_t* k_dev, int64_t k_cap);
 int32_t pose_state_take_aborted(void* host_state, uint32_t* k_max, uint32_t* tile_ovf);
+int32_t pose_state_aborted(const void* host_state);
 size_t pose_state_bytes();
 int pose_state_init(void* host_state, const double pose[12]);
 void pose_state_read(const void* host_state, double best_pose[12], double cur_pose[12], double* final_loss,
@@ -1999,8 +2000,29 @@ int gsb_pose_batch_step_async(gsb_ctx* ctx, gsb_pose_batch* b, int32_t iteration
 int gsb_pose_batch_sync(gsb_ctx* ctx, gsb_pose_batch* b) {
   if (int r = ensure_device(ctx)) return r;
   if (!b || b->ctx != ctx) return fail(GSB_ERR_INVALID_ARGUMENT, "pose batch / context mismatch");
-  for (gsb_session* s : b->sessions)
-    if (int r = session_sync(ctx, s)) return r;  // re-runs discarded iterations on the session's own graph
+  // Every session's status block in one round trip; only sessions that had
+  // iterations discarded go through session_sync, which re-runs them on the
+  // session's own graph.
+  const size_t sb = pose_state_bytes();
+  for (gsb_session* s : b->sessions) {
+    GSB_CUDA(cudaMemcpyAsync(s->host_state, s->state.p, sb, cudaMemcpyDeviceToHost, ctx->stream));
+    gsb_frame* f = session_frame(ctx, s);
+    if (f->counters.p)
+      GSB_CUDA(cudaMemcpyAsync(s->host_counters, f->counters.p, 3 * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+  }
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (gsb_session* s : b->sessions) {
+    if (pose_state_aborted(s->host_state) != 0) {
+      if (int r = session_sync(ctx, s)) return r;
+      continue;
+    }
+    pose_state_read(s->host_state, nullptr, nullptr, nullptr, nullptr, nullptr, &s->stopped, nullptr, nullptr, nullptr,
+                    nullptr);
+    s->n_splats = s->host_counters[0];
+    s->n_entries = s->host_counters[1];
+    s->pending = 0;
+  }
   return GSB_OK;
 }
 

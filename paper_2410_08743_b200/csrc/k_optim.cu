@@ -691,6 +691,7 @@ void pose_state_read(const void* host_state, double best_pose[12], double cur_po
   }
   if (step) *step = s->step;
 }
+int32_t pose_state_aborted(const void* host_state) { return static_cast<const PoseState*>(host_state)->aborted; }
 int32_t pose_state_take_aborted(void* host_state, uint32_t* k_max, uint32_t* tile_ovf) {
   PoseState* s = static_cast<PoseState*>(host_state);
   const int32_t a = s->aborted;
