@@ -82,26 +82,31 @@ __global__ void __launch_bounds__(kGeomBlock, (kFull ? 2 : GSB_GEOM_POSE_MIN_BLO
   __shared__ __align__(128) double s_dep[kGeomBlock];
   __shared__ CamDev cam;
   __shared__ double s_pose[8][6];
-  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bar, bar2;
   const int64_t i0 = (int64_t)blockIdx.x * kGeomBlock;
+  // Two transactions: the entry bookkeeping (counts, offsets, rects, depths)
+  // lands first and the partial-sum loop starts on it while the parameter
+  // and colour-Jacobian planes are still in flight.
   if (threadIdx.x == 0) {
     cam = *cam_p;
     mbar_init(&bar, 1);
+    mbar_init(&bar2, 1);
     const int64_t here = n - i0 < kGeomBlock ? n - i0 : kGeomBlock;
     const uint32_t bytes = (uint32_t)(((here * 4) + 15) & ~(int64_t)15);
     const uint32_t b8 = (uint32_t)(((here * 8) + 15) & ~(int64_t)15);
     const uint32_t brect = cutd.aux_g ? (uint32_t)(here * 16) : b8;
     // cnt_g / off_g are sized to whole 256-blocks (frame_reserve), colj to n_pad
-    mbar_arrive_expect_tx(&bar, bytes * (kGeomPlanes + 9 + 2) + b8 + brect);
+    mbar_arrive_expect_tx(&bar, bytes * 2 + b8 + brect);
+    tma_load_1d(s_cnt, cnt_g + i0, bytes, &bar);
+    tma_load_1d(s_off, off_g + i0, bytes, &bar);
     tma_load_1d(s_dep, cutd.depth_g + i0, b8, &bar);
     if (cutd.aux_g)
       tma_load_1d(s_rect, cutd.aux_g + i0, brect, &bar);
     else
       tma_load_1d(s_rect, cutd.rect_g + i0, brect, &bar);
-    for (int p = 0; p < kGeomPlanes; ++p) tma_load_1d(s_par + p * kGeomBlock, params + p * n_pad_g + i0, bytes, &bar);
-    for (int p = 0; p < 9; ++p) tma_load_1d(s_colj + p * kGeomBlock, colj + p * n_pad_g + i0, bytes, &bar);
-    tma_load_1d(s_cnt, cnt_g + i0, bytes, &bar);
-    tma_load_1d(s_off, off_g + i0, bytes, &bar);
+    mbar_arrive_expect_tx(&bar2, bytes * (kGeomPlanes + 9));
+    for (int p = 0; p < kGeomPlanes; ++p) tma_load_1d(s_par + p * kGeomBlock, params + p * n_pad_g + i0, bytes, &bar2);
+    for (int p = 0; p < 9; ++p) tma_load_1d(s_colj + p * kGeomBlock, colj + p * n_pad_g + i0, bytes, &bar2);
   }
   __syncthreads();
   mbar_wait(&bar, 0);
@@ -162,6 +167,7 @@ __global__ void __launch_bounds__(kGeomBlock, (kFull ? 2 : GSB_GEOM_POSE_MIN_BLO
         }
       }
     }
+    mbar_wait(&bar2, 0);
     const float* P = s_par + threadIdx.x;
     constexpr int64_t n_pad = kGeomBlock;  // plane stride of the staged copy
     const R mean0 = P[kMeanX * n_pad], mean1 = P[kMeanY * n_pad], mean2 = P[kMeanZ * n_pad];
@@ -334,6 +340,7 @@ __global__ void __launch_bounds__(kGeomBlock, (kFull ? 2 : GSB_GEOM_POSE_MIN_BLO
       grads[(int64_t)(nplanes + 1) * n_pad_g + i] = (float)dmu2y;
     }
   }
+  mbar_wait(&bar2, 0);  // no thread leaves before every bulk copy into this CTA's shared memory has landed
   // deterministic block reduction of the pose contributions
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double pcs[6] = {pc0, pc1, pc2, pc3, pc4, pc5};
