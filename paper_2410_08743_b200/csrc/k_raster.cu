@@ -39,7 +39,11 @@
 namespace gsb {
 
 constexpr int kThreads = 128;          // 2 pixels per thread
-constexpr int kBatch = kThreads;       // records staged per batch
+constexpr int kBatch = kThreads;       // records staged per batch (backward)
+#ifndef GSB_COMP_BATCH
+#define GSB_COMP_BATCH 128
+#endif
+constexpr int kCompBatch = GSB_COMP_BATCH;  // records staged per composite batch (multiple of 128, <= 256)
 constexpr int kWarps = kThreads / 32;  // 4 warps = 4 quadrants of 8x8
 constexpr int kSubs = 4;               // 8-lane sub-warps per warp = 4x4 regions
 constexpr unsigned kFull = 0xffffffffu;
@@ -120,8 +124,9 @@ __device__ __forceinline__ int region_of(int warp, int s) {
 // whose list position is below lim[s]) into list[s][...] in ascending order,
 // for the four sub-warps of this warp at once; returns this lane's
 // sub-warp count in *mine and the warp's largest count.
+template <int CB>
 __device__ __forceinline__ int build_lists(const uint16_t* s_mask, int cnt, int warp, const uint32_t lim[kSubs],
-                                           uint32_t b0, uint8_t (*list)[kBatch], int* mine) {
+                                           uint32_t b0, uint8_t (*list)[CB], int* mine) {
   const int lane = threadIdx.x & 31;
   const uint32_t lt = lanemask_lt_();
   int r[kSubs], n[kSubs];
@@ -131,7 +136,7 @@ __device__ __forceinline__ int build_lists(const uint16_t* s_mask, int cnt, int 
     n[s] = 0;
   }
 #pragma unroll
-  for (int c = 0; c < kBatch / 32; ++c) {
+  for (int c = 0; c < CB / 32; ++c) {
     const int e = c * 32 + lane;
     const uint32_t m = e < cnt ? s_mask[e] : 0u;
 #pragma unroll
@@ -231,9 +236,10 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ ranks, const SplatRec* __restrict__ rec,
     const CamDev* __restrict__ cam_p, RasterDev rc, float bg_r, float bg_g, float bg_b, int64_t npix,
     float* __restrict__ image, float* __restrict__ final_t, uint32_t* __restrict__ pixstate) {
-  __shared__ StagedSplat s_sp[kBatch];
-  __shared__ uint16_t s_mask[kBatch];
-  __shared__ uint8_t s_list[kWarps][kSubs][kBatch];
+  constexpr int CB = kCompBatch;
+  __shared__ StagedSplat s_sp[CB];
+  __shared__ uint16_t s_mask[CB];
+  __shared__ uint8_t s_list[kWarps][kSubs][CB];
   __shared__ int s_w, s_h, s_tx;
   if (threadIdx.x == 0) {
     s_w = cam_p->width;
@@ -254,13 +260,16 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
   const uint2 range = ranges[tile];
   PixFwd a{1.f, 0.f, 0.f, 0.f, (x < W && y < H) ? 0u : kDone};
   PixFwd b{1.f, 0.f, 0.f, 0.f, (x < W && y + 1 < H) ? 0u : kDone};
-  for (uint32_t base = range.x; base < range.y; base += kBatch) {
+  for (uint32_t base = range.x; base < range.y; base += CB) {
     if (__syncthreads_count(pix_done(a, rc) && pix_done(b, rc)) == kThreads) break;
-    const uint32_t e = base + threadIdx.x;
-    const int cnt = min((uint32_t)kBatch, range.y - base);
-    if (threadIdx.x < cnt)
-      s_mask[threadIdx.x] = (uint16_t)stage_splat(rec[ranks[e]], ox, oy, rc.cutoff2_f, &s_sp[threadIdx.x].geo,
-                                                  &s_sp[threadIdx.x].app, &s_sp[threadIdx.x].col_b);
+    const int cnt = min((uint32_t)CB, range.y - base);
+#pragma unroll
+    for (int u = 0; u < CB / kThreads; ++u) {
+      const int t = u * kThreads + threadIdx.x;
+      if (t < cnt)
+        s_mask[t] = (uint16_t)stage_splat(rec[ranks[base + t]], ox, oy, rc.cutoff2_f, &s_sp[t].geo, &s_sp[t].app,
+                                          &s_sp[t].col_b);
+    }
     __syncthreads();
     const uint32_t list0 = base - range.x;
     // a finished sub-warp lists nothing (its region's pixels are all terminated)
@@ -269,7 +278,7 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
 #pragma unroll
     for (int s = 0; s < kSubs; ++s) lim[s] = ((live >> (8 * s)) & 0xffu) ? 0xffffffffu : 0u;
     int mine = 0;
-    const int nmax = build_lists(s_mask, cnt, warp, lim, 0u, s_list[warp], &mine);
+    const int nmax = build_lists<CB>(s_mask, cnt, warp, lim, 0u, s_list[warp], &mine);
     for (int it = 0; it < nmax; ++it) {
       if (it < mine) {
         const int k = s_list[warp][sub][it];
