@@ -51,6 +51,9 @@ constexpr int kGeomBlock = 256;
 #ifndef GSB_GEOM_POSE_MIN_BLOCKS
 #define GSB_GEOM_POSE_MIN_BLOCKS 5  // 48 registers: occupancy over ~100 spilled bytes (measured: 4 -> 5 CTAs/SM, 0.087 -> 0.085 ms)
 #endif
+#ifndef GSB_GEOM_FULL_MIN_BLOCKS
+#define GSB_GEOM_FULL_MIN_BLOCKS 2
+#endif
 #ifndef GSB_POSE_CHAIN_T
 #define GSB_POSE_CHAIN_T float
 #endif
@@ -70,7 +73,7 @@ struct EntryCut {
 // bundle (joint_optimize's parameter gradients), float for the pose-only
 // path (the 6-vector itself is accumulated in FP64 either way).
 template <bool kFull, typename R>
-__global__ void __launch_bounds__(kGeomBlock, (kFull ? 2 : GSB_GEOM_POSE_MIN_BLOCKS)) backward_geom_kernel(
+__global__ void __launch_bounds__(kGeomBlock, (kFull ? GSB_GEOM_FULL_MIN_BLOCKS : GSB_GEOM_POSE_MIN_BLOCKS)) backward_geom_kernel(
     const float* __restrict__ params, int64_t n, int64_t n_pad_g, int sh_cap, int sh_active,
     const CamDev* __restrict__ cam_p, RasterDev rc, const uint32_t* __restrict__ cnt_g,
     const uint32_t* __restrict__ off_g, const float* __restrict__ colj, const float* __restrict__ partials,
