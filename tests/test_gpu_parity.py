@@ -85,6 +85,28 @@ def test_render_matches_oracle_conditioned(G, ctx, seed):
     assert np.all(d["accum_transmittance"] + d["final_transmittance"] == 1.0)
 
 
+@pytest.mark.parametrize("early", [0.0, 0.3, 2.0])
+def test_early_termination_configs_match_oracle(G, ctx, early):
+    """RasterConfig.early_termination beyond the default: 0 (never stop), a
+    large threshold, and > 1, where every pixel stops right after including
+    its first splat (rasterizer.cpp:257-258: T is updated, then compared).
+    Contrib counts bit-exact, image and final T within 1e-5, d_pose 1e-3."""
+    hc, ocam, bg, rng = scene(55, 12, 48)
+    cloud = to_dev(G, ctx, hc)
+    cam = dev_cam(G, ocam)
+    out = G.render(ctx, cloud, cam, bg, config=G.RasterConfig.default(early_termination=early))
+    ref = O.render(hc, ocam, bg, cfg=O.default_raster_config(early_termination=early), keep_handle=True)
+    d = out.download()
+    assert np.array_equal(d["contrib_count"], ref.contrib_count)
+    assert np.max(np.abs(d["image"] - ref.image)) < 1e-5
+    assert np.max(np.abs(d["final_transmittance"] - ref.final_transmittance)) < 1e-5
+    d_img = np.random.default_rng(7).uniform(-1, 1, ref.image.shape)
+    _, dp = G.render_backward(ctx, cloud, cam, out, d_img, pose_only=True)
+    gr = O.render_backward(hc, ocam, ref, d_img)
+    ref.free()
+    assert rel_err(dp, gr.d_pose) < 1e-3
+
+
 @pytest.fixture(params=["tile_local", "global"])
 def binning(request, G, ctx):
     mode = G.Context.BINNING_TILE_LOCAL if request.param == "tile_local" else G.Context.BINNING_GLOBAL
