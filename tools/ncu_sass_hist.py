@@ -1,7 +1,7 @@
 """Per-SASS-address executed warp instructions from an ncu report (--set
-full, -lineinfo), bucketed into address ranges: python tools/ncu_sass_hist.py
-report.ncu-rep [kernel-regex] — prints per-range instruction totals, the
-hottest addresses and thread utilisation (avg active threads per instruction)."""
+full, -lineinfo) of a one-kernel report, bucketed into 256-byte address
+ranges: python tools/ncu_sass_hist.py report.ncu-rep — prints each range's
+share of the executed instructions and its average active threads."""
 import csv
 import subprocess
 import sys
