@@ -426,6 +426,34 @@ def test_estimate_pose_trajectory_matches_oracle(G, ctx):
     assert np.max(np.abs(res["trace_loss"] - ref["trace_loss"])) < 1e-4
 
 
+def test_c1_pose_descent_log_matches_oracle(G, ctx):
+    """C1, the CPU-oracle parity config: 10k Gaussians SH-3,
+    256x256, orbit camera 0 of seed 99, perturb 15 deg / 0.15 from Rng(1002),
+    100 pose_descent iterations with the cosine schedule. The per-iteration
+    pose log stays within rot 0.1 deg / trans 1e-3 of the oracle's
+    (test_trainer.cpp:506-507). The loss log follows the poses (not part of
+    the contract): within 5e-3 relative per iteration (measured 1.2e-3 at
+    worst) and the final loss within 1e-3 relative."""
+    hc, poses = synth_scene(99, 10000, 256, scale_offset=math.log(500 / 10000) / 3)
+    cam = O.synth_camera(256, 256, poses[0])
+    target = O.render(hc, cam).image
+    noisy = O.perturb_pose(poses[0], 15.0, 0.15, O.make_rng(1002))
+    budget = 100
+    ref = O.estimate_pose(hc, target, cam.fx, cam.fy, cam.cx, cam.cy, noisy, budget=budget, pose_converged_eps=0.0)
+    cloud = to_dev(G, ctx, hc)
+    img = G.Image(ctx, target)
+    cfg = G.PoseConfig.default(budget=budget, pose_converged_eps=0.0)
+    res = G.estimate_pose(ctx, cloud, img, [cam.fx, cam.fy, cam.cx, cam.cy], noisy, cfg, trace=True)
+    assert res["steps"] == ref["steps"] == budget
+    worst = (0.0, 0.0)
+    for k in range(res["steps"]):
+        r, d = O.abs_pose_error(res["trace_pose"][k], ref["trace_pose"][k])
+        worst = (max(worst[0], r), max(worst[1], d))
+    assert worst[0] < 0.1 and worst[1] < 1e-3, worst
+    rel = np.abs(res["trace_loss"] - ref["trace_loss"]) / ref["trace_loss"]
+    assert np.max(rel) < 5e-3 and rel[-1] < 1e-3, (np.max(rel), rel[-1])
+
+
 def test_pose_batch_bitwise_equals_sequential_sessions(G, ctx):
     """A pose batch (sessions as parallel graph branches, private forward
     states) gives bit-identical per-view trajectories to stepping each
