@@ -91,30 +91,36 @@ __device__ __forceinline__ void stage_planes(float (*dst)[kSH][kSW + 1], const f
 }
 
 // Horizontal pass of the five SSIM statistics (a, b, a^2, b^2, ab) over the
-// staged rows: task = (row, 4-column group); 42 rows x 8 groups = 336 tasks.
+// staged rows: task = (row, HR-column group). Every output sums its 11 taps in
+// the same order whatever HR is (bit-identical); HR = 2 gives 42 x 16 = 672
+// tasks = 2.6 rounds of 256 threads instead of 336 = 1.3 rounds at HR = 4.
+#ifndef GSB_LOSS_HR
+#define GSB_LOSS_HR 4
+#endif
+constexpr int kHR = GSB_LOSS_HR;
 __device__ __forceinline__ void hpass5(const float (*st)[kSH][kSW + 1], double (*hq)[kSH][kTW + 1]) {
-  for (int task = threadIdx.x; task < kSH * (kTW / kR); task += kThr) {
-    const int r = task / (kTW / kR), q0 = (task - r * (kTW / kR)) * kR;
-    double x[kR + kWin - 1], y[kR + kWin - 1];
+  for (int task = threadIdx.x; task < kSH * (kTW / kHR); task += kThr) {
+    const int r = task / (kTW / kHR), q0 = (task - r * (kTW / kHR)) * kHR;
+    double x[kHR + kWin - 1], y[kHR + kWin - 1];
 #pragma unroll
-    for (int k = 0; k < kR + kWin - 1; ++k) {
+    for (int k = 0; k < kHR + kWin - 1; ++k) {
       x[k] = st[0][r][q0 + k];
       y[k] = st[1][r][q0 + k];
     }
 #pragma unroll
     for (int m = 0; m < 5; ++m) {
-      double acc[kR];
+      double acc[kHR];
 #pragma unroll
-      for (int j = 0; j < kR; ++j) acc[j] = 0.0;
+      for (int j = 0; j < kHR; ++j) acc[j] = 0.0;
 #pragma unroll
-      for (int k = 0; k < kR + kWin - 1; ++k) {
+      for (int k = 0; k < kHR + kWin - 1; ++k) {
         const double f = m == 0 ? x[k] : m == 1 ? y[k] : m == 2 ? x[k] * x[k] : m == 3 ? y[k] * y[k] : x[k] * y[k];
 #pragma unroll
-        for (int j = 0; j < kR; ++j)
+        for (int j = 0; j < kHR; ++j)
           if (k - j >= 0 && k - j < kWin) acc[j] = fma(c_win[k - j], f, acc[j]);
       }
 #pragma unroll
-      for (int j = 0; j < kR; ++j) hq[m][r][q0 + j] = acc[j];
+      for (int j = 0; j < kHR; ++j) hq[m][r][q0 + j] = acc[j];
     }
   }
 }
@@ -205,22 +211,22 @@ __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, 
 
 // Horizontal pass of the three gradient maps (back-convolution, losses.cpp:144-151).
 __device__ __forceinline__ void hpass3(const float (*st)[kSH][kSW + 1], double (*hq)[kSH][kTW + 1]) {
-  for (int task = threadIdx.x; task < kSH * (kTW / kR); task += kThr) {
-    const int r = task / (kTW / kR), q0 = (task - r * (kTW / kR)) * kR;
+  for (int task = threadIdx.x; task < kSH * (kTW / kHR); task += kThr) {
+    const int r = task / (kTW / kHR), q0 = (task - r * (kTW / kHR)) * kHR;
 #pragma unroll
     for (int m = 0; m < 3; ++m) {
-      double acc[kR];
+      double acc[kHR];
 #pragma unroll
-      for (int j = 0; j < kR; ++j) acc[j] = 0.0;
+      for (int j = 0; j < kHR; ++j) acc[j] = 0.0;
 #pragma unroll
-      for (int k = 0; k < kR + kWin - 1; ++k) {
+      for (int k = 0; k < kHR + kWin - 1; ++k) {
         const double f = st[m][r][q0 + k];
 #pragma unroll
-        for (int j = 0; j < kR; ++j)
+        for (int j = 0; j < kHR; ++j)
           if (k - j >= 0 && k - j < kWin) acc[j] = fma(c_win[k - j], f, acc[j]);
       }
 #pragma unroll
-      for (int j = 0; j < kR; ++j) hq[m][r][q0 + j] = acc[j];
+      for (int j = 0; j < kHR; ++j) hq[m][r][q0 + j] = acc[j];
     }
   }
 }
