@@ -385,6 +385,34 @@ def test_backward_c1_scene_pose_gradient(G, ctx):
     assert np.linalg.norm(dp - gr.d_pose) / np.linalg.norm(gr.d_pose) < 1e-3
 
 
+def test_backward_c3_scale_pose_gradient(G, ctx):
+    """The bench's workload size (C3: 1M Gaussians SH-3, 1008x756, view 0 at
+    its perturbed init pose) with the oracle's loss gradient as d_image: the
+    pose-only d_pose (half-quadrant K4a, per-tile cut, FP32 per-splat chain)
+    within 1e-3 relative of the FP64 oracle, and the rendered image within
+    1e-5 on all but the pixels an FP32 cutoff / termination decision flips."""
+    import bench
+    _, hc = bench._oracle_scene()
+    gt, init = bench.all_views()
+    intr = G.synth_intrinsics(bench.WIDTH, bench.HEIGHT)
+    cam_gt = O.make_camera(*intr, bench.WIDTH, bench.HEIGHT, *O.pose_split(gt[0]))
+    ocam = O.make_camera(*intr, bench.WIDTH, bench.HEIGHT, *O.pose_split(init[0]))
+    target = O.render(hc, cam_gt).image
+    ref = O.render(hc, ocam, keep_handle=True)
+    _, d_img = O.rgb_loss(ref.image, target, 0.2)
+    gr = O.render_backward(hc, ocam, ref, d_img)
+    ref.free()
+    cloud = G.Cloud(ctx, bench.N_GAUSS, bench.SH_DEGREE)
+    cloud.synth(bench.SCENE_SEED, bench.log_scale_offset(bench.N_GAUSS))
+    cam = G.Camera.from_pose12(*intr, bench.WIDTH, bench.HEIGHT, init[0])
+    out = G.render(ctx, cloud, cam)
+    err = np.max(np.abs(out.image - ref.image), axis=2)
+    assert np.mean(err < 1e-5) > 0.99, np.mean(err < 1e-5)
+    _, dp = G.render_backward(ctx, cloud, cam, out, d_img, pose_only=True)
+    rel = np.linalg.norm(dp - gr.d_pose) / np.linalg.norm(gr.d_pose)
+    assert rel < 1e-3, rel
+
+
 # ------------------------------------------------------------- optimiser
 def test_pose_step_matches_oracle(G, ctx):
     R, t = O.se3_exp(np.array([0.3, -0.2, 0.5, 0.4, -0.7, 0.2]))
