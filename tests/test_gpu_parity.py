@@ -413,6 +413,33 @@ def test_backward_c3_scale_pose_gradient(G, ctx):
     assert rel < 1e-3, rel
 
 
+def test_c3_scale_trajectory_matches_oracle(G, ctx):
+    """The bench's unit of work at full size: 10 pose_descent iterations of
+    C3 view 0 (1M Gaussians SH-3, 1008x756, early exits off) through the
+    device session against the FP64 oracle: every iteration's pose within
+    rot 0.1 deg / trans 1e-3 (test_trainer.cpp:506-507), loss within 1e-3
+    relative."""
+    import bench
+    _, hc = bench._oracle_scene()
+    gt, init = bench.all_views()
+    intr = G.synth_intrinsics(bench.WIDTH, bench.HEIGHT)
+    cam_gt = O.make_camera(*intr, bench.WIDTH, bench.HEIGHT, *O.pose_split(gt[0]))
+    target = O.render(hc, cam_gt).image
+    budget = 10
+    ref = O.estimate_pose(hc, target, *intr, init[0], budget=budget, pose_converged_eps=0.0)
+    cloud = G.Cloud(ctx, bench.N_GAUSS, bench.SH_DEGREE)
+    cloud.synth(bench.SCENE_SEED, bench.log_scale_offset(bench.N_GAUSS))
+    img = G.Image(ctx, target)
+    cfg = G.PoseConfig.default(budget=budget, pose_converged_eps=0.0)
+    res = G.estimate_pose(ctx, cloud, img, list(intr), init[0], cfg, trace=True)
+    assert res["steps"] == ref["steps"] == budget
+    for k in range(budget):
+        r, d = O.abs_pose_error(res["trace_pose"][k], ref["trace_pose"][k])
+        assert r < 0.1 and d < 1e-3, (k, r, d)
+    rel = np.abs(res["trace_loss"] - ref["trace_loss"]) / ref["trace_loss"]
+    assert np.max(rel) < 1e-3, rel
+
+
 # ------------------------------------------------------------- optimiser
 def test_pose_step_matches_oracle(G, ctx):
     R, t = O.se3_exp(np.array([0.3, -0.2, 0.5, 0.4, -0.7, 0.2]))
