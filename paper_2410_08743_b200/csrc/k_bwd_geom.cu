@@ -369,9 +369,20 @@ __global__ void __launch_bounds__(256) pose_reduce_kernel(const double* __restri
                                                           double* __restrict__ out) {
   __shared__ double s[6][256];
   double t[6] = {0, 0, 0, 0, 0, 0};
-  for (int64_t b = threadIdx.x; b < nb; b += 256) {
+  // four blocks' partials loaded per round (independent loads in flight),
+  // added in block order: the association is fixed, so the sum is deterministic
+  for (int64_t b0 = threadIdx.x; b0 < nb; b0 += 4 * 256) {
+    double u[4][6];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) t[k] += blocks[b * 6 + k];
+    for (int q = 0; q < 4; ++q) {
+      const int64_t b = b0 + (int64_t)q * 256;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) u[q][k] = b < nb ? blocks[b * 6 + k] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) t[k] += u[q][k];
   }
 #pragma unroll
   for (int k = 0; k < 6; ++k) s[k][threadIdx.x] = t[k];
