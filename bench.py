@@ -220,6 +220,7 @@ def run_ours(args, ws, rank, local):
     e2e_value = VIEWS_PER_GPU * ws * e2e_iters / e2e_s
 
     joint = None if args.no_joint else run_joint(args, ws, rank, local, dist)
+    single = None if args.no_joint else run_single_view(args, ws, rank, local)
     out = None
     if rank == 0:
         # roofline for the dominant stage
@@ -262,6 +263,8 @@ def run_ours(args, ws, rank, local):
         }
         if joint is not None:
             out["joint_c4"] = joint
+        if single is not None:
+            out["single_view_c2"] = single
         if cpu is not None:
             out["cpu_baseline"] = cpu
         if work is not None:
@@ -274,6 +277,38 @@ def run_ours(args, ws, rank, local):
 
 # ------------------------------------------------ C4: joint DP (secondary)
 C4_N, C4_VIEWS, C4_SEED = 300_000, 20, 4
+C2_N, C2_SEED = 300_000, 2
+
+
+def run_single_view(args, ws, rank, local):
+    """Secondary line, config C2: one view's pose_descent on a
+    300k-Gaussian forward-facing scene at 1008x756 (seed 2, perturb 15 deg /
+    0.15 from Rng(1002)) through one session — the single-view latency path
+    (one CUDA-graph replay per iteration, no other views to overlap with).
+    Rank 0 only (a replica per GPU would measure the same thing)."""
+    if rank != 0:
+        return None
+    from paper_2410_08743_b200 import gsb
+    ctx = gsb.Context(local)
+    cloud = gsb.Cloud(ctx, C2_N, SH_DEGREE)
+    cloud.synth(C2_SEED, log_scale_offset(C2_N))
+    gt = gsb.synth_poses(C2_SEED, C2_N, SH_DEGREE, 1, 1)
+    init = gsb.PoseRng(NOISE_SEED).perturb_pose(gt[0], 15.0, 0.15)
+    intr = gsb.synth_intrinsics(WIDTH, HEIGHT)
+    img = gsb.Image(ctx, gsb.render(ctx, cloud, gsb.Camera.from_pose12(*intr, WIDTH, HEIGHT, gt[0])).image)
+    steps = max(args.steps, 10)
+    s = gsb.PoseSession(ctx, cloud, img, intr, init,
+                        gsb.PoseConfig.default(budget=args.warmup + steps + 4, pose_converged_eps=0.0))
+    s.step(args.warmup)
+    ctx.timer_start()
+    s.step_async(steps)  # graph replays back to back, no host round trip
+    ms = ctx.timer_stop()
+    res = s.read()  # (re-runs any iteration discarded for capacity growth)
+    assert res["steps"] == args.warmup + steps, res["steps"]
+    return {"workload": f"C2 single-view pose estimation: {C2_N} Gaussians SH3, {WIDTH}x{HEIGHT}, forward-facing, "
+                        "perturb 15deg/0.15, one session", "iters_per_s": round(steps / (ms / 1e3), 2),
+            "ms_per_iter": round(ms / steps, 4), "steps": steps}
+
 
 
 def run_joint(args, ws, rank, local, dist):
