@@ -40,6 +40,13 @@ namespace gsb {
 
 constexpr int kThreads = 128;          // 2 pixels per thread
 constexpr int kBatch = kThreads;       // records staged per batch (backward)
+// Composite steps: every lane runs the (no-op when inactive) pair update and
+// only a step no lane of the warp hits is skipped (warp-uniform), instead of
+// per-lane branches around exhausted sub-lists and missing lanes: 0.107 ->
+// 0.103 ms.
+#ifndef GSB_COMP_UNIFORM_SKIP
+#define GSB_COMP_UNIFORM_SKIP 1
+#endif
 #ifndef GSB_COMP_BATCH
 #define GSB_COMP_BATCH 128
 #endif
@@ -189,12 +196,17 @@ __device__ __forceinline__ bool pix_done(const PixFwd& p, const RasterDev&) { re
 // Both pixels of a lane for one splat, branch free (alpha = 0 is an exact
 // no-op for a pixel that is done or outside the cutoff).
 __device__ __forceinline__ void composite_pair(PixFwd& a, PixFwd& b, const float4& ge, const float4& ap, float col_b,
-                                               float dx, float dy, const RasterDev& rc, uint32_t idx1) {
+                                               float dx, float dy, const RasterDev& rc, uint32_t idx1,
+                                               bool act = true) {
   const float ga = splat_power(ge.z, ge.w, ap.x, dx, dy);
   const float gb = splat_power(ge.z, ge.w, ap.x, dx, dy + 1.0f);
-  const bool ha = !pix_done(a, rc) && ga <= rc.cutoff2_f;
-  const bool hb = !pix_done(b, rc) && gb <= rc.cutoff2_f;
+  const bool ha = act && !pix_done(a, rc) && ga <= rc.cutoff2_f;
+  const bool hb = act && !pix_done(b, rc) && gb <= rc.cutoff2_f;
+#if GSB_COMP_UNIFORM_SKIP
+  if (!__any_sync(kFull, ha || hb)) return;  // warp-uniform: lanes without a hit run the no-op update
+#else
   if (!(ha || hb)) return;
+#endif
   const float al_a = ha ? fminf(rc.alpha_clamp_f, ap.y * exp_neg_half(ga)) : 0.f;
   const float al_b = hb ? fminf(rc.alpha_clamp_f, ap.y * exp_neg_half(gb)) : 0.f;
   const float wa = al_a * a.T, wb = al_b * b.T;
@@ -280,6 +292,18 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
     int mine = 0;
     const int nmax = build_lists<CB>(s_mask, cnt, warp, lim, 0u, s_list[warp], &mine);
     for (int it = 0; it < nmax; ++it) {
+#if GSB_COMP_UNIFORM_SKIP
+      {
+        const bool act = it < mine;
+        const int k = act ? s_list[warp][sub][it] : 0;
+        const StagedSplat& S = s_sp[k];
+        const float4 ge = S.geo;
+        const float4 ap = S.app;
+        const float cb = S.col_b;
+        const float dx = px - ge.x, dy = py - ge.y;
+        composite_pair(a, b, ge, ap, cb, dx, dy, rc, list0 + k + 1u, act);
+      }
+#else
       if (it < mine) {
         const int k = s_list[warp][sub][it];
         const StagedSplat& S = s_sp[k];
@@ -289,6 +313,7 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
         const float dx = px - ge.x, dy = py - ge.y;
         composite_pair(a, b, ge, ap, cb, dx, dy, rc, list0 + k + 1u);
       }
+#endif
       // a sub-warp whose 16 pixels have all terminated stops early
       if (__all_sync(kFull, (pix_done(a, rc) && pix_done(b, rc)) || it + 1 >= mine)) break;
     }
