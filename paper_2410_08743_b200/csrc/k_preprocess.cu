@@ -120,16 +120,20 @@ __device__ __forceinline__ void sh_colour(const float* __restrict__ P, int64_t n
   *clamp = cl;
 }
 
-// The CTA's 256-Gaussian segment of every parameter plane is staged into
+// The CTA's kPreBlock-Gaussian segment of every parameter plane is staged into
 // shared memory with one TMA bulk copy per plane (issued by one thread,
 // completing on an mbarrier), so all ~59 KB are in flight at once; the
 // per-thread reads below then come from shared memory (stride kPreBlock).
-constexpr int kPreBlock = 256;
+#ifndef GSB_PRE_BLOCK
+#define GSB_PRE_BLOCK 128
+#endif
+constexpr int kPreBlock = GSB_PRE_BLOCK;
 // (an explicit minBlocks of 1 lets ptxas spend 138 registers -> 1 CTA/SM;
-// the default form keeps 124 and 2 CTAs/SM; 3 CTAs/SM = 80 registers with
-// ~100 B spilled measured best: K1 0.107 -> 0.101 ms, pose batch +0.9 %)
+// the default form keeps 124 and 2 CTAs/SM of 256 threads; measured best:
+// 128-thread CTAs at 5 CTAs/SM — K1 0.107 (256 x 2) -> 0.101 (256 x 3) ->
+// 0.094 ms (128 x 5), pose batch +1.2 % over 256 x 2)
 #ifndef GSB_PRE_MIN_BLOCKS
-#define GSB_PRE_MIN_BLOCKS 3
+#define GSB_PRE_MIN_BLOCKS 5
 #endif
 #if GSB_PRE_MIN_BLOCKS > 1
 #define GSB_PRE_BOUNDS __launch_bounds__(kPreBlock, GSB_PRE_MIN_BLOCKS)
@@ -323,7 +327,7 @@ __device__ __forceinline__ void reserve_slots(const PreOut& o, int64_t i, uint32
   }
 }
 
-// K1 over `nviews` cameras at once: the CTA's 256-Gaussian segment of every
+// K1 over `nviews` cameras at once: the CTA's kPreBlock-Gaussian segment of every
 // parameter plane is staged into shared memory with one TMA bulk copy per
 // plane (issued by one thread, completing on an mbarrier), the
 // view-independent geometry is evaluated once, and each view's projection,
