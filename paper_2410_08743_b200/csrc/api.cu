@@ -403,7 +403,7 @@ static int frame_reserve(gsb_frame* f, const gsb_cloud* cloud, int64_t k_cap) {
   GSB_CUDA(f->loss_blocks.reserve(sizeof(double) * 2 * loss_block_count(f->width, f->height), &grew));
   GSB_CUDA(f->loss_val.reserve(sizeof(double) * 4, &grew));
   GSB_CUDA(f->partials.reserve(sizeof(float) * kPartial * k_cap, &grew));
-  GSB_CUDA(f->pose_blocks.reserve(sizeof(double) * 6 * ((n + 255) / 256 + 1), &grew));
+  GSB_CUDA(f->pose_blocks.reserve(sizeof(double) * 6 * ((n + 63) / 64 + 1), &grew));  // K4b blocks of >= 64
   GSB_CUDA(f->d_pose.reserve(sizeof(double) * 6, &grew));
   if (grew) {
     ++f->gen;

@@ -47,7 +47,11 @@ __device__ __forceinline__ void sh_basis_d(double x, double y, double z, int deg
 // The CTA's 256-Gaussian segments of the 11 geometry/opacity planes, the 9
 // colour-Jacobian planes, the tile counts and the entry offsets are staged
 // into shared memory by TMA bulk copies (one elected thread, one mbarrier).
-constexpr int kGeomBlock = 256;
+#ifndef GSB_GEOM_BLOCK
+#define GSB_GEOM_BLOCK 256
+#endif
+constexpr int kGeomBlock = GSB_GEOM_BLOCK;
+constexpr int kGeomWarps = kGeomBlock / 32;
 #ifndef GSB_GEOM_POSE_MIN_BLOCKS
 #define GSB_GEOM_POSE_MIN_BLOCKS 5  // 48 registers: occupancy over ~100 spilled bytes (measured: 4 -> 5 CTAs/SM, 0.087 -> 0.085 ms)
 #endif
@@ -84,7 +88,7 @@ __global__ void __launch_bounds__(kGeomBlock, (kFull ? GSB_GEOM_FULL_MIN_BLOCKS 
   __shared__ __align__(128) uint4 s_rect[kGeomBlock];  // SplatAux (tile-local) or uint2 rect pairs (global)
   __shared__ __align__(128) double s_dep[kGeomBlock];
   __shared__ CamDev cam;
-  __shared__ double s_pose[8][6];
+  __shared__ double s_pose[kGeomWarps][6];
   __shared__ __align__(8) uint64_t bar, bar2;
   const int64_t i0 = (int64_t)blockIdx.x * kGeomBlock;
   // Two transactions: the entry bookkeeping (counts, offsets, rects, depths)
@@ -357,7 +361,7 @@ __global__ void __launch_bounds__(kGeomBlock, (kFull ? GSB_GEOM_FULL_MIN_BLOCKS 
   __syncthreads();
   if (threadIdx.x < 6) {
     double t = 0.0;
-    for (int w2 = 0; w2 < 8; ++w2) t += s_pose[w2][threadIdx.x];
+    for (int w2 = 0; w2 < kGeomWarps; ++w2) t += s_pose[w2][threadIdx.x];
     pose_blocks[(int64_t)blockIdx.x * 6 + threadIdx.x] = t;
   }
 }
@@ -406,15 +410,15 @@ int launch_backward_geom(cudaStream_t st, const gsb_cloud* cloud, gsb_frame* f, 
   cutd.aux_g = f->binning == kBinTileLocal ? f->aux_g.as<SplatAux>() : nullptr;
   cutd.rect_g = f->rect_g.as<uint2>();
   cutd.tiles_x = f->tiles_x;
-  const int64_t nb = (n + 255) / 256;
+  const int64_t nb = (n + kGeomBlock - 1) / kGeomBlock;
   if (nb > 0) {
     if (full)
-      backward_geom_kernel<true, double><<<(unsigned)nb, 256, 0, st>>>(
+      backward_geom_kernel<true, double><<<(unsigned)nb, kGeomBlock, 0, st>>>(
           cloud->params.as<float>(), n, cloud->n_pad, cloud->sh_degree, cloud->active_sh_degree, f->cam.as<CamDev>(),
           rc, f->cnt_g.as<uint32_t>(), f->off_g.as<uint32_t>(), f->colj.as<float>(), f->partials.as<float>(), f->k_cap, cutd, grads,
           f->pose_blocks.as<double>());
     else
-      backward_geom_kernel<false, GSB_POSE_CHAIN_T><<<(unsigned)nb, 256, 0, st>>>(
+      backward_geom_kernel<false, GSB_POSE_CHAIN_T><<<(unsigned)nb, kGeomBlock, 0, st>>>(
           cloud->params.as<float>(), n, cloud->n_pad, cloud->sh_degree, cloud->active_sh_degree, f->cam.as<CamDev>(),
           rc, f->cnt_g.as<uint32_t>(), f->off_g.as<uint32_t>(), f->colj.as<float>(), f->partials.as<float>(), f->k_cap, cutd, nullptr,
           f->pose_blocks.as<double>());
