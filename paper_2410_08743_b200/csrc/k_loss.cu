@@ -304,9 +304,21 @@ __global__ void __launch_bounds__(256) loss_finalize_kernel(const double* __rest
   }
   __shared__ double s1[256], s2[256];
   double a = 0.0, b = 0.0;
-  for (int i = threadIdx.x; i < nb; i += 256) {
-    a += block_sums[2 * i];
-    b += block_sums[2 * i + 1];
+  // four blocks' sums loaded per round (independent loads in flight), added
+  // in block order: fixed association, deterministic
+  for (int i0 = threadIdx.x; i0 < nb; i0 += 4 * 256) {
+    double u[4][2];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = i0 + q * 256;
+      u[q][0] = i < nb ? block_sums[2 * i] : 0.0;
+      u[q][1] = i < nb ? block_sums[2 * i + 1] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      a += u[q][0];
+      b += u[q][1];
+    }
   }
   s1[threadIdx.x] = a;
   s2[threadIdx.x] = b;
