@@ -189,6 +189,106 @@ def lib():
     return _lib
 
 
+# ------------------------------------------------------------ backends
+# "port": the clean-room restatement (liboracle.so). "reference": the
+# reference's own sources compiled against oracle/shim (oracle/_ref, see
+# build_ref.py); entry points with a reference counterpart route there, the
+# rest (allocation helpers, work counters, generators without one) stay on
+# the port. Select with `with reference_backend(): ...`.
+REF_LIB_PATH = os.path.join(HERE, "_ref", "libgsopt_ref.so")
+_REF_NAMES = ("render", "render_free", "render_backward", "grads_free", "rgb_loss", "schedule", "pose_step",
+              "make_gradcheck_scene", "scene_is_conditioned", "gradcheck", "perturb_pose", "perturb_pose_tangent",
+              "joint_optimize", "cloud_free")
+_backend = ["port"]
+_ref_lib = None
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_LIB_PATH)
+
+
+def ref_lib():
+    """oracle/_ref/libgsopt_ref.so with argtypes (orc_* signatures, ref_* names)."""
+    global _ref_lib
+    if _ref_lib is None:
+        L = C.CDLL(REF_LIB_PATH)
+        port = lib()
+        for name in _REF_NAMES:
+            f, g = getattr(L, "ref_" + name), getattr(port, "orc_" + name)
+            f.restype, f.argtypes = g.restype, g.argtypes
+        P = C.POINTER
+        d, i32, vp = C.c_double, C.c_int32, C.c_void_p
+        L.ref_pose_descent_traced.restype = i32
+        L.ref_pose_descent_traced.argtypes = port.orc_estimate_pose.argtypes
+        L.ref_estimate_pose.restype = i32
+        L.ref_estimate_pose.argtypes = port.orc_estimate_pose.argtypes[:16]
+        L.ref_synth_scene.restype = None
+        L.ref_synth_scene.argtypes = [i32, i32, i32, i32, i32, i32, C.c_uint64, P(Cloud), vp, vp]
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_thread_count.restype = C.c_int
+        _ref_lib = L
+    return _ref_lib
+
+
+class _RefRouter:
+    def __getattr__(self, name):
+        base = name[4:] if name.startswith("orc_") else name
+        if base == "estimate_pose":
+            return ref_lib().ref_pose_descent_traced
+        if base in _REF_NAMES:
+            return getattr(ref_lib(), "ref_" + base)
+        return getattr(lib(), name)
+
+
+def _L():
+    return _RefRouter() if _backend[0] == "reference" else lib()
+
+
+class reference_backend:
+    """Context manager: route the wrappers below to the reference build."""
+
+    def __enter__(self):
+        if not ref_available():
+            raise FileNotFoundError(f"{REF_LIB_PATH} missing: run oracle/build_ref.py")
+        self.prev = _backend[0]
+        _backend[0] = "reference"
+        return self
+
+    def __exit__(self, *exc):
+        _backend[0] = self.prev
+        return False
+
+
+def ref_estimate_pose(cloud: "HostCloud", image, fx, fy, cx, cy, init12, budget=1000, cam_lr_start=1e-2,
+                      cam_lr_end=1e-4, beta=0.2, pose_converged_eps=1e-7, bg=(0, 0, 0), cfg=None):
+    """The reference's own estimate_pose (pipelines.cpp:218-222 -> 58-92), no traces."""
+    pc = PoseCfg()
+    pc.cam_lr_start, pc.cam_lr_end, pc.beta, pc.pose_converged_eps = cam_lr_start, cam_lr_end, beta, pose_converged_eps
+    for k in range(3):
+        pc.background[k] = bg[k]
+    pc.raster = cfg or default_raster_config()
+    img = np.ascontiguousarray(image, np.float64)
+    R0, t0 = pose_split(init12)
+    Ro, to = np.zeros(9), np.zeros(3)
+    fl, conv = C.c_double(), C.c_int32()
+    steps = ref_lib().ref_estimate_pose(cloud.c().ref(), _p(img), fx, fy, cx, cy, img.shape[1], img.shape[0], _p(R0),
+                                        _p(t0), C.byref(pc), budget, _p(Ro), _p(to),
+                                        C.cast(C.byref(fl), C.c_void_p), C.cast(C.byref(conv), C.c_void_p))
+    return dict(pose=pose_join(Ro, to), steps=steps, final_loss=fl.value, converged=bool(conv.value))
+
+
+def ref_synth_scene(gaussians, cameras, width, height, kind, sh_degree, seed, with_images=False):
+    """synth.cpp:33-135 run by the reference: (HostCloud, poses (cameras,12), images or None)."""
+    cc = Cloud()
+    poses = np.zeros((cameras, 12))
+    imgs = np.zeros((cameras, height, width, 3)) if with_images else None
+    ref_lib().ref_synth_scene(gaussians, cameras, width, height, kind, sh_degree, seed, C.byref(cc), _p(poses),
+                              _p(imgs) if with_images else None)
+    hc = _from_c_cloud(cc)
+    lib().orc_cloud_free(C.byref(cc))
+    return hc, poses, imgs
+
+
 def _p(a: np.ndarray):
     assert a.flags["C_CONTIGUOUS"]
     return a.ctypes.data_as(C.c_void_p)
@@ -203,13 +303,13 @@ def _arr(ptr, n, dtype=np.float64):
 # ------------------------------------------------------------------ types
 def make_rng(seed: int) -> Rng:
     r = Rng()
-    lib().orc_rng_init(C.byref(r), seed)
+    _L().orc_rng_init(C.byref(r), seed)
     return r
 
 
 def default_raster_config(**kw) -> RasterConfig:
     c = RasterConfig()
-    lib().orc_default_raster_config(C.byref(c))
+    _L().orc_default_raster_config(C.byref(c))
     for k, v in kw.items():
         setattr(c, k, v)
     return c
@@ -290,15 +390,15 @@ def _from_c_cloud(cc: Cloud) -> HostCloud:
 def synth_cloud(n: int, sh_degree: int, rng: Rng) -> HostCloud:
     """synth.cpp:45-62 draws (consumes rng)."""
     cc = Cloud()
-    lib().orc_synth_cloud(C.byref(cc), n, sh_degree, C.byref(rng))
+    _L().orc_synth_cloud(C.byref(cc), n, sh_degree, C.byref(rng))
     hc = _from_c_cloud(cc)
-    lib().orc_cloud_free(C.byref(cc))
+    _L().orc_cloud_free(C.byref(cc))
     return hc
 
 
 def synth_poses(kind: int, cameras: int, rng: Rng, orbit_radius=2.5, orbit_arc=2 * np.pi) -> np.ndarray:
     out = np.zeros((cameras, 12))
-    lib().orc_synth_poses(kind, cameras, orbit_radius, orbit_arc, C.byref(rng), _p(out))
+    _L().orc_synth_poses(kind, cameras, orbit_radius, orbit_arc, C.byref(rng), _p(out))
     return out
 
 
@@ -314,14 +414,14 @@ def pose_join(R, t):
 def perturb_pose(p12, rot_deg, trans, rng: Rng):
     R, t = pose_split(p12)
     Ro, to = np.zeros(9), np.zeros(3)
-    lib().orc_perturb_pose(_p(R), _p(t), rot_deg, trans, C.byref(rng), _p(Ro), _p(to))
+    _L().orc_perturb_pose(_p(R), _p(t), rot_deg, trans, C.byref(rng), _p(Ro), _p(to))
     return pose_join(Ro, to)
 
 
 def perturb_pose_tangent(p12, sigma, rng: Rng):
     R, t = pose_split(p12)
     Ro, to = np.zeros(9), np.zeros(3)
-    lib().orc_perturb_pose_tangent(_p(R), _p(t), sigma, C.byref(rng), _p(Ro), _p(to))
+    _L().orc_perturb_pose_tangent(_p(R), _p(t), sigma, C.byref(rng), _p(Ro), _p(to))
     return pose_join(Ro, to)
 
 
@@ -329,7 +429,7 @@ def abs_pose_error(pred12, gt12):
     Rp, tp = pose_split(pred12)
     Rg, tg = pose_split(gt12)
     r, d = C.c_double(), C.c_double()
-    lib().orc_abs_pose_error(_p(Rp), _p(tp), _p(Rg), _p(tg), C.cast(C.byref(r), C.c_void_p),
+    _L().orc_abs_pose_error(_p(Rp), _p(tp), _p(Rg), _p(tg), C.cast(C.byref(r), C.c_void_p),
                              C.cast(C.byref(d), C.c_void_p))
     return r.value, d.value
 
@@ -363,9 +463,11 @@ class RenderResult:
     fingerprint: int
     _ptr: object = None
 
+    _free: object = None
+
     def free(self):
         if self._ptr is not None:
-            lib().orc_render_free(self._ptr)
+            self._free(self._ptr)
             self._ptr = None
 
 
@@ -374,7 +476,7 @@ def render(cloud: HostCloud, cam: Camera, bg=(0.0, 0.0, 0.0), cfg: RasterConfig 
     cfg = cfg or default_raster_config()
     cv = cloud.c()
     bgv = np.asarray(bg, np.float64)
-    ptr = lib().orc_render(cv.ref(), C.byref(cam), _p(bgv), C.byref(cfg))
+    ptr = _L().orc_render(cv.ref(), C.byref(cam), _p(bgv), C.byref(cfg))
     o = ptr.contents
     P = o.width * o.height
     V = o.n_splats
@@ -399,8 +501,10 @@ def render(cloud: HostCloud, cam: Camera, bg=(0.0, 0.0, 0.0), cfg: RasterConfig 
     if keep_handle:
         rr._ptr = ptr
         rr._cloud_view = cv
+        rr._free = _L().orc_render_free
+        rr._lib = _L()
     else:
-        lib().orc_render_free(ptr)
+        _L().orc_render_free(ptr)
     return rr
 
 
@@ -427,7 +531,8 @@ def render_backward(cloud: HostCloud, cam: Camera, rr: RenderResult, d_image: np
     d = np.ascontiguousarray(d_image, np.float64)
     h, w = (d.shape[0], d.shape[1]) if d.ndim == 3 else (cam.height, cam.width)
     g = Grads()
-    rc = lib().orc_render_backward(cv.ref(), C.byref(cam), rr._ptr, _p(d), w, h, C.byref(g))
+    L = rr._lib
+    rc = L.orc_render_backward(cv.ref(), C.byref(cam), rr._ptr, _p(d), w, h, C.byref(g))
     if rc != 0:
         raise OracleError(rc, "state_mismatch" if rc == 6 else "dimension_mismatch")
     n = cloud.n
@@ -436,7 +541,7 @@ def render_backward(cloud: HostCloud, cam: Camera, rr: RenderResult, d_image: np
                      _arr(g.d_log_scales, 3 * n).reshape(n, 3), _arr(g.d_opacity_logits, n),
                      _arr(g.d_sh, 3 * b * n).reshape(n, 3, b), _arr(g.d_mu2d, 2 * n).reshape(n, 2),
                      np.array(g.d_pose[:]))
-    lib().orc_grads_free(C.byref(g))
+    _L().orc_grads_free(C.byref(g))
     return out
 
 
@@ -454,7 +559,7 @@ def bin_records(keep, mu2d, radius, depth, width, height, tile_size=16):
     cap = 1 << 16
     while True:
         lists = np.zeros(cap, np.int32)
-        k = lib().orc_bin_records(n, _p(keep), _p(mu2d), _p(radius), _p(depth), width, height, tile_size,
+        k = _L().orc_bin_records(n, _p(keep), _p(mu2d), _p(radius), _p(depth), width, height, tile_size,
                                   _p(sorted_g), C.cast(C.byref(nsp), C.c_void_p), _p(lists), cap, _p(ranges))
         if k >= 0:
             return sorted_g[:nsp.value].copy(), lists[:k].copy(), ranges
@@ -467,7 +572,7 @@ def rgb_loss(rendered, target, beta=0.2, want_grad=True):
     t = np.ascontiguousarray(target, np.float64)
     h, w = r.shape[0], r.shape[1]
     d = np.zeros_like(r) if want_grad else None
-    loss = lib().orc_rgb_loss(_p(r), _p(t), w, h, beta, _p(d) if want_grad else None)
+    loss = _L().orc_rgb_loss(_p(r), _p(t), w, h, beta, _p(d) if want_grad else None)
     return (loss, d) if want_grad else loss
 
 
@@ -475,40 +580,40 @@ def ssim(a, b, want_grad=False):
     a = np.ascontiguousarray(a, np.float64)
     b = np.ascontiguousarray(b, np.float64)
     d = np.zeros_like(a) if want_grad else None
-    v = lib().orc_ssim(_p(a), _p(b), a.shape[1], a.shape[0], _p(d) if want_grad else None)
+    v = _L().orc_ssim(_p(a), _p(b), a.shape[1], a.shape[0], _p(d) if want_grad else None)
     return (v, d) if want_grad else v
 
 
 def anisotropy_loss(log_scales, ratio=10.0):
     ls = np.ascontiguousarray(log_scales, np.float64)
     d = np.zeros_like(ls)
-    v = lib().orc_anisotropy_loss(_p(ls), ls.shape[0], ratio, _p(d))
+    v = _L().orc_anisotropy_loss(_p(ls), ls.shape[0], ratio, _p(d))
     return v, d
 
 
 # ---------------------------------------------------------------- trainer
 def schedule(kind, start, end, step, total):
-    return lib().orc_schedule(0 if kind == "cosine" else 1, start, end, step, total)
+    return _L().orc_schedule(0 if kind == "cosine" else 1, start, end, step, total)
 
 
 def pose_step(p12, d_pose, lr, adam: PoseAdam):
     R, t = pose_split(p12)
     dp = np.ascontiguousarray(d_pose, np.float64)
     Ro, to, ap = np.zeros(9), np.zeros(3), np.zeros(6)
-    lib().orc_pose_step(_p(R), _p(t), _p(dp), lr, C.byref(adam), _p(Ro), _p(to), _p(ap))
+    _L().orc_pose_step(_p(R), _p(t), _p(dp), lr, C.byref(adam), _p(Ro), _p(to), _p(ap))
     return pose_join(Ro, to), ap
 
 
 def se3_exp(tau):
     tau = np.ascontiguousarray(tau, np.float64)
     R, t = np.zeros(9), np.zeros(3)
-    lib().orc_se3_exp(_p(tau), _p(R), _p(t))
+    _L().orc_se3_exp(_p(tau), _p(R), _p(t))
     return R.reshape(3, 3), t
 
 
 def orthonormalize(R):
     R = np.ascontiguousarray(np.asarray(R, np.float64).reshape(9)).copy()
-    lib().orc_orthonormalize(_p(R))
+    _L().orc_orthonormalize(_p(R))
     return R.reshape(3, 3)
 
 
@@ -528,7 +633,7 @@ def estimate_pose(cloud: HostCloud, image, fx, fy, cx, cy, init12, budget=1000, 
     conv = C.c_int32()
     tp, tl, td = np.zeros((budget, 12)), np.zeros(budget), np.zeros((budget, 6))
     cv = cloud.c()
-    steps = lib().orc_estimate_pose(cv.ref(), _p(img), fx, fy, cx, cy, w, h, _p(R0), _p(t0), C.byref(pc), budget,
+    steps = _L().orc_estimate_pose(cv.ref(), _p(img), fx, fy, cx, cy, w, h, _p(R0), _p(t0), C.byref(pc), budget,
                                     _p(Ro), _p(to), C.cast(C.byref(fl), C.c_void_p),
                                     C.cast(C.byref(conv), C.c_void_p), _p(tp), _p(tl), _p(td))
     return dict(pose=pose_join(Ro, to), steps=steps, final_loss=fl.value, converged=bool(conv.value),
@@ -552,7 +657,7 @@ class CloudAdam:
         P = C.POINTER(C.c_double)
         og.d_means, og.d_rotations, og.d_log_scales, og.d_opacity_logits, og.d_sh = [b.ctypes.data_as(P) for b in bufs]
         lrs = np.ascontiguousarray(lrs, np.float64)
-        lib().orc_cloud_adam_step(self.view.ref(), C.byref(og), C.cast(self.states, C.c_void_p), _p(lrs))
+        _L().orc_cloud_adam_step(self.view.ref(), C.byref(og), C.cast(self.states, C.c_void_p), _p(lrs))
 
     def cloud(self) -> HostCloud:
         hc = self.view.hc
@@ -569,12 +674,12 @@ def densify_and_prune(cloud: HostCloud, grad_sum, count, grad_threshold=2e-4, si
     out = Cloud()
     fs = C.POINTER(C.c_int32)()
     rep = np.zeros(3, np.int32)
-    lib().orc_densify_and_prune(cv.ref(), _p(gs), _p(ct), grad_threshold, size_ratio, n_target, prune_opacity,
+    _L().orc_densify_and_prune(cv.ref(), _p(gs), _p(ct), grad_threshold, size_ratio, n_target, prune_opacity,
                                 C.byref(rng), C.byref(out), C.cast(C.byref(fs), C.c_void_p), _p(rep))
     res = _from_c_cloud(out)
     src = np.ctypeslib.as_array(fs, shape=(max(out.n, 1),))[:out.n].copy() if out.n else np.zeros(0, np.int32)
-    lib().orc_free(C.cast(fs, C.c_void_p))
-    lib().orc_cloud_free(C.byref(out))
+    _L().orc_free(C.cast(fs, C.c_void_p))
+    _L().orc_cloud_free(C.byref(out))
     return res, src, tuple(int(x) for x in rep)
 
 
@@ -601,14 +706,14 @@ def joint_config(iterations, **kw) -> JointCfg:
 def joint_schedule(rng: Rng, n_views: int, count: int) -> np.ndarray:
     """pipelines.cpp:122-129 view sequence (epoch shuffles in place)."""
     out = np.zeros(count, np.int32)
-    lib().orc_joint_schedule(C.byref(rng), n_views, count, _p(out))
+    _L().orc_joint_schedule(C.byref(rng), n_views, count, _p(out))
     return out
 
 
 def _alloc_c_cloud(hc: HostCloud) -> Cloud:
     """A malloc-backed copy (orc_cloud_alloc) the oracle may reallocate."""
     cc = Cloud()
-    lib().orc_cloud_alloc(C.byref(cc), hc.n, hc.sh_degree)
+    _L().orc_cloud_alloc(C.byref(cc), hc.n, hc.sh_degree)
     cc.active_sh_degree = hc.active_sh_degree
     for name, arr in (("means", hc.means), ("rotations", hc.rotations), ("log_scales", hc.log_scales),
                       ("opacity_logits", hc.opacity_logits), ("sh", hc.sh)):
@@ -626,10 +731,10 @@ def joint_optimize(cloud: HostCloud, images, intr, width, height, poses, cfg: Jo
     ptrs = (C.c_void_p * len(imgs))(*[im.ctypes.data for im in imgs])
     P = np.ascontiguousarray(np.asarray(poses, np.float64).reshape(-1, 12)).copy()
     tt, tl = np.zeros(cfg.iterations), np.zeros(cfg.iterations)
-    st = lib().orc_joint_optimize(C.byref(cc), C.cast(ptrs, C.c_void_p), len(imgs), intr[0], intr[1], intr[2],
+    st = _L().orc_joint_optimize(C.byref(cc), C.cast(ptrs, C.c_void_p), len(imgs), intr[0], intr[1], intr[2],
                                   intr[3], width, height, _p(P), C.byref(cfg), slots, C.byref(rng), _p(tt), _p(tl))
     out = _from_c_cloud(cc)
-    lib().orc_cloud_free(C.byref(cc))
+    _L().orc_cloud_free(C.byref(cc))
     return st, out, P, tt, tl
 
 
@@ -671,7 +776,7 @@ def masked_rgb_loss(rendered, target, mask, beta=0.2, want_grad=True):
     m = np.ascontiguousarray(mask, np.uint8).reshape(-1)
     d = np.zeros_like(r) if want_grad else None
     st = C.c_int32()
-    loss = lib().orc_masked_rgb_loss(_p(r), _p(t), r.shape[1], r.shape[0], _p(m), beta,
+    loss = _L().orc_masked_rgb_loss(_p(r), _p(t), r.shape[1], r.shape[0], _p(m), beta,
                                      _p(d) if d is not None else None, C.byref(st))
     if st.value:
         raise OracleError(st.value, "masked_l1: no pixel passes the mask")
@@ -686,7 +791,7 @@ def unproject(depth, valid, frame, intr, R, t, max_points):
     pts, cols = np.zeros((max_points, 3)), np.zeros((max_points, 3))
     Rm = np.ascontiguousarray(R, np.float64).reshape(9)
     tv = np.ascontiguousarray(t, np.float64).reshape(3)
-    n = lib().orc_unproject(_p(dep), _p(val), W, H, _p(img), intr[0], intr[1], intr[2], intr[3], _p(Rm), _p(tv),
+    n = _L().orc_unproject(_p(dep), _p(val), W, H, _p(img), intr[0], intr[1], intr[2], intr[3], _p(Rm), _p(tv),
                             max_points, _p(pts), _p(cols))
     if n < 0:
         raise OracleError(3, "unproject: empty validity mask")
@@ -696,7 +801,7 @@ def unproject(depth, valid, frame, intr, R, t, max_points):
 def mean_knn_distance(points, k=3):
     p = np.ascontiguousarray(points, np.float64)
     out = np.zeros(p.shape[0])
-    lib().orc_mean_knn_distance(_p(p), p.shape[0], k, _p(out))
+    _L().orc_mean_knn_distance(_p(p), p.shape[0], k, _p(out))
     return out
 
 
@@ -704,9 +809,9 @@ def init_from_points(points, colors, sh_degree=0) -> HostCloud:
     p = np.ascontiguousarray(points, np.float64)
     c = np.ascontiguousarray(colors, np.float64)
     out = Cloud()
-    lib().orc_init_from_points(_p(p), _p(c), p.shape[0], sh_degree, C.byref(out))
+    _L().orc_init_from_points(_p(p), _p(c), p.shape[0], sh_degree, C.byref(out))
     res = _from_c_cloud(out)
-    lib().orc_cloud_free(C.byref(out))
+    _L().orc_cloud_free(C.byref(out))
     return res
 
 
@@ -715,12 +820,12 @@ def fit_frame_gaussians(frame, depth, valid, intr, cfg: FitCfg) -> HostCloud:
     dep = np.ascontiguousarray(depth, np.float64)
     val = np.ascontiguousarray(valid, np.uint8)
     out = Cloud()
-    st = lib().orc_fit_frame_gaussians(_p(img), _p(dep), _p(val), img.shape[1], img.shape[0], intr[0], intr[1],
+    st = _L().orc_fit_frame_gaussians(_p(img), _p(dep), _p(val), img.shape[1], img.shape[0], intr[0], intr[1],
                                        intr[2], intr[3], C.byref(cfg), C.byref(out))
     if st:
         raise OracleError(3, "unproject: empty validity mask")
     res = _from_c_cloud(out)
-    lib().orc_cloud_free(C.byref(out))
+    _L().orc_cloud_free(C.byref(out))
     return res
 
 
@@ -729,7 +834,7 @@ def estimate_relative_pose(cloud: HostCloud, frame_next, intr, cfg: RelposeCfg):
     cv = cloud.c()
     img = np.ascontiguousarray(frame_next, np.float64)
     R, t, fl = np.zeros(9), np.zeros(3), C.c_double()
-    ok = lib().orc_estimate_relative_pose(cv.ref(), _p(img), img.shape[1], img.shape[0], intr[0], intr[1], intr[2],
+    ok = _L().orc_estimate_relative_pose(cv.ref(), _p(img), img.shape[1], img.shape[0], intr[0], intr[1], intr[2],
                                           intr[3], C.byref(cfg), _p(R), _p(t), C.byref(fl))
     return pose_join(R.reshape(3, 3), t), bool(ok), fl.value
 
@@ -741,7 +846,7 @@ def bootstrap_trajectory(frames, depths, valids, intr, fit: FitCfg, rel: Relpose
     va = [np.ascontiguousarray(v, np.uint8) for v in valids]
     arr = lambda xs: C.cast((C.c_void_p * n)(*[x.ctypes.data for x in xs]), C.c_void_p)  # noqa: E731
     poses, ok = np.zeros((n, 12)), np.zeros(max(n - 1, 1), np.int32)
-    st = lib().orc_bootstrap_trajectory(arr(fr), arr(de), arr(va), n, fr[0].shape[1], fr[0].shape[0], intr[0],
+    st = _L().orc_bootstrap_trajectory(arr(fr), arr(de), arr(va), n, fr[0].shape[1], fr[0].shape[0], intr[0],
                                         intr[1], intr[2], intr[3], C.byref(fit), C.byref(rel), _p(poses), _p(ok))
     if st:
         raise OracleError(3, "unproject: empty validity mask")
@@ -753,16 +858,16 @@ def make_gradcheck_scene(rng: Rng, n, image_size):
     cc = Cloud()
     cam = Camera()
     bg = np.zeros(3)
-    lib().orc_make_gradcheck_scene(C.byref(rng), n, image_size, C.byref(cc), C.byref(cam), _p(bg))
+    _L().orc_make_gradcheck_scene(C.byref(rng), n, image_size, C.byref(cc), C.byref(cam), _p(bg))
     hc = _from_c_cloud(cc)
-    lib().orc_cloud_free(C.byref(cc))
+    _L().orc_cloud_free(C.byref(cc))
     return hc, cam, bg
 
 
 def scene_is_conditioned(cloud: HostCloud, cam: Camera, bg, cfg=None) -> bool:
     cfg = cfg or default_raster_config()
     bgv = np.ascontiguousarray(bg, np.float64)
-    return bool(lib().orc_scene_is_conditioned(cloud.c().ref(), C.byref(cam), _p(bgv), C.byref(cfg)))
+    return bool(_L().orc_scene_is_conditioned(cloud.c().ref(), C.byref(cam), _p(bgv), C.byref(cfg)))
 
 
 def make_conditioned_scene(rng: Rng, n, image_size, cfg=None, max_attempts=64):
@@ -778,7 +883,7 @@ def gradcheck(cloud: HostCloud, cam: Camera, bg, rng: Rng, cfg=None, step=1e-5):
     bgv = np.ascontiguousarray(bg, np.float64)
     checked = C.c_int32()
     label = C.create_string_buffer(32)
-    err = lib().orc_gradcheck(cloud.c().ref(), C.byref(cam), _p(bgv), C.byref(cfg), C.byref(rng), step,
+    err = _L().orc_gradcheck(cloud.c().ref(), C.byref(cam), _p(bgv), C.byref(cfg), C.byref(rng), step,
                               C.byref(checked), label)
     return err, checked.value, label.value.decode()
 
@@ -788,9 +893,9 @@ def count_work(rr: RenderResult, d_image=None):
     assert rr._ptr is not None, "render(..., keep_handle=True) required"
     out = np.zeros(4, np.int64)
     d = None if d_image is None else np.ascontiguousarray(d_image, np.float64)
-    lib().orc_count_work(rr._ptr, _p(d) if d is not None else None, _p(out))
+    _L().orc_count_work(rr._ptr, _p(d) if d is not None else None, _p(out))
     return tuple(int(v) for v in out)
 
 
 def num_threads() -> int:
-    return lib().orc_num_threads()
+    return _L().orc_num_threads()
