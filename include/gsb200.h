@@ -139,6 +139,14 @@ int64_t gsb_ctx_launch_count(gsb_ctx* ctx);
 int gsb_ctx_timer_start(gsb_ctx* ctx);
 int gsb_ctx_timer_stop(gsb_ctx* ctx, double* ms_out);
 
+/* ---- measurement aids (no reference counterpart) ----
+ * FP32 FFMA throughput (TFLOP/s, FMA = 2 FLOP) and MUFU ex2 throughput
+ * (T ops/s) of `device`, measured by microbenchmark kernels at the clock the
+ * device runs at now: the denominators of the FP32-bound kernels' roofline. */
+int gsb_measure_fp32_peaks(int32_t device, double* ffma_tflops, double* mufu_tops);
+/* SHA-256 (hex) of the sources + flags this libgsb200.so was compiled from. */
+const char* gsb_build_id(void);
+
 /* ---- cloud (GaussianCloud, scene.hpp:22-46), stored as FP32 planes on device ---- */
 int gsb_cloud_create(gsb_ctx* ctx, int64_t n, int32_t sh_degree, gsb_cloud** out);
 int gsb_cloud_destroy(gsb_cloud* cloud);
@@ -294,6 +302,10 @@ int gsb_pose_batch_step(gsb_ctx* ctx, gsb_pose_batch* b, int32_t iterations);
 int gsb_pose_batch_step_async(gsb_ctx* ctx, gsb_pose_batch* b, int32_t iterations);
 /* waits for the batch; re-runs any iteration a session discarded (capacity growth) */
 int gsb_pose_batch_sync(gsb_ctx* ctx, gsb_pose_batch* b);
+/* Iterations the device discarded for entry-capacity growth (and the host
+ * re-ran in gsb_pose_batch_sync) since the batch's sessions were created.
+ * Measurement aid: a timed region must see 0. */
+int gsb_pose_batch_discarded(const gsb_pose_batch* b, int64_t* out);
 /* estimate_pose for `count` views of one cloud as one pose batch: init_poses /
  * poses_out are count x 12 (best pose per view); final_losses, steps_used optional. */
 int gsb_estimate_poses(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* const* targets, const double intr[4],

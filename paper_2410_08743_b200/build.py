@@ -30,11 +30,25 @@ def _headers():
     return glob.glob(os.path.join(PKG, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "gsb200.h")]
 
 
+def source_hash() -> str:
+    """SHA-256 over every source, header and compiler flag of the library; the
+    build stamps it into the .so (gsb_build_id) and beside it (OUT + '.id'), so
+    a shipped binary is reused only when it was built from exactly these sources."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in sorted(sources() + _headers()):
+        h.update(os.path.basename(f).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    h.update(" ".join(FLAGS).encode())
+    return h.hexdigest()
+
+
 def needs_build() -> bool:
-    if not os.path.exists(OUT):
+    if not os.path.exists(OUT) or not os.path.exists(OUT + ".id"):
         return True
-    t = os.path.getmtime(OUT)
-    return any(os.path.getmtime(s) > t for s in sources() + _headers())
+    with open(OUT + ".id") as fh:
+        return fh.read().strip() != source_hash()
 
 
 def _obj(src):
@@ -61,8 +75,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(compile_one, sources()))
-    subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", OUT + ".tmp"] + objs, cwd=PKG)
+    sh = source_hash()
+    id_src = os.path.join(OBJ, "build_id.cpp")
+    with open(id_src, "w") as fh:
+        fh.write(f'extern "C" const char* gsb_build_id(void) {{ return "{sh}"; }}\n')
+    id_obj = id_src + ".o"
+    subprocess.check_call(["g++", "-O2", "-fPIC", "-c", id_src, "-o", id_obj])
+    subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", OUT + ".tmp"] + objs + [id_obj], cwd=PKG)
     os.replace(OUT + ".tmp", OUT)
+    with open(OUT + ".id", "w") as fh:
+        fh.write(sh + "\n")
     return OUT
 
 

@@ -356,6 +356,12 @@ static int tile_bits(int n_tiles) {
 // Sizes every forward/backward buffer of the frame for (cloud, image size,
 // entry capacity). Any reallocation bumps f->gen (captured graphs hold raw
 // pointers and must be rebuilt).
+// First entry capacity of a forward state: 4 entries per Gaussian (the C3
+// scene has K ≈ 3.0 N at its views; 3 N left a few hundred entries of
+// headroom). An overflow is still detected on the device and the iteration
+// re-run with a larger capacity.
+static int64_t initial_k_cap(int64_t n) { return std::max<int64_t>(4 * n, 1 << 16); }
+
 static int frame_reserve(gsb_frame* f, const gsb_cloud* cloud, int64_t k_cap) {
   const int64_t n = std::max<int64_t>(cloud->n, 1);
   const int64_t np = std::max<int64_t>(cloud->n_pad, 1);
@@ -520,7 +526,7 @@ static void fall_back_to_global(gsb_frame* f) {
 // Synchronous forward for the host API: runs the async pass, reads (V, K)
 // and re-runs with a larger entry capacity if K overflowed it.
 static int render_sync(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, const RasterDev& rc) {
-  int64_t want = f->k_cap > 0 ? f->k_cap : std::max<int64_t>(3 * cloud->n, 1 << 16);
+  int64_t want = f->k_cap > 0 ? f->k_cap : initial_k_cap(cloud->n);
   for (int attempt = 0; attempt < 4; ++attempt) {
     if (int r = frame_reserve(f, cloud, want)) return r;
     if (int r = render_async(ctx, cloud, f, rc)) return r;
@@ -1471,6 +1477,7 @@ struct gsb_session {
   int64_t n_splats = 0, n_entries = 0;
   int32_t stopped = 0;
   int32_t pending = 0;  // iterations launched since the last status check
+  int64_t discarded = 0;  // iterations the device discarded (capacity growth) and the host re-ran
   cudaGraphExec_t exec = nullptr;
   int64_t graph_launches = 0;  // kernels per replay
   const gsb_frame* graph_frame = nullptr;
@@ -1479,6 +1486,7 @@ struct gsb_session {
   bool graph_profiled = false;
   cudaEvent_t ev[kNumStages][2] = {};
   bool have_events = false;
+  bool batch_events = false;  // the events were last recorded by a profiled pose-batch graph
   gsb_frame* own = nullptr;      // private forward state while the session is in a pose batch
   gsb_pose_batch* batch = nullptr;
 };
@@ -1497,6 +1505,7 @@ struct gsb_pose_batch {
   std::vector<uint64_t> graph_gen;
   std::vector<int64_t> graph_kcap;
   std::vector<int> graph_binning;
+  bool graph_profiled = false;  // branches carry per-stage event nodes (ctx profiling on at capture)
   int64_t graph_launches = 0;
 };
 
@@ -1562,6 +1571,7 @@ static int session_capture(gsb_ctx* ctx, gsb_session* s, gsb_frame* f) {
   s->graph_gen = f->gen;
   s->graph_kcap = f->k_cap;
   s->graph_profiled = ctx->profiling;
+  s->batch_events = false;
   if (debug_on())
     std::fprintf(stderr, "[gsb] session graph captured: %lld kernels, %.2f ms (binning %d, k_cap %lld)\n",
                  (long long)s->graph_launches, now_ms() - t_dbg, f->binning, (long long)f->k_cap);
@@ -1583,7 +1593,7 @@ static int session_frame_ready(gsb_ctx* ctx, gsb_session* s, gsb_frame** out) {
   gsb_frame* f = session_frame(ctx, s);
   f->lean = true;  // never exported (not reachable through gsb_frame_download)
   if (int r = frame_setup(ctx, f, s->cloud, &s->cam, s->cfg.background, &s->cfg.raster, false)) return r;
-  const int64_t want = f->k_cap > 0 ? f->k_cap : std::max<int64_t>(3 * s->cloud->n, 1 << 16);
+  const int64_t want = f->k_cap > 0 ? f->k_cap : initial_k_cap(s->cloud->n);
   if (int r = frame_reserve(f, s->cloud, want)) return r;
   *out = f;
   return GSB_OK;
@@ -1629,6 +1639,7 @@ static int session_sync(gsb_ctx* ctx, gsb_session* s) {
       s->pending = 0;
       return GSB_OK;
     }
+    s->discarded += aborted;
     if (debug_on())
       std::fprintf(stderr, "[gsb] %d iteration(s) discarded: K %u (cap %lld), tile overflow %u\n", aborted, abort_k,
                    (long long)f->k_cap, abort_tile);
@@ -1762,7 +1773,7 @@ int gsb_session_stage_times(gsb_session* s, double* ms_out) {
   if (!s || !ms_out) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
   if (int r = ensure_device(s->ctx)) return r;
   for (int k = 0; k < kNumStages; ++k) ms_out[k] = 0.0;
-  if (!s->have_events || !s->graph_profiled) return GSB_OK;
+  if (!s->have_events || !(s->graph_profiled || s->batch_events)) return GSB_OK;
   GSB_CUDA(cudaStreamSynchronize(s->ctx->stream));
   for (int k = 0; k < kNumStages; ++k) {
     float t = 0.f;
@@ -1841,8 +1852,18 @@ static int batch_capture(gsb_ctx* ctx, gsb_pose_batch* b) {
   const double t_dbg = debug_on() ? now_ms() : 0.0;
   const int64_t launches0 = ctx->launches;
   cudaStream_t main = ctx->stream;
-  const bool profiling = ctx->profiling;  // per-stage events are per session graph, not per batch
+  // With profiling on, each branch brackets its stages with its session's
+  // events, so stage times are those of the concurrent batch (the eager event
+  // pool stays off while capturing).
+  const bool profiling = ctx->profiling;
   ctx->profiling = false;
+  if (profiling)
+    for (gsb_session* s : b->sessions)
+      if (!s->have_events) {
+        for (int k = 0; k < kNumStages; ++k)
+          for (int j = 0; j < 2; ++j) GSB_CUDA(cudaEventCreate(&s->ev[k][j]));
+        s->have_events = true;
+      }
   GSB_CUDA(cudaStreamBeginCapture(main, cudaStreamCaptureModeThreadLocal));
   int r = GSB_OK;
   cudaError_t e = cudaSuccess;
@@ -1866,8 +1887,13 @@ static int batch_capture(gsb_ctx* ctx, gsb_pose_batch* b) {
         if (e != cudaSuccess) break;
       }
     if (e == cudaSuccess && !fr.empty()) {
-      r = launch_preprocess_multi(main, c0, make_rasterdev(&b->sessions[0]->cfg.raster), cams.data(), fr.data(),
-                                  (int)fr.size());
+      // profiling: the shared multi-view preprocess is charged to session 0's preprocess stage
+      if (profiling) e = cudaEventRecordWithFlags(b->sessions[0]->ev[kStPreprocess][0], main, cudaEventRecordExternal);
+      if (e == cudaSuccess)
+        r = launch_preprocess_multi(main, c0, make_rasterdev(&b->sessions[0]->cfg.raster), cams.data(), fr.data(),
+                                    (int)fr.size());
+      if (profiling && !r && e == cudaSuccess)
+        e = cudaEventRecordWithFlags(b->sessions[0]->ev[kStPreprocess][1], main, cudaEventRecordExternal);
       ctx->launches += (int64_t)((fr.size() + 15) / 16);
     }
   }
@@ -1876,7 +1902,9 @@ static int batch_capture(gsb_ctx* ctx, gsb_pose_batch* b) {
     e = cudaStreamWaitEvent(b->streams[i], b->fork, 0);
     if (e != cudaSuccess) break;
     ctx->stream = b->streams[i];
+    ctx->stage_events = profiling ? b->sessions[i]->ev : nullptr;
     r = session_launch_iteration(ctx, b->sessions[i], frames[i], shared[i] != 0);
+    ctx->stage_events = nullptr;
     ctx->stream = main;
     if (!r) e = cudaEventRecord(b->joins[i], b->streams[i]);
     if (!r && e == cudaSuccess) e = cudaStreamWaitEvent(main, b->joins[i], 0);
@@ -1900,7 +1928,9 @@ static int batch_capture(gsb_ctx* ctx, gsb_pose_batch* b) {
     b->graph_gen[i] = frames[i]->gen;
     b->graph_kcap[i] = frames[i]->k_cap;
     b->graph_binning[i] = frames[i]->binning;
+    b->sessions[i]->batch_events = profiling;
   }
+  b->graph_profiled = profiling;
   if (debug_on())
     std::fprintf(stderr, "[gsb] pose batch graph captured: %zu sessions, %lld kernels, %.2f ms\n", n,
                  (long long)b->graph_launches, now_ms() - t_dbg);
@@ -1908,7 +1938,7 @@ static int batch_capture(gsb_ctx* ctx, gsb_pose_batch* b) {
 }
 
 static int batch_prepare(gsb_ctx* ctx, gsb_pose_batch* b) {
-  bool stale = b->exec == nullptr;
+  bool stale = b->exec == nullptr || b->graph_profiled != ctx->profiling;
   for (size_t i = 0; i < b->sessions.size() && !stale; ++i) {
     const gsb_frame* f = b->sessions[i]->own;
     stale = f->gen != b->graph_gen[i] || f->k_cap != b->graph_kcap[i] || f->binning != b->graph_binning[i];
@@ -2023,6 +2053,14 @@ int gsb_pose_batch_sync(gsb_ctx* ctx, gsb_pose_batch* b) {
     s->n_entries = s->host_counters[1];
     s->pending = 0;
   }
+  return GSB_OK;
+}
+
+int gsb_pose_batch_discarded(const gsb_pose_batch* b, int64_t* out) {
+  if (!b || !out) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  int64_t t = 0;
+  for (const gsb_session* s : b->sessions) t += s->discarded;
+  *out = t;
   return GSB_OK;
 }
 
@@ -2544,7 +2582,7 @@ static int joint_frames_ready(gsb_ctx* ctx, gsb_joint* j) {
   for (gsb_frame* f : j->frames) {
     f->lean = true;
     if (int r = frame_setup(ctx, f, j->cloud, &j->cam, j->cfg.background, &j->cfg.raster, false)) return r;
-    const int64_t want = f->k_cap > 0 ? f->k_cap : std::max<int64_t>(3 * j->cloud->n, 1 << 16);
+    const int64_t want = f->k_cap > 0 ? f->k_cap : initial_k_cap(j->cloud->n);
     if (int r = frame_reserve(f, j->cloud, want)) return r;
   }
   return GSB_OK;

@@ -181,6 +181,8 @@ def _sigs():
         "gsb_ctx_set_binning": (C.c_int, [_vp, i32]),
         "gsb_ctx_stage_times": (C.c_int, [_vp, _vp, _vp, i32]),
         "gsb_ctx_launch_count": (i64, [_vp]),
+        "gsb_measure_fp32_peaks": (C.c_int, [i32, P(d), P(d)]),
+        "gsb_build_id": (C.c_char_p, []),
         "gsb_cloud_create": (C.c_int, [_vp, i64, i32, P(_vp)]),
         "gsb_cloud_destroy": (C.c_int, [_vp]),
         "gsb_cloud_upload": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, i32]),
@@ -225,6 +227,7 @@ def _sigs():
         "gsb_pose_batch_step": (C.c_int, [_vp, _vp, i32]),
         "gsb_pose_batch_step_async": (C.c_int, [_vp, _vp, i32]),
         "gsb_pose_batch_sync": (C.c_int, [_vp, _vp]),
+        "gsb_pose_batch_discarded": (C.c_int, [_vp, P(i64)]),
         "gsb_estimate_poses": (C.c_int, [_vp, _vp, _vp, _vp, _vp, i32, P(PoseConfig), _vp, _vp, _vp]),
         "gsb_comm_unique_id": (C.c_int, [_vp]),
         "gsb_comm_create": (C.c_int, [_vp, _vp, i32, i32, P(_vp)]),
@@ -620,6 +623,17 @@ class PoseSession:
         return fi
 
 
+def measure_fp32_peaks(device: int = 0) -> dict:
+    """FFMA TFLOP/s and MUFU ex2 Tops/s of the device by microbenchmark (gsb_measure_fp32_peaks)."""
+    f, m = C.c_double(), C.c_double()
+    _check(lib().gsb_measure_fp32_peaks(device, C.byref(f), C.byref(m)))
+    return {"ffma_tflops": f.value, "mufu_tops": m.value}
+
+
+def build_id() -> str:
+    return lib().gsb_build_id().decode()
+
+
 class PoseBatch:
     """Several sessions advanced by one CUDA-graph replay per iteration (gsb_pose_batch)."""
 
@@ -649,6 +663,12 @@ class PoseBatch:
 
     def sync(self):
         _check(lib().gsb_pose_batch_sync(self.ctx.h, self.h))
+
+    def discarded(self) -> int:
+        """Iterations discarded for entry-capacity growth (and re-run by sync) so far."""
+        v = C.c_int64()
+        _check(lib().gsb_pose_batch_discarded(self.h, C.byref(v)))
+        return int(v.value)
 
 
 def estimate_poses(ctx: Context, cloud: Cloud, targets, intr, init_poses, config: PoseConfig | None = None):
