@@ -246,7 +246,13 @@ def run_ours(args, ws, rank, local):
     out = None
     if rank == 0:
         # roofline for the dominant stage
-        per_iter_stage_ms = {k: v[0] / (VIEWS_PER_GPU * args.steps) for k, v in stages.items() if v[1] > 0}
+        # Kernel durations for the roofline come from the solo pass (each
+        # session's own graph, one at a time, event nodes around every stage):
+        # event nodes inside the concurrent batch's branches also time the
+        # queueing behind other branches' kernels, so they bound nothing; they
+        # are reported as "live" for reference only.
+        per_iter_stage_ms = {k: v / (VIEWS_PER_GPU * args.steps) for k, v in solo_stages.items()}
+        live_stage_ms = {k: v[0] / (VIEWS_PER_GPU * args.steps) for k, v in stages.items() if v[1] > 0}
         dom = max(per_iter_stage_ms, key=per_iter_stage_ms.get)
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
             os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
@@ -278,13 +284,14 @@ def run_ours(args, ws, rank, local):
             "scene": {"n_splats": int(fi.n_splats), "n_entries": int(fi.n_entries)},
             "wall_s": round(wall_s, 3),
             "attribution": {
-                "how": "stage times = CUDA event nodes inside every branch of the same pose-batch graph "
-                       f"(concurrent, {args.steps} more replays; the shared multi-view preprocess charged once "
-                       "per replay); solo = each session's own graph, one at a time",
+                "how": "stages_ms_per_iter / roofline: CUDA event nodes around every stage of each session's own "
+                       f"graph, sessions one at a time ({args.steps} iterations each, same process, same "
+                       "buffers); live: event nodes inside every branch of the timed pose-batch graph "
+                       "(the shared multi-view preprocess charged once per replay)",
                 "live_ms_per_step": round(live_ms / args.steps, 4),
                 "solo_ms_per_step": round(solo_ms / args.steps, 4),
-                "solo_stages_ms_per_iter": {k: round(v / (VIEWS_PER_GPU * args.steps), 4)
-                                            for k, v in solo_stages.items()}},
+                "live_stages_ms_per_iter (branch wall time incl. queueing)": {
+                    k: round(v, 4) for k, v in live_stage_ms.items()}},
             "discarded_in_timed_region": int(discarded),
             "build_id": gsb.build_id()[:16],
             "pose_check": {"view": int(views[0]), "final_loss": res["final_loss"], "steps": res["steps"]},

@@ -15,7 +15,12 @@
 // outputs from 14 inputs held in registers):
 //   loss_maps:  5 forward convolutions -> SSIM map sum, L1 sum, g maps;
 //   loss_grad:  3 back-convolutions + L1 sign term -> d_image.
-// Per-block partial sums are reduced in a fixed order (deterministic).
+// The separable convolutions run in FP32 (the images are FP32; the window is
+// the reference's FP64 window rounded once), the pointwise SSIM terms, the
+// L1 terms and every sum in FP64. Per-block partial sums are reduced in a
+// fixed order (deterministic). FP32 convolutions keep the identical-image
+// identities exact: equal inputs give bitwise-equal statistics, and
+// conv(-x) = -conv(x), conv(2x) = 2 conv(x) hold exactly in any precision.
 #include "gsb_internal.cuh"
 
 namespace gsb {
@@ -28,7 +33,7 @@ constexpr int kWin = 11;
 constexpr int kTW = 32, kTH = 32, kR = 4;
 constexpr int kSW = kTW + 2 * kHalf, kSH = kTH + 2 * kHalf;  // 42 x 42
 constexpr int kThr = 256;
-__constant__ double c_win[kWin];
+__constant__ float c_win[kWin];
 
 // Transmittance mask of masked_rgb_loss (losses.cpp:259-289): pixel p takes
 // part iff accum = 1 - final_T > thr; norms (device) = {L1 norm, SSIM scale,
@@ -98,10 +103,10 @@ __device__ __forceinline__ void stage_planes(float (*dst)[kSH][kSW + 1], const f
 #define GSB_LOSS_HR 4
 #endif
 constexpr int kHR = GSB_LOSS_HR;
-__device__ __forceinline__ void hpass5(const float (*st)[kSH][kSW + 1], double (*hq)[kSH][kTW + 1]) {
+__device__ __forceinline__ void hpass5(const float (*st)[kSH][kSW + 1], float (*hq)[kSH][kTW + 1]) {
   for (int task = threadIdx.x; task < kSH * (kTW / kHR); task += kThr) {
     const int r = task / (kTW / kHR), q0 = (task - r * (kTW / kHR)) * kHR;
-    double x[kHR + kWin - 1], y[kHR + kWin - 1];
+    float x[kHR + kWin - 1], y[kHR + kWin - 1];
 #pragma unroll
     for (int k = 0; k < kHR + kWin - 1; ++k) {
       x[k] = st[0][r][q0 + k];
@@ -109,15 +114,15 @@ __device__ __forceinline__ void hpass5(const float (*st)[kSH][kSW + 1], double (
     }
 #pragma unroll
     for (int m = 0; m < 5; ++m) {
-      double acc[kHR];
+      float acc[kHR];
 #pragma unroll
-      for (int j = 0; j < kHR; ++j) acc[j] = 0.0;
+      for (int j = 0; j < kHR; ++j) acc[j] = 0.f;
 #pragma unroll
       for (int k = 0; k < kHR + kWin - 1; ++k) {
-        const double f = m == 0 ? x[k] : m == 1 ? y[k] : m == 2 ? x[k] * x[k] : m == 3 ? y[k] * y[k] : x[k] * y[k];
+        const float f = m == 0 ? x[k] : m == 1 ? y[k] : m == 2 ? x[k] * x[k] : m == 3 ? y[k] * y[k] : x[k] * y[k];
 #pragma unroll
         for (int j = 0; j < kHR; ++j)
-          if (k - j >= 0 && k - j < kWin) acc[j] = fma(c_win[k - j], f, acc[j]);
+          if (k - j >= 0 && k - j < kWin) acc[j] = fmaf(c_win[k - j], f, acc[j]);
       }
 #pragma unroll
       for (int j = 0; j < kHR; ++j) hq[m][r][q0 + j] = acc[j];
@@ -136,8 +141,8 @@ __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, 
   if (mk.final_t) scale = mk.norms[1];
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float(*st)[kSH][kSW + 1] = reinterpret_cast<float(*)[kSH][kSW + 1]>(smem_raw);
-  double(*hq)[kSH][kTW + 1] =
-      reinterpret_cast<double(*)[kSH][kTW + 1]>(smem_raw + sizeof(float) * 2 * kSH * (kSW + 1) + 8);
+  float(*hq)[kSH][kTW + 1] =
+      reinterpret_cast<float(*)[kSH][kTW + 1]>(smem_raw + sizeof(float) * 2 * kSH * (kSW + 1));
   __shared__ double s_tmp[kThr / 32];
   const int64_t P = (int64_t)W * H;
   const int bx = blockIdx.x * kTW, by = blockIdx.y * kTH;
@@ -151,18 +156,18 @@ __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, 
     __syncthreads();
     hpass5(st, hq);
     __syncthreads();
-    double mv[5][kR];
+    float mv[5][kR];
 #pragma unroll
     for (int m = 0; m < 5; ++m) {
-      double acc[kR];
+      float acc[kR];
 #pragma unroll
-      for (int j = 0; j < kR; ++j) acc[j] = 0.0;
+      for (int j = 0; j < kR; ++j) acc[j] = 0.f;
 #pragma unroll
       for (int k = 0; k < kR + kWin - 1; ++k) {
-        const double f = hq[m][rg * kR + k][c];
+        const float f = hq[m][rg * kR + k][c];
 #pragma unroll
         for (int j = 0; j < kR; ++j)
-          if (k - j >= 0 && k - j < kWin) acc[j] = fma(c_win[k - j], f, acc[j]);
+          if (k - j >= 0 && k - j < kWin) acc[j] = fmaf(c_win[k - j], f, acc[j]);
       }
 #pragma unroll
       for (int j = 0; j < kR; ++j) mv[m][j] = acc[j];
@@ -210,20 +215,20 @@ __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, 
 }
 
 // Horizontal pass of the three gradient maps (back-convolution, losses.cpp:144-151).
-__device__ __forceinline__ void hpass3(const float (*st)[kSH][kSW + 1], double (*hq)[kSH][kTW + 1]) {
+__device__ __forceinline__ void hpass3(const float (*st)[kSH][kSW + 1], float (*hq)[kSH][kTW + 1]) {
   for (int task = threadIdx.x; task < kSH * (kTW / kHR); task += kThr) {
     const int r = task / (kTW / kHR), q0 = (task - r * (kTW / kHR)) * kHR;
 #pragma unroll
     for (int m = 0; m < 3; ++m) {
-      double acc[kHR];
+      float acc[kHR];
 #pragma unroll
-      for (int j = 0; j < kHR; ++j) acc[j] = 0.0;
+      for (int j = 0; j < kHR; ++j) acc[j] = 0.f;
 #pragma unroll
       for (int k = 0; k < kHR + kWin - 1; ++k) {
-        const double f = st[m][r][q0 + k];
+        const float f = st[m][r][q0 + k];
 #pragma unroll
         for (int j = 0; j < kHR; ++j)
-          if (k - j >= 0 && k - j < kWin) acc[j] = fma(c_win[k - j], f, acc[j]);
+          if (k - j >= 0 && k - j < kWin) acc[j] = fmaf(c_win[k - j], f, acc[j]);
       }
 #pragma unroll
       for (int j = 0; j < kHR; ++j) hq[m][r][q0 + j] = acc[j];
@@ -248,14 +253,14 @@ __global__ void GSB_LOSS_GRAD_BOUNDS loss_grad_kernel(const float* __restrict__ 
   }
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float(*st)[kSH][kSW + 1] = reinterpret_cast<float(*)[kSH][kSW + 1]>(smem_raw);
-  double(*hq)[kSH][kTW + 1] =
-      reinterpret_cast<double(*)[kSH][kTW + 1]>(smem_raw + sizeof(float) * 3 * kSH * (kSW + 1) + 8);
+  float(*hq)[kSH][kTW + 1] =
+      reinterpret_cast<float(*)[kSH][kTW + 1]>(smem_raw + sizeof(float) * 3 * kSH * (kSW + 1));
   const int64_t P = (int64_t)W * H;
   const int bx = blockIdx.x * kTW, by = blockIdx.y * kTH;
   const int c = threadIdx.x & (kTW - 1), rg = threadIdx.x / kTW;
   const int x = bx + c;
   for (int ch = 0; ch < 3; ++ch) {
-    double cv[3][kR];
+    float cv[3][kR];
     if (has_ssim) {
       const float* src[3] = {gmaps + (3 * ch + 0) * P, gmaps + (3 * ch + 1) * P, gmaps + (3 * ch + 2) * P};
       stage_planes<3>(st, src, W, H, bx - kHalf, by - kHalf);
@@ -264,15 +269,15 @@ __global__ void GSB_LOSS_GRAD_BOUNDS loss_grad_kernel(const float* __restrict__ 
       __syncthreads();
 #pragma unroll
       for (int m = 0; m < 3; ++m) {
-        double acc[kR];
+        float acc[kR];
 #pragma unroll
-        for (int j = 0; j < kR; ++j) acc[j] = 0.0;
+        for (int j = 0; j < kR; ++j) acc[j] = 0.f;
 #pragma unroll
         for (int k = 0; k < kR + kWin - 1; ++k) {
-          const double f = hq[m][rg * kR + k][c];
+          const float f = hq[m][rg * kR + k][c];
 #pragma unroll
           for (int j = 0; j < kR; ++j)
-            if (k - j >= 0 && k - j < kWin) acc[j] = fma(c_win[k - j], f, acc[j]);
+            if (k - j >= 0 && k - j < kWin) acc[j] = fmaf(c_win[k - j], f, acc[j]);
         }
 #pragma unroll
         for (int j = 0; j < kR; ++j) cv[m][j] = acc[j];
@@ -286,7 +291,8 @@ __global__ void GSB_LOSS_GRAD_BOUNDS loss_grad_kernel(const float* __restrict__ 
       const double a = ren[ch * P + p], b = tgt[ch * P + p];
       const double diff = a - b;
       const double dl1 = (diff == 0.0 || !mask_at(mk, p)) ? 0.0 : (diff > 0.0 ? l1_norm : -l1_norm);
-      const double dss = has_ssim ? a_(a_(cv[0][j], m_(m_(2.0, a), cv[1][j])), m_(b, cv[2][j])) : 0.0;
+      const double dss =
+          has_ssim ? a_(a_((double)cv[0][j], m_(m_(2.0, a), (double)cv[1][j])), m_(b, (double)cv[2][j])) : 0.0;
       d_image[ch * P + p] = (float)s_(m_(1.0 - beta, dl1), m_(beta, dss));
     }
     if (has_ssim) __syncthreads();
@@ -376,13 +382,14 @@ int init_loss_constants() {
     w[i] = exp(-d * d / (2.0 * 1.5 * 1.5));
     sum += w[i];
   }
-  for (int i = 0; i < kWin; ++i) w[i] /= sum;
-  GSB_CUDA(cudaMemcpyToSymbol(c_win, w, sizeof w));
+  float wf[kWin];
+  for (int i = 0; i < kWin; ++i) wf[i] = (float)(w[i] / sum);
+  GSB_CUDA(cudaMemcpyToSymbol(c_win, wf, sizeof wf));
   return GSB_OK;
 }
 
-constexpr size_t kMapsSmem = sizeof(float) * 2 * kSH * (kSW + 1) + 8 + sizeof(double) * 5 * kSH * (kTW + 1);
-constexpr size_t kGradSmem = sizeof(float) * 3 * kSH * (kSW + 1) + 8 + sizeof(double) * 3 * kSH * (kTW + 1);
+constexpr size_t kMapsSmem = sizeof(float) * 2 * kSH * (kSW + 1) + sizeof(float) * 5 * kSH * (kTW + 1);
+constexpr size_t kGradSmem = sizeof(float) * 3 * kSH * (kSW + 1) + sizeof(float) * 3 * kSH * (kTW + 1);
 
 int init_loss_attributes() {
   GSB_CUDA(cudaFuncSetAttribute(loss_maps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMapsSmem));
