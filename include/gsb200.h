@@ -8,6 +8,8 @@
  *   gsb_render            <- gsopt::render            include/gsopt/rasterizer.hpp:98-99
  *   gsb_frame_download    <- RenderOutput fields       include/gsopt/rasterizer.hpp:66-82
  *   gsb_render_backward   <- gsopt::render_backward   include/gsopt/rasterizer.hpp:112-113
+ *   gsb_render_expected_depth <- gsopt::render_expected_depth rasterizer.hpp:101-107
+ *                            (src/rasterizer.cpp:283-323; dataset generation, synth.cpp:117-127)
  *   gsb_rgb_loss          <- gsopt::rgb_loss          include/gsopt/losses.hpp:37
  *   gsb_pose_step         <- gsopt::pose_step         include/gsopt/trainer.hpp:99-100
  *   gsb_adam_step         <- gsopt::adam_step (both)  include/gsopt/trainer.hpp:85-87
@@ -195,6 +197,11 @@ int gsb_frame_destroy(gsb_frame* frame);
 int gsb_render(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, const double background[3],
                const gsb_raster_config* cfg, gsb_frame* frame, double* image_out);
 int gsb_frame_get_info(gsb_frame* frame, gsb_frame_info* info);
+/* render_expected_depth (rasterizer.cpp:283-323): per-pixel alpha-weighted
+ * mean view-space depth (0 where the weight sum is <= 1e-8) and the weight
+ * sum, host H*W FP32 each. Same cutoff / alpha decisions as gsb_render. */
+int gsb_render_expected_depth(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam,
+                              const gsb_raster_config* cfg, float* depth_out, float* weight_out);
 /* Copies every RenderOutput field to host (any pointer may be NULL). Per-splat
  * arrays are in depth order (n_splats), tile_lists holds indices into them
  * (n_entries), tile_ranges is tiles*2 (begin,end). conic is 2x2 row-major. */
@@ -361,9 +368,17 @@ int gsb_joint_schedule(uint64_t seed, int32_t n_views, int64_t count, int32_t* s
  * The cloud is optimised in place; targets stay owned by the caller.
  * comm may be NULL (single rank). */
 typedef struct gsb_joint gsb_joint;
+/* rng_state: the caller's Rng (core.hpp:58-102, xorshift64*) state — the
+ * reference's joint_optimize(..., Rng& rng, ...) draws its epoch shuffles and
+ * densify normals from it (pipelines.cpp:123-129, trainer.cpp:186-205); 0
+ * means Rng(0)'s state as in the Rng constructor. The run advances its own
+ * copy; gsb_joint_rng_state returns it so the caller's Rng can continue. */
 int gsb_joint_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* const* targets, int32_t n_views,
                      const double intr[4], const double* init_poses, const gsb_joint_config* cfg,
-                     uint64_t seed, int32_t local_views, gsb_comm* comm, gsb_joint** out);
+                     uint64_t rng_state, int32_t local_views, gsb_comm* comm, gsb_joint** out);
+/* The joint run's Rng state after the steps run so far (write it back into the
+ * caller's Rng). */
+int gsb_joint_rng_state(const gsb_joint* j, uint64_t* rng_state);
 int gsb_joint_destroy(gsb_joint* j);
 /* runs `steps` steps (blocking); GSB_ERR_DIVERGED at a non-finite total loss */
 int gsb_joint_step(gsb_ctx* ctx, gsb_joint* j, int32_t steps);

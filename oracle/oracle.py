@@ -224,6 +224,8 @@ def ref_lib():
         L.ref_estimate_pose.argtypes = port.orc_estimate_pose.argtypes[:16]
         L.ref_synth_scene.restype = None
         L.ref_synth_scene.argtypes = [i32, i32, i32, i32, i32, i32, C.c_uint64, P(Cloud), vp, vp]
+        L.ref_render_expected_depth.restype = None
+        L.ref_render_expected_depth.argtypes = [P(Cloud), P(Camera), P(RasterConfig), vp, vp]
         L.ref_last_error.restype = C.c_char_p
         L.ref_thread_count.restype = C.c_int
         _ref_lib = L
@@ -275,6 +277,15 @@ def ref_estimate_pose(cloud: "HostCloud", image, fx, fy, cx, cy, init12, budget=
                                         _p(t0), C.byref(pc), budget, _p(Ro), _p(to),
                                         C.cast(C.byref(fl), C.c_void_p), C.cast(C.byref(conv), C.c_void_p))
     return dict(pose=pose_join(Ro, to), steps=steps, final_loss=fl.value, converged=bool(conv.value))
+
+
+def ref_render_expected_depth(cloud: "HostCloud", cam: Camera, cfg=None):
+    """The reference's own render_expected_depth (rasterizer.cpp:283-323): (depth, weight) float32 (H, W)."""
+    depth = np.zeros((cam.height, cam.width), np.float32)
+    weight = np.zeros((cam.height, cam.width), np.float32)
+    ref_lib().ref_render_expected_depth(cloud.c().ref(), C.byref(cam), C.byref(cfg or default_raster_config()),
+                                        _p(depth), _p(weight))
+    return depth, weight
 
 
 def ref_synth_scene(gaussians, cameras, width, height, kind, sh_degree, seed, with_images=False):

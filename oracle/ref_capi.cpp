@@ -235,6 +235,15 @@ orc_render_out* ref_render(const orc_cloud* cloud, const orc_camera* cam, const 
   return &h->out;
 }
 
+// rasterizer.cpp:283-323 (render_expected_depth): depth / weight, H*W floats each.
+void ref_render_expected_depth(const orc_cloud* cloud, const orc_camera* cam, const orc_raster_config* cfg,
+                               float* depth_out, float* weight_out) {
+  std::vector<float> d, w;
+  render_expected_depth(to_cloud(cloud), to_camera(cam), to_config(cfg), &d, &w);
+  std::memcpy(depth_out, d.data(), d.size() * sizeof(float));
+  std::memcpy(weight_out, w.data(), w.size() * sizeof(float));
+}
+
 void ref_render_free(orc_render_out* out) {
   if (out == nullptr) return;
   auto* h = reinterpret_cast<RefRender*>(out);

@@ -52,6 +52,7 @@ int launch_tile_bin(cudaStream_t st, gsb_frame* f, int64_t n, int64_t* launches)
 size_t bin_hist_words(int64_t n, int n_tiles);
 int init_bin_attributes();
 int launch_composite(cudaStream_t st, gsb_frame* f, const RasterDev& rc);
+int launch_expected_depth(cudaStream_t st, gsb_frame* f, const RasterDev& rc, float* depth_out, float* weight_out);
 int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc, bool pose_only);
 int launch_backward_geom(cudaStream_t st, const gsb_cloud* cloud, gsb_frame* f, const RasterDev& rc, bool full,
                          float* grads, int64_t* launches);
@@ -93,8 +94,10 @@ size_t joint_xchg_doubles();
 void joint_state_read(const void* host, int64_t* t, int32_t* diverged, int32_t* aborted, double* k_max,
                       int32_t* tile);
 void joint_state_clear_abort(void* host);
-int launch_grad_accum(cudaStream_t st, const float* grads, int nplanes, int64_t n_pad, int64_t n,
-                      const uint32_t* cnt_g, double scale, double* gsum, int32_t* gcnt);
+int launch_grad_norm(cudaStream_t st, const float* grads, int nplanes, int64_t n_pad, int64_t n,
+                     const uint32_t* cnt_g, double scale, double* stage);
+int launch_grad_accum_commit(cudaStream_t st, const double* stage, int local, int64_t stride, int64_t n,
+                             const void* js, const JointCtl& ctl, const double* xchg, double* gsum, int32_t* gcnt);
 int densify_bbox_blocks();
 int launch_densify_bbox(cudaStream_t st, const float* params, int64_t n, int64_t n_pad, float* out);
 int launch_densify_action(cudaStream_t st, const float* params, int64_t n, int64_t n_pad, const double* gsum,
@@ -249,11 +252,16 @@ static uint64_t fnv1a(uint64_t h, const void* data, size_t n) {  // rasterizer.c
   return h;
 }
 
-// rasterizer.cpp:52-73 semantics: sizes, degrees and the full camera, then
-// the cloud's content identity. The cloud lives on the device and every
-// mutation goes through this API, so its (identity, version) pair stands in
-// for the reference's 64 strided host samples.
-static uint64_t fingerprint(const gsb_cloud* cloud, const gsb_camera* cam) {
+// rasterizer.cpp:52-73: FNV-1a over the sizes, degrees and the full camera,
+// then 64 strided samples of every parameter array. `exact` (exported forward
+// states, gsb_render): when the cloud holds exactly what was last uploaded
+// from the host, the samples are that upload's FP64 values and the result is
+// the reference's fingerprint bit for bit. A cloud changed on the device
+// (Adam, densify, synth, PLY) has no FP64 host copy: its (identity, version)
+// pair stands in for the samples — every mutation goes through this API and
+// bumps the version, so a stale forward state is still rejected. Internal
+// forward states (sessions, joint; never exported) always use the cheap form.
+static uint64_t fingerprint(const gsb_cloud* cloud, const gsb_camera* cam, bool exact) {
   uint64_t h = 0xcbf29ce484222325ull;
   const int64_t n = cloud->n;
   h = fnv1a(h, &n, sizeof n);
@@ -265,6 +273,7 @@ static uint64_t fingerprint(const gsb_cloud* cloud, const gsb_camera* cam) {
   h = fnv1a(h, wh, sizeof wh);
   h = fnv1a(h, cam->R, sizeof(double) * 9);
   h = fnv1a(h, cam->t, sizeof(double) * 3);
+  if (exact && cloud->fp_version == cloud->version) return fnv1a(h, cloud->fp_samples.data(), cloud->fp_samples.size());
   const uintptr_t id = reinterpret_cast<uintptr_t>(cloud);
   h = fnv1a(h, &id, sizeof id);
   h = fnv1a(h, &cloud->host_fingerprint, sizeof(uint64_t));
@@ -564,7 +573,7 @@ static int frame_setup(gsb_ctx* ctx, gsb_frame* f, const gsb_cloud* cloud, const
   for (int c = 0; c < 3; ++c) f->background[c] = bg ? bg[c] : 0.0;
   f->n_gaussians = cloud->n;
   f->cloud = cloud;
-  f->fingerprint = fingerprint(cloud, cam);
+  f->fingerprint = fingerprint(cloud, cam, !f->lean);
   f->cloud_version = cloud->version;
   f->valid = false;
   f->has_dimage = false;
@@ -883,15 +892,22 @@ int gsb_cloud_upload(gsb_cloud* c, const double* means, const double* rotations,
   // content hash of the uploaded FP64 arrays at 64 strided samples (rasterizer.cpp:62-71)
   uint64_t hsh = 0xcbf29ce484222325ull;
   const int64_t stride = std::max<int64_t>(1, n / 64);
+  c->fp_samples.clear();
+  auto put = [&](const double* p, size_t k) {
+    const unsigned char* b = reinterpret_cast<const unsigned char*>(p);
+    c->fp_samples.insert(c->fp_samples.end(), b, b + sizeof(double) * k);
+    hsh = fnv1a(hsh, p, sizeof(double) * k);
+  };
   for (int64_t i = 0; i < n; i += stride) {
-    hsh = fnv1a(hsh, means + 3 * i, sizeof(double) * 3);
-    hsh = fnv1a(hsh, rotations + 4 * i, sizeof(double) * 4);
-    hsh = fnv1a(hsh, log_scales + 3 * i, sizeof(double) * 3);
-    hsh = fnv1a(hsh, opacity_logits + i, sizeof(double));
-    hsh = fnv1a(hsh, sh + (size_t)i * 3 * B, sizeof(double) * 3 * B);
+    put(means + 3 * i, 3);
+    put(rotations + 4 * i, 4);
+    put(log_scales + 3 * i, 3);
+    put(opacity_logits + i, 1);
+    put(sh + (size_t)i * 3 * B, (size_t)3 * B);
   }
   c->host_fingerprint = hsh;
   c->version += 1;
+  c->fp_version = c->version;
   return GSB_OK;
 }
 
@@ -971,6 +987,37 @@ int gsb_render(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, const doub
   f->valid = true;
   if (image_out) return download_image(ctx, f->image.as<float>(), f->width, f->height, image_out);
   return GSB_OK;
+}
+
+int gsb_render_expected_depth(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, const gsb_raster_config* cfg,
+                              float* depth_out, float* weight_out) {
+  if (int r = ensure_device(ctx)) return r;
+  if (!cloud || !cam || !depth_out || !weight_out) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  gsb_raster_config dflt;
+  gsb_default_raster_config(&dflt);
+  if (!cfg) cfg = &dflt;
+  if (int r = validate_config(cfg)) return r;
+  gsb_frame* f = nullptr;
+  if (int r = gsb_frame_create(ctx, &f)) return r;
+  f->lean = true;
+  const RasterDev rc = make_rasterdev(cfg);
+  const int64_t P = (int64_t)cam->width * cam->height;
+  DevBuf out;
+  int r = frame_setup(ctx, f, cloud, cam, nullptr, cfg, true);
+  if (!r) r = render_sync(ctx, cloud, f, rc);
+  if (!r && out.reserve(sizeof(float) * 2 * std::max<int64_t>(P, 1)) != cudaSuccess)
+    r = fail(GSB_ERR_OUT_OF_MEMORY, "expected depth buffers");
+  if (!r) r = launch_expected_depth(ctx->stream, f, rc, out.as<float>(), out.as<float>() + P);
+  if (!r && P > 0) {
+    cudaError_t e = cudaMemcpyAsync(depth_out, out.p, sizeof(float) * P, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(weight_out, out.as<float>() + P, sizeof(float) * P, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) r = cuda_fail(e, "expected depth download");
+  }
+  out.release();
+  gsb_frame_destroy(f);
+  return r;
 }
 
 int gsb_frame_get_info(gsb_frame* f, gsb_frame_info* info) {
@@ -1296,7 +1343,8 @@ static int backward_common(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam
 }
 
 static int check_state(gsb_cloud* cloud, const gsb_camera* cam, gsb_frame* f) {
-  if (!f->valid || f->fingerprint != fingerprint(cloud, cam) || f->n_gaussians != cloud->n || f->cloud != cloud)
+  if (!f->valid || f->fingerprint != fingerprint(cloud, cam, !f->lean) || f->n_gaussians != cloud->n ||
+      f->cloud != cloud)
     return fail(GSB_ERR_STATE_MISMATCH, "render_backward: output does not match (cloud, camera)");
   return GSB_OK;
 }
@@ -2467,7 +2515,7 @@ struct gsb_joint {
   std::vector<int32_t> order;
   int64_t seq_next = 0;
   // GradAccum (trainer.cpp:134-142) on the device + densification bookkeeping
-  DevBuf acc_sum, acc_cnt;
+  DevBuf acc_sum, acc_cnt, acc_stage;  // acc_stage: per local slot, [local][n_pad] staged increments
   const void* graph_params = nullptr;
   int64_t graph_n = -1;
   int32_t densify_report[3] = {0, 0, 0};
@@ -2516,6 +2564,7 @@ static int joint_size_buffers(gsb_ctx* ctx, gsb_joint* j) {
   if (joint_accumulates(j)) {
     GSB_CUDA(j->acc_sum.reserve(sizeof(double) * n));
     GSB_CUDA(j->acc_cnt.reserve(sizeof(int32_t) * n));
+    GSB_CUDA(j->acc_stage.reserve(sizeof(double) * j->cloud->n_pad * j->local));
     GSB_CUDA(cudaMemsetAsync(j->acc_sum.p, 0, sizeof(double) * n, ctx->stream));
     GSB_CUDA(cudaMemsetAsync(j->acc_cnt.p, 0, sizeof(int32_t) * n, ctx->stream));
   }
@@ -2538,10 +2587,10 @@ static int joint_launch_step(gsb_ctx* ctx, gsb_joint* j) {
     if (int r = render_async(ctx, j->cloud, f, rc)) return r;
     if (int r = loss_device(ctx, f, tb, j->cfg.beta, true)) return r;
     if (int r = backward_device(ctx, j->cloud, f, true, gb)) return r;
-    if (joint_accumulates(j)) {  // GradAccum::add for this view (trainer.cpp:134-142)
-      if (int r = launch_grad_accum(st, gb, num_planes(j->cloud->sh_degree), j->cloud->n_pad, j->cloud->n,
-                                    f->cnt_g.as<uint32_t>(), 0.5 * std::max(j->cam.width, j->cam.height),
-                                    j->acc_sum.as<double>(), j->acc_cnt.as<int32_t>()))
+    if (joint_accumulates(j)) {  // GradAccum::add for this view (trainer.cpp:134-142), staged
+      if (int r = launch_grad_norm(st, gb, num_planes(j->cloud->sh_degree), j->cloud->n_pad, j->cloud->n,
+                                   f->cnt_g.as<uint32_t>(), 0.5 * std::max(j->cam.width, j->cam.height),
+                                   j->acc_stage.as<double>() + (size_t)b * j->cloud->n_pad))
         return r;
       ctx->launches += 1;
     }
@@ -2565,6 +2614,13 @@ static int joint_launch_step(gsb_ctx* ctx, gsb_joint* j) {
     ncclResult_t r3 = nc.group_end();
     if (r1 || r2 || r3) return nccl_fail(r1 ? r1 : (r2 ? r2 : r3), "ncclAllReduce (joint)");
   }
+  if (joint_accumulates(j)) {  // commit the staged GradAccum rows unless the step is discarded
+    if (int r = launch_grad_accum_commit(st, j->acc_stage.as<double>(), j->local, j->cloud->n_pad, j->cloud->n,
+                                         j->state.p, j->ctl, j->xchg.as<double>(), j->acc_sum.as<double>(),
+                                         j->acc_cnt.as<int32_t>()))
+      return r;
+    ctx->launches += 1;
+  }
   const int64_t nb = joint_adam_blocks(j->cloud->n);
   if (int r = launch_joint_adam(st, j->cloud->params.as<float>(), j->grads.as<float>(), j->adam_m.as<float>(),
                                 j->adam_v.as<float>(), j->cloud->n, j->cloud->n_pad, j->state.p, j->ctl,
@@ -2582,7 +2638,8 @@ static int joint_frames_ready(gsb_ctx* ctx, gsb_joint* j) {
   for (gsb_frame* f : j->frames) {
     f->lean = true;
     if (int r = frame_setup(ctx, f, j->cloud, &j->cam, j->cfg.background, &j->cfg.raster, false)) return r;
-    const int64_t want = f->k_cap > 0 ? f->k_cap : initial_k_cap(j->cloud->n);
+    // after densify_and_prune grows the cloud the capacity follows it
+    const int64_t want = std::max(f->k_cap, initial_k_cap(j->cloud->n));
     if (int r = frame_reserve(f, j->cloud, want)) return r;
   }
   return GSB_OK;
@@ -2785,7 +2842,8 @@ int gsb_joint_destroy(gsb_joint* j) {
   if (j->exec) cudaGraphExecDestroy(j->exec);
   for (gsb_frame* f : j->frames) gsb_frame_destroy(f);
   DevBuf* bufs[] = {&j->grads, &j->adam_m, &j->adam_v, &j->state, &j->seq, &j->poses, &j->cams, &j->tptrs,
-                    &j->tbuf, &j->xchg, &j->red, &j->trace_total, &j->trace_l1, &j->acc_sum, &j->acc_cnt};
+                    &j->tbuf, &j->xchg, &j->red, &j->trace_total, &j->trace_l1, &j->acc_sum, &j->acc_cnt,
+                    &j->acc_stage};
   for (DevBuf* b : bufs) b->release();
   if (j->host_state) cudaFreeHost(j->host_state);
   delete j;
@@ -2840,6 +2898,12 @@ int gsb_joint_step(gsb_ctx* ctx, gsb_joint* j, int32_t steps) {
                      (long long)j->cloud->n);
     }
   }
+  return GSB_OK;
+}
+
+int gsb_joint_rng_state(const gsb_joint* j, uint64_t* rng_state) {
+  if (!j || !rng_state) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  *rng_state = j->rng_state;
   return GSB_OK;
 }
 

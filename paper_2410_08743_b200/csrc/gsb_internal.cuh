@@ -206,6 +206,11 @@ struct gsb_cloud {
   gsb::DevBuf params;            // FP32 planes [num_planes][n_pad]
   uint64_t host_fingerprint = 0; // FNV-1a sample hash of the last uploaded FP64 arrays
   uint64_t version = 0;          // bumped by device-side updates (Adam)
+  // The reference's fingerprint samples (rasterizer.cpp:62-71: 64 strided
+  // Gaussians' FP64 parameters, in hash order) of the last host upload, valid
+  // while version == fp_version (no device-side change since).
+  std::vector<unsigned char> fp_samples;
+  uint64_t fp_version = ~0ull;
 };
 
 struct gsb_image {

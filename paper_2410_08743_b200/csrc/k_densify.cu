@@ -23,16 +23,22 @@ __device__ __forceinline__ double m_(double a, double b) { return __dmul_rn(a, b
 __device__ __forceinline__ double a_(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double s_(double a, double b) { return __dsub_rn(a, b); }
 
-// GradAccum::add for one rendered view: visible splats (tile count > 0)
-// accumulate |d_mu2d| * 0.5 max(W, H) and one count.
-__global__ void grad_accum_kernel(const float* __restrict__ grads, int nplanes, int64_t n_pad, int64_t n,
-                                  const uint32_t* __restrict__ cnt_g, double scale, double* __restrict__ gsum,
-                                  int32_t* __restrict__ gcnt) {
+// GradAccum::add for one rendered view, first half: the view's per-Gaussian
+// increment |d_mu2d| * 0.5 max(W, H) for visible splats (tile count > 0), -1
+// for the others, into a staging row. The joint step commits the rows in slot
+// order only once it knows the step is kept (grad_accum_commit_kernel,
+// k_optim.cu), so a step discarded for entry-capacity growth and re-run adds
+// its views exactly once.
+__global__ void grad_norm_kernel(const float* __restrict__ grads, int nplanes, int64_t n_pad, int64_t n,
+                                 const uint32_t* __restrict__ cnt_g, double scale, double* __restrict__ stage) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n || (cnt_g[i] & kCntMask) == 0u) return;
+  if (i >= n) return;
+  if ((cnt_g[i] & kCntMask) == 0u) {
+    stage[i] = -1.0;
+    return;
+  }
   const double x = grads[(int64_t)nplanes * n_pad + i], y = grads[(int64_t)(nplanes + 1) * n_pad + i];
-  gsum[i] = a_(gsum[i], m_(sqrt(a_(m_(x, x), m_(y, y))), scale));
-  gcnt[i] += 1;
+  stage[i] = m_(sqrt(a_(m_(x, x), m_(y, y))), scale);
 }
 
 // Per-block min / max of the means (exact in any order).
@@ -228,10 +234,10 @@ __global__ void __launch_bounds__(kKnnTile) knn3_mean_kernel(const double* __res
 
 static unsigned grid_of(int64_t n) { return (unsigned)std::max<int64_t>((n + kDenBlock - 1) / kDenBlock, 1); }
 
-int launch_grad_accum(cudaStream_t st, const float* grads, int nplanes, int64_t n_pad, int64_t n,
-                      const uint32_t* cnt_g, double scale, double* gsum, int32_t* gcnt) {
-  if (n > 0) grad_accum_kernel<<<grid_of(n), kDenBlock, 0, st>>>(grads, nplanes, n_pad, n, cnt_g, scale, gsum, gcnt);
-  GSB_CHECK_LAUNCH("grad_accum_kernel");
+int launch_grad_norm(cudaStream_t st, const float* grads, int nplanes, int64_t n_pad, int64_t n,
+                     const uint32_t* cnt_g, double scale, double* stage) {
+  if (n > 0) grad_norm_kernel<<<grid_of(n), kDenBlock, 0, st>>>(grads, nplanes, n_pad, n, cnt_g, scale, stage);
+  GSB_CHECK_LAUNCH("grad_norm_kernel");
   return GSB_OK;
 }
 int launch_knn3_mean(cudaStream_t st, const double* pts, int64_t n, double* out) {

@@ -415,6 +415,43 @@ __device__ __forceinline__ bool joint_step_discarded(const double* xchg, int slo
   return false;
 }
 
+// A step's updates are skipped when it has run out of iterations, an earlier
+// step diverged, some slot overflowed (the host re-runs the step), or a slot's
+// loss is non-finite (pipelines.cpp:159-162 raises `diverged` before
+// GradAccum::add, cloud_adam_step and the pose steps).
+__device__ __forceinline__ bool joint_step_skipped(const JointDev* js, const JointCtl& ctl, const double* xchg) {
+  if (js->t >= ctl.iterations || js->diverged || joint_step_discarded(xchg, ctl.slots)) return true;
+  for (int s = 0; s < ctl.slots; ++s)
+    if (!isfinite(xchg[(int64_t)s * kXchgW + kXRgb])) return true;
+  return false;
+}
+
+// GradAccum::add (trainer.cpp:134-142), second half: the step's local slots'
+// staged increments (grad_norm_kernel, -1 = not visible) added in slot order,
+// only for a step that is kept — a discarded step adds nothing, its re-run
+// adds its views once.
+__global__ void grad_accum_commit_kernel(const double* __restrict__ stage, int local, int64_t stride, int64_t n,
+                                         const JointDev* __restrict__ js, JointCtl ctl,
+                                         const double* __restrict__ xchg, double* __restrict__ gsum,
+                                         int32_t* __restrict__ gcnt) {
+  __shared__ int s_skip;
+  if (threadIdx.x == 0) s_skip = joint_step_skipped(js, ctl, xchg) ? 1 : 0;
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s_skip || i >= n) return;
+  double sum = gsum[i];
+  int32_t cnt = gcnt[i];
+  for (int b = 0; b < local; ++b) {
+    const double v = stage[(int64_t)b * stride + i];
+    if (v >= 0.0) {
+      sum = __dadd_rn(sum, v);
+      cnt += 1;
+    }
+  }
+  gsum[i] = sum;
+  gcnt[i] = cnt;
+}
+
 // cloud_adam_step (pipelines.cpp:18-41) on the averaged gradient plus the
 // regularisers, one thread per Gaussian over the FP32 planes; block partial
 // sums (aniso loss, opacity sum) for the step's total loss. Skipped when the
@@ -432,7 +469,7 @@ __global__ void __launch_bounds__(kJointBlock) joint_adam_kernel(float* __restri
   __shared__ double s_red[kJointBlock / 32][2];
   if (threadIdx.x == 0) {
     const int64_t t = js->t;
-    s_skip = (t >= ctl.iterations || js->diverged || joint_step_discarded(xchg, ctl.slots)) ? 1 : 0;
+    s_skip = joint_step_skipped(js, ctl, xchg) ? 1 : 0;
     s_opl1 = (t < ctl.opacity_l1_steps && ctl.opacity_l1_weight > 0.0) ? 1 : 0;
     const double st = (double)(js->adam_step + 1);
     s_bc1 = (float)(1.0 - pow(kB1, st));
@@ -572,7 +609,11 @@ __global__ void joint_finalize_kernel(JointDev* __restrict__ js, const int32_t* 
   const double total = rgb * ctl.inv_slots + aniso + ctl.opacity_l1_weight * (opl1 ? opsum : 0.0);
   if (trace_total) trace_total[j.t] = total;
   if (trace_l1) trace_l1[j.t] = l1 * ctl.inv_slots;
-  if (!isfinite(total)) j.diverged = (int32_t)(j.t + 1);
+  if (!isfinite(total)) {  // pipelines.cpp:159-162: throw before the cloud and pose updates
+    j.diverged = (int32_t)(j.t + 1);
+    *js = j;
+    return;
+  }
   if (ctl.optimize_poses) {
     const double lr = d_schedule(0, ctl.cam_lr_start, ctl.cam_lr_end, j.t, ctl.iterations);
     for (int s = 0; s < ctl.slots; ++s) {
@@ -607,6 +648,14 @@ int launch_joint_sum(cudaStream_t st, float* g0, const float* rest, int64_t len,
   if (nrest > 0 && len > 0)
     joint_sum_kernel<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(g0, rest, len, nrest, stride);
   GSB_CHECK_LAUNCH("joint_sum_kernel");
+  return GSB_OK;
+}
+int launch_grad_accum_commit(cudaStream_t st, const double* stage, int local, int64_t stride, int64_t n,
+                             const void* js, const JointCtl& ctl, const double* xchg, double* gsum, int32_t* gcnt) {
+  if (n > 0)
+    grad_accum_commit_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+        stage, local, stride, n, static_cast<const JointDev*>(js), ctl, xchg, gsum, gcnt);
+  GSB_CHECK_LAUNCH("grad_accum_commit_kernel");
   return GSB_OK;
 }
 int64_t joint_adam_blocks(int64_t n) { return (n + kJointBlock - 1) / kJointBlock; }

@@ -851,6 +851,60 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
   }
 }
 
+// render_expected_depth (rasterizer.cpp:283-323): the compositing loop with
+// the splat's view-space depth in place of its colour. Not on the hot path
+// (dataset generation, synth.cpp:117-127): one 256-thread CTA per tile, one
+// pixel per thread, records read from L2. The cutoff and alpha decisions use
+// the composite's exact FP32 arithmetic (tile-local offsets; the odd row of a
+// vertical pixel pair at dy + 1), so the expected depth sees the same hits
+// as the rendered image. Sums in FP64 as the reference.
+__global__ void __launch_bounds__(256) expected_depth_kernel(const uint2* __restrict__ ranges,
+                                                             const uint32_t* __restrict__ ranks,
+                                                             const SplatRec* __restrict__ rec,
+                                                             const SplatAux* __restrict__ aux,
+                                                             const double* __restrict__ depth_g,
+                                                             const CamDev* __restrict__ cam_p, RasterDev rc,
+                                                             float* __restrict__ depth_out,
+                                                             float* __restrict__ weight_out) {
+  const int W = cam_p->width, H = cam_p->height, tiles_x = cam_p->tiles_x;
+  const int tile = blockIdx.x, tx = tile % tiles_x, ty = tile / tiles_x;
+  const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
+  const int x = tx * kTile + lx, y = ty * kTile + ly;
+  if (x >= W || y >= H) return;
+  const double ox = (double)(tx * kTile), oy = (double)(ty * kTile);
+  const uint2 range = ranges[tile];
+  float T = 1.0f;
+  double dsum = 0.0, wsum = 0.0;
+  for (uint32_t e = range.x; e < range.y; ++e) {
+    const uint32_t r = ranks[e];
+    const SplatRec R = rec[r];
+    const float mx = (float)(R.mu_x - ox), my = (float)(R.mu_y - oy);
+    const float dx = (float)lx - mx;
+    const float dy = (ly & 1) ? ((float)(ly - 1) - my) + 1.0f : (float)ly - my;
+    const float g = splat_power(R.conic_a, R.conic_b, R.conic_c, dx, dy);
+    if (!(g <= rc.cutoff2_f)) continue;
+    const float al = fminf(rc.alpha_clamp_f, R.opacity * exp_neg_half(g));
+    const float w = al * T;
+    dsum += (double)w * depth_g[aux[r].gid];
+    wsum += (double)w;
+    T *= 1.0f - al;
+    if (T < rc.early_term_f) break;
+  }
+  const int64_t q = (int64_t)y * W + x;
+  weight_out[q] = (float)wsum;
+  depth_out[q] = wsum > 1e-8 ? (float)(dsum / wsum) : 0.0f;
+}
+
+int launch_expected_depth(cudaStream_t st, gsb_frame* f, const RasterDev& rc, float* depth_out, float* weight_out) {
+  const int n_tiles = f->tiles_x * f->tiles_y;
+  if (n_tiles > 0)
+    expected_depth_kernel<<<n_tiles, 256, 0, st>>>(f->ranges.as<uint2>(), f->list(), f->list_rec(), f->list_aux(),
+                                                    f->depth_g.as<double>(), f->cam.as<CamDev>(), rc, depth_out,
+                                                    weight_out);
+  GSB_CHECK_LAUNCH("expected_depth_kernel");
+  return GSB_OK;
+}
+
 int launch_composite(cudaStream_t st, gsb_frame* f, const RasterDev& rc) {
   const int n_tiles = f->tiles_x * f->tiles_y;
   const int64_t npix = (int64_t)f->width * f->height;

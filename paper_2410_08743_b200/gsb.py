@@ -235,6 +235,8 @@ def _sigs():
         "gsb_comm_allreduce_f32": (C.c_int, [_vp, _vp, i64]),
         "gsb_default_joint_config": (None, [P(JointConfig)]),
         "gsb_joint_schedule": (C.c_int, [u64, i32, i64, _vp]),
+        "gsb_joint_rng_state": (C.c_int, [_vp, P(u64)]),
+        "gsb_render_expected_depth": (C.c_int, [_vp, _vp, P(Camera), _vp, _vp, _vp]),
         "gsb_joint_create": (C.c_int, [_vp, _vp, _vp, i32, _vp, _vp, P(JointConfig), u64, i32, _vp, P(_vp)]),
         "gsb_joint_destroy": (C.c_int, [_vp]),
         "gsb_joint_step": (C.c_int, [_vp, _vp, i32]),
@@ -522,6 +524,15 @@ def render(ctx: Context, cloud: Cloud, cam: Camera, background=(0.0, 0.0, 0.0), 
     return RenderOutput(frame, img)
 
 
+def render_expected_depth(ctx: Context, cloud: Cloud, cam: Camera, config: RasterConfig | None = None):
+    """gsopt::render_expected_depth (rasterizer.cpp:283-323): (depth, weight), each (H, W) float32."""
+    cfg = config or RasterConfig.default()
+    depth = np.zeros((cam.height, cam.width), np.float32)
+    weight = np.zeros((cam.height, cam.width), np.float32)
+    _check(lib().gsb_render_expected_depth(ctx.h, cloud.h, C.byref(cam), C.byref(cfg), _p(depth), _p(weight)))
+    return depth, weight
+
+
 def render_backward(ctx: Context, cloud: Cloud, cam: Camera, out: RenderOutput, d_image: np.ndarray,
                     pose_only=False, grads: Grads | None = None):
     """gsopt::render_backward (rasterizer.hpp:112-113). Returns (grads dict | None, d_pose)."""
@@ -746,6 +757,12 @@ class JointOptimizer:
             self.close()
         except Exception:
             pass
+
+    def rng_state(self) -> int:
+        """The run's Rng state (gsb_joint_rng_state): continue the caller's Rng from it."""
+        v = C.c_uint64()
+        _check(lib().gsb_joint_rng_state(self.h, C.byref(v)))
+        return int(v.value)
 
     def step(self, steps: int = 1):
         _check(lib().gsb_joint_step(self.ctx.h, self.h, steps))

@@ -16,3 +16,7 @@ if [ "${LAUNCHES:-1}" = 1 ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_batch_$TAG.csv python tools/prof_batch.py 3 > /dev/null 2>&1
 python tools/launch_summary.py gpurun_out/launches_batch_$TAG.csv | head -30
 fi
+if [ "${DROPIN:-1}" = 1 ] && [ -x integration/_build/acceptance_b200 ]; then
+  for c in 2 3 4 7 8; do timeout 900 integration/_build/acceptance_b200 $c > gpurun_out/dropin_acc_$c.txt 2>&1; tail -1 gpurun_out/dropin_acc_$c.txt; done
+  for t in test_rasterizer test_trainer test_losses test_scene; do timeout 900 integration/_build/${t}_b200 > gpurun_out/dropin_$t.txt 2>&1; tail -3 gpurun_out/dropin_$t.txt; done
+fi
