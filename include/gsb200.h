@@ -63,7 +63,12 @@ extern "C" {
 
 /* render_backward flags */
 #define GSB_BWD_POSE_ONLY 1u   /* estimate_pose only consumes d_pose (pipelines.cpp:84) */
-#define GSB_BWD_FAST_ATOMIC 2u /* RasterConfig::deterministic == false (rasterizer.cpp:419-431) */
+/* RasterConfig::deterministic == false selects the reference's atomic
+ * phase-2 reduction (rasterizer.cpp:419-431). Accepted and has no effect:
+ * libgsb200's reduction is always the fixed-order one (no floating-point
+ * atomics anywhere), which the reference's own test requires to agree with
+ * the atomic mode within 1e-10 (test_rasterizer.cpp:357-375). */
+#define GSB_BWD_FAST_ATOMIC 2u
 
 typedef struct gsb_ctx gsb_ctx;
 typedef struct gsb_cloud gsb_cloud;
@@ -256,8 +261,15 @@ double gsb_schedule(int32_t kind /* 0 cosine, 1 exponential */, double start, do
 /* Runs on the device (FP64), like the batched step inside gsb_estimate_pose. */
 int gsb_pose_step(gsb_ctx* ctx, const double pose[12], const double d_pose[6], double lr,
                   gsb_pose_adam* state, double pose_out[12], double applied_update[6]);
+/* adam_step (trainer.hpp:85 / trainer.cpp:40-53): AdamState = (m, v, step),
+ * the caller's n-element arrays (zero-initialised before the first step, as
+ * AdamState::resize); updated in place, bit for bit the reference's FP64. */
 int gsb_adam_step(gsb_ctx* ctx, double* params, const double* grads, double* m, double* v,
                   int64_t* step, int64_t n, double lr);
+/* The per-index overload adam_step(..., lr_of) (trainer.hpp:86-87 /
+ * trainer.cpp:55-69): lr_of[i] is the learning rate of element i. */
+int gsb_adam_step_lrs(gsb_ctx* ctx, double* params, const double* grads, double* m, double* v,
+                      int64_t* step, int64_t n, const double* lr_of);
 int gsb_adam_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_adam** out);
 int gsb_adam_destroy(gsb_adam* adam);
 /* lrs = {pos, rot, scale, opacity, sh_dc, sh_rest} (pipelines.cpp:14-16). */

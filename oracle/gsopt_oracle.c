@@ -1070,6 +1070,43 @@ void orc_count_work(const orc_render_out* out, const double* d_image, int64_t co
   counts[3] = cb;
 }
 
+/* Test aid (no reference counterpart): per-pixel relative distance of the
+ * FP64 forward pass from its discrete decisions — min over the examined
+ * entries (j < contrib) of |g - cutoff^2| / cutoff^2 (rasterizer.cpp:254) and,
+ * over the hits, of |T - early_termination| / early_termination after the
+ * update (258). An FP32 evaluation can only take a different decision where
+ * this margin is below its rounding error; parity tests hold pixels with a
+ * margin above a stated threshold to the image tolerance and report the rest. */
+void orc_decision_margin(const orc_render_out* out, double* margin) {
+  const double cutoff2 = out->config.cutoff_sigma * out->config.cutoff_sigma;
+  const double et = out->config.early_termination, clampa = out->config.alpha_clamp;
+  const int tile = out->config.tile_size;
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int y = 0; y < out->height; ++y) {
+    for (int x = 0; x < out->width; ++x) {
+      const size_t pix = (size_t)y * out->width + x;
+      const int t = (y / tile) * out->tiles_x + x / tile;
+      const int32_t lb = out->tile_ranges[2 * t];
+      double m = INFINITY, T = 1.0;
+      for (int32_t j = 0; j < out->contrib_count[pix]; ++j) {
+        const orc_splat* rec = &out->splats[out->tile_lists[lb + j]];
+        const double d0 = x - rec->mu2d[0], d1 = y - rec->mu2d[1];
+        const double c0 = rec->conic[0] * d0 + rec->conic[1] * d1, c1 = rec->conic[2] * d0 + rec->conic[3] * d1;
+        const double g = d0 * c0 + d1 * c1;
+        const double mg = fabs(g - cutoff2) / cutoff2;
+        if (mg < m) m = mg;
+        if (g > cutoff2) continue;
+        double a = rec->opacity * exp(-0.5 * g);
+        if (a > clampa) a = clampa;
+        T *= 1.0 - a;
+        const double mt = fabs(T - et) / et;
+        if (mt < m) m = mt;
+      }
+      margin[pix] = m;
+    }
+  }
+}
+
 /* ---------------------------------------------------------------- losses */
 #define KWIN 11
 #define KHALF 5

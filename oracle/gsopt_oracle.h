@@ -263,6 +263,7 @@ double orc_gradcheck(const orc_cloud* cloud, const orc_camera* cam, const double
  * the same over pixels with a non-zero (unclamped) upstream gradient (H_b,
  * C_b). d_image may be NULL (then H_b = C_b = 0). */
 void orc_count_work(const orc_render_out* out, const double* d_image, int64_t counts[4]);
+void orc_decision_margin(const orc_render_out* out, double* margin);
 
 /* helpers for ctypes users */
 void orc_cloud_alloc(orc_cloud* c, int64_t n, int32_t sh_degree);

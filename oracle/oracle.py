@@ -165,6 +165,7 @@ def lib():
             "orc_cloud_free": (None, [P(Cloud)]),
             "orc_num_threads": (C.c_int, []),
             "orc_count_work": (None, [P(RenderOut), vp, vp]),
+            "orc_decision_margin": (None, [P(RenderOut), vp]),
             "orc_joint_schedule": (None, [P(Rng), i32, i64, vp]),
             "orc_cloud_adam_step": (None, [P(Cloud), P(Grads), vp, vp]),
             "orc_densify_and_prune": (None, [P(Cloud), vp, vp, d, d, i32, d, P(Rng), P(Cloud), vp, vp]),
@@ -224,6 +225,8 @@ def ref_lib():
         L.ref_estimate_pose.argtypes = port.orc_estimate_pose.argtypes[:16]
         L.ref_synth_scene.restype = None
         L.ref_synth_scene.argtypes = [i32, i32, i32, i32, i32, i32, C.c_uint64, P(Cloud), vp, vp]
+        L.ref_adam_step.restype = None
+        L.ref_adam_step.argtypes = [vp, vp, vp, vp, P(C.c_int64), C.c_int64, d, vp]
         L.ref_render_expected_depth.restype = None
         L.ref_render_expected_depth.argtypes = [P(Cloud), P(Camera), P(RasterConfig), vp, vp]
         L.ref_last_error.restype = C.c_char_p
@@ -906,6 +909,14 @@ def count_work(rr: RenderResult, d_image=None):
     d = None if d_image is None else np.ascontiguousarray(d_image, np.float64)
     _L().orc_count_work(rr._ptr, _p(d) if d is not None else None, _p(out))
     return tuple(int(v) for v in out)
+
+
+def decision_margin(rr: RenderResult) -> np.ndarray:
+    """Per-pixel relative margin (H, W) of the FP64 forward's discrete decisions
+    (cutoff test, early termination): pixels above a threshold cannot flip in FP32."""
+    m = np.zeros(rr.image.shape[0] * rr.image.shape[1])
+    lib().orc_decision_margin(rr._ptr, _p(m))
+    return m.reshape(rr.image.shape[:2])
 
 
 def num_threads() -> int:

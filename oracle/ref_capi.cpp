@@ -311,6 +311,22 @@ void ref_pose_step(const double R[9], const double t[3], const double d_pose[6],
   state->step = adam.step;
 }
 
+// trainer.cpp:40-69: both adam_step overloads; lrs == nullptr -> scalar lr.
+void ref_adam_step(double* params, const double* grads, double* m, double* v, int64_t* step, int64_t n, double lr,
+                   const double* lrs) {
+  AdamState st;
+  st.m.assign(m, m + n);
+  st.v.assign(v, v + n);
+  st.step = *step;
+  if (lrs)
+    adam_step(&st, params, grads, static_cast<std::size_t>(n), [lrs](std::size_t i) { return lrs[i]; });
+  else
+    adam_step(&st, params, grads, static_cast<std::size_t>(n), lr);
+  std::memcpy(m, st.m.data(), sizeof(double) * n);
+  std::memcpy(v, st.v.data(), sizeof(double) * n);
+  *step = st.step;
+}
+
 // pipelines.cpp:218-222 -> 58-92: the reference's own estimate_pose. Returns
 // steps_used; best pose out.
 int32_t ref_estimate_pose(const orc_cloud* cloud, const double* image, double fx, double fy, double cx, double cy,

@@ -76,7 +76,7 @@ void pose_state_read(const void* host_state, double best_pose[12], double cur_po
 void pose_state_set_adam(void* host_state, const double m[6], const double v[6], int64_t step);
 int launch_pose_step(cudaStream_t st, void* states, const double* dpose, double lr, int nb);
 int launch_adam_f64(cudaStream_t st, double* p, const double* g, double* m, double* v, int64_t n, double lr,
-                    int64_t step);
+                    const double* lrs, int64_t step);
 int launch_joint_slot_begin(cudaStream_t st, const void* js, const int32_t* seq, const JointCtl& ctl, int b,
                             const CamDev* cams, CamDev* frame_cam, const float* const* targets, float* tbuf,
                             int64_t n3p);
@@ -626,6 +626,30 @@ static int download_image(gsb_ctx* ctx, const float* dev_planes, int W, int H, d
   });
   return GSB_OK;
 }
+// A rendered frame's image to host FP64 HWC. Pixels no splat touched
+// (final T == 1 exactly and the stored value is the FP32 background) are the
+// background in FP64 exactly, as the reference composes them (C = 0 + bg * 1,
+// rasterizer.cpp:260-268; empty cloud = background, test_rasterizer.cpp:127-142).
+static int download_frame_image(gsb_ctx* ctx, const gsb_frame* f, double* out) {
+  if (int r = download_image(ctx, f->image.as<float>(), f->width, f->height, out)) return r;
+  const size_t P = (size_t)f->width * f->height;
+  std::vector<float> ft(P);
+  GSB_CUDA(cudaMemcpyAsync(ft.data(), f->final_t.p, sizeof(float) * P, cudaMemcpyDeviceToHost, ctx->stream));
+  GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  double bg[3];
+  float bgf[3];
+  for (int c = 0; c < 3; ++c) {
+    bg[c] = std::min(f->background[c], 1.0);
+    bgf[c] = std::min((float)f->background[c], 1.0f);
+  }
+  host_parallel(P, [&](size_t b, size_t e) {
+    for (size_t p = b; p < e; ++p)
+      if (ft[p] == 1.0f)
+        for (int c = 0; c < 3; ++c)
+          if (out[3 * p + c] == (double)bgf[c]) out[3 * p + c] = bg[c];
+  });
+  return GSB_OK;
+}
 // interleaved FP64 host -> planar FP32 device
 // Host FP64 HWC image -> device FP32 planes, stream ordered on ctx->stream.
 // Two pinned staging slots alternate: the conversion of the next image
@@ -859,6 +883,7 @@ int gsb_cloud_destroy(gsb_cloud* c) {
 
 int gsb_cloud_upload(gsb_cloud* c, const double* means, const double* rotations, const double* log_scales,
                      const double* opacity_logits, const double* sh, int32_t active) {
+  GSB_NVTX("gsb_cloud_upload");
   if (!c) return fail(GSB_ERR_INVALID_ARGUMENT, "null cloud");
   gsb_ctx* ctx = c->ctx;
   if (int r = ensure_device(ctx)) return r;
@@ -913,6 +938,7 @@ int gsb_cloud_upload(gsb_cloud* c, const double* means, const double* rotations,
 
 int gsb_cloud_download(gsb_cloud* c, double* means, double* rotations, double* log_scales, double* opacity_logits,
                        double* sh) {
+  GSB_NVTX("gsb_cloud_download");
   if (!c) return fail(GSB_ERR_INVALID_ARGUMENT, "null cloud");
   gsb_ctx* ctx = c->ctx;
   if (int r = ensure_device(ctx)) return r;
@@ -975,6 +1001,7 @@ int gsb_frame_destroy(gsb_frame* f) {
 
 int gsb_render(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, const double bg[3],
                const gsb_raster_config* cfg, gsb_frame* f, double* image_out) {
+  GSB_NVTX("gsb_render");
   if (int r = ensure_device(ctx)) return r;
   if (!cloud || !cam || !f) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
   gsb_raster_config dflt;
@@ -985,12 +1012,13 @@ int gsb_render(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, const doub
   const RasterDev rc = make_rasterdev(cfg);
   if (int r = render_sync(ctx, cloud, f, rc)) return r;
   f->valid = true;
-  if (image_out) return download_image(ctx, f->image.as<float>(), f->width, f->height, image_out);
+  if (image_out) return download_frame_image(ctx, f, image_out);
   return GSB_OK;
 }
 
 int gsb_render_expected_depth(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, const gsb_raster_config* cfg,
                               float* depth_out, float* weight_out) {
+  GSB_NVTX("gsb_render_expected_depth");
   if (int r = ensure_device(ctx)) return r;
   if (!cloud || !cam || !depth_out || !weight_out) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
   gsb_raster_config dflt;
@@ -1039,13 +1067,14 @@ int gsb_frame_download(gsb_frame* f, double* image, double* accum_t, double* fin
                        uint8_t* overflow, int32_t* s_gauss, double* s_mu2d, double* s_depth, double* s_conic,
                        double* s_color, double* s_opacity, double* s_radius, uint8_t* s_clamped, int32_t* tile_lists,
                        int32_t* tile_ranges) {
+  GSB_NVTX("gsb_frame_download");
   if (!f || !f->valid) return fail(GSB_ERR_INVALID_ARGUMENT, "frame holds no forward state");
   gsb_ctx* ctx = f->ctx;
   if (int r = ensure_device(ctx)) return r;
   const int64_t P = (int64_t)f->width * f->height, V = f->n_splats, K = f->n_entries;
   const int T = f->tiles_x * f->tiles_y;
   if (image)
-    if (int r = download_image(ctx, f->image.as<float>(), f->width, f->height, image)) return r;
+    if (int r = download_frame_image(ctx, f, image)) return r;
   std::vector<float> ft(P);
   std::vector<uint32_t> ps(P);
   GSB_CUDA(cudaMemcpyAsync(ft.data(), f->final_t.p, sizeof(float) * P, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1116,6 +1145,7 @@ int gsb_frame_download(gsb_frame* f, double* image, double* accum_t, double* fin
 
 // ------------------------------------------------------------------- loss
 int gsb_image_create(gsb_ctx* ctx, const double* img, int32_t W, int32_t H, gsb_image** out) {
+  GSB_NVTX("gsb_image_create");
   if (int r = ensure_device(ctx)) return r;
   if (!img || !out || W <= 0 || H <= 0) return fail(GSB_ERR_INVALID_ARGUMENT, "bad image");
   gsb_image* im = new gsb_image();
@@ -1162,6 +1192,7 @@ int gsb_image_destroy(gsb_image* im) {
 
 int gsb_rgb_loss(gsb_ctx* ctx, const double* rendered, const double* target, int32_t W, int32_t H, double beta,
                  double* loss_out, double* d_rendered) {
+  GSB_NVTX("gsb_rgb_loss");
   if (int r = ensure_device(ctx)) return r;
   if (!rendered || !target || W <= 0 || H <= 0) return fail(GSB_ERR_INVALID_ARGUMENT, "bad images");
   static thread_local gsb_frame* work = nullptr;
@@ -1188,6 +1219,7 @@ int gsb_rgb_loss(gsb_ctx* ctx, const double* rendered, const double* target, int
 }
 
 int gsb_frame_rgb_loss(gsb_ctx* ctx, gsb_frame* f, gsb_image* target, double beta, double* loss_out) {
+  GSB_NVTX("gsb_frame_rgb_loss");
   if (int r = ensure_device(ctx)) return r;
   if (!f || !f->valid || !target) return fail(GSB_ERR_INVALID_ARGUMENT, "frame / target missing");
   if (target->width != f->width || target->height != f->height)
@@ -1351,6 +1383,7 @@ static int check_state(gsb_cloud* cloud, const gsb_camera* cam, gsb_frame* f) {
 
 int gsb_render_backward(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, gsb_frame* f, const double* d_image,
                         int32_t W, int32_t H, uint32_t flags, gsb_grads* grads, double d_pose_out[6]) {
+  GSB_NVTX("gsb_render_backward");
   if (int r = ensure_device(ctx)) return r;
   if (!cloud || !cam || !f || !d_image) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
   if (int r = check_state(cloud, cam, f)) return r;  // rasterizer.cpp:338-340
@@ -1364,6 +1397,7 @@ int gsb_render_backward(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, g
 
 int gsb_render_backward_device(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, gsb_frame* f, uint32_t flags,
                                gsb_grads* grads, double d_pose_out[6]) {
+  GSB_NVTX("gsb_render_backward_device");
   if (int r = ensure_device(ctx)) return r;
   if (!cloud || !cam || !f) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
   if (int r = check_state(cloud, cam, f)) return r;
@@ -1381,6 +1415,7 @@ double gsb_schedule(int32_t kind, double start, double end, int64_t step, int64_
 
 int gsb_pose_step(gsb_ctx* ctx, const double pose[12], const double d_pose[6], double lr, gsb_pose_adam* state,
                   double pose_out[12], double applied[6]) {
+  GSB_NVTX("gsb_pose_step");
   if (int r = ensure_device(ctx)) return r;
   if (!pose || !d_pose || !state || !pose_out) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
   const size_t sb = pose_state_bytes();
@@ -1408,20 +1443,23 @@ int gsb_pose_step(gsb_ctx* ctx, const double pose[12], const double d_pose[6], d
   return GSB_OK;
 }
 
-int gsb_adam_step(gsb_ctx* ctx, double* params, const double* grads, double* m, double* v, int64_t* step, int64_t n,
-                  double lr) {
+namespace gsb {
+// Both adam_step overloads (trainer.cpp:40-69): lrs == nullptr -> scalar lr.
+static int adam_step_host(gsb_ctx* ctx, double* params, const double* grads, double* m, double* v, int64_t* step,
+                          int64_t n, double lr, const double* lrs) {
   if (int r = ensure_device(ctx)) return r;
   if (n < 0 || (n > 0 && (!params || !grads || !m || !v)) || !step) return fail(GSB_ERR_INVALID_ARGUMENT, "bad adam args");
   *step += 1;
   if (n == 0) return GSB_OK;
   DevBuf buf;
-  GSB_CUDA(buf.reserve(sizeof(double) * 4 * n));
+  GSB_CUDA(buf.reserve(sizeof(double) * (lrs ? 5 : 4) * n));
   double* d = buf.as<double>();
   GSB_CUDA(cudaMemcpyAsync(d, params, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
   GSB_CUDA(cudaMemcpyAsync(d + n, grads, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
   GSB_CUDA(cudaMemcpyAsync(d + 2 * n, m, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
   GSB_CUDA(cudaMemcpyAsync(d + 3 * n, v, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
-  int r = launch_adam_f64(ctx->stream, d, d + n, d + 2 * n, d + 3 * n, n, lr, *step);
+  if (lrs) GSB_CUDA(cudaMemcpyAsync(d + 4 * n, lrs, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  int r = launch_adam_f64(ctx->stream, d, d + n, d + 2 * n, d + 3 * n, n, lr, lrs ? d + 4 * n : nullptr, *step);
   if (r) {
     buf.release();
     return r;
@@ -1433,6 +1471,18 @@ int gsb_adam_step(gsb_ctx* ctx, double* params, const double* grads, double* m, 
   GSB_CUDA(cudaStreamSynchronize(ctx->stream));
   buf.release();
   return GSB_OK;
+}
+}  // namespace gsb
+
+int gsb_adam_step(gsb_ctx* ctx, double* params, const double* grads, double* m, double* v, int64_t* step, int64_t n,
+                  double lr) {
+  return adam_step_host(ctx, params, grads, m, v, step, n, lr, nullptr);
+}
+
+int gsb_adam_step_lrs(gsb_ctx* ctx, double* params, const double* grads, double* m, double* v, int64_t* step,
+                      int64_t n, const double* lr_of) {
+  if (n > 0 && !lr_of) return fail(GSB_ERR_INVALID_ARGUMENT, "null lr_of");
+  return adam_step_host(ctx, params, grads, m, v, step, n, 0.0, lr_of);
 }
 
 int gsb_adam_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_adam** out) {
@@ -1469,6 +1519,7 @@ int gsb_adam_destroy(gsb_adam* a) {
 }
 
 int gsb_cloud_adam_step(gsb_ctx* ctx, gsb_cloud* cloud, gsb_grads* grads, gsb_adam* adam, const double lrs[6]) {
+  GSB_NVTX("gsb_cloud_adam_step");
   if (int r = ensure_device(ctx)) return r;
   if (!cloud || !grads || !adam || !lrs) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
   if (grads->n != cloud->n || adam->n != cloud->n) return fail(GSB_ERR_DIMENSION_MISMATCH, "adam/grads/cloud sizes");
@@ -1798,6 +1849,7 @@ int gsb_session_destroy(gsb_session* s) {
 }
 
 int gsb_session_step(gsb_ctx* ctx, gsb_session* s, int32_t iterations) {
+  GSB_NVTX("gsb_session_step");
   if (int r = ensure_device(ctx)) return r;
   if (!s || s->ctx != ctx) return fail(GSB_ERR_INVALID_ARGUMENT, "session / context mismatch");
   const int32_t chunk = 16;
@@ -1811,6 +1863,7 @@ int gsb_session_step(gsb_ctx* ctx, gsb_session* s, int32_t iterations) {
 }
 
 int gsb_session_step_async(gsb_ctx* ctx, gsb_session* s, int32_t iterations) {
+  GSB_NVTX("gsb_session_step_async");
   if (int r = ensure_device(ctx)) return r;
   if (!s || s->ctx != ctx) return fail(GSB_ERR_INVALID_ARGUMENT, "session / context mismatch");
   if (iterations <= 0) return GSB_OK;
@@ -1860,6 +1913,7 @@ int gsb_session_frame_info(gsb_session* s, gsb_frame_info* info) {
 int gsb_estimate_pose(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* target, const double intr[4],
                       const double init_pose[12], const gsb_pose_config* cfg, double pose_out[12], double* final_loss,
                       int32_t* steps_used, int32_t* converged, double* trace_pose, double* trace_loss) {
+  GSB_NVTX("gsb_estimate_pose");
   if (!pose_out) return fail(GSB_ERR_INVALID_ARGUMENT, "null pose_out");
   gsb_session* s = nullptr;
   if (int r = gsb_session_create(ctx, cloud, target, intr, init_pose, cfg, &s)) return r;
@@ -2065,6 +2119,7 @@ int gsb_pose_batch_destroy(gsb_pose_batch* b) {
 }
 
 int gsb_pose_batch_step_async(gsb_ctx* ctx, gsb_pose_batch* b, int32_t iterations) {
+  GSB_NVTX("gsb_pose_batch_step_async");
   if (int r = ensure_device(ctx)) return r;
   if (!b || b->ctx != ctx) return fail(GSB_ERR_INVALID_ARGUMENT, "pose batch / context mismatch");
   if (iterations <= 0) return GSB_OK;
@@ -2076,6 +2131,7 @@ int gsb_pose_batch_step_async(gsb_ctx* ctx, gsb_pose_batch* b, int32_t iteration
 }
 
 int gsb_pose_batch_sync(gsb_ctx* ctx, gsb_pose_batch* b) {
+  GSB_NVTX("gsb_pose_batch_sync");
   if (int r = ensure_device(ctx)) return r;
   if (!b || b->ctx != ctx) return fail(GSB_ERR_INVALID_ARGUMENT, "pose batch / context mismatch");
   // Every session's status block in one round trip; only sessions that had
@@ -2113,6 +2169,7 @@ int gsb_pose_batch_discarded(const gsb_pose_batch* b, int64_t* out) {
 }
 
 int gsb_pose_batch_step(gsb_ctx* ctx, gsb_pose_batch* b, int32_t iterations) {
+  GSB_NVTX("gsb_pose_batch_step");
   const int32_t chunk = 16;
   while (iterations > 0) {
     bool all_stopped = true;
@@ -2131,6 +2188,7 @@ int gsb_pose_batch_step(gsb_ctx* ctx, gsb_pose_batch* b, int32_t iterations) {
 int gsb_estimate_poses(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* const* targets, const double intr[4],
                        const double* init_poses, int32_t count, const gsb_pose_config* cfg, double* poses_out,
                        double* final_losses, int32_t* steps_used) {
+  GSB_NVTX("gsb_estimate_poses");
   if (!targets || !init_poses || !poses_out || count <= 0) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
   std::vector<gsb_session*> ss(count, nullptr);
   int r = GSB_OK;
@@ -2330,6 +2388,7 @@ extern "C" {
 int gsb_densify_and_prune(gsb_ctx* ctx, gsb_cloud* cloud, const double* grad_sum, const int32_t* count,
                           double grad_threshold, double densify_size_ratio, int32_t n_target, double prune_opacity,
                           uint64_t* rng_state, gsb_adam* adam, int32_t report[3]) {
+  GSB_NVTX("gsb_densify_and_prune");
   if (int r = ensure_device(ctx)) return r;
   if (!cloud || !grad_sum || !count || !rng_state || !report) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
   if (adam && (adam->n != cloud->n || adam->n_pad != cloud->n_pad))
@@ -2851,6 +2910,7 @@ int gsb_joint_destroy(gsb_joint* j) {
 }
 
 int gsb_joint_step(gsb_ctx* ctx, gsb_joint* j, int32_t steps) {
+  GSB_NVTX("gsb_joint_step");
   if (int r = ensure_device(ctx)) return r;
   if (!j || j->ctx != ctx) return fail(GSB_ERR_INVALID_ARGUMENT, "joint / context mismatch");
   int64_t left = std::min<int64_t>(steps, (int64_t)j->cfg.iterations - j->t);

@@ -10,8 +10,20 @@
 #include <vector>
 
 #include "../../include/gsb200.h"
+#include <nvtx3/nvToolsExt.h>
 
 namespace gsb {
+
+// NVTX range over a C-ABI entry point (header-only NVTX v3: no link
+// dependency; a profiler such as nsys / ncu --nvtx attaches through its
+// injection library, otherwise the calls are no-ops).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define GSB_NVTX(name) ::gsb::NvtxRange gsb_nvtx_range_(name)
 
 constexpr int kTile = 16;         // rasterizer tile (RasterConfig::tile_size, rasterizer.hpp:31)
 constexpr int kTilePix = kTile * kTile;

@@ -278,16 +278,23 @@ __global__ void pose_step_kernel(PoseState* st, const double* __restrict__ dpose
 }
 
 // adam_step (trainer.cpp:40-53) on a flat FP64 array.
+// adam_step (trainer.cpp:40-69), both overloads: lrs == nullptr -> the scalar
+// lr, else lr_of(i) = lrs[i]. Explicitly rounded FP64 in the reference's
+// expression order (no FMA contraction), so the update is the reference's
+// bit for bit.
 __global__ void adam_f64_kernel(double* __restrict__ p, const double* __restrict__ g, double* __restrict__ m,
-                                double* __restrict__ v, int64_t n, double lr, double bc1, double bc2) {
+                                double* __restrict__ v, int64_t n, double lr, const double* __restrict__ lrs,
+                                double bc1, double bc2) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double gi = g[i];
-  const double mi = kB1 * m[i] + (1.0 - kB1) * gi;
-  const double vi = kB2 * v[i] + (1.0 - kB2) * gi * gi;
+  const double mi = __dadd_rn(__dmul_rn(kB1, m[i]), __dmul_rn(1.0 - kB1, gi));
+  const double vi = __dadd_rn(__dmul_rn(kB2, v[i]), __dmul_rn(__dmul_rn(1.0 - kB2, gi), gi));
   m[i] = mi;
   v[i] = vi;
-  p[i] -= lr * (mi / bc1) / (sqrt(vi / bc2) + kEps);
+  const double m_hat = __ddiv_rn(mi, bc1), v_hat = __ddiv_rn(vi, bc2);
+  const double step = __ddiv_rn(__dmul_rn(lrs ? lrs[i] : lr, m_hat), __dadd_rn(__dsqrt_rn(v_hat), kEps));
+  p[i] = __dsub_rn(p[i], step);
 }
 
 struct AdamCoef {
@@ -765,9 +772,9 @@ int launch_pose_step(cudaStream_t st, void* states, const double* dpose, double 
   return GSB_OK;
 }
 int launch_adam_f64(cudaStream_t st, double* p, const double* g, double* m, double* v, int64_t n, double lr,
-                    int64_t step) {
+                    const double* lrs, int64_t step) {
   const double bc1 = 1.0 - pow(kB1, (double)step), bc2 = 1.0 - pow(kB2, (double)step);
-  if (n > 0) adam_f64_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p, g, m, v, n, lr, bc1, bc2);
+  if (n > 0) adam_f64_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p, g, m, v, n, lr, lrs, bc1, bc2);
   GSB_CHECK_LAUNCH("adam_f64_kernel");
   return GSB_OK;
 }

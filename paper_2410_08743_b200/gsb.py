@@ -209,6 +209,7 @@ def _sigs():
         "gsb_schedule": (d, [i32, d, d, i64, i64]),
         "gsb_pose_step": (C.c_int, [_vp, _vp, _vp, d, P(PoseAdam), _vp, _vp]),
         "gsb_adam_step": (C.c_int, [_vp, _vp, _vp, _vp, _vp, P(i64), i64, d]),
+        "gsb_adam_step_lrs": (C.c_int, [_vp, _vp, _vp, _vp, _vp, P(i64), i64, _vp]),
         "gsb_adam_create": (C.c_int, [_vp, _vp, P(_vp)]),
         "gsb_adam_destroy": (C.c_int, [_vp]),
         "gsb_cloud_adam_step": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
@@ -522,6 +523,21 @@ def render(ctx: Context, cloud: Cloud, cam: Camera, background=(0.0, 0.0, 0.0), 
     cfg = config or RasterConfig.default()
     _check(lib().gsb_render(ctx.h, cloud.h, C.byref(cam), _p(bg), C.byref(cfg), frame.h, _p(img)))
     return RenderOutput(frame, img)
+
+
+def adam_step(ctx: Context, params, grads, m, v, step: int, lr) -> int:
+    """gsopt::adam_step (trainer.hpp:85-87): params / m / v (FP64 arrays) updated in
+    place; lr a scalar or a per-index array (the lr_of overload). Returns the new step."""
+    st = C.c_int64(step)
+    g = np.ascontiguousarray(grads, np.float64)
+    for a in (params, m, v):
+        assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]
+    if np.ndim(lr) == 0:
+        _check(lib().gsb_adam_step(ctx.h, _p(params), _p(g), _p(m), _p(v), C.byref(st), params.size, float(lr)))
+    else:
+        lrs = np.ascontiguousarray(lr, np.float64)
+        _check(lib().gsb_adam_step_lrs(ctx.h, _p(params), _p(g), _p(m), _p(v), C.byref(st), params.size, _p(lrs)))
+    return int(st.value)
 
 
 def render_expected_depth(ctx: Context, cloud: Cloud, cam: Camera, config: RasterConfig | None = None):

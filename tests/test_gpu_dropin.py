@@ -113,3 +113,26 @@ def test_render_expected_depth_matches_reference(G, ctx):
         assert m.any()
         assert np.max(np.abs(d[m] - d_ref[m]) / np.abs(d_ref[m])) < 1e-5
         assert np.all(d[w_ref <= 1e-8] == 0.0)
+
+
+@pytest.mark.parametrize("per_index", [False, True])
+def test_adam_step_bit_exact_vs_reference(G, ctx, per_index):
+    """Both adam_step overloads (trainer.cpp:40-69) against the reference
+    build, 5 steps: params / m / v bit for bit."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    r = np.random.default_rng(9)
+    n = 1000
+    p0 = r.normal(size=n)
+    lrs = np.abs(r.normal(1e-2, 3e-3, n)) if per_index else None
+    a = [p0.copy(), np.zeros(n), np.zeros(n)]
+    b = [p0.copy(), np.zeros(n), np.zeros(n)]
+    sa, sb = 0, O.C.c_int64(0)
+    for _ in range(5):
+        g = r.normal(size=n) * 1e-3
+        sa = G.adam_step(ctx, a[0], g, a[1], a[2], sa, lrs if per_index else 5e-3)
+        O.ref_lib().ref_adam_step(O._p(b[0]), O._p(g), O._p(b[1]), O._p(b[2]), O.C.byref(sb), n, 5e-3,
+                                  O._p(lrs) if per_index else None)
+    assert sa == sb.value == 5
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)

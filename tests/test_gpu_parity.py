@@ -172,19 +172,43 @@ def test_binning_bit_exact_c2_scale(G, ctx, binning):
     assert np.array_equal(ranges, d["tile_ranges"])
 
 
+MARGIN = 1e-4  # relative decision margin above which FP32 cannot flip a cutoff / termination decision
+
+
+def image_parity_report(name, img, ref_rr, extra=None):
+    """north_star's 1e-5 max-abs on every pixel whose FP64 decisions have a
+    relative margin > MARGIN (oracle decision_margin); the pixels below it are
+    counted and their worst error reported (gpurun_out/image_parity_*.json)."""
+    import json
+    import os
+    err = np.max(np.abs(img - ref_rr.image), axis=2)
+    margin = O.decision_margin(ref_rr)
+    stable = margin > MARGIN
+    rep = {"pixels": int(err.size), "near_decision_pixels": int((~stable).sum()),
+           "max_abs_stable": float(err[stable].max()) if stable.any() else 0.0,
+           "max_abs_near_decision": float(err[~stable].max()) if (~stable).any() else 0.0,
+           "pixels_over_1e-5": int((err > 1e-5).sum()), "worst_pixel": [int(v) for v in np.unravel_index(
+               np.argmax(err), err.shape)], "worst_abs": float(err.max())}
+    rep.update(extra or {})
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open(f"gpurun_out/image_parity_{name}.json", "w") as fh:
+        json.dump(rep, fh)
+    return rep
+
+
 def test_render_c1_scene_image(G, ctx):
-    """C1 (10k Gaussians, 256x256): max-abs over pixels without an FP32
-    decision flip (cutoff / early-termination) <= 1e-5; flips are rare."""
+    """C1 (10k Gaussians SH-3, 256x256): <= 1e-5 max-abs on every pixel whose
+    FP64 cutoff / termination decisions have a relative margin > 1e-4; the
+    near-decision pixels are a fraction of a percent and reported."""
     hc, poses = synth_scene(99, 10000, 256, scale_offset=math.log(500 / 10000) / 3)
     cam = O.synth_camera(256, 256, poses[0])
     cloud = to_dev(G, ctx, hc)
     d = G.render(ctx, cloud, dev_cam(G, cam)).download()
-    ref = O.render(hc, cam)
-    diff = np.max(np.abs(d["image"] - ref.image), axis=2).reshape(-1)
-    same_decisions = d["contrib_count"] == ref.contrib_count
-    assert np.mean(same_decisions) > 0.99
-    assert np.max(diff[same_decisions]) < 1e-4
-    assert np.mean(diff < 1e-5) > 0.99
+    ref = O.render(hc, cam, keep_handle=True)
+    rep = image_parity_report("c1", d["image"], ref)
+    ref.free()
+    assert rep["max_abs_stable"] < 1e-5, rep
+    assert rep["near_decision_pixels"] < 0.01 * rep["pixels"], rep
 
 
 def test_empty_cloud_and_culling(G, ctx):
@@ -268,8 +292,9 @@ def test_rgb_loss_matches_oracle(G, ctx):
     b = np.clip(a + r.uniform(-0.2, 0.2, a.shape), 0, 1).astype(np.float32).astype(np.float64)
     loss, d = G.rgb_loss(ctx, a, b, 0.2)
     lref, dref = O.rgb_loss(a, b, 0.2)
-    assert abs(loss - lref) < 1e-10
-    assert np.max(np.abs(d - dref)) < 1e-6 * np.max(np.abs(dref))
+    # K6: FP32 separable convolutions, FP64 pointwise terms and sums
+    assert abs(loss - lref) < 1e-7 * abs(lref)
+    assert np.max(np.abs(d - dref)) < 1e-4 * np.max(np.abs(dref))
     same, ds = G.rgb_loss(ctx, a, a, 0.2)
     assert same == 0.0 and np.all(ds == 0.0)  # test_losses.cpp:25-32
     l0 = G.rgb_loss(ctx, np.full((16, 16, 3), 0.6), np.full((16, 16, 3), 0.5), 0.0, want_grad=False)
@@ -401,15 +426,16 @@ def test_backward_c3_scale_pose_gradient(G, ctx):
     ref = O.render(hc, ocam, keep_handle=True)
     _, d_img = O.rgb_loss(ref.image, target, 0.2)
     gr = O.render_backward(hc, ocam, ref, d_img)
-    ref.free()
     cloud = G.Cloud(ctx, bench.N_GAUSS, bench.SH_DEGREE)
     cloud.synth(bench.SCENE_SEED, bench.log_scale_offset(bench.N_GAUSS))
     cam = G.Camera.from_pose12(*intr, bench.WIDTH, bench.HEIGHT, init[0])
     out = G.render(ctx, cloud, cam)
-    err = np.max(np.abs(out.image - ref.image), axis=2)
-    assert np.mean(err < 1e-5) > 0.99, np.mean(err < 1e-5)
+    rep = image_parity_report("c3", out.image, ref)
+    assert rep["max_abs_stable"] < 1e-5, rep
+    assert rep["near_decision_pixels"] < 0.01 * rep["pixels"], rep
     _, dp = G.render_backward(ctx, cloud, cam, out, d_img, pose_only=True)
     rel = np.linalg.norm(dp - gr.d_pose) / np.linalg.norm(gr.d_pose)
+    ref.free()
     assert rel < 1e-3, rel
 
 
