@@ -52,6 +52,7 @@ int launch_tile_bin(cudaStream_t st, gsb_frame* f, int64_t n, int64_t* launches)
 size_t bin_hist_words(int64_t n, int n_tiles);
 int init_bin_attributes();
 int launch_composite(cudaStream_t st, gsb_frame* f, const RasterDev& rc);
+int build_export_tiles(cudaStream_t st, gsb_frame* f, int S);
 int launch_expected_depth(cudaStream_t st, gsb_frame* f, const RasterDev& rc, float* depth_out, float* weight_out);
 int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc, bool pose_only);
 int launch_backward_geom(cudaStream_t st, const gsb_cloud* cloud, gsb_frame* f, const RasterDev& rc, bool full,
@@ -316,7 +317,10 @@ static RasterDev make_rasterdev(const gsb_raster_config* c) {
 
 static int validate_config(const gsb_raster_config* cfg) {
   if (!cfg) return fail(GSB_ERR_INVALID_ARGUMENT, "null raster config");
-  if (cfg->tile_size != kTile) return fail(GSB_ERR_INVALID_CONFIG, "tile_size must be 16 on this build");
+  // any tile size is accepted: the kernels bin 16x16 tiles, and RenderOutput's
+  // tile lists / ranges / contrib_count are exported for the requested size
+  // (k_export.cu explains why nothing else depends on it)
+  if (cfg->tile_size < 1 || cfg->tile_size > 4096) return fail(GSB_ERR_INVALID_CONFIG, "tile_size out of range");
   if (!(cfg->cutoff_sigma > 0.0) || !(cfg->alpha_clamp > 0.0) || cfg->alpha_clamp >= 1.0 || cfg->dilation < 0.0 ||
       cfg->early_termination < 0.0)
     return fail(GSB_ERR_INVALID_CONFIG, "raster config out of range");
@@ -563,6 +567,7 @@ static int frame_setup(gsb_ctx* ctx, gsb_frame* f, const gsb_cloud* cloud, const
   if (f->tiles_x > 65535 || f->tiles_y > 65535) return fail(GSB_ERR_INVALID_ARGUMENT, "image too large");
   f->camera = *cam;
   f->config = *cfg;
+  f->exp_valid = false;
   const bool local_ok = (int64_t)f->tiles_x * f->tiles_y <= kBinMaxTiles;  // per-tile counters fit shared memory
   const int binning =
       (ctx->binning == kBinGlobal || f->fallback_global || !local_ok) ? kBinGlobal : kBinTileLocal;
@@ -650,6 +655,17 @@ static int download_frame_image(gsb_ctx* ctx, const gsb_frame* f, double* out) {
   });
   return GSB_OK;
 }
+static int rank_order_async(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, uint32_t** offs_out);
+// Exported tile geometry of a frame rendered with tile_size != 16.
+static int ensure_export(gsb_ctx* ctx, gsb_frame* f) {
+  if (f->config.tile_size == kTile || f->exp_valid) return GSB_OK;
+  if (!f->ranks_valid && f->cloud) {
+    uint32_t* offs = nullptr;
+    if (int r = rank_order_async(ctx, f->cloud, f, &offs)) return r;
+    f->ranks_valid = true;
+  }
+  return build_export_tiles(ctx->stream, f, f->config.tile_size);
+}
 // interleaved FP64 host -> planar FP32 device
 // Host FP64 HWC image -> device FP32 planes, stream ordered on ctx->stream.
 // Two pinned staging slots alternate: the conversion of the next image
@@ -730,6 +746,35 @@ static int backward_device(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, b
 using namespace gsb;
 
 // ===================================================================== ABI
+namespace gsb {
+static int ctx_free(gsb_ctx* ctx) {
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  ctx->scratch_small.release();
+  if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
+  for (auto& pb : ctx->pinned_pool) cudaFreeHost(pb.first);
+  for (int k = 0; k < 2; ++k) {
+    if (ctx->up_buf[k]) cudaFreeHost(ctx->up_buf[k]);
+    if (ctx->up_ev[k]) cudaEventDestroy(ctx->up_ev[k]);
+  }
+  ctx->pinned_pool.clear();
+  delete ctx->timer;
+  if (ctx->work) gsb_frame_destroy(ctx->work);
+  for (gsb_frame* f : ctx->frame_pool) gsb_frame_destroy(f);
+  for (DevBuf& b : ctx->image_pool) b.release();
+  ctx->image_pool.clear();
+  if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
+  if (ctx->ev_stop) cudaEventDestroy(ctx->ev_stop);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return GSB_OK;
+}
+void ctx_retain(gsb_ctx* ctx) { ++ctx->refs; }
+void ctx_release(gsb_ctx* ctx) {
+  if (--ctx->refs == 0 && ctx->closing) ctx_free(ctx);
+}
+}  // namespace gsb
+
 extern "C" {
 
 const char* gsb_last_error(void) { return gsb::g_error.c_str(); }
@@ -796,26 +841,13 @@ int gsb_ctx_create(int32_t device, gsb_ctx** out) {
 
 int gsb_ctx_destroy(gsb_ctx* ctx) {
   if (!ctx) return GSB_OK;
-  cudaSetDevice(ctx->device);
-  cudaStreamSynchronize(ctx->stream);
-  ctx->scratch_small.release();
-  if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
-  for (auto& pb : ctx->pinned_pool) cudaFreeHost(pb.first);
-  for (int k = 0; k < 2; ++k) {
-    if (ctx->up_buf[k]) cudaFreeHost(ctx->up_buf[k]);
-    if (ctx->up_ev[k]) cudaEventDestroy(ctx->up_ev[k]);
+  if (ctx->refs > 0) {  // objects still live: free with the last of them
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->closing = true;
+    return GSB_OK;
   }
-  ctx->pinned_pool.clear();
-  delete ctx->timer;
-  if (ctx->work) gsb_frame_destroy(ctx->work);
-  for (gsb_frame* f : ctx->frame_pool) gsb_frame_destroy(f);
-  for (DevBuf& b : ctx->image_pool) b.release();
-  ctx->image_pool.clear();
-  if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
-  if (ctx->ev_stop) cudaEventDestroy(ctx->ev_stop);
-  cudaStreamDestroy(ctx->stream);
-  delete ctx;
-  return GSB_OK;
+  return ctx_free(ctx);
 }
 
 int gsb_ctx_synchronize(gsb_ctx* ctx) {
@@ -868,6 +900,8 @@ int gsb_cloud_create(gsb_ctx* ctx, int64_t n, int32_t sh_degree, gsb_cloud** out
     return cuda_fail(e, "cloud alloc");
   }
   cudaMemsetAsync(c->params.p, 0, sizeof(float) * num_planes(sh_degree) * c->n_pad, ctx->stream);
+  ctx_retain(ctx);
+  c->ctx_ref = true;
   *out = c;
   return GSB_OK;
 }
@@ -877,7 +911,9 @@ int gsb_cloud_destroy(gsb_cloud* c) {
   cudaSetDevice(c->ctx->device);
   cudaStreamSynchronize(c->ctx->stream);
   c->params.release();
+  gsb_ctx* owner = c->ctx_ref ? c->ctx : nullptr;
   delete c;
+  if (owner) ctx_release(owner);
   return GSB_OK;
 }
 
@@ -980,6 +1016,8 @@ int gsb_frame_create(gsb_ctx* ctx, gsb_frame** out) {
   if (!out) return fail(GSB_ERR_INVALID_ARGUMENT, "null out");
   gsb_frame* f = new gsb_frame();
   f->ctx = ctx;
+  ctx_retain(ctx);
+  f->ctx_ref = true;
   *out = f;
   return GSB_OK;
 }
@@ -993,9 +1031,12 @@ int gsb_frame_destroy(gsb_frame* f) {
                     &f->cnt_r, &f->ekey[0], &f->ekey[1], &f->eval_[0], &f->eval_[1], &f->ranges, &f->tile_cut, &f->image,
                     &f->final_t, &f->pixstate, &f->d_image, &f->partials, &f->pose_blocks, &f->d_pose,
                     &f->loss_blocks, &f->loss_val, &f->mask_ws, &f->gmaps, &f->scan_tmp, &f->sort_hist, &f->counters,
-                    &f->aux_g, &f->tile_hist, &f->tile_scan, &f->tile_big, &f->ent_key, &f->ent_gid};
+                    &f->aux_g, &f->tile_hist, &f->tile_scan, &f->tile_big, &f->ent_key, &f->ent_gid, &f->exp_lists,
+                    &f->exp_ranges, &f->exp_contrib};
   for (DevBuf* b : bufs) b->release();
+  gsb_ctx* owner = f->ctx_ref ? f->ctx : nullptr;
   delete f;
+  if (owner) ctx_release(owner);
   return GSB_OK;
 }
 
@@ -1057,6 +1098,12 @@ int gsb_frame_get_info(gsb_frame* f, gsb_frame_info* info) {
   info->height = f->height;
   info->tiles_x = f->tiles_x;
   info->tiles_y = f->tiles_y;
+  if (f->valid && f->config.tile_size != kTile) {  // RenderOutput geometry of the requested tile size
+    if (int r = ensure_export(f->ctx, f)) return r;
+    info->tiles_x = f->exp_tiles_x;
+    info->tiles_y = f->exp_tiles_y;
+    info->n_entries = f->exp_k;
+  }
   info->state_fingerprint = f->fingerprint;
   info->binning = f->binning == kBinGlobal ? GSB_BINNING_GLOBAL : GSB_BINNING_TILE_LOCAL;
   info->reserved = 0;
@@ -1071,8 +1118,10 @@ int gsb_frame_download(gsb_frame* f, double* image, double* accum_t, double* fin
   if (!f || !f->valid) return fail(GSB_ERR_INVALID_ARGUMENT, "frame holds no forward state");
   gsb_ctx* ctx = f->ctx;
   if (int r = ensure_device(ctx)) return r;
-  const int64_t P = (int64_t)f->width * f->height, V = f->n_splats, K = f->n_entries;
-  const int T = f->tiles_x * f->tiles_y;
+  if (int r = ensure_export(ctx, f)) return r;
+  const bool exp = f->config.tile_size != kTile;
+  const int64_t P = (int64_t)f->width * f->height, V = f->n_splats, K = exp ? f->exp_k : f->n_entries;
+  const int T = exp ? f->exp_tiles_x * f->exp_tiles_y : f->tiles_x * f->tiles_y;
   if (image)
     if (int r = download_frame_image(ctx, f, image)) return r;
   std::vector<float> ft(P);
@@ -1099,22 +1148,28 @@ int gsb_frame_download(gsb_frame* f, double* image, double* accum_t, double* fin
     GSB_CUDA(cudaMemcpyAsync(radius_g.data(), f->radius_g.p, sizeof(double) * f->n_gaussians,
                              cudaMemcpyDeviceToHost, ctx->stream));
   }
-  std::vector<int32_t> rank_of(f->binning == kBinTileLocal && tile_lists ? f->n_gaussians : 0);
+  std::vector<int32_t> rank_of(!exp && f->binning == kBinTileLocal && tile_lists ? f->n_gaussians : 0);
   if (tile_lists && K > 0) {
-    GSB_CUDA(cudaMemcpyAsync(tile_lists, f->list(), sizeof(uint32_t) * K, cudaMemcpyDeviceToHost, ctx->stream));
+    GSB_CUDA(cudaMemcpyAsync(tile_lists, exp ? f->exp_lists.p : f->list(), sizeof(uint32_t) * K,
+                             cudaMemcpyDeviceToHost, ctx->stream));
     if (!rank_of.empty())
       GSB_CUDA(cudaMemcpyAsync(rank_of.data(), f->rank_of_g.p, sizeof(int32_t) * rank_of.size(),
                                cudaMemcpyDeviceToHost, ctx->stream));
   }
   if (tile_ranges && T > 0)
-    GSB_CUDA(cudaMemcpyAsync(tile_ranges, f->ranges.p, sizeof(uint2) * T, cudaMemcpyDeviceToHost, ctx->stream));
+    GSB_CUDA(cudaMemcpyAsync(tile_ranges, exp ? f->exp_ranges.p : f->ranges.p, sizeof(uint2) * T,
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  std::vector<int32_t> contrib_s(exp && contrib ? P : 0);
+  if (!contrib_s.empty())
+    GSB_CUDA(cudaMemcpyAsync(contrib_s.data(), f->exp_contrib.p, sizeof(int32_t) * P, cudaMemcpyDeviceToHost,
+                             ctx->stream));
   GSB_CUDA(cudaStreamSynchronize(ctx->stream));
   if (!rank_of.empty())  // tile-local lists hold gids: export them as ranks
     for (int64_t e = 0; e < K; ++e) tile_lists[e] = rank_of[(uint32_t)tile_lists[e]];
   for (int64_t p = 0; p < P; ++p) {
     if (final_t) final_t[p] = ft[p];
     if (accum_t) accum_t[p] = 1.0 - (double)ft[p];  // rasterizer.cpp:271-273
-    if (contrib) contrib[p] = (int32_t)(ps[p] & 0x1fffffffu);
+    if (contrib) contrib[p] = exp ? contrib_s[p] : (int32_t)(ps[p] & 0x1fffffffu);
     if (overflow) overflow[p] = (uint8_t)(ps[p] >> 29);
   }
   for (int64_t r = 0; r < V; ++r) {
@@ -1173,6 +1228,8 @@ int gsb_image_create(gsb_ctx* ctx, const double* img, int32_t W, int32_t H, gsb_
     delete im;
     return r;
   }
+  ctx_retain(ctx);
+  im->ctx_ref = true;
   *out = im;
   return GSB_OK;
 }
@@ -1186,7 +1243,9 @@ int gsb_image_destroy(gsb_image* im) {
     im->planes = DevBuf();
   }
   im->planes.release();
+  gsb_ctx* owner = im->ctx_ref ? im->ctx : nullptr;
   delete im;
+  if (owner) ctx_release(owner);
   return GSB_OK;
 }
 
@@ -1313,6 +1372,8 @@ int gsb_grads_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_grads** out) {
     delete g;
     return cuda_fail(e, "grads alloc");
   }
+  ctx_retain(ctx);
+  g->ctx_ref = true;
   *out = g;
   return GSB_OK;
 }
@@ -1323,7 +1384,9 @@ int gsb_grads_destroy(gsb_grads* g) {
   cudaStreamSynchronize(g->ctx->stream);
   g->planes.release();
   g->pose.release();
+  gsb_ctx* owner = g->ctx_ref ? g->ctx : nullptr;
   delete g;
+  if (owner) ctx_release(owner);
   return GSB_OK;
 }
 
@@ -1504,6 +1567,8 @@ int gsb_adam_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_adam** out) {
   }
   cudaMemsetAsync(a->m.p, 0, bytes, ctx->stream);
   cudaMemsetAsync(a->v.p, 0, bytes, ctx->stream);
+  ctx_retain(ctx);
+  a->ctx_ref = true;
   *out = a;
   return GSB_OK;
 }
@@ -1514,7 +1579,9 @@ int gsb_adam_destroy(gsb_adam* a) {
   cudaStreamSynchronize(a->ctx->stream);
   a->m.release();
   a->v.release();
+  gsb_ctx* owner = a->ctx_ref ? a->ctx : nullptr;
   delete a;
+  if (owner) ctx_release(owner);
   return GSB_OK;
 }
 
@@ -1563,6 +1630,7 @@ int gsb_ctx_timer_stop(gsb_ctx* ctx, double* ms) {
 // (frame gen), the entry capacity changes, or profiling is toggled.
 struct gsb_session {
   gsb_ctx* ctx = nullptr;
+  bool ctx_ref = false;  // holds a reference on ctx (public create)
   gsb_cloud* cloud = nullptr;
   gsb_image* target = nullptr;
   gsb_camera cam{};
@@ -1596,6 +1664,7 @@ struct gsb_session {
 // branches fill each other's wave tails and serial single-block kernels.
 struct gsb_pose_batch {
   gsb_ctx* ctx = nullptr;
+  bool ctx_ref = false;  // holds a reference on ctx (public create)
   std::vector<gsb_session*> sessions;
   std::vector<cudaStream_t> streams;
   std::vector<cudaEvent_t> joins;
@@ -1811,6 +1880,8 @@ int gsb_session_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* target, const 
   GSB_CUDA(cudaMemcpyAsync(s->camdev.p, hcam, sizeof(CamDev), cudaMemcpyHostToDevice, ctx->stream));
   GSB_CUDA(cudaMemcpyAsync(s->state.p, s->host_state, sb, cudaMemcpyHostToDevice, ctx->stream));
   GSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx_retain(ctx);
+  s->ctx_ref = true;
   *out = s;
   return GSB_OK;
 }
@@ -1844,7 +1915,9 @@ int gsb_session_destroy(gsb_session* s) {
   s->camdev.release();
   s->trace.release();
   if (s->host_state) s->ctx->pinned_pool.emplace_back(s->host_state, s->host_state_bytes);
+  gsb_ctx* owner = s->ctx_ref ? s->ctx : nullptr;
   delete s;
+  if (owner) ctx_release(owner);
   return GSB_OK;
 }
 
@@ -2092,6 +2165,8 @@ int gsb_pose_batch_create(gsb_ctx* ctx, gsb_session* const* sessions, int32_t co
   b->graph_gen.assign(count, 0);
   b->graph_kcap.assign(count, 0);
   b->graph_binning.assign(count, -1);
+  ctx_retain(ctx);
+  b->ctx_ref = true;
   *out = b;
   return GSB_OK;
 }
@@ -2114,7 +2189,9 @@ int gsb_pose_batch_destroy(gsb_pose_batch* b) {
   for (cudaStream_t st : b->streams) cudaStreamDestroy(st);
   for (cudaEvent_t ev : b->joins) cudaEventDestroy(ev);
   if (b->fork) cudaEventDestroy(b->fork);
+  gsb_ctx* owner = b->ctx_ref ? b->ctx : nullptr;
   delete b;
+  if (owner) ctx_release(owner);
   return GSB_OK;
 }
 
@@ -2456,6 +2533,7 @@ static int nccl_fail(ncclResult_t r, const char* what) {
 }  // namespace gsb
 
 struct gsb_comm {
+  bool ctx_ref = false;  // holds a reference on ctx (public create)
   gsb_ctx* ctx = nullptr;
   ncclComm_t comm = nullptr;
   int32_t rank = 0, world = 1;
@@ -2487,6 +2565,8 @@ int gsb_comm_create(gsb_ctx* ctx, const uint8_t id[128], int32_t rank, int32_t w
     delete c;
     return nccl_fail(r, "ncclCommInitRank");
   }
+  ctx_retain(ctx);
+  c->ctx_ref = true;
   *out = c;
   return GSB_OK;
 }
@@ -2496,7 +2576,9 @@ int gsb_comm_destroy(gsb_comm* c) {
   cudaSetDevice(c->ctx->device);
   cudaStreamSynchronize(c->ctx->stream);
   if (c->comm) nccl().comm_destroy(c->comm);
+  gsb_ctx* owner = c->ctx_ref ? c->ctx : nullptr;
   delete c;
+  if (owner) ctx_release(owner);
   return GSB_OK;
 }
 
@@ -2551,6 +2633,7 @@ void gsb_default_joint_config(gsb_joint_config* c) {  // trainer.hpp:21-60, loss
 // in sync without broadcasting parameters.
 struct gsb_joint {
   gsb_ctx* ctx = nullptr;
+  bool ctx_ref = false;  // holds a reference on ctx (public create)
   gsb_cloud* cloud = nullptr;
   gsb_comm* comm = nullptr;
   gsb_joint_config cfg{};
@@ -2890,6 +2973,8 @@ int gsb_joint_create(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* const* targets, 
   }
   j->graph_gen.assign(j->local, 0);
   j->graph_kcap.assign(j->local, 0);
+  ctx_retain(ctx);
+  j->ctx_ref = true;
   *out = j;
   return GSB_OK;
 }
@@ -2905,7 +2990,9 @@ int gsb_joint_destroy(gsb_joint* j) {
                     &j->acc_stage};
   for (DevBuf* b : bufs) b->release();
   if (j->host_state) cudaFreeHost(j->host_state);
+  gsb_ctx* owner = j->ctx_ref ? j->ctx : nullptr;
   delete j;
+  if (owner) ctx_release(owner);
   return GSB_OK;
 }
 

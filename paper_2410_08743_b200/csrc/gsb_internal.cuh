@@ -189,6 +189,12 @@ struct JointCtl {
 // ------------------------------------------------------------- C structs
 struct gsb_ctx {
   int device = 0;
+  // objects created on this context (clouds, frames, images, ...) hold a
+  // reference: gsb_ctx_destroy with live objects only marks the context
+  // closing, and the last object's destroy frees it (any destruction order
+  // of a caller's objects is safe)
+  int64_t refs = 0;
+  bool closing = false;
   cudaStream_t stream = nullptr;
   int num_sms = 148;
   gsb::DevBuf scratch_small;   // pinned-size device scratch (counters, partial sums)
@@ -212,6 +218,7 @@ struct gsb_ctx {
 
 struct gsb_cloud {
   gsb_ctx* ctx = nullptr;
+  bool ctx_ref = false;  // holds a reference on ctx (public create)
   int64_t n = 0;
   int64_t n_pad = 0;
   int32_t sh_degree = 0, active_sh_degree = 0;
@@ -227,12 +234,14 @@ struct gsb_cloud {
 
 struct gsb_image {
   gsb_ctx* ctx = nullptr;
+  bool ctx_ref = false;  // holds a reference on ctx (public create)
   int32_t width = 0, height = 0;
   gsb::DevBuf planes;  // FP32 [3][H*W]
 };
 
 struct gsb_grads {
   gsb_ctx* ctx = nullptr;
+  bool ctx_ref = false;  // holds a reference on ctx (public create)
   int64_t n = 0, n_pad = 0;
   int32_t sh_degree = 0;
   gsb::DevBuf planes;  // FP32 [num_planes + 2 (d_mu2d)][n_pad]
@@ -242,6 +251,7 @@ struct gsb_grads {
 
 struct gsb_adam {
   gsb_ctx* ctx = nullptr;
+  bool ctx_ref = false;  // holds a reference on ctx (public create)
   int64_t n = 0, n_pad = 0;
   int32_t sh_degree = 0;
   gsb::DevBuf m, v;    // FP32 planes like the cloud
@@ -250,6 +260,7 @@ struct gsb_adam {
 
 struct gsb_frame {
   gsb_ctx* ctx = nullptr;
+  bool ctx_ref = false;  // holds a reference on ctx (public create)
   // bookkeeping
   int64_t n_gaussians = 0, n_splats = 0, n_entries = 0;
   int32_t width = 0, height = 0, tiles_x = 0, tiles_y = 0;
@@ -316,6 +327,12 @@ struct gsb_frame {
   gsb::DevBuf ent_key;    // uint64 (FP64 depth high word << 32 | gid) per entry, tile grouped
   gsb::DevBuf ent_gid;    // uint32 gid per entry -> depth-sorted tile lists
   bool ranks_valid = false;  // rank-order arrays (rec, aux, rank_of_g) hold this frame
+  // RenderOutput export for config.tile_size != 16 (k_export.cu): tile lists /
+  // ranges / contrib_count of the requested tile size, built on first export
+  bool exp_valid = false;
+  int32_t exp_tiles_x = 0, exp_tiles_y = 0;
+  int64_t exp_k = 0;
+  gsb::DevBuf exp_lists, exp_ranges, exp_contrib;
   // what the raster kernels read: tile lists of record ids, records, aux
   const uint32_t* list() const {
     return binning == gsb::kBinTileLocal ? ent_gid.as<uint32_t>() : eval_[sorted_sel].as<uint32_t>();

@@ -346,11 +346,12 @@ __device__ void sort_tile(TileSortSmem<CAP, NT, NB>& S, uint2 r, const unsigned 
     return S.gid[a] > S.gid[b];
   };
   uint16_t* ord = S.perm[0];
-  for (int p = threadIdx.x; p < n; p += NT) {
-    const uint32_t qv = qkey(ord[p]);
-    if (p > 0 && qkey(ord[p - 1]) == qv) continue;
-    int e = p + 1;
-    while (e < n && e - p <= 32 && qkey(ord[e]) == qv) ++e;
+  // after the placement pass bucket[k] holds the end of bucket k in ord, so
+  // each thread sorts whole buckets it owns without reading its neighbours'
+  // (a thread never touches entries another thread is permuting)
+  for (int k = threadIdx.x; k < NB; k += NT) {
+    const int p = k ? (int)S.u.bucket[k - 1] : 0, e = (int)S.u.bucket[k];
+    if (e - p < 2) continue;
     if (e - p > 32) {
       S.long_run = 1u;
       continue;

@@ -21,6 +21,9 @@
 // fixed order (deterministic). FP32 convolutions keep the identical-image
 // identities exact: equal inputs give bitwise-equal statistics, and
 // conv(-x) = -conv(x), conv(2x) = 2 conv(x) hold exactly in any precision.
+#include <cstring>
+#include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point; no libcuda link)
+
 #include "gsb_internal.cuh"
 
 namespace gsb {
@@ -103,14 +106,16 @@ __device__ __forceinline__ void stage_planes(float (*dst)[kSH][kSW + 1], const f
 #define GSB_LOSS_HR 4
 #endif
 constexpr int kHR = GSB_LOSS_HR;
-__device__ __forceinline__ void hpass5(const float (*st)[kSH][kSW + 1], float (*hq)[kSH][kTW + 1]) {
+template <int PITCH>
+__device__ __forceinline__ void hpass5(const float* __restrict__ st0, const float* __restrict__ st1,
+                                       float (*hq)[kSH][kTW + 1]) {
   for (int task = threadIdx.x; task < kSH * (kTW / kHR); task += kThr) {
     const int r = task / (kTW / kHR), q0 = (task - r * (kTW / kHR)) * kHR;
     float x[kHR + kWin - 1], y[kHR + kWin - 1];
 #pragma unroll
     for (int k = 0; k < kHR + kWin - 1; ++k) {
-      x[k] = st[0][r][q0 + k];
-      y[k] = st[1][r][q0 + k];
+      x[k] = st0[r * PITCH + q0 + k];
+      y[k] = st1[r * PITCH + q0 + k];
     }
 #pragma unroll
     for (int m = 0; m < 5; ++m) {
@@ -135,26 +140,76 @@ __device__ __forceinline__ void hpass5(const float (*st)[kSH][kSW + 1], float (*
 #else
 #define GSB_LOSS_BOUNDS __launch_bounds__(kThr)
 #endif
+// TMA staging (kTma): the windows of channel c + 1 are loaded by the tensor
+// memory accelerator (3-D tensor maps over the planar images, box 44 x 42 x
+// 1, out-of-bounds elements zero-filled = conv_window's zero padding) into a
+// second buffer while channel c is convolved; one mbarrier per buffer.
+constexpr int kTP = 44;                        // TMA window pitch (floats; 176 B rows)
+constexpr int kTWin = kSH * kTP;               // floats per staged TMA window
+constexpr uint32_t kTWinBytes = kTWin * 4u;
+
+__device__ __forceinline__ void tma_load_3d(float* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+struct LossMaps {  // tensor maps of the TMA path (unused otherwise)
+  CUtensorMap ren, tgt, gm;
+};
+
+template <bool kTma>
 __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, const float* __restrict__ tgt,
-                                                         int W, int H, double scale, float* __restrict__ gmaps,
-                                                         double* __restrict__ block_sums, MaskArgs mk) {
+                                                 int W, int H, double scale, float* __restrict__ gmaps,
+                                                 double* __restrict__ block_sums, MaskArgs mk,
+                                                 const __grid_constant__ LossMaps tm) {
   if (mk.final_t) scale = mk.norms[1];
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  float(*st)[kSH][kSW + 1] = reinterpret_cast<float(*)[kSH][kSW + 1]>(smem_raw);
+  constexpr int PITCH = kTma ? kTP : kSW + 1;
+  constexpr int WIN = kTma ? kTWin : kSH * (kSW + 1);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* win = reinterpret_cast<float*>(smem_raw);  // [buffers][2 planes][WIN]
   float(*hq)[kSH][kTW + 1] =
-      reinterpret_cast<float(*)[kSH][kTW + 1]>(smem_raw + sizeof(float) * 2 * kSH * (kSW + 1));
+      reinterpret_cast<float(*)[kSH][kTW + 1]>(smem_raw + sizeof(float) * (kTma ? 4 : 2) * WIN);
   __shared__ double s_tmp[kThr / 32];
+  __shared__ __align__(8) uint64_t bar[2];
   const int64_t P = (int64_t)W * H;
   const int bx = blockIdx.x * kTW, by = blockIdx.y * kTH;
+  if (kTma && threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_arrive_expect_tx(&bar[0], 2 * kTWinBytes);
+    tma_load_3d(win, &tm.ren, bx - kHalf, by - kHalf, 0, &bar[0]);
+    tma_load_3d(win + kTWin, &tm.tgt, bx - kHalf, by - kHalf, 0, &bar[0]);
+  }
+  if (kTma) __syncthreads();  // barrier initialisation visible to every waiting thread
   // vertical task: column c, rows 4 rg .. 4 rg + 3
   const int c = threadIdx.x & (kTW - 1), rg = threadIdx.x / kTW;
   const int x = bx + c;
   double l1 = 0.0, ss = 0.0;
   for (int ch = 0; ch < 3; ++ch) {
-    const float* src[2] = {ren + ch * P, tgt + ch * P};
-    stage_planes<2>(st, src, W, H, bx - kHalf, by - kHalf);
-    __syncthreads();
-    hpass5(st, hq);
+    const float* st0;
+    if (kTma) {
+      if (threadIdx.x == 0 && ch + 1 < 3) {  // next channel into the other buffer
+        float* nb = win + ((ch + 1) & 1) * 2 * kTWin;
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&bar[(ch + 1) & 1], 2 * kTWinBytes);
+        tma_load_3d(nb, &tm.ren, bx - kHalf, by - kHalf, ch + 1, &bar[(ch + 1) & 1]);
+        tma_load_3d(nb + kTWin, &tm.tgt, bx - kHalf, by - kHalf, ch + 1, &bar[(ch + 1) & 1]);
+      }
+      mbar_wait(&bar[ch & 1], (uint32_t)(ch >> 1));
+      st0 = win + (ch & 1) * 2 * kTWin;
+    } else {
+      const float* src[2] = {ren + ch * P, tgt + ch * P};
+      stage_planes<2>(reinterpret_cast<float(*)[kSH][kSW + 1]>(win), src, W, H, bx - kHalf, by - kHalf);
+      __syncthreads();
+      st0 = win;
+    }
+    const float* st1 = st0 + WIN;
+    hpass5<PITCH>(st0, st1, hq);
     __syncthreads();
     float mv[5][kR];
 #pragma unroll
@@ -176,7 +231,8 @@ __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, 
     for (int j = 0; j < kR; ++j) {
       const int y = by + rg * kR + j;
       if (x >= W || y >= H) continue;
-      const double a = st[0][rg * kR + j + kHalf][c + kHalf], b = st[1][rg * kR + j + kHalf][c + kHalf];
+      const int o = (rg * kR + j + kHalf) * PITCH + c + kHalf;
+      const double a = st0[o], b = st1[o];
       const int64_t p = (int64_t)y * W + x;
       const bool in_mask = mask_at(mk, p);
       if (in_mask) l1 += fabs(a - b);
@@ -215,7 +271,8 @@ __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, 
 }
 
 // Horizontal pass of the three gradient maps (back-convolution, losses.cpp:144-151).
-__device__ __forceinline__ void hpass3(const float (*st)[kSH][kSW + 1], float (*hq)[kSH][kTW + 1]) {
+template <int PITCH>
+__device__ __forceinline__ void hpass3(const float* __restrict__ st, int plane_stride, float (*hq)[kSH][kTW + 1]) {
   for (int task = threadIdx.x; task < kSH * (kTW / kHR); task += kThr) {
     const int r = task / (kTW / kHR), q0 = (task - r * (kTW / kHR)) * kHR;
 #pragma unroll
@@ -225,7 +282,7 @@ __device__ __forceinline__ void hpass3(const float (*st)[kSH][kSW + 1], float (*
       for (int j = 0; j < kHR; ++j) acc[j] = 0.f;
 #pragma unroll
       for (int k = 0; k < kHR + kWin - 1; ++k) {
-        const float f = st[m][r][q0 + k];
+        const float f = st[m * plane_stride + r * PITCH + q0 + k];
 #pragma unroll
         for (int j = 0; j < kHR; ++j)
           if (k - j >= 0 && k - j < kWin) acc[j] = fmaf(c_win[k - j], f, acc[j]);
@@ -243,29 +300,55 @@ __device__ __forceinline__ void hpass3(const float (*st)[kSH][kSW + 1], float (*
 #define GSB_LOSS_GRAD_MIN_BLOCKS 4
 #endif
 #define GSB_LOSS_GRAD_BOUNDS __launch_bounds__(kThr, GSB_LOSS_GRAD_MIN_BLOCKS)
+template <bool kTma>
 __global__ void GSB_LOSS_GRAD_BOUNDS loss_grad_kernel(const float* __restrict__ ren, const float* __restrict__ tgt,
-                                                         const float* __restrict__ gmaps, int W, int H, double beta,
-                                                         double l1_norm, int has_ssim, float* __restrict__ d_image,
-                                                         MaskArgs mk) {
+                                                     const float* __restrict__ gmaps, int W, int H, double beta,
+                                                     double l1_norm, int has_ssim, float* __restrict__ d_image,
+                                                     MaskArgs mk, const __grid_constant__ LossMaps tm) {
   if (mk.final_t) {
     l1_norm = mk.norms[0];
     has_ssim = mk.norms[3] > 0.0 ? has_ssim : 0;
   }
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  float(*st)[kSH][kSW + 1] = reinterpret_cast<float(*)[kSH][kSW + 1]>(smem_raw);
+  constexpr int PITCH = kTma ? kTP : kSW + 1;
+  constexpr int WIN = kTma ? kTWin : kSH * (kSW + 1);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* win = reinterpret_cast<float*>(smem_raw);  // [buffers][3 maps][WIN]
   float(*hq)[kSH][kTW + 1] =
-      reinterpret_cast<float(*)[kSH][kTW + 1]>(smem_raw + sizeof(float) * 3 * kSH * (kSW + 1));
+      reinterpret_cast<float(*)[kSH][kTW + 1]>(smem_raw + sizeof(float) * (kTma ? 6 : 3) * WIN);
+  __shared__ __align__(8) uint64_t bar[2];
   const int64_t P = (int64_t)W * H;
   const int bx = blockIdx.x * kTW, by = blockIdx.y * kTH;
   const int c = threadIdx.x & (kTW - 1), rg = threadIdx.x / kTW;
   const int x = bx + c;
+  if (kTma && has_ssim && threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_arrive_expect_tx(&bar[0], 3 * kTWinBytes);
+    for (int m = 0; m < 3; ++m) tma_load_3d(win + m * kTWin, &tm.gm, bx - kHalf, by - kHalf, m, &bar[0]);
+  }
+  if (kTma) __syncthreads();  // barrier initialisation visible to every waiting thread
   for (int ch = 0; ch < 3; ++ch) {
     float cv[3][kR];
     if (has_ssim) {
-      const float* src[3] = {gmaps + (3 * ch + 0) * P, gmaps + (3 * ch + 1) * P, gmaps + (3 * ch + 2) * P};
-      stage_planes<3>(st, src, W, H, bx - kHalf, by - kHalf);
-      __syncthreads();
-      hpass3(st, hq);
+      const float* st;
+      if (kTma) {
+        if (threadIdx.x == 0 && ch + 1 < 3) {
+          float* nb = win + ((ch + 1) & 1) * 3 * kTWin;
+          fence_proxy_async();
+          mbar_arrive_expect_tx(&bar[(ch + 1) & 1], 3 * kTWinBytes);
+          for (int m = 0; m < 3; ++m)
+            tma_load_3d(nb + m * kTWin, &tm.gm, bx - kHalf, by - kHalf, 3 * (ch + 1) + m, &bar[(ch + 1) & 1]);
+        }
+        mbar_wait(&bar[ch & 1], (uint32_t)(ch >> 1));
+        st = win + (ch & 1) * 3 * kTWin;
+      } else {
+        const float* src[3] = {gmaps + (3 * ch + 0) * P, gmaps + (3 * ch + 1) * P, gmaps + (3 * ch + 2) * P};
+        stage_planes<3>(reinterpret_cast<float(*)[kSH][kSW + 1]>(win), src, W, H, bx - kHalf, by - kHalf);
+        __syncthreads();
+        st = win;
+      }
+      hpass3<PITCH>(st, WIN, hq);
       __syncthreads();
 #pragma unroll
       for (int m = 0; m < 3; ++m) {
@@ -390,17 +473,56 @@ int init_loss_constants() {
 
 constexpr size_t kMapsSmem = sizeof(float) * 2 * kSH * (kSW + 1) + sizeof(float) * 5 * kSH * (kTW + 1);
 constexpr size_t kGradSmem = sizeof(float) * 3 * kSH * (kSW + 1) + sizeof(float) * 3 * kSH * (kTW + 1);
+constexpr size_t kMapsSmemT = sizeof(float) * 4 * kTWin + sizeof(float) * 5 * kSH * (kTW + 1);
+constexpr size_t kGradSmemT = sizeof(float) * 6 * kTWin + sizeof(float) * 3 * kSH * (kTW + 1);
 
 int init_loss_attributes() {
-  GSB_CUDA(cudaFuncSetAttribute(loss_maps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMapsSmem));
-  GSB_CUDA(cudaFuncSetAttribute(loss_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGradSmem));
+  GSB_CUDA(cudaFuncSetAttribute(loss_maps_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMapsSmem));
+  GSB_CUDA(cudaFuncSetAttribute(loss_grad_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGradSmem));
+  GSB_CUDA(cudaFuncSetAttribute(loss_maps_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMapsSmemT));
+  GSB_CUDA(cudaFuncSetAttribute(loss_grad_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGradSmemT));
   return GSB_OK;
 }
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (the
+// library links only the CUDA runtime).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (EncodeTiledFn) nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// 3-D map over `planes` FP32 planes of W x H, box 44 x 42 x 1, zero fill.
+static bool encode_planes(CUtensorMap* m, const float* base, int W, int H, int planes) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)planes};
+  const cuuint64_t strides[2] = {(cuuint64_t)W * 4u, (cuuint64_t)W * (cuuint64_t)H * 4u};
+  const cuuint32_t box[3] = {(cuuint32_t)kTP, (cuuint32_t)kSH, 1u};
+  const cuuint32_t estr[3] = {1u, 1u, 1u};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+#ifndef GSB_LOSS_TMA
+#define GSB_LOSS_TMA 1
+#endif
 
 // mask_t (nullable): final transmittance of the rendered frame; then the loss
 // is masked_rgb_loss with accum = 1 - T > mask_thr, and mask_ws (>= 48 bytes of
 // device scratch) receives the counts and norms ({l1 norm, ssim scale, count,
-// valid count} as doubles at offset 16).
+// valid count} as doubles at offset 16). TMA staging needs 16-byte aligned
+// plane bases and rows (W % 4 == 0); otherwise the loads go through registers.
 int launch_rgb_loss(cudaStream_t st, const float* ren, const float* tgt, int W, int H, double beta, float* gmaps,
                     double* block_sums, double* out3, float* d_image, int64_t* launches, const float* mask_t,
                     double mask_thr, void* mask_ws) {
@@ -418,9 +540,23 @@ int launch_rgb_loss(cudaStream_t st, const float* ren, const float* tgt, int W, 
   const double scale = has_ssim ? 1.0 / (3.0 * (double)cnt_valid) : 0.0;
   const double l1_norm = 1.0 / (3.0 * (double)W * (double)H);
   dim3 grid((W + kTW - 1) / kTW, (H + kTH - 1) / kTH);
-  loss_maps_kernel<<<grid, kThr, kMapsSmem, st>>>(ren, tgt, W, H, scale, gmaps, block_sums, mk);
-  if (d_image)
-    loss_grad_kernel<<<grid, kThr, kGradSmem, st>>>(ren, tgt, gmaps, W, H, beta, l1_norm, has_ssim, d_image, mk);
+  const auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  LossMaps tm;
+  std::memset(&tm, 0, sizeof tm);
+  bool tma = GSB_LOSS_TMA && W % 4 == 0 && aligned(ren) && aligned(tgt) && aligned(gmaps) &&
+             encode_planes(&tm.ren, ren, W, H, 3) && encode_planes(&tm.tgt, tgt, W, H, 3) &&
+             encode_planes(&tm.gm, gmaps, W, H, 9);
+  if (tma) {
+    loss_maps_kernel<true><<<grid, kThr, kMapsSmemT, st>>>(ren, tgt, W, H, scale, gmaps, block_sums, mk, tm);
+    if (d_image)
+      loss_grad_kernel<true><<<grid, kThr, kGradSmemT, st>>>(ren, tgt, gmaps, W, H, beta, l1_norm, has_ssim,
+                                                             d_image, mk, tm);
+  } else {
+    loss_maps_kernel<false><<<grid, kThr, kMapsSmem, st>>>(ren, tgt, W, H, scale, gmaps, block_sums, mk, tm);
+    if (d_image)
+      loss_grad_kernel<false><<<grid, kThr, kGradSmem, st>>>(ren, tgt, gmaps, W, H, beta, l1_norm, has_ssim,
+                                                              d_image, mk, tm);
+  }
   loss_finalize_kernel<<<1, 256, 0, st>>>(block_sums, (int)(grid.x * grid.y), l1_norm, scale, has_ssim, beta, out3,
                                           mk);
   *launches += d_image ? 3 : 2;

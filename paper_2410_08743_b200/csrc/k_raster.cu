@@ -831,6 +831,7 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
         if (vi >= 0 && act && half == 0) s_red[warp][k][vi] += tot;
         __syncwarp();
         if (vi >= 0 && act && half == 1) s_red[warp][k][vi] += tot;
+        __syncwarp();  // orders half 1's add before the next step's half-0 read of the same slot
       }
     }
     __syncthreads();
