@@ -145,8 +145,8 @@ __device__ __forceinline__ void hpass5(const float* __restrict__ st0, const floa
 // 1, out-of-bounds elements zero-filled = conv_window's zero padding) into a
 // second buffer while channel c is convolved; one mbarrier per buffer.
 constexpr int kTP = 44;                        // TMA window pitch (floats; 176 B rows)
-constexpr int kTWin = kSH * kTP;               // floats per staged TMA window
-constexpr uint32_t kTWinBytes = kTWin * 4u;
+constexpr uint32_t kTWinBytes = kSH * kTP * 4u;  // bytes one TMA window load delivers
+constexpr int kTWin = (kSH * kTP + 31) / 32 * 32;  // window stride in shared memory: 128-byte aligned destinations
 
 __device__ __forceinline__ void tma_load_3d(float* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
   asm volatile(

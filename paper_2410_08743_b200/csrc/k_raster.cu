@@ -738,6 +738,19 @@ __device__ __forceinline__ int half_reduce9(const float v[9], float* out) {
   return (xi < 3 && wi < 5 && vi < 9) ? vi : -1;
 }
 
+// cp.async (LDGSTS) staging for K4a (GSB_BWD_CPASYNC=1, off by default — see
+// profiles/README.md for the A/B): the next batch's raw records (48 B
+// SplatRec + 16 B SplatAux per entry, gathered by rank) are copied into a
+// second shared buffer while the current batch is replayed.
+#ifndef GSB_BWD_CPASYNC
+#define GSB_BWD_CPASYNC 0
+#endif
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 template <int NC>
 __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_half_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ ranks, const SplatRec* __restrict__ rec,
@@ -790,9 +803,45 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
   }
   const uint32_t len = min(range.y - range.x, maxc);
   const uint32_t nbatch = (len + kBatch - 1) / kBatch;
+#if GSB_BWD_CPASYNC
+  __shared__ __align__(16) SplatRec s_raw[2][kBatch];
+  __shared__ __align__(16) SplatAux s_rawx[2][kBatch];
+  auto issue = [&](int bj, int buf, uint32_t r) {
+    const uint32_t bb = (uint32_t)bj * kBatch;
+    if (threadIdx.x < min((uint32_t)kBatch, len - bb)) {
+      const char* src = reinterpret_cast<const char*>(rec + r);
+      char* dst = reinterpret_cast<char*>(&s_raw[buf][threadIdx.x]);
+      cp_async16(dst, src);
+      cp_async16(dst + 16, src + 16);
+      cp_async16(dst + 32, src + 32);
+      cp_async16(&s_rawx[buf][threadIdx.x], aux + r);
+    }
+    cp_async_commit();
+  };
+  auto rank_of = [&](int bj) -> uint32_t {
+    const uint32_t bb = (uint32_t)bj * kBatch;
+    return (bj >= 0 && threadIdx.x < min((uint32_t)kBatch, len - bb)) ? ranks[range.x + bb + threadIdx.x] : 0u;
+  };
+  if (nbatch > 0) issue((int)nbatch - 1, 0, rank_of((int)nbatch - 1));
+#endif
   for (int bi = (int)nbatch - 1; bi >= 0; --bi) {
     const uint32_t b0 = (uint32_t)bi * kBatch;  // list-local start
     const int cnt = (int)min((uint32_t)kBatch, len - b0);
+#if GSB_BWD_CPASYNC
+    const int buf = ((int)nbatch - 1 - bi) & 1;
+    const uint32_t r_next = rank_of(bi - 1);  // issued now, used after this batch's staging
+    cp_async_wait_all();
+    __syncthreads();
+    if (threadIdx.x < cnt) {
+      const SplatAux A = s_rawx[buf][threadIdx.x];
+      const uint32_t tx0 = A.tx0_ty0 & 0xffffu, ty0 = A.tx0_ty0 >> 16, nx = A.nx_ny & 0xffffu;
+      StagedSplat& S = s_sp[threadIdx.x];
+      S.slot = A.off + ((uint32_t)ty - ty0) * nx + ((uint32_t)tx - tx0);
+      s_mask[threadIdx.x] =
+          (uint8_t)half_mask(stage_splat(s_raw[buf][threadIdx.x], ox, oy, rc.cutoff2_f, &S.geo, &S.app, &S.col_b));
+    }
+    if (bi > 0) issue(bi - 1, buf ^ 1, r_next);
+#else
     if (threadIdx.x < cnt) {
       const uint32_t e = range.x + b0 + threadIdx.x;
       const uint32_t r = ranks[e];
@@ -802,6 +851,7 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
       S.slot = A.off + ((uint32_t)ty - ty0) * nx + ((uint32_t)tx - tx0);
       s_mask[threadIdx.x] = (uint8_t)half_mask(stage_splat(rec[r], ox, oy, rc.cutoff2_f, &S.geo, &S.app, &S.col_b));
     }
+#endif
     __syncthreads();
     if (b0 < wmax) {  // this warp has pixels that replay entries of this batch
       int n0, n1;
