@@ -106,7 +106,7 @@ __device__ __forceinline__ void stage_planes(float (*dst)[kSH][kSW + 1], const f
 #define GSB_LOSS_HR 4
 #endif
 constexpr int kHR = GSB_LOSS_HR;
-template <int PITCH>
+template <int PITCH, int XOFF>
 __device__ __forceinline__ void hpass5(const float* __restrict__ st0, const float* __restrict__ st1,
                                        float (*hq)[kSH][kTW + 1]) {
   for (int task = threadIdx.x; task < kSH * (kTW / kHR); task += kThr) {
@@ -114,8 +114,8 @@ __device__ __forceinline__ void hpass5(const float* __restrict__ st0, const floa
     float x[kHR + kWin - 1], y[kHR + kWin - 1];
 #pragma unroll
     for (int k = 0; k < kHR + kWin - 1; ++k) {
-      x[k] = st0[r * PITCH + q0 + k];
-      y[k] = st1[r * PITCH + q0 + k];
+      x[k] = st0[r * PITCH + XOFF + q0 + k];
+      y[k] = st1[r * PITCH + XOFF + q0 + k];
     }
 #pragma unroll
     for (int m = 0; m < 5; ++m) {
@@ -144,8 +144,12 @@ __device__ __forceinline__ void hpass5(const float* __restrict__ st0, const floa
 // memory accelerator (3-D tensor maps over the planar images, box 44 x 42 x
 // 1, out-of-bounds elements zero-filled = conv_window's zero padding) into a
 // second buffer while channel c is convolved; one mbarrier per buffer.
-constexpr int kTP = 44;                        // TMA window pitch (floats; 176 B rows)
-constexpr uint32_t kTWinBytes = kSH * kTP * 4u;  // bytes one TMA window load delivers
+// The box starts 8 columns left of the tile (a 16-byte aligned inner
+// coordinate, as the tensor unit requires; measured: a start at -5 columns
+// faults) and is 48 wide, so the 5-px halo window sits at column offset 3.
+constexpr int kTP = 48;                        // TMA window pitch (floats; 192 B rows)
+constexpr int kTX = 3;                         // column of the halo window inside the box
+constexpr uint32_t kTWinBytes = kSH * kTP * 4u;  // bytes one TMA window load delivers (8064)
 constexpr int kTWin = (kSH * kTP + 31) / 32 * 32;  // window stride in shared memory: 128-byte aligned destinations
 
 __device__ __forceinline__ void tma_load_3d(float* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
@@ -182,8 +186,8 @@ __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, 
     mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     mbar_arrive_expect_tx(&bar[0], 2 * kTWinBytes);
-    tma_load_3d(win, &tm.ren, bx - kHalf, by - kHalf, 0, &bar[0]);
-    tma_load_3d(win + kTWin, &tm.tgt, bx - kHalf, by - kHalf, 0, &bar[0]);
+    tma_load_3d(win, &tm.ren, bx - kHalf - kTX, by - kHalf, 0, &bar[0]);
+    tma_load_3d(win + kTWin, &tm.tgt, bx - kHalf - kTX, by - kHalf, 0, &bar[0]);
   }
   if (kTma) __syncthreads();  // barrier initialisation visible to every waiting thread
   // vertical task: column c, rows 4 rg .. 4 rg + 3
@@ -197,8 +201,8 @@ __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, 
         float* nb = win + ((ch + 1) & 1) * 2 * kTWin;
         fence_proxy_async();
         mbar_arrive_expect_tx(&bar[(ch + 1) & 1], 2 * kTWinBytes);
-        tma_load_3d(nb, &tm.ren, bx - kHalf, by - kHalf, ch + 1, &bar[(ch + 1) & 1]);
-        tma_load_3d(nb + kTWin, &tm.tgt, bx - kHalf, by - kHalf, ch + 1, &bar[(ch + 1) & 1]);
+        tma_load_3d(nb, &tm.ren, bx - kHalf - kTX, by - kHalf, ch + 1, &bar[(ch + 1) & 1]);
+        tma_load_3d(nb + kTWin, &tm.tgt, bx - kHalf - kTX, by - kHalf, ch + 1, &bar[(ch + 1) & 1]);
       }
       mbar_wait(&bar[ch & 1], (uint32_t)(ch >> 1));
       st0 = win + (ch & 1) * 2 * kTWin;
@@ -209,7 +213,7 @@ __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, 
       st0 = win;
     }
     const float* st1 = st0 + WIN;
-    hpass5<PITCH>(st0, st1, hq);
+    hpass5<PITCH, kTma ? kTX : 0>(st0, st1, hq);
     __syncthreads();
     float mv[5][kR];
 #pragma unroll
@@ -231,7 +235,7 @@ __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, 
     for (int j = 0; j < kR; ++j) {
       const int y = by + rg * kR + j;
       if (x >= W || y >= H) continue;
-      const int o = (rg * kR + j + kHalf) * PITCH + c + kHalf;
+      const int o = (rg * kR + j + kHalf) * PITCH + (kTma ? kTX : 0) + c + kHalf;
       const double a = st0[o], b = st1[o];
       const int64_t p = (int64_t)y * W + x;
       const bool in_mask = mask_at(mk, p);
@@ -271,7 +275,7 @@ __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, 
 }
 
 // Horizontal pass of the three gradient maps (back-convolution, losses.cpp:144-151).
-template <int PITCH>
+template <int PITCH, int XOFF>
 __device__ __forceinline__ void hpass3(const float* __restrict__ st, int plane_stride, float (*hq)[kSH][kTW + 1]) {
   for (int task = threadIdx.x; task < kSH * (kTW / kHR); task += kThr) {
     const int r = task / (kTW / kHR), q0 = (task - r * (kTW / kHR)) * kHR;
@@ -282,7 +286,7 @@ __device__ __forceinline__ void hpass3(const float* __restrict__ st, int plane_s
       for (int j = 0; j < kHR; ++j) acc[j] = 0.f;
 #pragma unroll
       for (int k = 0; k < kHR + kWin - 1; ++k) {
-        const float f = st[m * plane_stride + r * PITCH + q0 + k];
+        const float f = st[m * plane_stride + r * PITCH + XOFF + q0 + k];
 #pragma unroll
         for (int j = 0; j < kHR; ++j)
           if (k - j >= 0 && k - j < kWin) acc[j] = fmaf(c_win[k - j], f, acc[j]);
@@ -325,7 +329,7 @@ __global__ void GSB_LOSS_GRAD_BOUNDS loss_grad_kernel(const float* __restrict__ 
     mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     mbar_arrive_expect_tx(&bar[0], 3 * kTWinBytes);
-    for (int m = 0; m < 3; ++m) tma_load_3d(win + m * kTWin, &tm.gm, bx - kHalf, by - kHalf, m, &bar[0]);
+    for (int m = 0; m < 3; ++m) tma_load_3d(win + m * kTWin, &tm.gm, bx - kHalf - kTX, by - kHalf, m, &bar[0]);
   }
   if (kTma) __syncthreads();  // barrier initialisation visible to every waiting thread
   for (int ch = 0; ch < 3; ++ch) {
@@ -338,7 +342,7 @@ __global__ void GSB_LOSS_GRAD_BOUNDS loss_grad_kernel(const float* __restrict__ 
           fence_proxy_async();
           mbar_arrive_expect_tx(&bar[(ch + 1) & 1], 3 * kTWinBytes);
           for (int m = 0; m < 3; ++m)
-            tma_load_3d(nb + m * kTWin, &tm.gm, bx - kHalf, by - kHalf, 3 * (ch + 1) + m, &bar[(ch + 1) & 1]);
+            tma_load_3d(nb + m * kTWin, &tm.gm, bx - kHalf - kTX, by - kHalf, 3 * (ch + 1) + m, &bar[(ch + 1) & 1]);
         }
         mbar_wait(&bar[ch & 1], (uint32_t)(ch >> 1));
         st = win + (ch & 1) * 3 * kTWin;
@@ -348,7 +352,7 @@ __global__ void GSB_LOSS_GRAD_BOUNDS loss_grad_kernel(const float* __restrict__ 
         __syncthreads();
         st = win;
       }
-      hpass3<PITCH>(st, WIN, hq);
+      hpass3<PITCH, kTma ? kTX : 0>(st, WIN, hq);
       __syncthreads();
 #pragma unroll
       for (int m = 0; m < 3; ++m) {
