@@ -272,7 +272,9 @@ static uint64_t fingerprint(const gsb_cloud* cloud, const gsb_camera* cam, bool 
   h = fnv1a(h, f4, sizeof f4);
   const int32_t wh[2] = {cam->width, cam->height};
   h = fnv1a(h, wh, sizeof wh);
-  h = fnv1a(h, cam->R, sizeof(double) * 9);
+  // Se3Pose::rotation.data(): Eigen matrices are column-major
+  const double Rcm[9] = {cam->R[0], cam->R[3], cam->R[6], cam->R[1], cam->R[4], cam->R[7], cam->R[2], cam->R[5], cam->R[8]};
+  h = fnv1a(h, Rcm, sizeof Rcm);
   h = fnv1a(h, cam->t, sizeof(double) * 3);
   if (exact && cloud->fp_version == cloud->version) return fnv1a(h, cloud->fp_samples.data(), cloud->fp_samples.size());
   const uintptr_t id = reinterpret_cast<uintptr_t>(cloud);
@@ -2267,31 +2269,44 @@ int gsb_estimate_poses(gsb_ctx* ctx, gsb_cloud* cloud, gsb_image* const* targets
                        double* final_losses, int32_t* steps_used) {
   GSB_NVTX("gsb_estimate_poses");
   if (!targets || !init_poses || !poses_out || count <= 0) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
-  std::vector<gsb_session*> ss(count, nullptr);
+  // Views run in pose batches of kBatchViews (8: one batch's branches fill
+  // the GPU; more branches only add memory traffic — 64 views in one batch
+  // measured 1474 iters/s against 1923 at 8). Per-view results do not depend
+  // on the grouping (batches are bit-identical to sessions stepped alone).
+  static const int32_t kBatchViews = [] {
+    const char* e = std::getenv("GSB_POSE_BATCH_VIEWS");
+    const int v = e ? std::atoi(e) : 8;
+    return v > 0 ? v : 8;
+  }();
   int r = GSB_OK;
-  double t[6] = {debug_on() ? now_ms() : 0.0};
-  for (int32_t i = 0; i < count && !r; ++i)
-    r = gsb_session_create(ctx, cloud, targets[i], intr, init_poses + 12 * (size_t)i, cfg, &ss[i]);
-  if (debug_on()) t[1] = now_ms();
-  gsb_pose_batch* b = nullptr;
-  if (!r) r = gsb_pose_batch_create(ctx, ss.data(), count, &b);
-  if (debug_on()) t[2] = now_ms();
-  if (!r) r = gsb_pose_batch_step(ctx, b, cfg->budget);
-  if (debug_on()) t[3] = now_ms();
-  for (int32_t i = 0; i < count && !r; ++i) {
-    int32_t su = 0;
-    r = gsb_session_read(ss[i], nullptr, poses_out + 12 * (size_t)i, final_losses ? final_losses + i : nullptr, &su,
-                         nullptr, nullptr);
-    if (!r && steps_used) steps_used[i] = su;
-  }
-  if (debug_on()) t[4] = now_ms();
-  if (b) gsb_pose_batch_destroy(b);
-  for (gsb_session* s : ss)
-    if (s) gsb_session_destroy(s);
-  if (debug_on()) {
-    t[5] = now_ms();
-    std::fprintf(stderr, "[gsb] estimate_poses: create %.2f batch %.2f step %.2f read %.2f destroy %.2f ms\n",
-                 t[1] - t[0], t[2] - t[1], t[3] - t[2], t[4] - t[3], t[5] - t[4]);
+  for (int32_t g0 = 0; g0 < count && !r; g0 += kBatchViews) {
+    const int32_t gn = std::min(kBatchViews, count - g0);
+    std::vector<gsb_session*> ss(gn, nullptr);
+    double t[6] = {debug_on() ? now_ms() : 0.0};
+    for (int32_t i = 0; i < gn && !r; ++i)
+      r = gsb_session_create(ctx, cloud, targets[g0 + i], intr, init_poses + 12 * (size_t)(g0 + i), cfg, &ss[i]);
+    if (debug_on()) t[1] = now_ms();
+    gsb_pose_batch* b = nullptr;
+    if (!r) r = gsb_pose_batch_create(ctx, ss.data(), gn, &b);
+    if (debug_on()) t[2] = now_ms();
+    if (!r) r = gsb_pose_batch_step(ctx, b, cfg->budget);
+    if (debug_on()) t[3] = now_ms();
+    for (int32_t i = 0; i < gn && !r; ++i) {
+      int32_t su = 0;
+      const size_t v = (size_t)(g0 + i);
+      r = gsb_session_read(ss[i], nullptr, poses_out + 12 * v, final_losses ? final_losses + v : nullptr, &su,
+                           nullptr, nullptr);
+      if (!r && steps_used) steps_used[v] = su;
+    }
+    if (debug_on()) t[4] = now_ms();
+    if (b) gsb_pose_batch_destroy(b);
+    for (gsb_session* s : ss)
+      if (s) gsb_session_destroy(s);
+    if (debug_on()) {
+      t[5] = now_ms();
+      std::fprintf(stderr, "[gsb] estimate_poses views %d..%d: create %.2f batch %.2f step %.2f read %.2f destroy %.2f ms\n",
+                   g0, g0 + gn - 1, t[1] - t[0], t[2] - t[1], t[3] - t[2], t[4] - t[3], t[5] - t[4]);
+    }
   }
   return r;
 }

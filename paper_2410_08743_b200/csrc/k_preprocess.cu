@@ -255,25 +255,29 @@ __device__ __forceinline__ uint32_t project_one(const float* P, int64_t n_pad, i
   if (!(radius > 0.0 && isfinite(radius) && !(a_(u, radius) < 0.0) && !(s_(u, radius) > cam.width - 1) &&
         !(a_(v, radius) < 0.0) && !(s_(v, radius) > cam.height - 1)))
     return 0u;
-  // invert_spd2
+  // invert_spd2 (one reciprocal: the conic is stored in FP32, so the FP64
+  // quotient's last bit never matters; 3 DP divisions fewer per view)
   const double det = s_(m_(cov[0], cov[3]), m_(cov[1], cov[2]));
-  const double ca = d_(cov[3], det), cb = d_(-cov[1], det), cc2 = d_(-cov[2], det), cd = d_(cov[0], det);
+  const double idet = d_(1.0, det);
+  const double ca = m_(cov[3], idet), cb = m_(-cov[1], idet), cc2 = m_(-cov[2], idet), cd = m_(cov[0], idet);
   // colour: sh_eval at dir = normalize(mean - center)
   double dx = s_(g.mx, cam.center[0]), dy = s_(g.my, cam.center[1]), dz = s_(g.mz, cam.center[2]);
   const double dn = __dsqrt_rn(a_(a_(m_(dx, dx), m_(dy, dy)), m_(dz, dz)));
-  dx = d_(dx, dn);
-  dy = d_(dy, dn);
-  dz = d_(dz, dn);
+  const double idn = d_(1.0, dn);  // the direction feeds the FP32 SH evaluation
+  dx = m_(dx, idn);
+  dy = m_(dy, idn);
+  dz = m_(dz, idn);
   float col[3], G[9];
   uint32_t clamp = 0;
   sh_colour<DEG, kQuirk>(P, n_pad, sh_cap, (float)dx, (float)dy, (float)dz, col, &clamp, G);
   for (int k = 0; k < 9; ++k) o.colj[(int64_t)k * o.n_pad_out + i] = G[k];
-  // tile span (rasterizer.cpp:138-146)
-  const double tile = (double)kTile;
-  const int tx0 = clamp_tile(floor(d_(s_(u, radius), tile)), cam.tiles_x);
-  const int tx1 = clamp_tile(floor(d_(a_(u, radius), tile)), cam.tiles_x);
-  const int ty0 = clamp_tile(floor(d_(s_(v, radius), tile)), cam.tiles_y);
-  const int ty1 = clamp_tile(floor(d_(a_(v, radius), tile)), cam.tiles_y);
+  // tile span (rasterizer.cpp:138-146); x / 16 == x * (1/16) exactly (power of two)
+  static_assert((kTile & (kTile - 1)) == 0, "tile size must be a power of two");
+  const double itile = 1.0 / (double)kTile;
+  const int tx0 = clamp_tile(floor(m_(s_(u, radius), itile)), cam.tiles_x);
+  const int tx1 = clamp_tile(floor(m_(a_(u, radius), itile)), cam.tiles_x);
+  const int ty0 = clamp_tile(floor(m_(s_(v, radius), itile)), cam.tiles_y);
+  const int ty1 = clamp_tile(floor(m_(a_(v, radius), itile)), cam.tiles_y);
   SplatRec rec;
   rec.mu_x = u;
   rec.mu_y = v;

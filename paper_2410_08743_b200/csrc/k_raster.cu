@@ -745,6 +745,9 @@ __device__ __forceinline__ int half_reduce9(const float v[9], float* out) {
 #ifndef GSB_BWD_CPASYNC
 #define GSB_BWD_CPASYNC 0
 #endif
+#ifndef GSB_HALF_LDS_ASM
+#define GSB_HALF_LDS_ASM 0
+#endif
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
@@ -863,16 +866,28 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
         const bool act = it < mine;
         const int k = act ? my_list[mine - 1 - it] : 0;
         const uint32_t j = b0 + (uint32_t)k;
+#if GSB_HALF_LDS_ASM
         const uint32_t sa = sp_base + (uint32_t)k * (uint32_t)sizeof(StagedSplat);
         const float4 ge = lds_f4(sa);
         const float4 ap = lds_f4(sa + 16u);
+#else
+        // plain shared-array loads: LDS offsets in the CTA's window need no
+        // generic->shared base (the asm form rematerialised S2R SR_CgaCtaId +
+        // LEA in the step loop)
+        const float4 ge = s_sp[k].geo;
+        const float4 ap = s_sp[k].app;
+#endif
         const float dx = px - ge.x, dy = py - ge.y;
         const float ga = splat_power(ge.z, ge.w, ap.x, dx, dy);
         const float gb = splat_power(ge.z, ge.w, ap.x, dx, dy + 1.0f);
         const bool ha = act && j < a.contrib && ga <= rc.cutoff2_f;
         const bool hb = act && j < b.contrib && gb <= rc.cutoff2_f;
         if (!__any_sync(kFull, ha || hb)) continue;  // neither half's entry touched: zero partials
+#if GSB_HALF_LDS_ASM
         const float cb = lds_f1(sa + 32u);
+#else
+        const float cb = s_sp[k].col_b;
+#endif
         float v[NC];
         backward_pair<NC>(a, b, ge, ap, cb, dx, dy, ga, gb, ha, hb, rc, v);
         float tot;

@@ -7,7 +7,7 @@ tests/test_trainer.cpp:345-366, tests/test_losses.cpp:256-275).
 
 unproject is host code (no device): bit-exact on the CPU suite. Everything
 else runs on the GPU. Bars: kNN scales / init cloud bit-exact (FP64 kNN with
-the reference's rounding, stored as FP32); masked loss within 1e-7 relative (FP32 convolutions)
+the reference's rounding, stored as FP32); masked loss within 1e-6 relative (FP32 convolutions)
 (FP64 sums in another order over FP32-exact images), its gradient within
 FP32 rounding; the iterated fits and pose descents within the joint tests'
 tolerances (Adam over FP32 vs FP64 gradients; test_gpu_joint.py docstring).
@@ -150,9 +150,9 @@ def test_masked_rgb_loss_matches_oracle(G, ctx):
             mask[H // 2, W // 2] = 1
             l_d, g_d = G.masked_rgb_loss(ctx, r, t, mask, 0.2)
             l_o, g_o = O.masked_rgb_loss(r, t, mask, 0.2)
-            # K6's separable convolutions are FP32 (sums FP64): loss within 1e-7
+            # K6's separable convolutions are FP32 (sums FP64): loss within 1e-6
             # relative, gradient within 1e-4 of its largest entry
-            assert abs(l_d - l_o) <= 1e-7 * abs(l_o), (W, H, frac, l_d, l_o)
+            assert abs(l_d - l_o) <= 1e-6 * abs(l_o), (W, H, frac, l_d, l_o)
             assert np.max(np.abs(g_d - g_o)) <= 1e-4 * np.max(np.abs(g_o)) + 1e-12
     with pytest.raises(G.GsbError) as e:
         G.masked_rgb_loss(ctx, r, t, np.zeros((H, W), np.uint8))
@@ -192,7 +192,7 @@ def test_frame_masked_loss_uses_render_transmittance(G, ctx):
         loss, cnt = G.frame_masked_rgb_loss(ctx, fr, target, 0.2, thr)
         assert cnt == int(mask.sum())
         l_o = O.masked_rgb_loss(out["image"], imgs[1], mask, 0.2, want_grad=False)
-        assert abs(loss - l_o) <= 1e-7 * abs(l_o)
+        assert abs(loss - l_o) <= 1e-6 * abs(l_o)  # FP32 convolutions
 
 
 def fit_cfgs(G, fit_steps, rel_steps, points=50000):
