@@ -583,10 +583,13 @@ def run_c3_job(args, ws, rank, local, ctx, cloud, gt, init, intr):
     assert all(int(k) == 100 for k in out["steps"])
     rot = [gsb_abs_err(out["pose"][v], gt[v]) for v in range(TOTAL_VIEWS)]
     return {"workload": f"C3 complete job: {TOTAL_VIEWS} views x 100 iterations, {N_GAUSS} Gaussians, one GPU, "
-                        "one gsb_estimate_poses call (views advanced as one pose batch)",
+                        "one gsb_estimate_poses call (views advanced in pose batches of 8)",
             "views_per_s": round(TOTAL_VIEWS / (ms / 1e3), 3), "iters_per_s": round(TOTAL_VIEWS * 100 / (ms / 1e3), 2),
             "job_s": round(ms / 1e3, 3),
             "recovered_views": int(sum(1 for r, t in rot if r < 0.1 and t < 1e-3)),
+            "converged_views_acceptance": int(sum(1 for r, t in rot if r < 5.0 and t < 0.05)),
+            "note": "pose_descent's own convergence at C3's 100-iteration budget from 15 deg / 0.15 (the reference "
+                    "algorithm; the C2 parity test shows the reference CPU build no closer to GT)",
             "median_rot_err_deg": float(np.median([r for r, _ in rot])),
             "median_trans_err": float(np.median([t for _, t in rot]))}
 
