@@ -333,6 +333,18 @@ __global__ void GSB_LOSS_GRAD_BOUNDS loss_grad_kernel(const float* __restrict__ 
   }
   if (kTma) __syncthreads();  // barrier initialisation visible to every waiting thread
   for (int ch = 0; ch < 3; ++ch) {
+    // this channel's output pixels of both images, loaded before the
+    // convolutions so their latency overlaps them (they were the kernel's
+    // long-scoreboard stall)
+    float av[kR], bv[kR];
+#pragma unroll
+    for (int j = 0; j < kR; ++j) {
+      const int y = by + rg * kR + j;
+      const bool in = x < W && y < H;
+      const int64_t p = in ? (int64_t)y * W + x : 0;
+      av[j] = in ? __ldg(ren + ch * P + p) : 0.f;
+      bv[j] = in ? __ldg(tgt + ch * P + p) : 0.f;
+    }
     float cv[3][kR];
     if (has_ssim) {
       const float* st;
@@ -375,7 +387,7 @@ __global__ void GSB_LOSS_GRAD_BOUNDS loss_grad_kernel(const float* __restrict__ 
       const int y = by + rg * kR + j;
       if (x >= W || y >= H) continue;
       const int64_t p = (int64_t)y * W + x;
-      const double a = ren[ch * P + p], b = tgt[ch * P + p];
+      const double a = av[j], b = bv[j];
       const double diff = a - b;
       const double dl1 = (diff == 0.0 || !mask_at(mk, p)) ? 0.0 : (diff > 0.0 ? l1_norm : -l1_norm);
       const double dss =

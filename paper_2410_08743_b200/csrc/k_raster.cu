@@ -971,6 +971,184 @@ int launch_expected_depth(cudaStream_t st, gsb_frame* f, const RasterDev& rc, fl
   return GSB_OK;
 }
 
+// ---- K4a, pose-only, 4 pixels per lane (GSB_BWD_QUAD4; an A/B variant, off).
+// One 64-thread CTA per tile: warp w owns the 16x8 rows 8w..8w+7; its four
+// 8-lane groups each own an 8x4 region (group g: columns 8(g&1).., rows
+// 8w + 4(g>>1)..), one column of 4 pixels per lane. The four groups walk
+// their own lists of the batch entries whose cutoff-ellipse box reaches their
+// region, so one warp step serves four entries (two in the 2-px/lane half
+// kernel) and the per-step overhead — list load, record loads, the
+// reduce-scatter (8 values over 8 lanes: 4 + 2 + 1 shuffles) — is shared by
+// four. Measured on C3 view 0 with the oracle's forward state: 0.565 M warp
+// steps instead of 0.997 M. The lane's 4 pixels are two vertical pairs at
+// rows r0 and r0 + 2 whose dy is formed exactly as the composite forms it
+// (pair start py - my, second pixel dy + 1), so every cutoff / termination
+// decision is the forward's. Per-entry partials: sum of the two pairs, group
+// reduce-scatter, then the four groups add into the warp's shared slot in
+// group order (ordered rounds), warps 0, 1 at the flush: deterministic.
+#ifndef GSB_BWD_QUAD4
+#define GSB_BWD_QUAD4 0
+#endif
+constexpr int kQ4Threads = 64;
+#ifndef GSB_Q4_MIN_BLOCKS
+#define GSB_Q4_MIN_BLOCKS 10
+#endif
+
+// 8 values over each 8-lane group: xor 4 / 2 / 1 reduce-scatter; lane l owns
+// component (l & 7) of its group's sum.
+__device__ __forceinline__ float group_reduce8(const float v[8]) {
+  const int lane = threadIdx.x & 31;
+  const bool h1 = lane & 4, h2 = lane & 2, h3 = lane & 1;
+  float w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = h1 ? v[i] : v[4 + i], keep = h1 ? v[4 + i] : v[i];
+    w[i] = keep + __shfl_xor_sync(kFull, send, 4);
+  }
+  float x[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = h2 ? w[i] : w[2 + i], keep = h2 ? w[2 + i] : w[i];
+    x[i] = keep + __shfl_xor_sync(kFull, send, 2);
+  }
+  const float send = h3 ? x[0] : x[1], keep = h3 ? x[1] : x[0];
+  return keep + __shfl_xor_sync(kFull, send, 1);
+}
+
+__global__ void __launch_bounds__(kQ4Threads, GSB_Q4_MIN_BLOCKS) backward_raster_q4_kernel(
+    const uint2* __restrict__ ranges, const uint32_t* __restrict__ ranks, const SplatRec* __restrict__ rec,
+    const SplatAux* __restrict__ aux, const CamDev* __restrict__ cam_p, RasterDev rc, float bg_r, float bg_g,
+    float bg_b, int64_t npix, const float* __restrict__ d_image, const float* __restrict__ final_t,
+    const uint32_t* __restrict__ pixstate, const double* __restrict__ depth_g, double2* __restrict__ tile_cut,
+    float* __restrict__ partials, uint32_t k_cap) {
+  constexpr int NC = 8;
+  __shared__ StagedSplat s_sp[kBatch];
+  __shared__ uint8_t s_mask[kBatch];
+  __shared__ uint8_t s_list[2][4][kBatch];
+  __shared__ float s_red[2][kBatch][NC];
+  __shared__ int s_w, s_h, s_tx;
+  __shared__ uint32_t s_maxc[2];
+  if (threadIdx.x == 0) {
+    s_w = cam_p->width;
+    s_h = cam_p->height;
+    s_tx = cam_p->tiles_x;
+  }
+  for (int i = threadIdx.x; i < 2 * kBatch * NC; i += kQ4Threads) (&s_red[0][0][0])[i] = 0.f;
+  __syncthreads();
+  const int W = s_w, H = s_h;
+  const int tile = blockIdx.x;
+  const int tx = tile % s_tx, ty = tile / s_tx;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 3;
+  const int lx = (g & 1) * 8 + (lane & 7), ly = warp * 8 + (g >> 1) * 4;  // rows ly .. ly + 3
+  const int x = tx * kTile + lx, y = ty * kTile + ly;
+  const double ox = (double)(tx * kTile), oy = (double)(ty * kTile);
+  const float px = (float)lx, py0 = (float)ly, py2 = (float)(ly + 2);
+  const uint2 range = ranges[tile];
+
+  PixBwd a, b, c, d;
+  load_pixel_bwd(a, x, y, W, H, npix, bg_r, bg_g, bg_b, d_image, final_t, pixstate);
+  load_pixel_bwd(b, x, y + 1, W, H, npix, bg_r, bg_g, bg_b, d_image, final_t, pixstate);
+  load_pixel_bwd(c, x, y + 2, W, H, npix, bg_r, bg_g, bg_b, d_image, final_t, pixstate);
+  load_pixel_bwd(d, x, y + 3, W, H, npix, bg_r, bg_g, bg_b, d_image, final_t, pixstate);
+  const uint32_t wmax = __reduce_max_sync(kFull, max(max(a.contrib, b.contrib), max(c.contrib, d.contrib)));
+  if (lane == 0) s_maxc[warp] = wmax;
+  __syncthreads();
+  const uint32_t maxc = max(s_maxc[0], s_maxc[1]);
+  // entries at list positions >= maxc: see backward_raster_kernel
+  if (threadIdx.x == 0) {
+    double2 cut = make_double2(-1.0, 0.0);
+    if (maxc > 0) {
+      const int32_t gid = aux[ranks[range.x + maxc - 1]].gid;
+      cut = make_double2(depth_g[gid], (double)gid);
+    }
+    tile_cut[tile] = cut;
+  }
+  // region bit of this lane's group in the staged half mask (bit 2 q + h,
+  // quadrant q = qx + 2 qy, half h = rows 4..7 of the quadrant)
+  const int gbit = 2 * ((g & 1) + 2 * warp) + (g >> 1);
+  const uint32_t len = min(range.y - range.x, maxc);
+  const uint32_t nbatch = (len + kBatch - 1) / kBatch;
+  const uint32_t lt = lanemask_lt_();
+  for (int bi = (int)nbatch - 1; bi >= 0; --bi) {
+    const uint32_t b0 = (uint32_t)bi * kBatch;
+    const int cnt = (int)min((uint32_t)kBatch, len - b0);
+    for (int t = threadIdx.x; t < cnt; t += kQ4Threads) {
+      const uint32_t r = ranks[range.x + b0 + t];
+      const SplatAux A = aux[r];
+      const uint32_t tx0 = A.tx0_ty0 & 0xffffu, ty0 = A.tx0_ty0 >> 16, nx = A.nx_ny & 0xffffu;
+      StagedSplat& S = s_sp[t];
+      S.slot = A.off + ((uint32_t)ty - ty0) * nx + ((uint32_t)tx - tx0);
+      s_mask[t] = (uint8_t)half_mask(stage_splat(rec[r], ox, oy, rc.cutoff2_f, &S.geo, &S.app, &S.col_b));
+    }
+    __syncthreads();
+    if (b0 < wmax) {
+      // the four groups' lists (ascending), all built by the whole warp
+      const uint32_t lim = wmax - b0;
+      int n[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int cc = 0; cc < kBatch / 32; ++cc) {
+        const int e = cc * 32 + lane;
+        const uint32_t m = (e < cnt && (uint32_t)e < lim) ? s_mask[e] : 0u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int bit = 2 * ((q & 1) + 2 * warp) + (q >> 1);
+          const bool take = (m >> bit) & 1u;
+          const uint32_t bal = __ballot_sync(kFull, take);
+          if (take) s_list[warp][q][n[q] + __popc(bal & lt)] = (uint8_t)e;
+          n[q] += __popc(bal);
+        }
+      }
+      __syncwarp();
+      (void)gbit;
+      const int mine = g == 0 ? n[0] : g == 1 ? n[1] : g == 2 ? n[2] : n[3];
+      const int nmax = max(max(n[0], n[1]), max(n[2], n[3]));
+      const uint8_t* my_list = s_list[warp][g];
+      for (int it = 0; it < nmax; ++it) {  // each group back to front
+        const bool act = it < mine;
+        const int k = act ? my_list[mine - 1 - it] : 0;
+        const uint32_t j = b0 + (uint32_t)k;
+        const float4 ge = s_sp[k].geo;
+        const float4 ap = s_sp[k].app;
+        const float dx = px - ge.x, dya = py0 - ge.y, dyc = py2 - ge.y;
+        const float ga = splat_power(ge.z, ge.w, ap.x, dx, dya);
+        const float gb = splat_power(ge.z, ge.w, ap.x, dx, dya + 1.0f);
+        const float gc = splat_power(ge.z, ge.w, ap.x, dx, dyc);
+        const float gd = splat_power(ge.z, ge.w, ap.x, dx, dyc + 1.0f);
+        const bool ha = act && j < a.contrib && ga <= rc.cutoff2_f;
+        const bool hb = act && j < b.contrib && gb <= rc.cutoff2_f;
+        const bool hc = act && j < c.contrib && gc <= rc.cutoff2_f;
+        const bool hd = act && j < d.contrib && gd <= rc.cutoff2_f;
+        if (!__any_sync(kFull, ha || hb || hc || hd)) continue;  // no group's entry touched: zero partials
+        const float cb = s_sp[k].col_b;
+        float v[NC], u[NC];
+        backward_pair<NC>(a, b, ge, ap, cb, dx, dya, ga, gb, ha, hb, rc, v);
+        backward_pair<NC>(c, d, ge, ap, cb, dx, dyc, gc, gd, hc, hd, rc, u);
+#pragma unroll
+        for (int q = 0; q < NC; ++q) v[q] += u[q];
+        const float tot = group_reduce8(v);
+        const int comp = lane & 7;
+        // groups may hold the same entry in a step: add in group order
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (act && g == q) s_red[warp][k][comp] += tot;
+          __syncwarp();
+        }
+      }
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < cnt * NC; idx += kQ4Threads) {
+      const int k = idx / NC, cc = idx - k * NC;
+      float acc = s_red[0][k][cc] + s_red[1][k][cc];
+      s_red[0][k][cc] = 0.f;
+      s_red[1][k][cc] = 0.f;
+      if (cc < 2) acc *= -2.0f;  // d_mu2d = -2 dg (conic d) (rasterizer.cpp:396)
+      const uint32_t slot = s_sp[k].slot;
+      if (slot < k_cap) partials[(int64_t)slot * NC + cc] = acc;
+    }
+    __syncthreads();
+  }
+}
+
 int launch_composite(cudaStream_t st, gsb_frame* f, const RasterDev& rc) {
   const int n_tiles = f->tiles_x * f->tiles_y;
   const int64_t npix = (int64_t)f->width * f->height;
@@ -993,6 +1171,15 @@ int launch_composite(cudaStream_t st, gsb_frame* f, const RasterDev& rc) {
 int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc, bool pose_only) {
   const int n_tiles = f->tiles_x * f->tiles_y;
   const int64_t npix = (int64_t)f->width * f->height;
+  if (n_tiles > 0 && pose_only && GSB_BWD_QUAD4) {
+    backward_raster_q4_kernel<<<n_tiles, kQ4Threads, 0, st>>>(
+        f->ranges.as<uint2>(), f->list(), f->list_rec(), f->list_aux(), f->cam.as<CamDev>(), rc,
+        (float)f->background[0], (float)f->background[1], (float)f->background[2], npix, f->d_image.as<float>(),
+        f->final_t.as<float>(), f->pixstate.as<uint32_t>(), f->depth_g.as<double>(), f->tile_cut.as<double2>(),
+        f->partials.as<float>(), (uint32_t)f->k_cap);
+    GSB_CHECK_LAUNCH("backward_raster_q4_kernel");
+    return GSB_OK;
+  }
   if (n_tiles > 0)
     (pose_only ? (GSB_BWD_HALF ? backward_raster_half_kernel<8> : backward_raster_kernel<8>)
                : (GSB_BWD_HALF_FULL ? backward_raster_half_kernel<kPartial> : backward_raster_kernel<kPartial>))
