@@ -44,11 +44,26 @@ def log_scale_offset(n):
     return math.log(500.0 / n) / 3.0 if n > 500 else 0.0
 
 
+# Plumbing check on a box with fewer GPUs than ranks (GSB_BENCH_SHARE_GPU=1):
+# every rank uses GPU 0, torch.distributed runs over gloo and the NCCL joint
+# leg is skipped. Only for exercising the multi-rank code path; the numbers
+# of such a run are not a measurement of N GPUs.
+SHARE_GPU = os.environ.get("GSB_BENCH_SHARE_GPU", "0") == "1"
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    return ws, rank, 0 if SHARE_GPU else local
+
+
+def _reduce_max(dist, v, local):
+    """max over ranks of a host float (device tensor for NCCL, host for gloo)."""
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device="cpu" if SHARE_GPU else f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 class ClockSampler:
@@ -120,8 +135,11 @@ def run_ours(args, ws, rank, local):
     if ws > 1:
         import torch
         import torch.distributed as td
-        torch.cuda.set_device(local)
-        td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if SHARE_GPU:
+            td.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            td.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = td
     ctx = gsb.Context(local)
     fp32 = gsb.measure_fp32_peaks(local)  # FFMA / MUFU microbenchmarks: the FP32 roofline denominators
@@ -201,9 +219,7 @@ def run_ours(args, ws, rank, local):
     solo_stages = {k: v for k, v in solo_tot.items()}
     if dist:
         import torch
-        t = torch.tensor([dev_ms], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_ms = float(t.item())
+        dev_ms = _reduce_max(dist, dev_ms, local)
     iters = VIEWS_PER_GPU * ws * args.steps
     value = iters / (dev_ms / 1e3)
     for s in sessions:
@@ -235,12 +251,10 @@ def run_ours(args, ws, rank, local):
     e2e_s = time.perf_counter() - t0
     if dist:
         import torch
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s = _reduce_max(dist, e2e_s, local)
     e2e_value = VIEWS_PER_GPU * ws * e2e_iters / e2e_s
 
-    joint = None if args.no_joint else run_joint(args, ws, rank, local, dist)
+    joint = None if (args.no_joint or (SHARE_GPU and ws > 1)) else run_joint(args, ws, rank, local, dist)
     single = None if args.no_joint else run_single_view(args, ws, rank, local)
     c3_job = None if args.no_c3_job else run_c3_job(args, ws, rank, local, ctx, cloud, gt, init, intr)
     out = None
@@ -384,9 +398,7 @@ def run_joint(args, ws, rank, local, dist):
     ms = ctx.timer_stop()
     if dist:
         import torch
-        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = _reduce_max(dist, ms, local)
     res = j.read()
     j.close()
     if comm:
