@@ -685,6 +685,10 @@ def main():
     ap.add_argument("--no-joint", action="store_true", help="skip the secondary C4 joint-DP measurement")
     args = ap.parse_args()
     ws, rank, local = dist_env()
+    if rank == 0 and os.environ.get("OMP_NUM_THREADS") == "1" and ws > 1:
+        # torchrun pins every rank to one OpenMP thread; rank 0's host-side
+        # oracle work (FLOP counts) gets the host's cores back
+        os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
         sys.exit(spawn_ranks(args.gpus))
     if ws != args.gpus and args.gpus != 1:
