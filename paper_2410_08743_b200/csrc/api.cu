@@ -424,6 +424,7 @@ static int frame_reserve(gsb_frame* f, const gsb_cloud* cloud, int64_t k_cap) {
   GSB_CUDA(f->loss_blocks.reserve(sizeof(double) * 2 * loss_block_count(f->width, f->height), &grew));
   GSB_CUDA(f->loss_val.reserve(sizeof(double) * 4, &grew));
   GSB_CUDA(f->partials.reserve(sizeof(float) * kPartial * k_cap, &grew));
+  if (f->want_hits) GSB_CUDA(f->hits.reserve(sizeof(uint16_t) * 16 * k_cap, &grew));
   GSB_CUDA(f->pose_blocks.reserve(sizeof(double) * 6 * ((n + 63) / 64 + 1), &grew));  // K4b blocks of >= 64
   GSB_CUDA(f->d_pose.reserve(sizeof(double) * 6, &grew));
   if (grew) {
@@ -434,6 +435,7 @@ static int frame_reserve(gsb_frame* f, const gsb_cloud* cloud, int64_t k_cap) {
   f->k_cap = std::min<int64_t>(f->k_cap, (int64_t)(f->partials.bytes / (sizeof(float) * kPartial)));
   f->k_cap = std::min<int64_t>(f->k_cap, (int64_t)(f->ent_key.bytes / sizeof(uint64_t)));
   f->k_cap = std::min<int64_t>(f->k_cap, (int64_t)(f->ent_gid.bytes / sizeof(uint32_t)));
+  if (f->want_hits) f->k_cap = std::min<int64_t>(f->k_cap, (int64_t)(f->hits.bytes / (sizeof(uint16_t) * 16)));
   f->k_cap = std::min<int64_t>(f->k_cap, 0xffffffffll);
   return GSB_OK;
 }
@@ -1033,7 +1035,7 @@ int gsb_frame_destroy(gsb_frame* f) {
                     &f->cnt_r, &f->ekey[0], &f->ekey[1], &f->eval_[0], &f->eval_[1], &f->ranges, &f->tile_cut, &f->image,
                     &f->final_t, &f->pixstate, &f->d_image, &f->partials, &f->pose_blocks, &f->d_pose,
                     &f->loss_blocks, &f->loss_val, &f->mask_ws, &f->gmaps, &f->scan_tmp, &f->sort_hist, &f->counters,
-                    &f->aux_g, &f->tile_hist, &f->tile_scan, &f->tile_big, &f->ent_key, &f->ent_gid, &f->exp_lists,
+                    &f->aux_g, &f->tile_hist, &f->tile_scan, &f->tile_big, &f->ent_key, &f->ent_gid, &f->hits, &f->exp_lists,
                     &f->exp_ranges, &f->exp_contrib};
   for (DevBuf* b : bufs) b->release();
   gsb_ctx* owner = f->ctx_ref ? f->ctx : nullptr;
@@ -1051,6 +1053,7 @@ int gsb_render(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, const doub
   gsb_default_raster_config(&dflt);
   if (!cfg) cfg = &dflt;
   if (int r = validate_config(cfg)) return r;
+  f->want_hits = true;  // a pose-only gsb_render_backward may follow
   if (int r = frame_setup(ctx, f, cloud, cam, bg, cfg, true)) return r;
   const RasterDev rc = make_rasterdev(cfg);
   if (int r = render_sync(ctx, cloud, f, rc)) return r;
@@ -1762,6 +1765,7 @@ static gsb_frame* session_frame(gsb_ctx* ctx, gsb_session* s) { return s->own ? 
 static int session_frame_ready(gsb_ctx* ctx, gsb_session* s, gsb_frame** out) {
   gsb_frame* f = session_frame(ctx, s);
   f->lean = true;  // never exported (not reachable through gsb_frame_download)
+  f->want_hits = true;  // pose-only backward: K4a walks the composite's hit masks
   if (int r = frame_setup(ctx, f, s->cloud, &s->cam, s->cfg.background, &s->cfg.raster, false)) return r;
   const int64_t want = f->k_cap > 0 ? f->k_cap : initial_k_cap(s->cloud->n);
   if (int r = frame_reserve(f, s->cloud, want)) return r;

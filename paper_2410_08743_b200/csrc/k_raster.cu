@@ -195,9 +195,14 @@ __device__ __forceinline__ bool pix_done(const PixFwd& p, const RasterDev&) { re
 
 // Both pixels of a lane for one splat, branch free (alpha = 0 is an exact
 // no-op for a pixel that is done or outside the cutoff).
+// hrow (kHits): the batch entry's 16 region masks in shared memory; the
+// sub-warp's 8 lanes' pixel-pair hits go to slot `region` (pixel a of lane
+// l8 -> bit l8, pixel b -> bit 8 + l8), the exact set of (pixel, entry) pairs
+// the replay of render_backward visits (rasterizer.cpp:378-383).
+template <bool kHits>
 __device__ __forceinline__ void composite_pair(PixFwd& a, PixFwd& b, const float4& ge, const float4& ap, float col_b,
                                                float dx, float dy, const RasterDev& rc, uint32_t idx1,
-                                               bool act = true) {
+                                               bool act = true, uint16_t* hrow = nullptr, int region = 0) {
   const float ga = splat_power(ge.z, ge.w, ap.x, dx, dy);
   const float gb = splat_power(ge.z, ge.w, ap.x, dx, dy + 1.0f);
   const bool ha = act && !pix_done(a, rc) && ga <= rc.cutoff2_f;
@@ -207,6 +212,11 @@ __device__ __forceinline__ void composite_pair(PixFwd& a, PixFwd& b, const float
 #else
   if (!(ha || hb)) return;
 #endif
+  if (kHits) {
+    const uint32_t ba = __ballot_sync(kFull, ha), bb = __ballot_sync(kFull, hb);
+    const int lane = threadIdx.x & 31, sh = lane & 24;
+    if ((lane & 7) == 0 && act) hrow[region] = (uint16_t)(((ba >> sh) & 0xffu) | (((bb >> sh) & 0xffu) << 8));
+  }
   const float al_a = ha ? fminf(rc.alpha_clamp_f, ap.y * exp_neg_half(ga)) : 0.f;
   const float al_b = hb ? fminf(rc.alpha_clamp_f, ap.y * exp_neg_half(gb)) : 0.f;
   const float wa = al_a * a.T, wb = al_b * b.T;
@@ -244,14 +254,17 @@ __device__ __forceinline__ void write_pixel(const PixFwd& p, int x, int y, int W
 #else
 #define GSB_COMP_BOUNDS __launch_bounds__(kThreads)
 #endif
+template <bool kHits>
 __global__ void GSB_COMP_BOUNDS composite_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ ranks, const SplatRec* __restrict__ rec,
     const CamDev* __restrict__ cam_p, RasterDev rc, float bg_r, float bg_g, float bg_b, int64_t npix,
-    float* __restrict__ image, float* __restrict__ final_t, uint32_t* __restrict__ pixstate) {
+    float* __restrict__ image, float* __restrict__ final_t, uint32_t* __restrict__ pixstate,
+    uint16_t* __restrict__ hits, uint32_t k_cap) {
   constexpr int CB = kCompBatch;
   __shared__ StagedSplat s_sp[CB];
   __shared__ uint16_t s_mask[CB];
   __shared__ uint8_t s_list[kWarps][kSubs][CB];
+  __shared__ __align__(16) uint16_t s_hits[kHits ? CB : 1][16];
   __shared__ int s_w, s_h, s_tx;
   if (threadIdx.x == 0) {
     s_w = cam_p->width;
@@ -269,6 +282,7 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
   const int x = tx * kTile + lx, y = ty * kTile + ly;
   const double ox = (double)(tx * kTile), oy = (double)(ty * kTile);
   const float px = (float)lx, py = (float)ly;
+  const int region = region_of(warp, sub);
   const uint2 range = ranges[tile];
   PixFwd a{1.f, 0.f, 0.f, 0.f, (x < W && y < H) ? 0u : kDone};
   PixFwd b{1.f, 0.f, 0.f, 0.f, (x < W && y + 1 < H) ? 0u : kDone};
@@ -281,6 +295,11 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
       if (t < cnt)
         s_mask[t] = (uint16_t)stage_splat(rec[ranks[base + t]], ox, oy, rc.cutoff2_f, &s_sp[t].geo, &s_sp[t].app,
                                           &s_sp[t].col_b);
+      if (kHits) {
+        uint4* hz = reinterpret_cast<uint4*>(s_hits[t]);
+        hz[0] = make_uint4(0u, 0u, 0u, 0u);
+        hz[1] = make_uint4(0u, 0u, 0u, 0u);
+      }
     }
     __syncthreads();
     const uint32_t list0 = base - range.x;
@@ -301,7 +320,8 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
         const float4 ap = S.app;
         const float cb = S.col_b;
         const float dx = px - ge.x, dy = py - ge.y;
-        composite_pair(a, b, ge, ap, cb, dx, dy, rc, list0 + k + 1u, act);
+        composite_pair<kHits>(a, b, ge, ap, cb, dx, dy, rc, list0 + k + 1u, act, kHits ? s_hits[k] : nullptr,
+                              region);
       }
 #else
       if (it < mine) {
@@ -311,7 +331,7 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
         const float4 ap = S.app;
         const float cb = S.col_b;
         const float dx = px - ge.x, dy = py - ge.y;
-        composite_pair(a, b, ge, ap, cb, dx, dy, rc, list0 + k + 1u);
+        composite_pair<false>(a, b, ge, ap, cb, dx, dy, rc, list0 + k + 1u);
       }
 #endif
       // a sub-warp whose 16 pixels have all terminated stops early
@@ -320,6 +340,19 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
     (void)sub_mask;
     if (!pix_done(a, rc)) a.processed = list0 + (uint32_t)cnt;
     if (!pix_done(b, rc)) b.processed = list0 + (uint32_t)cnt;
+    if (kHits) {  // the batch's masks, 32 B per entry, coalesced
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < CB / kThreads; ++u) {
+        const int t = u * kThreads + threadIdx.x;
+        if (t < cnt && base + t < k_cap) {
+          const uint4* src = reinterpret_cast<const uint4*>(s_hits[t]);
+          uint4* dst = reinterpret_cast<uint4*>(hits + (size_t)(base + t) * 16);
+          dst[0] = src[0];
+          dst[1] = src[1];
+        }
+      }
+    }
   }
   write_pixel(a, x, y, W, H, bg_r, bg_g, bg_b, npix, image, final_t, pixstate);
   write_pixel(b, x, y + 1, W, H, bg_r, bg_g, bg_b, npix, image, final_t, pixstate);
@@ -754,14 +787,17 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-template <int NC>
+template <int NC, bool kHits>
 __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_half_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ ranks, const SplatRec* __restrict__ rec,
     const SplatAux* __restrict__ aux, const CamDev* __restrict__ cam_p, RasterDev rc, float bg_r, float bg_g,
     float bg_b, int64_t npix, const float* __restrict__ d_image, const float* __restrict__ final_t,
     const uint32_t* __restrict__ pixstate, const double* __restrict__ depth_g, double2* __restrict__ tile_cut,
-    float* __restrict__ partials, uint32_t k_cap) {
+    float* __restrict__ partials, uint32_t k_cap, const uint16_t* __restrict__ hits) {
   __shared__ StagedSplat s_sp[kBatch];
+  // kHits: the composite's hit masks of the batch entries, one 32-bit word per
+  // (quadrant, half) = its two 4x4 regions' 16-bit masks
+  __shared__ uint32_t s_hm[kHits ? kBatch : 1][8];
   __shared__ uint8_t s_mask[kBatch];
   __shared__ uint8_t s_list[kWarps][2][kBatch];
   __shared__ float s_red[kWarps][kBatch][NC];  // [warp][entry in batch][component]
@@ -804,6 +840,9 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
     }
     tile_cut[tile] = cut;
   }
+  // this lane's bit in its half's hit word: region column (lane & 7) >> 2,
+  // composite lane l8 = column % 4 + 4 (row % 4) / 2 (pixel a; b at + 8)
+  const int hbit = (((lane & 7) >> 2) << 4) + ((lane & 3) | (((lane >> 3) & 1) << 2));
   const uint32_t len = min(range.y - range.x, maxc);
   const uint32_t nbatch = (len + kBatch - 1) / kBatch;
 #if GSB_BWD_CPASYNC
@@ -852,7 +891,27 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
       const uint32_t tx0 = A.tx0_ty0 & 0xffffu, ty0 = A.tx0_ty0 >> 16, nx = A.nx_ny & 0xffffu;
       StagedSplat& S = s_sp[threadIdx.x];
       S.slot = A.off + ((uint32_t)ty - ty0) * nx + ((uint32_t)tx - tx0);
-      s_mask[threadIdx.x] = (uint8_t)half_mask(stage_splat(rec[r], ox, oy, rc.cutoff2_f, &S.geo, &S.app, &S.col_b));
+      const uint32_t bbox = half_mask(stage_splat(rec[r], ox, oy, rc.cutoff2_f, &S.geo, &S.app, &S.col_b));
+      if (kHits) {
+        // region r = 4 ry + rx; (quadrant q = qx + 2 qy, half h) holds regions
+        // 4 (2 qy + h) + 2 qx and + 1
+        const uint4* hp = reinterpret_cast<const uint4*>(hits + (size_t)e * 16);
+        const uint4 h0 = __ldg(hp), h1 = __ldg(hp + 1);
+        const uint32_t w[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};  // w[i] = regions 2i, 2i+1
+        uint32_t m = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int rg = 4 * (2 * (q >> 1) + h) + 2 * (q & 1);  // even: regions rg, rg + 1 = word rg / 2
+            const uint32_t word = w[rg >> 1];
+            s_hm[threadIdx.x][2 * q + h] = word;
+            if (word) m |= 1u << (2 * q + h);
+          }
+        s_mask[threadIdx.x] = (uint8_t)(m & bbox);
+      } else {
+        s_mask[threadIdx.x] = (uint8_t)bbox;
+      }
     }
 #endif
     __syncthreads();
@@ -880,8 +939,15 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
         const float dx = px - ge.x, dy = py - ge.y;
         const float ga = splat_power(ge.z, ge.w, ap.x, dx, dy);
         const float gb = splat_power(ge.z, ge.w, ap.x, dx, dy + 1.0f);
-        const bool ha = act && j < a.contrib && ga <= rc.cutoff2_f;
-        const bool hb = act && j < b.contrib && gb <= rc.cutoff2_f;
+        bool ha, hb;
+        if (kHits) {  // the composite's decisions (bits hb_sh, hb_sh + 8) gated by a non-zero upstream gradient
+          const uint32_t word = s_hm[k][2 * warp + half];
+          ha = act && a.contrib != 0u && ((word >> hbit) & 1u);
+          hb = act && b.contrib != 0u && ((word >> (hbit + 8)) & 1u);
+        } else {
+          ha = act && j < a.contrib && ga <= rc.cutoff2_f;
+          hb = act && j < b.contrib && gb <= rc.cutoff2_f;
+        }
         if (!__any_sync(kFull, ha || hb)) continue;  // neither half's entry touched: zero partials
 #if GSB_HALF_LDS_ASM
         const float cb = lds_f1(sa + 32u);
@@ -1149,14 +1215,20 @@ __global__ void __launch_bounds__(kQ4Threads, GSB_Q4_MIN_BLOCKS) backward_raster
   }
 }
 
+#ifndef GSB_BWD_HITS
+#define GSB_BWD_HITS 1  // pose-only K4a walks the composite's hit masks
+#endif
+
 int launch_composite(cudaStream_t st, gsb_frame* f, const RasterDev& rc) {
   const int n_tiles = f->tiles_x * f->tiles_y;
   const int64_t npix = (int64_t)f->width * f->height;
+  const bool hm = f->want_hits && GSB_BWD_HITS;
   if (n_tiles > 0)
-    composite_kernel<<<n_tiles, kThreads, 0, st>>>(
+    (hm ? composite_kernel<true> : composite_kernel<false>)<<<n_tiles, kThreads, 0, st>>>(
         f->ranges.as<uint2>(), f->list(), f->list_rec(), f->cam.as<CamDev>(), rc,
         (float)f->background[0], (float)f->background[1], (float)f->background[2], npix, f->image.as<float>(),
-        f->final_t.as<float>(), f->pixstate.as<uint32_t>());
+        f->final_t.as<float>(), f->pixstate.as<uint32_t>(), hm ? f->hits.as<uint16_t>() : nullptr,
+        (uint32_t)f->k_cap);
   GSB_CHECK_LAUNCH("composite_kernel");
   return GSB_OK;
 }
@@ -1165,9 +1237,8 @@ int launch_composite(cudaStream_t st, gsb_frame* f, const RasterDev& rc) {
 #ifndef GSB_BWD_HALF
 #define GSB_BWD_HALF 1
 #endif
-#ifndef GSB_BWD_HALF_FULL
-#define GSB_BWD_HALF_FULL 0  // the 9-component half variant measured slower for C4 (0.881 -> 0.903 ms per joint step)
-#endif
+// (the 9-component half-quadrant variant for the full gradient measured slower
+// for C4, 0.881 -> 0.903 ms per joint step, and was removed)
 int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc, bool pose_only) {
   const int n_tiles = f->tiles_x * f->tiles_y;
   const int64_t npix = (int64_t)f->width * f->height;
@@ -1180,9 +1251,18 @@ int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc, b
     GSB_CHECK_LAUNCH("backward_raster_q4_kernel");
     return GSB_OK;
   }
+  if (n_tiles > 0 && pose_only && GSB_BWD_HALF) {
+    const bool hm = f->want_hits && GSB_BWD_HITS;
+    (hm ? backward_raster_half_kernel<8, true> : backward_raster_half_kernel<8, false>)<<<n_tiles, kThreads, 0, st>>>(
+        f->ranges.as<uint2>(), f->list(), f->list_rec(), f->list_aux(), f->cam.as<CamDev>(), rc,
+        (float)f->background[0], (float)f->background[1], (float)f->background[2], npix, f->d_image.as<float>(),
+        f->final_t.as<float>(), f->pixstate.as<uint32_t>(), f->depth_g.as<double>(), f->tile_cut.as<double2>(),
+        f->partials.as<float>(), (uint32_t)f->k_cap, hm ? f->hits.as<uint16_t>() : nullptr);
+    GSB_CHECK_LAUNCH("backward_raster_half_kernel");
+    return GSB_OK;
+  }
   if (n_tiles > 0)
-    (pose_only ? (GSB_BWD_HALF ? backward_raster_half_kernel<8> : backward_raster_kernel<8>)
-               : (GSB_BWD_HALF_FULL ? backward_raster_half_kernel<kPartial> : backward_raster_kernel<kPartial>))
+    (pose_only ? backward_raster_kernel<8> : backward_raster_kernel<kPartial>)
         <<<n_tiles, kThreads, 0, st>>>(
         f->ranges.as<uint2>(), f->list(), f->list_rec(), f->list_aux(),
         f->cam.as<CamDev>(), rc, (float)f->background[0], (float)f->background[1], (float)f->background[2], npix,
@@ -1193,3 +1273,4 @@ int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc, b
 }
 
 }  // namespace gsb
+
