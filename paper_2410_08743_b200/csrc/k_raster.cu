@@ -207,15 +207,17 @@ __device__ __forceinline__ void composite_pair(PixFwd& a, PixFwd& b, const float
   const float gb = splat_power(ge.z, ge.w, ap.x, dx, dy + 1.0f);
   const bool ha = act && !pix_done(a, rc) && ga <= rc.cutoff2_f;
   const bool hb = act && !pix_done(b, rc) && gb <= rc.cutoff2_f;
-#if GSB_COMP_UNIFORM_SKIP
-  if (!__any_sync(kFull, ha || hb)) return;  // warp-uniform: lanes without a hit run the no-op update
-#else
-  if (!(ha || hb)) return;
-#endif
-  if (kHits) {
+  if (kHits) {  // the two ballots double as the warp-uniform skip test
     const uint32_t ba = __ballot_sync(kFull, ha), bb = __ballot_sync(kFull, hb);
+    if (!(ba | bb)) return;
     const int lane = threadIdx.x & 31, sh = lane & 24;
-    if ((lane & 7) == 0 && act) hrow[region] = (uint16_t)(((ba >> sh) & 0xffu) | (((bb >> sh) & 0xffu) << 8));
+    if ((lane & 7) == 0 && act) hrow[region] = (uint16_t)(__byte_perm(ba >> sh, bb >> sh, 0x0040));
+  } else {
+#if GSB_COMP_UNIFORM_SKIP
+    if (!__any_sync(kFull, ha || hb)) return;  // warp-uniform: lanes without a hit run the no-op update
+#else
+    if (!(ha || hb)) return;
+#endif
   }
   const float al_a = ha ? fminf(rc.alpha_clamp_f, ap.y * exp_neg_half(ga)) : 0.f;
   const float al_b = hb ? fminf(rc.alpha_clamp_f, ap.y * exp_neg_half(gb)) : 0.f;
@@ -787,8 +789,11 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+#ifndef GSB_BWD_HITS_MIN_BLOCKS
+#define GSB_BWD_HITS_MIN_BLOCKS 7  // the mask words cost registers: hold the 7 CTAs/SM of the bbox variant
+#endif
 template <int NC, bool kHits>
-__global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_half_kernel(
+__global__ void __launch_bounds__(kThreads, kHits ? GSB_BWD_HITS_MIN_BLOCKS : GSB_BWD_MIN_BLOCKS) backward_raster_half_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ ranks, const SplatRec* __restrict__ rec,
     const SplatAux* __restrict__ aux, const CamDev* __restrict__ cam_p, RasterDev rc, float bg_r, float bg_g,
     float bg_b, int64_t npix, const float* __restrict__ d_image, const float* __restrict__ final_t,
