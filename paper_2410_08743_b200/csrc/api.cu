@@ -52,6 +52,7 @@ int launch_tile_bin(cudaStream_t st, gsb_frame* f, int64_t n, int64_t* launches)
 size_t bin_hist_words(int64_t n, int n_tiles);
 int init_bin_attributes();
 int launch_composite(cudaStream_t st, gsb_frame* f, const RasterDev& rc);
+bool hit_masks_enabled();
 int build_export_tiles(cudaStream_t st, gsb_frame* f, int S);
 int launch_expected_depth(cudaStream_t st, gsb_frame* f, const RasterDev& rc, float* depth_out, float* weight_out);
 int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc, bool pose_only);
@@ -1053,7 +1054,7 @@ int gsb_render(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, const doub
   gsb_default_raster_config(&dflt);
   if (!cfg) cfg = &dflt;
   if (int r = validate_config(cfg)) return r;
-  f->want_hits = true;  // a pose-only gsb_render_backward may follow
+  f->want_hits = hit_masks_enabled();  // a pose-only gsb_render_backward may follow
   if (int r = frame_setup(ctx, f, cloud, cam, bg, cfg, true)) return r;
   const RasterDev rc = make_rasterdev(cfg);
   if (int r = render_sync(ctx, cloud, f, rc)) return r;
@@ -1765,7 +1766,7 @@ static gsb_frame* session_frame(gsb_ctx* ctx, gsb_session* s) { return s->own ? 
 static int session_frame_ready(gsb_ctx* ctx, gsb_session* s, gsb_frame** out) {
   gsb_frame* f = session_frame(ctx, s);
   f->lean = true;  // never exported (not reachable through gsb_frame_download)
-  f->want_hits = true;  // pose-only backward: K4a walks the composite's hit masks
+  f->want_hits = hit_masks_enabled();  // pose-only backward: K4a may walk the composite's hit masks
   if (int r = frame_setup(ctx, f, s->cloud, &s->cam, s->cfg.background, &s->cfg.raster, false)) return r;
   const int64_t want = f->k_cap > 0 ? f->k_cap : initial_k_cap(s->cloud->n);
   if (int r = frame_reserve(f, s->cloud, want)) return r;

@@ -790,7 +790,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 #ifndef GSB_BWD_HITS_MIN_BLOCKS
-#define GSB_BWD_HITS_MIN_BLOCKS 7  // the mask words cost registers: hold the 7 CTAs/SM of the bbox variant
+#define GSB_BWD_HITS_MIN_BLOCKS 6  // (7: 70 registers, 0.2168 ms; 6: 78 registers, 0.202 ms)
 #endif
 template <int NC, bool kHits>
 __global__ void __launch_bounds__(kThreads, kHits ? GSB_BWD_HITS_MIN_BLOCKS : GSB_BWD_MIN_BLOCKS) backward_raster_half_kernel(
@@ -1220,9 +1220,14 @@ __global__ void __launch_bounds__(kQ4Threads, GSB_Q4_MIN_BLOCKS) backward_raster
   }
 }
 
+// Hit masks (K3 records, pose-only K4a walks only entries that hit): measured
+// same box, C3 batch: K4a 0.218 -> 0.202 ms but the composite 0.103 -> 0.119 ms
+// (two ballots + a store per step and a 32-B block per entry): 2102 -> 2070
+// iters/s. Off; kept as an A/B knob (profiles/README.md).
 #ifndef GSB_BWD_HITS
-#define GSB_BWD_HITS 1  // pose-only K4a walks the composite's hit masks
+#define GSB_BWD_HITS 0
 #endif
+bool hit_masks_enabled() { return GSB_BWD_HITS != 0; }
 
 int launch_composite(cudaStream_t st, gsb_frame* f, const RasterDev& rc) {
   const int n_tiles = f->tiles_x * f->tiles_y;
