@@ -56,8 +56,9 @@ bool hit_masks_enabled();
 int build_export_tiles(cudaStream_t st, gsb_frame* f, int S);
 int launch_expected_depth(cudaStream_t st, gsb_frame* f, const RasterDev& rc, float* depth_out, float* weight_out);
 int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc, bool pose_only);
+int64_t bwd_geom_blocks(int64_t n);
 int launch_backward_geom(cudaStream_t st, const gsb_cloud* cloud, gsb_frame* f, const RasterDev& rc, bool full,
-                         float* grads, int64_t* launches);
+                         float* grads, int64_t* launches, bool reduce = true);
 int launch_rgb_loss(cudaStream_t st, const float* ren, const float* tgt, int W, int H, double beta, float* gmaps,
                     double* block_sums, double* out3, float* d_image, int64_t* launches, const float* mask_t = nullptr,
                     double mask_thr = 0.0, void* mask_ws = nullptr);
@@ -65,9 +66,9 @@ size_t loss_block_count(int W, int H);
 int init_loss_constants();
 int init_loss_attributes();
 int init_preprocess_attributes();
-int launch_pose_iter(cudaStream_t st, void* state, const double* dpose, const double* loss3, double lr_start,
-                     double lr_end, double eps, int budget, CamDev* cam, double* trace_pose, double* trace_loss,
-                     const uint32_t* k_dev, int64_t k_cap);
+int launch_pose_iter(cudaStream_t st, void* state, const double* pose_blocks, int64_t nb, double* dpose_out,
+                     const double* loss3, double lr_start, double lr_end, double eps, int budget, CamDev* cam,
+                     double* trace_pose, double* trace_loss, const uint32_t* k_dev, int64_t k_cap);
 int32_t pose_state_take_aborted(void* host_state, uint32_t* k_max, uint32_t* tile_ovf);
 int32_t pose_state_aborted(const void* host_state);
 size_t pose_state_bytes();
@@ -732,7 +733,8 @@ static int loss_device(gsb_ctx* ctx, gsb_frame* f, const float* target, double b
 }
 
 // Backward pass (buffers sized by frame_reserve).
-static int backward_device(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, bool full, float* grads) {
+static int backward_device(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, bool full, float* grads,
+                           bool reduce_pose = true) {
   const RasterDev rc = make_rasterdev(&f->config);
   {
     StageScope sc(ctx, kStBwdRaster);
@@ -741,7 +743,7 @@ static int backward_device(gsb_ctx* ctx, const gsb_cloud* cloud, gsb_frame* f, b
   }
   {
     StageScope sc(ctx, kStBwdGeom);
-    if (int r = launch_backward_geom(ctx->stream, cloud, f, rc, full, grads, &ctx->launches)) return r;
+    if (int r = launch_backward_geom(ctx->stream, cloud, f, rc, full, grads, &ctx->launches, reduce_pose)) return r;
   }
   return GSB_OK;
 }
@@ -1703,9 +1705,10 @@ static int session_launch_iteration(gsb_ctx* ctx, gsb_session* s, gsb_frame* f, 
     if (int r = render_async(ctx, s->cloud, f, rc)) return r;
   }
   if (int r = loss_device(ctx, f, s->target->planes.as<float>(), cfg.beta, true)) return r;
-  if (int r = backward_device(ctx, s->cloud, f, false, nullptr)) return r;
+  if (int r = backward_device(ctx, s->cloud, f, false, nullptr, /*reduce_pose=*/false)) return r;
   StageScope sc(ctx, kStOptim);
-  if (int r = launch_pose_iter(ctx->stream, s->state.p, f->d_pose.as<double>(), f->loss_val.as<double>(),
+  if (int r = launch_pose_iter(ctx->stream, s->state.p, f->pose_blocks.as<double>(), bwd_geom_blocks(s->cloud->n),
+                               f->d_pose.as<double>(), f->loss_val.as<double>(),
                                cfg.cam_lr_start, cfg.cam_lr_end, cfg.pose_converged_eps, cfg.budget,
                                s->camdev.as<CamDev>(), tp, tl, f->counters.as<uint32_t>() + 1, f->k_cap))
     return r;

@@ -105,6 +105,41 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+// Fixed-order sum of K4b's per-block pose partials (blocks[nb][6]) by a
+// 256-thread block: four blocks' partials per round in block order, then a
+// fixed binary tree — deterministic. Shared by pose_reduce_kernel and the
+// session's fused pose_iter_kernel, so both give the same bits. out (shared,
+// valid in thread 0): the 6-vector.
+__device__ __forceinline__ void block_reduce_pose(const double* __restrict__ blocks, int64_t nb,
+                                                  double (*s)[256], double out[6]) {
+  double t[6] = {0, 0, 0, 0, 0, 0};
+  for (int64_t b0 = threadIdx.x; b0 < nb; b0 += 4 * 256) {
+    double u[4][6];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t b = b0 + (int64_t)q * 256;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) u[q][k] = b < nb ? blocks[b * 6 + k] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) t[k] += u[q][k];
+  }
+#pragma unroll
+  for (int k = 0; k < 6; ++k) s[k][threadIdx.x] = t[k];
+  __syncthreads();
+  for (int h = 128; h > 0; h >>= 1) {
+    if (threadIdx.x < h) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) s[k][threadIdx.x] += s[k][threadIdx.x + h];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 6; ++k) out[k] = s[k][0];
+}
+
 // bytes: multiple of 16; src / dst 16-byte aligned.
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(

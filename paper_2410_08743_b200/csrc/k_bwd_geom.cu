@@ -372,37 +372,18 @@ __global__ void __launch_bounds__(kGeomBlock, (kFull ? GSB_GEOM_FULL_MIN_BLOCKS 
 __global__ void __launch_bounds__(256) pose_reduce_kernel(const double* __restrict__ blocks, int64_t nb,
                                                           double* __restrict__ out) {
   __shared__ double s[6][256];
-  double t[6] = {0, 0, 0, 0, 0, 0};
-  // four blocks' partials loaded per round (independent loads in flight),
-  // added in block order: the association is fixed, so the sum is deterministic
-  for (int64_t b0 = threadIdx.x; b0 < nb; b0 += 4 * 256) {
-    double u[4][6];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int64_t b = b0 + (int64_t)q * 256;
-#pragma unroll
-      for (int k = 0; k < 6; ++k) u[q][k] = b < nb ? blocks[b * 6 + k] : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-      for (int k = 0; k < 6; ++k) t[k] += u[q][k];
-  }
-#pragma unroll
-  for (int k = 0; k < 6; ++k) s[k][threadIdx.x] = t[k];
-  __syncthreads();
-  for (int h = 128; h > 0; h >>= 1) {
-    if (threadIdx.x < h) {
-#pragma unroll
-      for (int k = 0; k < 6; ++k) s[k][threadIdx.x] += s[k][threadIdx.x + h];
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x < 6) out[threadIdx.x] = s[threadIdx.x][0];
+  double r[6];
+  block_reduce_pose(blocks, nb, s, r);
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 6; ++k) out[k] = r[k];
 }
 
+int64_t bwd_geom_blocks(int64_t n) { return (n + kGeomBlock - 1) / kGeomBlock; }
+
+// reduce = false: the pose 6-vector stays as per-block partials in
+// f->pose_blocks (a session's pose_iter_kernel sums them itself).
 int launch_backward_geom(cudaStream_t st, const gsb_cloud* cloud, gsb_frame* f, const RasterDev& rc, bool full,
-                         float* grads, int64_t* launches) {
+                         float* grads, int64_t* launches, bool reduce) {
   const int64_t n = cloud->n;
   EntryCut cutd;
   cutd.tile_cut = f->tile_cut.as<double2>();
@@ -423,8 +404,8 @@ int launch_backward_geom(cudaStream_t st, const gsb_cloud* cloud, gsb_frame* f, 
           rc, f->cnt_g.as<uint32_t>(), f->off_g.as<uint32_t>(), f->colj.as<float>(), f->partials.as<float>(), f->k_cap, cutd, nullptr,
           f->pose_blocks.as<double>());
   }
-  pose_reduce_kernel<<<1, 256, 0, st>>>(f->pose_blocks.as<double>(), nb, f->d_pose.as<double>());
-  *launches += nb > 0 ? 2 : 1;
+  if (reduce) pose_reduce_kernel<<<1, 256, 0, st>>>(f->pose_blocks.as<double>(), nb, f->d_pose.as<double>());
+  *launches += (nb > 0 ? 1 : 0) + (reduce ? 1 : 0);
   GSB_CHECK_LAUNCH("backward_geom_kernel");
   return GSB_OK;
 }

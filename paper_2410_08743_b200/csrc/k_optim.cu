@@ -213,9 +213,20 @@ __device__ void d_write_cam(const PoseState& s, CamDev* cam) {
 }
 
 // One pose_descent iteration tail (after render + loss + backward).
-__global__ void pose_iter_kernel(PoseState* st, const double* __restrict__ dpose, const double* __restrict__ loss3,
-                                 PoseCtl ctl, CamDev* cam, double* trace_pose, double* trace_loss,
-                                 const uint32_t* __restrict__ k_dev, int64_t k_cap) {
+// One 256-thread block: the d_pose reduction of K4b's block partials
+// (block_reduce_pose, the same fixed order as pose_reduce_kernel) fused in
+// front of the pose step, which thread 0 runs. d_pose is also written to
+// dpose_out for the session's readers.
+__global__ void __launch_bounds__(256) pose_iter_kernel(PoseState* st, const double* __restrict__ pose_blocks,
+                                                        int64_t nb, double* __restrict__ dpose_out,
+                                                        const double* __restrict__ loss3, PoseCtl ctl, CamDev* cam,
+                                                        double* trace_pose, double* trace_loss,
+                                                        const uint32_t* __restrict__ k_dev, int64_t k_cap) {
+  __shared__ double s_red[6][256];
+  double dpose[6];
+  block_reduce_pose(pose_blocks, nb, s_red, dpose);
+  if (threadIdx.x != 0) return;
+  for (int k = 0; k < 6; ++k) dpose_out[k] = dpose[k];
   PoseState s = *st;
   if (s.stop) return;
   // k_dev = {K, tile overflow flag}: the entry capacity or the per-tile sort
@@ -702,12 +713,12 @@ void joint_state_clear_abort(void* host) {
 }
 
 // ------------------------------------------------------------- host glue
-int launch_pose_iter(cudaStream_t st, void* state, const double* dpose, const double* loss3, double lr_start,
-                     double lr_end, double eps, int budget, CamDev* cam, double* trace_pose, double* trace_loss,
-                     const uint32_t* k_dev, int64_t k_cap) {
+int launch_pose_iter(cudaStream_t st, void* state, const double* pose_blocks, int64_t nb, double* dpose_out,
+                     const double* loss3, double lr_start, double lr_end, double eps, int budget, CamDev* cam,
+                     double* trace_pose, double* trace_loss, const uint32_t* k_dev, int64_t k_cap) {
   PoseCtl ctl{lr_start, lr_end, eps, budget, 0};
-  pose_iter_kernel<<<1, 1, 0, st>>>(static_cast<PoseState*>(state), dpose, loss3, ctl, cam, trace_pose, trace_loss,
-                                    k_dev, k_cap);
+  pose_iter_kernel<<<1, 256, 0, st>>>(static_cast<PoseState*>(state), pose_blocks, nb, dpose_out, loss3, ctl, cam,
+                                      trace_pose, trace_loss, k_dev, k_cap);
   GSB_CHECK_LAUNCH("pose_iter_kernel");
   return GSB_OK;
 }
