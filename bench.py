@@ -183,12 +183,11 @@ def run_ours(args, ws, rank, local):
     discarded = batch.discarded() - discarded0
     if discarded:
         raise RuntimeError(f"{discarded} iteration(s) discarded for entry-capacity growth inside the timed region")
-    # Attribution: per-stage device times of the SAME batch graph (every branch
-    # brackets its stages with event nodes, so a stage's time is its duration
-    # inside the concurrent batch), K more replays read back one by one. The
-    # shared multi-view preprocess runs before the fork and is timed by ctx
-    # events around it in a separate replay set. Then the solo durations:
-    # sessions' own graphs one at a time (no overlap), for context.
+    # Attribution (untimed, after the timed region): per-stage CUDA event
+    # nodes (1) inside every branch of the same batch graph ("live": branch
+    # wall time, queueing behind the other branches included) and (2) around
+    # every stage of each session's own graph run one at a time ("solo": the
+    # kernel durations the roofline uses).
     ctx.set_profiling(True)
     batch.step_async(1)  # recaptures the batch graph with event nodes (untimed)
     batch.sync()
@@ -215,10 +214,7 @@ def run_ours(args, ws, rank, local):
                 solo_tot[k] = solo_tot.get(k, 0.0) + v
     solo_ms = ctx.timer_stop()
     ctx.set_profiling(False)
-    stages = {k: (v, 1) for k, v in live_tot.items()}
-    solo_stages = {k: v for k, v in solo_tot.items()}
     if dist:
-        import torch
         dev_ms = _reduce_max(dist, dev_ms, local)
     iters = VIEWS_PER_GPU * ws * args.steps
     value = iters / (dev_ms / 1e3)
@@ -250,7 +246,6 @@ def run_ours(args, ws, rank, local):
     ctx.synchronize()
     e2e_s = time.perf_counter() - t0
     if dist:
-        import torch
         e2e_s = _reduce_max(dist, e2e_s, local)
     e2e_value = VIEWS_PER_GPU * ws * e2e_iters / e2e_s
 
@@ -259,14 +254,9 @@ def run_ours(args, ws, rank, local):
     c3_job = None if args.no_c3_job else run_c3_job(args, ws, rank, local, ctx, cloud, gt, init, intr)
     out = None
     if rank == 0:
-        # roofline for the dominant stage
-        # Kernel durations for the roofline come from the solo pass (each
-        # session's own graph, one at a time, event nodes around every stage):
-        # event nodes inside the concurrent batch's branches also time the
-        # queueing behind other branches' kernels, so they bound nothing; they
-        # are reported as "live" for reference only.
-        per_iter_stage_ms = {k: v / (VIEWS_PER_GPU * args.steps) for k, v in solo_stages.items()}
-        live_stage_ms = {k: v[0] / (VIEWS_PER_GPU * args.steps) for k, v in stages.items() if v[1] > 0}
+        # roofline for the dominant stage, from the solo kernel durations
+        per_iter_stage_ms = {k: v / (VIEWS_PER_GPU * args.steps) for k, v in solo_tot.items()}
+        live_stage_ms = {k: v / (VIEWS_PER_GPU * args.steps) for k, v in live_tot.items()}
         dom = max(per_iter_stage_ms, key=per_iter_stage_ms.get)
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
             os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
@@ -397,7 +387,6 @@ def run_joint(args, ws, rank, local, dist):
     j.step(args.steps)
     ms = ctx.timer_stop()
     if dist:
-        import torch
         ms = _reduce_max(dist, ms, local)
     res = j.read()
     j.close()
