@@ -87,6 +87,7 @@ int launch_joint_slot_end(cudaStream_t st, const JointCtl& ctl, int b, const dou
                           const uint32_t* counters, int64_t k_cap, double* xchg);
 int launch_joint_sum(cudaStream_t st, float* g0, const float* rest, int64_t len, int nrest, int64_t stride);
 int64_t joint_adam_blocks(int64_t n);
+int64_t joint_red_doubles(int64_t n);
 int launch_joint_adam(cudaStream_t st, float* params, const float* grads, float* m, float* v, int64_t n,
                       int64_t n_pad, const void* js, const JointCtl& ctl, const double* xchg, double* red_blocks);
 int launch_joint_finalize(cudaStream_t st, void* js, const int32_t* seq, const JointCtl& ctl, const double* xchg,
@@ -2724,7 +2725,7 @@ static int joint_size_buffers(gsb_ctx* ctx, gsb_joint* j) {
   const int np = num_planes(j->cloud->sh_degree);
   j->glen = (int64_t)(np + 2) * j->cloud->n_pad;
   GSB_CUDA(j->grads.reserve(sizeof(float) * j->glen * j->local));
-  GSB_CUDA(j->red.reserve(sizeof(double) * 2 * joint_adam_blocks(n)));
+  GSB_CUDA(j->red.reserve(sizeof(double) * joint_red_doubles(n)));
   GSB_CUDA(cudaMemsetAsync(j->grads.p, 0, sizeof(float) * j->glen * j->local, ctx->stream));
   if (joint_accumulates(j)) {
     GSB_CUDA(j->acc_sum.reserve(sizeof(double) * n));
@@ -2795,7 +2796,7 @@ static int joint_launch_step(gsb_ctx* ctx, gsb_joint* j) {
                                     j->red.as<double>(), nb, j->poses.p, j->cams.as<CamDev>(),
                                     j->trace_total.as<double>(), j->trace_l1.as<double>()))
     return r;
-  ctx->launches += 2;
+  ctx->launches += 3;  // joint_adam, joint_adam_sh, joint_finalize
   return GSB_OK;
 }
 

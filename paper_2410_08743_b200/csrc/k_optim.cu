@@ -308,6 +308,20 @@ __global__ void adam_f64_kernel(double* __restrict__ p, const double* __restrict
   p[i] = __dsub_rn(p[i], step);
 }
 
+// CloudAdam's element update (pipelines.cpp:18-41) on an FP32 plane entry;
+// one definition for every kernel that steps cloud planes. Every operation is
+// an explicitly rounded intrinsic, so the result does not depend on how the
+// compiler contracts the expression in a given unrolling. Returns the new
+// parameter.
+__device__ __forceinline__ float adam_f32(float& m, float& v, float p, float gi, float lr, float bc1, float bc2) {
+  const float mi = __fmaf_rn(m, 0.9f, __fmul_rn(gi, 0.1f));                    // 0.9 m + 0.1 g
+  const float vi = __fmaf_rn(v, 0.999f, __fmul_rn(gi, __fmul_rn(gi, 0.001f)));  // 0.999 v + 0.001 g g
+  m = mi;
+  v = vi;
+  const float den = __fadd_rn(__fsqrt_rn(__fdiv_rn(vi, bc2)), 1e-15f);
+  return __fsub_rn(p, __fdiv_rn(__fmul_rn(lr, __fdiv_rn(mi, bc1)), den));
+}
+
 struct AdamCoef {
   float lr[6];  // pos, rot, scale, opacity, sh_dc, sh_rest
   float bc1[5], bc2[5];
@@ -321,30 +335,29 @@ __global__ void __launch_bounds__(256) cloud_adam_kernel(float* __restrict__ par
   if (i >= n) return;
   bool quat_moved = false;
   float q[4];
-  for (int p = 0; p < nplanes; ++p) {
+  auto step = [&](int p, int grp, float lr) {
     const int64_t k = (int64_t)p * n_pad + i;
-    int grp;
-    float lr;
-    if (p < kQuatW) { grp = 0; lr = c.lr[0]; }
-    else if (p < kScaleX) { grp = 1; lr = c.lr[1]; }
-    else if (p < kOpacity) { grp = 2; lr = c.lr[2]; }
-    else if (p == kOpacity) { grp = 3; lr = c.lr[3]; }
-    else { grp = 4; lr = ((p - kShBase) % basis == 0) ? c.lr[4] : c.lr[5]; }
-    const float gi = grads[k];
-    const float mi = 0.9f * m[k] + 0.1f * gi;
-    const float vi = 0.999f * v[k] + 0.001f * gi * gi;
-    m[k] = mi;
-    v[k] = vi;
+    float mk = m[k], vk = v[k];
     const float old = params[k];
-    const float nw = old - lr * (mi / c.bc1[grp]) / (sqrtf(vi / c.bc2[grp]) + 1e-15f);
+    const float nw = adam_f32(mk, vk, old, grads[k], lr, c.bc1[grp], c.bc2[grp]);
+    m[k] = mk;
+    v[k] = vk;
     params[k] = nw;
     if (grp == 1) {
       q[p - kQuatW] = nw;
       quat_moved = quat_moved || (nw != old);
     }
+  };
+  // geometry / opacity planes unrolled (constant group indices: no local memory)
+#pragma unroll
+  for (int p = 0; p < kShBase; ++p) {
+    const int grp = p < kQuatW ? 0 : p < kScaleX ? 1 : p < kOpacity ? 2 : 3;
+    step(p, grp, c.lr[grp]);
   }
+  for (int p = kShBase; p < nplanes; ++p) step(p, 4, ((p - kShBase) % basis == 0) ? c.lr[4] : c.lr[5]);
   if (quat_moved) {  // pipelines.cpp:36-40
     const float nn = sqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+#pragma unroll
     for (int k = 0; k < 4; ++k) params[(int64_t)(kQuatW + k) * n_pad + i] = q[k] / nn;
   }
 }
@@ -476,12 +489,19 @@ __global__ void grad_accum_commit_kernel(const double* __restrict__ stage, int l
 // step is discarded (some slot overflowed its entry capacity) or has already
 // run out of iterations.
 constexpr int kJointBlock = 256;
+// The step's Adam coefficients, written by the geometry kernel's block 0 for
+// the SH kernel (stored behind the block partials in the reduction buffer).
+struct JointCoef {
+  float lr_dc, lr_rest, bc1, bc2, inv_s;
+  int skip;
+};
 __global__ void __launch_bounds__(kJointBlock) joint_adam_kernel(float* __restrict__ params,
                                                                const float* __restrict__ grads, float* __restrict__ m,
                                                                float* __restrict__ v, int64_t n, int64_t n_pad,
                                                                const JointDev* __restrict__ js, JointCtl ctl,
                                                                const double* __restrict__ xchg,
-                                                               double* __restrict__ red_blocks) {
+                                                               double* __restrict__ red_blocks,
+                                                               JointCoef* __restrict__ coef) {
   __shared__ float s_lr[6], s_bc1, s_bc2;
   __shared__ int s_skip, s_opl1;
   __shared__ double s_red[kJointBlock / 32][2];
@@ -498,6 +518,7 @@ __global__ void __launch_bounds__(kJointBlock) joint_adam_kernel(float* __restri
     s_lr[3] = (float)ctl.opacity_lr;
     s_lr[4] = (float)ctl.sh_dc_lr;
     s_lr[5] = (float)ctl.sh_rest_lr;
+    if (blockIdx.x == 0) *coef = JointCoef{s_lr[4], s_lr[5], s_bc1, s_bc2, (float)ctl.inv_slots, s_skip};
   }
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -507,17 +528,24 @@ __global__ void __launch_bounds__(kJointBlock) joint_adam_kernel(float* __restri
     // anisotropy_loss (losses.cpp:217-244) on the pre-step log-scales
     double sc[3];
     for (int k = 0; k < 3; ++k) sc[k] = exp((double)params[(int64_t)(kScaleX + k) * n_pad + i]);
+    // first arg-max / arg-min, tracked in registers (no local memory)
     int amax = 0, amin = 0;
+    double smax = sc[0], smin = sc[0];
+#pragma unroll
     for (int k = 1; k < 3; ++k) {
-      if (sc[k] > sc[amax]) amax = k;
-      if (sc[k] < sc[amin]) amin = k;
+      if (sc[k] > smax) { amax = k; smax = sc[k]; }
+      if (sc[k] < smin) { amin = k; smin = sc[k]; }
     }
-    const double r = sc[amax] / sc[amin];
+    const double r = smax / smin;
     double dls[3] = {0.0, 0.0, 0.0};
     if (r > ctl.aniso_ratio) {
       aniso = (r - ctl.aniso_ratio) * inv_n;
-      dls[amax] += inv_n / sc[amin] * sc[amax];
-      dls[amin] += -inv_n * sc[amax] / (sc[amin] * sc[amin]) * sc[amin];
+      const double dmax = inv_n / smin * smax, dmin = -inv_n * smax / (smin * smin) * smin;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        if (amax == k) dls[k] += dmax;
+        if (amin == k) dls[k] += dmin;
+      }
     }
     // opacity_l1 (losses.cpp:246-257) through the sigmoid (pipelines.cpp:148-157)
     const double o = 1.0 / (1.0 + exp(-(double)params[(int64_t)kOpacity * n_pad + i]));
@@ -532,30 +560,22 @@ __global__ void __launch_bounds__(kJointBlock) joint_adam_kernel(float* __restri
         float gi = grads[k] * inv_s;
         if (p >= kScaleX && p < kOpacity) gi = (float)((double)gi + dls[p - kScaleX]);
         if (p == kOpacity) gi = (float)((double)gi + dop);
-        const float mi = 0.9f * m[k] + 0.1f * gi;
-        const float vi = 0.999f * v[k] + 0.001f * gi * gi;
-        m[k] = mi;
-        v[k] = vi;
+        float mk = m[k], vk = v[k];
         const float old = params[k];
-        const float nw = old - lr * (mi / s_bc1) / (sqrtf(vi / s_bc2) + 1e-15f);
+        const float nw = adam_f32(mk, vk, old, gi, lr, s_bc1, s_bc2);
+        m[k] = mk;
+        v[k] = vk;
         params[k] = nw;
         if (p >= kQuatW && p < kScaleX) {
           q[p - kQuatW] = nw;
           quat_moved = quat_moved || (nw != old);
         }
       };
-      // geometry / opacity planes (fixed count, unrolled)
+      // geometry / opacity planes (fixed count, unrolled); the SH planes are
+      // joint_adam_sh_kernel's
 #pragma unroll
       for (int p = 0; p < kShBase; ++p)
         step(p, p < kQuatW ? s_lr[0] : p < kScaleX ? s_lr[1] : p < kOpacity ? s_lr[2] : s_lr[3]);
-      // SH planes c * basis + b: DC band at b == 0 (pipelines.cpp:33); unrolled
-      // so that several planes' loads are in flight per thread
-      for (int c = 0; c < 3; ++c) {
-        const int p0 = kShBase + c * ctl.basis;
-        step(p0, s_lr[4]);
-#pragma unroll 4
-        for (int b = 1; b < ctl.basis; ++b) step(p0 + b, s_lr[5]);
-      }
       if (quat_moved) {  // pipelines.cpp:36-40
         const float nn = sqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
         for (int k = 0; k < 4; ++k) params[(int64_t)(kQuatW + k) * n_pad + i] = q[k] / nn;
@@ -582,6 +602,82 @@ __global__ void __launch_bounds__(kJointBlock) joint_adam_kernel(float* __restri
     }
     red_blocks[2 * blockIdx.x] = a;
     red_blocks[2 * blockIdx.x + 1] = b;
+  }
+}
+
+// The SH planes' Adam update (same arithmetic as the geometry kernel's
+// `step`): plain streaming over 3 * basis planes, blockIdx.y picks
+// kShPlanesPerThread of them, so that every thread has 4 × that many
+// independent loads in flight. Plane c * basis + b is the DC band at b == 0
+// (pipelines.cpp:33).
+#ifndef GSB_SH_PPT
+#define GSB_SH_PPT 1
+#endif
+#ifndef GSB_SH_VEC
+#define GSB_SH_VEC 1
+#endif
+constexpr int kShPlanesPerThread = GSB_SH_PPT;
+constexpr int kShVec = GSB_SH_VEC ? 4 : 1;  // consecutive Gaussians per thread (float4 accesses)
+__global__ void __launch_bounds__(kJointBlock) joint_adam_sh_kernel(float* __restrict__ params,
+                                                                  const float* __restrict__ grads,
+                                                                  float* __restrict__ m, float* __restrict__ v,
+                                                                  int64_t n, int64_t n_pad, int basis,
+                                                                  const JointCoef* __restrict__ coef) {
+  const JointCoef c = *coef;
+  const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kShVec;
+  if (c.skip || i0 >= n) return;
+  const int q0 = blockIdx.y * kShPlanesPerThread, nsh = 3 * basis;
+  if (kShVec == 4 && i0 + 4 <= n) {  // n_pad % 32 == 0: every plane row is 16-B aligned
+    float4 g[kShPlanesPerThread], mo[kShPlanesPerThread], vo[kShPlanesPerThread], po[kShPlanesPerThread];
+#pragma unroll
+    for (int u = 0; u < kShPlanesPerThread; ++u) {
+      if (q0 + u < nsh) {
+        const int64_t k = (int64_t)(kShBase + q0 + u) * n_pad + i0;
+        g[u] = __ldcs(reinterpret_cast<const float4*>(grads + k));
+        mo[u] = __ldcs(reinterpret_cast<const float4*>(m + k));
+        vo[u] = __ldcs(reinterpret_cast<const float4*>(v + k));
+        po[u] = *reinterpret_cast<const float4*>(params + k);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kShPlanesPerThread; ++u) {
+      if (q0 + u < nsh) {
+        const int64_t k = (int64_t)(kShBase + q0 + u) * n_pad + i0;
+        const float lr = ((q0 + u) % basis == 0) ? c.lr_dc : c.lr_rest;
+        float4 np;
+        np.x = adam_f32(mo[u].x, vo[u].x, po[u].x, g[u].x * c.inv_s, lr, c.bc1, c.bc2);
+        np.y = adam_f32(mo[u].y, vo[u].y, po[u].y, g[u].y * c.inv_s, lr, c.bc1, c.bc2);
+        np.z = adam_f32(mo[u].z, vo[u].z, po[u].z, g[u].z * c.inv_s, lr, c.bc1, c.bc2);
+        np.w = adam_f32(mo[u].w, vo[u].w, po[u].w, g[u].w * c.inv_s, lr, c.bc1, c.bc2);
+        *reinterpret_cast<float4*>(params + k) = np;
+        __stcs(reinterpret_cast<float4*>(m + k), mo[u]);
+        __stcs(reinterpret_cast<float4*>(v + k), vo[u]);
+      }
+    }
+    return;
+  }
+  for (int64_t i = i0; i < i0 + kShVec && i < n; ++i) {
+    float g[kShPlanesPerThread], mo[kShPlanesPerThread], vo[kShPlanesPerThread], po[kShPlanesPerThread];
+#pragma unroll
+    for (int u = 0; u < kShPlanesPerThread; ++u) {
+      if (q0 + u < nsh) {
+        const int64_t k = (int64_t)(kShBase + q0 + u) * n_pad + i;
+        g[u] = grads[k];
+        mo[u] = m[k];
+        vo[u] = v[k];
+        po[u] = params[k];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kShPlanesPerThread; ++u) {
+      if (q0 + u < nsh) {
+        const int64_t k = (int64_t)(kShBase + q0 + u) * n_pad + i;
+        const float lr = ((q0 + u) % basis == 0) ? c.lr_dc : c.lr_rest;
+        params[k] = adam_f32(mo[u], vo[u], po[u], g[u] * c.inv_s, lr, c.bc1, c.bc2);
+        m[k] = mo[u];
+        v[k] = vo[u];
+      }
+    }
   }
 }
 
@@ -677,13 +773,21 @@ int launch_grad_accum_commit(cudaStream_t st, const double* stage, int local, in
   return GSB_OK;
 }
 int64_t joint_adam_blocks(int64_t n) { return (n + kJointBlock - 1) / kJointBlock; }
+int64_t joint_red_doubles(int64_t n) { return 2 * joint_adam_blocks(n) + 4; }
+
 int launch_joint_adam(cudaStream_t st, float* params, const float* grads, float* m, float* v, int64_t n,
                       int64_t n_pad, const void* js, const JointCtl& ctl, const double* xchg, double* red_blocks) {
   const int64_t nb = joint_adam_blocks(n);
-  if (nb > 0)
-    joint_adam_kernel<<<(unsigned)nb, kJointBlock, 0, st>>>(params, grads, m, v, n, n_pad,
-                                                            static_cast<const JointDev*>(js), ctl, xchg, red_blocks);
+  if (nb <= 0) return GSB_OK;
+  static_assert(sizeof(JointCoef) <= 4 * sizeof(double), "joint_red_doubles");
+  JointCoef* coef = reinterpret_cast<JointCoef*>(red_blocks + 2 * nb);
+  joint_adam_kernel<<<(unsigned)nb, kJointBlock, 0, st>>>(params, grads, m, v, n, n_pad,
+                                                          static_cast<const JointDev*>(js), ctl, xchg, red_blocks, coef);
   GSB_CHECK_LAUNCH("joint_adam_kernel");
+  const dim3 grid((unsigned)((n + (int64_t)kJointBlock * kShVec - 1) / ((int64_t)kJointBlock * kShVec)),
+                  (unsigned)((3 * ctl.basis + kShPlanesPerThread - 1) / kShPlanesPerThread));
+  joint_adam_sh_kernel<<<grid, kJointBlock, 0, st>>>(params, grads, m, v, n, n_pad, ctl.basis, coef);
+  GSB_CHECK_LAUNCH("joint_adam_sh_kernel");
   return GSB_OK;
 }
 int launch_joint_finalize(cudaStream_t st, void* js, const int32_t* seq, const JointCtl& ctl, const double* xchg,

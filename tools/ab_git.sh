@@ -9,6 +9,16 @@ if [ "${1:-}" = "prep" ]; then
   exit $?
 fi
 mkdir -p gpurun_out
+if [ "${1:-}" = "runj" ]; then  # the C4 joint step: ms per step and the final loss (must match bitwise)
+  for rep in 1 2; do
+    for side in base head; do
+      dir=.; [ $side = base ] && dir=.ab_base
+      (cd $dir && timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --e2e-iters 8) > gpurun_out/abj_$side.json 2> gpurun_out/abj_$side.err
+      python -c "import json; d=json.loads(open('gpurun_out/abj_$side.json').read().strip().splitlines()[-1]); j=d['joint_c4']; print('$side', j['ms_per_step'], repr(j['final_total_loss']))" || tail -5 gpurun_out/abj_$side.err
+    done
+  done
+  exit 0
+fi
 for rep in 1 2; do
   for side in base head; do
     dir=.; [ $side = base ] && dir=.ab_base
