@@ -106,9 +106,54 @@ __device__ __forceinline__ void stage_planes(float (*dst)[kSH][kSW + 1], const f
 #define GSB_LOSS_HR 4
 #endif
 constexpr int kHR = GSB_LOSS_HR;
+// GSB_LOSS_HSPLIT: the 42 x 8 (row, column group) tasks are split three ways
+// — (mu_a, E[a^2]) from a, (mu_b, E[b^2]) from b, E[ab] from both — so the
+// 1008 tasks fill 4 rounds of 256 threads (98 %) instead of 336 filling 2
+// rounds (66 %); every output keeps its tap order (bit-identical).
+#ifndef GSB_LOSS_HSPLIT
+#define GSB_LOSS_HSPLIT 0  // measured slower (K6 0.073 -> 0.075 ms): the extra LDS outweigh the balance
+#endif
+template <int N>
+__device__ __forceinline__ void hconv(const float* f, float* acc) {
+#pragma unroll
+  for (int j = 0; j < kHR; ++j) acc[j] = 0.f;
+#pragma unroll
+  for (int k = 0; k < kHR + kWin - 1; ++k)
+#pragma unroll
+    for (int j = 0; j < kHR; ++j)
+      if (k - j >= 0 && k - j < kWin) acc[j] = fmaf(c_win[k - j], f[k], acc[j]);
+}
 template <int PITCH, int XOFF>
 __device__ __forceinline__ void hpass5(const float* __restrict__ st0, const float* __restrict__ st1,
                                        float (*hq)[kSH][kTW + 1]) {
+#if GSB_LOSS_HSPLIT
+  constexpr int kGroups = kSH * (kTW / kHR), kL = kHR + kWin - 1;
+  for (int task = threadIdx.x; task < 3 * kGroups; task += kThr) {
+    const int t = task >= 2 * kGroups ? 2 : task >= kGroups ? 1 : 0, g = task - t * kGroups;
+    const int r = g / (kTW / kHR), q0 = (g - r * (kTW / kHR)) * kHR;
+    float acc[kHR], f[kL];
+    if (t < 2) {
+      const float* st = t ? st1 : st0;
+      float x[kL];
+#pragma unroll
+      for (int k = 0; k < kL; ++k) x[k] = st[r * PITCH + XOFF + q0 + k];
+      hconv<kL>(x, acc);
+#pragma unroll
+      for (int j = 0; j < kHR; ++j) hq[t][r][q0 + j] = acc[j];
+#pragma unroll
+      for (int k = 0; k < kL; ++k) f[k] = x[k] * x[k];
+      hconv<kL>(f, acc);
+#pragma unroll
+      for (int j = 0; j < kHR; ++j) hq[2 + t][r][q0 + j] = acc[j];
+    } else {
+#pragma unroll
+      for (int k = 0; k < kL; ++k) f[k] = st0[r * PITCH + XOFF + q0 + k] * st1[r * PITCH + XOFF + q0 + k];
+      hconv<kL>(f, acc);
+#pragma unroll
+      for (int j = 0; j < kHR; ++j) hq[4][r][q0 + j] = acc[j];
+    }
+  }
+#else
   for (int task = threadIdx.x; task < kSH * (kTW / kHR); task += kThr) {
     const int r = task / (kTW / kHR), q0 = (task - r * (kTW / kHR)) * kHR;
     float x[kHR + kWin - 1], y[kHR + kWin - 1];
@@ -133,8 +178,12 @@ __device__ __forceinline__ void hpass5(const float* __restrict__ st0, const floa
       for (int j = 0; j < kHR; ++j) hq[m][r][q0 + j] = acc[j];
     }
   }
+#endif
 }
 
+#ifndef GSB_LOSS_RCP
+#define GSB_LOSS_RCP 1
+#endif
 #ifdef GSB_LOSS_MIN_BLOCKS
 #define GSB_LOSS_BOUNDS __launch_bounds__(kThr, GSB_LOSS_MIN_BLOCKS)
 #else
@@ -151,6 +200,14 @@ constexpr int kTP = 48;                        // TMA window pitch (floats; 192 
 constexpr int kTX = 3;                         // column of the halo window inside the box
 constexpr uint32_t kTWinBytes = kSH * kTP * 4u;  // bytes one TMA window load delivers (8064)
 constexpr int kTWin = (kSH * kTP + 31) / 32 * 32;  // window stride in shared memory: 128-byte aligned destinations
+// TMA window buffers per kernel: 2 = the next channel's windows load into the
+// other buffer while this one is convolved; 1 = one buffer, reloaded as soon
+// as the horizontal pass has consumed it (less shared memory: one more CTA
+// per SM)
+#ifndef GSB_LOSS_TMA_BUFS
+#define GSB_LOSS_TMA_BUFS 1  // (2: same K6 time, 16 KB more shared memory per CTA)
+#endif
+constexpr int kBufs = GSB_LOSS_TMA_BUFS;
 
 __device__ __forceinline__ void tma_load_3d(float* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
   asm volatile(
@@ -176,7 +233,7 @@ __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* win = reinterpret_cast<float*>(smem_raw);  // [buffers][2 planes][WIN]
   float(*hq)[kSH][kTW + 1] =
-      reinterpret_cast<float(*)[kSH][kTW + 1]>(smem_raw + sizeof(float) * (kTma ? 4 : 2) * WIN);
+      reinterpret_cast<float(*)[kSH][kTW + 1]>(smem_raw + sizeof(float) * (kTma ? 2 * kBufs : 2) * WIN);
   __shared__ double s_tmp[kThr / 32];
   __shared__ __align__(8) uint64_t bar[2];
   const int64_t P = (int64_t)W * H;
@@ -196,7 +253,10 @@ __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, 
   double l1 = 0.0, ss = 0.0;
   for (int ch = 0; ch < 3; ++ch) {
     const float* st0;
-    if (kTma) {
+    if (kTma && kBufs == 1) {
+      mbar_wait(&bar[0], (uint32_t)(ch & 1));
+      st0 = win;
+    } else if (kTma) {
       if (threadIdx.x == 0 && ch + 1 < 3) {  // next channel into the other buffer
         float* nb = win + ((ch + 1) & 1) * 2 * kTWin;
         fence_proxy_async();
@@ -214,7 +274,20 @@ __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, 
     }
     const float* st1 = st0 + WIN;
     hpass5<PITCH, kTma ? kTX : 0>(st0, st1, hq);
+    float av[kR], bv[kR];  // this thread's output pixels of both images
+#pragma unroll
+    for (int j = 0; j < kR; ++j) {
+      const int o = (rg * kR + j + kHalf) * PITCH + (kTma ? kTX : 0) + c + kHalf;
+      av[j] = st0[o];
+      bv[j] = st1[o];
+    }
     __syncthreads();
+    if (kTma && kBufs == 1 && threadIdx.x == 0 && ch + 1 < 3) {  // window consumed: next channel into it
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&bar[0], 2 * kTWinBytes);
+      tma_load_3d(win, &tm.ren, bx - kHalf - kTX, by - kHalf, ch + 1, &bar[0]);
+      tma_load_3d(win + kTWin, &tm.tgt, bx - kHalf - kTX, by - kHalf, ch + 1, &bar[0]);
+    }
     float mv[5][kR];
 #pragma unroll
     for (int m = 0; m < 5; ++m) {
@@ -235,8 +308,7 @@ __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, 
     for (int j = 0; j < kR; ++j) {
       const int y = by + rg * kR + j;
       if (x >= W || y >= H) continue;
-      const int o = (rg * kR + j + kHalf) * PITCH + (kTma ? kTX : 0) + c + kHalf;
-      const double a = st0[o], b = st1[o];
+      const double a = av[j], b = bv[j];
       const int64_t p = (int64_t)y * W + x;
       const bool in_mask = mask_at(mk, p);
       if (in_mask) l1 += fabs(a - b);
@@ -250,12 +322,26 @@ __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, 
         const double a1 = a_(m_(m_(2.0, ma), mb), C1), a2 = a_(m_(2.0, vab), C2);
         const double b1 = a_(a_(m_(ma, ma), m_(mb, mb)), C1), b2 = a_(a_(va, vb), C2);
         const double b12 = m_(b1, b2);
+#if GSB_LOSS_RCP
+        // one correctly rounded reciprocal instead of four divisions: the
+        // quotients move by an ulp or two (against FP32 statistics), and the
+        // two ratios identical inputs make exactly 1 (a1 a2 / b12, a2 / b2)
+        // are pinned to 1 on equality, so they still cancel exactly
+        const double r12 = __drcp_rn(b12), n12 = m_(a1, a2);
+        const double s = n12 == b12 ? 1.0 : m_(n12, r12);
+        ss += s;
+        const double gmu = m_(m_(scale, a_(m_(m_(2.0, mb), s_(a2, a1)), m_(m_(m_(2.0, ma), s), s_(b1, b2)))), r12);
+        const double qv = m_(a1, r12);
+        const double a2b2 = a2 == b2 ? 1.0 : m_(m_(a2, b1), r12);
+#else
         const double s = d_(m_(a1, a2), b12);
         ss += s;
         const double gmu = d_(m_(scale, a_(m_(m_(2.0, mb), s_(a2, a1)), m_(m_(m_(2.0, ma), s), s_(b1, b2)))), b12);
         const double qv = d_(a1, b12);
+        const double a2b2 = d_(a2, b2);
+#endif
         gmaps[(3 * ch + 0) * P + p] = (float)gmu;
-        gmaps[(3 * ch + 1) * P + p] = (float)m_(-m_(scale, qv), d_(a2, b2));
+        gmaps[(3 * ch + 1) * P + p] = (float)m_(-m_(scale, qv), a2b2);
         gmaps[(3 * ch + 2) * P + p] = (float)m_(2.0, m_(scale, qv));
       } else {
         gmaps[(3 * ch + 0) * P + p] = 0.f;
@@ -277,6 +363,19 @@ __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, 
 // Horizontal pass of the three gradient maps (back-convolution, losses.cpp:144-151).
 template <int PITCH, int XOFF>
 __device__ __forceinline__ void hpass3(const float* __restrict__ st, int plane_stride, float (*hq)[kSH][kTW + 1]) {
+#if GSB_LOSS_HSPLIT
+  constexpr int kGroups = kSH * (kTW / kHR), kL = kHR + kWin - 1;
+  for (int task = threadIdx.x; task < 3 * kGroups; task += kThr) {  // one map per task
+    const int m = task >= 2 * kGroups ? 2 : task >= kGroups ? 1 : 0, g = task - m * kGroups;
+    const int r = g / (kTW / kHR), q0 = (g - r * (kTW / kHR)) * kHR;
+    float f[kL], acc[kHR];
+#pragma unroll
+    for (int k = 0; k < kL; ++k) f[k] = st[m * plane_stride + r * PITCH + XOFF + q0 + k];
+    hconv<kL>(f, acc);
+#pragma unroll
+    for (int j = 0; j < kHR; ++j) hq[m][r][q0 + j] = acc[j];
+  }
+#else
   for (int task = threadIdx.x; task < kSH * (kTW / kHR); task += kThr) {
     const int r = task / (kTW / kHR), q0 = (task - r * (kTW / kHR)) * kHR;
 #pragma unroll
@@ -295,6 +394,7 @@ __device__ __forceinline__ void hpass3(const float* __restrict__ st, int plane_s
       for (int j = 0; j < kHR; ++j) hq[m][r][q0 + j] = acc[j];
     }
   }
+#endif
 }
 
 // 4 CTAs/SM (64 registers, 48 B of spills; 55 KB shared each): the kernel is
@@ -318,7 +418,7 @@ __global__ void GSB_LOSS_GRAD_BOUNDS loss_grad_kernel(const float* __restrict__ 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* win = reinterpret_cast<float*>(smem_raw);  // [buffers][3 maps][WIN]
   float(*hq)[kSH][kTW + 1] =
-      reinterpret_cast<float(*)[kSH][kTW + 1]>(smem_raw + sizeof(float) * (kTma ? 6 : 3) * WIN);
+      reinterpret_cast<float(*)[kSH][kTW + 1]>(smem_raw + sizeof(float) * (kTma ? 3 * kBufs : 3) * WIN);
   __shared__ __align__(8) uint64_t bar[2];
   const int64_t P = (int64_t)W * H;
   const int bx = blockIdx.x * kTW, by = blockIdx.y * kTH;
@@ -348,7 +448,10 @@ __global__ void GSB_LOSS_GRAD_BOUNDS loss_grad_kernel(const float* __restrict__ 
     float cv[3][kR];
     if (has_ssim) {
       const float* st;
-      if (kTma) {
+      if (kTma && kBufs == 1) {
+        mbar_wait(&bar[0], (uint32_t)(ch & 1));
+        st = win;
+      } else if (kTma) {
         if (threadIdx.x == 0 && ch + 1 < 3) {
           float* nb = win + ((ch + 1) & 1) * 3 * kTWin;
           fence_proxy_async();
@@ -366,6 +469,12 @@ __global__ void GSB_LOSS_GRAD_BOUNDS loss_grad_kernel(const float* __restrict__ 
       }
       hpass3<PITCH, kTma ? kTX : 0>(st, WIN, hq);
       __syncthreads();
+      if (kTma && kBufs == 1 && threadIdx.x == 0 && ch + 1 < 3) {  // window consumed: next channel into it
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&bar[0], 3 * kTWinBytes);
+        for (int m = 0; m < 3; ++m)
+          tma_load_3d(win + m * kTWin, &tm.gm, bx - kHalf - kTX, by - kHalf, 3 * (ch + 1) + m, &bar[0]);
+      }
 #pragma unroll
       for (int m = 0; m < 3; ++m) {
         float acc[kR];
@@ -489,8 +598,8 @@ int init_loss_constants() {
 
 constexpr size_t kMapsSmem = sizeof(float) * 2 * kSH * (kSW + 1) + sizeof(float) * 5 * kSH * (kTW + 1);
 constexpr size_t kGradSmem = sizeof(float) * 3 * kSH * (kSW + 1) + sizeof(float) * 3 * kSH * (kTW + 1);
-constexpr size_t kMapsSmemT = sizeof(float) * 4 * kTWin + sizeof(float) * 5 * kSH * (kTW + 1);
-constexpr size_t kGradSmemT = sizeof(float) * 6 * kTWin + sizeof(float) * 3 * kSH * (kTW + 1);
+constexpr size_t kMapsSmemT = sizeof(float) * 2 * kBufs * kTWin + sizeof(float) * 5 * kSH * (kTW + 1);
+constexpr size_t kGradSmemT = sizeof(float) * 3 * kBufs * kTWin + sizeof(float) * 3 * kSH * (kTW + 1);
 
 int init_loss_attributes() {
   GSB_CUDA(cudaFuncSetAttribute(loss_maps_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMapsSmem));
