@@ -208,6 +208,15 @@ constexpr int kTWin = (kSH * kTP + 31) / 32 * 32;  // window stride in shared me
 #define GSB_LOSS_TMA_BUFS 1  // (2: same K6 time, 16 KB more shared memory per CTA)
 #endif
 constexpr int kBufs = GSB_LOSS_TMA_BUFS;
+// GSB_LOSS_CH_SPLIT: one CTA per (tile, channel) (grid z = channel) instead of
+// one per tile looping over the channels: 3x the CTAs, so the last wave is a
+// small fraction of the launch (768 tile CTAs on 3-4 resident per SM leave
+// the second wave ~70 % empty). Measured: K6 alone 0.061 -> 0.057 ms, but the
+// pose batch, whose other branches already fill the tail, loses 0.7 % — off.
+#ifndef GSB_LOSS_CH_SPLIT
+#define GSB_LOSS_CH_SPLIT 0
+#endif
+constexpr bool kChSplit = GSB_LOSS_CH_SPLIT != 0;
 
 __device__ __forceinline__ void tma_load_3d(float* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
   asm volatile(
@@ -238,34 +247,36 @@ __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, 
   __shared__ __align__(8) uint64_t bar[2];
   const int64_t P = (int64_t)W * H;
   const int bx = blockIdx.x * kTW, by = blockIdx.y * kTH;
+  const int ch0 = kChSplit ? (int)blockIdx.z : 0, ch_end = kChSplit ? ch0 + 1 : 3;
   if (kTma && threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     mbar_arrive_expect_tx(&bar[0], 2 * kTWinBytes);
-    tma_load_3d(win, &tm.ren, bx - kHalf - kTX, by - kHalf, 0, &bar[0]);
-    tma_load_3d(win + kTWin, &tm.tgt, bx - kHalf - kTX, by - kHalf, 0, &bar[0]);
+    tma_load_3d(win, &tm.ren, bx - kHalf - kTX, by - kHalf, ch0, &bar[0]);
+    tma_load_3d(win + kTWin, &tm.tgt, bx - kHalf - kTX, by - kHalf, ch0, &bar[0]);
   }
   if (kTma) __syncthreads();  // barrier initialisation visible to every waiting thread
   // vertical task: column c, rows 4 rg .. 4 rg + 3
   const int c = threadIdx.x & (kTW - 1), rg = threadIdx.x / kTW;
   const int x = bx + c;
   double l1 = 0.0, ss = 0.0;
-  for (int ch = 0; ch < 3; ++ch) {
+  for (int ch = ch0; ch < ch_end; ++ch) {
+    const int it = ch - ch0;  // channel iteration of this CTA (buffer / phase index)
     const float* st0;
     if (kTma && kBufs == 1) {
-      mbar_wait(&bar[0], (uint32_t)(ch & 1));
+      mbar_wait(&bar[0], (uint32_t)(it & 1));
       st0 = win;
     } else if (kTma) {
-      if (threadIdx.x == 0 && ch + 1 < 3) {  // next channel into the other buffer
-        float* nb = win + ((ch + 1) & 1) * 2 * kTWin;
+      if (threadIdx.x == 0 && ch + 1 < ch_end) {  // next channel into the other buffer
+        float* nb = win + ((it + 1) & 1) * 2 * kTWin;
         fence_proxy_async();
-        mbar_arrive_expect_tx(&bar[(ch + 1) & 1], 2 * kTWinBytes);
-        tma_load_3d(nb, &tm.ren, bx - kHalf - kTX, by - kHalf, ch + 1, &bar[(ch + 1) & 1]);
-        tma_load_3d(nb + kTWin, &tm.tgt, bx - kHalf - kTX, by - kHalf, ch + 1, &bar[(ch + 1) & 1]);
+        mbar_arrive_expect_tx(&bar[(it + 1) & 1], 2 * kTWinBytes);
+        tma_load_3d(nb, &tm.ren, bx - kHalf - kTX, by - kHalf, ch + 1, &bar[(it + 1) & 1]);
+        tma_load_3d(nb + kTWin, &tm.tgt, bx - kHalf - kTX, by - kHalf, ch + 1, &bar[(it + 1) & 1]);
       }
-      mbar_wait(&bar[ch & 1], (uint32_t)(ch >> 1));
-      st0 = win + (ch & 1) * 2 * kTWin;
+      mbar_wait(&bar[it & 1], (uint32_t)(it >> 1));
+      st0 = win + (it & 1) * 2 * kTWin;
     } else {
       const float* src[2] = {ren + ch * P, tgt + ch * P};
       stage_planes<2>(reinterpret_cast<float(*)[kSH][kSW + 1]>(win), src, W, H, bx - kHalf, by - kHalf);
@@ -282,7 +293,7 @@ __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, 
       bv[j] = st1[o];
     }
     __syncthreads();
-    if (kTma && kBufs == 1 && threadIdx.x == 0 && ch + 1 < 3) {  // window consumed: next channel into it
+    if (kTma && kBufs == 1 && threadIdx.x == 0 && ch + 1 < ch_end) {  // window consumed: next channel into it
       fence_proxy_async();
       mbar_arrive_expect_tx(&bar[0], 2 * kTWinBytes);
       tma_load_3d(win, &tm.ren, bx - kHalf - kTX, by - kHalf, ch + 1, &bar[0]);
@@ -354,7 +365,7 @@ __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, 
   const double t1 = blk_reduce_sum(l1, s_tmp);
   const double t2 = blk_reduce_sum(ss, s_tmp);
   if (threadIdx.x == 0) {
-    const int bidx = blockIdx.y * gridDim.x + blockIdx.x;
+    const int bidx = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
     block_sums[2 * bidx] = t1;
     block_sums[2 * bidx + 1] = t2;
   }
@@ -422,6 +433,7 @@ __global__ void GSB_LOSS_GRAD_BOUNDS loss_grad_kernel(const float* __restrict__ 
   __shared__ __align__(8) uint64_t bar[2];
   const int64_t P = (int64_t)W * H;
   const int bx = blockIdx.x * kTW, by = blockIdx.y * kTH;
+  const int ch0 = kChSplit ? (int)blockIdx.z : 0, ch_end = kChSplit ? ch0 + 1 : 3;
   const int c = threadIdx.x & (kTW - 1), rg = threadIdx.x / kTW;
   const int x = bx + c;
   if (kTma && has_ssim && threadIdx.x == 0) {
@@ -429,10 +441,12 @@ __global__ void GSB_LOSS_GRAD_BOUNDS loss_grad_kernel(const float* __restrict__ 
     mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     mbar_arrive_expect_tx(&bar[0], 3 * kTWinBytes);
-    for (int m = 0; m < 3; ++m) tma_load_3d(win + m * kTWin, &tm.gm, bx - kHalf - kTX, by - kHalf, m, &bar[0]);
+    for (int m = 0; m < 3; ++m)
+      tma_load_3d(win + m * kTWin, &tm.gm, bx - kHalf - kTX, by - kHalf, 3 * ch0 + m, &bar[0]);
   }
   if (kTma) __syncthreads();  // barrier initialisation visible to every waiting thread
-  for (int ch = 0; ch < 3; ++ch) {
+  for (int ch = ch0; ch < ch_end; ++ch) {
+    const int it = ch - ch0;  // channel iteration of this CTA (buffer / phase index)
     // this channel's output pixels of both images, loaded before the
     // convolutions so their latency overlaps them (they were the kernel's
     // long-scoreboard stall)
@@ -449,18 +463,18 @@ __global__ void GSB_LOSS_GRAD_BOUNDS loss_grad_kernel(const float* __restrict__ 
     if (has_ssim) {
       const float* st;
       if (kTma && kBufs == 1) {
-        mbar_wait(&bar[0], (uint32_t)(ch & 1));
+        mbar_wait(&bar[0], (uint32_t)(it & 1));
         st = win;
       } else if (kTma) {
-        if (threadIdx.x == 0 && ch + 1 < 3) {
-          float* nb = win + ((ch + 1) & 1) * 3 * kTWin;
+        if (threadIdx.x == 0 && ch + 1 < ch_end) {
+          float* nb = win + ((it + 1) & 1) * 3 * kTWin;
           fence_proxy_async();
-          mbar_arrive_expect_tx(&bar[(ch + 1) & 1], 3 * kTWinBytes);
+          mbar_arrive_expect_tx(&bar[(it + 1) & 1], 3 * kTWinBytes);
           for (int m = 0; m < 3; ++m)
-            tma_load_3d(nb + m * kTWin, &tm.gm, bx - kHalf - kTX, by - kHalf, 3 * (ch + 1) + m, &bar[(ch + 1) & 1]);
+            tma_load_3d(nb + m * kTWin, &tm.gm, bx - kHalf - kTX, by - kHalf, 3 * (ch + 1) + m, &bar[(it + 1) & 1]);
         }
-        mbar_wait(&bar[ch & 1], (uint32_t)(ch >> 1));
-        st = win + (ch & 1) * 3 * kTWin;
+        mbar_wait(&bar[it & 1], (uint32_t)(it >> 1));
+        st = win + (it & 1) * 3 * kTWin;
       } else {
         const float* src[3] = {gmaps + (3 * ch + 0) * P, gmaps + (3 * ch + 1) * P, gmaps + (3 * ch + 2) * P};
         stage_planes<3>(reinterpret_cast<float(*)[kSH][kSW + 1]>(win), src, W, H, bx - kHalf, by - kHalf);
@@ -469,7 +483,7 @@ __global__ void GSB_LOSS_GRAD_BOUNDS loss_grad_kernel(const float* __restrict__ 
       }
       hpass3<PITCH, kTma ? kTX : 0>(st, WIN, hq);
       __syncthreads();
-      if (kTma && kBufs == 1 && threadIdx.x == 0 && ch + 1 < 3) {  // window consumed: next channel into it
+      if (kTma && kBufs == 1 && threadIdx.x == 0 && ch + 1 < ch_end) {  // window consumed: next channel into it
         fence_proxy_async();
         mbar_arrive_expect_tx(&bar[0], 3 * kTWinBytes);
         for (int m = 0; m < 3; ++m)
@@ -664,7 +678,7 @@ int launch_rgb_loss(cudaStream_t st, const float* ren, const float* tgt, int W, 
   const int has_ssim = cnt_valid > 0 ? 1 : 0;
   const double scale = has_ssim ? 1.0 / (3.0 * (double)cnt_valid) : 0.0;
   const double l1_norm = 1.0 / (3.0 * (double)W * (double)H);
-  dim3 grid((W + kTW - 1) / kTW, (H + kTH - 1) / kTH);
+  dim3 grid((W + kTW - 1) / kTW, (H + kTH - 1) / kTH, kChSplit ? 3 : 1);
   const auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   LossMaps tm;
   std::memset(&tm, 0, sizeof tm);
@@ -682,13 +696,15 @@ int launch_rgb_loss(cudaStream_t st, const float* ren, const float* tgt, int W, 
       loss_grad_kernel<false><<<grid, kThr, kGradSmem, st>>>(ren, tgt, gmaps, W, H, beta, l1_norm, has_ssim,
                                                               d_image, mk, tm);
   }
-  loss_finalize_kernel<<<1, 256, 0, st>>>(block_sums, (int)(grid.x * grid.y), l1_norm, scale, has_ssim, beta, out3,
+  loss_finalize_kernel<<<1, 256, 0, st>>>(block_sums, (int)(grid.x * grid.y * grid.z), l1_norm, scale, has_ssim, beta, out3,
                                           mk);
   *launches += d_image ? 3 : 2;
   GSB_CHECK_LAUNCH("rgb_loss kernels");
   return GSB_OK;
 }
 
-size_t loss_block_count(int W, int H) { return (size_t)((W + kTW - 1) / kTW) * ((H + kTH - 1) / kTH); }
+size_t loss_block_count(int W, int H) {
+  return (size_t)((W + kTW - 1) / kTW) * ((H + kTH - 1) / kTH) * (kChSplit ? 3 : 1);
+}
 
 }  // namespace gsb
