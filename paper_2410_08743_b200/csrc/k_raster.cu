@@ -684,18 +684,18 @@ __device__ __forceinline__ uint32_t half_mask(uint32_t m16) {
   return r;
 }
 
-// Lists of batch entries (list-local position < lim) reaching half 0 / 1 of
-// warp w's quadrant, ascending; returns both counts.
-__device__ __forceinline__ void build_half_lists(const uint8_t* s_mask, int cnt, int warp, uint32_t lim,
-                                                 uint8_t (*list)[kBatch], int* n0, int* n1) {
+// Lists of batch entries (list-local position < lim0 / lim1) reaching half 0 / 1
+// of warp w's quadrant, ascending; returns both counts.
+__device__ __forceinline__ void build_half_lists(const uint8_t* s_mask, int cnt, int warp, uint32_t lim0,
+                                                 uint32_t lim1, uint8_t (*list)[kBatch], int* n0, int* n1) {
   const int lane = threadIdx.x & 31;
   const uint32_t lt = lanemask_lt_();
   int c0 = 0, c1 = 0;
 #pragma unroll
   for (int c = 0; c < kBatch / 32; ++c) {
     const int e = c * 32 + lane;
-    const uint32_t m = (e < cnt && (uint32_t)e < lim) ? (s_mask[e] >> (2 * warp)) : 0u;
-    const bool t0 = m & 1u, t1 = m & 2u;
+    const uint32_t m = e < cnt ? (s_mask[e] >> (2 * warp)) : 0u;
+    const bool t0 = (m & 1u) && (uint32_t)e < lim0, t1 = (m & 2u) && (uint32_t)e < lim1;
     const uint32_t b0 = __ballot_sync(kFull, t0), b1 = __ballot_sync(kFull, t1);
     if (t0) list[0][c0 + __popc(b0 & lt)] = (uint8_t)e;
     if (t1) list[1][c1 + __popc(b1 & lt)] = (uint8_t)e;
@@ -705,6 +705,48 @@ __device__ __forceinline__ void build_half_lists(const uint8_t* s_mask, int cnt,
   __syncwarp();
   *n0 = c0;
   *n1 = c1;
+}
+
+// Exact culling of (entry, half) pairs (GSB_BWD_EXACT_CULL): the minimum of
+// the splat's power g = d^T conic d over the half's 8x4 rectangle of pixel
+// centres (tile-local [x0, x0 + 7] x [y0, y0 + 3]) — 0 if the mean is inside,
+// else the least of the four edge minima, each a clamped 1-D quadratic in
+// completed-square form (c (v - v*)^2 + (det / c) u^2: two non-negative terms,
+// no cancellation). A half whose minimum exceeds the cutoff by a margin far
+// above the FP32 rounding of the in-step g has no pixel the entry can touch:
+// its list skips the entry, whose contribution there is an exact zero.
+// Splats too elongated for that error bound (det < 1e-3 a c) keep the box test.
+// Measured on the bench: K4a 0.2162 -> 0.2209 ms (the staging cost exceeds the
+// steps it saves) — off.
+#ifndef GSB_BWD_EXACT_CULL
+#define GSB_BWD_EXACT_CULL 0
+#endif
+__device__ __forceinline__ float rect_min_power(float mx, float my, float a, float b, float c, float det, float x0,
+                                                float y0) {
+  const float u0 = x0 - mx, u1 = x0 + 7.0f - mx, v0 = y0 - my, v1 = y0 + 3.0f - my;
+  if (u0 <= 0.0f && u1 >= 0.0f && v0 <= 0.0f && v1 >= 0.0f) return 0.0f;
+  const float ia = 1.0f / a, ic = 1.0f / c, dc = det * ic, da = det * ia;
+  auto edge_x = [&](float u) {  // dx = u fixed, dy in [v0, v1]; minimiser v* = -b u / c
+    const float vs = -b * u * ic, w = fminf(fmaxf(vs, v0), v1) - vs;
+    return c * w * w + dc * u * u;
+  };
+  auto edge_y = [&](float v) {  // dy = v fixed, dx in [u0, u1]; minimiser u* = -b v / a
+    const float us = -b * v * ia, w = fminf(fmaxf(us, u0), u1) - us;
+    return a * w * w + da * v * v;
+  };
+  return fminf(fminf(edge_x(u0), edge_x(u1)), fminf(edge_y(v0), edge_y(v1)));
+}
+__device__ __forceinline__ uint32_t exact_half_mask(uint32_t m, const float4& ge, float c, float cutoff2) {
+  const float a = ge.z, b = ge.w, det = fmaf(a, c, -b * b);
+  if (!(a > 0.f && c > 0.f && det >= 1e-3f * a * c) || !(a * c < 1e30f)) return m;
+  const float thr = cutoff2 * 1.001f + 1e-3f;
+  uint32_t keep = 0u;
+  for (uint32_t r = m; r; r &= r - 1u) {
+    const int hb = __ffs(r) - 1, q = hb >> 1, h = hb & 1;
+    if (rect_min_power(ge.x, ge.y, a, b, c, det, (float)((q & 1) * 8), (float)((q >> 1) * 8 + 4 * h)) <= thr)
+      keep |= 1u << hb;
+  }
+  return keep;
 }
 
 // 8 values over each 16-lane half: xor 8 / 4 / 2 reduce-scatter (4 + 2 + 1
@@ -830,7 +872,10 @@ __global__ void __launch_bounds__(kThreads, kHits ? GSB_BWD_HITS_MIN_BLOCKS : GS
   PixBwd a, b;
   load_pixel_bwd(a, x, y, W, H, npix, bg_r, bg_g, bg_b, d_image, final_t, pixstate);
   load_pixel_bwd(b, x, y + 1, W, H, npix, bg_r, bg_g, bg_b, d_image, final_t, pixstate);
-  const uint32_t wmax = __reduce_max_sync(kFull, max(a.contrib, b.contrib));
+  const uint32_t pmax = max(a.contrib, b.contrib);
+  const uint32_t wmax = __reduce_max_sync(kFull, pmax);
+  // per-half replay depth: an entry at or past it is replayed by no pixel of the half
+  const uint32_t hmax0 = __reduce_max_sync(kFull, half ? 0u : pmax), hmax1 = __reduce_max_sync(kFull, half ? pmax : 0u);
   if (lane == 0) s_maxc[warp] = wmax;
   __syncthreads();
   uint32_t maxc = 0;
@@ -896,7 +941,8 @@ __global__ void __launch_bounds__(kThreads, kHits ? GSB_BWD_HITS_MIN_BLOCKS : GS
       const uint32_t tx0 = A.tx0_ty0 & 0xffffu, ty0 = A.tx0_ty0 >> 16, nx = A.nx_ny & 0xffffu;
       StagedSplat& S = s_sp[threadIdx.x];
       S.slot = A.off + ((uint32_t)ty - ty0) * nx + ((uint32_t)tx - tx0);
-      const uint32_t bbox = half_mask(stage_splat(rec[r], ox, oy, rc.cutoff2_f, &S.geo, &S.app, &S.col_b));
+      uint32_t bbox = half_mask(stage_splat(rec[r], ox, oy, rc.cutoff2_f, &S.geo, &S.app, &S.col_b));
+      if (GSB_BWD_EXACT_CULL && !kHits && bbox) bbox = exact_half_mask(bbox, S.geo, S.app.x, rc.cutoff2_f);
       if (kHits) {
         // region r = 4 ry + rx; (quadrant q = qx + 2 qy, half h) holds regions
         // 4 (2 qy + h) + 2 qx and + 1
@@ -922,7 +968,8 @@ __global__ void __launch_bounds__(kThreads, kHits ? GSB_BWD_HITS_MIN_BLOCKS : GS
     __syncthreads();
     if (b0 < wmax) {  // this warp has pixels that replay entries of this batch
       int n0, n1;
-      build_half_lists(s_mask, cnt, warp, wmax - b0, s_list[warp], &n0, &n1);
+      build_half_lists(s_mask, cnt, warp, hmax0 > b0 ? hmax0 - b0 : 0u, hmax1 > b0 ? hmax1 - b0 : 0u,
+                       s_list[warp], &n0, &n1);
       const int mine = half ? n1 : n0;
       const int nmax = max(n0, n1);
       const uint8_t* my_list = s_list[warp][half];
