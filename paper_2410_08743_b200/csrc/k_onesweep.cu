@@ -15,6 +15,8 @@
 // bases, then each pass is a single scatter kernel: stable in-tile ranks via
 // warp match_any + cross-warp prefix, per-digit look-back across tiles,
 // scatter to base + prefix + rank.
+#include <algorithm>
+
 #include "gsb_internal.cuh"
 
 namespace gsb {
@@ -175,10 +177,20 @@ __global__ void __launch_bounds__(kScanThreads) scan_onepass_kernel(const uint32
 
 size_t scan_onepass_words(int64_t cap) { return (size_t)((cap + kScanTile - 1) / kScanTile) + 2; }
 
+// Zeroes the scan's ticket and status words. A kernel rather than a memset
+// node: the same cost inside a captured graph, and compute-sanitizer's
+// initcheck tracks kernel stores (it reported the ticket word of the graph
+// memset as uninitialised).
+__global__ void zero_words_kernel(uint32_t* __restrict__ w, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) w[i] = 0u;
+}
+
 int scan_onepass(cudaStream_t st, const uint32_t* in, int64_t cap, const uint32_t* n_dev, bool flag, uint32_t* out,
                  uint32_t* status, uint32_t* total, int64_t* launches) {
   const int64_t ntiles = (cap + kScanTile - 1) / kScanTile;
-  GSB_CUDA(cudaMemsetAsync(status, 0, sizeof(uint32_t) * (ntiles + 2), st));
+  zero_words_kernel<<<(unsigned)std::min<int64_t>((ntiles + 2 + 255) / 256, 64), 256, 0, st>>>(status, ntiles + 2);
+  *launches += 1;
   const unsigned grid = (unsigned)(ntiles > 0 ? ntiles : 1);
   if (flag) scan_onepass_kernel<true><<<grid, kScanThreads, 0, st>>>(in, cap, n_dev, out, status, total);
   else scan_onepass_kernel<false><<<grid, kScanThreads, 0, st>>>(in, cap, n_dev, out, status, total);

@@ -16,3 +16,6 @@ tail -1 gpurun_out/prof_${TAG}_iter.log
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:preprocess -s 8 -c 1 \
   -o gpurun_out/prof_${TAG}_k1multi python tools/prof_batch.py 1 > gpurun_out/prof_${TAG}_k1.log 2>&1
 tail -1 gpurun_out/prof_${TAG}_k1.log
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+  --log-file gpurun_out/launches_joint_$TAG.csv python tools/prof_joint.py 6 > /dev/null 2>&1
+python tools/launch_summary.py gpurun_out/launches_joint_$TAG.csv | head -24
