@@ -58,6 +58,9 @@ constexpr int kGeomWarps = kGeomBlock / 32;
 #ifndef GSB_GEOM_FULL_MIN_BLOCKS
 #define GSB_GEOM_FULL_MIN_BLOCKS 2
 #endif
+#ifndef GSB_FULL_CHAIN_T
+#define GSB_FULL_CHAIN_T double
+#endif
 #ifndef GSB_POSE_CHAIN_T
 #define GSB_POSE_CHAIN_T float
 #endif
@@ -394,7 +397,7 @@ int launch_backward_geom(cudaStream_t st, const gsb_cloud* cloud, gsb_frame* f, 
   const int64_t nb = (n + kGeomBlock - 1) / kGeomBlock;
   if (nb > 0) {
     if (full)
-      backward_geom_kernel<true, double><<<(unsigned)nb, kGeomBlock, 0, st>>>(
+      backward_geom_kernel<true, GSB_FULL_CHAIN_T><<<(unsigned)nb, kGeomBlock, 0, st>>>(
           cloud->params.as<float>(), n, cloud->n_pad, cloud->sh_degree, cloud->active_sh_degree, f->cam.as<CamDev>(),
           rc, f->cnt_g.as<uint32_t>(), f->off_g.as<uint32_t>(), f->colj.as<float>(), f->partials.as<float>(), f->k_cap, cutd, grads,
           f->pose_blocks.as<double>());
