@@ -251,6 +251,7 @@ def run_ours(args, ws, rank, local):
 
     joint = None if (args.no_joint or (SHARE_GPU and ws > 1)) else run_joint(args, ws, rank, local, dist)
     single = None if args.no_joint else run_single_view(args, ws, rank, local)
+    kernel_only = None if args.no_joint else run_kernel_only(args, ws, rank, local)
     c3_job = None if args.no_c3_job else run_c3_job(args, ws, rank, local, ctx, cloud, gt, init, intr)
     out = None
     if rank == 0:
@@ -304,6 +305,8 @@ def run_ours(args, ws, rank, local):
             out["joint_c4"] = joint
         if single is not None:
             out["single_view_c2"] = single
+        if kernel_only is not None:
+            out["kernel_only_c3"] = kernel_only
         if c3_job is not None:
             out["c3_job_1gpu"] = c3_job
         out["fp32_peaks_measured"] = {k: round(v, 2) for k, v in fp32.items()}
@@ -351,6 +354,49 @@ def run_single_view(args, ws, rank, local):
                         "perturb 15deg/0.15, one session", "iters_per_s": round(steps / (ms / 1e3), 2),
             "ms_per_iter": round(ms / steps, 4), "steps": steps}
 
+
+def run_kernel_only(args, ws, rank, local):
+    """SURVEY §8d metric (1), kernel-only variant: render -> render_backward
+    (pose-only) through the reference-API calls with a fixed random d_image
+    already on the device (tests/gradcheck.hpp:204-208 reuses one d_image),
+    C3's scene at view 0's initial pose; no loss, no pose step. Host-driven:
+    two C-ABI calls per iteration (the backward returns d_pose to the host),
+    so this includes the per-call launch and synchronisation a drop-in caller
+    pays, unlike the graph-replayed sessions. Rank 0 only."""
+    if rank != 0:
+        return None
+    from paper_2410_08743_b200 import gsb
+    ctx = gsb.Context(local)
+    cloud = gsb.Cloud(ctx, N_GAUSS, SH_DEGREE)
+    cloud.synth(SCENE_SEED, log_scale_offset(N_GAUSS))
+    _, init = all_views()
+    intr = gsb.synth_intrinsics(WIDTH, HEIGHT)
+    cam = gsb.Camera.from_pose12(*intr, WIDTH, HEIGHT, init[0])
+    d_img = gsb.Image(ctx, np.random.default_rng(7).uniform(-1e-6, 1e-6, (HEIGHT, WIDTH, 3)))
+    frame = gsb.Frame(ctx)
+
+    def iteration():
+        out = gsb.render(ctx, cloud, cam, frame=frame, want_image=False)
+        return gsb.render_backward(ctx, cloud, cam, out, d_img, pose_only=True)[1]
+
+    for _ in range(max(args.warmup, 3)):
+        iteration()
+    steps = max(args.steps, 10)
+    ctx.synchronize()
+    launches0 = ctx.launch_count()
+    t0 = time.perf_counter()
+    ctx.timer_start()
+    for _ in range(steps):
+        dp = iteration()
+    ms = ctx.timer_stop()
+    wall = time.perf_counter() - t0
+    assert np.all(np.isfinite(dp)) and np.any(dp != 0.0)
+    return {"workload": f"render + render_backward(pose-only), fixed random d_image on the device, C3 scene "
+                        f"({N_GAUSS} Gaussians SH{SH_DEGREE}, {WIDTH}x{HEIGHT}) at view 0's initial pose, "
+                        "one C-ABI call each (gsb_render, gsb_render_backward_image)",
+            "iters_per_s": round(steps / (ms / 1e3), 2), "ms_per_iter": round(ms / steps, 4),
+            "wall_ms_per_iter": round(wall * 1e3 / steps, 4), "steps": steps,
+            "launches_per_iter": round((ctx.launch_count() - launches0) / steps, 1)}
 
 
 def run_joint(args, ws, rank, local, dist):

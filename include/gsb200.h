@@ -255,6 +255,14 @@ int gsb_render_backward_device(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera*
                                gsb_frame* frame, uint32_t flags, gsb_grads* grads,
                                double d_pose_out[6]);
 
+/* Same, upstream gradient = a device-resident Image (gsb_image_create, e.g. a
+ * fixed d_image reused across calls as tests/gradcheck.hpp:204-208 does):
+ * render_backward(cloud, camera, fwd, d_image) with d_image already on the
+ * device; GSB_ERR_DIMENSION_MISMATCH when its size differs from the camera's
+ * (rasterizer.cpp:341-343). */
+int gsb_render_backward_image(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, gsb_frame* frame,
+                              const gsb_image* d_image, uint32_t flags, gsb_grads* grads, double d_pose_out[6]);
+
 /* ---- optimiser (trainer.cpp:30-90, pipelines.cpp:18-41) ---- */
 double gsb_schedule(int32_t kind /* 0 cosine, 1 exponential */, double start, double end,
                     int64_t step, int64_t total);

@@ -1477,6 +1477,21 @@ int gsb_render_backward_device(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera*
   return backward_common(ctx, cloud, cam, f, flags, grads, d_pose_out);
 }
 
+int gsb_render_backward_image(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, gsb_frame* f,
+                              const gsb_image* d_image, uint32_t flags, gsb_grads* grads, double d_pose_out[6]) {
+  GSB_NVTX("gsb_render_backward_image");
+  if (int r = ensure_device(ctx)) return r;
+  if (!cloud || !cam || !f || !d_image) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  if (int r = check_state(cloud, cam, f)) return r;  // rasterizer.cpp:338-340
+  if (d_image->width != cam->width || d_image->height != cam->height)
+    return fail(GSB_ERR_DIMENSION_MISMATCH, "render_backward: d_image size mismatch");  // 341-343
+  const size_t bytes = sizeof(float) * 3 * (size_t)cam->width * cam->height;
+  GSB_RESERVE(f->d_image, bytes);
+  GSB_CUDA(cudaMemcpyAsync(f->d_image.p, d_image->planes.p, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  f->has_dimage = true;
+  return backward_common(ctx, cloud, cam, f, flags, grads, d_pose_out);
+}
+
 // --------------------------------------------------------------- optimiser
 double gsb_schedule(int32_t kind, double start, double end, int64_t step, int64_t total) {  // trainer.cpp:30-38
   if (total <= 0) return end;

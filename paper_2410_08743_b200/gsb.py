@@ -206,6 +206,7 @@ def _sigs():
         "gsb_grads_download": (C.c_int, [_vp] + [_vp] * 7),
         "gsb_render_backward": (C.c_int, [_vp, _vp, P(Camera), _vp, _vp, i32, i32, u32, _vp, _vp]),
         "gsb_render_backward_device": (C.c_int, [_vp, _vp, P(Camera), _vp, u32, _vp, _vp]),
+        "gsb_render_backward_image": (C.c_int, [_vp, _vp, P(Camera), _vp, _vp, u32, _vp, _vp]),
         "gsb_schedule": (d, [i32, d, d, i64, i64]),
         "gsb_pose_step": (C.c_int, [_vp, _vp, _vp, d, P(PoseAdam), _vp, _vp]),
         "gsb_adam_step": (C.c_int, [_vp, _vp, _vp, _vp, _vp, P(i64), i64, d]),
@@ -549,17 +550,22 @@ def render_expected_depth(ctx: Context, cloud: Cloud, cam: Camera, config: Raste
     return depth, weight
 
 
-def render_backward(ctx: Context, cloud: Cloud, cam: Camera, out: RenderOutput, d_image: np.ndarray,
+def render_backward(ctx: Context, cloud: Cloud, cam: Camera, out: RenderOutput, d_image,
                     pose_only=False, grads: Grads | None = None):
-    """gsopt::render_backward (rasterizer.hpp:112-113). Returns (grads dict | None, d_pose)."""
-    d = np.ascontiguousarray(d_image, np.float64)
-    h, w = (d.shape[0], d.shape[1]) if d.ndim == 3 else (0, 0)
+    """gsopt::render_backward (rasterizer.hpp:112-113). d_image: host (H, W, 3)
+    FP64 array, or an `Image` already on the device. Returns (grads dict | None, d_pose)."""
     flags = BWD_POSE_ONLY if pose_only else 0
     if not pose_only and grads is None:
         grads = Grads(ctx, cloud)
     dp = np.zeros(6)
-    _check(lib().gsb_render_backward(ctx.h, cloud.h, C.byref(cam), out.frame.h, _p(d), w, h, flags,
-                                     grads.h if grads is not None else None, _p(dp)))
+    gh = grads.h if grads is not None else None
+    if isinstance(d_image, Image):
+        _check(lib().gsb_render_backward_image(ctx.h, cloud.h, C.byref(cam), out.frame.h, d_image.h, flags, gh,
+                                               _p(dp)))
+        return (grads.download() if (grads is not None and not pose_only) else None), dp
+    d = np.ascontiguousarray(d_image, np.float64)
+    h, w = (d.shape[0], d.shape[1]) if d.ndim == 3 else (0, 0)
+    _check(lib().gsb_render_backward(ctx.h, cloud.h, C.byref(cam), out.frame.h, _p(d), w, h, flags, gh, _p(dp)))
     return (grads.download() if (grads is not None and not pose_only) else None), dp
 
 

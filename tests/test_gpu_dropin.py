@@ -182,3 +182,32 @@ def test_tile_size_export_matches_reference(G, ctx, tile):
     assert np.array_equal(dp_s, dp_16)
     for k in g_16:
         assert np.array_equal(g_s[k], g_16[k]), k
+
+
+def test_render_backward_device_image_equals_host(G, ctx):
+    """gsb_render_backward_image: render_backward with the upstream gradient
+    already on the device (a fixed d_image reused across calls, as
+    tests/gradcheck.hpp:204-208 does) gives the host path's results bit for
+    bit (both round the FP64 image to the same FP32 planes), and rejects a
+    d_image of another size (rasterizer.cpp:341-343)."""
+    import math
+    rng = O.make_rng(77)
+    hc = O.synth_cloud(3000, 3, rng)
+    hc.log_scales += math.log(500 / 3000) / 3
+    cam = O.synth_camera(96, 72, O.synth_poses(0, 3, rng)[0])
+    cloud = to_dev(G, ctx, hc.as_float32_exact())
+    dc = dev_cam(G, cam)
+    d_img = np.random.default_rng(5).uniform(-1e-3, 1e-3, (72, 96, 3))
+    dev_img = G.Image(ctx, d_img)
+    for pose_only in (True, False):
+        out = G.render(ctx, cloud, dc)
+        g_h, dp_h = G.render_backward(ctx, cloud, dc, out, d_img, pose_only=pose_only)
+        g_d, dp_d = G.render_backward(ctx, cloud, dc, out, dev_img, pose_only=pose_only)
+        assert np.array_equal(dp_h, dp_d) and np.any(dp_h != 0.0)
+        if not pose_only:
+            for k in g_h:
+                assert np.array_equal(g_h[k], g_d[k]), k
+    small = G.Image(ctx, d_img[:-1])
+    with pytest.raises(G.GsbError) as e:
+        G.render_backward(ctx, cloud, dc, out, small, pose_only=True)
+    assert e.value.code == G.ERR_DIMENSION_MISMATCH
