@@ -106,54 +106,9 @@ __device__ __forceinline__ void stage_planes(float (*dst)[kSH][kSW + 1], const f
 #define GSB_LOSS_HR 4
 #endif
 constexpr int kHR = GSB_LOSS_HR;
-// GSB_LOSS_HSPLIT: the 42 x 8 (row, column group) tasks are split three ways
-// — (mu_a, E[a^2]) from a, (mu_b, E[b^2]) from b, E[ab] from both — so the
-// 1008 tasks fill 4 rounds of 256 threads (98 %) instead of 336 filling 2
-// rounds (66 %); every output keeps its tap order (bit-identical).
-#ifndef GSB_LOSS_HSPLIT
-#define GSB_LOSS_HSPLIT 0  // measured slower (K6 0.073 -> 0.075 ms): the extra LDS outweigh the balance
-#endif
-template <int N>
-__device__ __forceinline__ void hconv(const float* f, float* acc) {
-#pragma unroll
-  for (int j = 0; j < kHR; ++j) acc[j] = 0.f;
-#pragma unroll
-  for (int k = 0; k < kHR + kWin - 1; ++k)
-#pragma unroll
-    for (int j = 0; j < kHR; ++j)
-      if (k - j >= 0 && k - j < kWin) acc[j] = fmaf(c_win[k - j], f[k], acc[j]);
-}
 template <int PITCH, int XOFF>
 __device__ __forceinline__ void hpass5(const float* __restrict__ st0, const float* __restrict__ st1,
                                        float (*hq)[kSH][kTW + 1]) {
-#if GSB_LOSS_HSPLIT
-  constexpr int kGroups = kSH * (kTW / kHR), kL = kHR + kWin - 1;
-  for (int task = threadIdx.x; task < 3 * kGroups; task += kThr) {
-    const int t = task >= 2 * kGroups ? 2 : task >= kGroups ? 1 : 0, g = task - t * kGroups;
-    const int r = g / (kTW / kHR), q0 = (g - r * (kTW / kHR)) * kHR;
-    float acc[kHR], f[kL];
-    if (t < 2) {
-      const float* st = t ? st1 : st0;
-      float x[kL];
-#pragma unroll
-      for (int k = 0; k < kL; ++k) x[k] = st[r * PITCH + XOFF + q0 + k];
-      hconv<kL>(x, acc);
-#pragma unroll
-      for (int j = 0; j < kHR; ++j) hq[t][r][q0 + j] = acc[j];
-#pragma unroll
-      for (int k = 0; k < kL; ++k) f[k] = x[k] * x[k];
-      hconv<kL>(f, acc);
-#pragma unroll
-      for (int j = 0; j < kHR; ++j) hq[2 + t][r][q0 + j] = acc[j];
-    } else {
-#pragma unroll
-      for (int k = 0; k < kL; ++k) f[k] = st0[r * PITCH + XOFF + q0 + k] * st1[r * PITCH + XOFF + q0 + k];
-      hconv<kL>(f, acc);
-#pragma unroll
-      for (int j = 0; j < kHR; ++j) hq[4][r][q0 + j] = acc[j];
-    }
-  }
-#else
   for (int task = threadIdx.x; task < kSH * (kTW / kHR); task += kThr) {
     const int r = task / (kTW / kHR), q0 = (task - r * (kTW / kHR)) * kHR;
     float x[kHR + kWin - 1], y[kHR + kWin - 1];
@@ -178,7 +133,6 @@ __device__ __forceinline__ void hpass5(const float* __restrict__ st0, const floa
       for (int j = 0; j < kHR; ++j) hq[m][r][q0 + j] = acc[j];
     }
   }
-#endif
 }
 
 #ifndef GSB_LOSS_RCP
@@ -374,19 +328,6 @@ __global__ void GSB_LOSS_BOUNDS loss_maps_kernel(const float* __restrict__ ren, 
 // Horizontal pass of the three gradient maps (back-convolution, losses.cpp:144-151).
 template <int PITCH, int XOFF>
 __device__ __forceinline__ void hpass3(const float* __restrict__ st, int plane_stride, float (*hq)[kSH][kTW + 1]) {
-#if GSB_LOSS_HSPLIT
-  constexpr int kGroups = kSH * (kTW / kHR), kL = kHR + kWin - 1;
-  for (int task = threadIdx.x; task < 3 * kGroups; task += kThr) {  // one map per task
-    const int m = task >= 2 * kGroups ? 2 : task >= kGroups ? 1 : 0, g = task - m * kGroups;
-    const int r = g / (kTW / kHR), q0 = (g - r * (kTW / kHR)) * kHR;
-    float f[kL], acc[kHR];
-#pragma unroll
-    for (int k = 0; k < kL; ++k) f[k] = st[m * plane_stride + r * PITCH + XOFF + q0 + k];
-    hconv<kL>(f, acc);
-#pragma unroll
-    for (int j = 0; j < kHR; ++j) hq[m][r][q0 + j] = acc[j];
-  }
-#else
   for (int task = threadIdx.x; task < kSH * (kTW / kHR); task += kThr) {
     const int r = task / (kTW / kHR), q0 = (task - r * (kTW / kHR)) * kHR;
 #pragma unroll
@@ -405,7 +346,6 @@ __device__ __forceinline__ void hpass3(const float* __restrict__ st, int plane_s
       for (int j = 0; j < kHR; ++j) hq[m][r][q0 + j] = acc[j];
     }
   }
-#endif
 }
 
 // 4 CTAs/SM (64 registers, 48 B of spills; 55 KB shared each): the kernel is
