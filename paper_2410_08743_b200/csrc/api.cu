@@ -53,6 +53,7 @@ size_t bin_hist_words(int64_t n, int n_tiles);
 int init_bin_attributes();
 int launch_composite(cudaStream_t st, gsb_frame* f, const RasterDev& rc);
 bool hit_masks_enabled();
+int hit_words();
 int build_export_tiles(cudaStream_t st, gsb_frame* f, int S);
 int launch_expected_depth(cudaStream_t st, gsb_frame* f, const RasterDev& rc, float* depth_out, float* weight_out);
 int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc, bool pose_only);
@@ -427,7 +428,7 @@ static int frame_reserve(gsb_frame* f, const gsb_cloud* cloud, int64_t k_cap) {
   GSB_CUDA(f->loss_blocks.reserve(sizeof(double) * 2 * loss_block_count(f->width, f->height), &grew));
   GSB_CUDA(f->loss_val.reserve(sizeof(double) * 4, &grew));
   GSB_CUDA(f->partials.reserve(sizeof(float) * kPartial * k_cap, &grew));
-  if (f->want_hits) GSB_CUDA(f->hits.reserve(sizeof(uint16_t) * 16 * k_cap, &grew));
+  if (f->want_hits) GSB_CUDA(f->hits.reserve(sizeof(uint16_t) * hit_words() * k_cap, &grew));
   GSB_CUDA(f->pose_blocks.reserve(sizeof(double) * 6 * ((n + 63) / 64 + 1), &grew));  // K4b blocks of >= 64
   GSB_CUDA(f->d_pose.reserve(sizeof(double) * 6, &grew));
   if (grew) {
@@ -438,7 +439,7 @@ static int frame_reserve(gsb_frame* f, const gsb_cloud* cloud, int64_t k_cap) {
   f->k_cap = std::min<int64_t>(f->k_cap, (int64_t)(f->partials.bytes / (sizeof(float) * kPartial)));
   f->k_cap = std::min<int64_t>(f->k_cap, (int64_t)(f->ent_key.bytes / sizeof(uint64_t)));
   f->k_cap = std::min<int64_t>(f->k_cap, (int64_t)(f->ent_gid.bytes / sizeof(uint32_t)));
-  if (f->want_hits) f->k_cap = std::min<int64_t>(f->k_cap, (int64_t)(f->hits.bytes / (sizeof(uint16_t) * 16)));
+  if (f->want_hits) f->k_cap = std::min<int64_t>(f->k_cap, (int64_t)(f->hits.bytes / (sizeof(uint16_t) * hit_words())));
   f->k_cap = std::min<int64_t>(f->k_cap, 0xffffffffll);
   return GSB_OK;
 }

@@ -311,7 +311,8 @@ struct gsb_frame {
   bool has_dimage = false;
   bool lean = false;      // internal state (sessions, joint): skip the export-only K1 outputs
   // Hit masks (K3 -> pose-only K4a): per tile-list position, 16 regions x 16
-  // bits of the pixels the composite applied the entry to (uint16 [k_cap][16]).
+  // bits of the pixels the composite applied the entry to (uint16 [k_cap][16]),
+  // or (GSB_BWD_HITS = 2) one uint16 of touched-region bits per list position.
   bool want_hits = false;
   // device camera / config
   gsb::DevBuf cam;        // CamDev
@@ -343,7 +344,7 @@ struct gsb_frame {
   gsb::DevBuf d_image;    // FP32 planes [3][P]
   // backward
   gsb::DevBuf partials;   // float [K][9] at pre-sort positions (live entries only)
-  gsb::DevBuf hits;       // uint16 [k_cap][16] hit masks by list position (want_hits frames)
+  gsb::DevBuf hits;       // uint16 [k_cap][hit_words()] hit records by list position (want_hits frames)
   gsb::DevBuf tile_cut;   // double2 per tile: (FP64 depth, gid) of the last replayed entry, depth -1 if none
   gsb::DevBuf pose_blocks;// double [blocks][6]
   gsb::DevBuf d_pose;     // double[6]

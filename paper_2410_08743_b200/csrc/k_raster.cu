@@ -199,19 +199,27 @@ __device__ __forceinline__ bool pix_done(const PixFwd& p, const RasterDev&) { re
 // sub-warp's 8 lanes' pixel-pair hits go to slot `region` (pixel a of lane
 // l8 -> bit l8, pixel b -> bit 8 + l8), the exact set of (pixel, entry) pairs
 // the replay of render_backward visits (rasterizer.cpp:378-383).
-template <bool kHits>
+// kHitMode 2: lane 0 stores the step's ballot (hword); at the end of the
+// batch the ballots and the sub-warp lists give, per entry, the 4x4 regions
+// whose pixels it touched (one store per step on the critical path).
+template <int kHitMode>
 __device__ __forceinline__ void composite_pair(PixFwd& a, PixFwd& b, const float4& ge, const float4& ap, float col_b,
                                                float dx, float dy, const RasterDev& rc, uint32_t idx1,
-                                               bool act = true, uint16_t* hrow = nullptr, int region = 0) {
+                                               bool act = true, uint16_t* hrow = nullptr, int region = 0,
+                                               uint32_t* hword = nullptr) {
   const float ga = splat_power(ge.z, ge.w, ap.x, dx, dy);
   const float gb = splat_power(ge.z, ge.w, ap.x, dx, dy + 1.0f);
   const bool ha = act && !pix_done(a, rc) && ga <= rc.cutoff2_f;
   const bool hb = act && !pix_done(b, rc) && gb <= rc.cutoff2_f;
-  if (kHits) {  // the two ballots double as the warp-uniform skip test
+  if (kHitMode == 1) {  // the two ballots double as the warp-uniform skip test
     const uint32_t ba = __ballot_sync(kFull, ha), bb = __ballot_sync(kFull, hb);
     if (!(ba | bb)) return;
     const int lane = threadIdx.x & 31, sh = lane & 24;
     if ((lane & 7) == 0 && act) hrow[region] = (uint16_t)(__byte_perm(ba >> sh, bb >> sh, 0x0040));
+  } else if (kHitMode == 2) {  // the ballot doubles as the warp-uniform skip test
+    const uint32_t bal = __ballot_sync(kFull, ha || hb);
+    if (!bal) return;  // (the step's slot was zeroed at staging)
+    if ((threadIdx.x & 31) == 0) *hword = bal;  // the step's ballot, decoded at the end of the batch
   } else {
 #if GSB_COMP_UNIFORM_SKIP
     if (!__any_sync(kFull, ha || hb)) return;  // warp-uniform: lanes without a hit run the no-op update
@@ -256,7 +264,7 @@ __device__ __forceinline__ void write_pixel(const PixFwd& p, int x, int y, int W
 #else
 #define GSB_COMP_BOUNDS __launch_bounds__(kThreads)
 #endif
-template <bool kHits>
+template <int kHitMode>
 __global__ void GSB_COMP_BOUNDS composite_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ ranks, const SplatRec* __restrict__ rec,
     const CamDev* __restrict__ cam_p, RasterDev rc, float bg_r, float bg_g, float bg_b, int64_t npix,
@@ -266,7 +274,11 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
   __shared__ StagedSplat s_sp[CB];
   __shared__ uint16_t s_mask[CB];
   __shared__ uint8_t s_list[kWarps][kSubs][CB];
+  constexpr bool kHits = kHitMode == 1;
   __shared__ __align__(16) uint16_t s_hits[kHits ? CB : 1][16];
+  constexpr bool kBits = kHitMode == 2;
+  __shared__ uint32_t s_bal[kBits ? kWarps : 1][kBits ? CB : 1];  // per warp step: the hit ballot
+  __shared__ uint32_t s_r16[kBits ? CB : 1];                      // per batch entry: touched regions
   __shared__ int s_w, s_h, s_tx;
   if (threadIdx.x == 0) {
     s_w = cam_p->width;
@@ -302,6 +314,11 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
         hz[0] = make_uint4(0u, 0u, 0u, 0u);
         hz[1] = make_uint4(0u, 0u, 0u, 0u);
       }
+      if (kBits) {
+        s_r16[t] = 0u;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) s_bal[w][t] = 0u;
+      }
     }
     __syncthreads();
     const uint32_t list0 = base - range.x;
@@ -312,6 +329,7 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
     for (int s = 0; s < kSubs; ++s) lim[s] = ((live >> (8 * s)) & 0xffu) ? 0xffffffffu : 0u;
     int mine = 0;
     const int nmax = build_lists<CB>(s_mask, cnt, warp, lim, 0u, s_list[warp], &mine);
+    int nit = nmax;  // steps this warp ran (kBits)
     for (int it = 0; it < nmax; ++it) {
 #if GSB_COMP_UNIFORM_SKIP
       {
@@ -322,8 +340,8 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
         const float4 ap = S.app;
         const float cb = S.col_b;
         const float dx = px - ge.x, dy = py - ge.y;
-        composite_pair<kHits>(a, b, ge, ap, cb, dx, dy, rc, list0 + k + 1u, act, kHits ? s_hits[k] : nullptr,
-                              region);
+        composite_pair<kHitMode>(a, b, ge, ap, cb, dx, dy, rc, list0 + k + 1u, act, kHits ? s_hits[k] : nullptr,
+                                 region, kBits ? &s_bal[warp][it] : nullptr);
       }
 #else
       if (it < mine) {
@@ -333,15 +351,36 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
         const float4 ap = S.app;
         const float cb = S.col_b;
         const float dx = px - ge.x, dy = py - ge.y;
-        composite_pair<false>(a, b, ge, ap, cb, dx, dy, rc, list0 + k + 1u);
+        composite_pair<0>(a, b, ge, ap, cb, dx, dy, rc, list0 + k + 1u);
       }
 #endif
       // a sub-warp whose 16 pixels have all terminated stops early
-      if (__all_sync(kFull, (pix_done(a, rc) && pix_done(b, rc)) || it + 1 >= mine)) break;
+      if (__all_sync(kFull, (pix_done(a, rc) && pix_done(b, rc)) || it + 1 >= mine)) {
+        nit = it + 1;
+        break;
+      }
+    }
+    if (kBits) {  // this warp's steps: ballots -> per-entry region bits (lanes over steps)
+      __syncwarp();
+      for (int it = lane; it < nit; it += 32) {
+        const uint32_t bal = s_bal[warp][it];
+        if (!bal) continue;
+#pragma unroll
+        for (int q = 0; q < kSubs; ++q)  // a sub-warp past its list end held no hit
+          if ((bal >> (8 * q)) & 0xffu) atomicOr(&s_r16[s_list[warp][q][it]], 1u << region_of(warp, q));
+      }
     }
     (void)sub_mask;
     if (!pix_done(a, rc)) a.processed = list0 + (uint32_t)cnt;
     if (!pix_done(b, rc)) b.processed = list0 + (uint32_t)cnt;
+    if (kBits) {  // the batch's region bits, 2 B per entry, coalesced
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < CB / kThreads; ++u) {
+        const int t = u * kThreads + threadIdx.x;
+        if (t < cnt && base + t < k_cap) hits[base + t] = (uint16_t)s_r16[t];
+      }
+    }
     if (kHits) {  // the batch's masks, 32 B per entry, coalesced
       __syncthreads();
 #pragma unroll
@@ -834,14 +873,17 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef GSB_BWD_HITS_MIN_BLOCKS
 #define GSB_BWD_HITS_MIN_BLOCKS 6  // (7: 70 registers, 0.2168 ms; 6: 78 registers, 0.202 ms)
 #endif
-template <int NC, bool kHits>
-__global__ void __launch_bounds__(kThreads, kHits ? GSB_BWD_HITS_MIN_BLOCKS : GSB_BWD_MIN_BLOCKS) backward_raster_half_kernel(
+template <int NC, int kHitMode>
+__global__ void __launch_bounds__(kThreads, kHitMode == 1 ? GSB_BWD_HITS_MIN_BLOCKS : GSB_BWD_MIN_BLOCKS) backward_raster_half_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ ranks, const SplatRec* __restrict__ rec,
     const SplatAux* __restrict__ aux, const CamDev* __restrict__ cam_p, RasterDev rc, float bg_r, float bg_g,
     float bg_b, int64_t npix, const float* __restrict__ d_image, const float* __restrict__ final_t,
     const uint32_t* __restrict__ pixstate, const double* __restrict__ depth_g, double2* __restrict__ tile_cut,
     float* __restrict__ partials, uint32_t k_cap, const uint16_t* __restrict__ hits) {
   __shared__ StagedSplat s_sp[kBatch];
+  constexpr bool kHits = kHitMode == 1;
+  // kHitMode 2: the composite's region bits (one uint16 per list position)
+  // narrow each entry's half mask to the halves it touched.
   // kHits: the composite's hit masks of the batch entries, one 32-bit word per
   // (quadrant, half) = its two 4x4 regions' 16-bit masks
   __shared__ uint32_t s_hm[kHits ? kBatch : 1][8];
@@ -960,6 +1002,8 @@ __global__ void __launch_bounds__(kThreads, kHits ? GSB_BWD_HITS_MIN_BLOCKS : GS
             if (word) m |= 1u << (2 * q + h);
           }
         s_mask[threadIdx.x] = (uint8_t)(m & bbox);
+      } else if (kHitMode == 2) {
+        s_mask[threadIdx.x] = (uint8_t)(bbox & half_mask(__ldg(hits + e)));
       } else {
         s_mask[threadIdx.x] = (uint8_t)bbox;
       }
@@ -1267,21 +1311,25 @@ __global__ void __launch_bounds__(kQ4Threads, GSB_Q4_MIN_BLOCKS) backward_raster
   }
 }
 
-// Hit masks (K3 records, pose-only K4a walks only entries that hit): measured
-// same box, C3 batch: K4a 0.218 -> 0.202 ms but the composite 0.103 -> 0.119 ms
-// (two ballots + a store per step and a 32-B block per entry): 2102 -> 2070
-// iters/s. Off; kept as an A/B knob (profiles/README.md).
+// Hit records (K3 records, the pose-only K4a lists only the halves an entry
+// touched). GSB_BWD_HITS = 2 (default): one 16-bit word of touched-region bits
+// per list position — the composite stores each hit step's ballot and decodes
+// them per entry at the end of the batch, 2 B written per entry — measured
+// same box, C3: K4a 0.218 -> 0.196 ms, composite 0.103 -> 0.120 ms, pose
+// batch +0.5-1.1 %. GSB_BWD_HITS = 1: per-pixel masks, 32 B per list
+// position (K4a 0.202, composite 0.119 ms: batch -1.5 %). 0: off.
 #ifndef GSB_BWD_HITS
-#define GSB_BWD_HITS 0
+#define GSB_BWD_HITS 2
 #endif
 bool hit_masks_enabled() { return GSB_BWD_HITS != 0; }
+int hit_words() { return GSB_BWD_HITS == 1 ? 16 : 1; }  // uint16 per list position
 
 int launch_composite(cudaStream_t st, gsb_frame* f, const RasterDev& rc) {
   const int n_tiles = f->tiles_x * f->tiles_y;
   const int64_t npix = (int64_t)f->width * f->height;
   const bool hm = f->want_hits && GSB_BWD_HITS;
   if (n_tiles > 0)
-    (hm ? composite_kernel<true> : composite_kernel<false>)<<<n_tiles, kThreads, 0, st>>>(
+    (!hm ? composite_kernel<0> : GSB_BWD_HITS == 1 ? composite_kernel<1> : composite_kernel<2>)<<<n_tiles, kThreads, 0, st>>>(
         f->ranges.as<uint2>(), f->list(), f->list_rec(), f->cam.as<CamDev>(), rc,
         (float)f->background[0], (float)f->background[1], (float)f->background[2], npix, f->image.as<float>(),
         f->final_t.as<float>(), f->pixstate.as<uint32_t>(), hm ? f->hits.as<uint16_t>() : nullptr,
@@ -1310,7 +1358,9 @@ int launch_backward_raster(cudaStream_t st, gsb_frame* f, const RasterDev& rc, b
   }
   if (n_tiles > 0 && pose_only && GSB_BWD_HALF) {
     const bool hm = f->want_hits && GSB_BWD_HITS;
-    (hm ? backward_raster_half_kernel<8, true> : backward_raster_half_kernel<8, false>)<<<n_tiles, kThreads, 0, st>>>(
+    (!hm ? backward_raster_half_kernel<8, 0>
+         : GSB_BWD_HITS == 1 ? backward_raster_half_kernel<8, 1> : backward_raster_half_kernel<8, 2>)
+        <<<n_tiles, kThreads, 0, st>>>(
         f->ranges.as<uint2>(), f->list(), f->list_rec(), f->list_aux(), f->cam.as<CamDev>(), rc,
         (float)f->background[0], (float)f->background[1], (float)f->background[2], npix, f->d_image.as<float>(),
         f->final_t.as<float>(), f->pixstate.as<uint32_t>(), f->depth_g.as<double>(), f->tile_cut.as<double2>(),
