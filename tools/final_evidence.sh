@@ -18,4 +18,4 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:prep
 tail -1 gpurun_out/prof_${TAG}_k1.log
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file gpurun_out/launches_joint_$TAG.csv python tools/prof_joint.py 6 > /dev/null 2>&1
-python tools/launch_summary.py gpurun_out/launches_joint_$TAG.csv | head -24
+python tools/launch_summary.py gpurun_out/launches_joint_$TAG.csv | head -40
