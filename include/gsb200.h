@@ -202,6 +202,10 @@ int gsb_frame_destroy(gsb_frame* frame);
 int gsb_render(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, const double background[3],
                const gsb_raster_config* cfg, gsb_frame* frame, double* image_out);
 int gsb_frame_get_info(gsb_frame* frame, gsb_frame_info* info);
+/* The state_fingerprint gsb_render(cloud, cam, ...) stamps on its forward
+ * state (rasterizer.cpp:52-73), without rendering: lets a caller that keys
+ * forward states by fingerprint re-render into the state it already holds. */
+int gsb_state_fingerprint(gsb_cloud* cloud, const gsb_camera* cam, uint64_t* out);
 /* render_expected_depth (rasterizer.cpp:283-323): per-pixel alpha-weighted
  * mean view-space depth (0 where the weight sum is <= 1e-8) and the weight
  * sum, host H*W FP32 each. Same cutoff / alpha decisions as gsb_render. */

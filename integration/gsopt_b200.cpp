@@ -164,10 +164,22 @@ struct FrameCache {
       if (e.fp == fp) return e.f;
     return nullptr;
   }
+  // Takes the state cached under fp out of the list (the caller re-renders
+  // into it and puts it back): a render of the same (cloud, camera) reuses
+  // its device buffers instead of allocating a new state.
+  gsb_frame* take(std::uint64_t fp) {
+    for (auto it = entries.begin(); it != entries.end(); ++it)
+      if (it->fp == fp) {
+        gsb_frame* f = it->f;
+        entries.erase(it);
+        return f;
+      }
+    return nullptr;
+  }
   void put(std::uint64_t fp, gsb_frame* f) {
     for (auto it = entries.begin(); it != entries.end(); ++it)
       if (it->fp == fp) {
-        gsb_frame_destroy(it->f);
+        if (it->f != f) gsb_frame_destroy(it->f);
         entries.erase(it);
         break;
       }
@@ -233,10 +245,14 @@ Scalar splat_alpha(const Vec2& mu2d, const Mat2& inv_cov2d, Scalar opacity, cons
 RenderOutput render(const GaussianCloud& cloud, const Camera& cam, const Vec3& background,
                     const RasterConfig& cfg) {
   gsb_cloud* dc = upload(cloud);
-  gsb_frame* f = nullptr;
-  check(gsb_frame_create(dev().ctx, &f));
-  std::unique_ptr<gsb_frame, int (*)(gsb_frame*)> guard(f, gsb_frame_destroy);
   const gsb_camera gc = to_abi(cam);
+  // the state fingerprint is the cache key (the reference's own, rasterizer.cpp:52-73):
+  // re-rendering the same (cloud, camera) overwrites that state in place
+  std::uint64_t fp = 0;
+  check(gsb_state_fingerprint(dc, &gc, &fp));
+  gsb_frame* f = frames().take(fp);
+  if (!f) check(gsb_frame_create(dev().ctx, &f));
+  std::unique_ptr<gsb_frame, int (*)(gsb_frame*)> guard(f, gsb_frame_destroy);
   const gsb_raster_config rc = to_abi(cfg);
   const double bg[3] = {background(0), background(1), background(2)};
   RenderOutput out;

@@ -1067,6 +1067,12 @@ int gsb_render(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, const doub
   return GSB_OK;
 }
 
+int gsb_state_fingerprint(gsb_cloud* cloud, const gsb_camera* cam, uint64_t* out) {
+  if (!cloud || !cam || !out) return fail(GSB_ERR_INVALID_ARGUMENT, "null argument");
+  *out = fingerprint(cloud, cam, true);  // what gsb_render stamps on a (non-lean) frame
+  return GSB_OK;
+}
+
 int gsb_render_expected_depth(gsb_ctx* ctx, gsb_cloud* cloud, const gsb_camera* cam, const gsb_raster_config* cfg,
                               float* depth_out, float* weight_out) {
   GSB_NVTX("gsb_render_expected_depth");

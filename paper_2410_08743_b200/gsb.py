@@ -196,6 +196,7 @@ def _sigs():
         "gsb_frame_destroy": (C.c_int, [_vp]),
         "gsb_render": (C.c_int, [_vp, _vp, P(Camera), _vp, P(RasterConfig), _vp, _vp]),
         "gsb_frame_get_info": (C.c_int, [_vp, P(FrameInfo)]),
+        "gsb_state_fingerprint": (C.c_int, [_vp, P(Camera), P(C.c_uint64)]),
         "gsb_frame_download": (C.c_int, [_vp] + [_vp] * 15),
         "gsb_rgb_loss": (C.c_int, [_vp, _vp, _vp, i32, i32, d, P(d), _vp]),
         "gsb_image_create": (C.c_int, [_vp, _vp, i32, i32, P(_vp)]),
@@ -524,6 +525,14 @@ def render(ctx: Context, cloud: Cloud, cam: Camera, background=(0.0, 0.0, 0.0), 
     cfg = config or RasterConfig.default()
     _check(lib().gsb_render(ctx.h, cloud.h, C.byref(cam), _p(bg), C.byref(cfg), frame.h, _p(img)))
     return RenderOutput(frame, img)
+
+
+def state_fingerprint(cloud: Cloud, cam: Camera) -> int:
+    """The RenderOutput::state_fingerprint render(cloud, cam) stamps
+    (rasterizer.cpp:52-73), without rendering."""
+    fp = C.c_uint64()
+    _check(lib().gsb_state_fingerprint(cloud.h, C.byref(cam), C.byref(fp)))
+    return int(fp.value)
 
 
 def adam_step(ctx: Context, params, grads, m, v, step: int, lr) -> int:

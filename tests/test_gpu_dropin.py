@@ -86,6 +86,7 @@ def test_fingerprint_equals_reference(G, ctx):
     cloud = to_dev(G, ctx, hc)
     out = G.render(ctx, cloud, dev_cam(G, cam))
     assert out.frame.info().state_fingerprint == ref.fingerprint  # rasterizer.cpp:52-73 bit for bit
+    assert G.state_fingerprint(cloud, dev_cam(G, cam)) == ref.fingerprint  # the same key, without rendering
     # a device-side change (here: a re-upload of different content) changes it
     hc2 = hc.copy()
     hc2.opacity_logits = hc2.opacity_logits + 0.5
