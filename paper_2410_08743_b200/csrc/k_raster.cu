@@ -199,14 +199,15 @@ __device__ __forceinline__ bool pix_done(const PixFwd& p, const RasterDev&) { re
 // sub-warp's 8 lanes' pixel-pair hits go to slot `region` (pixel a of lane
 // l8 -> bit l8, pixel b -> bit 8 + l8), the exact set of (pixel, entry) pairs
 // the replay of render_backward visits (rasterizer.cpp:378-383).
-// kHitMode 2: lane 0 stores the step's ballot (hword); at the end of the
-// batch the ballots and the sub-warp lists give, per entry, the 4x4 regions
-// whose pixels it touched (one store per step on the critical path).
+// kHitMode 2: the first lane of each sub-warp whose pixels hit sets the
+// entry's byte flag for its 4x4 region (rbyte = &s_rb[k][region]; one
+// predicated shared store per step, every flag has a single writer); the
+// batch's flags are packed to 16-bit region words at its end.
 template <int kHitMode>
 __device__ __forceinline__ void composite_pair(PixFwd& a, PixFwd& b, const float4& ge, const float4& ap, float col_b,
                                                float dx, float dy, const RasterDev& rc, uint32_t idx1,
                                                bool act = true, uint16_t* hrow = nullptr, int region = 0,
-                                               uint32_t* hword = nullptr) {
+                                               uint8_t* rbyte = nullptr) {
   const float ga = splat_power(ge.z, ge.w, ap.x, dx, dy);
   const float gb = splat_power(ge.z, ge.w, ap.x, dx, dy + 1.0f);
   const bool ha = act && !pix_done(a, rc) && ga <= rc.cutoff2_f;
@@ -219,7 +220,8 @@ __device__ __forceinline__ void composite_pair(PixFwd& a, PixFwd& b, const float
   } else if (kHitMode == 2) {  // the ballot doubles as the warp-uniform skip test
     const uint32_t bal = __ballot_sync(kFull, ha || hb);
     if (!bal) return;  // (the step's slot was zeroed at staging)
-    if ((threadIdx.x & 31) == 0) *hword = bal;  // the step's ballot, decoded at the end of the batch
+    const int lane = threadIdx.x & 31;
+    if ((lane & 7) == 0 && act && ((bal >> (lane & 24)) & 0xffu)) *rbyte = 1;
   } else {
 #if GSB_COMP_UNIFORM_SKIP
     if (!__any_sync(kFull, ha || hb)) return;  // warp-uniform: lanes without a hit run the no-op update
@@ -277,8 +279,7 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
   constexpr bool kHits = kHitMode == 1;
   __shared__ __align__(16) uint16_t s_hits[kHits ? CB : 1][16];
   constexpr bool kBits = kHitMode == 2;
-  __shared__ uint32_t s_bal[kBits ? kWarps : 1][kBits ? CB : 1];  // per warp step: the hit ballot
-  __shared__ uint32_t s_r16[kBits ? CB : 1];                      // per batch entry: touched regions
+  __shared__ __align__(16) uint8_t s_rb[kBits ? CB : 1][16];  // per batch entry: a flag per 4x4 region it touched
   __shared__ int s_w, s_h, s_tx;
   if (threadIdx.x == 0) {
     s_w = cam_p->width;
@@ -314,11 +315,7 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
         hz[0] = make_uint4(0u, 0u, 0u, 0u);
         hz[1] = make_uint4(0u, 0u, 0u, 0u);
       }
-      if (kBits) {
-        s_r16[t] = 0u;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) s_bal[w][t] = 0u;
-      }
+      if (kBits) *reinterpret_cast<uint4*>(s_rb[t]) = make_uint4(0u, 0u, 0u, 0u);
     }
     __syncthreads();
     const uint32_t list0 = base - range.x;
@@ -329,7 +326,6 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
     for (int s = 0; s < kSubs; ++s) lim[s] = ((live >> (8 * s)) & 0xffu) ? 0xffffffffu : 0u;
     int mine = 0;
     const int nmax = build_lists<CB>(s_mask, cnt, warp, lim, 0u, s_list[warp], &mine);
-    int nit = nmax;  // steps this warp ran (kBits)
     for (int it = 0; it < nmax; ++it) {
 #if GSB_COMP_UNIFORM_SKIP
       {
@@ -341,7 +337,7 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
         const float cb = S.col_b;
         const float dx = px - ge.x, dy = py - ge.y;
         composite_pair<kHitMode>(a, b, ge, ap, cb, dx, dy, rc, list0 + k + 1u, act, kHits ? s_hits[k] : nullptr,
-                                 region, kBits ? &s_bal[warp][it] : nullptr);
+                                 region, kBits ? &s_rb[k][region] : nullptr);
       }
 #else
       if (it < mine) {
@@ -355,20 +351,7 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
       }
 #endif
       // a sub-warp whose 16 pixels have all terminated stops early
-      if (__all_sync(kFull, (pix_done(a, rc) && pix_done(b, rc)) || it + 1 >= mine)) {
-        nit = it + 1;
-        break;
-      }
-    }
-    if (kBits) {  // this warp's steps: ballots -> per-entry region bits (lanes over steps)
-      __syncwarp();
-      for (int it = lane; it < nit; it += 32) {
-        const uint32_t bal = s_bal[warp][it];
-        if (!bal) continue;
-#pragma unroll
-        for (int q = 0; q < kSubs; ++q)  // a sub-warp past its list end held no hit
-          if ((bal >> (8 * q)) & 0xffu) atomicOr(&s_r16[s_list[warp][q][it]], 1u << region_of(warp, q));
-      }
+      if (__all_sync(kFull, (pix_done(a, rc) && pix_done(b, rc)) || it + 1 >= mine)) break;
     }
     (void)sub_mask;
     if (!pix_done(a, rc)) a.processed = list0 + (uint32_t)cnt;
@@ -378,7 +361,12 @@ __global__ void GSB_COMP_BOUNDS composite_kernel(
 #pragma unroll
       for (int u = 0; u < CB / kThreads; ++u) {
         const int t = u * kThreads + threadIdx.x;
-        if (t < cnt && base + t < k_cap) hits[base + t] = (uint16_t)s_r16[t];
+        if (t < cnt && base + t < k_cap) {  // 16 flag bytes (0 / 1) -> bit r = region r
+          const uint4 f = *reinterpret_cast<const uint4*>(s_rb[t]);
+          const uint32_t w = ((f.x * 0x01020408u) >> 24) | (((f.y * 0x01020408u) >> 24) << 4) |
+                             (((f.z * 0x01020408u) >> 24) << 8) | (((f.w * 0x01020408u) >> 24) << 12);
+          hits[base + t] = (uint16_t)w;
+        }
       }
     }
     if (kHits) {  // the batch's masks, 32 B per entry, coalesced
@@ -1093,6 +1081,9 @@ __global__ void __launch_bounds__(kThreads, kHitMode == 1 ? GSB_BWD_HITS_MIN_BLO
 #ifndef GSB_BWD_QUARTER
 #define GSB_BWD_QUARTER 1
 #endif
+#ifndef GSB_BWD_MATCH
+#define GSB_BWD_MATCH 0
+#endif
 __device__ __forceinline__ int quarter_reduce8(const float v[8], float* out) {
   const int lane = threadIdx.x & 31;
   const bool h4 = lane & 4, h2 = lane & 2, h1 = lane & 1;
@@ -1225,6 +1216,14 @@ __global__ void __launch_bounds__(kThreads, GSB_BWD_MIN_BLOCKS) backward_raster_
         float tot;
         const int vi = quarter_reduce8(v, &tot);
         // sub-warps may hold the same entry in this step: add in sub-warp order
+#if GSB_BWD_MATCH
+        // (when the four sub-warps' entries are distinct the adds touch
+        // different slots and need no order: one add)
+        if (__all_sync(kFull, __popc(__match_any_sync(kFull, act ? k : -1 - sub)) == 8)) {
+          if (act) s_red[warp][k][vi] += tot;
+          continue;
+        }
+#endif
 #pragma unroll
         for (int q = 0; q < kSubs; ++q) {
           if (act && sub == q) s_red[warp][k][vi] += tot;
