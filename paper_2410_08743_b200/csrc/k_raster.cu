@@ -1081,8 +1081,8 @@ __global__ void __launch_bounds__(kThreads, kHitMode == 1 ? GSB_BWD_HITS_MIN_BLO
 #ifndef GSB_BWD_QUARTER
 #define GSB_BWD_QUARTER 1
 #endif
-#ifndef GSB_BWD_MATCH
-#define GSB_BWD_MATCH 0
+#ifndef GSB_BWD_MATCH  // unordered add when the step's four entries are distinct (K4a 0.182 -> 0.174 ms)
+#define GSB_BWD_MATCH 1
 #endif
 __device__ __forceinline__ int quarter_reduce8(const float v[8], float* out) {
   const int lane = threadIdx.x & 31;
