@@ -49,11 +49,20 @@ def dev_cam(G, ocam):
                          np.array(ocam.R[:]).reshape(3, 3), np.array(ocam.t[:]))
 
 
-def _run(exe, *args, timeout=900):
+def _run(exe, *args, timeout=450):
     path = os.path.join(BUILD, exe)
     if not os.path.exists(path):
         pytest.skip(f"{path} not built (integration/build.py needs /root/reference at build time)")
-    r = subprocess.run([path, *map(str, args)], capture_output=True, text=True, timeout=timeout)
+    # The reference's host code runs on its own Pool (core.cpp:39-80), whose
+    # unlocked job reset can hang run() (tests/test_ref_pins.py); a hung run
+    # is retried once (criterion 2 normally takes ~120 s).
+    for attempt in range(2):
+        try:
+            r = subprocess.run([path, *map(str, args)], capture_output=True, text=True, timeout=timeout)
+            break
+        except subprocess.TimeoutExpired:
+            if attempt == 1:
+                raise
     out_dir = os.path.join(ROOT, "gpurun_out")
     os.makedirs(out_dir, exist_ok=True)
     with open(os.path.join(out_dir, f"dropin_{exe}_{'_'.join(map(str, args)) or 'all'}.txt"), "w") as fh:
